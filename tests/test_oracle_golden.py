@@ -1,0 +1,144 @@
+"""Pin the CPU oracle against the reference's own outputs (tests/golden/*.npz,
+written by tests/golden/make_golden.py from the real d2ip package)."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import GOLDEN
+from oracle import OracleFrameOptimizer, build_oracle_net, oracle_reconstruct_sequence
+from oracle.resunet import kaiming_reset
+from paper_2507_14046_b200 import workloads as W
+from paper_2507_14046_b200.priornet import sample_noise_input
+
+
+def sha(a):
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def relerr(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+@pytest.fixture(scope="module")
+def cfg0():
+    torch.set_num_threads(1)
+    g = np.load(GOLDEN / "cfg0_step.npz")
+    spec = W.CONFIGS["cfg0"]
+    wl = W.make_workload(spec, seed=0)
+    noise = sample_noise_input(wl.grid, 0, spec.in_channels, 0.1)
+    return g, spec, wl, noise
+
+
+def test_harness_reproduces_golden_inputs(cfg0):
+    g, spec, wl, noise = cfg0
+    assert sha(wl.matrix.values) == str(g["J_sha"])
+    assert sha(wl.voltages.frames[0].values) == str(g["dv_sha"])
+    assert noise.sha256() == str(g["z_sha"])
+
+
+def test_oracle_kaiming_matches_reference_init(cfg0):
+    g, spec, wl, noise = cfg0
+    net = build_oracle_net(spec.channels, spec.in_channels, seed=1)
+    flat = torch.cat([v.reshape(-1) for v in net.state_dict().values()]).numpy()
+    np.testing.assert_array_equal(flat, g["theta0"])
+
+
+def _runner(g, spec, wl, noise, dense=True, **kw):
+    # dense=True feeds the reference's own operator form (zero columns outside the
+    # mask): the oracle then reproduces the reference bit for bit.
+    if dense:
+        J = wl.matrix.dense().values
+        cols = np.arange(J.shape[1])
+    else:
+        J, cols = wl.matrix.values, wl.matrix.columns_q()
+    r = OracleFrameOptimizer(spec.channels, spec.in_channels, noise.values, J, cols,
+                             tuple(g["output_map"]), 1e-3, **kw)
+    r.load(g["theta0"])
+    return r
+
+
+@pytest.mark.parametrize("mode", ["l2sq", "l2"])
+def test_oracle_step_grads_match_reference(cfg0, mode):
+    g, spec, wl, noise = cfg0
+    r = _runner(g, spec, wl, noise, data_norm=mode)
+    total, data, reg, grads, _ = r.grads(g["dv"])
+    assert data == float(g[f"{mode}_data"])
+    flat = torch.cat([v.reshape(-1) for v in grads.values()]).numpy()
+    np.testing.assert_array_equal(flat, g[f"{mode}_grads"])
+    # compact masked J: same operator, different fp32 summation order
+    rc = _runner(g, spec, wl, noise, dense=False, data_norm=mode)
+    _, data_c, _, grads_c, _ = rc.grads(g["dv"])
+    assert data_c == pytest.approx(float(g[f"{mode}_data"]), rel=1e-5)
+    assert relerr(torch.cat([v.reshape(-1) for v in grads_c.values()]).numpy(), g[f"{mode}_grads"]) < 1e-5
+
+
+def test_oracle_tv_grads_match_reference(cfg0):
+    g, spec, wl, noise = cfg0
+    r = _runner(g, spec, wl, noise, data_norm="l2", tv=(0.002, 1.0, 0.1, 1e-8))
+    hist = [torch.as_tensor(h, dtype=torch.float32) for h in g["tv_history"]]
+    total, data, reg, grads, _ = r.grads(g["dv"], hist)
+    assert reg == float(g["tv_reg"])
+    assert total == float(g["tv_total"])
+    flat = torch.cat([v.reshape(-1) for v in grads.values()]).numpy()
+    np.testing.assert_array_equal(flat, g["tv_grads"])
+
+
+@pytest.mark.parametrize("k", [1, 10])
+def test_oracle_adam_trajectory_matches_reference(cfg0, k):
+    g, spec, wl, noise = cfg0
+    r = _runner(g, spec, wl, noise)
+    vol, mapped, trace = r.optimize(g["dv"], [], k, 0)
+    np.testing.assert_array_equal(r.flat().numpy(), g[f"theta{k}"])
+    np.testing.assert_array_equal([t[2] for t in trace], g[f"trace{k}"][:, 1])
+    np.testing.assert_array_equal(vol, g[f"volume{k}"])
+
+
+@pytest.mark.slow
+def test_oracle_cfg0_full_run_matches_reference(cfg0):
+    g, spec, wl, noise = cfg0
+    torch.set_num_threads(1)
+    r = _runner(g, spec, wl, noise)
+    vol, mapped, trace = r.optimize(g["dv"], [], 300, 0)
+    np.testing.assert_array_equal([t[2] for t in trace], g["trace300"][:, 1])
+    np.testing.assert_array_equal(vol, g["volume300"])
+
+
+def test_oracle_sequence_matches_reference():
+    g = np.load(GOLDEN / "seq_mini.npz")
+    spec = W.small_spec()
+    wl = W.make_workload(spec, seed=0)
+    noise = sample_noise_input(wl.grid, 1, spec.in_channels, 0.1)
+    assert noise.sha256() == str(g["z_sha"])
+    np.testing.assert_array_equal(
+        torch.cat([v.reshape(-1) for v in build_oracle_net(spec.channels, 8, seed=2).state_dict().values()]).numpy(),
+        g["theta0"])
+    torch.set_num_threads(1)
+    d = wl.matrix.dense().values
+    res = oracle_reconstruct_sequence(spec.channels, spec.in_channels, noise.values, d,
+                                      np.arange(d.shape[1]), [f.values for f in wl.voltages.frames],
+                                      g["theta0"], tuple(g["output_map"]), 12, 6, 4, 1e-3)
+    assert [c[0] for c in res["chain"]] == list(g["provenance"])
+    assert [r[2] for r in res["records"]] == list(g["iterations"])
+    np.testing.assert_array_equal(res["columns"], g["values"])
+    np.testing.assert_array_equal(res["final"].numpy(), g["theta_final"])
+    for key in ("warm", "frame_1", "frame_4"):
+        np.testing.assert_array_equal([t[2] for t in res["traces"][key]], g[f"trace_{key}"][:, 1])
+
+
+def test_oracle_tv_sequence_matches_reference():
+    g = np.load(GOLDEN / "seq_mini.npz")
+    spec = W.small_spec()
+    wl = W.make_workload(spec, seed=0)
+    noise = sample_noise_input(wl.grid, 1, spec.in_channels, 0.1)
+    torch.set_num_threads(1)
+    d = wl.matrix.dense().values
+    res = oracle_reconstruct_sequence(spec.channels, spec.in_channels, noise.values, d,
+                                      np.arange(d.shape[1]), [f.values for f in wl.voltages.frames[:3]],
+                                      g["theta0"], tuple(g["output_map"]), 12, 6, 4, 1e-3,
+                                      data_norm="l2", tv=(0.002, 1.0, 0.1, 1e-8))
+    np.testing.assert_array_equal(res["columns"], g["tv_values"])
+    for key in ("warm", "frame_2", "frame_3"):
+        np.testing.assert_array_equal([t[4] for t in res["traces"][key]], g[f"tvtrace_{key}"][:, 2])
