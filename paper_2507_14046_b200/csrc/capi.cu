@@ -1,0 +1,134 @@
+// C ABI wrappers (include/d2ip_b200.h) and the convolution dispatcher.
+#include <stdarg.h>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace d2ip {
+
+static thread_local char g_err[1024] = "";
+static thread_local const char* g_variant = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+void set_variant(const char* name) { g_variant = name; }
+
+// Convolution dispatch: tcgen05 implicit GEMM where the shape and precision
+// allow it, the exact-fp32 direct kernel otherwise (C_out = 1 tail, odd C_in,
+// or precision FP32).
+int conv_fwd(d2ip_act x, const float* w, const float* bias, long long wbs, int ks, int stride,
+             d2ip_act y, int accumulate, int precision, int batch, cudaStream_t st) {
+  if (conv_tc_supported(x.c, y.c, ks, stride, precision))
+    return conv_fwd_tc(x, w, bias, wbs, ks, stride, y, accumulate, precision, batch, st);
+  return conv_fwd_direct(x, w, bias, wbs, ks, stride, y, accumulate, batch, st);
+}
+
+int conv_dgrad(d2ip_act gy, const float* w, long long wbs, int ks, int stride, d2ip_act gx,
+               int accumulate, int precision, int batch, cudaStream_t st) {
+  return conv_dgrad_direct(gy, w, wbs, ks, stride, gx, accumulate, batch, st);
+}
+
+size_t conv_wgrad_ws(int cin, int cout, int ks, long long V, int batch, int precision) {
+  (void)precision;
+  return conv_wgrad_direct_ws(cin, cout, ks, V, batch);
+}
+
+int conv_wgrad(d2ip_act x, d2ip_act gy, int ks, int stride, float* gw, long long gwbs, void* ws,
+               size_t ws_bytes, int precision, int batch, cudaStream_t st) {
+  (void)precision;
+  return conv_wgrad_direct(x, gy, ks, stride, gw, gwbs, ws, ws_bytes, batch, st);
+}
+
+static int check_conv_shapes(const d2ip_act& x, const d2ip_act& y, int ks, int stride) {
+  D2IP_CHECK_ARG(ks == 1 || ks == 3, "ksize must be 1 or 3, got %d", ks);
+  D2IP_CHECK_ARG(stride == 1 || stride == 2, "stride must be 1 or 2, got %d", stride);
+  const int pad = ks / 2;
+  D2IP_CHECK_ARG(y.d == (x.d + 2 * pad - ks) / stride + 1 && y.h == (x.h + 2 * pad - ks) / stride + 1 &&
+                     y.w == (x.w + 2 * pad - ks) / stride + 1,
+                 "conv3d: output (%d,%d,%d) does not match input (%d,%d,%d) k=%d s=%d", y.d, y.h, y.w, x.d,
+                 x.h, x.w, ks, stride);
+  D2IP_CHECK_ARG(x.cstride >= x.c && y.cstride >= y.c && x.c >= 1 && y.c >= 1, "bad channel view");
+  return D2IP_OK;
+}
+
+}  // namespace d2ip
+
+extern "C" {
+
+int d2ip_abi_version(void) { return D2IP_ABI_VERSION; }
+const char* d2ip_last_error(void) { return d2ip::g_err; }
+const char* d2ip_last_variant(void) { return d2ip::g_variant; }
+
+int d2ip_conv3d_fwd(d2ip_act x, const float* w, const float* bias, long long wbstride, int ksize, int stride,
+                    d2ip_act y, int accumulate, int precision, int batch, void* stream) {
+  D2IP_RET(d2ip::check_conv_shapes(x, y, ksize, stride));
+  return d2ip::conv_fwd(x, w, bias, wbstride, ksize, stride, y, accumulate, precision, batch, d2ip::S(stream));
+}
+
+int d2ip_conv3d_dgrad(d2ip_act gy, const float* w, long long wbstride, int ksize, int stride, d2ip_act gx,
+                      int accumulate, int precision, int batch, void* stream) {
+  D2IP_RET(d2ip::check_conv_shapes(gx, gy, ksize, stride));
+  return d2ip::conv_dgrad(gy, w, wbstride, ksize, stride, gx, accumulate, precision, batch, d2ip::S(stream));
+}
+
+size_t d2ip_conv3d_wgrad_ws_bytes(d2ip_act x, d2ip_act gy, int ksize, int batch) {
+  return d2ip::conv_wgrad_ws(x.c, gy.c, ksize, (long long)gy.d * gy.h * gy.w, batch, 0);
+}
+
+int d2ip_conv3d_wgrad(d2ip_act x, d2ip_act gy, int ksize, int stride, float* gw, long long gwbstride, void* ws,
+                      size_t ws_bytes, int precision, int batch, void* stream) {
+  D2IP_RET(d2ip::check_conv_shapes(x, gy, ksize, stride));
+  return d2ip::conv_wgrad(x, gy, ksize, stride, gw, gwbstride, ws, ws_bytes, precision, batch, d2ip::S(stream));
+}
+
+int d2ip_norm_act_fwd(d2ip_act y, const float* gamma, const float* beta, long long pbstride, d2ip_act res,
+                      int act, float slope, d2ip_act out, float* xhat, float* rstd, int batch, void* stream) {
+  return d2ip::norm_act_fwd(y, gamma, beta, pbstride, res, act, slope, out, xhat, rstd, batch, d2ip::S(stream));
+}
+
+size_t d2ip_norm_act_bwd_ws_bytes(int v, int c, int batch) { return d2ip::norm_act_bwd_ws(v, c, batch); }
+
+int d2ip_norm_act_bwd(d2ip_act gout, d2ip_act out, int act, float slope, const float* xhat, const float* rstd,
+                      const float* gamma, long long pbstride, d2ip_act gy_pre, d2ip_act gc, float* dgb,
+                      long long dgbstride, void* ws, size_t ws_bytes, int batch, void* stream) {
+  return d2ip::norm_act_bwd(gout, out, act, slope, xhat, rstd, gamma, pbstride, gy_pre, gc, dgb, dgbstride, ws,
+                            ws_bytes, batch, d2ip::S(stream));
+}
+
+int d2ip_upsample2x_fwd(d2ip_act x, d2ip_act y, int batch, void* stream) {
+  return d2ip::upsample2x_fwd(x, y, batch, d2ip::S(stream));
+}
+
+int d2ip_upsample2x_bwd(d2ip_act gy, d2ip_act gx, int accumulate, int batch, void* stream) {
+  return d2ip::upsample2x_bwd(gy, gx, accumulate, batch, d2ip::S(stream));
+}
+
+int d2ip_jac_nseg(int vp) { return d2ip::jac_nseg(vp); }
+
+int d2ip_jac_fwd(const float* J, long long jbstride, const float* sigma, long long sbstride, int m, int vp,
+                 float* partial, int nseg, int batch, void* stream) {
+  return d2ip::jac_fwd_partial(J, jbstride, sigma, sbstride, m, vp, partial, nseg, batch, d2ip::S(stream));
+}
+
+size_t d2ip_jac_adj_ws_bytes(int m, int vp, int batch) { return d2ip::jac_adj_ws(m, vp, batch); }
+
+int d2ip_jac_adj(const float* J, long long jbstride, const float* rs, int m, int vp, float* g, long long gbstride,
+                 void* ws, size_t ws_bytes, int batch, void* stream) {
+  using namespace d2ip;
+  D2IP_CHECK_ARG(ws_bytes >= jac_adj_ws(m, vp, batch), "jac_adj: workspace too small");
+  const int rsplit = jac_adj_rows(m, vp, batch);
+  float* partial = reinterpret_cast<float*>(ws);
+  D2IP_RET(jac_adj_partial(J, jbstride, rs, m, vp, partial, rsplit, batch, S(stream)));
+  return reduce_chunks(partial, rsplit, vp, g, gbstride, batch, S(stream));
+}
+
+int d2ip_adam(float* p, const float* g, float* m, float* v, long long n, float lr, float beta1, float beta2,
+              float eps, const int* step, void* stream) {
+  return d2ip::adam_flat(p, g, m, v, n, lr, beta1, beta2, eps, step, nullptr, d2ip::S(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,78 @@
+// Shared helpers for the sm_100a DIP-step kernels.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+
+#include <string>
+
+#include "../../include/d2ip_b200.h"
+
+namespace d2ip {
+
+void set_error(const char* fmt, ...);
+void set_variant(const char* name);
+
+#define D2IP_CHECK_ARG(cond, ...)             \
+  do {                                        \
+    if (!(cond)) {                            \
+      ::d2ip::set_error(__VA_ARGS__);         \
+      return D2IP_E_ARG;                      \
+    }                                         \
+  } while (0)
+
+#define D2IP_CUDA(call)                                                          \
+  do {                                                                           \
+    cudaError_t err__ = (call);                                                  \
+    if (err__ != cudaSuccess) {                                                  \
+      ::d2ip::set_error("%s:%d %s: %s", __FILE__, __LINE__, #call,               \
+                        cudaGetErrorString(err__));                              \
+      return D2IP_E_CUDA;                                                        \
+    }                                                                            \
+  } while (0)
+
+#define D2IP_LAUNCH_CHECK() D2IP_CUDA(cudaGetLastError())
+
+#define D2IP_RET(call)        \
+  do {                        \
+    int rc__ = (call);        \
+    if (rc__ != D2IP_OK) return rc__; \
+  } while (0)
+
+inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+__device__ __forceinline__ long long vox_count(const d2ip_act& a) {
+  return (long long)a.d * a.h * a.w;
+}
+
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Deterministic block sum (fixed tree order); all threads get the result.
+template <int NT>
+__device__ __forceinline__ float block_sum(float v, float* smem /* >= NT/32 */) {
+  v = warp_sum(v);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  __syncthreads();
+  if (lane == 0) smem[warp] = v;
+  __syncthreads();
+  float t = 0.f;
+  if (warp == 0) {
+    t = lane < NT / 32 ? smem[lane] : 0.f;
+    t = warp_sum(t);
+    if (lane == 0) smem[0] = t;
+  }
+  __syncthreads();
+  t = smem[0];
+  return t;
+}
+
+__device__ __forceinline__ float lrelu(float x, float s) { return x > 0.f ? x : x * s; }
+
+}  // namespace d2ip

@@ -1,0 +1,251 @@
+// Direct (CUDA-core, fp32) 3^3 / 1^3 convolutions: forward, data gradient,
+// weight gradient. These are the exact-fp32 kernels (precision D2IP_PREC_FP32)
+// and the fallback for shapes the tcgen05 implicit-GEMM kernels do not take
+// (C_out = 1 tail, C_in not a multiple of 4). Layout: NDHWC activations,
+// OIDHW weights (the reference's nn.Conv3d layout, priornet.py:111-117).
+#include "common.cuh"
+#include "kernels.h"
+
+namespace d2ip {
+
+template <int KS>
+struct Taps {
+  static constexpr int K3 = KS * KS * KS;
+  static constexpr int PAD = KS / 2;
+};
+
+// One thread computes CG consecutive output channels of one output voxel.
+template <int KS, int CG>
+__global__ void __launch_bounds__(256) conv_fwd_direct_k(d2ip_act x, const float* __restrict__ w,
+                                                         const float* __restrict__ bias,
+                                                         long long wbs, int stride, d2ip_act y,
+                                                         int accumulate) {
+  constexpr int K3 = Taps<KS>::K3, PAD = Taps<KS>::PAD;
+  const int b = blockIdx.z;
+  const int groups = y.c / CG;
+  const long long total = (long long)y.d * y.h * y.w * groups;
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= total) return;
+  const int g = (int)(idx % groups);
+  const long long v = idx / groups;
+  const int ow = (int)(v % y.w), oh = (int)((v / y.w) % y.h), od = (int)(v / ((long long)y.w * y.h));
+  const int cin = x.c, co0 = g * CG;
+  const float* wb = w + b * wbs;
+  float acc[CG];
+#pragma unroll
+  for (int j = 0; j < CG; ++j) acc[j] = bias ? __ldg(bias + b * wbs + co0 + j) : 0.f;
+  const float* xb = x.ptr + b * x.bstride;
+  for (int kd = 0; kd < KS; ++kd) {
+    const int id = od * stride + kd - PAD;
+    if (id < 0 || id >= x.d) continue;
+    for (int kh = 0; kh < KS; ++kh) {
+      const int ih = oh * stride + kh - PAD;
+      if (ih < 0 || ih >= x.h) continue;
+      for (int kw = 0; kw < KS; ++kw) {
+        const int iw = ow * stride + kw - PAD;
+        if (iw < 0 || iw >= x.w) continue;
+        const float* xp = xb + (((long long)id * x.h + ih) * x.w + iw) * x.cstride;
+        const int tap = (kd * KS + kh) * KS + kw;
+        for (int ci = 0; ci < cin; ++ci) {
+          const float xv = __ldg(xp + ci);
+#pragma unroll
+          for (int j = 0; j < CG; ++j)
+            acc[j] = fmaf(xv, __ldg(wb + ((long long)(co0 + j) * cin + ci) * K3 + tap), acc[j]);
+        }
+      }
+    }
+  }
+  float* yp = y.ptr + b * y.bstride + v * y.cstride + co0;
+#pragma unroll
+  for (int j = 0; j < CG; ++j) yp[j] = accumulate ? yp[j] + acc[j] : acc[j];
+}
+
+// One thread computes CG consecutive input-channel gradients of one input voxel.
+template <int KS, int CG>
+__global__ void __launch_bounds__(256) conv_dgrad_direct_k(d2ip_act gy, const float* __restrict__ w,
+                                                           long long wbs, int stride, d2ip_act gx,
+                                                           int accumulate) {
+  constexpr int K3 = Taps<KS>::K3, PAD = Taps<KS>::PAD;
+  const int b = blockIdx.z;
+  const int groups = gx.c / CG;
+  const long long total = (long long)gx.d * gx.h * gx.w * groups;
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= total) return;
+  const int g = (int)(idx % groups);
+  const long long v = idx / groups;
+  const int iw = (int)(v % gx.w), ih = (int)((v / gx.w) % gx.h), id = (int)(v / ((long long)gx.w * gx.h));
+  const int cin = gx.c, cout = gy.c, ci0 = g * CG;
+  const float* wb = w + b * wbs;
+  const float* gb = gy.ptr + b * gy.bstride;
+  float acc[CG];
+#pragma unroll
+  for (int j = 0; j < CG; ++j) acc[j] = 0.f;
+  for (int kd = 0; kd < KS; ++kd) {
+    const int td = id + PAD - kd;
+    if (td < 0 || td % stride) continue;
+    const int od = td / stride;
+    if (od >= gy.d) continue;
+    for (int kh = 0; kh < KS; ++kh) {
+      const int th = ih + PAD - kh;
+      if (th < 0 || th % stride) continue;
+      const int oh = th / stride;
+      if (oh >= gy.h) continue;
+      for (int kw = 0; kw < KS; ++kw) {
+        const int tw = iw + PAD - kw;
+        if (tw < 0 || tw % stride) continue;
+        const int ow = tw / stride;
+        if (ow >= gy.w) continue;
+        const float* gp = gb + (((long long)od * gy.h + oh) * gy.w + ow) * gy.cstride;
+        const int tap = (kd * KS + kh) * KS + kw;
+        for (int co = 0; co < cout; ++co) {
+          const float gv = __ldg(gp + co);
+#pragma unroll
+          for (int j = 0; j < CG; ++j)
+            acc[j] = fmaf(gv, __ldg(wb + ((long long)co * cin + ci0 + j) * K3 + tap), acc[j]);
+        }
+      }
+    }
+  }
+  float* xp = gx.ptr + b * gx.bstride + v * gx.cstride + ci0;
+#pragma unroll
+  for (int j = 0; j < CG; ++j) xp[j] = accumulate ? xp[j] + acc[j] : acc[j];
+}
+
+// Split-K partial weight gradient: one thread per (co, ci, tap) entry (plus
+// one per bias entry), summing its chunk of output voxels.
+template <int KS>
+__global__ void __launch_bounds__(256) conv_wgrad_partial_k(d2ip_act x, d2ip_act gy, int stride,
+                                                            float* __restrict__ partial, int nchunks,
+                                                            int chunk) {
+  constexpr int K3 = Taps<KS>::K3, PAD = Taps<KS>::PAD;
+  const int b = blockIdx.z, c = blockIdx.y;
+  const int cin = x.c, cout = gy.c;
+  const int nW = cout * cin * K3, nE = nW + cout;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nE) return;
+  const long long V = (long long)gy.d * gy.h * gy.w;
+  const long long v0 = (long long)c * chunk;
+  const long long v1 = min(V, v0 + chunk);
+  const float* gb = gy.ptr + b * gy.bstride;
+  float acc = 0.f;
+  if (e >= nW) {
+    const int co = e - nW;
+    for (long long v = v0; v < v1; ++v) acc += __ldg(gb + v * gy.cstride + co);
+  } else {
+    const int co = e / (cin * K3);
+    const int rem = e - co * cin * K3;
+    const int ci = rem / K3, tap = rem - ci * K3;
+    const int kd = tap / (KS * KS), kh = (tap / KS) % KS, kw = tap % KS;
+    const float* xb = x.ptr + b * x.bstride;
+    for (long long v = v0; v < v1; ++v) {
+      const int ow = (int)(v % gy.w), oh = (int)((v / gy.w) % gy.h), od = (int)(v / ((long long)gy.w * gy.h));
+      const int id = od * stride + kd - PAD, ih = oh * stride + kh - PAD, iw = ow * stride + kw - PAD;
+      if (id < 0 || id >= x.d || ih < 0 || ih >= x.h || iw < 0 || iw >= x.w) continue;
+      acc = fmaf(__ldg(gb + v * gy.cstride + co),
+                 __ldg(xb + (((long long)id * x.h + ih) * x.w + iw) * x.cstride + ci), acc);
+    }
+  }
+  partial[((long long)b * nchunks + c) * nE + e] = acc;
+}
+
+__global__ void reduce_chunks_k(const float* __restrict__ partial, int nchunks, int n, float* out,
+                                long long obs) {
+  const int b = blockIdx.y;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  const float* p = partial + (long long)b * nchunks * n + e;
+  float s = 0.f;
+  for (int c = 0; c < nchunks; ++c) s += p[(long long)c * n];
+  out[b * obs + e] = s;
+}
+
+int reduce_chunks(const float* partial, int nchunks, int n, float* out, long long obs, int batch,
+                  cudaStream_t st) {
+  dim3 grid(cdiv(n, 256), batch);
+  reduce_chunks_k<<<grid, 256, 0, st>>>(partial, nchunks, n, out, obs);
+  D2IP_LAUNCH_CHECK();
+  return D2IP_OK;
+}
+
+// ---------------------------------------------------------------------------
+
+int conv_fwd_direct(d2ip_act x, const float* w, const float* bias, long long wbs, int ks, int stride,
+                    d2ip_act y, int accumulate, int batch, cudaStream_t st) {
+  const long long V = (long long)y.d * y.h * y.w;
+#define LAUNCH_F(KS_, CG_)                                                              \
+  do {                                                                                  \
+    long long total = V * (y.c / CG_);                                                  \
+    dim3 grid(cdiv(total, 256), 1, batch);                                              \
+    conv_fwd_direct_k<KS_, CG_><<<grid, 256, 0, st>>>(x, w, bias, wbs, stride, y, accumulate); \
+  } while (0)
+  const int cg = (y.c % 8 == 0) ? 8 : (y.c % 4 == 0 ? 4 : 1);
+  if (ks == 3) {
+    if (cg == 8) LAUNCH_F(3, 8); else if (cg == 4) LAUNCH_F(3, 4); else LAUNCH_F(3, 1);
+  } else {
+    if (cg == 8) LAUNCH_F(1, 8); else if (cg == 4) LAUNCH_F(1, 4); else LAUNCH_F(1, 1);
+  }
+#undef LAUNCH_F
+  set_variant("direct_fp32");
+  D2IP_LAUNCH_CHECK();
+  return D2IP_OK;
+}
+
+int conv_dgrad_direct(d2ip_act gy, const float* w, long long wbs, int ks, int stride, d2ip_act gx,
+                      int accumulate, int batch, cudaStream_t st) {
+  const long long V = (long long)gx.d * gx.h * gx.w;
+#define LAUNCH_D(KS_, CG_)                                                                 \
+  do {                                                                                     \
+    long long total = V * (gx.c / CG_);                                                    \
+    dim3 grid(cdiv(total, 256), 1, batch);                                                 \
+    conv_dgrad_direct_k<KS_, CG_><<<grid, 256, 0, st>>>(gy, w, wbs, stride, gx, accumulate); \
+  } while (0)
+  const int cg = (gx.c % 8 == 0) ? 8 : (gx.c % 4 == 0 ? 4 : 1);
+  if (ks == 3) {
+    if (cg == 8) LAUNCH_D(3, 8); else if (cg == 4) LAUNCH_D(3, 4); else LAUNCH_D(3, 1);
+  } else {
+    if (cg == 8) LAUNCH_D(1, 8); else if (cg == 4) LAUNCH_D(1, 4); else LAUNCH_D(1, 1);
+  }
+#undef LAUNCH_D
+  set_variant("direct_fp32");
+  D2IP_LAUNCH_CHECK();
+  return D2IP_OK;
+}
+
+void wgrad_split(int nE, long long V, int batch, int* nchunks, int* chunk) {
+  long long target = 148LL * 2048 * 2;
+  long long want = (target + (long long)nE * batch - 1) / ((long long)nE * batch);
+  long long maxc = (V + 63) / 64;
+  if (want > maxc) want = maxc;
+  if (want < 1) want = 1;
+  int c = (int)((V + want - 1) / want);
+  *chunk = c;
+  *nchunks = (int)((V + c - 1) / c);
+}
+
+size_t conv_wgrad_direct_ws(int cin, int cout, int ks, long long V, int batch) {
+  const int nE = cout * cin * ks * ks * ks + cout;
+  int nchunks, chunk;
+  wgrad_split(nE, V, batch, &nchunks, &chunk);
+  return (size_t)batch * nchunks * nE * sizeof(float);
+}
+
+int conv_wgrad_direct(d2ip_act x, d2ip_act gy, int ks, int stride, float* gw, long long gwbs,
+                      void* ws, size_t ws_bytes, int batch, cudaStream_t st) {
+  const int nE = gy.c * x.c * ks * ks * ks + gy.c;
+  const long long V = (long long)gy.d * gy.h * gy.w;
+  int nchunks, chunk;
+  wgrad_split(nE, V, batch, &nchunks, &chunk);
+  D2IP_CHECK_ARG(ws_bytes >= (size_t)batch * nchunks * nE * sizeof(float),
+                 "conv3d_wgrad: workspace too small (%zu < %zu)", ws_bytes,
+                 (size_t)batch * nchunks * nE * sizeof(float));
+  float* partial = reinterpret_cast<float*>(ws);
+  dim3 grid(cdiv(nE, 256), nchunks, batch);
+  if (ks == 3)
+    conv_wgrad_partial_k<3><<<grid, 256, 0, st>>>(x, gy, stride, partial, nchunks, chunk);
+  else
+    conv_wgrad_partial_k<1><<<grid, 256, 0, st>>>(x, gy, stride, partial, nchunks, chunk);
+  D2IP_LAUNCH_CHECK();
+  return reduce_chunks(partial, nchunks, nE, gw, gwbs, batch, st);
+}
+
+}  // namespace d2ip

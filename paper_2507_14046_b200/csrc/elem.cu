@@ -1,0 +1,328 @@
+// Per-voxel kernels: ChannelLayerNorm (+residual) (+LeakyReLU) forward and
+// backward, trilinear x2 upsample (align_corners=False) forward and gather
+// backward, and the tail conv + sigmoid + output map + mask gather.
+//
+// ChannelLayerNorm   : pkg/src/d2ip/priornet.py:96-108 (eps 1e-5, biased var)
+// ResConv3d add/act  : priornet.py:145-148
+// F.interpolate      : priornet.py:229 (trilinear, align_corners=False)
+// sigmoid + map      : priornet.py:231, pipeline.py:276-278
+#include "common.cuh"
+#include "kernels.h"
+
+namespace d2ip {
+
+constexpr float kLnEps = 1e-5f;
+
+__global__ void __launch_bounds__(256) norm_act_fwd_k(d2ip_act y, const float* __restrict__ gamma,
+                                                      const float* __restrict__ beta, long long pbs,
+                                                      d2ip_act res, int act, float slope, d2ip_act out,
+                                                      float* __restrict__ xhat, float* __restrict__ rstd) {
+  const int b = blockIdx.y;
+  const long long V = (long long)y.d * y.h * y.w;
+  const long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= V) return;
+  const int C = y.c;
+  const float* yp = y.ptr + b * y.bstride + v * y.cstride;
+  float mean = 0.f;
+  for (int c = 0; c < C; ++c) mean += yp[c];
+  mean /= (float)C;
+  float var = 0.f;
+  for (int c = 0; c < C; ++c) {
+    const float d = yp[c] - mean;
+    var = fmaf(d, d, var);
+  }
+  var /= (float)C;
+  const float rs = 1.0f / sqrtf(var + kLnEps);
+  rstd[b * V + v] = rs;
+  float* xh = xhat + ((long long)b * V + v) * C;
+  const float* g = gamma + b * pbs;
+  const float* be = beta + b * pbs;
+  const float* rp = res.ptr ? res.ptr + b * res.bstride + v * res.cstride : nullptr;
+  float* op = out.ptr + b * out.bstride + v * out.cstride;
+  for (int c = 0; c < C; ++c) {
+    const float x = (yp[c] - mean) * rs;
+    xh[c] = x;
+    float o = fmaf(x, __ldg(g + c), __ldg(be + c));
+    if (rp) o += rp[c];
+    if (act) o = lrelu(o, slope);
+    op[c] = o;
+  }
+}
+
+int norm_act_fwd(d2ip_act y, const float* gamma, const float* beta, long long pbs, d2ip_act res,
+                 int act, float slope, d2ip_act out, float* xhat, float* rstd, int batch,
+                 cudaStream_t st) {
+  const long long V = (long long)y.d * y.h * y.w;
+  dim3 grid(cdiv(V, 128), batch);
+  norm_act_fwd_k<<<grid, 128, 0, st>>>(y, gamma, beta, pbs, res, act, slope, out, xhat, rstd);
+  D2IP_LAUNCH_CHECK();
+  return D2IP_OK;
+}
+
+// gpre = gout * act'(out); gc = rstd * (gpre*gamma - mean(gpre*gamma) - xhat*mean(gpre*gamma*xhat))
+__global__ void __launch_bounds__(128) norm_act_bwd_k(d2ip_act gout, d2ip_act out, int act, float slope,
+                                                      const float* __restrict__ xhat,
+                                                      const float* __restrict__ rstd,
+                                                      const float* __restrict__ gamma, long long pbs,
+                                                      d2ip_act gpre, d2ip_act gc) {
+  const int b = blockIdx.y;
+  const long long V = (long long)gout.d * gout.h * gout.w;
+  const long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= V) return;
+  const int C = gout.c;
+  const float* go = gout.ptr + b * gout.bstride + v * gout.cstride;
+  const float* op = act ? out.ptr + b * out.bstride + v * out.cstride : nullptr;
+  const float* xh = xhat + ((long long)b * V + v) * C;
+  const float* g = gamma + b * pbs;
+  float* gp = gpre.ptr + b * gpre.bstride + v * gpre.cstride;
+  float s1 = 0.f, s2 = 0.f;
+  for (int c = 0; c < C; ++c) {
+    float t = go[c];
+    if (act) t = op[c] > 0.f ? t : t * slope;
+    gp[c] = t;
+    const float gx = t * __ldg(g + c);
+    s1 += gx;
+    s2 = fmaf(gx, xh[c], s2);
+  }
+  const float m1 = s1 / (float)C, m2 = s2 / (float)C;
+  const float rs = rstd[b * V + v];
+  float* gcp = gc.ptr + b * gc.bstride + v * gc.cstride;
+  for (int c = 0; c < C; ++c) {
+    const float gx = gp[c] * __ldg(g + c);
+    gcp[c] = rs * (gx - m1 - xh[c] * m2);
+  }
+}
+
+// partial[b][chunk][0..C) = sum gpre*xhat, [C..2C) = sum gpre over the chunk's voxels.
+__global__ void __launch_bounds__(256) norm_colsum_k(d2ip_act gpre, const float* __restrict__ xhat,
+                                                     float* __restrict__ partial, int chunk, int nchunks) {
+  __shared__ float sm[2][256];
+  const int b = blockIdx.y, ch = blockIdx.x;
+  const int C = gpre.c;
+  const long long V = (long long)gpre.d * gpre.h * gpre.w;
+  const int rows = 256 / C;
+  const int c = threadIdx.x % C, r = threadIdx.x / C;
+  float a1 = 0.f, a2 = 0.f;
+  const long long v0 = (long long)ch * chunk, v1 = min(V, v0 + chunk);
+  if (r < rows) {
+    const float* gp = gpre.ptr + b * gpre.bstride;
+    const float* xh = xhat + (long long)b * V * C;
+    for (long long v = v0 + r; v < v1; v += rows) {
+      const float t = gp[v * gpre.cstride + c];
+      a1 = fmaf(t, xh[v * C + c], a1);
+      a2 += t;
+    }
+  }
+  sm[0][threadIdx.x] = a1;
+  sm[1][threadIdx.x] = a2;
+  __syncthreads();
+  if (threadIdx.x < C) {
+    float s1 = 0.f, s2 = 0.f;
+    for (int rr = 0; rr < rows; ++rr) {
+      s1 += sm[0][rr * C + threadIdx.x];
+      s2 += sm[1][rr * C + threadIdx.x];
+    }
+    float* p = partial + ((long long)b * nchunks + ch) * 2 * C;
+    p[threadIdx.x] = s1;
+    p[C + threadIdx.x] = s2;
+  }
+}
+
+static void colsum_split(long long V, int batch, int* nchunks, int* chunk) {
+  long long want = (148LL * 4 + batch - 1) / batch;
+  long long maxc = (V + 255) / 256;
+  if (want > maxc) want = maxc;
+  if (want < 1) want = 1;
+  *chunk = (int)((V + want - 1) / want);
+  *nchunks = (int)((V + *chunk - 1) / *chunk);
+}
+
+size_t norm_act_bwd_ws(long long V, int C, int batch) {
+  int n, c;
+  colsum_split(V, batch, &n, &c);
+  return (size_t)batch * n * 2 * C * sizeof(float);
+}
+
+int norm_act_bwd(d2ip_act gout, d2ip_act out, int act, float slope, const float* xhat,
+                 const float* rstd, const float* gamma, long long pbs, d2ip_act gpre, d2ip_act gc,
+                 float* dgb, long long dgbs, void* ws, size_t ws_bytes, int batch, cudaStream_t st) {
+  const long long V = (long long)gout.d * gout.h * gout.w;
+  const int C = gout.c;
+  D2IP_CHECK_ARG(C <= 256, "norm_act_bwd: C=%d > 256", C);
+  dim3 grid(cdiv(V, 128), batch);
+  norm_act_bwd_k<<<grid, 128, 0, st>>>(gout, out, act, slope, xhat, rstd, gamma, pbs, gpre, gc);
+  D2IP_LAUNCH_CHECK();
+  int nchunks, chunk;
+  colsum_split(V, batch, &nchunks, &chunk);
+  D2IP_CHECK_ARG(ws_bytes >= (size_t)batch * nchunks * 2 * C * sizeof(float), "norm_act_bwd: ws");
+  float* partial = reinterpret_cast<float*>(ws);
+  norm_colsum_k<<<dim3(nchunks, batch), 256, 0, st>>>(gpre, xhat, partial, chunk, nchunks);
+  D2IP_LAUNCH_CHECK();
+  return reduce_chunks(partial, nchunks, 2 * C, dgb, dgbs, batch, st);
+}
+
+// ---------------------------------------------------------------------------
+// Trilinear x2, align_corners=False. Along one axis (n = low-res size):
+//   dst = 0      -> in[0]
+//   dst = 2m     -> 0.25 in[m-1] + 0.75 in[m]          (m >= 1)
+//   dst = 2m + 1 -> 0.75 in[m] + 0.25 in[min(m+1, n-1)]
+// (src = (dst + 0.5)/2 - 0.5 clamped at 0, aten upsample_trilinear3d.)
+
+struct Lin {
+  int i0, i1;
+  float l0, l1;
+};
+
+__device__ __forceinline__ Lin lin_src(int dst, int n) {
+  float src = 0.5f * ((float)dst + 0.5f) - 0.5f;
+  if (src < 0.f) src = 0.f;
+  Lin r;
+  r.i0 = (int)src;
+  r.i1 = r.i0 + ((r.i0 < n - 1) ? 1 : 0);
+  r.l1 = src - (float)r.i0;
+  r.l0 = 1.f - r.l1;
+  return r;
+}
+
+__global__ void __launch_bounds__(256) upsample2x_fwd_k(d2ip_act x, d2ip_act y) {
+  const int b = blockIdx.y;
+  const int C = x.c;
+  const long long total = (long long)y.d * y.h * y.w * C;
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= total) return;
+  const int c = (int)(idx % C);
+  const long long v = idx / C;
+  const int ow = (int)(v % y.w), oh = (int)((v / y.w) % y.h), od = (int)(v / ((long long)y.w * y.h));
+  const Lin ld = lin_src(od, x.d), lh = lin_src(oh, x.h), lw = lin_src(ow, x.w);
+  const float* xb = x.ptr + b * x.bstride + c;
+  auto at = [&](int d, int h, int w) { return xb[(((long long)d * x.h + h) * x.w + w) * x.cstride]; };
+  const float v00 = lw.l0 * at(ld.i0, lh.i0, lw.i0) + lw.l1 * at(ld.i0, lh.i0, lw.i1);
+  const float v01 = lw.l0 * at(ld.i0, lh.i1, lw.i0) + lw.l1 * at(ld.i0, lh.i1, lw.i1);
+  const float v10 = lw.l0 * at(ld.i1, lh.i0, lw.i0) + lw.l1 * at(ld.i1, lh.i0, lw.i1);
+  const float v11 = lw.l0 * at(ld.i1, lh.i1, lw.i0) + lw.l1 * at(ld.i1, lh.i1, lw.i1);
+  const float r = ld.l0 * (lh.l0 * v00 + lh.l1 * v01) + ld.l1 * (lh.l0 * v10 + lh.l1 * v11);
+  y.ptr[b * y.bstride + v * y.cstride + c] = r;
+}
+
+int upsample2x_fwd(d2ip_act x, d2ip_act y, int batch, cudaStream_t st) {
+  D2IP_CHECK_ARG(y.d == 2 * x.d && y.h == 2 * x.h && y.w == 2 * x.w && y.c == x.c,
+                 "upsample2x: shape mismatch");
+  const long long total = (long long)y.d * y.h * y.w * y.c;
+  upsample2x_fwd_k<<<dim3(cdiv(total, 256), batch), 256, 0, st>>>(x, y);
+  D2IP_LAUNCH_CHECK();
+  return D2IP_OK;
+}
+
+// Contributions of low-res index m to high-res indices along one axis.
+__device__ __forceinline__ int lin_adj(int m, int n, int* hi, float* wt) {
+  int k = 0;
+  if (m >= 1) { hi[k] = 2 * m - 1; wt[k++] = 0.25f; }
+  hi[k] = 2 * m;     wt[k++] = (m == 0) ? 1.0f : 0.75f;
+  hi[k] = 2 * m + 1; wt[k++] = (m == n - 1) ? 1.0f : 0.75f;
+  if (m + 1 <= n - 1) { hi[k] = 2 * m + 2; wt[k++] = 0.25f; }
+  return k;
+}
+
+__global__ void __launch_bounds__(256) upsample2x_bwd_k(d2ip_act gy, d2ip_act gx, int accumulate) {
+  const int b = blockIdx.y;
+  const int C = gx.c;
+  const long long total = (long long)gx.d * gx.h * gx.w * C;
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= total) return;
+  const int c = (int)(idx % C);
+  const long long v = idx / C;
+  const int iw = (int)(v % gx.w), ih = (int)((v / gx.w) % gx.h), id = (int)(v / ((long long)gx.w * gx.h));
+  int hd[4], hh[4], hw[4];
+  float wd[4], wh[4], ww[4];
+  const int nd = lin_adj(id, gx.d, hd, wd), nh = lin_adj(ih, gx.h, hh, wh), nw = lin_adj(iw, gx.w, hw, ww);
+  const float* gb = gy.ptr + b * gy.bstride + c;
+  float acc = 0.f;
+  for (int a = 0; a < nd; ++a)
+    for (int e = 0; e < nh; ++e) {
+      float row = 0.f;
+      for (int f = 0; f < nw; ++f)
+        row = fmaf(ww[f], gb[(((long long)hd[a] * gy.h + hh[e]) * gy.w + hw[f]) * gy.cstride], row);
+      acc = fmaf(wd[a] * wh[e], row, acc);
+    }
+  float* o = gx.ptr + b * gx.bstride + v * gx.cstride + c;
+  *o = accumulate ? *o + acc : acc;
+}
+
+int upsample2x_bwd(d2ip_act gy, d2ip_act gx, int accumulate, int batch, cudaStream_t st) {
+  D2IP_CHECK_ARG(gy.d == 2 * gx.d && gy.h == 2 * gx.h && gy.w == 2 * gx.w && gy.c == gx.c,
+                 "upsample2x_bwd: shape mismatch");
+  const long long total = (long long)gx.d * gx.h * gx.w * gx.c;
+  upsample2x_bwd_k<<<dim3(cdiv(total, 256), batch), 256, 0, st>>>(gy, gx, accumulate);
+  D2IP_LAUNCH_CHECK();
+  return D2IP_OK;
+}
+
+// ---------------------------------------------------------------------------
+// Tail: conv3(c0 -> 1) + bias -> sigmoid -> lo + scale * s, and the gather of
+// the mapped value into J's column order (sigma_c[col_of_vox[v]]).
+__global__ void __launch_bounds__(128) tail_fwd_k(d2ip_act x, const float* __restrict__ w,
+                                                  const float* __restrict__ bias, long long wbs,
+                                                  float lo, float scale, float* __restrict__ sig,
+                                                  float* __restrict__ mapped, float* __restrict__ sigma_c,
+                                                  long long sc_bs, const int* __restrict__ col_of_vox) {
+  const int b = blockIdx.y;
+  const long long V = (long long)x.d * x.h * x.w;
+  const long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= V) return;
+  const int ow = (int)(v % x.w), oh = (int)((v / x.w) % x.h), od = (int)(v / ((long long)x.w * x.h));
+  const int cin = x.c;
+  const float* wb = w + b * wbs;
+  const float* xb = x.ptr + b * x.bstride;
+  float acc = __ldg(bias + b * wbs);
+  for (int kd = 0; kd < 3; ++kd) {
+    const int id = od + kd - 1;
+    if (id < 0 || id >= x.d) continue;
+    for (int kh = 0; kh < 3; ++kh) {
+      const int ih = oh + kh - 1;
+      if (ih < 0 || ih >= x.h) continue;
+      for (int kw = 0; kw < 3; ++kw) {
+        const int iw = ow + kw - 1;
+        if (iw < 0 || iw >= x.w) continue;
+        const float* xp = xb + (((long long)id * x.h + ih) * x.w + iw) * x.cstride;
+        const int tap = (kd * 3 + kh) * 3 + kw;
+        for (int ci = 0; ci < cin; ++ci) acc = fmaf(xp[ci], __ldg(wb + ci * 27 + tap), acc);
+      }
+    }
+  }
+  const float s = 1.0f / (1.0f + expf(-acc));
+  const float mp = lo + scale * s;
+  sig[b * V + v] = s;
+  mapped[b * V + v] = mp;
+  const int col = col_of_vox[v];
+  if (col >= 0) sigma_c[b * sc_bs + col] = mp;
+}
+
+int tail_fwd(d2ip_act x, const float* w, const float* bias, long long wbs, float lo, float scale,
+             float* sig, float* mapped, float* sigma_c, long long sc_bs, const int* col_of_vox,
+             int batch, cudaStream_t st) {
+  const long long V = (long long)x.d * x.h * x.w;
+  tail_fwd_k<<<dim3(cdiv(V, 128), batch), 128, 0, st>>>(x, w, bias, wbs, lo, scale, sig, mapped,
+                                                         sigma_c, sc_bs, col_of_vox);
+  D2IP_LAUNCH_CHECK();
+  return D2IP_OK;
+}
+
+// gtail = gmapped * scale * (1 - s) * s over all voxels (TV on: gmapped holds
+// TV + data gradients for every voxel).
+__global__ void tail_bwd_prep_k(const float* __restrict__ gm, const float* __restrict__ sig, float scale,
+                                float* __restrict__ gt, long long n) {
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float s = sig[i];
+  gt[i] = (gm[i] * scale) * (1.f - s) * s;
+}
+
+int tail_bwd_prep(const float* gmapped, const float* sig, float scale, float* gtail, long long V0,
+                  int batch, cudaStream_t st) {
+  const long long n = V0 * batch;
+  tail_bwd_prep_k<<<cdiv(n, 256), 256, 0, st>>>(gmapped, sig, scale, gtail, n);
+  D2IP_LAUNCH_CHECK();
+  return D2IP_OK;
+}
+
+}  // namespace d2ip

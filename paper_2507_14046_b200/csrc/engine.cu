@@ -1,0 +1,601 @@
+// The DIP-step engine: launch plan of one whole iteration of the canonical
+// config ResUNet for `batch` independent sequences in lockstep,
+// replayed with CUDA graphs. Replaces the Python loop body of the reference's
+// `_FrameOptimizer.optimize` (pkg/src/d2ip/pipeline.py:310-331):
+//   forward (priornet.py:217-232 topology), output map (pipeline.py:276-278),
+//   data term (+ 4D-TV) (pipeline.py:279-283), non-finite check and trace
+//   (pipeline.py:312-328, device-side), backward (pipeline.py:330), Adam
+//   (pipeline.py:331).
+//
+// Memory: every activation, saved tensor and gradient lives in one caller-
+// provided workspace (planned here, allocated by the host as a torch uint8
+// tensor); parameters, gradients and Adam moments are flat [batch][n_params]
+// fp32 buffers in the reference's state_dict order / OIDHW layout.
+#include <cstring>
+#include <vector>
+
+#include "common.cuh"
+#include "kernels.h"
+
+namespace d2ip {
+
+struct ConvP {
+  long long ow = 0, ob = 0;
+  int cin = 0, cout = 0, ks = 3, stride = 1;
+};
+struct NormP {
+  long long og = 0, ob = 0;
+  int c = 0;
+};
+struct Block {
+  ConvP c1, c2, sk;
+  NormP n1, n2;
+  int lin = 0, lout = 0;  // spatial level of input / output
+  d2ip_act x{}, out{}, gx{}, gout{};
+  int gx_acc = 0;
+  float *h1 = nullptr, *xh1 = nullptr, *rs1 = nullptr, *xh2 = nullptr, *rs2 = nullptr;
+};
+
+}  // namespace d2ip
+
+struct d2ip_engine {
+  d2ip_net_desc d{};
+  long long nparams = 0;
+  int L = 0;
+  int D[8]{}, H[8]{}, W[8]{};
+  long long V[8]{};
+  d2ip::ConvP stem, tail;
+  d2ip::NormP stem_n;
+  std::vector<d2ip::Block> enc, dec;
+  d2ip::Block neck;
+  d2ip_bindings b{};
+  bool bound = false;
+  // workspace carve-up
+  float* cat[8]{};
+  float* gcat[8]{};
+  int catw[8]{};
+  float *elast = nullptr, *gelast = nullptr, *bout = nullptr, *gbout = nullptr;
+  float* decout[8]{};
+  float* gdecout[8]{};
+  float *stem_xh = nullptr, *stem_rs = nullptr;
+  float *raw = nullptr, *raw2 = nullptr, *sc[5]{};
+  float *sigma_c = nullptr, *rs = nullptr, *jpart = nullptr, *adjpart = nullptr;
+  float *gtail = nullptr, *gmapped = nullptr, *regpart = nullptr;
+  void* wg_ws = nullptr;
+  size_t wg_ws_bytes = 0;
+  void* na_ws = nullptr;
+  size_t na_ws_bytes = 0;
+  size_t ws_total = 0;
+  long long maxvc = 0;
+  int nseg = 0, rsplit = 0, n_reg = 0;
+  cudaGraph_t graph = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  int launches = 0;
+};
+
+namespace d2ip {
+
+static d2ip_act view(const d2ip_engine& E, float* p, int lvl, int c, int cs) {
+  d2ip_act a;
+  a.ptr = p;
+  a.d = E.D[lvl];
+  a.h = E.H[lvl];
+  a.w = E.W[lvl];
+  a.c = c;
+  a.cstride = cs;
+  a.bstride = E.V[lvl] * cs;
+  return a;
+}
+
+// Param offsets in the exact order of priornet.param_schema().
+static void plan_params(d2ip_engine& E) {
+  long long o = 0;
+  auto conv = [&](int cin, int cout, int ks, int stride) {
+    ConvP c;
+    c.cin = cin;
+    c.cout = cout;
+    c.ks = ks;
+    c.stride = stride;
+    c.ow = o;
+    o += (long long)cout * cin * ks * ks * ks;
+    c.ob = o;
+    o += cout;
+    return c;
+  };
+  auto norm = [&](int c) {
+    NormP n;
+    n.c = c;
+    n.og = o;
+    o += c;
+    n.ob = o;
+    o += c;
+    return n;
+  };
+  auto block = [&](int cin, int cout, int stride) {
+    Block b;
+    b.c1 = conv(cin, cout, 3, stride);
+    b.n1 = norm(cout);
+    b.c2 = conv(cout, cout, 3, 1);
+    b.n2 = norm(cout);
+    b.sk = conv(cin, cout, 1, stride);
+    return b;
+  };
+  const int* c = E.d.channels;
+  const int L = E.L;
+  E.stem = conv(E.d.in_channels, c[0], 3, 1);
+  E.stem_n = norm(c[0]);
+  E.enc.clear();
+  for (int i = 1; i < L; ++i) {
+    Block b = block(c[i - 1], c[i], 2);
+    b.lin = i - 1;
+    b.lout = i;
+    E.enc.push_back(b);
+  }
+  E.neck = block(c[L - 1], c[L - 1], 1);
+  E.neck.lin = E.neck.lout = L - 1;
+  E.dec.clear();
+  for (int lvl = L - 2; lvl >= 0; --lvl) {
+    Block b = block(c[lvl + 1] + c[lvl], c[lvl], 1);
+    b.lin = b.lout = lvl;
+    E.dec.push_back(b);
+  }
+  E.tail = conv(c[0], 1, 3, 1);
+  E.nparams = o;
+}
+
+// Assign workspace pointers (base may be null: size query). Returns bytes.
+static size_t plan_workspace(d2ip_engine& E, char* base) {
+  size_t off = 0;
+  const int B = E.d.batch;
+  auto take = [&](size_t bytes) -> char* {
+    off = (off + 255) & ~(size_t)255;
+    char* p = base ? base + off : nullptr;
+    off += bytes;
+    return p;
+  };
+  auto takef = [&](long long n) { return reinterpret_cast<float*>(take((size_t)n * sizeof(float))); };
+  const int* c = E.d.channels;
+  const int L = E.L;
+  for (int l = 0; l + 1 < L; ++l) {
+    E.catw[l] = c[l + 1] + c[l];
+    E.cat[l] = takef((long long)B * E.V[l] * E.catw[l]);
+    E.gcat[l] = takef((long long)B * E.V[l] * E.catw[l]);
+    E.decout[l] = takef((long long)B * E.V[l] * c[l]);
+    E.gdecout[l] = takef((long long)B * E.V[l] * c[l]);
+  }
+  E.elast = takef((long long)B * E.V[L - 1] * c[L - 1]);
+  E.gelast = takef((long long)B * E.V[L - 1] * c[L - 1]);
+  E.bout = takef((long long)B * E.V[L - 1] * c[L - 1]);
+  E.gbout = takef((long long)B * E.V[L - 1] * c[L - 1]);
+  E.stem_xh = takef((long long)B * E.V[0] * c[0]);
+  E.stem_rs = takef((long long)B * E.V[0]);
+  long long maxvc = E.V[0] * c[0];
+  auto saved = [&](Block& bl) {
+    const long long vc = E.V[bl.lout] * bl.c1.cout;
+    if (vc > maxvc) maxvc = vc;
+    bl.h1 = takef(B * vc);
+    bl.xh1 = takef(B * vc);
+    bl.xh2 = takef(B * vc);
+    bl.rs1 = takef((long long)B * E.V[bl.lout]);
+    bl.rs2 = takef((long long)B * E.V[bl.lout]);
+  };
+  for (auto& bl : E.enc) saved(bl);
+  saved(E.neck);
+  for (auto& bl : E.dec) saved(bl);
+  E.maxvc = maxvc;
+  E.raw = takef(B * maxvc);
+  E.raw2 = takef(B * maxvc);
+  for (int i = 0; i < 5; ++i) E.sc[i] = takef(B * maxvc);
+  // data term
+  const int M = E.d.M, Vp = E.d.Vp;
+  E.nseg = jac_nseg(Vp);
+  E.rsplit = jac_adj_rows(M, Vp, B);
+  E.sigma_c = takef((long long)B * Vp);
+  E.rs = takef((long long)B * M);
+  E.jpart = takef((long long)B * M * E.nseg);
+  E.adjpart = reinterpret_cast<float*>(take(jac_adj_ws(M, Vp, B)));
+  E.gtail = takef((long long)B * E.V[0]);
+  E.gmapped = takef((long long)B * E.V[0]);
+  E.n_reg = tv_nblocks(E.V[0]);
+  E.regpart = takef((long long)B * E.n_reg);
+  // reduction workspaces: max over layers
+  size_t wg = 0, na = 0;
+  auto conv_ws = [&](const ConvP& cv, int lout) {
+    size_t s = conv_wgrad_ws(cv.cin, cv.cout, cv.ks, E.V[lout], B, E.d.precision);
+    if (s > wg) wg = s;
+  };
+  auto blk_ws = [&](const Block& bl) {
+    conv_ws(bl.c1, bl.lout);
+    conv_ws(bl.c2, bl.lout);
+    conv_ws(bl.sk, bl.lout);
+    size_t s = norm_act_bwd_ws(E.V[bl.lout], bl.c1.cout, B);
+    if (s > na) na = s;
+  };
+  conv_ws(E.stem, 0);
+  conv_ws(E.tail, 0);
+  {
+    size_t s = norm_act_bwd_ws(E.V[0], c[0], B);
+    if (s > na) na = s;
+  }
+  for (auto& bl : E.enc) blk_ws(bl);
+  blk_ws(E.neck);
+  for (auto& bl : E.dec) blk_ws(bl);
+  E.wg_ws_bytes = wg;
+  E.na_ws_bytes = na;
+  E.wg_ws = take(wg);
+  E.na_ws = take(na);
+  return (off + 255) & ~(size_t)255;
+}
+
+// Views of every block's input / output / gradients (after plan_workspace).
+static void plan_views(d2ip_engine& E) {
+  const int* c = E.d.channels;
+  const int L = E.L;
+  for (int i = 1; i < L; ++i) {
+    Block& bl = E.enc[i - 1];
+    const int l = i - 1;
+    bl.x = view(E, E.cat[l] + c[l + 1], l, c[l], E.catw[l]);
+    bl.gx = view(E, E.gcat[l] + c[l + 1], l, c[l], E.catw[l]);
+    bl.gx_acc = 1;  // the decoder's concat gradient is already there
+    if (i < L - 1) {
+      bl.out = view(E, E.cat[i] + c[i + 1], i, c[i], E.catw[i]);
+      bl.gout = view(E, E.gcat[i] + c[i + 1], i, c[i], E.catw[i]);
+    } else {
+      bl.out = view(E, E.elast, i, c[i], c[i]);
+      bl.gout = view(E, E.gelast, i, c[i], c[i]);
+    }
+  }
+  E.neck.x = view(E, E.elast, L - 1, c[L - 1], c[L - 1]);
+  E.neck.gx = view(E, E.gelast, L - 1, c[L - 1], c[L - 1]);
+  E.neck.gx_acc = 0;
+  E.neck.out = view(E, E.bout, L - 1, c[L - 1], c[L - 1]);
+  E.neck.gout = view(E, E.gbout, L - 1, c[L - 1], c[L - 1]);
+  for (size_t j = 0; j < E.dec.size(); ++j) {
+    Block& bl = E.dec[j];
+    const int l = bl.lout;
+    bl.x = view(E, E.cat[l], l, E.catw[l], E.catw[l]);
+    bl.gx = view(E, E.gcat[l], l, E.catw[l], E.catw[l]);
+    bl.gx_acc = 0;
+    bl.out = view(E, E.decout[l], l, c[l], c[l]);
+    bl.gout = view(E, E.gdecout[l], l, c[l], c[l]);
+  }
+}
+
+// ---------------------------------------------------------------------------
+
+struct Ctx {
+  d2ip_engine& E;
+  cudaStream_t st;
+  int B;
+  long long pbs;
+  int prec;
+  float slope;
+  float* th() const { return E.b.theta; }
+  float* gr() const { return E.b.grad; }
+};
+
+static int block_fwd(Ctx& k, Block& bl) {
+  d2ip_engine& E = k.E;
+  const int co = bl.c1.cout;
+  d2ip_act raw = view(E, E.raw, bl.lout, co, co);
+  d2ip_act raw2 = view(E, E.raw2, bl.lout, co, co);
+  d2ip_act h1 = view(E, bl.h1, bl.lout, co, co);
+  d2ip_act none{};
+  D2IP_RET(conv_fwd(bl.x, k.th() + bl.c1.ow, k.th() + bl.c1.ob, k.pbs, 3, bl.c1.stride, raw, 0, k.prec, k.B, k.st));
+  D2IP_RET(norm_act_fwd(raw, k.th() + bl.n1.og, k.th() + bl.n1.ob, k.pbs, none, 1, k.slope, h1, bl.xh1, bl.rs1, k.B, k.st));
+  D2IP_RET(conv_fwd(h1, k.th() + bl.c2.ow, k.th() + bl.c2.ob, k.pbs, 3, 1, raw, 0, k.prec, k.B, k.st));
+  D2IP_RET(conv_fwd(bl.x, k.th() + bl.sk.ow, k.th() + bl.sk.ob, k.pbs, 1, bl.sk.stride, raw2, 0, k.prec, k.B, k.st));
+  D2IP_RET(norm_act_fwd(raw, k.th() + bl.n2.og, k.th() + bl.n2.ob, k.pbs, raw2, 1, k.slope, bl.out, bl.xh2, bl.rs2, k.B, k.st));
+  return D2IP_OK;
+}
+
+static int block_bwd(Ctx& k, Block& bl) {
+  d2ip_engine& E = k.E;
+  const int co = bl.c1.cout;
+  auto S = [&](int i) { return view(E, E.sc[i], bl.lout, co, co); };
+  d2ip_act gpre = S(0), gc2 = S(1), gh1 = S(2), gpre1 = S(3), gc1 = S(4);
+  d2ip_act h1 = view(E, bl.h1, bl.lout, co, co);
+  D2IP_RET(norm_act_bwd(bl.gout, bl.out, 1, k.slope, bl.xh2, bl.rs2, k.th() + bl.n2.og, k.pbs, gpre, gc2,
+                        k.gr() + bl.n2.og, k.pbs, E.na_ws, E.na_ws_bytes, k.B, k.st));
+  D2IP_RET(conv_wgrad(h1, gc2, 3, 1, k.gr() + bl.c2.ow, k.pbs, E.wg_ws, E.wg_ws_bytes, k.prec, k.B, k.st));
+  D2IP_RET(conv_dgrad(gc2, k.th() + bl.c2.ow, k.pbs, 3, 1, gh1, 0, k.prec, k.B, k.st));
+  D2IP_RET(norm_act_bwd(gh1, h1, 1, k.slope, bl.xh1, bl.rs1, k.th() + bl.n1.og, k.pbs, gpre1, gc1,
+                        k.gr() + bl.n1.og, k.pbs, E.na_ws, E.na_ws_bytes, k.B, k.st));
+  D2IP_RET(conv_wgrad(bl.x, gc1, 3, bl.c1.stride, k.gr() + bl.c1.ow, k.pbs, E.wg_ws, E.wg_ws_bytes, k.prec, k.B, k.st));
+  D2IP_RET(conv_wgrad(bl.x, gpre, 1, bl.sk.stride, k.gr() + bl.sk.ow, k.pbs, E.wg_ws, E.wg_ws_bytes, k.prec, k.B, k.st));
+  D2IP_RET(conv_dgrad(gc1, k.th() + bl.c1.ow, k.pbs, 3, bl.c1.stride, bl.gx, bl.gx_acc, k.prec, k.B, k.st));
+  D2IP_RET(conv_dgrad(gpre, k.th() + bl.sk.ow, k.pbs, 1, bl.sk.stride, bl.gx, 1, k.prec, k.B, k.st));
+  return D2IP_OK;
+}
+
+static int forward(Ctx& k) {
+  d2ip_engine& E = k.E;
+  const int* c = E.d.channels;
+  const int L = E.L;
+  d2ip_act z = view(E, const_cast<float*>(E.b.z), 0, E.d.in_channels, E.d.in_channels);
+  d2ip_act raw = view(E, E.raw, 0, c[0], c[0]);
+  d2ip_act a0 = view(E, E.cat[0] + c[1], 0, c[0], E.catw[0]);
+  d2ip_act none{};
+  D2IP_RET(conv_fwd(z, k.th() + E.stem.ow, k.th() + E.stem.ob, k.pbs, 3, 1, raw, 0, k.prec, k.B, k.st));
+  D2IP_RET(norm_act_fwd(raw, k.th() + E.stem_n.og, k.th() + E.stem_n.ob, k.pbs, none, 1, k.slope, a0, E.stem_xh,
+                        E.stem_rs, k.B, k.st));
+  for (auto& bl : E.enc) D2IP_RET(block_fwd(k, bl));
+  D2IP_RET(block_fwd(k, E.neck));
+  for (size_t j = 0; j < E.dec.size(); ++j) {
+    Block& bl = E.dec[j];
+    const int l = bl.lout;
+    d2ip_act prev = (j == 0) ? E.neck.out : E.dec[j - 1].out;
+    d2ip_act up = view(E, E.cat[l], l, c[l + 1], E.catw[l]);
+    D2IP_RET(upsample2x_fwd(prev, up, k.B, k.st));
+    D2IP_RET(block_fwd(k, bl));
+  }
+  (void)L;
+  const float lo = E.d.lo;
+  const float scale = (float)((double)E.d.hi - (double)E.d.lo);
+  D2IP_RET(tail_fwd(E.dec.back().out, k.th() + E.tail.ow, k.th() + E.tail.ob, k.pbs, lo, scale, E.b.sig, E.b.mapped,
+                    E.sigma_c, E.d.Vp, E.b.col_of_vox, k.B, k.st));
+  return D2IP_OK;
+}
+
+static bool tv_on(const d2ip_engine& E) { return E.d.lambda_tv > 0.f; }
+
+static int loss(Ctx& k) {
+  d2ip_engine& E = k.E;
+  const long long jbs = E.d.j_shared ? 0 : (long long)E.d.M * E.d.Vp;
+  if (tv_on(E))
+    D2IP_RET(tv_fwd_bwd(E.b.mapped, E.b.history, E.d.max_history, E.b.status, E.d.R, E.d.C, E.d.P,
+                        E.d.lambda_tv, E.d.lambda_s, E.d.lambda_t, E.d.tv_eps, E.gmapped, E.regpart, k.B, k.st));
+  D2IP_RET(jac_fwd_partial(E.b.J, jbs, E.sigma_c, E.d.Vp, E.d.M, E.d.Vp, E.jpart, E.nseg, k.B, k.st));
+  D2IP_RET(jac_loss(E.jpart, E.nseg, E.d.M, E.b.dv, E.d.n_rhs, E.d.data_norm, E.regpart, tv_on(E) ? E.n_reg : 0,
+                    E.d.lambda_tv, E.rs, E.b.trace, E.d.max_iters, E.b.status, k.B, k.st));
+  return D2IP_OK;
+}
+
+static int backward(Ctx& k) {
+  d2ip_engine& E = k.E;
+  const int* c = E.d.channels;
+  const long long jbs = E.d.j_shared ? 0 : (long long)E.d.M * E.d.Vp;
+  const float scale = (float)((double)E.d.hi - (double)E.d.lo);
+  D2IP_RET(jac_adj_partial(E.b.J, jbs, E.rs, E.d.M, E.d.Vp, E.adjpart, E.rsplit, k.B, k.st));
+  if (tv_on(E)) {
+    D2IP_RET(jac_adj_finish(E.adjpart, E.rsplit, E.d.Vp, E.d.V, E.b.vox_of_col, E.b.sig, scale, E.gmapped, E.V[0],
+                            1, k.B, k.st));
+    D2IP_RET(tail_bwd_prep(E.gmapped, E.b.sig, scale, E.gtail, E.V[0], k.B, k.st));
+  } else {
+    D2IP_RET(jac_adj_finish(E.adjpart, E.rsplit, E.d.Vp, E.d.V, E.b.vox_of_col, E.b.sig, scale, E.gtail, E.V[0],
+                            0, k.B, k.st));
+  }
+  d2ip_act gt = view(E, E.gtail, 0, 1, 1);
+  Block& last = E.dec.back();
+  D2IP_RET(conv_wgrad(last.out, gt, 3, 1, k.gr() + E.tail.ow, k.pbs, E.wg_ws, E.wg_ws_bytes, k.prec, k.B, k.st));
+  D2IP_RET(conv_dgrad(gt, k.th() + E.tail.ow, k.pbs, 3, 1, last.gout, 0, k.prec, k.B, k.st));
+  for (int j = (int)E.dec.size() - 1; j >= 0; --j) {
+    Block& bl = E.dec[j];
+    const int l = bl.lout;
+    D2IP_RET(block_bwd(k, bl));
+    d2ip_act gup = view(E, E.gcat[l], l, c[l + 1], E.catw[l]);
+    d2ip_act gprev = (j == 0) ? E.neck.gout : E.dec[j - 1].gout;
+    D2IP_RET(upsample2x_bwd(gup, gprev, 0, k.B, k.st));
+  }
+  D2IP_RET(block_bwd(k, E.neck));
+  for (int i = (int)E.enc.size() - 1; i >= 0; --i) D2IP_RET(block_bwd(k, E.enc[i]));
+  // stem: LN/act backward + weight gradient (no data gradient: Z is fixed)
+  d2ip_act a0 = view(E, E.cat[0] + c[1], 0, c[0], E.catw[0]);
+  d2ip_act ga0 = view(E, E.gcat[0] + c[1], 0, c[0], E.catw[0]);
+  d2ip_act gpre = view(E, E.sc[0], 0, c[0], c[0]);
+  d2ip_act gc = view(E, E.sc[1], 0, c[0], c[0]);
+  D2IP_RET(norm_act_bwd(ga0, a0, 1, k.slope, E.stem_xh, E.stem_rs, k.th() + E.stem_n.og, k.pbs, gpre, gc,
+                        k.gr() + E.stem_n.og, k.pbs, E.na_ws, E.na_ws_bytes, k.B, k.st));
+  d2ip_act z = view(E, const_cast<float*>(E.b.z), 0, E.d.in_channels, E.d.in_channels);
+  D2IP_RET(conv_wgrad(z, gc, 3, 1, k.gr() + E.stem.ow, k.pbs, E.wg_ws, E.wg_ws_bytes, k.prec, k.B, k.st));
+  return D2IP_OK;
+}
+
+static int adam(Ctx& k) {
+  d2ip_engine& E = k.E;
+  return adam_flat(E.b.theta, E.b.grad, E.b.adam_m, E.b.adam_v, (long long)k.B * E.nparams, E.d.lr, E.d.beta1,
+                   E.d.beta2, E.d.eps, E.b.status, E.b.status + 1, k.st);
+}
+
+static Ctx ctx(d2ip_engine& E, void* stream) {
+  return Ctx{E, S(stream), E.d.batch, E.nparams, E.d.precision, E.d.negative_slope};
+}
+
+int engine_step(d2ip_engine& E, void* stream) {
+  Ctx k = ctx(E, stream);
+  D2IP_RET(forward(k));
+  D2IP_RET(loss(k));
+  D2IP_RET(backward(k));
+  D2IP_RET(adam(k));
+  return D2IP_OK;
+}
+
+int engine_grads(d2ip_engine& E, void* stream) {
+  Ctx k = ctx(E, stream);
+  D2IP_RET(forward(k));
+  D2IP_RET(loss(k));
+  D2IP_RET(backward(k));
+  return D2IP_OK;
+}
+
+int engine_predict(d2ip_engine& E, float* y, void* stream) {
+  Ctx k = ctx(E, stream);
+  D2IP_RET(forward(k));
+  const long long jbs = E.d.j_shared ? 0 : (long long)E.d.M * E.d.Vp;
+  D2IP_RET(jac_fwd_partial(E.b.J, jbs, E.sigma_c, E.d.Vp, E.d.M, E.d.Vp, E.jpart, E.nseg, k.B, k.st));
+  return jac_sum(E.jpart, E.nseg, E.d.M, y, k.B, k.st);
+}
+
+int engine_forward(d2ip_engine& E, int with_loss, void* stream) {
+  Ctx k = ctx(E, stream);
+  D2IP_RET(forward(k));
+  if (with_loss) D2IP_RET(loss(k));
+  return D2IP_OK;
+}
+
+__global__ void status_k(int* status, int batch, int mode, int value) {
+  const int b = threadIdx.x;
+  if (b >= batch) return;
+  if (mode == 0) {
+    status[b * 4 + 0] = 0;
+    status[b * 4 + 1] = 0;
+  } else {
+    status[b * 4 + 2] = value;
+  }
+}
+
+int engine_reset_frame(d2ip_engine& E, void* stream) {
+  const size_t bytes = (size_t)E.d.batch * E.nparams * sizeof(float);
+  D2IP_CUDA(cudaMemsetAsync(E.b.adam_m, 0, bytes, S(stream)));
+  D2IP_CUDA(cudaMemsetAsync(E.b.adam_v, 0, bytes, S(stream)));
+  status_k<<<1, 1024, 0, S(stream)>>>(E.b.status, E.d.batch, 0, 0);
+  D2IP_LAUNCH_CHECK();
+  return D2IP_OK;
+}
+
+int engine_set_history(d2ip_engine& E, int n, void* stream) {
+  D2IP_CHECK_ARG(n >= 0 && n <= E.d.max_history, "history count %d outside [0, %d]", n, E.d.max_history);
+  status_k<<<1, 1024, 0, S(stream)>>>(E.b.status, E.d.batch, 1, n);
+  D2IP_LAUNCH_CHECK();
+  return D2IP_OK;
+}
+
+static void drop_graph(d2ip_engine& E) {
+  if (E.gexec) cudaGraphExecDestroy(E.gexec);
+  if (E.graph) cudaGraphDestroy(E.graph);
+  E.gexec = nullptr;
+  E.graph = nullptr;
+}
+
+int engine_run(d2ip_engine& E, int iters, void* stream) {
+  cudaStream_t st = S(stream);
+  if (!E.gexec) {
+    D2IP_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
+    int rc = engine_step(E, stream);
+    cudaGraph_t g = nullptr;
+    cudaError_t ce = cudaStreamEndCapture(st, &g);
+    if (rc != D2IP_OK) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    D2IP_CUDA(ce);
+    E.graph = g;
+    D2IP_CUDA(cudaGraphInstantiate(&E.gexec, g, 0));
+    size_t n = 0;
+    D2IP_CUDA(cudaGraphGetNodes(g, nullptr, &n));
+    E.launches = (int)n;
+  }
+  for (int i = 0; i < iters; ++i) D2IP_CUDA(cudaGraphLaunch(E.gexec, st));
+  return D2IP_OK;
+}
+
+}  // namespace d2ip
+
+// ---------------------------------------------------------------------------
+extern "C" {
+
+int d2ip_engine_create(const d2ip_net_desc* desc, d2ip_engine** out) {
+  using namespace d2ip;
+  D2IP_CHECK_ARG(desc && out, "null argument");
+  const d2ip_net_desc& d = *desc;
+  D2IP_CHECK_ARG(d.levels >= 2 && d.levels <= 8, "levels must be in [2, 8]");
+  D2IP_CHECK_ARG(d.batch >= 1, "batch must be >= 1");
+  const int f = 1 << (d.levels - 1);
+  D2IP_CHECK_ARG(d.R % f == 0 && d.C % f == 0 && d.P % f == 0, "grid (%d,%d,%d) not divisible by %d", d.R, d.C,
+                 d.P, f);
+  D2IP_CHECK_ARG(d.Vp % 4 == 0 && d.Vp >= d.V && d.V >= 1, "bad V/Vp");
+  D2IP_CHECK_ARG(d.M >= 1 && d.n_rhs >= 1, "bad M / n_rhs");
+  D2IP_CHECK_ARG(d.max_iters >= 1, "max_iters must be >= 1");
+  for (int l = 0; l < d.levels; ++l) D2IP_CHECK_ARG(d.channels[l] >= 1, "channel count must be positive");
+  d2ip_engine* E = new d2ip_engine();
+  E->d = d;
+  E->L = d.levels;
+  for (int l = 0; l < d.levels; ++l) {
+    E->D[l] = d.R >> l;
+    E->H[l] = d.C >> l;
+    E->W[l] = d.P >> l;
+    E->V[l] = (long long)E->D[l] * E->H[l] * E->W[l];
+  }
+  plan_params(*E);
+  E->ws_total = plan_workspace(*E, nullptr);
+  *out = E;
+  return D2IP_OK;
+}
+
+void d2ip_engine_destroy(d2ip_engine* e) {
+  if (!e) return;
+  d2ip::drop_graph(*e);
+  delete e;
+}
+
+long long d2ip_engine_param_count(const d2ip_engine* e) { return e ? e->nparams : -1; }
+size_t d2ip_engine_workspace_bytes(const d2ip_engine* e) { return e ? e->ws_total : 0; }
+int d2ip_engine_launches_per_iter(const d2ip_engine* e) { return e ? e->launches : 0; }
+
+int d2ip_engine_bind(d2ip_engine* e, const d2ip_bindings* b) {
+  using namespace d2ip;
+  D2IP_CHECK_ARG(e && b, "null argument");
+  D2IP_CHECK_ARG(b->workspace_bytes >= e->ws_total, "workspace too small: %zu < %zu", b->workspace_bytes,
+                 e->ws_total);
+  D2IP_CHECK_ARG(b->theta && b->grad && b->adam_m && b->adam_v && b->z && b->J && b->vox_of_col &&
+                     b->col_of_vox && b->dv && b->mapped && b->sig && b->trace && b->status,
+                 "missing binding");
+  D2IP_CHECK_ARG(e->d.lambda_tv <= 0.f || b->history || e->d.max_history == 0, "TV needs a history buffer");
+  drop_graph(*e);
+  e->b = *b;
+  plan_workspace(*e, reinterpret_cast<char*>(b->workspace));
+  plan_views(*e);
+  // one-time zero: J padding columns of sigma_c, unmasked tail gradients
+  D2IP_CUDA(cudaMemset(b->workspace, 0, e->ws_total));
+  e->bound = true;
+  return D2IP_OK;
+}
+
+int d2ip_engine_set_history(d2ip_engine* e, int n_history) {
+  // stream 0 ordering is not required: the host calls this between frames
+  // after a stream synchronisation.
+  using namespace d2ip;
+  D2IP_CHECK_ARG(e && e->bound, "engine not bound");
+  D2IP_RET(engine_set_history(*e, n_history, nullptr));
+  D2IP_CUDA(cudaStreamSynchronize(nullptr));
+  return D2IP_OK;
+}
+
+int d2ip_engine_reset_frame(d2ip_engine* e, void* stream) {
+  using namespace d2ip;
+  D2IP_CHECK_ARG(e && e->bound, "engine not bound");
+  return engine_reset_frame(*e, stream);
+}
+
+int d2ip_engine_step(d2ip_engine* e, void* stream) {
+  using namespace d2ip;
+  D2IP_CHECK_ARG(e && e->bound, "engine not bound");
+  return engine_step(*e, stream);
+}
+
+int d2ip_engine_grads(d2ip_engine* e, void* stream) {
+  using namespace d2ip;
+  D2IP_CHECK_ARG(e && e->bound, "engine not bound");
+  return engine_grads(*e, stream);
+}
+
+int d2ip_engine_run(d2ip_engine* e, int iters, void* stream) {
+  using namespace d2ip;
+  D2IP_CHECK_ARG(e && e->bound, "engine not bound");
+  D2IP_CHECK_ARG(iters >= 0, "iters must be >= 0");
+  return engine_run(*e, iters, stream);
+}
+
+int d2ip_engine_predict(d2ip_engine* e, float* y, void* stream) {
+  using namespace d2ip;
+  D2IP_CHECK_ARG(e && e->bound && y, "engine not bound / null output");
+  return engine_predict(*e, y, stream);
+}
+
+int d2ip_engine_forward(d2ip_engine* e, int with_loss, void* stream) {
+  using namespace d2ip;
+  D2IP_CHECK_ARG(e && e->bound, "engine not bound");
+  return engine_forward(*e, with_loss, stream);
+}
+
+}  // extern "C"

@@ -1,0 +1,75 @@
+// Internal (C++) entry points of the kernel library; the C ABI in capi.cu and
+// the engine in engine.cu call these.
+#pragma once
+#include "common.cuh"
+
+namespace d2ip {
+
+// conv_direct.cu — exact fp32 CUDA-core convolutions
+int conv_fwd_direct(d2ip_act x, const float* w, const float* bias, long long wbs, int ks, int stride,
+                    d2ip_act y, int accumulate, int batch, cudaStream_t st);
+int conv_dgrad_direct(d2ip_act gy, const float* w, long long wbs, int ks, int stride, d2ip_act gx,
+                      int accumulate, int batch, cudaStream_t st);
+size_t conv_wgrad_direct_ws(int cin, int cout, int ks, long long V, int batch);
+int conv_wgrad_direct(d2ip_act x, d2ip_act gy, int ks, int stride, float* gw, long long gwbs,
+                      void* ws, size_t ws_bytes, int batch, cudaStream_t st);
+int reduce_chunks(const float* partial, int nchunks, int n, float* out, long long obs, int batch,
+                  cudaStream_t st);
+
+// conv_tc.cu — tcgen05 implicit-GEMM convolutions (tf32 / bf16 operands)
+bool conv_tc_supported(int cin, int cout, int ks, int stride, int precision);
+int conv_fwd_tc(d2ip_act x, const float* w, const float* bias, long long wbs, int ks, int stride,
+                d2ip_act y, int accumulate, int precision, int batch, cudaStream_t st);
+
+// conv dispatch (conv_dispatch in capi.cu)
+int conv_fwd(d2ip_act x, const float* w, const float* bias, long long wbs, int ks, int stride,
+             d2ip_act y, int accumulate, int precision, int batch, cudaStream_t st);
+int conv_dgrad(d2ip_act gy, const float* w, long long wbs, int ks, int stride, d2ip_act gx,
+               int accumulate, int precision, int batch, cudaStream_t st);
+size_t conv_wgrad_ws(int cin, int cout, int ks, long long V, int batch, int precision);
+int conv_wgrad(d2ip_act x, d2ip_act gy, int ks, int stride, float* gw, long long gwbs, void* ws,
+               size_t ws_bytes, int precision, int batch, cudaStream_t st);
+
+// elem.cu — normalisation / activation / resampling / output map
+int norm_act_fwd(d2ip_act y, const float* gamma, const float* beta, long long pbs, d2ip_act res,
+                 int act, float slope, d2ip_act out, float* xhat, float* rstd, int batch,
+                 cudaStream_t st);
+size_t norm_act_bwd_ws(long long V, int C, int batch);
+int norm_act_bwd(d2ip_act gout, d2ip_act out, int act, float slope, const float* xhat,
+                 const float* rstd, const float* gamma, long long pbs, d2ip_act gpre, d2ip_act gc,
+                 float* dgb, long long dgbs, void* ws, size_t ws_bytes, int batch, cudaStream_t st);
+int upsample2x_fwd(d2ip_act x, d2ip_act y, int batch, cudaStream_t st);
+int upsample2x_bwd(d2ip_act gy, d2ip_act gx, int accumulate, int batch, cudaStream_t st);
+int tail_fwd(d2ip_act x, const float* w, const float* bias, long long wbs, float lo, float scale,
+             float* sig, float* mapped, float* sigma_c, long long sc_bs, const int* col_of_vox,
+             int batch, cudaStream_t st);
+int tail_bwd_prep(const float* gmapped, const float* sig, float scale, float* gtail, long long V0,
+                  int batch, cudaStream_t st);
+
+// jacobian.cu — HBM-streaming J.sigma / J^T r, data term
+int jac_nseg(int vp);
+int jac_fwd_partial(const float* J, long long jbs, const float* sigma, long long sbs, int m, int vp,
+                    float* partial, int nseg, int batch, cudaStream_t st);
+int jac_loss(const float* partial, int nseg, int m, const float* dv, int n_rhs, int norm,
+             const float* reg_partial, int n_reg, float reg_scale, float* rs, float* trace,
+             int max_iters, int* status, int batch, cudaStream_t st);
+int jac_sum(const float* partial, int nseg, int m, float* y, int batch, cudaStream_t st);
+int jac_adj_rows(int m, int vp, int batch);
+size_t jac_adj_ws(int m, int vp, int batch);
+int jac_adj_partial(const float* J, long long jbs, const float* rs, int m, int vp, float* partial,
+                    int rsplit, int batch, cudaStream_t st);
+int jac_adj_finish(const float* partial, int rsplit, int vp, int v, const int* vox_of_col,
+                   const float* sig, float scale, float* gout, long long V0, int add_to_gmapped,
+                   int batch, cudaStream_t st);
+
+// tv.cu — 4D-TV value partials + gradient w.r.t. mapped
+int tv_nblocks(long long V0);
+int tv_fwd_bwd(const float* mapped, const float* history, int max_history, const int* status,
+               int R, int C, int P, float lam_tv, float lam_s, float lam_t, float eps,
+               float* gmapped, float* reg_partial, int batch, cudaStream_t st);
+
+// adam.cu
+int adam_flat(float* p, const float* g, float* m, float* v, long long n, float lr, float b1, float b2,
+              float eps, const int* step, const int* bad, cudaStream_t st);
+
+}  // namespace d2ip

@@ -1,0 +1,336 @@
+"""Device-resident runner over the sm_100a engine (host side of the boundary).
+
+`DeviceNet` owns, for `batch` sequences in lockstep, every device buffer the
+DIP step touches (θ, gradients, Adam moments, Z, the masked J, Δv, the TV
+history, outputs, trace, status and one workspace) and drives the C-ABI engine
+(`include/d2ip_b200.h`). torch is used only to allocate device memory and to
+name the current stream; every arithmetic step of an iteration runs in the
+extension's kernels. Data layout in HBM:
+
+  θ, grad, m, v   [B][n_params] fp32, reference state_dict order, OIDHW convs
+  Z               [B][R][C][P][C_z] fp32 (NDHWC; D=R, H=C, W=P)
+  J               [B or 1][M][Vp] fp32, columns = masked voxels in memory order,
+                  zero-padded to Vp = round_up(V, 4)
+  vox_of_col      [V] int32  voxel offset (r*C + c)*P + p of column j
+  col_of_vox      [Q] int32  column of each voxel, -1 outside the mask
+  Δv              [B][n_rhs][M] fp32
+"""
+
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+from .errors import NativeLibraryError
+from .forward import as_masked
+from .geometry import vectorize
+from .priornet import ResUNetConfig, param_schema, state_from_flat
+
+TICK_S = 1.024e-6  # trace timestamp unit (globaltimer >> 10)
+
+
+def _stream_ptr() -> int:
+    return torch.cuda.current_stream().cuda_stream
+
+
+def require_cuda() -> None:
+    if not torch.cuda.is_available():
+        raise NativeLibraryError("no CUDA device: the DIP engine runs only on the GPU (no CPU fallback)")
+    N.lib()
+
+
+@dataclass
+class ColumnMap:
+    """Permutation of J's canonical (q-ordered) mask columns into memory order."""
+
+    perm: np.ndarray        # canonical column index of device column j
+    vox_of_col: np.ndarray  # memory offset of device column j
+    col_of_vox: np.ndarray  # device column of each memory offset, -1 outside
+
+    @classmethod
+    def from_mask(cls, mask: np.ndarray) -> "ColumnMap":
+        R, C, P = mask.shape
+        q_cols = np.flatnonzero(vectorize(mask))           # canonical q of each column
+        p = q_cols // (R * C)
+        r = (q_cols // C) % R
+        c = q_cols % C
+        vmem = (r * C + c) * P + p
+        perm = np.argsort(vmem, kind="stable")
+        vox = vmem[perm].astype(np.int32)
+        col = np.full(R * C * P, -1, dtype=np.int32)
+        col[vox] = np.arange(vox.size, dtype=np.int32)
+        return cls(perm, vox, col)
+
+
+def noise_to_device(values: np.ndarray) -> torch.Tensor:
+    """(R,C,P) or (C_z,R,C,P) host noise -> [R][C][P][C_z] fp32 on the GPU."""
+    v = np.asarray(values)
+    if v.ndim == 3:
+        v = v[None]
+    t = torch.from_numpy(np.ascontiguousarray(v, dtype=np.float32))
+    return t.permute(1, 2, 3, 0).contiguous().cuda()
+
+
+def upload_masked_J(values: np.ndarray, perm: np.ndarray, vp: int) -> torch.Tensor:
+    """Host M x V block -> device M x Vp fp32, columns permuted to memory order."""
+    M, V = values.shape
+    raw = torch.from_numpy(np.ascontiguousarray(values, dtype=np.float32)).cuda()
+    out = torch.zeros((M, vp), dtype=torch.float32, device="cuda")
+    out[:, :V] = raw.index_select(1, torch.from_numpy(perm).long().cuda())
+    return out
+
+
+class DeviceNet:
+    """One bound engine: `batch` sequences of one network config in lockstep."""
+
+    def __init__(self, cfg: ResUNetConfig, grid_shape, M: int, mask: np.ndarray, *, batch: int = 1,
+                 n_rhs: int = 1, j_shared: bool = True, data_norm: str = "l2sq", output_map=(-0.135, 0.0),
+                 lr: float = 1e-3, betas=(0.9, 0.999), eps: float = 1e-8, precision: str = "fp32",
+                 tv=(0.0, 1.0, 0.1, 1e-8), max_history: int = 0, max_iters: int = 4096):
+        require_cuda()
+        if not isinstance(cfg, ResUNetConfig):
+            param_schema(cfg)  # raises NotImplementedError for the reference FastResUNet3D
+        if precision not in N.PREC:
+            raise ValueError(f"precision must be one of {sorted(N.PREC)}")
+        if data_norm not in N.NORM:
+            raise ValueError(f"data_norm must be one of {sorted(N.NORM)}")
+        self.cfg = cfg
+        self.schema = param_schema(cfg)
+        self.R, self.C, self.P = (int(x) for x in grid_shape)
+        self.Q = self.R * self.C * self.P
+        self.batch, self.n_rhs, self.M = batch, n_rhs, int(M)
+        self.colmap = ColumnMap.from_mask(np.asarray(mask, dtype=bool))
+        self.V = int(self.colmap.vox_of_col.size)
+        self.Vp = (self.V + 3) // 4 * 4
+        self.j_shared = j_shared
+        self.output_map = (float(output_map[0]), float(output_map[1]))
+        self.max_iters = int(max_iters)
+        self.max_history = int(max_history)
+        self.tv = tuple(float(x) for x in tv)
+        d = N.NetDesc()
+        d.batch, d.R, d.C, d.P = batch, self.R, self.C, self.P
+        ch = cfg.channels
+        d.levels = len(ch)
+        for i, c in enumerate(ch):
+            d.channels[i] = c
+        d.in_channels = cfg.in_channels
+        d.negative_slope = cfg.negative_slope
+        d.M, d.V, d.Vp, d.n_rhs = self.M, self.V, self.Vp, n_rhs
+        d.j_shared = 1 if j_shared else 0
+        d.data_norm = N.NORM[data_norm]
+        d.lo, d.hi = self.output_map
+        d.lr, d.beta1, d.beta2, d.eps = lr, betas[0], betas[1], eps
+        d.precision = N.PREC[precision]
+        d.lambda_tv, d.lambda_s, d.lambda_t, d.tv_eps = self.tv
+        d.max_history = self.max_history
+        d.max_iters = self.max_iters
+        self.desc = d
+        L = N.lib()
+        h = N.C.c_void_p()
+        N.check(L.d2ip_engine_create(N.C.byref(d), N.C.byref(h)), "engine_create")
+        self._h = h
+        self.n_params = int(L.d2ip_engine_param_count(h))
+        expect = sum(e.numel for e in self.schema)
+        if self.n_params != expect:
+            raise NativeLibraryError(f"engine parameter count {self.n_params} != schema {expect}")
+        dev = "cuda"
+        f32 = dict(dtype=torch.float32, device=dev)
+        B = batch
+        self.theta = torch.zeros((B, self.n_params), **f32)
+        self.grad = torch.zeros((B, self.n_params), **f32)
+        self.adam_m = torch.zeros((B, self.n_params), **f32)
+        self.adam_v = torch.zeros((B, self.n_params), **f32)
+        self.z = torch.zeros((B, self.R, self.C, self.P, cfg.in_channels), **f32)
+        self.J = None
+        self.vox_of_col = torch.from_numpy(self.colmap.vox_of_col).cuda()
+        self.col_of_vox = torch.from_numpy(self.colmap.col_of_vox).cuda()
+        self.dv = torch.zeros((B, n_rhs, self.M), **f32)
+        self.history = torch.zeros((B, max(self.max_history, 1), self.Q), **f32)
+        self.mapped = torch.zeros((B, self.Q), **f32)
+        self.sig = torch.zeros((B, self.Q), **f32)
+        self.trace = torch.zeros((B, self.max_iters, 4), **f32)
+        self.status = torch.zeros((B, 4), dtype=torch.int32, device=dev)
+        self.ws = torch.zeros(int(L.d2ip_engine_workspace_bytes(h)), dtype=torch.uint8, device=dev)
+        self.n_history = 0
+        self._bound = False
+
+    # -- binding ------------------------------------------------------------
+    def set_J(self, J_dev: torch.Tensor) -> None:
+        """J_dev: [M][Vp] (shared) or [B][M][Vp] device fp32, memory column order."""
+        J_dev = J_dev.contiguous()
+        want = (self.M, self.Vp) if self.j_shared else (self.batch, self.M, self.Vp)
+        if tuple(J_dev.shape) != want:
+            raise ValueError(f"J shape {tuple(J_dev.shape)} != {want}")
+        self.J = J_dev
+        self._bound = False
+
+    def set_J_host(self, values: np.ndarray, b: int | None = None) -> None:
+        Jd = upload_masked_J(values, self.colmap.perm, self.Vp)
+        if self.j_shared:
+            self.set_J(Jd)
+        else:
+            if self.J is None:
+                self.J = torch.zeros((self.batch, self.M, self.Vp), dtype=torch.float32, device="cuda")
+            self.J[b].copy_(Jd)
+            self._bound = False
+
+    def _bind(self):
+        if self._bound:
+            return
+        if self.J is None:
+            raise ValueError("J not set")
+        b = N.Bindings()
+        b.theta, b.grad = self.theta.data_ptr(), self.grad.data_ptr()
+        b.adam_m, b.adam_v = self.adam_m.data_ptr(), self.adam_v.data_ptr()
+        b.z, b.J = self.z.data_ptr(), self.J.data_ptr()
+        b.vox_of_col, b.col_of_vox = self.vox_of_col.data_ptr(), self.col_of_vox.data_ptr()
+        b.dv, b.history = self.dv.data_ptr(), self.history.data_ptr()
+        b.mapped, b.sig = self.mapped.data_ptr(), self.sig.data_ptr()
+        b.trace, b.status = self.trace.data_ptr(), self.status.data_ptr()
+        b.workspace, b.workspace_bytes = self.ws.data_ptr(), self.ws.numel()
+        torch.cuda.current_stream().synchronize()
+        N.check(N.lib().d2ip_engine_bind(self._h, N.C.byref(b)), "engine_bind")
+        self._bound = True
+        if self.n_history:
+            self.set_history_count(self.n_history)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            N.lib().d2ip_engine_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    # -- inputs ---------------------------------------------------------------
+    def set_noise(self, values, b: int | None = None) -> None:
+        zt = noise_to_device(values)
+        if zt.shape[-1] != self.cfg.in_channels:
+            raise ValueError(f"noise has {zt.shape[-1]} channels, network expects {self.cfg.in_channels}")
+        if b is None:
+            self.z.copy_(zt.expand_as(self.z))
+        else:
+            self.z[b].copy_(zt)
+
+    def set_theta(self, flat: torch.Tensor, b: int | None = None) -> None:
+        flat = torch.as_tensor(flat, dtype=torch.float32).reshape(-1)
+        if flat.numel() != self.n_params:
+            raise ValueError(f"theta has {flat.numel()} values, network needs {self.n_params}")
+        if b is None:
+            self.theta.copy_(flat.to("cuda").expand_as(self.theta))
+        else:
+            self.theta[b].copy_(flat.to("cuda"))
+
+    def set_dv(self, dv, b: int | None = None) -> None:
+        t = torch.as_tensor(np.asarray(dv, dtype=np.float32) if not torch.is_tensor(dv) else dv,
+                            dtype=torch.float32).to("cuda").reshape(-1, self.M)
+        if b is None:
+            self.dv.copy_(t.reshape(1, -1, self.M).expand_as(self.dv) if t.shape[0] == self.n_rhs
+                          else t.reshape(self.batch, self.n_rhs, self.M))
+        else:
+            self.dv[b].copy_(t.reshape(self.n_rhs, self.M))
+
+    def set_history(self, frames, b: int | None = None) -> None:
+        frames = list(frames)
+        if len(frames) > self.max_history:
+            raise ValueError(f"history holds {len(frames)} frames, capacity {self.max_history}")
+        for k, f in enumerate(frames):
+            t = torch.as_tensor(np.asarray(f) if not torch.is_tensor(f) else f, dtype=torch.float32)
+            t = t.to("cuda").reshape(-1)
+            if b is None:
+                self.history[:, k].copy_(t.expand(self.batch, -1))
+            else:
+                self.history[b, k].copy_(t)
+        self.set_history_count(len(frames))
+
+    def append_history_from_mapped(self) -> None:
+        """history[n] = current mapped volume (TPP frame hand-off, on device)."""
+        if self.max_history == 0:
+            return
+        if self.n_history >= self.max_history:
+            raise ValueError("TV history capacity exceeded")
+        self.history[:, self.n_history].copy_(self.mapped)
+        self.set_history_count(self.n_history + 1)
+
+    def set_history_count(self, n: int) -> None:
+        self.n_history = int(n)
+        if self._bound:
+            torch.cuda.current_stream().synchronize()
+            N.check(N.lib().d2ip_engine_set_history(self._h, self.n_history), "set_history")
+
+    # -- execution ----------------------------------------------------------
+    def reset_frame(self) -> None:
+        self._bind()
+        N.check(N.lib().d2ip_engine_reset_frame(self._h, N.C.c_void_p(_stream_ptr())), "reset_frame")
+
+    def run(self, iters: int, graph: bool = True) -> None:
+        self._bind()
+        L = N.lib()
+        s = N.C.c_void_p(_stream_ptr())
+        if iters <= 0:
+            return
+        if graph:
+            N.check(L.d2ip_engine_run(self._h, int(iters), s), "engine_run")
+        else:
+            for _ in range(iters):
+                N.check(L.d2ip_engine_step(self._h, s), "engine_step")
+
+    def forward(self, with_loss: bool = False) -> None:
+        self._bind()
+        N.check(N.lib().d2ip_engine_forward(self._h, 1 if with_loss else 0, N.C.c_void_p(_stream_ptr())),
+                "engine_forward")
+
+    def grads(self) -> None:
+        self._bind()
+        N.check(N.lib().d2ip_engine_grads(self._h, N.C.c_void_p(_stream_ptr())), "engine_grads")
+
+    def predict(self) -> torch.Tensor:
+        """y = J sigma for every sequence: [B][M] device fp32."""
+        self._bind()
+        y = torch.empty((self.batch, self.M), dtype=torch.float32, device="cuda")
+        N.check(N.lib().d2ip_engine_predict(self._h, N.C.c_void_p(y.data_ptr()), N.C.c_void_p(_stream_ptr())),
+                "engine_predict")
+        return y
+
+    def launches_per_iter(self) -> int:
+        return int(N.lib().d2ip_engine_launches_per_iter(self._h))
+
+    # -- outputs ------------------------------------------------------------
+    def status_host(self) -> np.ndarray:
+        return self.status.cpu().numpy()
+
+    def trace_host(self, b: int, n: int) -> np.ndarray:
+        return self.trace[b, :n].cpu().numpy()
+
+    def theta_state(self, b: int = 0, iteration_counter: int = 0, provenance: str = "kaiming_init"):
+        return state_from_flat(self.theta[b], self.schema, iteration_counter, provenance)
+
+    def grads_state(self, b: int = 0):
+        return {e.name: t for e, t in zip(self.schema, torch.split(self.grad[b].cpu(), [e.numel for e in self.schema]))}
+
+    def volume(self, b: int = 0) -> np.ndarray:
+        """(R, C, P) fp64 volume lo + (hi-lo)*sigmoid, affine map in float64
+        (pipeline.py:290-291)."""
+        lo, hi = self.output_map
+        s = self.sig[b].cpu().numpy().astype(np.float64).reshape(self.R, self.C, self.P)
+        return lo + (hi - lo) * s
+
+    def mapped_volume(self, b: int = 0) -> torch.Tensor:
+        return self.mapped[b].reshape(self.R, self.C, self.P)
+
+
+def trace_seconds(ticks: np.ndarray) -> np.ndarray:
+    """Device timestamps (int bits in a float32 array) -> seconds since the
+    frame's first iteration (wrap-safe)."""
+    t = np.asarray(ticks, dtype=np.float32).view(np.int32).astype(np.int64)
+    if t.size == 0:
+        return t.astype(np.float64)
+    d = (t - t[0]) % (1 << 31)
+    return d * TICK_S

@@ -1,0 +1,227 @@
+"""End-to-end parity of the B200 engine against the reference (golden
+fixtures written by the real d2ip package) and the CPU oracle.
+
+Bars (north star): single-step loss and parameter gradients within relative
+error 1e-3 in fp32/TF32; final reconstructions MSSIM >= 0.99 and relative data
+misfit within 2% of the reference's.
+"""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import GOLDEN
+from oracle import oracle_loss_and_grads
+from oracle.metrics import misfit, mssim
+from paper_2507_14046_b200 import (
+    FrameHistory,
+    ReconstructionAborted,
+    RunConfig,
+    TVWeights,
+    reconstruct_frame,
+    reconstruct_sequence,
+    upws_pretrain,
+)
+from paper_2507_14046_b200 import workloads as W
+from paper_2507_14046_b200.engine import DeviceNet
+from paper_2507_14046_b200.pipeline import loss, predict_measurements
+from paper_2507_14046_b200.priornet import ResUNetConfig, kaiming_flat, sample_noise_input, state_from_flat, param_schema
+
+pytestmark = pytest.mark.gpu
+
+GRAD_TOL = {"fp32": 1e-4, "tf32": 1e-3}
+
+
+def rel(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+@pytest.fixture(scope="module")
+def cfg0():
+    g = np.load(GOLDEN / "cfg0_step.npz")
+    spec = W.CONFIGS["cfg0"]
+    wl = W.make_workload(spec, seed=0)
+    noise = sample_noise_input(wl.grid, 0, spec.in_channels, 0.1)
+    return g, spec, wl, noise
+
+
+def _net(g, spec, wl, noise, prec, mode="l2sq", tv=(0.0, 1.0, 0.1, 1e-8), max_history=0, max_iters=512):
+    dn = DeviceNet(spec.network(), wl.grid.shape, wl.matrix.n_measurements, wl.matrix.mask,
+                   data_norm=mode, output_map=tuple(g["output_map"]), precision=prec, tv=tv,
+                   max_history=max_history, max_iters=max_iters)
+    dn.set_noise(noise.values)
+    dn.set_J_host(wl.matrix.values)
+    dn.set_theta(g["theta0"])
+    dn.set_dv(g["dv"])
+    return dn
+
+
+def test_init_matches_reference_kaiming(cfg0):
+    g, spec, wl, noise = cfg0
+    np.testing.assert_array_equal(kaiming_flat(spec.network(seed=1)).numpy(), g["theta0"])
+
+
+@pytest.mark.parametrize("prec", ["fp32", "tf32"])
+@pytest.mark.parametrize("mode", ["l2sq", "l2"])
+def test_step_loss_and_grads_vs_reference(cfg0, prec, mode):
+    g, spec, wl, noise = cfg0
+    dn = _net(g, spec, wl, noise, prec, mode)
+    dn.reset_frame()
+    dn.grads()
+    torch.cuda.synchronize()
+    data = float(dn.trace_host(0, 1)[0, 0])
+    assert data == pytest.approx(float(g[f"{mode}_data"]), rel=GRAD_TOL[prec])
+    assert rel(dn.grad[0].cpu().numpy(), g[f"{mode}_grads"]) < GRAD_TOL[prec]
+    # per-tensor check: every parameter tensor within the bar (norm-relative)
+    schema = param_schema(spec.network())
+    o = 0
+    gd = dn.grad[0].cpu().numpy()
+    for e in schema:
+        ref = g[f"{mode}_grads"][o:o + e.numel]
+        if np.linalg.norm(ref) > 1e-6 * np.linalg.norm(g[f"{mode}_grads"]):
+            assert rel(gd[o:o + e.numel], ref) < 10 * GRAD_TOL[prec], e.name
+        o += e.numel
+
+
+def test_tv_step_vs_reference(cfg0):
+    g, spec, wl, noise = cfg0
+    dn = _net(g, spec, wl, noise, "fp32", "l2", tv=(0.002, 1.0, 0.1, 1e-8), max_history=2)
+    dn.set_history(list(g["tv_history"]))
+    dn.reset_frame()
+    dn.grads()
+    torch.cuda.synchronize()
+    t = dn.trace_host(0, 1)[0]
+    assert float(t[1]) == pytest.approx(float(g["tv_reg"]), rel=1e-4)
+    assert float(t[2]) == pytest.approx(float(g["tv_total"]), rel=1e-4)
+    assert rel(dn.grad[0].cpu().numpy(), g["tv_grads"]) < 1e-4
+
+
+@pytest.mark.parametrize("k", [1, 10])
+def test_adam_trajectory_vs_reference(cfg0, k):
+    g, spec, wl, noise = cfg0
+    dn = _net(g, spec, wl, noise, "fp32")
+    dn.reset_frame()
+    dn.run(k)
+    torch.cuda.synchronize()
+    assert int(dn.status_host()[0, 0]) == k
+    assert rel(dn.theta[0].cpu().numpy(), g[f"theta{k}"]) < 1e-4
+    np.testing.assert_allclose(dn.trace_host(0, k)[:, 0], g[f"trace{k}"][:, 1], rtol=1e-3)
+
+
+def test_graph_replay_equals_eager(cfg0):
+    g, spec, wl, noise = cfg0
+    a = _net(g, spec, wl, noise, "fp32")
+    b = _net(g, spec, wl, noise, "fp32")
+    a.reset_frame(); a.run(5, graph=True)
+    b.reset_frame(); b.run(5, graph=False)
+    torch.cuda.synchronize()
+    assert torch.equal(a.theta, b.theta)  # deterministic kernels: bitwise
+
+
+@pytest.mark.parametrize("prec", ["fp32", "tf32"])
+def test_cfg0_full_run_vs_reference(cfg0, prec):
+    """BASELINE cfg0: 300 Adam iterations; MSSIM >= 0.99, misfit within 2%."""
+    g, spec, wl, noise = cfg0
+    cfg = W.run_config_for(spec, tuple(g["output_map"]), iters_warm=300, precision=prec)
+    cfg = RunConfig(**{**cfg.__dict__, "network": spec.network(seed=1)})
+    theta0 = state_from_flat(torch.from_numpy(g["theta0"]), param_schema(spec.network()))
+    vol, theta, trace = reconstruct_frame(theta0, wl.matrix, g["dv"], [], 300, cfg, noise)
+    ref = g["volume300"]
+    assert mssim(vol, ref) >= 0.99
+    qc = wl.matrix.columns_q()
+    m_dev, m_ref = misfit(wl.matrix.values, qc, vol, g["dv"]), misfit(wl.matrix.values, qc, ref, g["dv"])
+    assert abs(m_dev - m_ref) <= 0.02 * m_ref + 1e-6
+    assert len(trace) == 300 and trace.is_finite()
+
+
+def test_sequence_driver_vs_reference():
+    gq = np.load(GOLDEN / "seq_mini.npz")
+    spec = W.small_spec()
+    wl = W.make_workload(spec, seed=0)
+    cfg = RunConfig(iters_warm=12, iters_first=6, iters_next=4, learning_rate=1e-3,
+                    tv_weights=TVWeights(lambda_tv=0.0), seed=1, network=spec.network(),
+                    output_map=tuple(gq["output_map"]), data_norm="l2sq", precision="fp32")
+    res = reconstruct_sequence(wl.matrix, wl.voltages, cfg, wl.grid)
+    assert [s.provenance for s in res.provenance_chain] == list(gq["provenance"])
+    assert [f.iterations for f in res.frame_records] == list(gq["iterations"])
+    for prev, nxt in zip(res.frame_records, res.frame_records[1:]):
+        assert nxt.init_checksum == prev.final_checksum
+    np.testing.assert_array_equal(torch.cat([t.reshape(-1) for t in res.states["init"].tensors.values()]).numpy(),
+                                  gq["theta0"])
+    R = wl.grid.shape
+    for i in range(res.sequence.n_frames):
+        a = np.transpose(res.sequence.values[:, i].reshape(R[2], R[0], R[1]), (1, 2, 0))
+        b = np.transpose(gq["values"][:, i].reshape(R[2], R[0], R[1]), (1, 2, 0))
+        assert mssim(a, b) >= 0.99
+    assert rel(res.states["final"].flat().numpy(), gq["theta_final"]) < 1e-3
+
+
+def test_tv_sequence_vs_reference():
+    gq = np.load(GOLDEN / "seq_mini.npz")
+    spec = W.small_spec()
+    wl = W.make_workload(spec, seed=0)
+    from paper_2507_14046_b200.forward import VoltageSequence
+    cfg = RunConfig(iters_warm=12, iters_first=6, iters_next=4, learning_rate=1e-3, tv_weights=TVWeights(),
+                    seed=1, network=spec.network(), output_map=tuple(gq["output_map"]), data_norm="l2",
+                    precision="fp32")
+    res = reconstruct_sequence(wl.matrix, VoltageSequence(wl.voltages.frames[:3]), cfg, wl.grid)
+    for key in ("warm", "frame_2", "frame_3"):
+        np.testing.assert_allclose(res.traces[key].totals(), gq[f"tvtrace_{key}"][:, 2], rtol=1e-3)
+    assert rel(res.sequence.values, gq["tv_values"]) < 1e-3
+
+
+def test_divergence_reports_frame():
+    spec = W.small_spec()
+    wl = W.make_workload(spec, seed=0)
+    cfg = RunConfig(iters_warm=12, iters_first=6, iters_next=4, learning_rate=1e12, seed=1, network=spec.network(),
+                    output_map=wl.output_map, data_norm="l2sq", tv_weights=TVWeights(lambda_tv=0.0))
+    with pytest.raises(ReconstructionAborted) as info:
+        reconstruct_sequence(wl.matrix, wl.voltages, cfg, wl.grid)
+    assert info.value.frame_index >= 0
+
+
+def test_loss_and_predict_api(cfg0):
+    g, spec, wl, noise = cfg0
+    net = spec.network(seed=1)
+    theta = state_from_flat(torch.from_numpy(g["theta0"]), param_schema(net))
+    total, data, reg = loss(net, theta, noise, wl.matrix, g["dv"], weights=TVWeights(lambda_tv=0.0),
+                            output_map=tuple(g["output_map"]), data_norm="l2sq")
+    assert data == pytest.approx(float(g["l2sq_data"]), rel=1e-4) and reg == 0.0 and total == data
+    y = predict_measurements(net, theta, noise, wl.matrix, output_map=tuple(g["output_map"]))
+    total2, data2, _ = loss(net, theta, noise, wl.matrix, y, weights=TVWeights(lambda_tv=0.0),
+                            output_map=tuple(g["output_map"]), data_norm="l2sq")
+    assert data2 <= 1e-6 * data
+
+
+def test_batched_sequences_match_single():
+    """cfg3 path: B sequences with their own J / theta / Z in lockstep equal B separate runs."""
+    spec = W.small_spec(grid=(8, 8, 8), channels=(8, 16), in_channels=4, rings=(0.5,))
+    wls = [W.make_workload(spec, seed=s, frames=1) for s in range(3)]
+    net = spec.network()
+    nets = []
+    for s, wl in enumerate(wls):
+        dn = DeviceNet(net, wl.grid.shape, wl.matrix.n_measurements, wl.matrix.mask, output_map=(-0.6, 0.3),
+                       max_iters=8)
+        dn.set_noise(sample_noise_input(wl.grid, s, 4, 0.1).values)
+        dn.set_J_host(wl.matrix.values)
+        dn.set_theta(kaiming_flat(net, seed=s + 1))
+        dn.set_dv(wl.voltages.frames[0].values)
+        dn.reset_frame(); dn.run(5)
+        nets.append(dn)
+    bn = DeviceNet(net, wls[0].grid.shape, wls[0].matrix.n_measurements, wls[0].matrix.mask, batch=3,
+                   j_shared=False, output_map=(-0.6, 0.3), max_iters=8)
+    for s, wl in enumerate(wls):
+        bn.set_noise(sample_noise_input(wl.grid, s, 4, 0.1).values, b=s)
+        bn.set_J_host(wl.matrix.values, b=s)
+        bn.set_theta(kaiming_flat(net, seed=s + 1), b=s)
+        bn.set_dv(wl.voltages.frames[0].values, b=s)
+    bn.reset_frame(); bn.run(5)
+    torch.cuda.synchronize()
+    for s in range(3):
+        assert torch.equal(bn.theta[s], nets[s].theta[0])
+
+
+def test_smoke_entry():
+    import __graft_entry__
+    __graft_entry__.smoke()

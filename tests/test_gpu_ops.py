@@ -1,0 +1,242 @@
+"""Per-kernel parity on the B200 through the C ABI, against plain PyTorch fp32
+CPU references of the same op (the ops the reference runs through PyTorch:
+nn.Conv3d, ChannelLayerNorm, LeakyReLU, F.interpolate, mv, torch.optim.Adam).
+
+Tolerances (relative, ||dev - ref|| / ||ref||): 1e-5 for exact-fp32 kernels,
+2e-3 for TF32 tensor-core convolutions (10-bit mantissa operands, fp32
+accumulation), 1e-2 for bf16 operands — the north star's bars.
+"""
+
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+import torch.nn.functional as F
+
+from paper_2507_14046_b200 import _native as N
+
+pytestmark = pytest.mark.gpu
+
+TOL = {"fp32": 1e-5, "tf32": 2e-3, "bf16": 1e-2}
+
+
+def rel(a, b):
+    a = a.detach().double().cpu()
+    b = b.detach().double().cpu()
+    return float((a - b).norm() / max(b.norm(), 1e-30))
+
+
+def stream():
+    return C.c_void_p(torch.cuda.current_stream().cuda_stream)
+
+
+def to_ndhwc(x):  # [B][C][D][H][W] -> [B][D][H][W][C] cuda
+    return x.permute(0, 2, 3, 4, 1).contiguous().cuda()
+
+
+def from_ndhwc(t):
+    return t.permute(0, 4, 1, 2, 3).contiguous().cpu()
+
+
+def act_of(t, c=None, coff=0):
+    B, D, H, W, CS = t.shape
+    a = N.Act()
+    a.ptr = t.data_ptr() + coff * 4
+    a.d, a.h, a.w = D, H, W
+    a.c = CS if c is None else c
+    a.cstride = CS
+    a.bstride = D * H * W * CS
+    return a
+
+
+CONV_CASES = [
+    # cin, cout, ks, stride, spatial
+    (4, 8, 3, 1, (8, 8, 8)),
+    (8, 16, 3, 2, (8, 8, 8)),
+    (16, 16, 3, 1, (8, 8, 8)),
+    (24, 8, 3, 1, (8, 8, 16)),
+    (16, 32, 1, 2, (8, 8, 8)),
+    (48, 16, 1, 1, (4, 8, 8)),
+    (16, 1, 3, 1, (8, 8, 8)),
+    (64, 64, 3, 1, (4, 4, 4)),
+    (96, 32, 3, 1, (8, 8, 8)),
+]
+
+
+@pytest.mark.parametrize("prec", ["fp32", "tf32"])
+@pytest.mark.parametrize("cin,cout,ks,stride,sp", CONV_CASES)
+def test_conv3d_fwd(cin, cout, ks, stride, sp, prec):
+    torch.manual_seed(0)
+    B = 2
+    x = torch.randn(B, cin, *sp)
+    w = torch.randn(B, cout, cin, ks, ks, ks) * (2.0 / (cin * ks ** 3)) ** 0.5
+    b = torch.randn(B, cout)
+    ref = torch.stack([F.conv3d(x[i:i + 1], w[i], b[i], stride=stride, padding=ks // 2)[0] for i in range(B)])
+    # x lives in a wider channel buffer (channel-strided view)
+    pad = 8
+    xb = torch.zeros(B, *sp, cin + pad)
+    xb[..., pad:] = x.permute(0, 2, 3, 4, 1)
+    xb = xb.cuda()
+    params = torch.cat([torch.cat([w[i].reshape(-1), b[i]]) for i in range(B)]).cuda()
+    P = params.numel() // B
+    out = torch.zeros(B, *ref.shape[2:], cout, device="cuda")
+    xa = act_of(xb, cin, pad)
+    ya = act_of(out)
+    rc = N.lib().d2ip_conv3d_fwd(xa, C.c_void_p(params.data_ptr()), C.c_void_p(params.data_ptr() + cout * cin * ks ** 3 * 4),
+                                 P, ks, stride, ya, 0, N.PREC[prec], B, stream())
+    N.check(rc, "conv3d_fwd")
+    torch.cuda.synchronize()
+    assert rel(from_ndhwc(out), ref) < TOL[prec]
+    # accumulate mode adds on top
+    N.check(N.lib().d2ip_conv3d_fwd(xa, C.c_void_p(params.data_ptr()), None, P, ks, stride, ya, 1, N.PREC[prec], B,
+                                    stream()), "conv3d_fwd acc")
+    torch.cuda.synchronize()
+    ref2 = ref + (ref - b[:, :, None, None, None])
+    assert rel(from_ndhwc(out), ref2) < TOL[prec]
+
+
+@pytest.mark.parametrize("prec", ["fp32", "tf32"])
+@pytest.mark.parametrize("cin,cout,ks,stride,sp", CONV_CASES)
+def test_conv3d_dgrad_wgrad(cin, cout, ks, stride, sp, prec):
+    torch.manual_seed(1)
+    B = 2
+    x = torch.randn(B, cin, *sp, requires_grad=True)
+    w = (torch.randn(B, cout, cin, ks, ks, ks) * 0.2).requires_grad_(True)
+    b = torch.randn(B, cout, requires_grad=True)
+    y = torch.stack([F.conv3d(x[i:i + 1], w[i], b[i], stride=stride, padding=ks // 2)[0] for i in range(B)])
+    gy = torch.randn_like(y)
+    y.backward(gy)
+    gyd = to_ndhwc(gy)
+    params = torch.cat([torch.cat([w[i].detach().reshape(-1), b[i].detach()]) for i in range(B)]).cuda()
+    P = params.numel() // B
+    gx = torch.full((B, *sp, cin), 7.0, device="cuda")
+    N.check(N.lib().d2ip_conv3d_dgrad(act_of(gyd), C.c_void_p(params.data_ptr()), P, ks, stride, act_of(gx), 0,
+                                      N.PREC[prec], B, stream()), "dgrad")
+    xd = to_ndhwc(x.detach())
+    gw = torch.zeros(B, P, device="cuda")
+    ws_n = N.lib().d2ip_conv3d_wgrad_ws_bytes(act_of(xd), act_of(gyd), ks, B)
+    ws = torch.empty(max(ws_n, 1), dtype=torch.uint8, device="cuda")
+    N.check(N.lib().d2ip_conv3d_wgrad(act_of(xd), act_of(gyd), ks, stride, C.c_void_p(gw.data_ptr()), P,
+                                      C.c_void_p(ws.data_ptr()), ws_n, N.PREC[prec], B, stream()), "wgrad")
+    torch.cuda.synchronize()
+    assert rel(from_ndhwc(gx), x.grad) < TOL[prec]
+    ref_gw = torch.cat([torch.cat([w.grad[i].reshape(-1), b.grad[i]]) for i in range(B)]).reshape(B, P)
+    nW = cout * cin * ks ** 3
+    assert rel(gw[:, :nW].cpu(), ref_gw[:, :nW]) < TOL[prec]
+    assert rel(gw[:, nW:].cpu(), ref_gw[:, nW:]) < 1e-5
+
+
+def channel_ln(x, g, b):
+    xp = x.movedim(1, -1)
+    return F.layer_norm(xp, (xp.shape[-1],), g, b, 1e-5).movedim(-1, 1)
+
+
+@pytest.mark.parametrize("C_,res", [(8, False), (16, True), (48, True), (64, False)])
+def test_norm_act_fwd_bwd(C_, res):
+    torch.manual_seed(2)
+    B, sp = 2, (4, 8, 8)
+    y = torch.randn(B, C_, *sp, requires_grad=True)
+    g = (1 + 0.3 * torch.randn(B, C_)).requires_grad_(True)
+    be = (0.2 * torch.randn(B, C_)).requires_grad_(True)
+    r = torch.randn(B, C_, *sp)
+    out = torch.stack([F.leaky_relu(channel_ln(y[i:i + 1], g[i], be[i])[0] + (r[i] if res else 0), 0.2)
+                       for i in range(B)])
+    go = torch.randn_like(out)
+    out.backward(go)
+    yd, rd = to_ndhwc(y.detach()), to_ndhwc(r)
+    gam = torch.cat([torch.cat([g[i].detach(), be[i].detach()]) for i in range(B)]).cuda()
+    od = torch.zeros(B, *sp, C_, device="cuda")
+    V = int(np.prod(sp))
+    xh = torch.zeros(B, V, C_, device="cuda")
+    rs = torch.zeros(B, V, device="cuda")
+    L = N.lib()
+    N.check(L.d2ip_norm_act_fwd(act_of(yd), C.c_void_p(gam.data_ptr()), C.c_void_p(gam.data_ptr() + C_ * 4), 2 * C_,
+                                act_of(rd) if res else N.Act(), 1, 0.2, act_of(od), C.c_void_p(xh.data_ptr()),
+                                C.c_void_p(rs.data_ptr()), B, stream()), "norm fwd")
+    god = to_ndhwc(go)
+    gpre = torch.zeros_like(od)
+    gc = torch.zeros_like(od)
+    dgb = torch.zeros(B, 2 * C_, device="cuda")
+    wsn = L.d2ip_norm_act_bwd_ws_bytes(V, C_, B)
+    ws = torch.empty(wsn, dtype=torch.uint8, device="cuda")
+    N.check(L.d2ip_norm_act_bwd(act_of(god), act_of(od), 1, 0.2, C.c_void_p(xh.data_ptr()), C.c_void_p(rs.data_ptr()),
+                                C.c_void_p(gam.data_ptr()), 2 * C_, act_of(gpre), act_of(gc),
+                                C.c_void_p(dgb.data_ptr()), 2 * C_, C.c_void_p(ws.data_ptr()), wsn, B, stream()),
+            "norm bwd")
+    torch.cuda.synchronize()
+    assert rel(from_ndhwc(od), out.detach()) < 1e-5
+    assert rel(from_ndhwc(gc), y.grad) < 1e-4
+    assert rel(dgb[:, :C_].cpu(), g.grad) < 1e-4
+    assert rel(dgb[:, C_:].cpu(), be.grad) < 1e-5
+
+
+@pytest.mark.parametrize("sp", [(2, 2, 2), (4, 8, 8), (8, 4, 2)])
+def test_upsample2x(sp):
+    torch.manual_seed(3)
+    B, C_ = 2, 12
+    x = torch.randn(B, C_, *sp, requires_grad=True)
+    y = F.interpolate(x, scale_factor=2, mode="trilinear", align_corners=False)
+    gy = torch.randn_like(y)
+    y.backward(gy)
+    xd = to_ndhwc(x.detach())
+    big = torch.zeros(B, *[2 * s for s in sp], C_ + 4, device="cuda")  # slice of a concat buffer
+    L = N.lib()
+    N.check(L.d2ip_upsample2x_fwd(act_of(xd), act_of(big, C_, 0), B, stream()), "up fwd")
+    gyd = torch.zeros_like(big)
+    gyd[..., :C_] = to_ndhwc(gy)
+    gx = torch.zeros_like(xd)
+    N.check(L.d2ip_upsample2x_bwd(act_of(gyd, C_, 0), act_of(gx), 0, B, stream()), "up bwd")
+    torch.cuda.synchronize()
+    assert rel(from_ndhwc(big[..., :C_].contiguous()), y.detach()) < 1e-6
+    assert rel(from_ndhwc(gx), x.grad) < 1e-6
+
+
+@pytest.mark.parametrize("M,V,B", [(208, 3328, 1), (928, 25984, 1), (37, 1001, 3)])
+def test_jacobian_fwd_adj(M, V, B):
+    torch.manual_seed(4)
+    Vp = (V + 3) // 4 * 4
+    J = torch.zeros(B, M, Vp)
+    J[..., :V] = torch.randn(B, M, V)
+    s = torch.zeros(B, Vp)
+    s[:, :V] = torch.randn(B, V)
+    r = torch.randn(B, M)
+    Jd, sd, rd = J.cuda(), s.cuda(), r.cuda()
+    L = N.lib()
+    nseg = L.d2ip_jac_nseg(Vp)
+    part = torch.zeros(B, M, nseg, device="cuda")
+    N.check(L.d2ip_jac_fwd(C.c_void_p(Jd.data_ptr()), M * Vp, C.c_void_p(sd.data_ptr()), Vp, M, Vp,
+                           C.c_void_p(part.data_ptr()), nseg, B, stream()), "jac fwd")
+    g = torch.zeros(B, Vp, device="cuda")
+    wsn = L.d2ip_jac_adj_ws_bytes(M, Vp, B)
+    ws = torch.empty(wsn, dtype=torch.uint8, device="cuda")
+    N.check(L.d2ip_jac_adj(C.c_void_p(Jd.data_ptr()), M * Vp, C.c_void_p(rd.data_ptr()), M, Vp,
+                           C.c_void_p(g.data_ptr()), Vp, C.c_void_p(ws.data_ptr()), wsn, B, stream()), "jac adj")
+    torch.cuda.synchronize()
+    y = part.sum(-1).cpu()
+    assert rel(y, torch.einsum("bmv,bv->bm", J, s)) < 1e-5
+    assert rel(g.cpu(), torch.einsum("bmv,bm->bv", J, r)) < 1e-5
+
+
+def test_adam_matches_torch():
+    torch.manual_seed(5)
+    n = 1003
+    p0 = torch.randn(n)
+    p = p0.clone().requires_grad_(True)
+    opt = torch.optim.Adam([p], lr=1e-3, betas=(0.9, 0.999))
+    pd = p0.clone().cuda()
+    md = torch.zeros(n, device="cuda")
+    vd = torch.zeros(n, device="cuda")
+    step = torch.zeros(1, dtype=torch.int32, device="cuda")
+    L = N.lib()
+    for k in range(1, 6):
+        g = torch.randn(n)
+        p.grad = g.clone()
+        opt.step()
+        step.fill_(k)
+        gd = g.cuda()
+        N.check(L.d2ip_adam(C.c_void_p(pd.data_ptr()), C.c_void_p(gd.data_ptr()), C.c_void_p(md.data_ptr()),
+                            C.c_void_p(vd.data_ptr()), n, 1e-3, 0.9, 0.999, 1e-8, C.c_void_p(step.data_ptr()),
+                            stream()), "adam")
+    torch.cuda.synchronize()
+    assert rel(pd.cpu(), p.detach()) < 1e-6
