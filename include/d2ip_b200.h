@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define D2IP_ABI_VERSION 1
+#define D2IP_ABI_VERSION 2
 
 enum {
   D2IP_OK = 0,
@@ -64,16 +64,20 @@ const char* d2ip_last_variant(void);
 /* ---- K1: 3^3 / 1^3 convolution forward ---------------------------------
  * y = conv3d(x, W, b) (+ y if accumulate). ksize 3 -> padding 1, ksize 1 ->
  * padding 0; stride 1 or 2. Replaces `nn.Conv3d` forward
- * (priornet.py:117,143,200,215 / oracle ConfigResUNet). */
+ * (priornet.py:117,143,200,215 / oracle ConfigResUNet). precision TF32 on a
+ * stride-1 3^3 layer runs the tcgen05 implicit GEMM, whose packed weights
+ * need `d2ip_conv3d_ws_bytes()` of workspace (0 for the direct kernels). */
+size_t d2ip_conv3d_ws_bytes(int cin, int cout, int ksize, int stride, int precision, int batch);
 int d2ip_conv3d_fwd(d2ip_act x, const float* w, const float* bias, long long wbstride,
                     int ksize, int stride, d2ip_act y, int accumulate, int precision,
-                    int batch, void* stream);
+                    void* ws, size_t ws_bytes, int batch, void* stream);
 
 /* ---- K2: convolution data gradient -------------------------------------
  * gx (+)= conv_transpose(gy, W). Replaces autograd's conv backward (input)
  * triggered by `total.backward()` (pipeline.py:330). */
 int d2ip_conv3d_dgrad(d2ip_act gy, const float* w, long long wbstride, int ksize, int stride,
-                      d2ip_act gx, int accumulate, int precision, int batch, void* stream);
+                      d2ip_act gx, int accumulate, int precision, void* ws, size_t ws_bytes,
+                      int batch, void* stream);
 
 /* ---- K3: convolution weight + bias gradient ----------------------------
  * gw = sum_v gy (x) x-patch  (OIDHW), gb = sum_v gy; written to gw[0 ..

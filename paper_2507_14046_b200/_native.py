@@ -14,7 +14,7 @@ from pathlib import Path
 from .errors import NativeLibraryError
 
 LIB_PATH = Path(__file__).resolve().parent / "_d2ip_b200.so"
-ABI_VERSION = 1
+ABI_VERSION = 2
 
 PREC = {"fp32": 0, "tf32": 1, "bf16": 2}
 NORM = {"l2sq": 0, "l2": 1}
@@ -93,10 +93,11 @@ _SIGS = {
     "d2ip_abi_version": (C.c_int, []),
     "d2ip_last_error": (C.c_char_p, []),
     "d2ip_last_variant": (C.c_char_p, []),
+    "d2ip_conv3d_ws_bytes": (C.c_size_t, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int]),
     "d2ip_conv3d_fwd": (C.c_int, [Act, C.c_void_p, C.c_void_p, C.c_longlong, C.c_int, C.c_int, Act, C.c_int,
-                                  C.c_int, C.c_int, C.c_void_p]),
+                                  C.c_int, C.c_void_p, C.c_size_t, C.c_int, C.c_void_p]),
     "d2ip_conv3d_dgrad": (C.c_int, [Act, C.c_void_p, C.c_longlong, C.c_int, C.c_int, Act, C.c_int, C.c_int,
-                                    C.c_int, C.c_void_p]),
+                                    C.c_void_p, C.c_size_t, C.c_int, C.c_void_p]),
     "d2ip_conv3d_wgrad_ws_bytes": (C.c_size_t, [Act, Act, C.c_int, C.c_int]),
     "d2ip_conv3d_wgrad": (C.c_int, [Act, Act, C.c_int, C.c_int, C.c_void_p, C.c_longlong, C.c_void_p, C.c_size_t,
                                     C.c_int, C.c_int, C.c_void_p]),

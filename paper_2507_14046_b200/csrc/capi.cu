@@ -17,19 +17,14 @@ void set_error(const char* fmt, ...) {
 }
 void set_variant(const char* name) { g_variant = name; }
 
-// Convolution dispatch: tcgen05 implicit GEMM where the shape and precision
-// allow it, the exact-fp32 direct kernel otherwise (C_out = 1 tail, odd C_in,
-// or precision FP32).
-int conv_fwd(d2ip_act x, const float* w, const float* bias, long long wbs, int ks, int stride,
-             d2ip_act y, int accumulate, int precision, int batch, cudaStream_t st) {
-  if (conv_tc_supported(x.c, y.c, ks, stride, precision))
-    return conv_fwd_tc(x, w, bias, wbs, ks, stride, y, accumulate, precision, batch, st);
-  return conv_fwd_direct(x, w, bias, wbs, ks, stride, y, accumulate, batch, st);
-}
-
-int conv_dgrad(d2ip_act gy, const float* w, long long wbs, int ks, int stride, d2ip_act gx,
-               int accumulate, int precision, int batch, cudaStream_t st) {
-  return conv_dgrad_direct(gy, w, wbs, ks, stride, gx, accumulate, batch, st);
+// Convolution dispatch for the standalone ABI: tcgen05 implicit GEMM where the
+// shape and precision allow it (weights packed into the caller's workspace),
+// the exact-fp32 direct kernel otherwise (C_out = 1 tail, stride 2, 1^3,
+// C_in not a multiple of 8, or precision FP32).
+static size_t conv_ws(int cin, int cout, int ks, int stride, int precision, int batch, int dgrad) {
+  const int K = dgrad ? cout : cin, N = dgrad ? cin : cout;
+  if (!conv_tc_supported(K, N, ks, stride, precision)) return 0;
+  return (size_t)batch * conv_tc_pack_floats(K, N) * sizeof(float);
 }
 
 size_t conv_wgrad_ws(int cin, int cout, int ks, long long V, int batch, int precision) {
@@ -63,16 +58,39 @@ int d2ip_abi_version(void) { return D2IP_ABI_VERSION; }
 const char* d2ip_last_error(void) { return d2ip::g_err; }
 const char* d2ip_last_variant(void) { return d2ip::g_variant; }
 
+size_t d2ip_conv3d_ws_bytes(int cin, int cout, int ksize, int stride, int precision, int batch) {
+  const size_t a = d2ip::conv_ws(cin, cout, ksize, stride, precision, batch, 0);
+  const size_t b = d2ip::conv_ws(cin, cout, ksize, stride, precision, batch, 1);
+  return a > b ? a : b;
+}
+
 int d2ip_conv3d_fwd(d2ip_act x, const float* w, const float* bias, long long wbstride, int ksize, int stride,
-                    d2ip_act y, int accumulate, int precision, int batch, void* stream) {
-  D2IP_RET(d2ip::check_conv_shapes(x, y, ksize, stride));
-  return d2ip::conv_fwd(x, w, bias, wbstride, ksize, stride, y, accumulate, precision, batch, d2ip::S(stream));
+                    d2ip_act y, int accumulate, int precision, void* ws, size_t ws_bytes, int batch,
+                    void* stream) {
+  using namespace d2ip;
+  D2IP_RET(check_conv_shapes(x, y, ksize, stride));
+  if (conv_tc_supported(x.c, y.c, ksize, stride, precision)) {
+    D2IP_CHECK_ARG(ws && ws_bytes >= conv_ws(x.c, y.c, ksize, stride, precision, batch, 0),
+                   "conv3d_fwd: workspace too small for the packed weights");
+    float* pk = reinterpret_cast<float*>(ws);
+    D2IP_RET(conv_tc_pack(w, wbstride, x.c, y.c, 0, pk, batch, S(stream)));
+    return conv_tc_run(x, pk, x.c, y.c, bias, wbstride, y, accumulate, batch, S(stream));
+  }
+  return conv_fwd_direct(x, w, bias, wbstride, ksize, stride, y, accumulate, batch, S(stream));
 }
 
 int d2ip_conv3d_dgrad(d2ip_act gy, const float* w, long long wbstride, int ksize, int stride, d2ip_act gx,
-                      int accumulate, int precision, int batch, void* stream) {
-  D2IP_RET(d2ip::check_conv_shapes(gx, gy, ksize, stride));
-  return d2ip::conv_dgrad(gy, w, wbstride, ksize, stride, gx, accumulate, precision, batch, d2ip::S(stream));
+                      int accumulate, int precision, void* ws, size_t ws_bytes, int batch, void* stream) {
+  using namespace d2ip;
+  D2IP_RET(check_conv_shapes(gx, gy, ksize, stride));
+  if (conv_tc_supported(gy.c, gx.c, ksize, stride, precision)) {
+    D2IP_CHECK_ARG(ws && ws_bytes >= conv_ws(gx.c, gy.c, ksize, stride, precision, batch, 1),
+                   "conv3d_dgrad: workspace too small for the packed weights");
+    float* pk = reinterpret_cast<float*>(ws);
+    D2IP_RET(conv_tc_pack(w, wbstride, gy.c, gx.c, 1, pk, batch, S(stream)));
+    return conv_tc_run(gy, pk, gy.c, gx.c, nullptr, 0, gx, accumulate, batch, S(stream));
+  }
+  return conv_dgrad_direct(gy, w, wbstride, ksize, stride, gx, accumulate, batch, S(stream));
 }
 
 size_t d2ip_conv3d_wgrad_ws_bytes(d2ip_act x, d2ip_act gy, int ksize, int batch) {

@@ -1,15 +1,273 @@
-// tcgen05 implicit-GEMM convolutions (placeholder until the kernel lands).
+// K1 / K2: stride-1 3x3x3 convolution as a tcgen05 implicit GEMM (TF32
+// operands, FP32 accumulation in TMEM). Replaces nn.Conv3d forward and the
+// data gradient of autograd's conv backward (priornet.py:117,200,215;
+// pipeline.py:330) for every stride-1 3^3 layer of the ResUNet.
+//
+// GEMM view (no im2col): rows are positions u of a *virtual* zero-padded
+// grid (D+2)(H+2)(W+2), u = ((d+1)*Sh + (h+1)*Sw + (w+1)), Sh=(H+2)(W+2),
+// Sw=W+2; a tap (kd,kh,kw) is the constant row shift
+// (kd-1)*Sh + (kh-1)*Sw + (kw-1). One CTA owns 128 consecutive rows (the
+// TMEM accumulator: 128 lanes x N fp32 columns) and all N output channels.
+// For each plane tap kd it stages one window of 128 + 2*Sw + 2 input rows
+// (x CB channels) in shared memory in the UMMA K-major "interleaved" layout
+// ([channel chunk][row][16 B]); the nine (kh,kw) taps are then nine
+// descriptors into the same window, shifted by kh*Sw + kw rows — the input is
+// read once per plane tap, never expanded 27x. Weights arrive pre-packed
+// ([tap][chunk][N][16 B], N padded to 16) so B tiles are contiguous copies.
+// Border rows of the virtual grid are computed and discarded by the
+// epilogue. The data gradient is the same kernel on gy with the flipped,
+// transposed weight packing (conv_transpose stride 1 == conv with W^T[26-t]).
+//
+// Pipeline: 2 smem stages filled with cp.async (16 B, zero-fill outside the
+// grid) by all 128 threads; thread 0 issues the MMAs of a stage and commits
+// them to that stage's mbarrier, which gates the refill of the buffer.
 #include "common.cuh"
 #include "kernels.h"
+#include "tc.cuh"
 
 namespace d2ip {
 
-bool conv_tc_supported(int, int, int, int, int) { return false; }
+constexpr int kTcThreads = 128;
+constexpr int kTcRows = 128;
+constexpr size_t kTcStageBudget = 110 * 1024;  // both stages; allows 2 CTAs/SM
 
-int conv_fwd_tc(d2ip_act, const float*, const float*, long long, int, int, d2ip_act, int, int, int,
-                cudaStream_t) {
-  set_error("tcgen05 conv not built");
-  return D2IP_E_UNSUPPORTED;
+static inline int np_of(int n) { return (n + 15) / 16 * 16; }
+static inline int wr_of(int sw) { return kTcRows + 2 * sw + 2; }
+static inline int wrp_of(int wr) { return wr + ((1 - wr) % 8 + 8) % 8; }  // = 1 mod 8: conflict-free fills
+
+struct TcConv {
+  d2ip_act x;
+  const float* wp;
+  long long wpbs;
+  const float* bias;
+  long long bbs;
+  d2ip_act y;
+  int accumulate;
+  int N, Np, Kc, CB, n_cb, WR, WRp, Sw, Sh, u_first, tmem_cols;
+  uint32_t idesc;
+};
+
+static int choose_cb(int kc, int np, int wrp) {
+  int best = 0;
+  for (int cb = 8; cb <= kc; cb *= 2) {
+    if (kc % cb) continue;
+    const size_t a = (size_t)cb * wrp * 4, b = (size_t)9 * cb * np * 4;
+    if (2 * (a + b) <= kTcStageBudget) best = cb;
+  }
+  return best;
+}
+
+static size_t tc_smem_bytes(const TcConv& a) {
+  const size_t A = (size_t)a.CB * a.WRp * 4, B = (size_t)9 * a.CB * a.Np * 4;
+  return 2 * (A + B) + 3 * a.WR * sizeof(int) + 64;
+}
+
+__global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int b = blockIdx.y;
+  const int u0 = a.u_first + blockIdx.x * kTcRows;
+  const int nkc = a.CB >> 2;
+  const size_t Abytes = (size_t)a.CB * a.WRp * 4, Bbytes = (size_t)9 * a.CB * a.Np * 4;
+  uint8_t* Abuf[2] = {smem, smem + Abytes};
+  uint8_t* Bbuf[2] = {smem + 2 * Abytes, smem + 2 * Abytes + Bbytes};
+  int* rowmap = reinterpret_cast<int*>(smem + 2 * (Abytes + Bbytes));
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(rowmap + 3 * a.WR + ((3 * a.WR) & 1));
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(mbar + 2);
+
+  if (warp == 0) tc::tmem_alloc(tslot, a.tmem_cols);
+  if (tid == 0) {
+    tc::mbar_init(&mbar[0], 1);
+    tc::mbar_init(&mbar[1], 1);
+    tc::fence_mbar_init();
+  }
+  // voxel offset of every window row for the three plane taps (-1 = padding)
+  const d2ip_act x = a.x;
+  for (int i = tid; i < 3 * a.WR; i += kTcThreads) {
+    const int kd = i / a.WR, r = i - kd * a.WR;
+    const int u = u0 + (kd - 1) * a.Sh - a.Sw - 1 + r;
+    int off = -1;
+    if (u >= 0) {
+      const int dp = u / a.Sh, rem = u - dp * a.Sh;
+      const int hp = rem / a.Sw, wp = rem - hp * a.Sw;
+      if (dp >= 1 && dp <= x.d && hp >= 1 && hp <= x.h && wp >= 1 && wp <= x.w)
+        off = ((dp - 1) * x.h + (hp - 1)) * x.w + (wp - 1);
+    }
+    rowmap[i] = off;
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tslot;
+  const float* xb = x.ptr + b * x.bstride;
+  const float* wpb = a.wp + b * a.wpbs;
+  const int S = 3 * a.n_cb;
+
+  auto load = [&](int s, int buf) {
+    const int kd = s / a.n_cb, cb = s - kd * a.n_cb;
+    const int* rm = rowmap + kd * a.WR;
+    uint8_t* A = Abuf[buf];
+    const int nA = a.WR * nkc;
+    for (int i = tid; i < nA; i += kTcThreads) {
+      const int r = i / nkc, kc = i - r * nkc;  // nkc is a power of two
+      const int off = rm[r];
+      const float* src = off >= 0 ? xb + (long long)off * x.cstride + cb * a.CB + 4 * kc : xb;
+      tc::cp_async16(A + ((size_t)kc * a.WRp + r) * 16, src, off >= 0 ? 16u : 0u);
+    }
+    uint8_t* Bt = Bbuf[buf];
+    const int per_tap = nkc * a.Np;  // 16-B units per tap in this stage
+    const int nB = 9 * per_tap;
+    const int kc_all = a.Kc >> 2;
+    for (int i = tid; i < nB; i += kTcThreads) {
+      const int t9 = i / per_tap, rem = i - t9 * per_tap;
+      const float* src = wpb + ((long long)((kd * 9 + t9) * kc_all + cb * nkc) * a.Np + rem) * 4;
+      tc::cp_async16(Bt + (size_t)i * 16, src, 16u);
+    }
+    tc::cp_async_commit();
+  };
+
+  load(0, 0);
+  for (int s = 0; s < S; ++s) {
+    const int buf = s & 1;
+    if (s + 1 < S) {
+      const int nb = (s + 1) & 1;
+      if (s + 1 >= 2) tc::mbar_wait(&mbar[nb], ((s - 1) >> 1) & 1);  // MMAs of stage s-1 done with nb
+      load(s + 1, nb);
+      tc::cp_async_wait<1>();
+    } else {
+      tc::cp_async_wait<0>();
+    }
+    tc::fence_proxy_async();
+    __syncthreads();
+    if (tid == 0) {
+      tc::fence_after();
+      const uint32_t abase = tc::smem_u32(Abuf[buf]), bbase = tc::smem_u32(Bbuf[buf]);
+      for (int t9 = 0; t9 < 9; ++t9) {
+        const int rowoff = (t9 / 3) * a.Sw + (t9 % 3);
+        for (int j = 0; j < (a.CB >> 3); ++j) {
+          const uint64_t ad = tc::make_desc(abase + (uint32_t)((2 * j * a.WRp + rowoff) * 16), a.WRp * 16, 128);
+          const uint64_t bd = tc::make_desc(bbase + (uint32_t)((t9 * nkc + 2 * j) * a.Np * 16), a.Np * 16, 128);
+          tc::mma_tf32(tmem, ad, bd, a.idesc, (s | t9 | j) ? 1u : 0u);
+        }
+      }
+      tc::commit(&mbar[buf]);
+    }
+  }
+  tc::mbar_wait(&mbar[(S - 1) & 1], ((S - 1) >> 1) & 1);
+  tc::fence_after();
+
+  // epilogue: TMEM lane = GEMM row; each thread owns one row / voxel.
+  const int row = warp * 32 + lane;
+  const int u = u0 + row;
+  int v = -1;
+  {
+    const int dp = u / a.Sh, rem = u - dp * a.Sh;
+    const int hp = rem / a.Sw, wp = rem - hp * a.Sw;
+    if (dp >= 1 && dp <= x.d && hp >= 1 && hp <= x.h && wp >= 1 && wp <= x.w)
+      v = ((dp - 1) * x.h + (hp - 1)) * x.w + (wp - 1);
+  }
+  const d2ip_act y = a.y;
+  float* yp = v >= 0 ? y.ptr + b * y.bstride + (long long)v * y.cstride : nullptr;
+  const float* bias = a.bias ? a.bias + b * a.bbs : nullptr;
+  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+  for (int c0 = 0; c0 < a.Np; c0 += 8) {
+    float vals[8];
+    tc::tmem_ld8(trow + c0, vals);
+    if (yp) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const int n = c0 + j;
+        if (n < a.N) {
+          float o = vals[j] + (bias ? __ldg(bias + n) : 0.f);
+          if (a.accumulate) o += yp[n];
+          yp[n] = o;
+        }
+      }
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_free(tmem, a.tmem_cols);
+}
+
+// Pack OIDHW weights into [b][tap][K/4][Np][4] (K-major B tiles).
+//   forward: K = C_in,  N = C_out:  P[t][k][n] = W[n][k][t]
+//   dgrad  : K = C_out, N = C_in :  P[t][k][n] = W[k][n][26 - t]
+__global__ void conv_tc_pack_k(const float* __restrict__ w, long long wbs, int K, int N, int Np, int dgrad,
+                               float* __restrict__ out, long long obs) {
+  const int b = blockIdx.y;
+  const long long total = 27LL * K * Np;
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= total) return;
+  const int j = (int)(i & 3);
+  const long long q = i >> 2;
+  const int n = (int)(q % Np);
+  const long long q2 = q / Np;
+  const int kc = (int)(q2 % (K / 4));
+  const int t = (int)(q2 / (K / 4));
+  const int k = 4 * kc + j;
+  float val = 0.f;
+  if (n < N) {
+    const float* wb = w + b * wbs;
+    val = dgrad ? wb[((long long)k * N + n) * 27 + (26 - t)] : wb[((long long)n * K + k) * 27 + t];
+  }
+  out[b * obs + i] = val;
+}
+
+bool conv_tc_supported(int cin, int cout, int ks, int stride, int precision) {
+  if (precision != D2IP_PREC_TF32 || ks != 3 || stride != 1) return false;
+  if (cin % 8 || cin < 8 || cout < 1 || np_of(cout) > 256) return false;
+  return true;
+}
+
+long long conv_tc_pack_floats(int K, int N) { return 27LL * K * np_of(N); }
+
+int conv_tc_pack(const float* w, long long wbs, int K, int N, int dgrad, float* out, int batch, cudaStream_t st) {
+  const long long total = conv_tc_pack_floats(K, N);
+  conv_tc_pack_k<<<dim3(cdiv(total, 256), batch), 256, 0, st>>>(w, wbs, K, N, np_of(N), dgrad, out, total);
+  D2IP_LAUNCH_CHECK();
+  return D2IP_OK;
+}
+
+int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, long long bbs, d2ip_act y,
+                int accumulate, int batch, cudaStream_t st) {
+  D2IP_CHECK_ARG(x.c == K && y.c == N, "conv_tc: channel mismatch");
+  D2IP_CHECK_ARG(x.cstride % 4 == 0 && ((uintptr_t)x.ptr & 15) == 0, "conv_tc: input view must be 16B aligned");
+  TcConv a{};
+  a.x = x;
+  a.wp = wp;
+  a.wpbs = conv_tc_pack_floats(K, N);
+  a.bias = bias;
+  a.bbs = bbs;
+  a.y = y;
+  a.accumulate = accumulate;
+  a.N = N;
+  a.Np = np_of(N);
+  a.Kc = K;
+  a.Sw = x.w + 2;
+  a.Sh = (x.h + 2) * a.Sw;
+  a.WR = wr_of(a.Sw);
+  a.WRp = wrp_of(a.WR);
+  a.CB = choose_cb(K, a.Np, a.WRp);
+  D2IP_CHECK_ARG(a.CB >= 8, "conv_tc: no channel blocking fits shared memory (K=%d N=%d W=%d)", K, N, x.w);
+  a.n_cb = K / a.CB;
+  a.u_first = a.Sh + a.Sw + 1;
+  const int u_last = x.d * a.Sh + x.h * a.Sw + x.w;
+  const int tiles = cdiv(u_last - a.u_first + 1, kTcRows);
+  int cols = 32;
+  while (cols < a.Np) cols *= 2;
+  a.tmem_cols = cols;
+  a.idesc = tc::make_idesc(2, kTcRows, a.Np);
+  const size_t smem = tc_smem_bytes(a);
+  static bool attr_set = false;
+  if (!attr_set) {
+    D2IP_CUDA(cudaFuncSetAttribute(conv_tc_k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    attr_set = true;
+  }
+  conv_tc_k<<<dim3(tiles, batch), kTcThreads, smem, st>>>(a);
+  set_variant("tcgen05_tf32");
+  D2IP_LAUNCH_CHECK();
+  return D2IP_OK;
 }
 
 }  // namespace d2ip

@@ -22,6 +22,9 @@ namespace d2ip {
 struct ConvP {
   long long ow = 0, ob = 0;
   int cin = 0, cout = 0, ks = 3, stride = 1;
+  bool tcf = false, tcd = false;  // tcgen05 forward / data-gradient path
+  float* pkf = nullptr;           // packed weights [B][27][cin/4][Np][4] (forward)
+  float* pkd = nullptr;           // packed flipped W^T (data gradient)
 };
 struct NormP {
   long long og = 0, ob = 0;
@@ -70,6 +73,7 @@ struct d2ip_engine {
   int nseg = 0, rsplit = 0, n_reg = 0;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t gexec = nullptr;
+  cudaStream_t cap_stream = nullptr;
   int launches = 0;
 };
 
@@ -224,6 +228,24 @@ static size_t plan_workspace(d2ip_engine& E, char* base) {
   E.na_ws_bytes = na;
   E.wg_ws = take(wg);
   E.na_ws = take(na);
+  // packed tcgen05 weight tiles, refreshed from theta at the start of every forward
+  auto packs = [&](ConvP& cv, bool need_dgrad) {
+    cv.tcf = conv_tc_supported(cv.cin, cv.cout, cv.ks, cv.stride, E.d.precision);
+    cv.tcd = need_dgrad && conv_tc_supported(cv.cout, cv.cin, cv.ks, cv.stride, E.d.precision);
+    cv.pkf = cv.tcf ? takef((long long)B * conv_tc_pack_floats(cv.cin, cv.cout)) : nullptr;
+    cv.pkd = cv.tcd ? takef((long long)B * conv_tc_pack_floats(cv.cout, cv.cin)) : nullptr;
+  };
+  packs(E.stem, false);
+  packs(E.tail, true);
+  for (auto* v : {&E.enc, &E.dec})
+    for (auto& bl : *v) {
+      packs(bl.c1, true);
+      packs(bl.c2, true);
+      packs(bl.sk, true);
+    }
+  packs(E.neck.c1, true);
+  packs(E.neck.c2, true);
+  packs(E.neck.sk, true);
   return (off + 255) & ~(size_t)255;
 }
 
@@ -274,6 +296,42 @@ struct Ctx {
   float* gr() const { return E.b.grad; }
 };
 
+static int cfwd(Ctx& k, const ConvP& c, d2ip_act x, d2ip_act y, int acc) {
+  if (c.tcf) return conv_tc_run(x, c.pkf, c.cin, c.cout, k.th() + c.ob, k.pbs, y, acc, k.B, k.st);
+  return conv_fwd_direct(x, k.th() + c.ow, k.th() + c.ob, k.pbs, c.ks, c.stride, y, acc, k.B, k.st);
+}
+
+static int cdgrad(Ctx& k, const ConvP& c, d2ip_act gy, d2ip_act gx, int acc) {
+  if (c.tcd) return conv_tc_run(gy, c.pkd, c.cout, c.cin, nullptr, 0, gx, acc, k.B, k.st);
+  return conv_dgrad_direct(gy, k.th() + c.ow, k.pbs, c.ks, c.stride, gx, acc, k.B, k.st);
+}
+
+static int cwgrad(Ctx& k, const ConvP& c, d2ip_act x, d2ip_act gy) {
+  return conv_wgrad(x, gy, c.ks, c.stride, k.gr() + c.ow, k.pbs, k.E.wg_ws, k.E.wg_ws_bytes, k.prec, k.B, k.st);
+}
+
+static int pack_one(Ctx& k, const ConvP& c) {
+  if (c.tcf) D2IP_RET(conv_tc_pack(k.th() + c.ow, k.pbs, c.cin, c.cout, 0, c.pkf, k.B, k.st));
+  if (c.tcd) D2IP_RET(conv_tc_pack(k.th() + c.ow, k.pbs, c.cout, c.cin, 1, c.pkd, k.B, k.st));
+  return D2IP_OK;
+}
+
+static int pack_all(Ctx& k) {
+  d2ip_engine& E = k.E;
+  D2IP_RET(pack_one(k, E.stem));
+  D2IP_RET(pack_one(k, E.tail));
+  for (auto* v : {&E.enc, &E.dec})
+    for (auto& bl : *v) {
+      D2IP_RET(pack_one(k, bl.c1));
+      D2IP_RET(pack_one(k, bl.c2));
+      D2IP_RET(pack_one(k, bl.sk));
+    }
+  D2IP_RET(pack_one(k, E.neck.c1));
+  D2IP_RET(pack_one(k, E.neck.c2));
+  D2IP_RET(pack_one(k, E.neck.sk));
+  return D2IP_OK;
+}
+
 static int block_fwd(Ctx& k, Block& bl) {
   d2ip_engine& E = k.E;
   const int co = bl.c1.cout;
@@ -281,10 +339,10 @@ static int block_fwd(Ctx& k, Block& bl) {
   d2ip_act raw2 = view(E, E.raw2, bl.lout, co, co);
   d2ip_act h1 = view(E, bl.h1, bl.lout, co, co);
   d2ip_act none{};
-  D2IP_RET(conv_fwd(bl.x, k.th() + bl.c1.ow, k.th() + bl.c1.ob, k.pbs, 3, bl.c1.stride, raw, 0, k.prec, k.B, k.st));
+  D2IP_RET(cfwd(k, bl.c1, bl.x, raw, 0));
   D2IP_RET(norm_act_fwd(raw, k.th() + bl.n1.og, k.th() + bl.n1.ob, k.pbs, none, 1, k.slope, h1, bl.xh1, bl.rs1, k.B, k.st));
-  D2IP_RET(conv_fwd(h1, k.th() + bl.c2.ow, k.th() + bl.c2.ob, k.pbs, 3, 1, raw, 0, k.prec, k.B, k.st));
-  D2IP_RET(conv_fwd(bl.x, k.th() + bl.sk.ow, k.th() + bl.sk.ob, k.pbs, 1, bl.sk.stride, raw2, 0, k.prec, k.B, k.st));
+  D2IP_RET(cfwd(k, bl.c2, h1, raw, 0));
+  D2IP_RET(cfwd(k, bl.sk, bl.x, raw2, 0));
   D2IP_RET(norm_act_fwd(raw, k.th() + bl.n2.og, k.th() + bl.n2.ob, k.pbs, raw2, 1, k.slope, bl.out, bl.xh2, bl.rs2, k.B, k.st));
   return D2IP_OK;
 }
@@ -297,14 +355,14 @@ static int block_bwd(Ctx& k, Block& bl) {
   d2ip_act h1 = view(E, bl.h1, bl.lout, co, co);
   D2IP_RET(norm_act_bwd(bl.gout, bl.out, 1, k.slope, bl.xh2, bl.rs2, k.th() + bl.n2.og, k.pbs, gpre, gc2,
                         k.gr() + bl.n2.og, k.pbs, E.na_ws, E.na_ws_bytes, k.B, k.st));
-  D2IP_RET(conv_wgrad(h1, gc2, 3, 1, k.gr() + bl.c2.ow, k.pbs, E.wg_ws, E.wg_ws_bytes, k.prec, k.B, k.st));
-  D2IP_RET(conv_dgrad(gc2, k.th() + bl.c2.ow, k.pbs, 3, 1, gh1, 0, k.prec, k.B, k.st));
+  D2IP_RET(cwgrad(k, bl.c2, h1, gc2));
+  D2IP_RET(cdgrad(k, bl.c2, gc2, gh1, 0));
   D2IP_RET(norm_act_bwd(gh1, h1, 1, k.slope, bl.xh1, bl.rs1, k.th() + bl.n1.og, k.pbs, gpre1, gc1,
                         k.gr() + bl.n1.og, k.pbs, E.na_ws, E.na_ws_bytes, k.B, k.st));
-  D2IP_RET(conv_wgrad(bl.x, gc1, 3, bl.c1.stride, k.gr() + bl.c1.ow, k.pbs, E.wg_ws, E.wg_ws_bytes, k.prec, k.B, k.st));
-  D2IP_RET(conv_wgrad(bl.x, gpre, 1, bl.sk.stride, k.gr() + bl.sk.ow, k.pbs, E.wg_ws, E.wg_ws_bytes, k.prec, k.B, k.st));
-  D2IP_RET(conv_dgrad(gc1, k.th() + bl.c1.ow, k.pbs, 3, bl.c1.stride, bl.gx, bl.gx_acc, k.prec, k.B, k.st));
-  D2IP_RET(conv_dgrad(gpre, k.th() + bl.sk.ow, k.pbs, 1, bl.sk.stride, bl.gx, 1, k.prec, k.B, k.st));
+  D2IP_RET(cwgrad(k, bl.c1, bl.x, gc1));
+  D2IP_RET(cwgrad(k, bl.sk, bl.x, gpre));
+  D2IP_RET(cdgrad(k, bl.c1, gc1, bl.gx, bl.gx_acc));
+  D2IP_RET(cdgrad(k, bl.sk, gpre, bl.gx, 1));
   return D2IP_OK;
 }
 
@@ -316,7 +374,8 @@ static int forward(Ctx& k) {
   d2ip_act raw = view(E, E.raw, 0, c[0], c[0]);
   d2ip_act a0 = view(E, E.cat[0] + c[1], 0, c[0], E.catw[0]);
   d2ip_act none{};
-  D2IP_RET(conv_fwd(z, k.th() + E.stem.ow, k.th() + E.stem.ob, k.pbs, 3, 1, raw, 0, k.prec, k.B, k.st));
+  D2IP_RET(pack_all(k));
+  D2IP_RET(cfwd(k, E.stem, z, raw, 0));
   D2IP_RET(norm_act_fwd(raw, k.th() + E.stem_n.og, k.th() + E.stem_n.ob, k.pbs, none, 1, k.slope, a0, E.stem_xh,
                         E.stem_rs, k.B, k.st));
   for (auto& bl : E.enc) D2IP_RET(block_fwd(k, bl));
@@ -367,8 +426,8 @@ static int backward(Ctx& k) {
   }
   d2ip_act gt = view(E, E.gtail, 0, 1, 1);
   Block& last = E.dec.back();
-  D2IP_RET(conv_wgrad(last.out, gt, 3, 1, k.gr() + E.tail.ow, k.pbs, E.wg_ws, E.wg_ws_bytes, k.prec, k.B, k.st));
-  D2IP_RET(conv_dgrad(gt, k.th() + E.tail.ow, k.pbs, 3, 1, last.gout, 0, k.prec, k.B, k.st));
+  D2IP_RET(cwgrad(k, E.tail, last.out, gt));
+  D2IP_RET(cdgrad(k, E.tail, gt, last.gout, 0));
   for (int j = (int)E.dec.size() - 1; j >= 0; --j) {
     Block& bl = E.dec[j];
     const int l = bl.lout;
@@ -387,7 +446,7 @@ static int backward(Ctx& k) {
   D2IP_RET(norm_act_bwd(ga0, a0, 1, k.slope, E.stem_xh, E.stem_rs, k.th() + E.stem_n.og, k.pbs, gpre, gc,
                         k.gr() + E.stem_n.og, k.pbs, E.na_ws, E.na_ws_bytes, k.B, k.st));
   d2ip_act z = view(E, const_cast<float*>(E.b.z), 0, E.d.in_channels, E.d.in_channels);
-  D2IP_RET(conv_wgrad(z, gc, 3, 1, k.gr() + E.stem.ow, k.pbs, E.wg_ws, E.wg_ws_bytes, k.prec, k.B, k.st));
+  D2IP_RET(cwgrad(k, E.stem, z, gc));
   return D2IP_OK;
 }
 
@@ -470,10 +529,13 @@ static void drop_graph(d2ip_engine& E) {
 int engine_run(d2ip_engine& E, int iters, void* stream) {
   cudaStream_t st = S(stream);
   if (!E.gexec) {
-    D2IP_CUDA(cudaStreamBeginCapture(st, cudaStreamCaptureModeThreadLocal));
-    int rc = engine_step(E, stream);
+    // Capture on a private non-blocking stream (the caller's stream may be the
+    // legacy default stream, which cannot be captured); replay on the caller's.
+    if (!E.cap_stream) D2IP_CUDA(cudaStreamCreateWithFlags(&E.cap_stream, cudaStreamNonBlocking));
+    D2IP_CUDA(cudaStreamBeginCapture(E.cap_stream, cudaStreamCaptureModeThreadLocal));
+    int rc = engine_step(E, E.cap_stream);
     cudaGraph_t g = nullptr;
-    cudaError_t ce = cudaStreamEndCapture(st, &g);
+    cudaError_t ce = cudaStreamEndCapture(E.cap_stream, &g);
     if (rc != D2IP_OK) {
       if (g) cudaGraphDestroy(g);
       return rc;
@@ -525,6 +587,7 @@ int d2ip_engine_create(const d2ip_net_desc* desc, d2ip_engine** out) {
 void d2ip_engine_destroy(d2ip_engine* e) {
   if (!e) return;
   d2ip::drop_graph(*e);
+  if (e->cap_stream) cudaStreamDestroy(e->cap_stream);
   delete e;
 }
 

@@ -18,14 +18,11 @@ int reduce_chunks(const float* partial, int nchunks, int n, float* out, long lon
 
 // conv_tc.cu — tcgen05 implicit-GEMM convolutions (tf32 / bf16 operands)
 bool conv_tc_supported(int cin, int cout, int ks, int stride, int precision);
-int conv_fwd_tc(d2ip_act x, const float* w, const float* bias, long long wbs, int ks, int stride,
-                d2ip_act y, int accumulate, int precision, int batch, cudaStream_t st);
+long long conv_tc_pack_floats(int K, int N);
+int conv_tc_pack(const float* w, long long wbs, int K, int N, int dgrad, float* out, int batch, cudaStream_t st);
+int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, long long bbs, d2ip_act y,
+                int accumulate, int batch, cudaStream_t st);
 
-// conv dispatch (conv_dispatch in capi.cu)
-int conv_fwd(d2ip_act x, const float* w, const float* bias, long long wbs, int ks, int stride,
-             d2ip_act y, int accumulate, int precision, int batch, cudaStream_t st);
-int conv_dgrad(d2ip_act gy, const float* w, long long wbs, int ks, int stride, d2ip_act gx,
-               int accumulate, int precision, int batch, cudaStream_t st);
 size_t conv_wgrad_ws(int cin, int cout, int ks, long long V, int batch, int precision);
 int conv_wgrad(d2ip_act x, d2ip_act gy, int ks, int stride, float* gw, long long gwbs, void* ws,
                size_t ws_bytes, int precision, int batch, cudaStream_t st);

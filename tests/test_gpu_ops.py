@@ -61,6 +61,11 @@ CONV_CASES = [
     (16, 1, 3, 1, (8, 8, 8)),
     (64, 64, 3, 1, (4, 4, 4)),
     (96, 32, 3, 1, (8, 8, 8)),
+    (48, 16, 3, 1, (32, 32, 32)),
+    (32, 32, 3, 1, (16, 16, 16)),
+    (8, 16, 3, 1, (32, 32, 32)),
+    (128, 128, 3, 1, (8, 8, 4)),
+    (192, 64, 3, 1, (16, 16, 8)),
 ]
 
 
@@ -83,14 +88,19 @@ def test_conv3d_fwd(cin, cout, ks, stride, sp, prec):
     out = torch.zeros(B, *ref.shape[2:], cout, device="cuda")
     xa = act_of(xb, cin, pad)
     ya = act_of(out)
-    rc = N.lib().d2ip_conv3d_fwd(xa, C.c_void_p(params.data_ptr()), C.c_void_p(params.data_ptr() + cout * cin * ks ** 3 * 4),
-                                 P, ks, stride, ya, 0, N.PREC[prec], B, stream())
+    L = N.lib()
+    wsn = L.d2ip_conv3d_ws_bytes(cin, cout, ks, stride, N.PREC[prec], B)
+    ws = torch.empty(max(wsn, 16), dtype=torch.uint8, device="cuda")
+    rc = L.d2ip_conv3d_fwd(xa, C.c_void_p(params.data_ptr()), C.c_void_p(params.data_ptr() + cout * cin * ks ** 3 * 4),
+                           P, ks, stride, ya, 0, N.PREC[prec], C.c_void_p(ws.data_ptr()), wsn, B, stream())
     N.check(rc, "conv3d_fwd")
     torch.cuda.synchronize()
+    if prec == "tf32" and ks == 3 and stride == 1 and cin % 8 == 0:
+        assert L.d2ip_last_variant() == b"tcgen05_tf32"
     assert rel(from_ndhwc(out), ref) < TOL[prec]
     # accumulate mode adds on top
-    N.check(N.lib().d2ip_conv3d_fwd(xa, C.c_void_p(params.data_ptr()), None, P, ks, stride, ya, 1, N.PREC[prec], B,
-                                    stream()), "conv3d_fwd acc")
+    N.check(L.d2ip_conv3d_fwd(xa, C.c_void_p(params.data_ptr()), None, P, ks, stride, ya, 1, N.PREC[prec],
+                              C.c_void_p(ws.data_ptr()), wsn, B, stream()), "conv3d_fwd acc")
     torch.cuda.synchronize()
     ref2 = ref + (ref - b[:, :, None, None, None])
     assert rel(from_ndhwc(out), ref2) < TOL[prec]
@@ -111,8 +121,10 @@ def test_conv3d_dgrad_wgrad(cin, cout, ks, stride, sp, prec):
     params = torch.cat([torch.cat([w[i].detach().reshape(-1), b[i].detach()]) for i in range(B)]).cuda()
     P = params.numel() // B
     gx = torch.full((B, *sp, cin), 7.0, device="cuda")
+    wsn = N.lib().d2ip_conv3d_ws_bytes(cin, cout, ks, stride, N.PREC[prec], B)
+    wsd = torch.empty(max(wsn, 16), dtype=torch.uint8, device="cuda")
     N.check(N.lib().d2ip_conv3d_dgrad(act_of(gyd), C.c_void_p(params.data_ptr()), P, ks, stride, act_of(gx), 0,
-                                      N.PREC[prec], B, stream()), "dgrad")
+                                      N.PREC[prec], C.c_void_p(wsd.data_ptr()), wsn, B, stream()), "dgrad")
     xd = to_ndhwc(x.detach())
     gw = torch.zeros(B, P, device="cuda")
     ws_n = N.lib().d2ip_conv3d_wgrad_ws_bytes(act_of(xd), act_of(gyd), ks, B)
