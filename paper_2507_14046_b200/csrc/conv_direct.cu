@@ -148,6 +148,89 @@ __global__ void __launch_bounds__(256) conv_wgrad_partial_k(d2ip_act x, d2ip_act
   partial[((long long)b * nchunks + c) * nE + e] = acc;
 }
 
+// Register-tiled split-K weight gradient: one thread owns a 4 (C_in) x COG
+// (C_out) tile of one tap (or, for tap == K3, COG bias entries) and streams
+// its chunk of output voxels, 1-2 float4 loads of gy and one float4 load of x
+// per 4*COG FMAs. Output layout matches conv_wgrad_partial_k (OIDHW + bias).
+template <int KS, int COG>
+__global__ void __launch_bounds__(128) conv_wgrad_tiled_k(d2ip_act x, d2ip_act gy, int stride,
+                                                          float* __restrict__ partial, int nchunks, int chunk) {
+  constexpr int K3 = Taps<KS>::K3, PAD = Taps<KS>::PAD;
+  const int b = blockIdx.z, c = blockIdx.y;
+  const int cin = x.c, cout = gy.c;
+  const int nci = cin >> 2, nco = cout / COG;
+  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int ngroups = (K3 + 1) * nci * nco;
+  if (gid >= ngroups) return;
+  const int cog = gid % nco;
+  const int rest = gid / nco;
+  const int ci4 = rest % nci;
+  const int t = rest / nci;
+  if (t == K3 && ci4 != 0) return;  // bias groups: one per co-group
+  const int co0 = cog * COG, ci0 = ci4 * 4;
+  const int nW = cout * cin * K3, nE = nW + cout;
+  const long long V = (long long)gy.d * gy.h * gy.w;
+  const long long v0 = (long long)c * chunk;
+  const long long v1 = min(V, v0 + chunk);
+  const float* gb = gy.ptr + b * gy.bstride + co0;
+  float acc[4][COG];
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < COG; ++j) acc[i][j] = 0.f;
+  if (t == K3) {
+    for (long long v = v0; v < v1; ++v) {
+      const float* g = gb + v * gy.cstride;
+#pragma unroll
+      for (int j = 0; j < COG; ++j) acc[0][j] += __ldg(g + j);
+    }
+    float* p = partial + ((long long)b * nchunks + c) * nE + nW + co0;
+#pragma unroll
+    for (int j = 0; j < COG; ++j) p[j] = acc[0][j];
+    return;
+  }
+  const int kd = t / (KS * KS), kh = (t / KS) % KS, kw = t % KS;
+  const float* xb = x.ptr + b * x.bstride + ci0;
+  int ow = (int)(v0 % gy.w), oh = (int)((v0 / gy.w) % gy.h), od = (int)(v0 / ((long long)gy.w * gy.h));
+  for (long long v = v0; v < v1; ++v) {
+    const int id = od * stride + kd - PAD, ih = oh * stride + kh - PAD, iw = ow * stride + kw - PAD;
+    if (id >= 0 && id < x.d && ih >= 0 && ih < x.h && iw >= 0 && iw < x.w) {
+      const float4 xv = __ldg(reinterpret_cast<const float4*>(xb + (((long long)id * x.h + ih) * x.w + iw) * x.cstride));
+      float g[COG];
+      const float* gp = gb + v * gy.cstride;
+      if constexpr (COG % 4 == 0) {
+#pragma unroll
+        for (int j = 0; j < COG; j += 4) {
+          const float4 q = __ldg(reinterpret_cast<const float4*>(gp + j));
+          g[j] = q.x; g[j + 1] = q.y; g[j + 2] = q.z; g[j + 3] = q.w;
+        }
+      } else {
+#pragma unroll
+        for (int j = 0; j < COG; ++j) g[j] = __ldg(gp + j);
+      }
+#pragma unroll
+      for (int j = 0; j < COG; ++j) {
+        acc[0][j] = fmaf(xv.x, g[j], acc[0][j]);
+        acc[1][j] = fmaf(xv.y, g[j], acc[1][j]);
+        acc[2][j] = fmaf(xv.z, g[j], acc[2][j]);
+        acc[3][j] = fmaf(xv.w, g[j], acc[3][j]);
+      }
+    }
+    if (++ow == gy.w) {
+      ow = 0;
+      if (++oh == gy.h) {
+        oh = 0;
+        ++od;
+      }
+    }
+  }
+  float* p = partial + ((long long)b * nchunks + c) * nE;
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < COG; ++j) p[((long long)(co0 + j) * cin + ci0 + i) * K3 + t] = acc[i][j];
+}
+
 __global__ void reduce_chunks_k(const float* __restrict__ partial, int nchunks, int n, float* out,
                                 long long obs) {
   const int b = blockIdx.y;
@@ -211,10 +294,10 @@ int conv_dgrad_direct(d2ip_act gy, const float* w, long long wbs, int ks, int st
   return D2IP_OK;
 }
 
-void wgrad_split(int nE, long long V, int batch, int* nchunks, int* chunk) {
-  long long target = 148LL * 2048 * 2;
-  long long want = (target + (long long)nE * batch - 1) / ((long long)nE * batch);
-  long long maxc = (V + 63) / 64;
+void wgrad_split(int nthreads, long long V, int batch, int* nchunks, int* chunk) {
+  long long target = 148LL * 2048;
+  long long want = (target + (long long)nthreads * batch - 1) / ((long long)nthreads * batch);
+  long long maxc = (V + 255) / 256;  // >= 256 voxels per chunk keeps the partials small
   if (want > maxc) want = maxc;
   if (want < 1) want = 1;
   int c = (int)((V + want - 1) / want);
@@ -226,7 +309,26 @@ size_t conv_wgrad_direct_ws(int cin, int cout, int ks, long long V, int batch) {
   const int nE = cout * cin * ks * ks * ks + cout;
   int nchunks, chunk;
   wgrad_split(nE, V, batch, &nchunks, &chunk);
-  return (size_t)batch * nchunks * nE * sizeof(float);
+  int most = nchunks;
+  for (int cog : {8, 4, 1}) {  // any tiled variant the views may select
+    if (cin % 4 || cout % cog) continue;
+    wgrad_split((ks * ks * ks + 1) * (cin / 4) * (cout / cog), V, batch, &nchunks, &chunk);
+    if (nchunks > most) most = nchunks;
+  }
+  return (size_t)batch * most * nE * sizeof(float);
+}
+
+static int tiled_cog(const d2ip_act& x, const d2ip_act& gy) {
+  const bool xa = x.c % 4 == 0 && x.cstride % 4 == 0 && ((uintptr_t)x.ptr & 15) == 0;
+  const bool ga = gy.cstride % 4 == 0 && ((uintptr_t)gy.ptr & 15) == 0;
+  if (!xa) return 0;
+  if (gy.c % 8 == 0 && ga) return 8;
+  if (gy.c % 4 == 0 && ga) return 4;
+  return 1;
+}
+
+static int tiled_threads(const d2ip_act& x, const d2ip_act& gy, int ks, int cog) {
+  return (ks * ks * ks + 1) * (x.c / 4) * (gy.c / cog);
 }
 
 int conv_wgrad_direct(d2ip_act x, d2ip_act gy, int ks, int stride, float* gw, long long gwbs,
@@ -234,6 +336,23 @@ int conv_wgrad_direct(d2ip_act x, d2ip_act gy, int ks, int stride, float* gw, lo
   const int nE = gy.c * x.c * ks * ks * ks + gy.c;
   const long long V = (long long)gy.d * gy.h * gy.w;
   int nchunks, chunk;
+  const int cog = tiled_cog(x, gy);
+  if (cog) {
+    const int nthr = tiled_threads(x, gy, ks, cog);
+    wgrad_split(nthr, V, batch, &nchunks, &chunk);
+    D2IP_CHECK_ARG(ws_bytes >= (size_t)batch * nchunks * nE * sizeof(float), "conv3d_wgrad: workspace too small");
+    float* partial = reinterpret_cast<float*>(ws);
+    dim3 grid(cdiv(nthr, 128), nchunks, batch);
+#define LAUNCH_T(KS_, COG_) conv_wgrad_tiled_k<KS_, COG_><<<grid, 128, 0, st>>>(x, gy, stride, partial, nchunks, chunk)
+    if (ks == 3) {
+      if (cog == 8) LAUNCH_T(3, 8); else if (cog == 4) LAUNCH_T(3, 4); else LAUNCH_T(3, 1);
+    } else {
+      if (cog == 8) LAUNCH_T(1, 8); else if (cog == 4) LAUNCH_T(1, 4); else LAUNCH_T(1, 1);
+    }
+#undef LAUNCH_T
+    D2IP_LAUNCH_CHECK();
+    return reduce_chunks(partial, nchunks, nE, gw, gwbs, batch, st);
+  }
   wgrad_split(nE, V, batch, &nchunks, &chunk);
   D2IP_CHECK_ARG(ws_bytes >= (size_t)batch * nchunks * nE * sizeof(float),
                  "conv3d_wgrad: workspace too small (%zu < %zu)", ws_bytes,

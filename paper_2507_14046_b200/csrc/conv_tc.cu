@@ -1,22 +1,30 @@
-// K1 / K2: stride-1 3x3x3 convolution as a tcgen05 implicit GEMM (TF32
-// operands, FP32 accumulation in TMEM). Replaces nn.Conv3d forward and the
-// data gradient of autograd's conv backward (priornet.py:117,200,215;
-// pipeline.py:330) for every stride-1 3^3 layer of the ResUNet.
+// K1 / K2: stride-1 3x3x3 convolution as a tcgen05 implicit GEMM on the TF32
+// tensor-core path with error compensation (3xTF32), FP32 accumulation in
+// TMEM. Replaces nn.Conv3d forward and the data gradient of autograd's conv
+// backward (priornet.py:117,200,215; pipeline.py:330) for every stride-1 3^3
+// layer of the ResUNet.
 //
 // GEMM view (no im2col): rows are positions u of a *virtual* zero-padded
 // grid (D+2)(H+2)(W+2), u = ((d+1)*Sh + (h+1)*Sw + (w+1)), Sh=(H+2)(W+2),
 // Sw=W+2; a tap (kd,kh,kw) is the constant row shift
 // (kd-1)*Sh + (kh-1)*Sw + (kw-1). One CTA owns 128 consecutive rows (the
 // TMEM accumulator: 128 lanes x N fp32 columns) and all N output channels.
-// For each plane tap kd it stages one window of 128 + 2*Sw + 2 input rows
-// (x CB channels) in shared memory in the UMMA K-major "interleaved" layout
-// ([channel chunk][row][16 B]); the nine (kh,kw) taps are then nine
-// descriptors into the same window, shifted by kh*Sw + kw rows — the input is
-// read once per plane tap, never expanded 27x. Weights arrive pre-packed
-// ([tap][chunk][N][16 B], N padded to 16) so B tiles are contiguous copies.
-// Border rows of the virtual grid are computed and discarded by the
-// epilogue. The data gradient is the same kernel on gy with the flipped,
-// transposed weight packing (conv_transpose stride 1 == conv with W^T[26-t]).
+// For each plane tap kd (and channel block) it stages one window of
+// 128 + 2*Sw + 2 input rows in shared memory in the UMMA K-major
+// "interleaved" layout ([channel chunk][row][16 B]); the nine (kh,kw) taps are
+// nine descriptors into the same window, shifted by kh*Sw + kw rows — the
+// input is read once per plane tap, never expanded 27x. Border rows of the
+// virtual grid are computed and discarded by the epilogue. The data gradient
+// is the same kernel on gy with the flipped, transposed weight packing
+// (conv_transpose at stride 1 == conv with W^T[26-t]).
+//
+// Precision: a single TF32 pass (10-bit mantissa operands) misses the 1e-3
+// gradient bar of the north star over a whole ResUNet backward (measured
+// ~6e-3). Each operand is split x = hi + lo with hi = x truncated to TF32 and
+// lo = x - hi; the kernel accumulates hi*hi + hi*lo + lo*hi, leaving only the
+// lo*lo term (~2^-22 relative) — FP32-level accuracy on the tensor cores.
+// Weights are split once per iteration by the pack kernel; the activation
+// window is split in shared memory after it lands.
 //
 // Pipeline: 2 smem stages filled with cp.async (16 B, zero-fill outside the
 // grid) by all 128 threads; thread 0 issues the MMAs of a stage and commits
@@ -37,41 +45,48 @@ static inline int wrp_of(int wr) { return wr + ((1 - wr) % 8 + 8) % 8; }  // = 1
 
 struct TcConv {
   d2ip_act x;
-  const float* wp;
+  const float* wp;  // packed [hi | lo] halves, each [27][K/4][Np][4]
   long long wpbs;
+  long long wlo;    // float offset of the lo half
   const float* bias;
   long long bbs;
   d2ip_act y;
   int accumulate;
-  int N, Np, Kc, CB, n_cb, WR, WRp, Sw, Sh, u_first, tmem_cols;
+  int N, Np, Ns, Kc, CB, n_cb, WR, WRp, Sw, Sh, u_first, tmem_cols;  // Ns: N columns per CTA (slice)
   uint32_t idesc;
 };
 
-static int choose_cb(int kc, int np, int wrp) {
+// Per stage: A hi + A lo windows, B hi + B lo tiles.
+static size_t stage_bytes(int cb, int np, int wrp) {
+  return 2 * ((size_t)cb * wrp * 4 + (size_t)9 * cb * np * 4);
+}
+
+static int choose_cb(int kc, int np, int wrp, size_t budget) {
   int best = 0;
   for (int cb = 8; cb <= kc; cb *= 2) {
     if (kc % cb) continue;
-    const size_t a = (size_t)cb * wrp * 4, b = (size_t)9 * cb * np * 4;
-    if (2 * (a + b) <= kTcStageBudget) best = cb;
+    if (2 * stage_bytes(cb, np, wrp) <= budget) best = cb;
   }
   return best;
 }
 
 static size_t tc_smem_bytes(const TcConv& a) {
-  const size_t A = (size_t)a.CB * a.WRp * 4, B = (size_t)9 * a.CB * a.Np * 4;
-  return 2 * (A + B) + 3 * a.WR * sizeof(int) + 64;
+  return 2 * stage_bytes(a.CB, a.Ns, a.WRp) + 3 * a.WR * sizeof(int) + 64;
 }
+
+__device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 
 __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-  const int b = blockIdx.y;
+  const int b = blockIdx.z;
+  const int n0 = blockIdx.y * a.Ns;  // first output channel of this CTA's slice
   const int u0 = a.u_first + blockIdx.x * kTcRows;
   const int nkc = a.CB >> 2;
-  const size_t Abytes = (size_t)a.CB * a.WRp * 4, Bbytes = (size_t)9 * a.CB * a.Np * 4;
-  uint8_t* Abuf[2] = {smem, smem + Abytes};
-  uint8_t* Bbuf[2] = {smem + 2 * Abytes, smem + 2 * Abytes + Bbytes};
-  int* rowmap = reinterpret_cast<int*>(smem + 2 * (Abytes + Bbytes));
+  const size_t Ab = (size_t)a.CB * a.WRp * 4, Bb = (size_t)9 * a.CB * a.Ns * 4;
+  const size_t Sb = 2 * (Ab + Bb);
+  // stage layout: [A hi][A lo][B hi][B lo]
+  int* rowmap = reinterpret_cast<int*>(smem + 2 * Sb);
   uint64_t* mbar = reinterpret_cast<uint64_t*>(rowmap + 3 * a.WR + ((3 * a.WR) & 1));
   uint32_t* tslot = reinterpret_cast<uint32_t*>(mbar + 2);
 
@@ -102,28 +117,45 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
   const float* xb = x.ptr + b * x.bstride;
   const float* wpb = a.wp + b * a.wpbs;
   const int S = 3 * a.n_cb;
+  const int nA = a.WR * nkc;
 
   auto load = [&](int s, int buf) {
     const int kd = s / a.n_cb, cb = s - kd * a.n_cb;
     const int* rm = rowmap + kd * a.WR;
-    uint8_t* A = Abuf[buf];
-    const int nA = a.WR * nkc;
+    uint8_t* A = smem + buf * Sb;
     for (int i = tid; i < nA; i += kTcThreads) {
       const int r = i / nkc, kc = i - r * nkc;  // nkc is a power of two
       const int off = rm[r];
       const float* src = off >= 0 ? xb + (long long)off * x.cstride + cb * a.CB + 4 * kc : xb;
       tc::cp_async16(A + ((size_t)kc * a.WRp + r) * 16, src, off >= 0 ? 16u : 0u);
     }
-    uint8_t* Bt = Bbuf[buf];
-    const int per_tap = nkc * a.Np;  // 16-B units per tap in this stage
+    uint8_t* Bt = smem + buf * Sb + 2 * Ab;
+    const int per_tap = nkc * a.Ns;  // 16-B units per tap in this stage
     const int nB = 9 * per_tap;
     const int kc_all = a.Kc >> 2;
     for (int i = tid; i < nB; i += kTcThreads) {
       const int t9 = i / per_tap, rem = i - t9 * per_tap;
-      const float* src = wpb + ((long long)((kd * 9 + t9) * kc_all + cb * nkc) * a.Np + rem) * 4;
+      const int kcl = rem / a.Ns, n = rem - kcl * a.Ns;
+      const float* src = wpb + ((long long)((kd * 9 + t9) * kc_all + cb * nkc + kcl) * a.Np + n0 + n) * 4;
       tc::cp_async16(Bt + (size_t)i * 16, src, 16u);
+      tc::cp_async16(Bt + Bb + (size_t)i * 16, src + a.wlo, 16u);
     }
     tc::cp_async_commit();
+  };
+  // split the landed activation window into hi (in place) and lo; every thread
+  // touches exactly the 16-B elements its own cp.async wrote.
+  auto split = [&](int buf) {
+    uint8_t* A = smem + buf * Sb;
+    for (int i = tid; i < nA; i += kTcThreads) {
+      const int r = i / nkc, kc = i - r * nkc;
+      float4* hp = reinterpret_cast<float4*>(A + ((size_t)kc * a.WRp + r) * 16);
+      float4* lp = reinterpret_cast<float4*>(A + Ab + ((size_t)kc * a.WRp + r) * 16);
+      float4 v = *hp, h, l;
+      h.x = tf32_hi(v.x); h.y = tf32_hi(v.y); h.z = tf32_hi(v.z); h.w = tf32_hi(v.w);
+      l.x = v.x - h.x; l.y = v.y - h.y; l.z = v.z - h.z; l.w = v.w - h.w;
+      *hp = h;
+      *lp = l;
+    }
   };
 
   load(0, 0);
@@ -137,17 +169,23 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
     } else {
       tc::cp_async_wait<0>();
     }
+    split(buf);
     tc::fence_proxy_async();
     __syncthreads();
     if (tid == 0) {
       tc::fence_after();
-      const uint32_t abase = tc::smem_u32(Abuf[buf]), bbase = tc::smem_u32(Bbuf[buf]);
+      const uint32_t ahi = tc::smem_u32(smem + buf * Sb), alo = ahi + (uint32_t)Ab;
+      const uint32_t bhi = ahi + (uint32_t)(2 * Ab), blo = bhi + (uint32_t)Bb;
       for (int t9 = 0; t9 < 9; ++t9) {
         const int rowoff = (t9 / 3) * a.Sw + (t9 % 3);
         for (int j = 0; j < (a.CB >> 3); ++j) {
-          const uint64_t ad = tc::make_desc(abase + (uint32_t)((2 * j * a.WRp + rowoff) * 16), a.WRp * 16, 128);
-          const uint64_t bd = tc::make_desc(bbase + (uint32_t)((t9 * nkc + 2 * j) * a.Np * 16), a.Np * 16, 128);
-          tc::mma_tf32(tmem, ad, bd, a.idesc, (s | t9 | j) ? 1u : 0u);
+          const uint32_t ao = (uint32_t)((2 * j * a.WRp + rowoff) * 16);
+          const uint32_t bo = (uint32_t)((t9 * nkc + 2 * j) * a.Ns * 16);
+          const uint32_t alb = a.WRp * 16, blb = a.Ns * 16;
+          const uint32_t first = (s | t9 | j) ? 1u : 0u;
+          tc::mma_tf32(tmem, tc::make_desc(alo + ao, alb, 128), tc::make_desc(bhi + bo, blb, 128), a.idesc, first);
+          tc::mma_tf32(tmem, tc::make_desc(ahi + ao, alb, 128), tc::make_desc(blo + bo, blb, 128), a.idesc, 1u);
+          tc::mma_tf32(tmem, tc::make_desc(ahi + ao, alb, 128), tc::make_desc(bhi + bo, blb, 128), a.idesc, 1u);
         }
       }
       tc::commit(&mbar[buf]);
@@ -170,13 +208,13 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
   float* yp = v >= 0 ? y.ptr + b * y.bstride + (long long)v * y.cstride : nullptr;
   const float* bias = a.bias ? a.bias + b * a.bbs : nullptr;
   const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
-  for (int c0 = 0; c0 < a.Np; c0 += 8) {
+  for (int c0 = 0; c0 < a.Ns; c0 += 8) {
     float vals[8];
     tc::tmem_ld8(trow + c0, vals);
     if (yp) {
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
-        const int n = c0 + j;
+        const int n = n0 + c0 + j;
         if (n < a.N) {
           float o = vals[j] + (bias ? __ldg(bias + n) : 0.f);
           if (a.accumulate) o += yp[n];
@@ -190,15 +228,14 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
   if (warp == 0) tc::tmem_free(tmem, a.tmem_cols);
 }
 
-// Pack OIDHW weights into [b][tap][K/4][Np][4] (K-major B tiles).
+// Pack OIDHW weights into [b][hi|lo][tap][K/4][Np][4] (K-major B tiles).
 //   forward: K = C_in,  N = C_out:  P[t][k][n] = W[n][k][t]
 //   dgrad  : K = C_out, N = C_in :  P[t][k][n] = W[k][n][26 - t]
 __global__ void conv_tc_pack_k(const float* __restrict__ w, long long wbs, int K, int N, int Np, int dgrad,
-                               float* __restrict__ out, long long obs) {
+                               float* __restrict__ out, long long half, long long obs) {
   const int b = blockIdx.y;
-  const long long total = 27LL * K * Np;
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= total) return;
+  if (i >= half) return;
   const int j = (int)(i & 3);
   const long long q = i >> 2;
   const int n = (int)(q % Np);
@@ -211,7 +248,9 @@ __global__ void conv_tc_pack_k(const float* __restrict__ w, long long wbs, int K
     const float* wb = w + b * wbs;
     val = dgrad ? wb[((long long)k * N + n) * 27 + (26 - t)] : wb[((long long)n * K + k) * 27 + t];
   }
-  out[b * obs + i] = val;
+  const float hi = tf32_hi(val);
+  out[b * obs + i] = hi;
+  out[b * obs + half + i] = val - hi;
 }
 
 bool conv_tc_supported(int cin, int cout, int ks, int stride, int precision) {
@@ -220,11 +259,11 @@ bool conv_tc_supported(int cin, int cout, int ks, int stride, int precision) {
   return true;
 }
 
-long long conv_tc_pack_floats(int K, int N) { return 27LL * K * np_of(N); }
+long long conv_tc_pack_floats(int K, int N) { return 2 * 27LL * K * np_of(N); }
 
 int conv_tc_pack(const float* w, long long wbs, int K, int N, int dgrad, float* out, int batch, cudaStream_t st) {
-  const long long total = conv_tc_pack_floats(K, N);
-  conv_tc_pack_k<<<dim3(cdiv(total, 256), batch), 256, 0, st>>>(w, wbs, K, N, np_of(N), dgrad, out, total);
+  const long long total = conv_tc_pack_floats(K, N), half = total / 2;
+  conv_tc_pack_k<<<dim3(cdiv(half, 256), batch), 256, 0, st>>>(w, wbs, K, N, np_of(N), dgrad, out, half, total);
   D2IP_LAUNCH_CHECK();
   return D2IP_OK;
 }
@@ -237,6 +276,7 @@ int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, lo
   a.x = x;
   a.wp = wp;
   a.wpbs = conv_tc_pack_floats(K, N);
+  a.wlo = a.wpbs / 2;
   a.bias = bias;
   a.bbs = bbs;
   a.y = y;
@@ -248,24 +288,33 @@ int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, lo
   a.Sh = (x.h + 2) * a.Sw;
   a.WR = wr_of(a.Sw);
   a.WRp = wrp_of(a.WR);
-  a.CB = choose_cb(K, a.Np, a.WRp);
+  // widest N slice whose 2-stage pipeline fits (2 CTAs/SM preferred, then 1)
+  a.CB = 0;
+  for (size_t budget : {kTcStageBudget, (size_t)210 * 1024}) {
+    for (int ns = a.Np; ns >= 16 && a.CB == 0; ns -= 16) {
+      if (a.Np % ns) continue;
+      a.CB = choose_cb(K, ns, a.WRp, budget);
+      if (a.CB) a.Ns = ns;
+    }
+    if (a.CB) break;
+  }
   D2IP_CHECK_ARG(a.CB >= 8, "conv_tc: no channel blocking fits shared memory (K=%d N=%d W=%d)", K, N, x.w);
   a.n_cb = K / a.CB;
   a.u_first = a.Sh + a.Sw + 1;
   const int u_last = x.d * a.Sh + x.h * a.Sw + x.w;
   const int tiles = cdiv(u_last - a.u_first + 1, kTcRows);
   int cols = 32;
-  while (cols < a.Np) cols *= 2;
+  while (cols < a.Ns) cols *= 2;
   a.tmem_cols = cols;
-  a.idesc = tc::make_idesc(2, kTcRows, a.Np);
+  a.idesc = tc::make_idesc(2, kTcRows, a.Ns);
   const size_t smem = tc_smem_bytes(a);
   static bool attr_set = false;
   if (!attr_set) {
     D2IP_CUDA(cudaFuncSetAttribute(conv_tc_k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr_set = true;
   }
-  conv_tc_k<<<dim3(tiles, batch), kTcThreads, smem, st>>>(a);
-  set_variant("tcgen05_tf32");
+  conv_tc_k<<<dim3(tiles, a.Np / a.Ns, batch), kTcThreads, smem, st>>>(a);
+  set_variant("tcgen05_tf32x3");
   D2IP_LAUNCH_CHECK();
   return D2IP_OK;
 }

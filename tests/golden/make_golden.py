@@ -217,7 +217,47 @@ def case_sequence():
     print("sequence:", list(out["provenance"]), list(out["iterations"]))
 
 
+def case_sequence_long():
+    """Converged budgets (300 UPWS / 60 / 60, 4 frames): the end-to-end bar
+    (MSSIM >= 0.99, data misfit within 2%) is judged on these volumes."""
+    spec = W.small_spec()
+    wl = W.make_workload(spec, seed=0)
+    grid = wl.grid
+    net = GoldenNetCfg(spec.channels, spec.in_channels, seed=0)
+    P.sample_noise_input = lambda g, s: _Noise(sample_noise_input(grid, s, spec.in_channels, 0.1))
+    cfg = P.RunConfig(iters_warm=300, iters_first=60, iters_next=60, learning_rate=1e-3,
+                      tv_weights=TVWeights(lambda_tv=0.0), seed=1, network=net,
+                      output_map=wl.output_map, data_norm="l2sq")
+    matrix = dense_matrix(wl.matrix)
+    volts = VoltageSequence([VoltageFrame(f.values, f.frame_index) for f in wl.voltages.frames])
+    res = P.reconstruct_sequence(matrix, volts, cfg, grid)
+    out = {"values": res.sequence.values, "output_map": np.array(wl.output_map),
+           "iterations": np.array([f.iterations for f in res.frame_records])}
+    for key, tr in res.traces.items():
+        out[f"trace_{key}"] = np.array([[r.iteration, r.data_term, r.total] for r in tr.records])
+    # Natural fp32 variability band: the same algorithm with only the
+    # summation order of J.sigma changed (compact masked J, CPU oracle). Long
+    # DIP trajectories are chaotic, so this is the yardstick for end-to-end
+    # agreement (DESIGN.md §6).
+    sys.path.insert(0, str(ROOT))
+    from oracle import oracle_reconstruct_sequence
+    theta0 = flat_state(res.states["init"])
+    band = oracle_reconstruct_sequence(spec.channels, spec.in_channels,
+                                       sample_noise_input(grid, 1, spec.in_channels, 0.1).values,
+                                       wl.matrix.values, wl.matrix.columns_q(),
+                                       [f.values for f in wl.voltages.frames], theta0, wl.output_map,
+                                       300, 60, 60, 1e-3)
+    out["band_values"] = band["columns"]
+    np.savez_compressed(OUT / "seq_long.npz", **out)
+    print("long sequence: final data terms", [float(out[f"trace_frame_{i}"][-1, 1]) for i in range(1, 5)])
+
+
 if __name__ == "__main__":
     torch.set_num_threads(1)
-    case_cfg0()
-    case_sequence()
+    which = sys.argv[1:] or ["cfg0", "sequence", "long"]
+    if "cfg0" in which:
+        case_cfg0()
+    if "sequence" in which:
+        case_sequence()
+    if "long" in which:
+        case_sequence_long()

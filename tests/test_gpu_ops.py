@@ -3,7 +3,7 @@ CPU references of the same op (the ops the reference runs through PyTorch:
 nn.Conv3d, ChannelLayerNorm, LeakyReLU, F.interpolate, mv, torch.optim.Adam).
 
 Tolerances (relative, ||dev - ref|| / ||ref||): 1e-5 for exact-fp32 kernels,
-2e-3 for TF32 tensor-core convolutions (10-bit mantissa operands, fp32
+1e-4 for the TF32 tensor-core convolutions (error-compensated 3xTF32, fp32
 accumulation), 1e-2 for bf16 operands — the north star's bars.
 """
 
@@ -18,7 +18,7 @@ from paper_2507_14046_b200 import _native as N
 
 pytestmark = pytest.mark.gpu
 
-TOL = {"fp32": 1e-5, "tf32": 2e-3, "bf16": 1e-2}
+TOL = {"fp32": 1e-5, "tf32": 1e-4, "bf16": 1e-2}
 
 
 def rel(a, b):
@@ -96,7 +96,7 @@ def test_conv3d_fwd(cin, cout, ks, stride, sp, prec):
     N.check(rc, "conv3d_fwd")
     torch.cuda.synchronize()
     if prec == "tf32" and ks == 3 and stride == 1 and cin % 8 == 0:
-        assert L.d2ip_last_variant() == b"tcgen05_tf32"
+        assert L.d2ip_last_variant() == b"tcgen05_tf32x3"
     assert rel(from_ndhwc(out), ref) < TOL[prec]
     # accumulate mode adds on top
     N.check(L.d2ip_conv3d_fwd(xa, C.c_void_p(params.data_ptr()), None, P, ks, stride, ya, 1, N.PREC[prec],
