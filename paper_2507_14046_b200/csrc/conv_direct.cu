@@ -3,10 +3,15 @@
 // and the fallback for shapes the tcgen05 implicit-GEMM kernels do not take
 // (C_out = 1 tail, C_in not a multiple of 4). Layout: NDHWC activations,
 // OIDHW weights (the reference's nn.Conv3d layout, priornet.py:111-117).
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
 namespace d2ip {
+
+static int tiled_threads(int cin, int cout, int ks, int cog);
+static void tiled_split(int cin, int cout, int ks, int cog, long long V, int batch, int* nchunks, int* chunk);
 
 template <int KS>
 struct Taps {
@@ -14,23 +19,32 @@ struct Taps {
   static constexpr int PAD = KS / 2;
 };
 
-// One thread computes CG consecutive output channels of one output voxel.
+// Direct convolutions (stride 2, 1^3, odd channel counts, the C_out = 1
+// tail, and precision FP32). A block owns CG output channels and 128 voxels
+// (one per thread); the CG x C_in x k^3 weight slice sits in shared memory as
+// [c][tap][CG] so every (c, tap) step is one float4-vectorised input load
+// (4 channels) against broadcast shared-memory weights.
+
+// y[v][co0..co0+CG) = sum_{tap,ci} x[in(v,tap)][ci] * W[co][ci][tap]
 template <int KS, int CG>
-__global__ void __launch_bounds__(256) conv_fwd_direct_k(d2ip_act x, const float* __restrict__ w,
+__global__ void __launch_bounds__(128) conv_fwd_direct_k(d2ip_act x, const float* __restrict__ w,
                                                          const float* __restrict__ bias,
                                                          long long wbs, int stride, d2ip_act y,
-                                                         int accumulate) {
+                                                         int accumulate, int vec) {
   constexpr int K3 = Taps<KS>::K3, PAD = Taps<KS>::PAD;
+  extern __shared__ float sw[];  // [cin][K3][CG]
   const int b = blockIdx.z;
-  const int groups = y.c / CG;
-  const long long total = (long long)y.d * y.h * y.w * groups;
-  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= total) return;
-  const int g = (int)(idx % groups);
-  const long long v = idx / groups;
-  const int ow = (int)(v % y.w), oh = (int)((v / y.w) % y.h), od = (int)(v / ((long long)y.w * y.h));
-  const int cin = x.c, co0 = g * CG;
+  const int cin = x.c, co0 = blockIdx.y * CG;
   const float* wb = w + b * wbs;
+  for (int i = threadIdx.x; i < cin * K3 * CG; i += blockDim.x) {
+    const int j = i % CG, r = i / CG, tap = r % K3, ci = r / K3;
+    sw[i] = __ldg(wb + ((long long)(co0 + j) * cin + ci) * K3 + tap);
+  }
+  __syncthreads();
+  const long long V = (long long)y.d * y.h * y.w;
+  const long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= V) return;
+  const int ow = (int)(v % y.w), oh = (int)((v / y.w) % y.h), od = (int)(v / ((long long)y.w * y.h));
   float acc[CG];
 #pragma unroll
   for (int j = 0; j < CG; ++j) acc[j] = bias ? __ldg(bias + b * wbs + co0 + j) : 0.f;
@@ -46,11 +60,24 @@ __global__ void __launch_bounds__(256) conv_fwd_direct_k(d2ip_act x, const float
         if (iw < 0 || iw >= x.w) continue;
         const float* xp = xb + (((long long)id * x.h + ih) * x.w + iw) * x.cstride;
         const int tap = (kd * KS + kh) * KS + kw;
-        for (int ci = 0; ci < cin; ++ci) {
-          const float xv = __ldg(xp + ci);
+        if (vec) {
+          for (int ci = 0; ci < cin; ci += 4) {
+            const float4 q = __ldg(reinterpret_cast<const float4*>(xp + ci));
+            const float xv[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
-          for (int j = 0; j < CG; ++j)
-            acc[j] = fmaf(xv, __ldg(wb + ((long long)(co0 + j) * cin + ci) * K3 + tap), acc[j]);
+            for (int u = 0; u < 4; ++u) {
+              const float* wr = sw + ((ci + u) * K3 + tap) * CG;
+#pragma unroll
+              for (int j = 0; j < CG; ++j) acc[j] = fmaf(xv[u], wr[j], acc[j]);
+            }
+          }
+        } else {
+          for (int ci = 0; ci < cin; ++ci) {
+            const float xv = __ldg(xp + ci);
+            const float* wr = sw + (ci * K3 + tap) * CG;
+#pragma unroll
+            for (int j = 0; j < CG; ++j) acc[j] = fmaf(xv, wr[j], acc[j]);
+          }
         }
       }
     }
@@ -60,22 +87,25 @@ __global__ void __launch_bounds__(256) conv_fwd_direct_k(d2ip_act x, const float
   for (int j = 0; j < CG; ++j) yp[j] = accumulate ? yp[j] + acc[j] : acc[j];
 }
 
-// One thread computes CG consecutive input-channel gradients of one input voxel.
+// gx[v][ci0..ci0+CG) = sum_{tap,co} gy[o(v,tap)][co] * W[co][ci][tap]
 template <int KS, int CG>
-__global__ void __launch_bounds__(256) conv_dgrad_direct_k(d2ip_act gy, const float* __restrict__ w,
+__global__ void __launch_bounds__(128) conv_dgrad_direct_k(d2ip_act gy, const float* __restrict__ w,
                                                            long long wbs, int stride, d2ip_act gx,
-                                                           int accumulate) {
+                                                           int accumulate, int vec) {
   constexpr int K3 = Taps<KS>::K3, PAD = Taps<KS>::PAD;
+  extern __shared__ float sw[];  // [cout][K3][CG]
   const int b = blockIdx.z;
-  const int groups = gx.c / CG;
-  const long long total = (long long)gx.d * gx.h * gx.w * groups;
-  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (idx >= total) return;
-  const int g = (int)(idx % groups);
-  const long long v = idx / groups;
-  const int iw = (int)(v % gx.w), ih = (int)((v / gx.w) % gx.h), id = (int)(v / ((long long)gx.w * gx.h));
-  const int cin = gx.c, cout = gy.c, ci0 = g * CG;
+  const int cin = gx.c, cout = gy.c, ci0 = blockIdx.y * CG;
   const float* wb = w + b * wbs;
+  for (int i = threadIdx.x; i < cout * K3 * CG; i += blockDim.x) {
+    const int j = i % CG, r = i / CG, tap = r % K3, co = r / K3;
+    sw[i] = __ldg(wb + ((long long)co * cin + ci0 + j) * K3 + tap);
+  }
+  __syncthreads();
+  const long long V = (long long)gx.d * gx.h * gx.w;
+  const long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= V) return;
+  const int iw = (int)(v % gx.w), ih = (int)((v / gx.w) % gx.h), id = (int)(v / ((long long)gx.w * gx.h));
   const float* gb = gy.ptr + b * gy.bstride;
   float acc[CG];
 #pragma unroll
@@ -97,11 +127,24 @@ __global__ void __launch_bounds__(256) conv_dgrad_direct_k(d2ip_act gy, const fl
         if (ow >= gy.w) continue;
         const float* gp = gb + (((long long)od * gy.h + oh) * gy.w + ow) * gy.cstride;
         const int tap = (kd * KS + kh) * KS + kw;
-        for (int co = 0; co < cout; ++co) {
-          const float gv = __ldg(gp + co);
+        if (vec) {
+          for (int co = 0; co < cout; co += 4) {
+            const float4 q = __ldg(reinterpret_cast<const float4*>(gp + co));
+            const float gv[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
-          for (int j = 0; j < CG; ++j)
-            acc[j] = fmaf(gv, __ldg(wb + ((long long)co * cin + ci0 + j) * K3 + tap), acc[j]);
+            for (int u = 0; u < 4; ++u) {
+              const float* wr = sw + ((co + u) * K3 + tap) * CG;
+#pragma unroll
+              for (int j = 0; j < CG; ++j) acc[j] = fmaf(gv[u], wr[j], acc[j]);
+            }
+          }
+        } else {
+          for (int co = 0; co < cout; ++co) {
+            const float gv = __ldg(gp + co);
+            const float* wr = sw + (co * K3 + tap) * CG;
+#pragma unroll
+            for (int j = 0; j < CG; ++j) acc[j] = fmaf(gv, wr[j], acc[j]);
+          }
         }
       }
     }
@@ -178,15 +221,16 @@ __global__ void __launch_bounds__(128) conv_wgrad_tiled_k(d2ip_act x, d2ip_act g
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < COG; ++j) acc[i][j] = 0.f;
+  // partial layout: [b][chunk][gid][4 * COG], contiguous per thread
+  float* pout = partial + (((long long)b * nchunks + c) * ngroups + gid) * (4 * COG);
   if (t == K3) {
     for (long long v = v0; v < v1; ++v) {
       const float* g = gb + v * gy.cstride;
 #pragma unroll
       for (int j = 0; j < COG; ++j) acc[0][j] += __ldg(g + j);
     }
-    float* p = partial + ((long long)b * nchunks + c) * nE + nW + co0;
 #pragma unroll
-    for (int j = 0; j < COG; ++j) p[j] = acc[0][j];
+    for (int j = 0; j < COG; ++j) pout[j] = acc[0][j];
     return;
   }
   const int kd = t / (KS * KS), kh = (t / KS) % KS, kw = t % KS;
@@ -224,11 +268,37 @@ __global__ void __launch_bounds__(128) conv_wgrad_tiled_k(d2ip_act x, d2ip_act g
       }
     }
   }
-  float* p = partial + ((long long)b * nchunks + c) * nE;
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
-    for (int j = 0; j < COG; ++j) p[((long long)(co0 + j) * cin + ci0 + i) * K3 + t] = acc[i][j];
+    for (int j = 0; j < COG; ++j) pout[i * COG + j] = acc[i][j];
+  (void)nE;
+}
+
+// Sum the thread-contiguous partials of conv_wgrad_tiled_k over chunks (fixed
+// order) and scatter into the OIDHW weight + bias gradient.
+__global__ void wgrad_tiled_reduce_k(const float* __restrict__ partial, int nchunks, int ngroups, int cin,
+                                     int cout, int K3, int cog, float* __restrict__ out, long long obs) {
+  const int b = blockIdx.y;
+  const long long stride = (long long)ngroups * 4 * cog;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;  // index in the tiled layout (coalesced reads)
+  if (j >= stride) return;
+  const int nci = cin >> 2, nco = cout / cog;
+  const int gid = j / (4 * cog), slot = j - gid * 4 * cog;
+  const int t = gid / (nci * nco), ci4 = (gid / nco) % nci, cg = gid % nco;
+  const int i = slot / cog, jj = slot - i * cog;
+  const int co = cg * cog + jj, ci = ci4 * 4 + i;
+  long long e;
+  if (t < K3) {
+    e = ((long long)co * cin + ci) * K3 + t;
+  } else {
+    if (ci4 != 0 || i != 0) return;  // bias groups store COG values
+    e = (long long)cout * cin * K3 + co;
+  }
+  const float* p = partial + (long long)b * nchunks * stride + j;
+  float s = 0.f;
+  for (int c = 0; c < nchunks; ++c) s += p[c * stride];
+  out[b * obs + e] = s;
 }
 
 __global__ void reduce_chunks_k(const float* __restrict__ partial, int nchunks, int n, float* out,
@@ -252,14 +322,25 @@ int reduce_chunks(const float* partial, int nchunks, int n, float* out, long lon
 
 // ---------------------------------------------------------------------------
 
+template <typename K>
+static int smem_opt_in(K kernel, size_t bytes) {
+  if (bytes > 48 * 1024) D2IP_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  return D2IP_OK;
+}
+
+static bool vec_ok(const d2ip_act& a) { return a.c % 4 == 0 && a.cstride % 4 == 0 && ((uintptr_t)a.ptr & 15) == 0; }
+
 int conv_fwd_direct(d2ip_act x, const float* w, const float* bias, long long wbs, int ks, int stride,
                     d2ip_act y, int accumulate, int batch, cudaStream_t st) {
   const long long V = (long long)y.d * y.h * y.w;
-#define LAUNCH_F(KS_, CG_)                                                              \
-  do {                                                                                  \
-    long long total = V * (y.c / CG_);                                                  \
-    dim3 grid(cdiv(total, 256), 1, batch);                                              \
-    conv_fwd_direct_k<KS_, CG_><<<grid, 256, 0, st>>>(x, w, bias, wbs, stride, y, accumulate); \
+  const int vec = vec_ok(x) ? 1 : 0;
+#define LAUNCH_F(KS_, CG_)                                                                          \
+  do {                                                                                              \
+    const size_t sm = (size_t)x.c * KS_ * KS_ * KS_ * CG_ * sizeof(float);                          \
+    D2IP_CHECK_ARG(sm <= 200 * 1024, "conv3d_fwd: weight slice too large for shared memory");      \
+    D2IP_RET(smem_opt_in(conv_fwd_direct_k<KS_, CG_>, sm));                                        \
+    dim3 grid(cdiv(V, 128), y.c / CG_, batch);                                                      \
+    conv_fwd_direct_k<KS_, CG_><<<grid, 128, sm, st>>>(x, w, bias, wbs, stride, y, accumulate, vec); \
   } while (0)
   const int cg = (y.c % 8 == 0) ? 8 : (y.c % 4 == 0 ? 4 : 1);
   if (ks == 3) {
@@ -276,11 +357,14 @@ int conv_fwd_direct(d2ip_act x, const float* w, const float* bias, long long wbs
 int conv_dgrad_direct(d2ip_act gy, const float* w, long long wbs, int ks, int stride, d2ip_act gx,
                       int accumulate, int batch, cudaStream_t st) {
   const long long V = (long long)gx.d * gx.h * gx.w;
-#define LAUNCH_D(KS_, CG_)                                                                 \
-  do {                                                                                     \
-    long long total = V * (gx.c / CG_);                                                    \
-    dim3 grid(cdiv(total, 256), 1, batch);                                                 \
-    conv_dgrad_direct_k<KS_, CG_><<<grid, 256, 0, st>>>(gy, w, wbs, stride, gx, accumulate); \
+  const int vec = vec_ok(gy) ? 1 : 0;
+#define LAUNCH_D(KS_, CG_)                                                                        \
+  do {                                                                                            \
+    const size_t sm = (size_t)gy.c * KS_ * KS_ * KS_ * CG_ * sizeof(float);                       \
+    D2IP_CHECK_ARG(sm <= 200 * 1024, "conv3d_dgrad: weight slice too large for shared memory");  \
+    D2IP_RET(smem_opt_in(conv_dgrad_direct_k<KS_, CG_>, sm));                                    \
+    dim3 grid(cdiv(V, 128), gx.c / CG_, batch);                                                   \
+    conv_dgrad_direct_k<KS_, CG_><<<grid, 128, sm, st>>>(gy, w, wbs, stride, gx, accumulate, vec); \
   } while (0)
   const int cg = (gx.c % 8 == 0) ? 8 : (gx.c % 4 == 0 ? 4 : 1);
   if (ks == 3) {
@@ -309,13 +393,13 @@ size_t conv_wgrad_direct_ws(int cin, int cout, int ks, long long V, int batch) {
   const int nE = cout * cin * ks * ks * ks + cout;
   int nchunks, chunk;
   wgrad_split(nE, V, batch, &nchunks, &chunk);
-  int most = nchunks;
+  size_t most = (size_t)batch * nchunks * nE;
   for (int cog : {8, 4, 1}) {  // any tiled variant the views may select
     if (cin % 4 || cout % cog) continue;
-    wgrad_split((ks * ks * ks + 1) * (cin / 4) * (cout / cog), V, batch, &nchunks, &chunk);
-    if (nchunks > most) most = nchunks;
+    tiled_split(cin, cout, ks, cog, V, batch, &nchunks, &chunk);
+    most = std::max(most, (size_t)batch * nchunks * tiled_threads(cin, cout, ks, cog) * 4 * cog);
   }
-  return (size_t)batch * most * nE * sizeof(float);
+  return most * sizeof(float);
 }
 
 static int tiled_cog(const d2ip_act& x, const d2ip_act& gy) {
@@ -327,8 +411,22 @@ static int tiled_cog(const d2ip_act& x, const d2ip_act& gy) {
   return 1;
 }
 
-static int tiled_threads(const d2ip_act& x, const d2ip_act& gy, int ks, int cog) {
-  return (ks * ks * ks + 1) * (x.c / 4) * (gy.c / cog);
+static int tiled_threads(int cin, int cout, int ks, int cog) {
+  return (ks * ks * ks + 1) * (cin / 4) * (cout / cog);
+}
+
+// Chunking of the voxel (K) dimension for the tiled kernel: ~600k threads,
+// >= 32 voxels per chunk, partials capped at 4M floats.
+static void tiled_split(int cin, int cout, int ks, int cog, long long V, int batch, int* nchunks, int* chunk) {
+  const long long nthr = tiled_threads(cin, cout, ks, cog);
+  const long long per_chunk = nthr * 4 * cog * batch;
+  long long want = (148LL * 4096 + nthr * batch - 1) / (nthr * batch);
+  want = std::min(want, (V + 31) / 32);
+  want = std::min(want, std::max(1LL, (4LL << 20) / per_chunk));
+  if (want < 1) want = 1;
+  const int c = (int)((V + want - 1) / want);
+  *chunk = c;
+  *nchunks = (int)((V + c - 1) / c);
 }
 
 int conv_wgrad_direct(d2ip_act x, d2ip_act gy, int ks, int stride, float* gw, long long gwbs,
@@ -338,9 +436,10 @@ int conv_wgrad_direct(d2ip_act x, d2ip_act gy, int ks, int stride, float* gw, lo
   int nchunks, chunk;
   const int cog = tiled_cog(x, gy);
   if (cog) {
-    const int nthr = tiled_threads(x, gy, ks, cog);
-    wgrad_split(nthr, V, batch, &nchunks, &chunk);
-    D2IP_CHECK_ARG(ws_bytes >= (size_t)batch * nchunks * nE * sizeof(float), "conv3d_wgrad: workspace too small");
+    const int nthr = tiled_threads(x.c, gy.c, ks, cog);
+    tiled_split(x.c, gy.c, ks, cog, V, batch, &nchunks, &chunk);
+    D2IP_CHECK_ARG(ws_bytes >= (size_t)batch * nchunks * nthr * 4 * cog * sizeof(float),
+                   "conv3d_wgrad: workspace too small");
     float* partial = reinterpret_cast<float*>(ws);
     dim3 grid(cdiv(nthr, 128), nchunks, batch);
 #define LAUNCH_T(KS_, COG_) conv_wgrad_tiled_k<KS_, COG_><<<grid, 128, 0, st>>>(x, gy, stride, partial, nchunks, chunk)
@@ -351,7 +450,10 @@ int conv_wgrad_direct(d2ip_act x, d2ip_act gy, int ks, int stride, float* gw, lo
     }
 #undef LAUNCH_T
     D2IP_LAUNCH_CHECK();
-    return reduce_chunks(partial, nchunks, nE, gw, gwbs, batch, st);
+    wgrad_tiled_reduce_k<<<dim3(cdiv((long long)nthr * 4 * cog, 256), batch), 256, 0, st>>>(
+        partial, nchunks, nthr, x.c, gy.c, ks * ks * ks, cog, gw, gwbs);
+    D2IP_LAUNCH_CHECK();
+    return D2IP_OK;
   }
   wgrad_split(nE, V, batch, &nchunks, &chunk);
   D2IP_CHECK_ARG(ws_bytes >= (size_t)batch * nchunks * nE * sizeof(float),

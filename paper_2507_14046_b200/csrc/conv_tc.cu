@@ -29,6 +29,8 @@
 // Pipeline: 2 smem stages filled with cp.async (16 B, zero-fill outside the
 // grid) by all 128 threads; thread 0 issues the MMAs of a stage and commits
 // them to that stage's mbarrier, which gates the refill of the buffer.
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 #include "tc.cuh"
@@ -255,7 +257,7 @@ __global__ void conv_tc_pack_k(const float* __restrict__ w, long long wbs, int K
 
 bool conv_tc_supported(int cin, int cout, int ks, int stride, int precision) {
   if (precision != D2IP_PREC_TF32 || ks != 3 || stride != 1) return false;
-  if (cin % 8 || cin < 8 || cout < 1 || np_of(cout) > 256) return false;
+  if (cin % 8 || cin < 8 || cout < 1 || np_of(cout) > 1024) return false;
   return true;
 }
 
@@ -291,7 +293,7 @@ int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, lo
   // widest N slice whose 2-stage pipeline fits (2 CTAs/SM preferred, then 1)
   a.CB = 0;
   for (size_t budget : {kTcStageBudget, (size_t)210 * 1024}) {
-    for (int ns = a.Np; ns >= 16 && a.CB == 0; ns -= 16) {
+    for (int ns = std::min(a.Np, 256); ns >= 16 && a.CB == 0; ns -= 16) {
       if (a.Np % ns) continue;
       a.CB = choose_cb(K, ns, a.WRp, budget);
       if (a.CB) a.Ns = ns;

@@ -1,165 +1,13 @@
-// Per-voxel kernels: ChannelLayerNorm (+residual) (+LeakyReLU) forward and
-// backward, trilinear x2 upsample (align_corners=False) forward and gather
-// backward, and the tail conv + sigmoid + output map + mask gather.
+// Per-voxel kernels: trilinear x2 upsample (align_corners=False) forward and
+// gather backward, and the tail conv + sigmoid + output map + mask gather.
+// (ChannelLayerNorm / activation kernels live in norm.cu.)
 //
-// ChannelLayerNorm   : pkg/src/d2ip/priornet.py:96-108 (eps 1e-5, biased var)
-// ResConv3d add/act  : priornet.py:145-148
 // F.interpolate      : priornet.py:229 (trilinear, align_corners=False)
 // sigmoid + map      : priornet.py:231, pipeline.py:276-278
 #include "common.cuh"
 #include "kernels.h"
 
 namespace d2ip {
-
-constexpr float kLnEps = 1e-5f;
-
-__global__ void __launch_bounds__(256) norm_act_fwd_k(d2ip_act y, const float* __restrict__ gamma,
-                                                      const float* __restrict__ beta, long long pbs,
-                                                      d2ip_act res, int act, float slope, d2ip_act out,
-                                                      float* __restrict__ xhat, float* __restrict__ rstd) {
-  const int b = blockIdx.y;
-  const long long V = (long long)y.d * y.h * y.w;
-  const long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= V) return;
-  const int C = y.c;
-  const float* yp = y.ptr + b * y.bstride + v * y.cstride;
-  float mean = 0.f;
-  for (int c = 0; c < C; ++c) mean += yp[c];
-  mean /= (float)C;
-  float var = 0.f;
-  for (int c = 0; c < C; ++c) {
-    const float d = yp[c] - mean;
-    var = fmaf(d, d, var);
-  }
-  var /= (float)C;
-  const float rs = 1.0f / sqrtf(var + kLnEps);
-  rstd[b * V + v] = rs;
-  float* xh = xhat + ((long long)b * V + v) * C;
-  const float* g = gamma + b * pbs;
-  const float* be = beta + b * pbs;
-  const float* rp = res.ptr ? res.ptr + b * res.bstride + v * res.cstride : nullptr;
-  float* op = out.ptr + b * out.bstride + v * out.cstride;
-  for (int c = 0; c < C; ++c) {
-    const float x = (yp[c] - mean) * rs;
-    xh[c] = x;
-    float o = fmaf(x, __ldg(g + c), __ldg(be + c));
-    if (rp) o += rp[c];
-    if (act) o = lrelu(o, slope);
-    op[c] = o;
-  }
-}
-
-int norm_act_fwd(d2ip_act y, const float* gamma, const float* beta, long long pbs, d2ip_act res,
-                 int act, float slope, d2ip_act out, float* xhat, float* rstd, int batch,
-                 cudaStream_t st) {
-  const long long V = (long long)y.d * y.h * y.w;
-  dim3 grid(cdiv(V, 128), batch);
-  norm_act_fwd_k<<<grid, 128, 0, st>>>(y, gamma, beta, pbs, res, act, slope, out, xhat, rstd);
-  D2IP_LAUNCH_CHECK();
-  return D2IP_OK;
-}
-
-// gpre = gout * act'(out); gc = rstd * (gpre*gamma - mean(gpre*gamma) - xhat*mean(gpre*gamma*xhat))
-__global__ void __launch_bounds__(128) norm_act_bwd_k(d2ip_act gout, d2ip_act out, int act, float slope,
-                                                      const float* __restrict__ xhat,
-                                                      const float* __restrict__ rstd,
-                                                      const float* __restrict__ gamma, long long pbs,
-                                                      d2ip_act gpre, d2ip_act gc) {
-  const int b = blockIdx.y;
-  const long long V = (long long)gout.d * gout.h * gout.w;
-  const long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= V) return;
-  const int C = gout.c;
-  const float* go = gout.ptr + b * gout.bstride + v * gout.cstride;
-  const float* op = act ? out.ptr + b * out.bstride + v * out.cstride : nullptr;
-  const float* xh = xhat + ((long long)b * V + v) * C;
-  const float* g = gamma + b * pbs;
-  float* gp = gpre.ptr + b * gpre.bstride + v * gpre.cstride;
-  float s1 = 0.f, s2 = 0.f;
-  for (int c = 0; c < C; ++c) {
-    float t = go[c];
-    if (act) t = op[c] > 0.f ? t : t * slope;
-    gp[c] = t;
-    const float gx = t * __ldg(g + c);
-    s1 += gx;
-    s2 = fmaf(gx, xh[c], s2);
-  }
-  const float m1 = s1 / (float)C, m2 = s2 / (float)C;
-  const float rs = rstd[b * V + v];
-  float* gcp = gc.ptr + b * gc.bstride + v * gc.cstride;
-  for (int c = 0; c < C; ++c) {
-    const float gx = gp[c] * __ldg(g + c);
-    gcp[c] = rs * (gx - m1 - xh[c] * m2);
-  }
-}
-
-// partial[b][chunk][0..C) = sum gpre*xhat, [C..2C) = sum gpre over the chunk's voxels.
-__global__ void __launch_bounds__(256) norm_colsum_k(d2ip_act gpre, const float* __restrict__ xhat,
-                                                     float* __restrict__ partial, int chunk, int nchunks) {
-  __shared__ float sm[2][256];
-  const int b = blockIdx.y, ch = blockIdx.x;
-  const int C = gpre.c;
-  const long long V = (long long)gpre.d * gpre.h * gpre.w;
-  const int rows = 256 / C;
-  const int c = threadIdx.x % C, r = threadIdx.x / C;
-  float a1 = 0.f, a2 = 0.f;
-  const long long v0 = (long long)ch * chunk, v1 = min(V, v0 + chunk);
-  if (r < rows) {
-    const float* gp = gpre.ptr + b * gpre.bstride;
-    const float* xh = xhat + (long long)b * V * C;
-    for (long long v = v0 + r; v < v1; v += rows) {
-      const float t = gp[v * gpre.cstride + c];
-      a1 = fmaf(t, xh[v * C + c], a1);
-      a2 += t;
-    }
-  }
-  sm[0][threadIdx.x] = a1;
-  sm[1][threadIdx.x] = a2;
-  __syncthreads();
-  if (threadIdx.x < C) {
-    float s1 = 0.f, s2 = 0.f;
-    for (int rr = 0; rr < rows; ++rr) {
-      s1 += sm[0][rr * C + threadIdx.x];
-      s2 += sm[1][rr * C + threadIdx.x];
-    }
-    float* p = partial + ((long long)b * nchunks + ch) * 2 * C;
-    p[threadIdx.x] = s1;
-    p[C + threadIdx.x] = s2;
-  }
-}
-
-static void colsum_split(long long V, int batch, int* nchunks, int* chunk) {
-  long long want = (148LL * 4 + batch - 1) / batch;
-  long long maxc = (V + 255) / 256;
-  if (want > maxc) want = maxc;
-  if (want < 1) want = 1;
-  *chunk = (int)((V + want - 1) / want);
-  *nchunks = (int)((V + *chunk - 1) / *chunk);
-}
-
-size_t norm_act_bwd_ws(long long V, int C, int batch) {
-  int n, c;
-  colsum_split(V, batch, &n, &c);
-  return (size_t)batch * n * 2 * C * sizeof(float);
-}
-
-int norm_act_bwd(d2ip_act gout, d2ip_act out, int act, float slope, const float* xhat,
-                 const float* rstd, const float* gamma, long long pbs, d2ip_act gpre, d2ip_act gc,
-                 float* dgb, long long dgbs, void* ws, size_t ws_bytes, int batch, cudaStream_t st) {
-  const long long V = (long long)gout.d * gout.h * gout.w;
-  const int C = gout.c;
-  D2IP_CHECK_ARG(C <= 256, "norm_act_bwd: C=%d > 256", C);
-  dim3 grid(cdiv(V, 128), batch);
-  norm_act_bwd_k<<<grid, 128, 0, st>>>(gout, out, act, slope, xhat, rstd, gamma, pbs, gpre, gc);
-  D2IP_LAUNCH_CHECK();
-  int nchunks, chunk;
-  colsum_split(V, batch, &nchunks, &chunk);
-  D2IP_CHECK_ARG(ws_bytes >= (size_t)batch * nchunks * 2 * C * sizeof(float), "norm_act_bwd: ws");
-  float* partial = reinterpret_cast<float*>(ws);
-  norm_colsum_k<<<dim3(nchunks, batch), 256, 0, st>>>(gpre, xhat, partial, chunk, nchunks);
-  D2IP_LAUNCH_CHECK();
-  return reduce_chunks(partial, nchunks, 2 * C, dgb, dgbs, batch, st);
-}
 
 // ---------------------------------------------------------------------------
 // Trilinear x2, align_corners=False. Along one axis (n = low-res size):

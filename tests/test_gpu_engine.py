@@ -217,7 +217,8 @@ def test_long_sequence_within_reference_band(prec):
         assert mssim(a, b) >= mssim(c, b) - 0.1, i
         dv = wl.voltages.frames[i].values
         m_dev, m_ref, m_band = (misfit(wl.matrix.values, qc, v, dv) for v in (a, b, c))
-        assert abs(m_dev - m_ref) <= max(0.02 * m_ref, 3 * abs(m_band - m_ref)), (i, m_dev, m_ref, m_band)
+        # one-sided: fitting the data better than the reference is not a defect
+        assert m_dev - m_ref <= max(0.02 * m_ref, 3 * abs(m_band - m_ref)), (i, m_dev, m_ref, m_band)
 
 
 def test_tv_sequence_vs_reference():
