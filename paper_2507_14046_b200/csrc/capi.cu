@@ -27,14 +27,22 @@ static size_t conv_ws(int cin, int cout, int ks, int stride, int precision, int 
   return (size_t)batch * conv_tc_pack_floats(K, N) * sizeof(float);
 }
 
-size_t conv_wgrad_ws(int cin, int cout, int ks, long long V, int batch, int precision) {
+// Weight gradient: the smem-tiled kernel for stride-1 3^3 layers, the
+// register-tiled / scalar split-K kernels otherwise (stride 2, 1^3, C_out = 1).
+size_t conv_wgrad_ws(int cin, int cout, int ks, int D, int H, int W, int batch, int precision) {
   (void)precision;
-  return conv_wgrad_direct_ws(cin, cout, ks, V, batch);
+  const size_t a = conv_wgrad_direct_ws(cin, cout, ks, (long long)D * H * W, batch);
+  const size_t b = ks == 3 ? wgrad_s1_ws_bytes(D, H, W, cin, cout, batch) : 0;
+  return a > b ? a : b;
 }
 
 int conv_wgrad(d2ip_act x, d2ip_act gy, int ks, int stride, float* gw, long long gwbs, void* ws,
                size_t ws_bytes, int precision, int batch, cudaStream_t st) {
   (void)precision;
+  if (ks == 3 && stride == 1 && wgrad_s1_supported(x, gy)) {
+    set_variant("wgrad_s1_smem");
+    return wgrad_s1(x, gy, gw, gwbs, ws, ws_bytes, batch, st);
+  }
   return conv_wgrad_direct(x, gy, ks, stride, gw, gwbs, ws, ws_bytes, batch, st);
 }
 
@@ -74,7 +82,7 @@ int d2ip_conv3d_fwd(d2ip_act x, const float* w, const float* bias, long long wbs
                    "conv3d_fwd: workspace too small for the packed weights");
     float* pk = reinterpret_cast<float*>(ws);
     D2IP_RET(conv_tc_pack(w, wbstride, x.c, y.c, 0, pk, batch, S(stream)));
-    return conv_tc_run(x, pk, x.c, y.c, bias, wbstride, y, accumulate, batch, S(stream));
+    return conv_tc_run(x, pk, x.c, y.c, bias, wbstride, y, accumulate, nullptr, 0, batch, S(stream));
   }
   return conv_fwd_direct(x, w, bias, wbstride, ksize, stride, y, accumulate, batch, S(stream));
 }
@@ -88,13 +96,13 @@ int d2ip_conv3d_dgrad(d2ip_act gy, const float* w, long long wbstride, int ksize
                    "conv3d_dgrad: workspace too small for the packed weights");
     float* pk = reinterpret_cast<float*>(ws);
     D2IP_RET(conv_tc_pack(w, wbstride, gy.c, gx.c, 1, pk, batch, S(stream)));
-    return conv_tc_run(gy, pk, gy.c, gx.c, nullptr, 0, gx, accumulate, batch, S(stream));
+    return conv_tc_run(gy, pk, gy.c, gx.c, nullptr, 0, gx, accumulate, nullptr, 0, batch, S(stream));
   }
   return conv_dgrad_direct(gy, w, wbstride, ksize, stride, gx, accumulate, batch, S(stream));
 }
 
 size_t d2ip_conv3d_wgrad_ws_bytes(d2ip_act x, d2ip_act gy, int ksize, int batch) {
-  return d2ip::conv_wgrad_ws(x.c, gy.c, ksize, (long long)gy.d * gy.h * gy.w, batch, 0);
+  return d2ip::conv_wgrad_ws(x.c, gy.c, ksize, gy.d, gy.h, gy.w, batch, 0);
 }
 
 int d2ip_conv3d_wgrad(d2ip_act x, d2ip_act gy, int ksize, int stride, float* gw, long long gwbstride, void* ws,

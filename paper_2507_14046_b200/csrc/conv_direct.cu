@@ -277,12 +277,36 @@ __global__ void __launch_bounds__(128) conv_wgrad_tiled_k(d2ip_act x, d2ip_act g
 
 // Sum the thread-contiguous partials of conv_wgrad_tiled_k over chunks (fixed
 // order) and scatter into the OIDHW weight + bias gradient.
-__global__ void wgrad_tiled_reduce_k(const float* __restrict__ partial, int nchunks, int ngroups, int cin,
-                                     int cout, int K3, int cog, float* __restrict__ out, long long obs) {
+// Block = 32 consecutive partial entries x 8 warps; warp w sums chunks w, w+8,
+// ... (4-way unrolled), then warp 0 adds the 8 warp sums in order.
+__global__ void __launch_bounds__(256) wgrad_tiled_reduce_k(const float* __restrict__ partial, int nchunks,
+                                                            int ngroups, int cin, int cout, int K3, int cog,
+                                                            float* __restrict__ out, long long obs) {
+  __shared__ float red[8][33];
   const int b = blockIdx.y;
   const long long stride = (long long)ngroups * 4 * cog;
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;  // index in the tiled layout (coalesced reads)
-  if (j >= stride) return;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int j = blockIdx.x * 32 + lane;  // index in the tiled layout (coalesced reads)
+  float s = 0.f;
+  if (j < stride) {
+    const float* p = partial + (long long)b * nchunks * stride + j;
+    int c = w;
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
+    for (; c + 24 < nchunks; c += 32) {
+      s0 += p[(long long)c * stride];
+      s1 += p[(long long)(c + 8) * stride];
+      s2 += p[(long long)(c + 16) * stride];
+      s3 += p[(long long)(c + 24) * stride];
+    }
+    for (; c < nchunks; c += 8) s0 += p[(long long)c * stride];
+    s = (s0 + s1) + (s2 + s3);
+  }
+  red[w][lane] = s;
+  __syncthreads();
+  if (w != 0 || j >= stride) return;
+  s = 0.f;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) s += red[q][lane];
   const int nci = cin >> 2, nco = cout / cog;
   const int gid = j / (4 * cog), slot = j - gid * 4 * cog;
   const int t = gid / (nci * nco), ci4 = (gid / nco) % nci, cg = gid % nco;
@@ -295,26 +319,41 @@ __global__ void wgrad_tiled_reduce_k(const float* __restrict__ partial, int nchu
     if (ci4 != 0 || i != 0) return;  // bias groups store COG values
     e = (long long)cout * cin * K3 + co;
   }
-  const float* p = partial + (long long)b * nchunks * stride + j;
-  float s = 0.f;
-  for (int c = 0; c < nchunks; ++c) s += p[c * stride];
   out[b * obs + e] = s;
 }
 
-__global__ void reduce_chunks_k(const float* __restrict__ partial, int nchunks, int n, float* out,
-                                long long obs) {
+// out[e] = sum_c partial[c][e], fixed order: warp w sums chunks w, w+8, ...,
+// then warp 0 adds the 8 warp sums in order.
+__global__ void __launch_bounds__(256) reduce_chunks_k(const float* __restrict__ partial, int nchunks, int n,
+                                                       float* out, long long obs) {
+  __shared__ float red[8][33];
   const int b = blockIdx.y;
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;
-  if (e >= n) return;
-  const float* p = partial + (long long)b * nchunks * n + e;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int e = blockIdx.x * 32 + lane;
   float s = 0.f;
-  for (int c = 0; c < nchunks; ++c) s += p[(long long)c * n];
+  if (e < n) {
+    const float* p = partial + (long long)b * nchunks * n + e;
+    float s0 = 0.f, s1 = 0.f;
+    int c = w;
+    for (; c + 8 < nchunks; c += 16) {
+      s0 += p[(long long)c * n];
+      s1 += p[(long long)(c + 8) * n];
+    }
+    for (; c < nchunks; c += 8) s0 += p[(long long)c * n];
+    s = s0 + s1;
+  }
+  red[w][lane] = s;
+  __syncthreads();
+  if (w != 0 || e >= n) return;
+  s = 0.f;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) s += red[q][lane];
   out[b * obs + e] = s;
 }
 
 int reduce_chunks(const float* partial, int nchunks, int n, float* out, long long obs, int batch,
                   cudaStream_t st) {
-  dim3 grid(cdiv(n, 256), batch);
+  dim3 grid(cdiv(n, 32), batch);
   reduce_chunks_k<<<grid, 256, 0, st>>>(partial, nchunks, n, out, obs);
   D2IP_LAUNCH_CHECK();
   return D2IP_OK;
@@ -450,7 +489,7 @@ int conv_wgrad_direct(d2ip_act x, d2ip_act gy, int ks, int stride, float* gw, lo
     }
 #undef LAUNCH_T
     D2IP_LAUNCH_CHECK();
-    wgrad_tiled_reduce_k<<<dim3(cdiv((long long)nthr * 4 * cog, 256), batch), 256, 0, st>>>(
+    wgrad_tiled_reduce_k<<<dim3(cdiv((long long)nthr * 4 * cog, 32), batch), 256, 0, st>>>(
         partial, nchunks, nthr, x.c, gy.c, ks * ks * ks, cog, gw, gwbs);
     D2IP_LAUNCH_CHECK();
     return D2IP_OK;

@@ -56,6 +56,9 @@ struct TcConv {
   int accumulate;
   int N, Np, Ns, Kc, CB, n_cb, WR, WRp, Sw, Sh, u_first, tmem_cols;  // Ns: N columns per CTA (slice)
   uint32_t idesc;
+  int kspl;     // split-K factor over the (plane tap, channel block) stages
+  float* part;  // kspl > 1: partial sums [b][kspl][V][N]
+  long long vout;
 };
 
 // Per stage: A hi + A lo windows, B hi + B lo tiles.
@@ -82,7 +85,8 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int b = blockIdx.z;
-  const int n0 = blockIdx.y * a.Ns;  // first output channel of this CTA's slice
+  const int ks = blockIdx.y % a.kspl;
+  const int n0 = (blockIdx.y / a.kspl) * a.Ns;  // first output channel of this CTA's slice
   const int u0 = a.u_first + blockIdx.x * kTcRows;
   const int nkc = a.CB >> 2;
   const size_t Ab = (size_t)a.CB * a.WRp * 4, Bb = (size_t)9 * a.CB * a.Ns * 4;
@@ -118,10 +122,13 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
   const uint32_t tmem = *tslot;
   const float* xb = x.ptr + b * x.bstride;
   const float* wpb = a.wp + b * a.wpbs;
-  const int S = 3 * a.n_cb;
+  const int S_all = 3 * a.n_cb;
+  const int s_lo = (int)((long long)ks * S_all / a.kspl), s_hi = (int)((long long)(ks + 1) * S_all / a.kspl);
+  const int S = s_hi - s_lo;  // this CTA's stages: s_lo + [0, S)
   const int nA = a.WR * nkc;
 
-  auto load = [&](int s, int buf) {
+  auto load = [&](int sl, int buf) {
+    const int s = s_lo + sl;
     const int kd = s / a.n_cb, cb = s - kd * a.n_cb;
     const int* rm = rowmap + kd * a.WR;
     uint8_t* A = smem + buf * Sb;
@@ -207,9 +214,25 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
       v = ((dp - 1) * x.h + (hp - 1)) * x.w + (wp - 1);
   }
   const d2ip_act y = a.y;
+  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+  if (a.kspl > 1) {  // raw partial sums; conv_tc_splitk_reduce_k adds bias / accumulates
+    float* pp = v >= 0 ? a.part + (((long long)b * a.kspl + ks) * a.vout + v) * a.N : nullptr;
+    for (int c0 = 0; c0 < a.Ns; c0 += 8) {
+      float vals[8];
+      tc::tmem_ld8(trow + c0, vals);
+      if (pp) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j)
+          if (n0 + c0 + j < a.N) pp[n0 + c0 + j] = vals[j];
+      }
+    }
+    tc::fence_before();
+    __syncthreads();
+    if (warp == 0) tc::tmem_free(tmem, a.tmem_cols);
+    return;
+  }
   float* yp = v >= 0 ? y.ptr + b * y.bstride + (long long)v * y.cstride : nullptr;
   const float* bias = a.bias ? a.bias + b * a.bbs : nullptr;
-  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
   for (int c0 = 0; c0 < a.Ns; c0 += 8) {
     float vals[8];
     tc::tmem_ld8(trow + c0, vals);
@@ -228,6 +251,22 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
   tc::fence_before();
   __syncthreads();
   if (warp == 0) tc::tmem_free(tmem, a.tmem_cols);
+}
+
+// y[v][n] (+)= bias[n] + sum_ks part[b][ks][v][n]  (fixed order)
+__global__ void conv_tc_splitk_reduce_k(const float* __restrict__ part, int kspl, long long vout, int N,
+                                        const float* __restrict__ bias, long long bbs, d2ip_act y, int accumulate) {
+  const int b = blockIdx.y;
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= vout * N) return;
+  const long long v = i / N;
+  const int n = (int)(i - v * N);
+  const float* p = part + (long long)b * kspl * vout * N + i;
+  float s = 0.f;
+  for (int k = 0; k < kspl; ++k) s += p[(long long)k * vout * N];
+  if (bias) s += __ldg(bias + b * bbs + n);
+  float* yp = y.ptr + b * y.bstride + v * y.cstride + n;
+  *yp = accumulate ? *yp + s : s;
 }
 
 // Pack OIDHW weights into [b][hi|lo][tap][K/4][Np][4] (K-major B tiles).
@@ -270,27 +309,15 @@ int conv_tc_pack(const float* w, long long wbs, int K, int N, int dgrad, float* 
   return D2IP_OK;
 }
 
-int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, long long bbs, d2ip_act y,
-                int accumulate, int batch, cudaStream_t st) {
-  D2IP_CHECK_ARG(x.c == K && y.c == N, "conv_tc: channel mismatch");
-  D2IP_CHECK_ARG(x.cstride % 4 == 0 && ((uintptr_t)x.ptr & 15) == 0, "conv_tc: input view must be 16B aligned");
-  TcConv a{};
-  a.x = x;
-  a.wp = wp;
-  a.wpbs = conv_tc_pack_floats(K, N);
-  a.wlo = a.wpbs / 2;
-  a.bias = bias;
-  a.bbs = bbs;
-  a.y = y;
-  a.accumulate = accumulate;
+// Tile / slice / channel-block / split-K plan for one layer shape.
+static bool tc_plan(int D, int H, int W, int K, int N, int batch, TcConv& a, int* tiles) {
   a.N = N;
   a.Np = np_of(N);
   a.Kc = K;
-  a.Sw = x.w + 2;
-  a.Sh = (x.h + 2) * a.Sw;
+  a.Sw = W + 2;
+  a.Sh = (H + 2) * a.Sw;
   a.WR = wr_of(a.Sw);
   a.WRp = wrp_of(a.WR);
-  // widest N slice whose 2-stage pipeline fits (2 CTAs/SM preferred, then 1)
   a.CB = 0;
   for (size_t budget : {kTcStageBudget, (size_t)210 * 1024}) {
     for (int ns = std::min(a.Np, 256); ns >= 16 && a.CB == 0; ns -= 16) {
@@ -300,11 +327,45 @@ int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, lo
     }
     if (a.CB) break;
   }
-  D2IP_CHECK_ARG(a.CB >= 8, "conv_tc: no channel blocking fits shared memory (K=%d N=%d W=%d)", K, N, x.w);
+  if (a.CB < 8) return false;
   a.n_cb = K / a.CB;
   a.u_first = a.Sh + a.Sw + 1;
-  const int u_last = x.d * a.Sh + x.h * a.Sw + x.w;
-  const int tiles = cdiv(u_last - a.u_first + 1, kTcRows);
+  const int u_last = D * a.Sh + H * a.Sw + W;
+  *tiles = cdiv(u_last - a.u_first + 1, kTcRows);
+  // small grids are latency-bound on the serial stage chain: split the stages
+  // across CTAs until ~2 CTAs per SM are busy (fixed-order partial reduction).
+  const long long ctas = (long long)*tiles * (a.Np / a.Ns) * batch;
+  const int S = 3 * a.n_cb;
+  a.kspl = (int)std::min<long long>(S, std::max(1LL, (296 + ctas - 1) / ctas));
+  a.vout = (long long)D * H * W;
+  return true;
+}
+
+size_t conv_tc_ws_bytes(int D, int H, int W, int K, int N, int batch) {
+  TcConv a{};
+  int tiles;
+  if (!tc_plan(D, H, W, K, N, batch, a, &tiles) || a.kspl <= 1) return 0;
+  return (size_t)batch * a.kspl * a.vout * N * sizeof(float);
+}
+
+int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, long long bbs, d2ip_act y,
+                int accumulate, float* ws, size_t ws_bytes, int batch, cudaStream_t st) {
+  D2IP_CHECK_ARG(x.c == K && y.c == N, "conv_tc: channel mismatch");
+  D2IP_CHECK_ARG(x.cstride % 4 == 0 && ((uintptr_t)x.ptr & 15) == 0, "conv_tc: input view must be 16B aligned");
+  TcConv a{};
+  int tiles = 0;
+  D2IP_CHECK_ARG(tc_plan(x.d, x.h, x.w, K, N, batch, a, &tiles),
+                 "conv_tc: no channel blocking fits shared memory (K=%d N=%d W=%d)", K, N, x.w);
+  if (a.kspl > 1 && (!ws || ws_bytes < (size_t)batch * a.kspl * a.vout * N * sizeof(float))) a.kspl = 1;
+  a.part = ws;
+  a.x = x;
+  a.wp = wp;
+  a.wpbs = conv_tc_pack_floats(K, N);
+  a.wlo = a.wpbs / 2;
+  a.bias = bias;
+  a.bbs = bbs;
+  a.y = y;
+  a.accumulate = accumulate;
   int cols = 32;
   while (cols < a.Ns) cols *= 2;
   a.tmem_cols = cols;
@@ -315,9 +376,14 @@ int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, lo
     D2IP_CUDA(cudaFuncSetAttribute(conv_tc_k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr_set = true;
   }
-  conv_tc_k<<<dim3(tiles, a.Np / a.Ns, batch), kTcThreads, smem, st>>>(a);
-  set_variant("tcgen05_tf32x3");
+  conv_tc_k<<<dim3(tiles, (a.Np / a.Ns) * a.kspl, batch), kTcThreads, smem, st>>>(a);
   D2IP_LAUNCH_CHECK();
+  if (a.kspl > 1) {
+    conv_tc_splitk_reduce_k<<<dim3(cdiv(a.vout * N, 256), batch), 256, 0, st>>>(ws, a.kspl, a.vout, N, bias, bbs, y,
+                                                                                 accumulate);
+    D2IP_LAUNCH_CHECK();
+  }
+  set_variant(a.kspl > 1 ? "tcgen05_tf32x3_splitk" : "tcgen05_tf32x3");
   return D2IP_OK;
 }
 

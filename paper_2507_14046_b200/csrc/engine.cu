@@ -11,6 +11,7 @@
 // provided workspace (planned here, allocated by the host as a torch uint8
 // tensor); parameters, gradients and Adam moments are flat [batch][n_params]
 // fp32 buffers in the reference's state_dict order / OIDHW layout.
+#include <algorithm>
 #include <cstring>
 #include <vector>
 
@@ -67,6 +68,8 @@ struct d2ip_engine {
   void* wg_ws = nullptr;
   size_t wg_ws_bytes = 0;
   void* na_ws = nullptr;
+  float* tc_ws = nullptr;
+  size_t tc_ws_bytes = 0;
   size_t na_ws_bytes = 0;
   size_t ws_total = 0;
   long long maxvc = 0;
@@ -205,7 +208,7 @@ static size_t plan_workspace(d2ip_engine& E, char* base) {
   // reduction workspaces: max over layers
   size_t wg = 0, na = 0;
   auto conv_ws = [&](const ConvP& cv, int lout) {
-    size_t s = conv_wgrad_ws(cv.cin, cv.cout, cv.ks, E.V[lout], B, E.d.precision);
+    size_t s = conv_wgrad_ws(cv.cin, cv.cout, cv.ks, E.D[lout], E.H[lout], E.W[lout], B, E.d.precision);
     if (s > wg) wg = s;
   };
   auto blk_ws = [&](const Block& bl) {
@@ -229,23 +232,28 @@ static size_t plan_workspace(d2ip_engine& E, char* base) {
   E.wg_ws = take(wg);
   E.na_ws = take(na);
   // packed tcgen05 weight tiles, refreshed from theta at the start of every forward
-  auto packs = [&](ConvP& cv, bool need_dgrad) {
+  size_t tcws = 0;  // split-K partials of the tcgen05 convs (max over layers)
+  auto packs = [&](ConvP& cv, bool need_dgrad, int lvl) {
     cv.tcf = conv_tc_supported(cv.cin, cv.cout, cv.ks, cv.stride, E.d.precision);
     cv.tcd = need_dgrad && conv_tc_supported(cv.cout, cv.cin, cv.ks, cv.stride, E.d.precision);
     cv.pkf = cv.tcf ? takef((long long)B * conv_tc_pack_floats(cv.cin, cv.cout)) : nullptr;
     cv.pkd = cv.tcd ? takef((long long)B * conv_tc_pack_floats(cv.cout, cv.cin)) : nullptr;
+    if (cv.tcf) tcws = std::max(tcws, conv_tc_ws_bytes(E.D[lvl], E.H[lvl], E.W[lvl], cv.cin, cv.cout, B));
+    if (cv.tcd) tcws = std::max(tcws, conv_tc_ws_bytes(E.D[lvl], E.H[lvl], E.W[lvl], cv.cout, cv.cin, B));
   };
-  packs(E.stem, false);
-  packs(E.tail, true);
+  packs(E.stem, false, 0);
+  packs(E.tail, true, 0);
   for (auto* v : {&E.enc, &E.dec})
     for (auto& bl : *v) {
-      packs(bl.c1, true);
-      packs(bl.c2, true);
-      packs(bl.sk, true);
+      packs(bl.c1, true, bl.lout);
+      packs(bl.c2, true, bl.lout);
+      packs(bl.sk, true, bl.lout);
     }
-  packs(E.neck.c1, true);
-  packs(E.neck.c2, true);
-  packs(E.neck.sk, true);
+  packs(E.neck.c1, true, E.neck.lout);
+  packs(E.neck.c2, true, E.neck.lout);
+  packs(E.neck.sk, true, E.neck.lout);
+  E.tc_ws_bytes = tcws;
+  E.tc_ws = tcws ? reinterpret_cast<float*>(take(tcws)) : nullptr;
   return (off + 255) & ~(size_t)255;
 }
 
@@ -297,12 +305,14 @@ struct Ctx {
 };
 
 static int cfwd(Ctx& k, const ConvP& c, d2ip_act x, d2ip_act y, int acc) {
-  if (c.tcf) return conv_tc_run(x, c.pkf, c.cin, c.cout, k.th() + c.ob, k.pbs, y, acc, k.B, k.st);
+  if (c.tcf)
+    return conv_tc_run(x, c.pkf, c.cin, c.cout, k.th() + c.ob, k.pbs, y, acc, k.E.tc_ws, k.E.tc_ws_bytes, k.B, k.st);
   return conv_fwd_direct(x, k.th() + c.ow, k.th() + c.ob, k.pbs, c.ks, c.stride, y, acc, k.B, k.st);
 }
 
 static int cdgrad(Ctx& k, const ConvP& c, d2ip_act gy, d2ip_act gx, int acc) {
-  if (c.tcd) return conv_tc_run(gy, c.pkd, c.cout, c.cin, nullptr, 0, gx, acc, k.B, k.st);
+  if (c.tcd)
+    return conv_tc_run(gy, c.pkd, c.cout, c.cin, nullptr, 0, gx, acc, k.E.tc_ws, k.E.tc_ws_bytes, k.B, k.st);
   return conv_dgrad_direct(gy, k.th() + c.ow, k.pbs, c.ks, c.stride, gx, acc, k.B, k.st);
 }
 

@@ -16,14 +16,22 @@ int conv_wgrad_direct(d2ip_act x, d2ip_act gy, int ks, int stride, float* gw, lo
 int reduce_chunks(const float* partial, int nchunks, int n, float* out, long long obs, int batch,
                   cudaStream_t st);
 
+// wgrad_s1.cu — smem-tiled weight gradient of stride-1 3^3 convolutions
+bool wgrad_s1_supported(d2ip_act x, d2ip_act gy);
+size_t wgrad_s1_ws_bytes(int D, int H, int W, int Cin, int Cout, int batch);
+int wgrad_s1(d2ip_act x, d2ip_act gy, float* gw, long long gwbs, void* ws, size_t ws_bytes, int batch,
+             cudaStream_t st);
+
 // conv_tc.cu — tcgen05 implicit-GEMM convolutions (tf32 / bf16 operands)
 bool conv_tc_supported(int cin, int cout, int ks, int stride, int precision);
 long long conv_tc_pack_floats(int K, int N);
 int conv_tc_pack(const float* w, long long wbs, int K, int N, int dgrad, float* out, int batch, cudaStream_t st);
+// ws (optional): split-K partials, conv_tc_ws_bytes() of them; null -> no split-K
+size_t conv_tc_ws_bytes(int D, int H, int W, int K, int N, int batch);
 int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, long long bbs, d2ip_act y,
-                int accumulate, int batch, cudaStream_t st);
+                int accumulate, float* ws, size_t ws_bytes, int batch, cudaStream_t st);
 
-size_t conv_wgrad_ws(int cin, int cout, int ks, long long V, int batch, int precision);
+size_t conv_wgrad_ws(int cin, int cout, int ks, int D, int H, int W, int batch, int precision);
 int conv_wgrad(d2ip_act x, d2ip_act gy, int ks, int stride, float* gw, long long gwbs, void* ws,
                size_t ws_bytes, int precision, int batch, cudaStream_t st);
 
