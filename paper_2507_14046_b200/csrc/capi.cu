@@ -32,16 +32,16 @@ static size_t conv_ws(int cin, int cout, int ks, int stride, int precision, int 
 size_t conv_wgrad_ws(int cin, int cout, int ks, int D, int H, int W, int batch, int precision) {
   (void)precision;
   const size_t a = conv_wgrad_direct_ws(cin, cout, ks, (long long)D * H * W, batch);
-  const size_t b = ks == 3 ? wgrad_s1_ws_bytes(D, H, W, cin, cout, batch) : 0;
+  const size_t b = wgrad_s1_ws_bytes(D, H, W, cin, cout, ks, batch);
   return a > b ? a : b;
 }
 
 int conv_wgrad(d2ip_act x, d2ip_act gy, int ks, int stride, float* gw, long long gwbs, void* ws,
                size_t ws_bytes, int precision, int batch, cudaStream_t st) {
   (void)precision;
-  if (ks == 3 && stride == 1 && wgrad_s1_supported(x, gy)) {
+  if (stride == 1 && wgrad_s1_supported(x, gy, ks)) {
     set_variant("wgrad_s1_smem");
-    return wgrad_s1(x, gy, gw, gwbs, ws, ws_bytes, batch, st);
+    return wgrad_s1(x, gy, ks, gw, gwbs, ws, ws_bytes, batch, st);
   }
   return conv_wgrad_direct(x, gy, ks, stride, gw, gwbs, ws, ws_bytes, batch, st);
 }

@@ -378,10 +378,13 @@ int conv_fwd_direct(d2ip_act x, const float* w, const float* bias, long long wbs
     const size_t sm = (size_t)x.c * KS_ * KS_ * KS_ * CG_ * sizeof(float);                          \
     D2IP_CHECK_ARG(sm <= 200 * 1024, "conv3d_fwd: weight slice too large for shared memory");      \
     D2IP_RET(smem_opt_in(conv_fwd_direct_k<KS_, CG_>, sm));                                        \
-    dim3 grid(cdiv(V, 128), y.c / CG_, batch);                                                      \
-    conv_fwd_direct_k<KS_, CG_><<<grid, 128, sm, st>>>(x, w, bias, wbs, stride, y, accumulate, vec); \
+    dim3 grid(cdiv(V, thr), y.c / CG_, batch);                                                      \
+    conv_fwd_direct_k<KS_, CG_><<<grid, thr, sm, st>>>(x, w, bias, wbs, stride, y, accumulate, vec); \
   } while (0)
-  const int cg = (y.c % 8 == 0) ? 8 : (y.c % 4 == 0 ? 4 : 1);
+  // small layers: narrower channel groups and 64-thread blocks to fill the SMs
+  const bool small = V * (y.c / 8 + 1) * batch < 296LL * 128;
+  const int cg = (y.c % 8 == 0 && !small) ? 8 : (y.c % 4 == 0 ? 4 : 1);
+  const int thr = small ? 64 : 128;
   if (ks == 3) {
     if (cg == 8) LAUNCH_F(3, 8); else if (cg == 4) LAUNCH_F(3, 4); else LAUNCH_F(3, 1);
   } else {
@@ -402,10 +405,12 @@ int conv_dgrad_direct(d2ip_act gy, const float* w, long long wbs, int ks, int st
     const size_t sm = (size_t)gy.c * KS_ * KS_ * KS_ * CG_ * sizeof(float);                       \
     D2IP_CHECK_ARG(sm <= 200 * 1024, "conv3d_dgrad: weight slice too large for shared memory");  \
     D2IP_RET(smem_opt_in(conv_dgrad_direct_k<KS_, CG_>, sm));                                    \
-    dim3 grid(cdiv(V, 128), gx.c / CG_, batch);                                                   \
-    conv_dgrad_direct_k<KS_, CG_><<<grid, 128, sm, st>>>(gy, w, wbs, stride, gx, accumulate, vec); \
+    dim3 grid(cdiv(V, thr), gx.c / CG_, batch);                                                   \
+    conv_dgrad_direct_k<KS_, CG_><<<grid, thr, sm, st>>>(gy, w, wbs, stride, gx, accumulate, vec); \
   } while (0)
-  const int cg = (gx.c % 8 == 0) ? 8 : (gx.c % 4 == 0 ? 4 : 1);
+  const bool small = V * (gx.c / 8 + 1) * batch < 296LL * 128;
+  const int cg = (gx.c % 8 == 0 && !small) ? 8 : (gx.c % 4 == 0 ? 4 : 1);
+  const int thr = small ? 64 : 128;
   if (ks == 3) {
     if (cg == 8) LAUNCH_D(3, 8); else if (cg == 4) LAUNCH_D(3, 4); else LAUNCH_D(3, 1);
   } else {
@@ -462,6 +467,7 @@ static void tiled_split(int cin, int cout, int ks, int cog, long long V, int bat
   long long want = (148LL * 4096 + nthr * batch - 1) / (nthr * batch);
   want = std::min(want, (V + 31) / 32);
   want = std::min(want, std::max(1LL, (4LL << 20) / per_chunk));
+  want = std::min(want, 256LL);  // keeps the fixed-order chunk reduction short
   if (want < 1) want = 1;
   const int c = (int)((V + want - 1) / want);
   *chunk = c;

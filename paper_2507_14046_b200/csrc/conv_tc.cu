@@ -41,7 +41,7 @@ constexpr int kTcThreads = 128;
 constexpr int kTcRows = 128;
 constexpr size_t kTcStageBudget = 110 * 1024;  // both stages; allows 2 CTAs/SM
 
-static inline int np_of(int n) { return (n + 15) / 16 * 16; }
+__host__ __device__ static inline int np_of(int n) { return (n + 15) / 16 * 16; }
 static inline int wr_of(int sw) { return kTcRows + 2 * sw + 2; }
 static inline int wrp_of(int wr) { return wr + ((1 - wr) % 8 + 8) % 8; }  // = 1 mod 8: conflict-free fills
 
@@ -292,6 +292,51 @@ __global__ void conv_tc_pack_k(const float* __restrict__ w, long long wbs, int K
   const float hi = tf32_hi(val);
   out[b * obs + i] = hi;
   out[b * obs + half + i] = val - hi;
+}
+
+// All layers' packs in one launch: blockIdx.x walks the concatenated job ranges.
+__global__ void conv_tc_pack_multi_k(PackJobs j) {
+  const int b = blockIdx.y;
+  int q = 0;
+  while (q + 1 < j.n && blockIdx.x >= j.block0[q + 1]) ++q;
+  const long long half = j.half[q];
+  const long long i = (long long)(blockIdx.x - j.block0[q]) * blockDim.x + threadIdx.x;
+  if (i >= half) return;
+  const int K = j.K[q], N = j.N[q], Np = np_of(N);
+  const int jj = (int)(i & 3);
+  const long long qq = i >> 2;
+  const int n = (int)(qq % Np);
+  const long long q2 = qq / Np;
+  const int kc = (int)(q2 % (K / 4));
+  const int t = (int)(q2 / (K / 4));
+  const int k = 4 * kc + jj;
+  float val = 0.f;
+  if (n < N) {
+    const float* wb = j.w[q] + b * j.wbs;
+    val = j.dgrad[q] ? wb[((long long)k * N + n) * 27 + (26 - t)] : wb[((long long)n * K + k) * 27 + t];
+  }
+  const float hi = tf32_hi(val);
+  float* out = j.out[q] + b * 2 * half;
+  out[i] = hi;
+  out[half + i] = val - hi;
+}
+
+int conv_tc_pack_multi(const PackJobs& jobs, int batch, cudaStream_t st) {
+  if (jobs.n == 0) return D2IP_OK;
+  conv_tc_pack_multi_k<<<dim3(jobs.block0[jobs.n], batch), 256, 0, st>>>(jobs);
+  D2IP_LAUNCH_CHECK();
+  return D2IP_OK;
+}
+
+void pack_jobs_add(PackJobs& j, const float* w, int K, int N, int dgrad, float* out) {
+  const int q = j.n++;
+  j.w[q] = w;
+  j.out[q] = out;
+  j.K[q] = K;
+  j.N[q] = N;
+  j.dgrad[q] = dgrad;
+  j.half[q] = 27LL * K * np_of(N);
+  j.block0[q + 1] = j.block0[q] + (int)((j.half[q] + 255) / 256);
 }
 
 bool conv_tc_supported(int cin, int cout, int ks, int stride, int precision) {

@@ -113,14 +113,18 @@ __global__ void __launch_bounds__(128) tail_fwd_k(d2ip_act x, const float* __res
                                                   float lo, float scale, float* __restrict__ sig,
                                                   float* __restrict__ mapped, float* __restrict__ sigma_c,
                                                   long long sc_bs, const int* __restrict__ col_of_vox) {
+  extern __shared__ float sw[];  // [tap][cin]
   const int b = blockIdx.y;
+  const int cin = x.c;
+  const float* wb = w + b * wbs;
+  for (int i = threadIdx.x; i < 27 * cin; i += blockDim.x) sw[i] = __ldg(wb + (i % cin) * 27 + i / cin);
+  __syncthreads();
   const long long V = (long long)x.d * x.h * x.w;
   const long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (v >= V) return;
   const int ow = (int)(v % x.w), oh = (int)((v / x.w) % x.h), od = (int)(v / ((long long)x.w * x.h));
-  const int cin = x.c;
-  const float* wb = w + b * wbs;
   const float* xb = x.ptr + b * x.bstride;
+  const bool vec = (cin % 4 == 0) && (x.cstride % 4 == 0) && (((uintptr_t)x.ptr & 15) == 0);
   float acc = __ldg(bias + b * wbs);
   for (int kd = 0; kd < 3; ++kd) {
     const int id = od + kd - 1;
@@ -132,8 +136,18 @@ __global__ void __launch_bounds__(128) tail_fwd_k(d2ip_act x, const float* __res
         const int iw = ow + kw - 1;
         if (iw < 0 || iw >= x.w) continue;
         const float* xp = xb + (((long long)id * x.h + ih) * x.w + iw) * x.cstride;
-        const int tap = (kd * 3 + kh) * 3 + kw;
-        for (int ci = 0; ci < cin; ++ci) acc = fmaf(xp[ci], __ldg(wb + ci * 27 + tap), acc);
+        const float* wr = sw + ((kd * 3 + kh) * 3 + kw) * cin;
+        if (vec) {
+          for (int ci = 0; ci < cin; ci += 4) {
+            const float4 q = __ldg(reinterpret_cast<const float4*>(xp + ci));
+            acc = fmaf(q.x, wr[ci], acc);
+            acc = fmaf(q.y, wr[ci + 1], acc);
+            acc = fmaf(q.z, wr[ci + 2], acc);
+            acc = fmaf(q.w, wr[ci + 3], acc);
+          }
+        } else {
+          for (int ci = 0; ci < cin; ++ci) acc = fmaf(xp[ci], wr[ci], acc);
+        }
       }
     }
   }
@@ -149,7 +163,8 @@ int tail_fwd(d2ip_act x, const float* w, const float* bias, long long wbs, float
              float* sig, float* mapped, float* sigma_c, long long sc_bs, const int* col_of_vox,
              int batch, cudaStream_t st) {
   const long long V = (long long)x.d * x.h * x.w;
-  tail_fwd_k<<<dim3(cdiv(V, 128), batch), 128, 0, st>>>(x, w, bias, wbs, lo, scale, sig, mapped,
+  D2IP_CHECK_ARG(27 * x.c * sizeof(float) <= 48 * 1024, "tail: C_in too large");
+  tail_fwd_k<<<dim3(cdiv(V, 128), batch), 128, 27 * x.c * sizeof(float), st>>>(x, w, bias, wbs, lo, scale, sig, mapped,
                                                          sigma_c, sc_bs, col_of_vox);
   D2IP_LAUNCH_CHECK();
   return D2IP_OK;

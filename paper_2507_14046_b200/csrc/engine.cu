@@ -70,6 +70,7 @@ struct d2ip_engine {
   void* na_ws = nullptr;
   float* tc_ws = nullptr;
   size_t tc_ws_bytes = 0;
+  d2ip::PackJobs packjobs;
   size_t na_ws_bytes = 0;
   size_t ws_total = 0;
   long long maxvc = 0;
@@ -320,27 +321,29 @@ static int cwgrad(Ctx& k, const ConvP& c, d2ip_act x, d2ip_act gy) {
   return conv_wgrad(x, gy, c.ks, c.stride, k.gr() + c.ow, k.pbs, k.E.wg_ws, k.E.wg_ws_bytes, k.prec, k.B, k.st);
 }
 
-static int pack_one(Ctx& k, const ConvP& c) {
-  if (c.tcf) D2IP_RET(conv_tc_pack(k.th() + c.ow, k.pbs, c.cin, c.cout, 0, c.pkf, k.B, k.st));
-  if (c.tcd) D2IP_RET(conv_tc_pack(k.th() + c.ow, k.pbs, c.cout, c.cin, 1, c.pkd, k.B, k.st));
-  return D2IP_OK;
-}
-
-static int pack_all(Ctx& k) {
-  d2ip_engine& E = k.E;
-  D2IP_RET(pack_one(k, E.stem));
-  D2IP_RET(pack_one(k, E.tail));
+// The job table of every tcgen05 layer's weight packs (built once at bind).
+static void build_pack_jobs(d2ip_engine& E) {
+  PackJobs& j = E.packjobs;
+  j = PackJobs{};
+  j.wbs = E.nparams;
+  auto add = [&](const ConvP& c) {
+    if (c.tcf) pack_jobs_add(j, E.b.theta + c.ow, c.cin, c.cout, 0, c.pkf);
+    if (c.tcd) pack_jobs_add(j, E.b.theta + c.ow, c.cout, c.cin, 1, c.pkd);
+  };
+  add(E.stem);
+  add(E.tail);
   for (auto* v : {&E.enc, &E.dec})
     for (auto& bl : *v) {
-      D2IP_RET(pack_one(k, bl.c1));
-      D2IP_RET(pack_one(k, bl.c2));
-      D2IP_RET(pack_one(k, bl.sk));
+      add(bl.c1);
+      add(bl.c2);
+      add(bl.sk);
     }
-  D2IP_RET(pack_one(k, E.neck.c1));
-  D2IP_RET(pack_one(k, E.neck.c2));
-  D2IP_RET(pack_one(k, E.neck.sk));
-  return D2IP_OK;
+  add(E.neck.c1);
+  add(E.neck.c2);
+  add(E.neck.sk);
 }
+
+static int pack_all(Ctx& k) { return conv_tc_pack_multi(k.E.packjobs, k.B, k.st); }
 
 static int block_fwd(Ctx& k, Block& bl) {
   d2ip_engine& E = k.E;
@@ -618,6 +621,8 @@ int d2ip_engine_bind(d2ip_engine* e, const d2ip_bindings* b) {
   e->b = *b;
   plan_workspace(*e, reinterpret_cast<char*>(b->workspace));
   plan_views(*e);
+  build_pack_jobs(*e);
+  D2IP_CHECK_ARG(e->packjobs.n <= PackJobs::kMax, "too many tcgen05 layers for one pack launch");
   // one-time zero: J padding columns of sigma_c, unmasked tail gradients
   D2IP_CUDA(cudaMemset(b->workspace, 0, e->ws_total));
   e->bound = true;

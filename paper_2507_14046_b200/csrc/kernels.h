@@ -17,15 +17,28 @@ int reduce_chunks(const float* partial, int nchunks, int n, float* out, long lon
                   cudaStream_t st);
 
 // wgrad_s1.cu — smem-tiled weight gradient of stride-1 3^3 convolutions
-bool wgrad_s1_supported(d2ip_act x, d2ip_act gy);
-size_t wgrad_s1_ws_bytes(int D, int H, int W, int Cin, int Cout, int batch);
-int wgrad_s1(d2ip_act x, d2ip_act gy, float* gw, long long gwbs, void* ws, size_t ws_bytes, int batch,
+bool wgrad_s1_supported(d2ip_act x, d2ip_act gy, int ks);
+size_t wgrad_s1_ws_bytes(int D, int H, int W, int Cin, int Cout, int ks, int batch);
+int wgrad_s1(d2ip_act x, d2ip_act gy, int ks, float* gw, long long gwbs, void* ws, size_t ws_bytes, int batch,
              cudaStream_t st);
 
 // conv_tc.cu — tcgen05 implicit-GEMM convolutions (tf32 / bf16 operands)
 bool conv_tc_supported(int cin, int cout, int ks, int stride, int precision);
 long long conv_tc_pack_floats(int K, int N);
 int conv_tc_pack(const float* w, long long wbs, int K, int N, int dgrad, float* out, int batch, cudaStream_t st);
+// One launch packing every tcgen05 layer of the network (weights change each step).
+struct PackJobs {
+  static constexpr int kMax = 64;
+  int n = 0;
+  long long wbs = 0;  // per-sequence parameter stride
+  const float* w[kMax];
+  float* out[kMax];
+  int K[kMax], N[kMax], dgrad[kMax];
+  long long half[kMax];
+  int block0[kMax + 1] = {0};
+};
+void pack_jobs_add(PackJobs& j, const float* w, int K, int N, int dgrad, float* out);
+int conv_tc_pack_multi(const PackJobs& jobs, int batch, cudaStream_t st);
 // ws (optional): split-K partials, conv_tc_ws_bytes() of them; null -> no split-K
 size_t conv_tc_ws_bytes(int D, int H, int W, int K, int N, int batch);
 int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, long long bbs, d2ip_act y,

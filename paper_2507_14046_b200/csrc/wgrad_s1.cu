@@ -27,6 +27,7 @@ struct WgS1 {
   int Sw, Sh, WR, u_first, u_last;
   int CIB, COB, ncib, ncob;
   int rg, chunks_per_rg, nchunks;
+  int ks;  // 3: 27 taps; 1: the 1^3 skip convolution (centre tap only)
   float* part;  // [b][rg][tiles][32]  (+ bias block [b][rg][cout])
   long long tiles;
 };
@@ -36,13 +37,14 @@ __global__ void __launch_bounds__(288) wgrad_s1_k(WgS1 a) {
   const int b = blockIdx.z;
   const int rg = blockIdx.x;
   const int job = blockIdx.y;
-  const int kd = job % 3, cib = (job / 3) % a.ncib, cob = job / (3 * a.ncib);
+  const int nkd = a.ks == 3 ? 3 : 1;
+  const int kd = a.ks == 3 ? job % 3 : 1, cib = (job / nkd) % a.ncib, cob = job / (nkd * a.ncib);
   const int CIB = a.CIB, COB = a.COB;
   const int nci4 = CIB / 4, nco8 = COB / 8;
   const int tid = threadIdx.x;
-  const int t9 = tid / (nci4 * nco8), rem = tid % (nci4 * nco8);
+  const int t9 = a.ks == 3 ? tid / (nci4 * nco8) : 4, rem = tid % (nci4 * nco8);
   const int ci4 = rem / nco8, co8 = rem % nco8;
-  const int nthr = 9 * nci4 * nco8;
+  const int nthr = (a.ks == 3 ? 9 : 1) * nci4 * nco8;
   const d2ip_act x = a.x, gy = a.gy;
   const int Cin = x.c, Cout = gy.c;
   const float* xb = x.ptr + b * x.bstride + cib * CIB;
@@ -52,7 +54,7 @@ __global__ void __launch_bounds__(288) wgrad_s1_k(WgS1 a) {
   float* G[2] = {sm, sm + gsz + xsz};
   float* X[2] = {sm + gsz, sm + 2 * gsz + xsz};
   const bool active = tid < nthr;
-  const bool do_bias = active && kd == 0 && cib == 0 && t9 == 4 && ci4 == 0;
+  const bool do_bias = active && (a.ks == 1 || kd == 0) && cib == 0 && t9 == 4 && ci4 == 0;
   const int rowoff = (t9 / 3) * a.Sw + (t9 % 3);
   float acc[4][8], bacc[8];
 #pragma unroll
@@ -126,7 +128,8 @@ __global__ void __launch_bounds__(288) wgrad_s1_k(WgS1 a) {
   if (!active) return;
   // tile id in [0, 27 * Cin/4 * Cout/8)
   const int ci4g = cib * nci4 + ci4, co8g = cob * nco8 + co8;
-  const long long tile = ((long long)(kd * 9 + t9) * (Cin / 4) + ci4g) * (Cout / 8) + co8g;
+  const int tap = a.ks == 3 ? kd * 9 + t9 : 0;
+  const long long tile = ((long long)tap * (Cin / 4) + ci4g) * (Cout / 8) + co8g;
   float* p = a.part + (((long long)b * a.rg + rg) * (a.tiles * 32 + Cout)) + tile * 32;
 #pragma unroll
   for (int i = 0; i < 4; ++i)
@@ -141,7 +144,8 @@ __global__ void __launch_bounds__(288) wgrad_s1_k(WgS1 a) {
 
 // sum over row groups (fixed order) and scatter to OIDHW weight + bias grads
 __global__ void __launch_bounds__(256) wgrad_s1_reduce_k(const float* __restrict__ part, int rg, long long tiles,
-                                                         int Cin, int Cout, float* __restrict__ out, long long obs) {
+                                                         int Cin, int Cout, int K3, float* __restrict__ out,
+                                                         long long obs) {
   __shared__ float red[8][33];
   const int b = blockIdx.y;
   const long long n = tiles * 32 + Cout;
@@ -173,9 +177,9 @@ __global__ void __launch_bounds__(256) wgrad_s1_reduce_k(const float* __restrict
     const long long r2 = tile / (Cout / 8);
     const int ci4 = (int)(r2 % (Cin / 4)), t = (int)(r2 / (Cin / 4));
     const int co = co8 * 8 + jj, ci = ci4 * 4 + i;
-    e = ((long long)co * Cin + ci) * 27 + t;
+    e = ((long long)co * Cin + ci) * K3 + t;
   } else {
-    e = (long long)Cout * Cin * 27 + (j - tiles * 32);
+    e = (long long)Cout * Cin * K3 + (j - tiles * 32);
   }
   out[b * obs + e] = s;
 }
@@ -186,7 +190,8 @@ static int pick_block(int c, std::initializer_list<int> opts) {
   return 0;
 }
 
-static bool wg_plan(int D, int H, int W, int Cin, int Cout, int batch, WgS1& a) {
+static bool wg_plan(int D, int H, int W, int Cin, int Cout, int ks, int batch, WgS1& a) {
+  a.ks = ks;
   if (Cin % 4 || Cout % 8) return false;
   a.CIB = pick_block(Cin, {32, 16, 8, 4});
   a.COB = pick_block(Cout, {32, 16, 8});
@@ -199,35 +204,35 @@ static bool wg_plan(int D, int H, int W, int Cin, int Cout, int batch, WgS1& a) 
   a.u_first = a.Sh + a.Sw + 1;
   a.u_last = D * a.Sh + H * a.Sw + W;
   a.nchunks = cdiv(a.u_last - a.u_first + 1, kWgRows);
-  const long long jobs = 3LL * a.ncib * a.ncob * batch;
+  const long long jobs = (ks == 3 ? 3LL : 1LL) * a.ncib * a.ncob * batch;
   int rg = (int)std::max(1LL, std::min<long long>(a.nchunks, (148LL * 4 + jobs - 1) / jobs));
   a.chunks_per_rg = cdiv(a.nchunks, rg);
   a.rg = cdiv(a.nchunks, a.chunks_per_rg);
-  a.tiles = 27LL * (Cin / 4) * (Cout / 8);
+  a.tiles = (long long)ks * ks * ks * (Cin / 4) * (Cout / 8);
   return true;
 }
 
 static size_t wg_smem(const WgS1& a) { return 2 * (size_t)(kWgRows * a.COB + a.WR * a.CIB) * sizeof(float); }
 
-bool wgrad_s1_supported(d2ip_act x, d2ip_act gy) {
+bool wgrad_s1_supported(d2ip_act x, d2ip_act gy, int ks) {
   if (x.d != gy.d || x.h != gy.h || x.w != gy.w) return false;
   if (x.cstride % 4 || gy.cstride % 4 || ((uintptr_t)x.ptr & 15) || ((uintptr_t)gy.ptr & 15)) return false;
   WgS1 a{};
-  if (!wg_plan(x.d, x.h, x.w, x.c, gy.c, 1, a)) return false;
+  if (!wg_plan(x.d, x.h, x.w, x.c, gy.c, ks, 1, a)) return false;
   return wg_smem(a) <= 200 * 1024;
 }
 
-size_t wgrad_s1_ws_bytes(int D, int H, int W, int Cin, int Cout, int batch) {
+size_t wgrad_s1_ws_bytes(int D, int H, int W, int Cin, int Cout, int ks, int batch) {
   WgS1 a{};
-  if (!wg_plan(D, H, W, Cin, Cout, batch, a)) return 0;
+  if (!wg_plan(D, H, W, Cin, Cout, ks, batch, a)) return 0;
   return (size_t)batch * a.rg * (a.tiles * 32 + Cout) * sizeof(float);
 }
 
-int wgrad_s1(d2ip_act x, d2ip_act gy, float* gw, long long gwbs, void* ws, size_t ws_bytes, int batch,
+int wgrad_s1(d2ip_act x, d2ip_act gy, int ks, float* gw, long long gwbs, void* ws, size_t ws_bytes, int batch,
              cudaStream_t st) {
   WgS1 a{};
-  D2IP_CHECK_ARG(wg_plan(x.d, x.h, x.w, x.c, gy.c, batch, a), "wgrad_s1: unsupported shape");
-  D2IP_CHECK_ARG(ws_bytes >= wgrad_s1_ws_bytes(x.d, x.h, x.w, x.c, gy.c, batch), "wgrad_s1: workspace too small");
+  D2IP_CHECK_ARG(wg_plan(x.d, x.h, x.w, x.c, gy.c, ks, batch, a), "wgrad_s1: unsupported shape");
+  D2IP_CHECK_ARG(ws_bytes >= wgrad_s1_ws_bytes(x.d, x.h, x.w, x.c, gy.c, ks, batch), "wgrad_s1: workspace too small");
   a.x = x;
   a.gy = gy;
   a.part = reinterpret_cast<float*>(ws);
@@ -237,12 +242,13 @@ int wgrad_s1(d2ip_act x, d2ip_act gy, float* gw, long long gwbs, void* ws, size_
     D2IP_CUDA(cudaFuncSetAttribute(wgrad_s1_k, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
     attr = true;
   }
-  const int nthr = 9 * (a.CIB / 4) * (a.COB / 8);
+  const int nthr = (ks == 3 ? 9 : 1) * (a.CIB / 4) * (a.COB / 8);
   const int threads = (nthr + 31) / 32 * 32;
-  wgrad_s1_k<<<dim3(a.rg, 3 * a.ncib * a.ncob, batch), threads, smem, st>>>(a);
+  wgrad_s1_k<<<dim3(a.rg, (ks == 3 ? 3 : 1) * a.ncib * a.ncob, batch), threads, smem, st>>>(a);
   D2IP_LAUNCH_CHECK();
   const long long n = a.tiles * 32 + gy.c;
-  wgrad_s1_reduce_k<<<dim3(cdiv(n, 32), batch), 256, 0, st>>>(a.part, a.rg, a.tiles, x.c, gy.c, gw, gwbs);
+  wgrad_s1_reduce_k<<<dim3(cdiv(n, 32), batch), 256, 0, st>>>(a.part, a.rg, a.tiles, x.c, gy.c, ks * ks * ks, gw,
+                                                               gwbs);
   D2IP_LAUNCH_CHECK();
   return D2IP_OK;
 }

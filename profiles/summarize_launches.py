@@ -17,9 +17,13 @@ def load(path):
 
 def main():
     data = load(sys.argv[1])
-    per = int(sys.argv[2]) if len(sys.argv) > 2 else None
     ours = [(k, v) for k, v in data if "d2ip" in k]
-    if per:
+    # one iteration = the launches between two consecutive data-term kernels
+    marks = [i for i, (k, _) in enumerate(ours) if "jac_loss_k" in k]
+    if len(marks) >= 3:
+        ours = ours[marks[-3] + 1:marks[-2] + 1]
+    elif len(sys.argv) > 2:
+        per = int(sys.argv[2])
         ours = ours[-2 * per:-per] if len(ours) >= 2 * per else ours[-per:]
     agg = collections.defaultdict(lambda: [0, 0.0])
     for k, v in ours:
