@@ -71,7 +71,7 @@ class Clocks:
         try:
             self.fh = open(self.path, "w")
             self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.Q}",
-                                          "--format=csv,noheader,nounits", "-lms", "200"],
+                                          "--format=csv,noheader,nounits", "-lms", "50"],
                                          stdout=self.fh, stderr=subprocess.DEVNULL)
         except Exception:
             self.proc = None
@@ -167,16 +167,35 @@ def run_gpu(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     spec = W.CONFIGS[args.workload]
     seed = rank
-    wl = W.make_workload(spec, seed=seed, frames=min(spec.frames, 20))
-    net = spec.network(seed=seed + 1)
-    noise = sample_noise_input(wl.grid, seed, spec.in_channels, 0.1)
-    dn = DeviceNet(net, wl.grid.shape, wl.matrix.n_measurements, wl.matrix.mask, data_norm="l2sq",
-                   output_map=wl.output_map, lr=spec.learning_rate, precision=args.precision or spec.precision,
-                   max_iters=args.warmup + args.steps + 8)
-    dn.set_noise(noise.values)
-    dn.set_J_host(wl.matrix.values)
-    dn.set_theta(kaiming_flat(net))
-    dn.set_dv(wl.voltages.frames[0].values)
+    if spec.sequences > 1:
+        # cfg3: this rank's share of the independent sequences, batched in lockstep
+        from paper_2507_14046_b200.distributed import shard
+        mine = list(shard(spec.sequences, ws, rank))
+        wl = W.make_workload(spec, seed=mine[0], frames=1)
+        net = spec.network()
+        dn = DeviceNet(net, wl.grid.shape, wl.matrix.n_measurements, wl.matrix.mask, batch=len(mine),
+                       j_shared=False, data_norm="l2sq", output_map=wl.output_map, lr=spec.learning_rate,
+                       precision=args.precision or spec.precision, max_iters=args.warmup + args.steps + 8)
+        for b, s in enumerate(mine):
+            Jd, _ = W.jacobian_device(spec, s)
+            dn.set_J_device(Jd, b=b)
+            del Jd
+            dn.set_noise(sample_noise_input(wl.grid, s, spec.in_channels, 0.1).values, b=b)
+            dn.set_theta(kaiming_flat(net, seed=s + 1), b=b)
+            dn.set_dv(wl.voltages.frames[0].values, b=b)
+        units_per_step = len(mine)
+    else:
+        wl = W.make_workload(spec, seed=seed, frames=min(spec.frames, 20))
+        net = spec.network(seed=seed + 1)
+        noise = sample_noise_input(wl.grid, seed, spec.in_channels, 0.1)
+        dn = DeviceNet(net, wl.grid.shape, wl.matrix.n_measurements, wl.matrix.mask, data_norm="l2sq",
+                       output_map=wl.output_map, lr=spec.learning_rate,
+                       precision=args.precision or spec.precision, max_iters=args.warmup + args.steps + 8)
+        dn.set_noise(noise.values)
+        dn.set_J_host(wl.matrix.values)
+        dn.set_theta(kaiming_flat(net))
+        dn.set_dv(wl.voltages.frames[0].values)
+        units_per_step = 1
     dn.reset_frame()
     torch.cuda.synchronize()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
@@ -203,7 +222,7 @@ def run_gpu(args):
     status = dn.status_host()
     assert status[0, 1] == 0, "non-finite loss during the benchmark"
     launches = dn.launches_per_iter()
-    its = ws * args.steps / t_dev
+    its = ws * units_per_step * args.steps / t_dev
 
     # --- no-flush steady state (informational): J may stay L2-resident
     torch.cuda.synchronize()
@@ -212,36 +231,49 @@ def run_gpu(args):
     dn.run(args.steps)
     s1.record()
     torch.cuda.synchronize()
-    its_hot = args.steps / (s0.elapsed_time(s1) / 1e3)
+    its_hot = units_per_step * args.steps / (s0.elapsed_time(s1) / 1e3)
 
     # --- roofline of the dominant kernels, timed live on this stream
     pk, pk_kind = peaks()
     units = algorithmic_units(spec, net, dn.M, dn.Vp)
     L = N.lib()
     st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
-    nseg = L.d2ip_jac_nseg(dn.Vp)
-    part = torch.empty(dn.M * nseg, device="cuda")
-    sig = torch.randn(dn.Vp, device="cuda")
-
-    def jac_fwd():
-        flush.zero_()
-        N.check(L.d2ip_jac_fwd(C.c_void_p(dn.J.data_ptr()), 0, C.c_void_p(sig.data_ptr()), 0, dn.M, dn.Vp,
-                               C.c_void_p(part.data_ptr()), nseg, 1, st), "jac_fwd")
-
     t_flush = time_kernel(lambda: flush.zero_())
-    t_jac = max(time_kernel(jac_fwd) - t_flush, 1e-9)
-    jac_gbs = units["jac_bytes_per_pass"] / t_jac / 1e9
+
+    def jac_probe(M, Vp, J):
+        nseg = L.d2ip_jac_nseg(Vp)
+        part = torch.empty(M * nseg, device="cuda")
+        sig = torch.randn(Vp, device="cuda")
+
+        def run():
+            flush.zero_()
+            N.check(L.d2ip_jac_fwd(C.c_void_p(J.data_ptr()), 0, C.c_void_p(sig.data_ptr()), 0, M, Vp,
+                                   C.c_void_p(part.data_ptr()), nseg, 1, st), "jac_fwd")
+        t = max(time_kernel(run) - t_flush, 1e-9)
+        byt = 4.0 * M * Vp + 4.0 * Vp
+        return {"bound": "hbm", "kernel": "jac_fwd (K5, J.sigma GEMV)", "M": M, "Vp": Vp,
+                "achieved": round(byt / t / 1e9, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
+                "frac": round(byt / t / 1e9 / pk["hbm_gbs"], 4), "algorithmic_bytes_per_launch": byt,
+                "avg_launch_s": t, "peak_source": pk_kind}
+
+    jac_cfg = jac_probe(dn.M, dn.Vp, dn.J)
+    # the same kernel on cfg2's 3,904 x 103,296 operator (1.6 GB, far beyond L2)
+    hbm_probe = None
+    if not args.skip_probe:
+        Vp2 = (103296 + 3) // 4 * 4
+        J2 = torch.randn(3904, Vp2, device="cuda")
+        hbm_probe = jac_probe(3904, Vp2, J2)
+        del J2
+    # dominant kernel: the tcgen05 conv on cfg1's largest layer (dec0.conv1,
+    # 48 -> 16 channels at 32^3), one launch timed live through the C ABI
+    conv_roof = conv_probe(L, N, C, st, pk, pk_kind, flush, t_flush) if spec.channels[0] == 16 else None
     # whole-iteration tensor-throughput view of the convolutions
-    conv_tflops = units["conv_flops"] / (t_dev / args.steps) / 1e12
-    roofline = {"bound": "hbm", "kernel": "jac_fwd (K5, J.sigma GEMV)", "achieved": round(jac_gbs, 1),
-                "peak": pk["hbm_gbs"], "unit": "GB/s", "frac": round(jac_gbs / pk["hbm_gbs"], 4),
-                "traffic": None, "peak_source": pk_kind,
-                "algorithmic_bytes_per_launch": units["jac_bytes_per_pass"],
-                "avg_launch_s": t_jac}
+    conv_tflops = units["conv_flops"] * units_per_step / (t_dev / args.steps) / 1e12
+    roofline = conv_roof or jac_cfg
 
     # --- e2e through the public API (rank-local, one full sequence)
     e2e = None
-    if not args.skip_e2e:
+    if not args.skip_e2e and units_per_step == 1:
         e2e = run_e2e(spec, wl, args, ws)
 
     out = {
@@ -254,14 +286,19 @@ def run_gpu(args):
                    "precision": args.precision or spec.precision,
                    "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
                    "l2": "flushed between timed iterations (256 MB write)"},
-        "frames_per_sec": round(its / ws * spec.frames / (spec.iters_warm + spec.frames * spec.iters_next), 4),
-        "its_no_flush": round(its_hot, 2),
+        "frames_per_sec": round(its * spec.frames / (spec.iters_warm + spec.frames * spec.iters_next), 4),
+        "its_no_flush": round(its_hot * ws, 2),
         "conv_tflops_effective": round(conv_tflops, 3),
         "gpu_launches": launches * args.steps,
         "launches_per_step": launches,
         "roofline": roofline,
+        "roofline_jac_cfg": jac_cfg,
+        "roofline_jac_hbm": hbm_probe,
         "clocks": clk.summary(),
     }
+    if units_per_step > 1:
+        out["config"]["sequences_per_gpu"] = units_per_step
+        out["config"]["parallelism"] = f"{spec.sequences} sequences sharded over {ws} GPU(s), batched in lockstep"
     if e2e is not None:
         out["e2e"] = e2e
     if rank == 0 and ws == 1 and not args.skip_cpu:
@@ -270,6 +307,40 @@ def run_gpu(args):
         print(json.dumps(out))
     if ws > 1:
         dist.destroy_process_group()
+
+
+def conv_probe(L, N, C, st, pk, pk_kind, flush, t_flush):
+    """One launch of the tcgen05 conv on cfg1's dec0.conv1 shape (48 -> 16 @ 32^3),
+    timed with CUDA events; algorithmic FLOPs = 2*27*Cin*Cout*V."""
+    import torch
+
+    cin, cout, D = 48, 16, 32
+    x = torch.randn(1, D, D, D, cin, device="cuda")
+    y = torch.empty(1, D, D, D, cout, device="cuda")
+    w = torch.randn(cout * cin * 27 + cout, device="cuda") * 0.05
+
+    def act(t, c):
+        a = N.Act()
+        a.ptr, a.d, a.h, a.w, a.c, a.cstride = t.data_ptr(), D, D, D, c, c
+        a.bstride = D * D * D * c
+        return a
+
+    wsn = L.d2ip_conv3d_ws_bytes(cin, cout, 3, 1, N.PREC["tf32"], 1)
+    ws = torch.empty(wsn, dtype=torch.uint8, device="cuda")
+    xa, ya = act(x, cin), act(y, cout)
+
+    def run():
+        flush.zero_()
+        N.check(L.d2ip_conv3d_fwd(xa, C.c_void_p(w.data_ptr()), C.c_void_p(w.data_ptr() + 4 * cout * cin * 27), 0,
+                                  3, 1, ya, 0, N.PREC["tf32"], C.c_void_p(ws.data_ptr()), wsn, 1, st), "conv")
+    t = max(time_kernel(run) - t_flush, 1e-9)
+    flops = 2.0 * 27 * cin * cout * D ** 3
+    peak = pk.get("bf16_tflops", 1590.0) / 2  # dense TF32 = 1/2 bf16 (no measured TF32 peak)
+    return {"bound": "tensor", "kernel": "conv_tc_k (K1, tcgen05 3xTF32 implicit GEMM) incl. weight pack",
+            "layer": "dec0.conv1 48->16 @ 32^3", "achieved": round(flops / t / 1e12, 2), "peak": peak,
+            "unit": "TFLOP/s", "frac": round(flops / t / 1e12 / peak, 4), "traffic": None,
+            "algorithmic_flops_per_launch": flops, "avg_launch_s": t,
+            "peak_source": f"{pk_kind} bf16 burst / 2 (TF32 dense); 3xTF32 issues 3 MMAs per product"}
 
 
 def run_e2e(spec, wl, args, ws):
@@ -378,13 +449,14 @@ def run_reference(args):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--steps", type=int, default=300)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--workload", default="cfg1")
     ap.add_argument("--precision", default=None)
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")
+    ap.add_argument("--skip-probe", action="store_true", help="skip the 1.6 GB HBM probe of the J kernel")
     ap.add_argument("--cpu-seconds", type=float, default=15.0)
     ap.add_argument("--e2e-frames", type=int, default=20)
     ap.add_argument("--e2e-warm", type=int, default=2000)

@@ -199,6 +199,9 @@ int d2ip_engine_run(d2ip_engine* e, int iters, void* stream);
 int d2ip_engine_forward(d2ip_engine* e, int with_loss, void* stream);
 /* Forward + y = J sigma into y [batch][M] (predict_measurements, pipeline.py:375-391). */
 int d2ip_engine_predict(d2ip_engine* e, float* y, void* stream);
+/* The Adam update alone, on the current gradient buffer (data-parallel joint
+ * warm-start: grads -> all-reduce -> adam). */
+int d2ip_engine_adam(d2ip_engine* e, void* stream);
 /* Forward + loss + backward without the Adam update (gradient parity). */
 int d2ip_engine_grads(d2ip_engine* e, void* stream);
 /* Kernel launches one graph-replayed iteration issues. */

@@ -129,6 +129,7 @@ _SIGS = {
     "d2ip_engine_forward": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
     "d2ip_engine_grads": (C.c_int, [C.c_void_p, C.c_void_p]),
     "d2ip_engine_predict": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "d2ip_engine_adam": (C.c_int, [C.c_void_p, C.c_void_p]),
     "d2ip_engine_launches_per_iter": (C.c_int, [C.c_void_p]),
 }
 

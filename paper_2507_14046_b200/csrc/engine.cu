@@ -664,6 +664,13 @@ int d2ip_engine_run(d2ip_engine* e, int iters, void* stream) {
   return engine_run(*e, iters, stream);
 }
 
+int d2ip_engine_adam(d2ip_engine* e, void* stream) {
+  using namespace d2ip;
+  D2IP_CHECK_ARG(e && e->bound, "engine not bound");
+  Ctx k = ctx(*e, stream);
+  return adam(k);
+}
+
 int d2ip_engine_predict(d2ip_engine* e, float* y, void* stream) {
   using namespace d2ip;
   D2IP_CHECK_ARG(e && e->bound && y, "engine not bound / null output");

@@ -178,6 +178,18 @@ class DeviceNet:
             self.J[b].copy_(Jd)
             self._bound = False
 
+    def set_J_device(self, J_canon: torch.Tensor, b: int | None = None) -> None:
+        """J already on the GPU, [M][V] in canonical (q-ordered) mask columns."""
+        Jd = torch.zeros((self.M, self.Vp), dtype=torch.float32, device="cuda")
+        Jd[:, :self.V] = J_canon.index_select(1, torch.from_numpy(self.colmap.perm).long().cuda())
+        if self.j_shared:
+            self.set_J(Jd)
+        else:
+            if self.J is None:
+                self.J = torch.zeros((self.batch, self.M, self.Vp), dtype=torch.float32, device="cuda")
+            self.J[b].copy_(Jd)
+            self._bound = False
+
     def _bind(self):
         if self._bound:
             return
@@ -290,6 +302,11 @@ class DeviceNet:
     def grads(self) -> None:
         self._bind()
         N.check(N.lib().d2ip_engine_grads(self._h, N.C.c_void_p(_stream_ptr())), "engine_grads")
+
+    def adam(self) -> None:
+        """Adam on the current gradient buffer (after an external all-reduce)."""
+        self._bind()
+        N.check(N.lib().d2ip_engine_adam(self._h, N.C.c_void_p(_stream_ptr())), "engine_adam")
 
     def predict(self) -> torch.Tensor:
         """y = J sigma for every sequence: [B][M] device fp32."""

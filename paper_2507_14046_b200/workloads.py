@@ -116,6 +116,26 @@ def jacobian(spec: WorkloadSpec, seed: int = 0, row_chunk: int = 256) -> MaskedS
     return MaskedSensitivity(out, mask, grid.ref_id, f"adjacent{spec.n_electrodes}")
 
 
+def jacobian_device(spec: WorkloadSpec, seed: int = 0):
+    """The same J model generated directly on the GPU (torch RNG, seeded) for
+    the large benchmark configs where host generation of M x V normals would
+    dominate the setup. Returns (J [M][V] fp32 cuda, mask). Statistically the
+    same inputs as `jacobian`, not bit-identical (different RNG)."""
+    import torch
+
+    grid = spec.geometry()
+    mask = cylinder_mask(grid)
+    cq = torch.from_numpy(voxel_centres(grid)[vectorize(mask)]).cuda().float()
+    cent = torch.from_numpy(measurement_centroids(spec)).cuda().float()
+    g = torch.Generator(device="cuda").manual_seed(int(seed))
+    J = torch.empty((cent.shape[0], cq.shape[0]), dtype=torch.float32, device="cuda")
+    for r0 in range(0, J.shape[0], 512):
+        r1 = min(J.shape[0], r0 + 512)
+        d = torch.cdist(cent[r0:r1], cq)
+        J[r0:r1] = torch.randn((r1 - r0, cq.shape[0]), generator=g, device="cuda") * torch.exp(-d / spec.decay_length)
+    return J, mask
+
+
 def _ellipsoid(grid: GridGeometry, centre, axes) -> np.ndarray:
     ys, xs, zs = grid.axis_centers()
     u = ((xs[None, :, None] - centre[0]) / axes[0]) ** 2

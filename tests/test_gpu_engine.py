@@ -292,6 +292,46 @@ def test_batched_sequences_match_single():
         assert torch.equal(bn.theta[s], nets[s].theta[0])
 
 
+def test_batched_driver_matches_sequence_driver():
+    """cfg3 per-rank body: sequences in lockstep == reconstruct_sequence each."""
+    from paper_2507_14046_b200.distributed import reconstruct_batched
+    spec = W.small_spec(grid=(8, 8, 8), channels=(8, 16), in_channels=4, rings=(0.5,), frames=3)
+    wls = [W.make_workload(spec, seed=s) for s in range(3)]
+    cfg = RunConfig(iters_warm=8, iters_first=4, iters_next=3, learning_rate=1e-3, seed=0,
+                    network=spec.network(), output_map=(-0.6, 0.3), data_norm="l2sq",
+                    tv_weights=TVWeights(lambda_tv=0.0), precision="fp32")
+    res = reconstruct_batched(wls, cfg, seeds=[0, 1, 2])
+    for s, wl in enumerate(wls):
+        one = reconstruct_sequence(wl.matrix, wl.voltages, RunConfig(**{**cfg.__dict__, "seed": s}), wl.grid)
+        for i in range(3):
+            np.testing.assert_array_equal(np.transpose(res.volumes[s, i], (2, 0, 1)).reshape(-1),
+                                          one.sequence.values[:, i])
+
+
+def test_joint_upws_equals_mean_frame_upws():
+    """cfg4's joint warm-start over F frames with one Z has the gradient of
+    F * ||J sigma - mean dv||^2; Adam is scale-invariant (up to eps)."""
+    spec = W.small_spec(grid=(8, 8, 8), channels=(8, 16), in_channels=4, rings=(0.5,), frames=4)
+    wl = W.make_workload(spec, seed=0)
+    net = spec.network()
+    noise = sample_noise_input(wl.grid, 0, 4, 0.1)
+    dvs = np.stack([f.values for f in wl.voltages.frames])
+    nets = []
+    for n_rhs, dv in ((4, dvs), (1, dvs.mean(0))):
+        dn = DeviceNet(net, wl.grid.shape, wl.matrix.n_measurements, wl.matrix.mask, n_rhs=n_rhs,
+                       output_map=wl.output_map, max_iters=16)
+        dn.set_noise(noise.values)
+        dn.set_J_host(wl.matrix.values)
+        dn.set_theta(kaiming_flat(net, seed=1))
+        dn.set_dv(dv)
+        dn.reset_frame()
+        from paper_2507_14046_b200.distributed import joint_upws
+        joint_upws(dn, 10)  # world size 1: grads -> (no-op all-reduce) -> adam
+        nets.append(dn)
+    torch.cuda.synchronize()
+    assert rel(nets[0].theta[0].cpu().numpy(), nets[1].theta[0].cpu().numpy()) < 1e-4
+
+
 def test_smoke_entry():
     import __graft_entry__
     __graft_entry__.smoke()
