@@ -28,6 +28,7 @@ __global__ void __launch_bounds__(256) adam_k(float4* __restrict__ p, const floa
                                               float4* __restrict__ m, float4* __restrict__ v, long long n4,
                                               float lr, float b1, float b2, float eps,
                                               const int* __restrict__ step, const int* __restrict__ bad) {
+  D2IP_PDL_ENTRY();
   if (bad && *bad) return;
   const int t = *step;
   const double bc1 = 1.0 - pow((double)b1, (double)t);
@@ -50,6 +51,7 @@ __global__ void __launch_bounds__(256) adam_k(float4* __restrict__ p, const floa
 
 __global__ void adam_tail_k(float* p, const float* g, float* m, float* v, long long start, long long n,
                             float lr, float b1, float b2, float eps, const int* step, const int* bad) {
+  D2IP_PDL_ENTRY();
   if (bad && *bad) return;
   const long long i = start + blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -67,14 +69,14 @@ int adam_flat(float* p, const float* g, float* m, float* v, long long n, float l
   if (n4 > 0) {
     long long blocks = (n4 + 255) / 256;
     if (blocks > 148LL * 16) blocks = 148LL * 16;
-    adam_k<<<(int)blocks, 256, 0, st>>>(reinterpret_cast<float4*>(p), reinterpret_cast<const float4*>(g),
+    D2IP_CUDA(launch_pdl(adam_k, (int)blocks, 256, 0, st, reinterpret_cast<float4*>(p), reinterpret_cast<const float4*>(g),
                                         reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v), n4, lr,
-                                        b1, b2, eps, step, bad);
+                                        b1, b2, eps, step, bad));
     D2IP_LAUNCH_CHECK();
   }
   const long long rest = n - n4 * 4;
   if (rest > 0) {
-    adam_tail_k<<<cdiv(rest, 256), 256, 0, st>>>(p, g, m, v, n4 * 4, n, lr, b1, b2, eps, step, bad);
+    D2IP_CUDA(launch_pdl(adam_tail_k, cdiv(rest, 256), 256, 0, st, p, g, m, v, n4 * 4, n, lr, b1, b2, eps, step, bad));
     D2IP_LAUNCH_CHECK();
   }
   return D2IP_OK;

@@ -42,6 +42,34 @@ void set_variant(const char* name);
 
 inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// Programmatic dependent launch: every kernel is launched with the
+// programmatic-stream-serialisation attribute (also inside the captured CUDA
+// graph), waits for its predecessor's completion with griddepcontrol.wait at
+// its top, and immediately allows its successor to be scheduled — so the ~110
+// launches of an iteration overlap their launch latency with the previous
+// kernel's tail. The wait covers the whole predecessor grid and its memory, so
+// early triggering is always safe; dependencies are transitive.
+#define D2IP_PDL_ENTRY()                                              \
+  do {                                                                \
+    asm volatile("griddepcontrol.wait;" ::: "memory");                \
+  } while (0)
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+}
+
 inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
 
 __device__ __forceinline__ long long vox_count(const d2ip_act& a) {

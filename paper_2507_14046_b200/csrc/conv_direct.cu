@@ -31,6 +31,7 @@ __global__ void __launch_bounds__(128) conv_fwd_direct_k(d2ip_act x, const float
                                                          const float* __restrict__ bias,
                                                          long long wbs, int stride, d2ip_act y,
                                                          int accumulate, int vec) {
+  D2IP_PDL_ENTRY();
   constexpr int K3 = Taps<KS>::K3, PAD = Taps<KS>::PAD;
   extern __shared__ float sw[];  // [cin][K3][CG]
   const int b = blockIdx.z;
@@ -92,6 +93,7 @@ template <int KS, int CG>
 __global__ void __launch_bounds__(128) conv_dgrad_direct_k(d2ip_act gy, const float* __restrict__ w,
                                                            long long wbs, int stride, d2ip_act gx,
                                                            int accumulate, int vec) {
+  D2IP_PDL_ENTRY();
   constexpr int K3 = Taps<KS>::K3, PAD = Taps<KS>::PAD;
   extern __shared__ float sw[];  // [cout][K3][CG]
   const int b = blockIdx.z;
@@ -160,6 +162,7 @@ template <int KS>
 __global__ void __launch_bounds__(256) conv_wgrad_partial_k(d2ip_act x, d2ip_act gy, int stride,
                                                             float* __restrict__ partial, int nchunks,
                                                             int chunk) {
+  D2IP_PDL_ENTRY();
   constexpr int K3 = Taps<KS>::K3, PAD = Taps<KS>::PAD;
   const int b = blockIdx.z, c = blockIdx.y;
   const int cin = x.c, cout = gy.c;
@@ -198,6 +201,7 @@ __global__ void __launch_bounds__(256) conv_wgrad_partial_k(d2ip_act x, d2ip_act
 template <int KS, int COG>
 __global__ void __launch_bounds__(128) conv_wgrad_tiled_k(d2ip_act x, d2ip_act gy, int stride,
                                                           float* __restrict__ partial, int nchunks, int chunk) {
+  D2IP_PDL_ENTRY();
   constexpr int K3 = Taps<KS>::K3, PAD = Taps<KS>::PAD;
   const int b = blockIdx.z, c = blockIdx.y;
   const int cin = x.c, cout = gy.c;
@@ -282,6 +286,7 @@ __global__ void __launch_bounds__(128) conv_wgrad_tiled_k(d2ip_act x, d2ip_act g
 __global__ void __launch_bounds__(256) wgrad_tiled_reduce_k(const float* __restrict__ partial, int nchunks,
                                                             int ngroups, int cin, int cout, int K3, int cog,
                                                             float* __restrict__ out, long long obs) {
+  D2IP_PDL_ENTRY();
   __shared__ float red[8][33];
   const int b = blockIdx.y;
   const long long stride = (long long)ngroups * 4 * cog;
@@ -326,6 +331,7 @@ __global__ void __launch_bounds__(256) wgrad_tiled_reduce_k(const float* __restr
 // then warp 0 adds the 8 warp sums in order.
 __global__ void __launch_bounds__(256) reduce_chunks_k(const float* __restrict__ partial, int nchunks, int n,
                                                        float* out, long long obs) {
+  D2IP_PDL_ENTRY();
   __shared__ float red[8][33];
   const int b = blockIdx.y;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
@@ -354,7 +360,7 @@ __global__ void __launch_bounds__(256) reduce_chunks_k(const float* __restrict__
 int reduce_chunks(const float* partial, int nchunks, int n, float* out, long long obs, int batch,
                   cudaStream_t st) {
   dim3 grid(cdiv(n, 32), batch);
-  reduce_chunks_k<<<grid, 256, 0, st>>>(partial, nchunks, n, out, obs);
+  D2IP_CUDA(launch_pdl(reduce_chunks_k, grid, 256, 0, st, partial, nchunks, n, out, obs));
   D2IP_LAUNCH_CHECK();
   return D2IP_OK;
 }
@@ -379,7 +385,7 @@ int conv_fwd_direct(d2ip_act x, const float* w, const float* bias, long long wbs
     D2IP_CHECK_ARG(sm <= 200 * 1024, "conv3d_fwd: weight slice too large for shared memory");      \
     D2IP_RET(smem_opt_in(conv_fwd_direct_k<KS_, CG_>, sm));                                        \
     dim3 grid(cdiv(V, thr), y.c / CG_, batch);                                                      \
-    conv_fwd_direct_k<KS_, CG_><<<grid, thr, sm, st>>>(x, w, bias, wbs, stride, y, accumulate, vec); \
+    D2IP_CUDA(launch_pdl((conv_fwd_direct_k<KS_, CG_>), grid, thr, sm, st, x, w, bias, wbs, stride, y, accumulate, vec)); \
   } while (0)
   // small layers: narrower channel groups and 64-thread blocks to fill the SMs
   const bool small = V * (y.c / 8 + 1) * batch < 296LL * 128;
@@ -406,7 +412,7 @@ int conv_dgrad_direct(d2ip_act gy, const float* w, long long wbs, int ks, int st
     D2IP_CHECK_ARG(sm <= 200 * 1024, "conv3d_dgrad: weight slice too large for shared memory");  \
     D2IP_RET(smem_opt_in(conv_dgrad_direct_k<KS_, CG_>, sm));                                    \
     dim3 grid(cdiv(V, thr), gx.c / CG_, batch);                                                   \
-    conv_dgrad_direct_k<KS_, CG_><<<grid, thr, sm, st>>>(gy, w, wbs, stride, gx, accumulate, vec); \
+    D2IP_CUDA(launch_pdl((conv_dgrad_direct_k<KS_, CG_>), grid, thr, sm, st, gy, w, wbs, stride, gx, accumulate, vec)); \
   } while (0)
   const bool small = V * (gx.c / 8 + 1) * batch < 296LL * 128;
   const int cg = (gx.c % 8 == 0 && !small) ? 8 : (gx.c % 4 == 0 ? 4 : 1);
@@ -487,7 +493,8 @@ int conv_wgrad_direct(d2ip_act x, d2ip_act gy, int ks, int stride, float* gw, lo
                    "conv3d_wgrad: workspace too small");
     float* partial = reinterpret_cast<float*>(ws);
     dim3 grid(cdiv(nthr, 128), nchunks, batch);
-#define LAUNCH_T(KS_, COG_) conv_wgrad_tiled_k<KS_, COG_><<<grid, 128, 0, st>>>(x, gy, stride, partial, nchunks, chunk)
+#define LAUNCH_T(KS_, COG_) \
+  D2IP_CUDA(launch_pdl((conv_wgrad_tiled_k<KS_, COG_>), grid, 128, 0, st, x, gy, stride, partial, nchunks, chunk))
     if (ks == 3) {
       if (cog == 8) LAUNCH_T(3, 8); else if (cog == 4) LAUNCH_T(3, 4); else LAUNCH_T(3, 1);
     } else {
@@ -495,8 +502,8 @@ int conv_wgrad_direct(d2ip_act x, d2ip_act gy, int ks, int stride, float* gw, lo
     }
 #undef LAUNCH_T
     D2IP_LAUNCH_CHECK();
-    wgrad_tiled_reduce_k<<<dim3(cdiv((long long)nthr * 4 * cog, 32), batch), 256, 0, st>>>(
-        partial, nchunks, nthr, x.c, gy.c, ks * ks * ks, cog, gw, gwbs);
+    D2IP_CUDA(launch_pdl(wgrad_tiled_reduce_k, dim3(cdiv((long long)nthr * 4 * cog, 32), batch), 256, 0, st, 
+        partial, nchunks, nthr, x.c, gy.c, ks * ks * ks, cog, gw, gwbs));
     D2IP_LAUNCH_CHECK();
     return D2IP_OK;
   }
@@ -507,9 +514,9 @@ int conv_wgrad_direct(d2ip_act x, d2ip_act gy, int ks, int stride, float* gw, lo
   float* partial = reinterpret_cast<float*>(ws);
   dim3 grid(cdiv(nE, 256), nchunks, batch);
   if (ks == 3)
-    conv_wgrad_partial_k<3><<<grid, 256, 0, st>>>(x, gy, stride, partial, nchunks, chunk);
+    D2IP_CUDA(launch_pdl(conv_wgrad_partial_k<3>, grid, 256, 0, st, x, gy, stride, partial, nchunks, chunk));
   else
-    conv_wgrad_partial_k<1><<<grid, 256, 0, st>>>(x, gy, stride, partial, nchunks, chunk);
+    D2IP_CUDA(launch_pdl(conv_wgrad_partial_k<1>, grid, 256, 0, st, x, gy, stride, partial, nchunks, chunk));
   D2IP_LAUNCH_CHECK();
   return reduce_chunks(partial, nchunks, nE, gw, gwbs, batch, st);
 }

@@ -82,6 +82,7 @@ static size_t tc_smem_bytes(const TcConv& a) {
 __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 
 __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
+  D2IP_PDL_ENTRY();
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int b = blockIdx.z;
@@ -256,6 +257,7 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
 // y[v][n] (+)= bias[n] + sum_ks part[b][ks][v][n]  (fixed order)
 __global__ void conv_tc_splitk_reduce_k(const float* __restrict__ part, int kspl, long long vout, int N,
                                         const float* __restrict__ bias, long long bbs, d2ip_act y, int accumulate) {
+  D2IP_PDL_ENTRY();
   const int b = blockIdx.y;
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= vout * N) return;
@@ -274,6 +276,7 @@ __global__ void conv_tc_splitk_reduce_k(const float* __restrict__ part, int kspl
 //   dgrad  : K = C_out, N = C_in :  P[t][k][n] = W[k][n][26 - t]
 __global__ void conv_tc_pack_k(const float* __restrict__ w, long long wbs, int K, int N, int Np, int dgrad,
                                float* __restrict__ out, long long half, long long obs) {
+  D2IP_PDL_ENTRY();
   const int b = blockIdx.y;
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= half) return;
@@ -296,6 +299,7 @@ __global__ void conv_tc_pack_k(const float* __restrict__ w, long long wbs, int K
 
 // All layers' packs in one launch: blockIdx.x walks the concatenated job ranges.
 __global__ void conv_tc_pack_multi_k(PackJobs j) {
+  D2IP_PDL_ENTRY();
   const int b = blockIdx.y;
   int q = 0;
   while (q + 1 < j.n && blockIdx.x >= j.block0[q + 1]) ++q;
@@ -323,7 +327,7 @@ __global__ void conv_tc_pack_multi_k(PackJobs j) {
 
 int conv_tc_pack_multi(const PackJobs& jobs, int batch, cudaStream_t st) {
   if (jobs.n == 0) return D2IP_OK;
-  conv_tc_pack_multi_k<<<dim3(jobs.block0[jobs.n], batch), 256, 0, st>>>(jobs);
+  D2IP_CUDA(launch_pdl(conv_tc_pack_multi_k, dim3(jobs.block0[jobs.n], batch), 256, 0, st, jobs));
   D2IP_LAUNCH_CHECK();
   return D2IP_OK;
 }
@@ -349,7 +353,7 @@ long long conv_tc_pack_floats(int K, int N) { return 2 * 27LL * K * np_of(N); }
 
 int conv_tc_pack(const float* w, long long wbs, int K, int N, int dgrad, float* out, int batch, cudaStream_t st) {
   const long long total = conv_tc_pack_floats(K, N), half = total / 2;
-  conv_tc_pack_k<<<dim3(cdiv(half, 256), batch), 256, 0, st>>>(w, wbs, K, N, np_of(N), dgrad, out, half, total);
+  D2IP_CUDA(launch_pdl(conv_tc_pack_k, dim3(cdiv(half, 256), batch), 256, 0, st, w, wbs, K, N, np_of(N), dgrad, out, half, total));
   D2IP_LAUNCH_CHECK();
   return D2IP_OK;
 }
@@ -394,7 +398,7 @@ size_t conv_tc_ws_bytes(int D, int H, int W, int K, int N, int batch) {
 }
 
 int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, long long bbs, d2ip_act y,
-                int accumulate, float* ws, size_t ws_bytes, int batch, cudaStream_t st) {
+                int accumulate, float* ws, size_t ws_bytes, int batch, cudaStream_t st, int* deferred) {
   D2IP_CHECK_ARG(x.c == K && y.c == N, "conv_tc: channel mismatch");
   D2IP_CHECK_ARG(x.cstride % 4 == 0 && ((uintptr_t)x.ptr & 15) == 0, "conv_tc: input view must be 16B aligned");
   TcConv a{};
@@ -421,11 +425,12 @@ int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, lo
     D2IP_CUDA(cudaFuncSetAttribute(conv_tc_k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr_set = true;
   }
-  conv_tc_k<<<dim3(tiles, (a.Np / a.Ns) * a.kspl, batch), kTcThreads, smem, st>>>(a);
+  D2IP_CUDA(launch_pdl(conv_tc_k, dim3(tiles, (a.Np / a.Ns) * a.kspl, batch), kTcThreads, smem, st, a));
   D2IP_LAUNCH_CHECK();
-  if (a.kspl > 1) {
-    conv_tc_splitk_reduce_k<<<dim3(cdiv(a.vout * N, 256), batch), 256, 0, st>>>(ws, a.kspl, a.vout, N, bias, bbs, y,
-                                                                                 accumulate);
+  if (deferred) *deferred = a.kspl > 1 ? a.kspl : 0;
+  if (a.kspl > 1 && !deferred) {
+    D2IP_CUDA(launch_pdl(conv_tc_splitk_reduce_k, dim3(cdiv(a.vout * N, 256), batch), 256, 0, st, ws, a.kspl,
+                         a.vout, N, bias, bbs, y, accumulate));
     D2IP_LAUNCH_CHECK();
   }
   set_variant(a.kspl > 1 ? "tcgen05_tf32x3_splitk" : "tcgen05_tf32x3");

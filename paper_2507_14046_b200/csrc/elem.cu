@@ -33,6 +33,7 @@ __device__ __forceinline__ Lin lin_src(int dst, int n) {
 }
 
 __global__ void __launch_bounds__(256) upsample2x_fwd_k(d2ip_act x, d2ip_act y) {
+  D2IP_PDL_ENTRY();
   const int b = blockIdx.y;
   const int C = x.c;
   const long long total = (long long)y.d * y.h * y.w * C;
@@ -56,7 +57,7 @@ int upsample2x_fwd(d2ip_act x, d2ip_act y, int batch, cudaStream_t st) {
   D2IP_CHECK_ARG(y.d == 2 * x.d && y.h == 2 * x.h && y.w == 2 * x.w && y.c == x.c,
                  "upsample2x: shape mismatch");
   const long long total = (long long)y.d * y.h * y.w * y.c;
-  upsample2x_fwd_k<<<dim3(cdiv(total, 256), batch), 256, 0, st>>>(x, y);
+  D2IP_CUDA(launch_pdl(upsample2x_fwd_k, dim3(cdiv(total, 256), batch), 256, 0, st, x, y));
   D2IP_LAUNCH_CHECK();
   return D2IP_OK;
 }
@@ -72,6 +73,7 @@ __device__ __forceinline__ int lin_adj(int m, int n, int* hi, float* wt) {
 }
 
 __global__ void __launch_bounds__(256) upsample2x_bwd_k(d2ip_act gy, d2ip_act gx, int accumulate) {
+  D2IP_PDL_ENTRY();
   const int b = blockIdx.y;
   const int C = gx.c;
   const long long total = (long long)gx.d * gx.h * gx.w * C;
@@ -100,7 +102,7 @@ int upsample2x_bwd(d2ip_act gy, d2ip_act gx, int accumulate, int batch, cudaStre
   D2IP_CHECK_ARG(gy.d == 2 * gx.d && gy.h == 2 * gx.h && gy.w == 2 * gx.w && gy.c == gx.c,
                  "upsample2x_bwd: shape mismatch");
   const long long total = (long long)gx.d * gx.h * gx.w * gx.c;
-  upsample2x_bwd_k<<<dim3(cdiv(total, 256), batch), 256, 0, st>>>(gy, gx, accumulate);
+  D2IP_CUDA(launch_pdl(upsample2x_bwd_k, dim3(cdiv(total, 256), batch), 256, 0, st, gy, gx, accumulate));
   D2IP_LAUNCH_CHECK();
   return D2IP_OK;
 }
@@ -113,6 +115,7 @@ __global__ void __launch_bounds__(128) tail_fwd_k(d2ip_act x, const float* __res
                                                   float lo, float scale, float* __restrict__ sig,
                                                   float* __restrict__ mapped, float* __restrict__ sigma_c,
                                                   long long sc_bs, const int* __restrict__ col_of_vox) {
+  D2IP_PDL_ENTRY();
   extern __shared__ float sw[];  // [tap][cin]
   const int b = blockIdx.y;
   const int cin = x.c;
@@ -164,8 +167,8 @@ int tail_fwd(d2ip_act x, const float* w, const float* bias, long long wbs, float
              int batch, cudaStream_t st) {
   const long long V = (long long)x.d * x.h * x.w;
   D2IP_CHECK_ARG(27 * x.c * sizeof(float) <= 48 * 1024, "tail: C_in too large");
-  tail_fwd_k<<<dim3(cdiv(V, 128), batch), 128, 27 * x.c * sizeof(float), st>>>(x, w, bias, wbs, lo, scale, sig, mapped,
-                                                         sigma_c, sc_bs, col_of_vox);
+  D2IP_CUDA(launch_pdl(tail_fwd_k, dim3(cdiv(V, 128), batch), 128, 27 * x.c * sizeof(float), st, x, w, bias, wbs, lo, scale, sig, mapped,
+                                                         sigma_c, sc_bs, col_of_vox));
   D2IP_LAUNCH_CHECK();
   return D2IP_OK;
 }
@@ -174,6 +177,7 @@ int tail_fwd(d2ip_act x, const float* w, const float* bias, long long wbs, float
 // TV + data gradients for every voxel).
 __global__ void tail_bwd_prep_k(const float* __restrict__ gm, const float* __restrict__ sig, float scale,
                                 float* __restrict__ gt, long long n) {
+  D2IP_PDL_ENTRY();
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const float s = sig[i];
@@ -183,7 +187,7 @@ __global__ void tail_bwd_prep_k(const float* __restrict__ gm, const float* __res
 int tail_bwd_prep(const float* gmapped, const float* sig, float scale, float* gtail, long long V0,
                   int batch, cudaStream_t st) {
   const long long n = V0 * batch;
-  tail_bwd_prep_k<<<cdiv(n, 256), 256, 0, st>>>(gmapped, sig, scale, gtail, n);
+  D2IP_CUDA(launch_pdl(tail_bwd_prep_k, cdiv(n, 256), 256, 0, st, gmapped, sig, scale, gtail, n));
   D2IP_LAUNCH_CHECK();
   return D2IP_OK;
 }

@@ -305,9 +305,17 @@ struct Ctx {
   float* gr() const { return E.b.grad; }
 };
 
-static int cfwd(Ctx& k, const ConvP& c, d2ip_act x, d2ip_act y, int acc) {
-  if (c.tcf)
-    return conv_tc_run(x, c.pkf, c.cin, c.cout, k.th() + c.ob, k.pbs, y, acc, k.E.tc_ws, k.E.tc_ws_bytes, k.B, k.st);
+// Forward conv; with `sk`, a split-K tcgen05 result is left as partials for
+// the consuming LayerNorm kernel to reduce (one launch fewer per layer).
+static int cfwd(Ctx& k, const ConvP& c, d2ip_act x, d2ip_act y, int acc, SplitK* sk = nullptr) {
+  if (c.tcf) {
+    int kspl = 0;
+    D2IP_RET(conv_tc_run(x, c.pkf, c.cin, c.cout, k.th() + c.ob, k.pbs, y, acc, k.E.tc_ws, k.E.tc_ws_bytes, k.B, k.st,
+                         sk && !acc ? &kspl : nullptr));
+    if (sk) *sk = kspl ? SplitK{k.E.tc_ws, kspl, k.th() + c.ob, k.pbs} : SplitK{};
+    return D2IP_OK;
+  }
+  if (sk) *sk = SplitK{};
   return conv_fwd_direct(x, k.th() + c.ow, k.th() + c.ob, k.pbs, c.ks, c.stride, y, acc, k.B, k.st);
 }
 
@@ -352,11 +360,14 @@ static int block_fwd(Ctx& k, Block& bl) {
   d2ip_act raw2 = view(E, E.raw2, bl.lout, co, co);
   d2ip_act h1 = view(E, bl.h1, bl.lout, co, co);
   d2ip_act none{};
-  D2IP_RET(cfwd(k, bl.c1, bl.x, raw, 0));
-  D2IP_RET(norm_act_fwd(raw, k.th() + bl.n1.og, k.th() + bl.n1.ob, k.pbs, none, 1, k.slope, h1, bl.xh1, bl.rs1, k.B, k.st));
-  D2IP_RET(cfwd(k, bl.c2, h1, raw, 0));
-  D2IP_RET(cfwd(k, bl.sk, bl.x, raw2, 0));
-  D2IP_RET(norm_act_fwd(raw, k.th() + bl.n2.og, k.th() + bl.n2.ob, k.pbs, raw2, 1, k.slope, bl.out, bl.xh2, bl.rs2, k.B, k.st));
+  SplitK sk;
+  D2IP_RET(cfwd(k, bl.c1, bl.x, raw, 0, &sk));
+  D2IP_RET(norm_act_fwd(raw, k.th() + bl.n1.og, k.th() + bl.n1.ob, k.pbs, none, 1, k.slope, h1, bl.xh1, bl.rs1, k.B,
+                        k.st, sk));
+  D2IP_RET(cfwd(k, bl.c2, h1, raw, 0, &sk));
+  D2IP_RET(cfwd(k, bl.sk, bl.x, raw2, 0));  // 1^3 skip: direct kernel, leaves the split-K partials intact
+  D2IP_RET(norm_act_fwd(raw, k.th() + bl.n2.og, k.th() + bl.n2.ob, k.pbs, raw2, 1, k.slope, bl.out, bl.xh2, bl.rs2,
+                        k.B, k.st, sk));
   return D2IP_OK;
 }
 
@@ -388,9 +399,10 @@ static int forward(Ctx& k) {
   d2ip_act a0 = view(E, E.cat[0] + c[1], 0, c[0], E.catw[0]);
   d2ip_act none{};
   D2IP_RET(pack_all(k));
-  D2IP_RET(cfwd(k, E.stem, z, raw, 0));
+  SplitK sk;
+  D2IP_RET(cfwd(k, E.stem, z, raw, 0, &sk));
   D2IP_RET(norm_act_fwd(raw, k.th() + E.stem_n.og, k.th() + E.stem_n.ob, k.pbs, none, 1, k.slope, a0, E.stem_xh,
-                        E.stem_rs, k.B, k.st));
+                        E.stem_rs, k.B, k.st, sk));
   for (auto& bl : E.enc) D2IP_RET(block_fwd(k, bl));
   D2IP_RET(block_fwd(k, E.neck));
   for (size_t j = 0; j < E.dec.size(); ++j) {
@@ -506,6 +518,7 @@ int engine_forward(d2ip_engine& E, int with_loss, void* stream) {
 }
 
 __global__ void status_k(int* status, int batch, int mode, int value) {
+  D2IP_PDL_ENTRY();
   const int b = threadIdx.x;
   if (b >= batch) return;
   if (mode == 0) {
@@ -520,14 +533,14 @@ int engine_reset_frame(d2ip_engine& E, void* stream) {
   const size_t bytes = (size_t)E.d.batch * E.nparams * sizeof(float);
   D2IP_CUDA(cudaMemsetAsync(E.b.adam_m, 0, bytes, S(stream)));
   D2IP_CUDA(cudaMemsetAsync(E.b.adam_v, 0, bytes, S(stream)));
-  status_k<<<1, 1024, 0, S(stream)>>>(E.b.status, E.d.batch, 0, 0);
+  D2IP_CUDA(launch_pdl(status_k, 1, 1024, 0, S(stream), E.b.status, E.d.batch, 0, 0));
   D2IP_LAUNCH_CHECK();
   return D2IP_OK;
 }
 
 int engine_set_history(d2ip_engine& E, int n, void* stream) {
   D2IP_CHECK_ARG(n >= 0 && n <= E.d.max_history, "history count %d outside [0, %d]", n, E.d.max_history);
-  status_k<<<1, 1024, 0, S(stream)>>>(E.b.status, E.d.batch, 1, n);
+  D2IP_CUDA(launch_pdl(status_k, 1, 1024, 0, S(stream), E.b.status, E.d.batch, 1, n));
   D2IP_LAUNCH_CHECK();
   return D2IP_OK;
 }

@@ -26,6 +26,7 @@ int jac_nseg(int vp) { return cdiv(vp, kGemvSeg); }
 __global__ void __launch_bounds__(kGemvThreads) jac_fwd_k(const float* __restrict__ J, long long jbs,
                                                           const float* __restrict__ sigma, long long sbs,
                                                           int vp, float* __restrict__ partial, int nseg) {
+  D2IP_PDL_ENTRY();
   __shared__ float red[kGemvThreads / 32];
   const int seg = blockIdx.x, m = blockIdx.y, b = blockIdx.z;
   const float4* row = reinterpret_cast<const float4*>(J + b * jbs + (long long)m * vp);
@@ -61,7 +62,7 @@ int jac_fwd_partial(const float* J, long long jbs, const float* sigma, long long
   D2IP_CHECK_ARG(vp % 4 == 0, "jac: Vp=%d not a multiple of 4", vp);
   D2IP_CHECK_ARG(((uintptr_t)J & 15) == 0 && ((uintptr_t)sigma & 15) == 0, "jac: J/sigma not 16B aligned");
   dim3 grid(nseg, m, batch);
-  jac_fwd_k<<<grid, kGemvThreads, 0, st>>>(J, jbs, sigma, sbs, vp, partial, nseg);
+  D2IP_CUDA(launch_pdl(jac_fwd_k, grid, kGemvThreads, 0, st, J, jbs, sigma, sbs, vp, partial, nseg));
   D2IP_LAUNCH_CHECK();
   return D2IP_OK;
 }
@@ -74,6 +75,7 @@ __global__ void __launch_bounds__(1024) jac_loss_k(const float* __restrict__ par
                                                    float reg_scale, float* __restrict__ rs,
                                                    float* __restrict__ trace, int max_iters,
                                                    int* __restrict__ status) {
+  D2IP_PDL_ENTRY();
   __shared__ float red[32];
   const int b = blockIdx.x;
   float acc = 0.f;
@@ -125,13 +127,14 @@ __global__ void __launch_bounds__(1024) jac_loss_k(const float* __restrict__ par
 int jac_loss(const float* partial, int nseg, int m, const float* dv, int n_rhs, int norm,
              const float* reg_partial, int n_reg, float reg_scale, float* rs, float* trace,
              int max_iters, int* status, int batch, cudaStream_t st) {
-  jac_loss_k<<<batch, 1024, 0, st>>>(partial, nseg, m, dv, n_rhs, norm, reg_partial, n_reg, reg_scale,
-                                     rs, trace, max_iters, status);
+  D2IP_CUDA(launch_pdl(jac_loss_k, batch, 1024, 0, st, partial, nseg, m, dv, n_rhs, norm, reg_partial, n_reg, reg_scale,
+                                     rs, trace, max_iters, status));
   D2IP_LAUNCH_CHECK();
   return D2IP_OK;
 }
 
 __global__ void jac_sum_k(const float* __restrict__ partial, int nseg, int M, float* __restrict__ y) {
+  D2IP_PDL_ENTRY();
   const int b = blockIdx.y;
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= M) return;
@@ -142,7 +145,7 @@ __global__ void jac_sum_k(const float* __restrict__ partial, int nseg, int M, fl
 }
 
 int jac_sum(const float* partial, int nseg, int m, float* y, int batch, cudaStream_t st) {
-  jac_sum_k<<<dim3(cdiv(m, 256), batch), 256, 0, st>>>(partial, nseg, m, y);
+  D2IP_CUDA(launch_pdl(jac_sum_k, dim3(cdiv(m, 256), batch), 256, 0, st, partial, nseg, m, y));
   D2IP_LAUNCH_CHECK();
   return D2IP_OK;
 }
@@ -166,6 +169,7 @@ size_t jac_adj_ws(int m, int vp, int batch) {
 __global__ void __launch_bounds__(kAdjThreads) jac_adj_k(const float* __restrict__ J, long long jbs,
                                                          const float* __restrict__ rs, int M, int vp,
                                                          float* __restrict__ partial, int rsplit) {
+  D2IP_PDL_ENTRY();
   extern __shared__ float rsm[];
   const int b = blockIdx.z, sp = blockIdx.y;
   const int rows = (M + rsplit - 1) / rsplit;
@@ -206,7 +210,7 @@ int jac_adj_partial(const float* J, long long jbs, const float* rs, int m, int v
                     int rsplit, int batch, cudaStream_t st) {
   const int rows = cdiv(m, rsplit);
   dim3 grid(cdiv(vp, kAdjCols), rsplit, batch);
-  jac_adj_k<<<grid, kAdjThreads, rows * sizeof(float), st>>>(J, jbs, rs, m, vp, partial, rsplit);
+  D2IP_CUDA(launch_pdl(jac_adj_k, grid, kAdjThreads, rows * sizeof(float), st, J, jbs, rs, m, vp, partial, rsplit));
   D2IP_LAUNCH_CHECK();
   return D2IP_OK;
 }
@@ -217,6 +221,7 @@ int jac_adj_partial(const float* J, long long jbs, const float* rs, int m, int v
 __global__ void jac_adj_finish_k(const float* __restrict__ partial, int rsplit, int vp, int V,
                                  const int* __restrict__ vox_of_col, const float* __restrict__ sig,
                                  float scale, float* __restrict__ gout, long long V0, int add) {
+  D2IP_PDL_ENTRY();
   const int b = blockIdx.y;
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= V) return;
@@ -235,8 +240,8 @@ __global__ void jac_adj_finish_k(const float* __restrict__ partial, int rsplit, 
 int jac_adj_finish(const float* partial, int rsplit, int vp, int v, const int* vox_of_col,
                    const float* sig, float scale, float* gout, long long V0, int add_to_gmapped,
                    int batch, cudaStream_t st) {
-  jac_adj_finish_k<<<dim3(cdiv(v, 256), batch), 256, 0, st>>>(partial, rsplit, vp, v, vox_of_col, sig,
-                                                               scale, gout, V0, add_to_gmapped);
+  D2IP_CUDA(launch_pdl(jac_adj_finish_k, dim3(cdiv(v, 256), batch), 256, 0, st, partial, rsplit, vp, v, vox_of_col, sig,
+                                                               scale, gout, V0, add_to_gmapped));
   D2IP_LAUNCH_CHECK();
   return D2IP_OK;
 }

@@ -41,8 +41,19 @@ void pack_jobs_add(PackJobs& j, const float* w, int K, int N, int dgrad, float* 
 int conv_tc_pack_multi(const PackJobs& jobs, int batch, cudaStream_t st);
 // ws (optional): split-K partials, conv_tc_ws_bytes() of them; null -> no split-K
 size_t conv_tc_ws_bytes(int D, int H, int W, int K, int N, int batch);
+// deferred != null: a split-K result is left as partials in ws (*deferred =
+// kspl, 0 if not split) for the consumer to reduce (norm_act_fwd's `part`).
 int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, long long bbs, d2ip_act y,
-                int accumulate, float* ws, size_t ws_bytes, int batch, cudaStream_t st);
+                int accumulate, float* ws, size_t ws_bytes, int batch, cudaStream_t st, int* deferred = nullptr);
+
+// Split-K partial sums handed from a convolution to its consumer:
+// y[v][n] = bias[n] + sum_k part[b][k][v][n].
+struct SplitK {
+  const float* part = nullptr;
+  int kspl = 0;
+  const float* bias = nullptr;
+  long long bbs = 0;
+};
 
 size_t conv_wgrad_ws(int cin, int cout, int ks, int D, int H, int W, int batch, int precision);
 int conv_wgrad(d2ip_act x, d2ip_act gy, int ks, int stride, float* gw, long long gwbs, void* ws,
@@ -51,7 +62,7 @@ int conv_wgrad(d2ip_act x, d2ip_act gy, int ks, int stride, float* gw, long long
 // elem.cu — normalisation / activation / resampling / output map
 int norm_act_fwd(d2ip_act y, const float* gamma, const float* beta, long long pbs, d2ip_act res,
                  int act, float slope, d2ip_act out, float* xhat, float* rstd, int batch,
-                 cudaStream_t st);
+                 cudaStream_t st, SplitK sk = SplitK{});
 size_t norm_act_bwd_ws(long long V, int C, int batch);
 int norm_act_bwd(d2ip_act gout, d2ip_act out, int act, float slope, const float* xhat,
                  const float* rstd, const float* gamma, long long pbs, d2ip_act gpre, d2ip_act gc,

@@ -57,7 +57,8 @@ __global__ void __launch_bounds__(kNormThreads) norm_act_fwd_k(d2ip_act y, const
                                                                const float* __restrict__ beta, long long pbs,
                                                                d2ip_act res, int act, float slope, d2ip_act out,
                                                                float* __restrict__ xhat, float* __restrict__ rstd,
-                                                               int G) {
+                                                               int G, SplitK sk) {
+  D2IP_PDL_ENTRY();
   const int b = blockIdx.y;
   const int C = y.c, L = C / VPL;
   const long long V = (long long)y.d * y.h * y.w;
@@ -79,7 +80,21 @@ __global__ void __launch_bounds__(kNormThreads) norm_act_fwd_k(d2ip_act y, const
     float x[VPL];
 #pragma unroll
     for (int i = 0; i < VPL; ++i) x[i] = 0.f;
-    if (ok) ld<VPL>(y.ptr + b * y.bstride + v * y.cstride + c0, x);
+    if (ok) {
+      if (sk.part) {  // the producing convolution's split-K partials + bias (fixed order)
+        const float* p = sk.part + ((long long)b * sk.kspl * V + v) * C + c0;
+#pragma unroll
+        for (int i = 0; i < VPL; ++i) x[i] = __ldg(sk.bias + b * sk.bbs + c0 + i);
+        for (int k = 0; k < sk.kspl; ++k) {
+          float t[VPL];
+          ld<VPL>(p + (long long)k * V * C, t);
+#pragma unroll
+          for (int i = 0; i < VPL; ++i) x[i] += t[i];
+        }
+      } else {
+        ld<VPL>(y.ptr + b * y.bstride + v * y.cstride + c0, x);
+      }
+    }
     float s = 0.f;
 #pragma unroll
     for (int i = 0; i < VPL; ++i) s += x[i];
@@ -117,18 +132,21 @@ static int norm_blocks(long long V, int G, int batch) {
 }
 
 int norm_act_fwd(d2ip_act y, const float* gamma, const float* beta, long long pbs, d2ip_act res, int act,
-                 float slope, d2ip_act out, float* xhat, float* rstd, int batch, cudaStream_t st) {
+                 float slope, d2ip_act out, float* xhat, float* rstd, int batch, cudaStream_t st, SplitK sk) {
   const int C = y.c;
   D2IP_CHECK_ARG(C % 4 == 0 && C <= 256, "norm_act: C=%d must be a multiple of 4, <= 256", C);
   D2IP_CHECK_ARG(y.cstride % 4 == 0 && out.cstride % 4 == 0 && (!res.ptr || res.cstride % 4 == 0),
                  "norm_act: views must be float4 aligned");
+  D2IP_CHECK_ARG(!sk.part || sk.bias, "norm_act: split-K partials need the bias");
   const NormGeom g = norm_geom(C);
   const long long V = (long long)y.d * y.h * y.w;
   dim3 grid(norm_blocks(V, g.G, batch), batch);
   if (g.vpl == 4)
-    norm_act_fwd_k<4><<<grid, kNormThreads, 0, st>>>(y, gamma, beta, pbs, res, act, slope, out, xhat, rstd, g.G);
+    D2IP_CUDA(launch_pdl(norm_act_fwd_k<4>, grid, kNormThreads, 0, st, y, gamma, beta, pbs, res, act, slope, out,
+                         xhat, rstd, g.G, sk));
   else
-    norm_act_fwd_k<8><<<grid, kNormThreads, 0, st>>>(y, gamma, beta, pbs, res, act, slope, out, xhat, rstd, g.G);
+    D2IP_CUDA(launch_pdl(norm_act_fwd_k<8>, grid, kNormThreads, 0, st, y, gamma, beta, pbs, res, act, slope, out,
+                         xhat, rstd, g.G, sk));
   D2IP_LAUNCH_CHECK();
   return D2IP_OK;
 }
@@ -142,6 +160,7 @@ __global__ void __launch_bounds__(kNormThreads) norm_act_bwd_k(d2ip_act gout, d2
                                                                const float* __restrict__ gamma, long long pbs,
                                                                d2ip_act gpre, d2ip_act gc,
                                                                float* __restrict__ partial, int G) {
+  D2IP_PDL_ENTRY();
   extern __shared__ float red[];  // [groups][2C]
   const int b = blockIdx.y;
   const int C = gout.c, L = C / VPL;
@@ -229,11 +248,11 @@ int norm_act_bwd(d2ip_act gout, d2ip_act out, int act, float slope, const float*
   const size_t smem = (size_t)(kNormThreads / g.G) * 2 * C * sizeof(float);
   dim3 grid(nb, batch);
   if (g.vpl == 4)
-    norm_act_bwd_k<4><<<grid, kNormThreads, smem, st>>>(gout, out, act, slope, xhat, rstd, gamma, pbs, gpre, gc,
-                                                        partial, g.G);
+    D2IP_CUDA(launch_pdl(norm_act_bwd_k<4>, grid, kNormThreads, smem, st, gout, out, act, slope, xhat, rstd, gamma, pbs, gpre, gc,
+                                                        partial, g.G));
   else
-    norm_act_bwd_k<8><<<grid, kNormThreads, smem, st>>>(gout, out, act, slope, xhat, rstd, gamma, pbs, gpre, gc,
-                                                        partial, g.G);
+    D2IP_CUDA(launch_pdl(norm_act_bwd_k<8>, grid, kNormThreads, smem, st, gout, out, act, slope, xhat, rstd, gamma, pbs, gpre, gc,
+                                                        partial, g.G));
   D2IP_LAUNCH_CHECK();
   return reduce_chunks(partial, nb, 2 * C, dgb, dgbs, batch, st);
 }

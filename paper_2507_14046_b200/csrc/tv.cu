@@ -36,6 +36,7 @@ __global__ void __launch_bounds__(kTvThreads) tv_k(const float* __restrict__ map
                                                    const int* __restrict__ status, int R, int C, int P,
                                                    float lam_tv, float lam_s, float lam_t, float eps,
                                                    float* __restrict__ gmapped, float* __restrict__ reg_partial) {
+  D2IP_PDL_ENTRY();
   __shared__ float red[kTvThreads / 32];
   const int b = blockIdx.y;
   const long long Q = (long long)R * C * P;
@@ -81,8 +82,8 @@ int tv_fwd_bwd(const float* mapped, const float* history, int max_history, const
                int R, int C, int P, float lam_tv, float lam_s, float lam_t, float eps,
                float* gmapped, float* reg_partial, int batch, cudaStream_t st) {
   const long long Q = (long long)R * C * P;
-  tv_k<<<dim3(tv_nblocks(Q), batch), kTvThreads, 0, st>>>(mapped, history, max_history, status, R, C, P,
-                                                           lam_tv, lam_s, lam_t, eps, gmapped, reg_partial);
+  D2IP_CUDA(launch_pdl(tv_k, dim3(tv_nblocks(Q), batch), kTvThreads, 0, st, mapped, history, max_history, status, R, C, P,
+                                                           lam_tv, lam_s, lam_t, eps, gmapped, reg_partial));
   D2IP_LAUNCH_CHECK();
   return D2IP_OK;
 }

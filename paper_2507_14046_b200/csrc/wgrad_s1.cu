@@ -33,6 +33,7 @@ struct WgS1 {
 };
 
 __global__ void __launch_bounds__(288) wgrad_s1_k(WgS1 a) {
+  D2IP_PDL_ENTRY();
   extern __shared__ __align__(16) float sm[];
   const int b = blockIdx.z;
   const int rg = blockIdx.x;
@@ -146,6 +147,7 @@ __global__ void __launch_bounds__(288) wgrad_s1_k(WgS1 a) {
 __global__ void __launch_bounds__(256) wgrad_s1_reduce_k(const float* __restrict__ part, int rg, long long tiles,
                                                          int Cin, int Cout, int K3, float* __restrict__ out,
                                                          long long obs) {
+  D2IP_PDL_ENTRY();
   __shared__ float red[8][33];
   const int b = blockIdx.y;
   const long long n = tiles * 32 + Cout;
@@ -244,11 +246,11 @@ int wgrad_s1(d2ip_act x, d2ip_act gy, int ks, float* gw, long long gwbs, void* w
   }
   const int nthr = (ks == 3 ? 9 : 1) * (a.CIB / 4) * (a.COB / 8);
   const int threads = (nthr + 31) / 32 * 32;
-  wgrad_s1_k<<<dim3(a.rg, (ks == 3 ? 3 : 1) * a.ncib * a.ncob, batch), threads, smem, st>>>(a);
+  D2IP_CUDA(launch_pdl(wgrad_s1_k, dim3(a.rg, (ks == 3 ? 3 : 1) * a.ncib * a.ncob, batch), threads, smem, st, a));
   D2IP_LAUNCH_CHECK();
   const long long n = a.tiles * 32 + gy.c;
-  wgrad_s1_reduce_k<<<dim3(cdiv(n, 32), batch), 256, 0, st>>>(a.part, a.rg, a.tiles, x.c, gy.c, ks * ks * ks, gw,
-                                                               gwbs);
+  D2IP_CUDA(launch_pdl(wgrad_s1_reduce_k, dim3(cdiv(n, 32), batch), 256, 0, st, a.part, a.rg, a.tiles, x.c, gy.c, ks * ks * ks, gw,
+                                                               gwbs));
   D2IP_LAUNCH_CHECK();
   return D2IP_OK;
 }
