@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define D2IP_ABI_VERSION 2
+#define D2IP_ABI_VERSION 3
 
 enum {
   D2IP_OK = 0,
@@ -46,6 +46,11 @@ enum {
 
 enum { D2IP_PREC_FP32 = 0, D2IP_PREC_TF32 = 1, D2IP_PREC_BF16 = 2 };
 enum { D2IP_NORM_L2SQ = 0, D2IP_NORM_L2 = 1 };
+/* Network program of the engine. */
+enum {
+  D2IP_ARCH_CONFIG_RESUNET = 0, /* canonical config ResUNet (LeakyReLU, C_z-channel noise) */
+  D2IP_ARCH_FAST_RESUNET = 1    /* reference FastResUNet3D (priornet.py:183-232; SiLU, SE, ASPP, attention) */
+};
 
 /* A channels-last activation view (see conventions). */
 typedef struct {
@@ -136,8 +141,10 @@ int d2ip_adam(float* p, const float* g, float* m, float* v, long long n, float l
               float beta2, float eps, const int* step, void* stream);
 
 /* ---- Engine: one whole DIP iteration, graph-captured --------------------
- * Owns the launch plan of the canonical ResUNet for `batch`
- * independent sequences in lockstep (cfg3) and replays it with CUDA graphs.
+ * Owns the launch plan of one network program (`arch`: the canonical config
+ * ResUNet of SURVEY §7.1, or the reference's FastResUNet3D with levels = 4,
+ * channels = b,2b,4b,8b, in_channels = 1) for `batch` independent sequences
+ * in lockstep (cfg3) and replays it with CUDA graphs.
  * Replaces the Python loop body pipeline.py:310-331. */
 typedef struct {
   int batch;                 /* independent sequences, each its own theta/Z/J */
@@ -158,6 +165,11 @@ typedef struct {
   float lambda_tv, lambda_s, lambda_t, tv_eps;
   int max_history;           /* TV history capacity (frames) */
   int max_iters;             /* trace capacity */
+  /* ABI 3 */
+  int arch;                  /* D2IP_ARCH_* */
+  int depthwise;             /* FastResUNet3D: depthwise-separable 3^3 (NetworkConfig.use_depthwise) */
+  int n_dil;                 /* FastResUNet3D: ASPP branches (NetworkConfig.aspp_dilations) */
+  int dil[8];
 } d2ip_net_desc;
 
 typedef struct {

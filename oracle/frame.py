@@ -62,11 +62,12 @@ def oracle_tv4d(history, current, lambda_s=1.0, lambda_t=0.1, eps=1e-8):
 
 
 class OracleFrameOptimizer:
-    """pipeline.py:266-338 for the config ResUNet."""
+    """pipeline.py:266-338 for the config ResUNet (or any prebuilt `model`)."""
 
     def __init__(self, channels, in_channels, z, J, qcols, output_map, lr, betas=(0.9, 0.999),
-                 data_norm="l2sq", tv=(0.0, 1.0, 0.1, 1e-8), slope=0.2, record_every=1):
-        self.model = build_oracle_net(channels, in_channels, slope)
+                 data_norm="l2sq", tv=(0.0, 1.0, 0.1, 1e-8), slope=0.2, record_every=1, model=None):
+        # model: a prebuilt network (e.g. oracle.refnet.OracleFastResUNet); else the config ResUNet
+        self.model = model if model is not None else build_oracle_net(channels, in_channels, slope)
         self.z = torch.tensor(np.asarray(z), dtype=torch.float32)
         self.J = torch.tensor(np.asarray(J), dtype=torch.float32)
         self.qcols = torch.tensor(np.asarray(qcols), dtype=torch.long)
@@ -135,9 +136,9 @@ class OracleFrameOptimizer:
 
 
 def oracle_loss_and_grads(channels, in_channels, z, J, qcols, dv, theta_flat, output_map,
-                          data_norm="l2sq", history=(), tv=(0.0, 1.0, 0.1, 1e-8)):
+                          data_norm="l2sq", history=(), tv=(0.0, 1.0, 0.1, 1e-8), model=None):
     opt = OracleFrameOptimizer(channels, in_channels, z, J, qcols, output_map, 1e-3,
-                               data_norm=data_norm, tv=tv)
+                               data_norm=data_norm, tv=tv, model=model)
     opt.load(theta_flat)
     return opt.grads(dv, history)
 
@@ -145,10 +146,10 @@ def oracle_loss_and_grads(channels, in_channels, z, J, qcols, dv, theta_flat, ou
 def oracle_reconstruct_sequence(channels, in_channels, z, J, qcols, frames_dv, theta0_flat,
                                 output_map, iters_warm, iters_first, iters_next, lr,
                                 data_norm="l2sq", tv=(0.0, 1.0, 0.1, 1e-8), warm_frame=1,
-                                disable_upws=False, disable_tpp=False):
+                                disable_upws=False, disable_tpp=False, model=None):
     """pipeline.py:444-560 (UPWS -> frame 1 -> TPP chain); returns a dict."""
     runner = OracleFrameOptimizer(channels, in_channels, z, J, qcols, output_map, lr,
-                                  data_norm=data_norm, tv=tv)
+                                  data_norm=data_norm, tv=tv, model=model)
     theta0 = torch.as_tensor(theta0_flat, dtype=torch.float32).clone()
     chain = [("kaiming_init", 0)]
     traces = {}

@@ -14,7 +14,9 @@ from pathlib import Path
 from .errors import NativeLibraryError
 
 LIB_PATH = Path(__file__).resolve().parent / "_d2ip_b200.so"
-ABI_VERSION = 2
+ABI_VERSION = 3
+ARCH_CONFIG_RESUNET = 0  # D2IP_ARCH_* (include/d2ip_b200.h)
+ARCH_FAST_RESUNET = 1
 
 PREC = {"fp32": 0, "tf32": 1, "bf16": 2}
 NORM = {"l2sq": 0, "l2": 1}
@@ -65,6 +67,10 @@ class NetDesc(C.Structure):
         ("tv_eps", C.c_float),
         ("max_history", C.c_int),
         ("max_iters", C.c_int),
+        ("arch", C.c_int),
+        ("depthwise", C.c_int),
+        ("n_dil", C.c_int),
+        ("dil", C.c_int * 8),
     ]
 
 

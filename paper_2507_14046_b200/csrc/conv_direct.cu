@@ -30,7 +30,7 @@ template <int KS, int CG>
 __global__ void __launch_bounds__(128) conv_fwd_direct_k(d2ip_act x, const float* __restrict__ w,
                                                          const float* __restrict__ bias,
                                                          long long wbs, int stride, d2ip_act y,
-                                                         int accumulate, int vec) {
+                                                         int accumulate, int vec, int dil) {
   D2IP_PDL_ENTRY();
   constexpr int K3 = Taps<KS>::K3, PAD = Taps<KS>::PAD;
   extern __shared__ float sw[];  // [cin][K3][CG]
@@ -51,13 +51,13 @@ __global__ void __launch_bounds__(128) conv_fwd_direct_k(d2ip_act x, const float
   for (int j = 0; j < CG; ++j) acc[j] = bias ? __ldg(bias + b * wbs + co0 + j) : 0.f;
   const float* xb = x.ptr + b * x.bstride;
   for (int kd = 0; kd < KS; ++kd) {
-    const int id = od * stride + kd - PAD;
+    const int id = od * stride + (kd - PAD) * dil;
     if (id < 0 || id >= x.d) continue;
     for (int kh = 0; kh < KS; ++kh) {
-      const int ih = oh * stride + kh - PAD;
+      const int ih = oh * stride + (kh - PAD) * dil;
       if (ih < 0 || ih >= x.h) continue;
       for (int kw = 0; kw < KS; ++kw) {
-        const int iw = ow * stride + kw - PAD;
+        const int iw = ow * stride + (kw - PAD) * dil;
         if (iw < 0 || iw >= x.w) continue;
         const float* xp = xb + (((long long)id * x.h + ih) * x.w + iw) * x.cstride;
         const int tap = (kd * KS + kh) * KS + kw;
@@ -92,7 +92,7 @@ __global__ void __launch_bounds__(128) conv_fwd_direct_k(d2ip_act x, const float
 template <int KS, int CG>
 __global__ void __launch_bounds__(128) conv_dgrad_direct_k(d2ip_act gy, const float* __restrict__ w,
                                                            long long wbs, int stride, d2ip_act gx,
-                                                           int accumulate, int vec) {
+                                                           int accumulate, int vec, int dil) {
   D2IP_PDL_ENTRY();
   constexpr int K3 = Taps<KS>::K3, PAD = Taps<KS>::PAD;
   extern __shared__ float sw[];  // [cout][K3][CG]
@@ -113,17 +113,17 @@ __global__ void __launch_bounds__(128) conv_dgrad_direct_k(d2ip_act gy, const fl
 #pragma unroll
   for (int j = 0; j < CG; ++j) acc[j] = 0.f;
   for (int kd = 0; kd < KS; ++kd) {
-    const int td = id + PAD - kd;
+    const int td = id + (PAD - kd) * dil;
     if (td < 0 || td % stride) continue;
     const int od = td / stride;
     if (od >= gy.d) continue;
     for (int kh = 0; kh < KS; ++kh) {
-      const int th = ih + PAD - kh;
+      const int th = ih + (PAD - kh) * dil;
       if (th < 0 || th % stride) continue;
       const int oh = th / stride;
       if (oh >= gy.h) continue;
       for (int kw = 0; kw < KS; ++kw) {
-        const int tw = iw + PAD - kw;
+        const int tw = iw + (PAD - kw) * dil;
         if (tw < 0 || tw % stride) continue;
         const int ow = tw / stride;
         if (ow >= gy.w) continue;
@@ -200,7 +200,8 @@ __global__ void __launch_bounds__(256) conv_wgrad_partial_k(d2ip_act x, d2ip_act
 // per 4*COG FMAs. Output layout matches conv_wgrad_partial_k (OIDHW + bias).
 template <int KS, int COG>
 __global__ void __launch_bounds__(128) conv_wgrad_tiled_k(d2ip_act x, d2ip_act gy, int stride,
-                                                          float* __restrict__ partial, int nchunks, int chunk) {
+                                                          float* __restrict__ partial, int nchunks, int chunk,
+                                                          int dil) {
   D2IP_PDL_ENTRY();
   constexpr int K3 = Taps<KS>::K3, PAD = Taps<KS>::PAD;
   const int b = blockIdx.z, c = blockIdx.y;
@@ -241,7 +242,8 @@ __global__ void __launch_bounds__(128) conv_wgrad_tiled_k(d2ip_act x, d2ip_act g
   const float* xb = x.ptr + b * x.bstride + ci0;
   int ow = (int)(v0 % gy.w), oh = (int)((v0 / gy.w) % gy.h), od = (int)(v0 / ((long long)gy.w * gy.h));
   for (long long v = v0; v < v1; ++v) {
-    const int id = od * stride + kd - PAD, ih = oh * stride + kh - PAD, iw = ow * stride + kw - PAD;
+    const int id = od * stride + (kd - PAD) * dil, ih = oh * stride + (kh - PAD) * dil,
+              iw = ow * stride + (kw - PAD) * dil;
     if (id >= 0 && id < x.d && ih >= 0 && ih < x.h && iw >= 0 && iw < x.w) {
       const float4 xv = __ldg(reinterpret_cast<const float4*>(xb + (((long long)id * x.h + ih) * x.w + iw) * x.cstride));
       float g[COG];
@@ -376,7 +378,7 @@ static int smem_opt_in(K kernel, size_t bytes) {
 static bool vec_ok(const d2ip_act& a) { return a.c % 4 == 0 && a.cstride % 4 == 0 && ((uintptr_t)a.ptr & 15) == 0; }
 
 int conv_fwd_direct(d2ip_act x, const float* w, const float* bias, long long wbs, int ks, int stride,
-                    d2ip_act y, int accumulate, int batch, cudaStream_t st) {
+                    d2ip_act y, int accumulate, int batch, cudaStream_t st, int dil) {
   const long long V = (long long)y.d * y.h * y.w;
   const int vec = vec_ok(x) ? 1 : 0;
 #define LAUNCH_F(KS_, CG_)                                                                          \
@@ -385,7 +387,7 @@ int conv_fwd_direct(d2ip_act x, const float* w, const float* bias, long long wbs
     D2IP_CHECK_ARG(sm <= 200 * 1024, "conv3d_fwd: weight slice too large for shared memory");      \
     D2IP_RET(smem_opt_in(conv_fwd_direct_k<KS_, CG_>, sm));                                        \
     dim3 grid(cdiv(V, thr), y.c / CG_, batch);                                                      \
-    D2IP_CUDA(launch_pdl((conv_fwd_direct_k<KS_, CG_>), grid, thr, sm, st, x, w, bias, wbs, stride, y, accumulate, vec)); \
+    D2IP_CUDA(launch_pdl((conv_fwd_direct_k<KS_, CG_>), grid, thr, sm, st, x, w, bias, wbs, stride, y, accumulate, vec, dil)); \
   } while (0)
   // small layers: narrower channel groups and 64-thread blocks to fill the SMs
   const bool small = V * (y.c / 8 + 1) * batch < 296LL * 128;
@@ -403,7 +405,7 @@ int conv_fwd_direct(d2ip_act x, const float* w, const float* bias, long long wbs
 }
 
 int conv_dgrad_direct(d2ip_act gy, const float* w, long long wbs, int ks, int stride, d2ip_act gx,
-                      int accumulate, int batch, cudaStream_t st) {
+                      int accumulate, int batch, cudaStream_t st, int dil) {
   const long long V = (long long)gx.d * gx.h * gx.w;
   const int vec = vec_ok(gy) ? 1 : 0;
 #define LAUNCH_D(KS_, CG_)                                                                        \
@@ -412,7 +414,7 @@ int conv_dgrad_direct(d2ip_act gy, const float* w, long long wbs, int ks, int st
     D2IP_CHECK_ARG(sm <= 200 * 1024, "conv3d_dgrad: weight slice too large for shared memory");  \
     D2IP_RET(smem_opt_in(conv_dgrad_direct_k<KS_, CG_>, sm));                                    \
     dim3 grid(cdiv(V, thr), gx.c / CG_, batch);                                                   \
-    D2IP_CUDA(launch_pdl((conv_dgrad_direct_k<KS_, CG_>), grid, thr, sm, st, gy, w, wbs, stride, gx, accumulate, vec)); \
+    D2IP_CUDA(launch_pdl((conv_dgrad_direct_k<KS_, CG_>), grid, thr, sm, st, gy, w, wbs, stride, gx, accumulate, vec, dil)); \
   } while (0)
   const bool small = V * (gx.c / 8 + 1) * batch < 296LL * 128;
   const int cg = (gx.c % 8 == 0 && !small) ? 8 : (gx.c % 4 == 0 ? 4 : 1);
@@ -481,7 +483,7 @@ static void tiled_split(int cin, int cout, int ks, int cog, long long V, int bat
 }
 
 int conv_wgrad_direct(d2ip_act x, d2ip_act gy, int ks, int stride, float* gw, long long gwbs,
-                      void* ws, size_t ws_bytes, int batch, cudaStream_t st) {
+                      void* ws, size_t ws_bytes, int batch, cudaStream_t st, int dil) {
   const int nE = gy.c * x.c * ks * ks * ks + gy.c;
   const long long V = (long long)gy.d * gy.h * gy.w;
   int nchunks, chunk;
@@ -494,7 +496,7 @@ int conv_wgrad_direct(d2ip_act x, d2ip_act gy, int ks, int stride, float* gw, lo
     float* partial = reinterpret_cast<float*>(ws);
     dim3 grid(cdiv(nthr, 128), nchunks, batch);
 #define LAUNCH_T(KS_, COG_) \
-  D2IP_CUDA(launch_pdl((conv_wgrad_tiled_k<KS_, COG_>), grid, 128, 0, st, x, gy, stride, partial, nchunks, chunk))
+  D2IP_CUDA(launch_pdl((conv_wgrad_tiled_k<KS_, COG_>), grid, 128, 0, st, x, gy, stride, partial, nchunks, chunk, dil))
     if (ks == 3) {
       if (cog == 8) LAUNCH_T(3, 8); else if (cog == 4) LAUNCH_T(3, 4); else LAUNCH_T(3, 1);
     } else {
@@ -507,6 +509,7 @@ int conv_wgrad_direct(d2ip_act x, d2ip_act gy, int ks, int stride, float* gw, lo
     D2IP_LAUNCH_CHECK();
     return D2IP_OK;
   }
+  D2IP_CHECK_ARG(dil == 1, "conv3d_wgrad: dilation needs channel counts that are multiples of 4");
   wgrad_split(nE, V, batch, &nchunks, &chunk);
   D2IP_CHECK_ARG(ws_bytes >= (size_t)batch * nchunks * nE * sizeof(float),
                  "conv3d_wgrad: workspace too small (%zu < %zu)", ws_bytes,

@@ -18,82 +18,9 @@
 #include "common.cuh"
 #include "kernels.h"
 
-namespace d2ip {
-
-struct ConvP {
-  long long ow = 0, ob = 0;
-  int cin = 0, cout = 0, ks = 3, stride = 1;
-  bool tcf = false, tcd = false;  // tcgen05 forward / data-gradient path
-  float* pkf = nullptr;           // packed weights [B][27][cin/4][Np][4] (forward)
-  float* pkd = nullptr;           // packed flipped W^T (data gradient)
-};
-struct NormP {
-  long long og = 0, ob = 0;
-  int c = 0;
-};
-struct Block {
-  ConvP c1, c2, sk;
-  NormP n1, n2;
-  int lin = 0, lout = 0;  // spatial level of input / output
-  d2ip_act x{}, out{}, gx{}, gout{};
-  int gx_acc = 0;
-  float *h1 = nullptr, *xh1 = nullptr, *rs1 = nullptr, *xh2 = nullptr, *rs2 = nullptr;
-};
-
-}  // namespace d2ip
-
-struct d2ip_engine {
-  d2ip_net_desc d{};
-  long long nparams = 0;
-  int L = 0;
-  int D[8]{}, H[8]{}, W[8]{};
-  long long V[8]{};
-  d2ip::ConvP stem, tail;
-  d2ip::NormP stem_n;
-  std::vector<d2ip::Block> enc, dec;
-  d2ip::Block neck;
-  d2ip_bindings b{};
-  bool bound = false;
-  // workspace carve-up
-  float* cat[8]{};
-  float* gcat[8]{};
-  int catw[8]{};
-  float *elast = nullptr, *gelast = nullptr, *bout = nullptr, *gbout = nullptr;
-  float* decout[8]{};
-  float* gdecout[8]{};
-  float *stem_xh = nullptr, *stem_rs = nullptr;
-  float *raw = nullptr, *raw2 = nullptr, *sc[5]{};
-  float *sigma_c = nullptr, *rs = nullptr, *jpart = nullptr, *adjpart = nullptr;
-  float *gtail = nullptr, *gmapped = nullptr, *regpart = nullptr;
-  void* wg_ws = nullptr;
-  size_t wg_ws_bytes = 0;
-  void* na_ws = nullptr;
-  float* tc_ws = nullptr;
-  size_t tc_ws_bytes = 0;
-  d2ip::PackJobs packjobs;
-  size_t na_ws_bytes = 0;
-  size_t ws_total = 0;
-  long long maxvc = 0;
-  int nseg = 0, rsplit = 0, n_reg = 0;
-  cudaGraph_t graph = nullptr;
-  cudaGraphExec_t gexec = nullptr;
-  cudaStream_t cap_stream = nullptr;
-  int launches = 0;
-};
+#include "engine_impl.h"
 
 namespace d2ip {
-
-static d2ip_act view(const d2ip_engine& E, float* p, int lvl, int c, int cs) {
-  d2ip_act a;
-  a.ptr = p;
-  a.d = E.D[lvl];
-  a.h = E.H[lvl];
-  a.w = E.W[lvl];
-  a.c = c;
-  a.cstride = cs;
-  a.bstride = E.V[lvl] * cs;
-  return a;
-}
 
 // Param offsets in the exact order of priornet.param_schema().
 static void plan_params(d2ip_engine& E) {
@@ -151,17 +78,10 @@ static void plan_params(d2ip_engine& E) {
   E.nparams = o;
 }
 
-// Assign workspace pointers (base may be null: size query). Returns bytes.
-static size_t plan_workspace(d2ip_engine& E, char* base) {
-  size_t off = 0;
+// Network buffers of the config ResUNet (base may be null: size query).
+static void config_plan_workspace(d2ip_engine& E, Arena& A) {
   const int B = E.d.batch;
-  auto take = [&](size_t bytes) -> char* {
-    off = (off + 255) & ~(size_t)255;
-    char* p = base ? base + off : nullptr;
-    off += bytes;
-    return p;
-  };
-  auto takef = [&](long long n) { return reinterpret_cast<float*>(take((size_t)n * sizeof(float))); };
+  auto takef = [&](long long n) { return A.f(n); };
   const int* c = E.d.channels;
   const int L = E.L;
   for (int l = 0; l + 1 < L; ++l) {
@@ -194,18 +114,6 @@ static size_t plan_workspace(d2ip_engine& E, char* base) {
   E.raw = takef(B * maxvc);
   E.raw2 = takef(B * maxvc);
   for (int i = 0; i < 5; ++i) E.sc[i] = takef(B * maxvc);
-  // data term
-  const int M = E.d.M, Vp = E.d.Vp;
-  E.nseg = jac_nseg(Vp);
-  E.rsplit = jac_adj_rows(M, Vp, B);
-  E.sigma_c = takef((long long)B * Vp);
-  E.rs = takef((long long)B * M);
-  E.jpart = takef((long long)B * M * E.nseg);
-  E.adjpart = reinterpret_cast<float*>(take(jac_adj_ws(M, Vp, B)));
-  E.gtail = takef((long long)B * E.V[0]);
-  E.gmapped = takef((long long)B * E.V[0]);
-  E.n_reg = tv_nblocks(E.V[0]);
-  E.regpart = takef((long long)B * E.n_reg);
   // reduction workspaces: max over layers
   size_t wg = 0, na = 0;
   auto conv_ws = [&](const ConvP& cv, int lout) {
@@ -230,8 +138,6 @@ static size_t plan_workspace(d2ip_engine& E, char* base) {
   for (auto& bl : E.dec) blk_ws(bl);
   E.wg_ws_bytes = wg;
   E.na_ws_bytes = na;
-  E.wg_ws = take(wg);
-  E.na_ws = take(na);
   // packed tcgen05 weight tiles, refreshed from theta at the start of every forward
   size_t tcws = 0;  // split-K partials of the tcgen05 convs (max over layers)
   auto packs = [&](ConvP& cv, bool need_dgrad, int lvl) {
@@ -254,8 +160,32 @@ static size_t plan_workspace(d2ip_engine& E, char* base) {
   packs(E.neck.c2, true, E.neck.lout);
   packs(E.neck.sk, true, E.neck.lout);
   E.tc_ws_bytes = tcws;
-  E.tc_ws = tcws ? reinterpret_cast<float*>(take(tcws)) : nullptr;
-  return (off + 255) & ~(size_t)255;
+}
+
+// Assign workspace pointers (base may be null: size query). Returns bytes.
+static size_t plan_workspace(d2ip_engine& E, char* base) {
+  Arena A{base};
+  const int B = E.d.batch;
+  if (E.d.arch == D2IP_ARCH_FAST_RESUNET)
+    refnet_plan_workspace(E, A);
+  else
+    config_plan_workspace(E, A);
+  // data term
+  const int M = E.d.M, Vp = E.d.Vp;
+  E.nseg = jac_nseg(Vp);
+  E.rsplit = jac_adj_rows(M, Vp, B);
+  E.sigma_c = A.f((long long)B * Vp);
+  E.rs = A.f((long long)B * M);
+  E.jpart = A.f((long long)B * M * E.nseg);
+  E.adjpart = reinterpret_cast<float*>(A.take(jac_adj_ws(M, Vp, B)));
+  E.gtail = A.f((long long)B * E.V[0]);
+  E.gmapped = A.f((long long)B * E.V[0]);
+  E.n_reg = tv_nblocks(E.V[0]);
+  E.regpart = A.f((long long)B * E.n_reg);
+  E.wg_ws = A.take(E.wg_ws_bytes);
+  E.na_ws = A.take(E.na_ws_bytes);
+  E.tc_ws = E.tc_ws_bytes ? reinterpret_cast<float*>(A.take(E.tc_ws_bytes)) : nullptr;
+  return A.total();
 }
 
 // Views of every block's input / output / gradients (after plan_workspace).
@@ -294,20 +224,11 @@ static void plan_views(d2ip_engine& E) {
 
 // ---------------------------------------------------------------------------
 
-struct Ctx {
-  d2ip_engine& E;
-  cudaStream_t st;
-  int B;
-  long long pbs;
-  int prec;
-  float slope;
-  float* th() const { return E.b.theta; }
-  float* gr() const { return E.b.grad; }
-};
+
 
 // Forward conv; with `sk`, a split-K tcgen05 result is left as partials for
 // the consuming LayerNorm kernel to reduce (one launch fewer per layer).
-static int cfwd(Ctx& k, const ConvP& c, d2ip_act x, d2ip_act y, int acc, SplitK* sk = nullptr) {
+int cfwd(Ctx& k, const ConvP& c, d2ip_act x, d2ip_act y, int acc, SplitK* sk) {
   if (c.tcf) {
     int kspl = 0;
     D2IP_RET(conv_tc_run(x, c.pkf, c.cin, c.cout, k.th() + c.ob, k.pbs, y, acc, k.E.tc_ws, k.E.tc_ws_bytes, k.B, k.st,
@@ -316,16 +237,18 @@ static int cfwd(Ctx& k, const ConvP& c, d2ip_act x, d2ip_act y, int acc, SplitK*
     return D2IP_OK;
   }
   if (sk) *sk = SplitK{};
-  return conv_fwd_direct(x, k.th() + c.ow, k.th() + c.ob, k.pbs, c.ks, c.stride, y, acc, k.B, k.st);
+  return conv_fwd_direct(x, k.th() + c.ow, k.th() + c.ob, k.pbs, c.ks, c.stride, y, acc, k.B, k.st, c.dil);
 }
 
-static int cdgrad(Ctx& k, const ConvP& c, d2ip_act gy, d2ip_act gx, int acc) {
+int cdgrad(Ctx& k, const ConvP& c, d2ip_act gy, d2ip_act gx, int acc) {
   if (c.tcd)
     return conv_tc_run(gy, c.pkd, c.cout, c.cin, nullptr, 0, gx, acc, k.E.tc_ws, k.E.tc_ws_bytes, k.B, k.st);
-  return conv_dgrad_direct(gy, k.th() + c.ow, k.pbs, c.ks, c.stride, gx, acc, k.B, k.st);
+  return conv_dgrad_direct(gy, k.th() + c.ow, k.pbs, c.ks, c.stride, gx, acc, k.B, k.st, c.dil);
 }
 
-static int cwgrad(Ctx& k, const ConvP& c, d2ip_act x, d2ip_act gy) {
+int cwgrad(Ctx& k, const ConvP& c, d2ip_act x, d2ip_act gy) {
+  if (c.dil != 1)
+    return conv_wgrad_direct(x, gy, c.ks, c.stride, k.gr() + c.ow, k.pbs, k.E.wg_ws, k.E.wg_ws_bytes, k.B, k.st, c.dil);
   return conv_wgrad(x, gy, c.ks, c.stride, k.gr() + c.ow, k.pbs, k.E.wg_ws, k.E.wg_ws_bytes, k.prec, k.B, k.st);
 }
 
@@ -338,6 +261,10 @@ static void build_pack_jobs(d2ip_engine& E) {
     if (c.tcf) pack_jobs_add(j, E.b.theta + c.ow, c.cin, c.cout, 0, c.pkf);
     if (c.tcd) pack_jobs_add(j, E.b.theta + c.ow, c.cout, c.cin, 1, c.pkd);
   };
+  if (E.d.arch == D2IP_ARCH_FAST_RESUNET) {
+    refnet_pack_jobs(E);
+    return;
+  }
   add(E.stem);
   add(E.tail);
   for (auto* v : {&E.enc, &E.dec})
@@ -392,6 +319,10 @@ static int block_bwd(Ctx& k, Block& bl) {
 
 static int forward(Ctx& k) {
   d2ip_engine& E = k.E;
+  if (E.d.arch == D2IP_ARCH_FAST_RESUNET) {
+    D2IP_RET(pack_all(k));
+    return refnet_forward(k);
+  }
   const int* c = E.d.channels;
   const int L = E.L;
   d2ip_act z = view(E, const_cast<float*>(E.b.z), 0, E.d.in_channels, E.d.in_channels);
@@ -449,6 +380,7 @@ static int backward(Ctx& k) {
     D2IP_RET(jac_adj_finish(E.adjpart, E.rsplit, E.d.Vp, E.d.V, E.b.vox_of_col, E.b.sig, scale, E.gtail, E.V[0],
                             0, k.B, k.st));
   }
+  if (E.d.arch == D2IP_ARCH_FAST_RESUNET) return refnet_backward(k);
   d2ip_act gt = view(E, E.gtail, 0, 1, 1);
   Block& last = E.dec.back();
   D2IP_RET(cwgrad(k, E.tail, last.out, gt));
@@ -588,6 +520,7 @@ int d2ip_engine_create(const d2ip_net_desc* desc, d2ip_engine** out) {
   const d2ip_net_desc& d = *desc;
   D2IP_CHECK_ARG(d.levels >= 2 && d.levels <= 8, "levels must be in [2, 8]");
   D2IP_CHECK_ARG(d.batch >= 1, "batch must be >= 1");
+  D2IP_CHECK_ARG(d.arch == D2IP_ARCH_CONFIG_RESUNET || d.arch == D2IP_ARCH_FAST_RESUNET, "unknown arch %d", d.arch);
   const int f = 1 << (d.levels - 1);
   D2IP_CHECK_ARG(d.R % f == 0 && d.C % f == 0 && d.P % f == 0, "grid (%d,%d,%d) not divisible by %d", d.R, d.C,
                  d.P, f);
@@ -604,7 +537,16 @@ int d2ip_engine_create(const d2ip_net_desc* desc, d2ip_engine** out) {
     E->W[l] = d.P >> l;
     E->V[l] = (long long)E->D[l] * E->H[l] * E->W[l];
   }
-  plan_params(*E);
+  if (d.arch == D2IP_ARCH_FAST_RESUNET) {
+    int rc = refnet_plan_params(*E);
+    if (rc != D2IP_OK) {
+      refnet_destroy(*E);
+      delete E;
+      return rc;
+    }
+  } else {
+    plan_params(*E);
+  }
   E->ws_total = plan_workspace(*E, nullptr);
   *out = E;
   return D2IP_OK;
@@ -613,6 +555,7 @@ int d2ip_engine_create(const d2ip_net_desc* desc, d2ip_engine** out) {
 void d2ip_engine_destroy(d2ip_engine* e) {
   if (!e) return;
   d2ip::drop_graph(*e);
+  d2ip::refnet_destroy(*e);
   if (e->cap_stream) cudaStreamDestroy(e->cap_stream);
   delete e;
 }
@@ -633,7 +576,10 @@ int d2ip_engine_bind(d2ip_engine* e, const d2ip_bindings* b) {
   drop_graph(*e);
   e->b = *b;
   plan_workspace(*e, reinterpret_cast<char*>(b->workspace));
-  plan_views(*e);
+  if (e->d.arch == D2IP_ARCH_FAST_RESUNET)
+    refnet_plan_views(*e);
+  else
+    plan_views(*e);
   build_pack_jobs(*e);
   D2IP_CHECK_ARG(e->packjobs.n <= PackJobs::kMax, "too many tcgen05 layers for one pack launch");
   // one-time zero: J padding columns of sigma_c, unmasked tail gradients

@@ -6,13 +6,37 @@
 namespace d2ip {
 
 // conv_direct.cu — exact fp32 CUDA-core convolutions
+// dil: dilation of 3^3 kernels (ASPP3d branches, priornet.py:156-158); padding = dil
 int conv_fwd_direct(d2ip_act x, const float* w, const float* bias, long long wbs, int ks, int stride,
-                    d2ip_act y, int accumulate, int batch, cudaStream_t st);
+                    d2ip_act y, int accumulate, int batch, cudaStream_t st, int dil = 1);
 int conv_dgrad_direct(d2ip_act gy, const float* w, long long wbs, int ks, int stride, d2ip_act gx,
-                      int accumulate, int batch, cudaStream_t st);
+                      int accumulate, int batch, cudaStream_t st, int dil = 1);
 size_t conv_wgrad_direct_ws(int cin, int cout, int ks, long long V, int batch);
 int conv_wgrad_direct(d2ip_act x, d2ip_act gy, int ks, int stride, float* gw, long long gwbs,
-                      void* ws, size_t ws_bytes, int batch, cudaStream_t st);
+                      void* ws, size_t ws_bytes, int batch, cudaStream_t st, int dil = 1);
+
+// refnet_kernels.cu — FastResUNet3D extras (priornet.py:111-180)
+int dw_conv_fwd(d2ip_act x, const float* w, const float* bias, long long wbs, int stride, d2ip_act y, int batch,
+                cudaStream_t st);
+int dw_conv_dgrad(d2ip_act gy, const float* w, long long wbs, int stride, d2ip_act gx, int accumulate, int batch,
+                  cudaStream_t st);
+size_t dw_wgrad_ws(int C, long long V, int batch);
+int dw_conv_wgrad(d2ip_act x, d2ip_act gy, int stride, float* gw, long long gwbs, void* ws, size_t ws_bytes,
+                  int batch, cudaStream_t st);
+size_t colsum_ws(int C, long long V, int batch);
+// SE state per sequence: [pooled C][z1 hid][gate C][gpool C]  (sbs >= 3C + hid)
+int se_forward(d2ip_act x, const float* w1, const float* b1, const float* w2, const float* b2, long long pbs, int hid,
+               float* state, int sbs, d2ip_act out, void* ws, size_t ws_bytes, int batch, cudaStream_t st);
+int se_backward(d2ip_act x, d2ip_act gs, const float* w1, const float* b1, const float* w2, long long pbs, int hid,
+                float* state, int sbs, float* g1, float* g2, d2ip_act gx, int accumulate, void* ws, size_t ws_bytes,
+                int batch, cudaStream_t st);
+int add_silu(d2ip_act k, d2ip_act q, float* pre, d2ip_act a, int batch, cudaStream_t st);
+int silu_bwd(d2ip_act ga, const float* pre, d2ip_act gpre, int batch, cudaStream_t st);
+int sigmoid_inplace(float* t, long long n, cudaStream_t st);
+int sigmoid_bwd(float* g, const float* s, long long n, cudaStream_t st);
+int att_gate_fwd(d2ip_act s, const float* att, d2ip_act out, int batch, cudaStream_t st);
+int att_gate_bwd(d2ip_act gg, d2ip_act s, const float* att, d2ip_act gs, int accumulate, float* gatt, int batch,
+                 cudaStream_t st);
 int reduce_chunks(const float* partial, int nchunks, int n, float* out, long long obs, int batch,
                   cudaStream_t st);
 
@@ -60,9 +84,11 @@ int conv_wgrad(d2ip_act x, d2ip_act gy, int ks, int stride, float* gw, long long
                size_t ws_bytes, int precision, int batch, cudaStream_t st);
 
 // elem.cu — normalisation / activation / resampling / output map
+// act: 0 none, 1 LeakyReLU(slope), 2 SiLU (then `pre` receives the
+// pre-activation, which norm_act_bwd takes as its `out` view for act 2)
 int norm_act_fwd(d2ip_act y, const float* gamma, const float* beta, long long pbs, d2ip_act res,
                  int act, float slope, d2ip_act out, float* xhat, float* rstd, int batch,
-                 cudaStream_t st, SplitK sk = SplitK{});
+                 cudaStream_t st, SplitK sk = SplitK{}, d2ip_act pre = d2ip_act{});
 size_t norm_act_bwd_ws(long long V, int C, int batch);
 int norm_act_bwd(d2ip_act gout, d2ip_act out, int act, float slope, const float* xhat,
                  const float* rstd, const float* gamma, long long pbs, d2ip_act gpre, d2ip_act gc,

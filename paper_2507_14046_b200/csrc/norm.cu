@@ -57,7 +57,7 @@ __global__ void __launch_bounds__(kNormThreads) norm_act_fwd_k(d2ip_act y, const
                                                                const float* __restrict__ beta, long long pbs,
                                                                d2ip_act res, int act, float slope, d2ip_act out,
                                                                float* __restrict__ xhat, float* __restrict__ rstd,
-                                                               int G, SplitK sk) {
+                                                               int G, SplitK sk, d2ip_act pre) {
   D2IP_PDL_ENTRY();
   const int b = blockIdx.y;
   const int C = y.c, L = C / VPL;
@@ -112,11 +112,14 @@ __global__ void __launch_bounds__(kNormThreads) norm_act_fwd_k(d2ip_act y, const
       for (int i = 0; i < VPL; ++i) xh[i] = (x[i] - mean) * rs;
       if (res.ptr) ld<VPL>(res.ptr + b * res.bstride + v * res.cstride + c0, r);
 #pragma unroll
+      float pr[VPL];
       for (int i = 0; i < VPL; ++i) {
         float t = fmaf(xh[i], gm[i], bt[i]);
         if (res.ptr) t += r[i];
-        o[i] = act ? lrelu(t, slope) : t;
+        pr[i] = t;
+        o[i] = act == 1 ? lrelu(t, slope) : (act == 2 ? t / (1.0f + expf(-t)) : t);
       }
+      if (pre.ptr) st<VPL>(pre.ptr + b * pre.bstride + v * pre.cstride + c0, pr);
       st<VPL>(xhat + ((long long)b * V + v) * C + c0, xh);
       st<VPL>(out.ptr + b * out.bstride + v * out.cstride + c0, o);
       if (li == 0) rstd[b * V + v] = rs;
@@ -132,7 +135,8 @@ static int norm_blocks(long long V, int G, int batch) {
 }
 
 int norm_act_fwd(d2ip_act y, const float* gamma, const float* beta, long long pbs, d2ip_act res, int act,
-                 float slope, d2ip_act out, float* xhat, float* rstd, int batch, cudaStream_t st, SplitK sk) {
+                 float slope, d2ip_act out, float* xhat, float* rstd, int batch, cudaStream_t st, SplitK sk,
+                 d2ip_act pre) {
   const int C = y.c;
   D2IP_CHECK_ARG(C % 4 == 0 && C <= 256, "norm_act: C=%d must be a multiple of 4, <= 256", C);
   D2IP_CHECK_ARG(y.cstride % 4 == 0 && out.cstride % 4 == 0 && (!res.ptr || res.cstride % 4 == 0),
@@ -143,10 +147,10 @@ int norm_act_fwd(d2ip_act y, const float* gamma, const float* beta, long long pb
   dim3 grid(norm_blocks(V, g.G, batch), batch);
   if (g.vpl == 4)
     D2IP_CUDA(launch_pdl(norm_act_fwd_k<4>, grid, kNormThreads, 0, st, y, gamma, beta, pbs, res, act, slope, out,
-                         xhat, rstd, g.G, sk));
+                         xhat, rstd, g.G, sk, pre));
   else
     D2IP_CUDA(launch_pdl(norm_act_fwd_k<8>, grid, kNormThreads, 0, st, y, gamma, beta, pbs, res, act, slope, out,
-                         xhat, rstd, g.G, sk));
+                         xhat, rstd, g.G, sk, pre));
   D2IP_LAUNCH_CHECK();
   return D2IP_OK;
 }
@@ -188,7 +192,14 @@ __global__ void __launch_bounds__(kNormThreads) norm_act_bwd_k(d2ip_act gout, d2
         float o[VPL];
         ld<VPL>(out.ptr + b * out.bstride + v * out.cstride + c0, o);
 #pragma unroll
-        for (int i = 0; i < VPL; ++i) g[i] = o[i] > 0.f ? g[i] : g[i] * slope;
+        for (int i = 0; i < VPL; ++i) {
+          if (act == 1) {
+            g[i] = o[i] > 0.f ? g[i] : g[i] * slope;
+          } else {  // SiLU': `out` holds the pre-activation
+            const float s = 1.0f / (1.0f + expf(-o[i]));
+            g[i] *= s * (1.0f + o[i] * (1.0f - s));
+          }
+        }
       }
     }
     float s1 = 0.f, s2 = 0.f;

@@ -28,7 +28,7 @@ from . import _native as N
 from .errors import NativeLibraryError
 from .forward import as_masked
 from .geometry import vectorize
-from .priornet import ResUNetConfig, param_schema, state_from_flat
+from .priornet import NetworkConfig, ResUNetConfig, param_schema, state_from_flat
 
 TICK_S = 1.024e-6  # trace timestamp unit (globaltimer >> 10)
 
@@ -84,16 +84,34 @@ def upload_masked_J(values: np.ndarray, perm: np.ndarray, vp: int) -> torch.Tens
     return out
 
 
+def net_fields(cfg) -> dict:
+    """Engine description of a network config (d2ip_net_desc's network fields).
+
+    NetworkConfig -> the reference's FastResUNet3D (priornet.py:183-232):
+    channels b, 2b, 4b, 8b over 4 levels, 1-channel noise, SiLU.
+    ResUNetConfig -> the canonical config ResUNet of SURVEY §7.1."""
+    if isinstance(cfg, NetworkConfig):
+        b = cfg.base_channels
+        if b % 4 or 8 * b > 256:
+            raise ValueError(f"the engine runs FastResUNet3D with base_channels a multiple of 4 in [4, 32], got {b}")
+        if len(cfg.aspp_dilations) > 8:
+            raise ValueError("at most 8 ASPP dilations")
+        return dict(arch=N.ARCH_FAST_RESUNET, channels=(b, 2 * b, 4 * b, 8 * b), in_channels=1, negative_slope=0.0,
+                    depthwise=1 if cfg.use_depthwise else 0, dilations=tuple(cfg.aspp_dilations))
+    return dict(arch=N.ARCH_CONFIG_RESUNET, channels=tuple(cfg.channels), in_channels=cfg.in_channels,
+                negative_slope=cfg.negative_slope, depthwise=0, dilations=())
+
+
 class DeviceNet:
     """One bound engine: `batch` sequences of one network config in lockstep."""
 
-    def __init__(self, cfg: ResUNetConfig, grid_shape, M: int, mask: np.ndarray, *, batch: int = 1,
+    def __init__(self, cfg, grid_shape, M: int, mask: np.ndarray, *, batch: int = 1,
                  n_rhs: int = 1, j_shared: bool = True, data_norm: str = "l2sq", output_map=(-0.135, 0.0),
                  lr: float = 1e-3, betas=(0.9, 0.999), eps: float = 1e-8, precision: str = "fp32",
                  tv=(0.0, 1.0, 0.1, 1e-8), max_history: int = 0, max_iters: int = 4096):
         require_cuda()
-        if not isinstance(cfg, ResUNetConfig):
-            param_schema(cfg)  # raises NotImplementedError for the reference FastResUNet3D
+        if not isinstance(cfg, (ResUNetConfig, NetworkConfig)):
+            raise TypeError(f"unknown network config {type(cfg).__name__}")
         if precision not in N.PREC:
             raise ValueError(f"precision must be one of {sorted(N.PREC)}")
         if data_norm not in N.NORM:
@@ -113,12 +131,19 @@ class DeviceNet:
         self.tv = tuple(float(x) for x in tv)
         d = N.NetDesc()
         d.batch, d.R, d.C, d.P = batch, self.R, self.C, self.P
-        ch = cfg.channels
+        arch = net_fields(cfg)
+        ch = arch["channels"]
         d.levels = len(ch)
         for i, c in enumerate(ch):
             d.channels[i] = c
-        d.in_channels = cfg.in_channels
-        d.negative_slope = cfg.negative_slope
+        d.in_channels = arch["in_channels"]
+        d.negative_slope = arch["negative_slope"]
+        d.arch = arch["arch"]
+        d.depthwise = arch["depthwise"]
+        d.n_dil = len(arch["dilations"])
+        for i, x in enumerate(arch["dilations"]):
+            d.dil[i] = x
+        self.in_channels = arch["in_channels"]
         d.M, d.V, d.Vp, d.n_rhs = self.M, self.V, self.Vp, n_rhs
         d.j_shared = 1 if j_shared else 0
         d.data_norm = N.NORM[data_norm]
@@ -144,7 +169,7 @@ class DeviceNet:
         self.grad = torch.zeros((B, self.n_params), **f32)
         self.adam_m = torch.zeros((B, self.n_params), **f32)
         self.adam_v = torch.zeros((B, self.n_params), **f32)
-        self.z = torch.zeros((B, self.R, self.C, self.P, cfg.in_channels), **f32)
+        self.z = torch.zeros((B, self.R, self.C, self.P, self.in_channels), **f32)
         self.J = None
         self.vox_of_col = torch.from_numpy(self.colmap.vox_of_col).cuda()
         self.col_of_vox = torch.from_numpy(self.colmap.col_of_vox).cuda()
@@ -224,8 +249,8 @@ class DeviceNet:
     # -- inputs ---------------------------------------------------------------
     def set_noise(self, values, b: int | None = None) -> None:
         zt = noise_to_device(values)
-        if zt.shape[-1] != self.cfg.in_channels:
-            raise ValueError(f"noise has {zt.shape[-1]} channels, network expects {self.cfg.in_channels}")
+        if zt.shape[-1] != self.in_channels:
+            raise ValueError(f"noise has {zt.shape[-1]} channels, network expects {self.in_channels}")
         if b is None:
             self.z.copy_(zt.expand_as(self.z))
         else:

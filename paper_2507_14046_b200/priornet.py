@@ -188,14 +188,55 @@ def _resconv(prefix, cin, cout):
     )
 
 
+def _conv3(prefix, cin, cout, depthwise):
+    # `_conv3` (priornet.py:111-117): depthwise 3^3 (groups=cin) + pointwise 1^3, or dense 3^3
+    if depthwise:
+        return _conv(f"{prefix}.0", 1, cin, 3) + _conv(f"{prefix}.1", cin, cout, 1)
+    return _conv(prefix, cin, cout, 3)
+
+
+def _resconv_ref(prefix, cin, cout, depthwise):
+    # ResConv3d (priornet.py:134-148)
+    return (
+        _conv3(f"{prefix}.conv1", cin, cout, depthwise)
+        + _norm(f"{prefix}.norm1", cout)
+        + _conv3(f"{prefix}.conv2", cout, cout, depthwise)
+        + _norm(f"{prefix}.norm2", cout)
+        + _conv(f"{prefix}.skip", cin, cout, 1)
+    )
+
+
+def fast_resunet_schema(cfg: NetworkConfig) -> list[ParamEntry]:
+    """State-dict order of FastResUNet3D (priornet.py:183-215)."""
+    b = cfg.base_channels
+    ch = [b, 2 * b, 4 * b, 8 * b]
+    dw = cfg.use_depthwise
+    out = _conv("stem.0", 1, b, 3) + _norm("stem.1", b)
+    for i in range(3):  # SqueezeExcite (priornet.py:120-131)
+        hid = max(ch[i] // 4, 1)
+        out += _conv(f"enc_se.{i}.fc1", ch[i], hid, 1) + _conv(f"enc_se.{i}.fc2", hid, ch[i], 1)
+    for i in range(3):
+        out += _resconv_ref(f"enc_block.{i}", ch[i], ch[i + 1], dw)
+    for j, _d in enumerate(cfg.aspp_dilations):  # ASPP3d (priornet.py:151-164)
+        out += _conv(f"bottleneck.branches.{j}", ch[3], ch[3], 3)
+    out += _conv("bottleneck.project", ch[3] * len(cfg.aspp_dilations), ch[3], 1) + _norm("bottleneck.norm", ch[3])
+    for j, i in enumerate(reversed(range(3))):  # AttentionGate3d (priornet.py:167-180)
+        inter = max(ch[i] // 2, 4)
+        out += (_conv(f"dec_att.{j}.key", ch[i], inter, 1) + _conv(f"dec_att.{j}.query", ch[i + 1], inter, 1)
+                + _conv(f"dec_att.{j}.score", inter, 1, 1))
+    for j, i in enumerate(reversed(range(3))):
+        out += _resconv_ref(f"dec_block.{j}", ch[i + 1] + ch[i], ch[i], dw)
+    out += _conv("tail", b, 1, 3)
+    return out
+
+
 def param_schema(cfg) -> list[ParamEntry]:
     """State-dict order of the network (module registration order,
-    `priornet.py:199-215` minus SE/ASPP/attention)."""
+    `priornet.py:199-215`; the config ResUNet drops SE/ASPP/attention)."""
+    if isinstance(cfg, NetworkConfig):
+        return fast_resunet_schema(cfg)
     if not isinstance(cfg, ResUNetConfig):
-        raise NotImplementedError(
-            "FastResUNet3D (SE/ASPP/attention/depthwise, priornet.py:183-232) is a "
-            "SURVEY §8(f) next item; use ResUNetConfig"
-        )
+        raise TypeError(f"unknown network config {type(cfg).__name__}")
     c = cfg.channels
     L = len(c)
     out = _conv("stem.0", cfg.in_channels, c[0], 3) + _norm("stem.1", c[0])

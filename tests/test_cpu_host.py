@@ -162,7 +162,16 @@ def test_trace_and_timing_csv(tmp_path):
     assert [r[0] for r in rows] == ["warm", "frame_1", "frame_2"] and rows[-1][2] == pytest.approx(2.25)
 
 
-def test_reference_network_raises_not_implemented():
+def test_reference_network_engine_fields():
+    """NetworkConfig maps onto the engine's FastResUNet3D program (ABI 3 desc fields)."""
     from paper_2507_14046_b200 import NetworkConfig
-    with pytest.raises(NotImplementedError):
-        param_schema(NetworkConfig())
+    from paper_2507_14046_b200 import _native as N
+    from paper_2507_14046_b200.engine import net_fields
+    f = net_fields(NetworkConfig(base_channels=8, use_depthwise=False, aspp_dilations=(1, 3)))
+    assert f["arch"] == N.ARCH_FAST_RESUNET and f["channels"] == (8, 16, 32, 64)
+    assert f["in_channels"] == 1 and f["depthwise"] == 0 and f["dilations"] == (1, 3)
+    with pytest.raises(ValueError):
+        net_fields(NetworkConfig(base_channels=6))  # channels must stay multiples of 4
+    assert param_schema(NetworkConfig())[0].name == "stem.0.weight"
+    names = [n for n, _ in N.NetDesc._fields_]
+    assert names[-4:] == ["arch", "depthwise", "n_dil", "dil"]

@@ -1,0 +1,184 @@
+"""The engine's FastResUNet3D program (csrc/refnet.cu) against the REAL
+reference backbone (tests/golden/refnet.npz, unpatched d2ip package) and the
+CPU oracle (oracle/refnet.py). Same bars as the config ResUNet: single-step
+loss and parameter gradients within relative error 1e-4 (fp32) / 1e-3 (tf32),
+every parameter tensor within 10x that."""
+
+import numpy as np
+import pytest
+import torch
+
+from conftest import GOLDEN
+from oracle import OracleFrameOptimizer, build_oracle_refnet
+from paper_2507_14046_b200 import RunConfig, TVWeights, reconstruct_sequence
+from paper_2507_14046_b200 import workloads as W
+from paper_2507_14046_b200.engine import DeviceNet
+from paper_2507_14046_b200.priornet import NetworkConfig, kaiming_flat, param_schema, sample_noise_input
+
+pytestmark = pytest.mark.gpu
+
+GRAD_TOL = {"fp32": 1e-4, "tf32": 1e-3}
+VARIANTS = {"dw4": dict(base_channels=4, use_depthwise=True, seed=1),
+            "dense4": dict(base_channels=4, use_depthwise=False, seed=1),
+            "dw8": dict(seed=1)}
+
+
+def rel(a, b):
+    a, b = np.asarray(a, np.float64), np.asarray(b, np.float64)
+    return float(np.linalg.norm(a - b) / max(np.linalg.norm(b), 1e-30))
+
+
+@pytest.fixture(scope="module")
+def gold():
+    g = np.load(GOLDEN / "refnet.npz")
+    wl = W.make_workload(W.small_spec(), seed=0)
+    return g, wl
+
+
+def _net(g, wl, tag, prec, mode="l2sq", tv=(0.0, 1.0, 0.1, 1e-8), max_history=0, max_iters=64, batch=1):
+    cfg = NetworkConfig(**VARIANTS[tag])
+    dn = DeviceNet(cfg, wl.grid.shape, wl.matrix.n_measurements, wl.matrix.mask, data_norm=mode,
+                   output_map=tuple(g["output_map"]), precision=prec, tv=tv, max_history=max_history,
+                   max_iters=max_iters, batch=batch)
+    dn.set_noise(sample_noise_input(wl.grid, 0).values)
+    dn.set_J_host(wl.matrix.values)
+    dn.set_theta(kaiming_flat(cfg))
+    dn.set_dv(g["dv"])
+    return dn, cfg
+
+
+def _per_tensor(cfg, got, ref, tol):
+    o, bad = 0, []
+    for e in param_schema(cfg):
+        r = ref[o:o + e.numel]
+        if np.linalg.norm(r) > 1e-6 * np.linalg.norm(ref):
+            err = rel(got[o:o + e.numel], r)
+            if err > 10 * tol:
+                bad.append((e.name, err))
+        o += e.numel
+    return bad
+
+
+@pytest.mark.parametrize("prec", ["fp32", "tf32"])
+@pytest.mark.parametrize("tag,mode", [("dw4", "l2sq"), ("dw4", "l2"), ("dense4", "l2sq"), ("dense4", "l2"),
+                                      ("dw8", "l2sq")])
+def test_refnet_step_grads_vs_reference(gold, tag, mode, prec):
+    g, wl = gold
+    dn, cfg = _net(g, wl, tag, prec, mode)
+    assert dn.n_params == g[f"{tag}_l2sq_grads"].size
+    dn.reset_frame()
+    dn.grads()
+    torch.cuda.synchronize()
+    assert float(dn.trace_host(0, 1)[0, 0]) == pytest.approx(float(g[f"{tag}_{mode}_data"]), rel=GRAD_TOL[prec])
+    gd = dn.grad[0].cpu().numpy()
+    ref = g[f"{tag}_{mode}_grads"]
+    assert rel(gd, ref) < GRAD_TOL[prec]
+    bad = _per_tensor(cfg, gd, ref, GRAD_TOL[prec])
+    assert not bad, bad
+
+
+@pytest.mark.parametrize("tag", ["dw4", "dense4"])
+def test_refnet_tv_step_vs_reference(gold, tag):
+    g, wl = gold
+    dn, _ = _net(g, wl, tag, "fp32", "l2", tv=(0.002, 1.0, 0.1, 1e-8), max_history=2)
+    dn.set_history(list(g["tv_history"]))
+    dn.reset_frame()
+    dn.grads()
+    torch.cuda.synchronize()
+    t = dn.trace_host(0, 1)[0]
+    assert float(t[1]) == pytest.approx(float(g[f"{tag}_tv_reg"]), rel=1e-4)
+    assert float(t[2]) == pytest.approx(float(g[f"{tag}_tv_total"]), rel=1e-4)
+    assert rel(dn.grad[0].cpu().numpy(), g[f"{tag}_tv_grads"]) < 1e-4
+
+
+@pytest.mark.parametrize("tag", ["dw4", "dense4"])
+@pytest.mark.parametrize("k", [1, 10])
+def test_refnet_adam_trajectory_vs_reference(gold, tag, k):
+    g, wl = gold
+    dn, _ = _net(g, wl, tag, "fp32")
+    dn.reset_frame()
+    dn.run(k)
+    torch.cuda.synchronize()
+    assert int(dn.status_host()[0, 0]) == k
+    assert rel(dn.theta[0].cpu().numpy(), g[f"{tag}_theta{k}"]) < 1e-4
+    np.testing.assert_allclose(dn.trace_host(0, k)[:, 0], g[f"{tag}_trace{k}"][:, 1], rtol=1e-3)
+
+
+def test_refnet_graph_replay_equals_eager(gold):
+    g, wl = gold
+    a, _ = _net(g, wl, "dw4", "tf32")
+    b, _ = _net(g, wl, "dw4", "tf32")
+    a.reset_frame(); a.run(4, graph=True)
+    b.reset_frame(); b.run(4, graph=False)
+    torch.cuda.synchronize()
+    assert torch.equal(a.theta, b.theta)  # deterministic kernels: bitwise
+
+
+def test_refnet_batched_equals_single(gold):
+    """B sequences in lockstep (own theta / Z) equal B separate engines. The
+    split-K / chunk plans depend on the batch, so agreement is to fp32
+    summation order, not bitwise."""
+    g, wl = gold
+    singles = []
+    for s in range(2):
+        dn, cfg = _net(g, wl, "dw4", "tf32")
+        dn.set_noise(sample_noise_input(wl.grid, s).values)
+        dn.set_theta(kaiming_flat(cfg, seed=s + 5))
+        dn.reset_frame(); dn.grads()
+        singles.append(dn)
+    bn, cfg = _net(g, wl, "dw4", "tf32", batch=2)
+    for s in range(2):
+        bn.set_noise(sample_noise_input(wl.grid, s).values, b=s)
+        bn.set_theta(kaiming_flat(cfg, seed=s + 5), b=s)
+    bn.reset_frame(); bn.grads()
+    torch.cuda.synchronize()
+    for s in range(2):
+        assert rel(bn.grad[s].cpu().numpy(), singles[s].grad[0].cpu().numpy()) < 1e-5
+        assert bn.trace_host(s, 1)[0, 0] == pytest.approx(singles[s].trace_host(0, 1)[0, 0], rel=1e-6)
+
+
+@pytest.mark.parametrize("prec", ["fp32", "tf32"])
+def test_refnet_default_config_cfg1_grid_vs_oracle(prec):
+    """The reference default NetworkConfig (b=8, depthwise, dilations 1,2,4) on the
+    cfg1 32^3 grid, against the CPU oracle, per tensor."""
+    spec = W.CONFIGS["cfg1"]
+    wl = W.make_workload(spec, seed=0, frames=1)
+    cfg = NetworkConfig(seed=3)
+    z = sample_noise_input(wl.grid, 2).values
+    theta = kaiming_flat(cfg)
+    dv = wl.voltages.frames[0].values
+    dn = DeviceNet(cfg, wl.grid.shape, wl.matrix.n_measurements, wl.matrix.mask, output_map=wl.output_map,
+                   precision=prec, max_iters=4)
+    dn.set_noise(z)
+    dn.set_J_host(wl.matrix.values)
+    dn.set_theta(theta)
+    dn.set_dv(dv)
+    dn.reset_frame()
+    dn.grads()
+    torch.cuda.synchronize()
+    r = OracleFrameOptimizer(None, 1, z, wl.matrix.values, wl.matrix.columns_q(), wl.output_map, 1e-3,
+                             model=build_oracle_refnet(8, True, (1, 2, 4)))
+    r.load(theta)
+    _, data_ref, _, g_ref, _ = r.grads(dv)
+    assert float(dn.trace_host(0, 1)[0, 0]) == pytest.approx(data_ref, rel=GRAD_TOL[prec])
+    flat_ref = torch.cat([v.reshape(-1) for v in g_ref.values()]).numpy()
+    gd = dn.grad[0].cpu().numpy()
+    assert rel(gd, flat_ref) < GRAD_TOL[prec]
+    bad = _per_tensor(cfg, gd, flat_ref, GRAD_TOL[prec])
+    assert not bad, bad
+
+
+def test_refnet_sequence_driver_vs_reference(gold):
+    """The whole reference driver with its default backbone family (base 4)."""
+    g, wl = gold
+    cfg = RunConfig(iters_warm=12, iters_first=6, iters_next=4, learning_rate=1e-3,
+                    tv_weights=TVWeights(lambda_tv=0.0), seed=1, network=NetworkConfig(base_channels=4, seed=0),
+                    output_map=tuple(g["output_map"]), data_norm="l2sq", precision="fp32")
+    res = reconstruct_sequence(wl.matrix, wl.voltages, cfg, wl.grid)
+    assert [s.provenance for s in res.provenance_chain] == list(g["seq_provenance"])
+    assert [f.iterations for f in res.frame_records] == list(g["seq_iterations"])
+    np.testing.assert_array_equal(torch.cat([t.reshape(-1) for t in res.states["init"].tensors.values()]).numpy(),
+                                  g["seq_theta0"])
+    np.testing.assert_allclose(res.traces["warm"].data_terms(), g["seq_trace_warm"][:, 1], rtol=1e-3)
+    assert rel(res.sequence.values[:, 0], g["seq_values"][:, 0]) < 1e-2
+    assert rel(res.sequence.values, g["seq_values"]) < 0.1
