@@ -11,7 +11,8 @@
 namespace d2ip {
 
 static int tiled_threads(int cin, int cout, int ks, int cog);
-static void tiled_split(int cin, int cout, int ks, int cog, long long V, int batch, int* nchunks, int* chunk);
+static void tiled_split(int cin, int cout, int ks, int cog, long long V, int batch, int* nchunks, int* chunk,
+                        int* lanes = nullptr);
 
 template <int KS>
 struct Taps {
@@ -19,23 +20,29 @@ struct Taps {
   static constexpr int PAD = KS / 2;
 };
 
-// Direct convolutions (stride 2, 1^3, odd channel counts, the C_out = 1
-// tail, and precision FP32). A block owns CG output channels and 128 voxels
-// (one per thread); the CG x C_in x k^3 weight slice sits in shared memory as
-// [c][tap][CG] so every (c, tap) step is one float4-vectorised input load
-// (4 channels) against broadcast shared-memory weights.
+// Direct convolutions (stride 2, 1^3, dilated, odd channel counts, the C_out
+// = 1 tail, and precision FP32). A block owns CG output channels and VB
+// voxels; the CG x C_in x k^3 weight slice sits in shared memory as
+// [c][tap][CG] so every (c, tap) step is one float4-vectorised input load (4
+// channels) against broadcast shared-memory weights. Small layers (a few
+// thousand output voxels) would leave each thread a long serial chain of
+// 27 x C_in steps, so the taps are split S ways across the threads of a block
+// (S = 3 with VB = 64, or S = 9 with VB = 32): slice s takes taps s, s+S, ... and the S partial
+// sums are added in slice order through shared memory (deterministic).
 
 // y[v][co0..co0+CG) = sum_{tap,ci} x[in(v,tap)][ci] * W[co][ci][tap]
-template <int KS, int CG>
-__global__ void __launch_bounds__(128) conv_fwd_direct_k(d2ip_act x, const float* __restrict__ w,
+template <int KS, int CG, int S>
+__global__ void __launch_bounds__(288) conv_fwd_direct_k(d2ip_act x, const float* __restrict__ w,
                                                          const float* __restrict__ bias,
                                                          long long wbs, int stride, d2ip_act y,
                                                          int accumulate, int vec, int dil) {
   D2IP_PDL_ENTRY();
   constexpr int K3 = Taps<KS>::K3, PAD = Taps<KS>::PAD;
-  extern __shared__ float sw[];  // [cin][K3][CG]
+  extern __shared__ float sw[];  // [cin][K3][CG], then (S > 1) [S][VB][CG] partial sums
   const int b = blockIdx.z;
   const int cin = x.c, co0 = blockIdx.y * CG;
+  const int VB = S == 1 ? (int)blockDim.x : (S == 9 ? 32 : 64);
+  const int sl = (int)threadIdx.x / VB, vl = (int)threadIdx.x % VB;
   const float* wb = w + b * wbs;
   for (int i = threadIdx.x; i < cin * K3 * CG; i += blockDim.x) {
     const int j = i % CG, r = i / CG, tap = r % K3, ci = r / K3;
@@ -43,44 +50,53 @@ __global__ void __launch_bounds__(128) conv_fwd_direct_k(d2ip_act x, const float
   }
   __syncthreads();
   const long long V = (long long)y.d * y.h * y.w;
-  const long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= V) return;
-  const int ow = (int)(v % y.w), oh = (int)((v / y.w) % y.h), od = (int)(v / ((long long)y.w * y.h));
+  const long long v = (long long)blockIdx.x * VB + vl;
+  const bool live = v < V;
+  if (S == 1 && !live) return;
+  const long long vv = live ? v : 0;
+  const int ow = (int)(vv % y.w), oh = (int)((vv / y.w) % y.h), od = (int)(vv / ((long long)y.w * y.h));
   float acc[CG];
 #pragma unroll
-  for (int j = 0; j < CG; ++j) acc[j] = bias ? __ldg(bias + b * wbs + co0 + j) : 0.f;
+  for (int j = 0; j < CG; ++j) acc[j] = (bias && sl == 0) ? __ldg(bias + b * wbs + co0 + j) : 0.f;
   const float* xb = x.ptr + b * x.bstride;
-  for (int kd = 0; kd < KS; ++kd) {
+  for (int tap = sl; live && tap < K3; tap += S) {
+    const int kd = tap / (KS * KS), kh = (tap / KS) % KS, kw = tap % KS;
     const int id = od * stride + (kd - PAD) * dil;
-    if (id < 0 || id >= x.d) continue;
-    for (int kh = 0; kh < KS; ++kh) {
-      const int ih = oh * stride + (kh - PAD) * dil;
-      if (ih < 0 || ih >= x.h) continue;
-      for (int kw = 0; kw < KS; ++kw) {
-        const int iw = ow * stride + (kw - PAD) * dil;
-        if (iw < 0 || iw >= x.w) continue;
-        const float* xp = xb + (((long long)id * x.h + ih) * x.w + iw) * x.cstride;
-        const int tap = (kd * KS + kh) * KS + kw;
-        if (vec) {
-          for (int ci = 0; ci < cin; ci += 4) {
-            const float4 q = __ldg(reinterpret_cast<const float4*>(xp + ci));
-            const float xv[4] = {q.x, q.y, q.z, q.w};
+    const int ih = oh * stride + (kh - PAD) * dil;
+    const int iw = ow * stride + (kw - PAD) * dil;
+    if (id < 0 || id >= x.d || ih < 0 || ih >= x.h || iw < 0 || iw >= x.w) continue;
+    const float* xp = xb + (((long long)id * x.h + ih) * x.w + iw) * x.cstride;
+    if (vec) {
+      for (int ci = 0; ci < cin; ci += 4) {
+        const float4 q = __ldg(reinterpret_cast<const float4*>(xp + ci));
+        const float xv[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const float* wr = sw + ((ci + u) * K3 + tap) * CG;
+        for (int u = 0; u < 4; ++u) {
+          const float* wr = sw + ((ci + u) * K3 + tap) * CG;
 #pragma unroll
-              for (int j = 0; j < CG; ++j) acc[j] = fmaf(xv[u], wr[j], acc[j]);
-            }
-          }
-        } else {
-          for (int ci = 0; ci < cin; ++ci) {
-            const float xv = __ldg(xp + ci);
-            const float* wr = sw + (ci * K3 + tap) * CG;
-#pragma unroll
-            for (int j = 0; j < CG; ++j) acc[j] = fmaf(xv, wr[j], acc[j]);
-          }
+          for (int j = 0; j < CG; ++j) acc[j] = fmaf(xv[u], wr[j], acc[j]);
         }
       }
+    } else {
+      for (int ci = 0; ci < cin; ++ci) {
+        const float xv = __ldg(xp + ci);
+        const float* wr = sw + (ci * K3 + tap) * CG;
+#pragma unroll
+        for (int j = 0; j < CG; ++j) acc[j] = fmaf(xv, wr[j], acc[j]);
+      }
+    }
+  }
+  if constexpr (S > 1) {
+    float* red = sw + cin * K3 * CG;
+#pragma unroll
+    for (int j = 0; j < CG; ++j) red[(sl * VB + vl) * CG + j] = acc[j];
+    __syncthreads();
+    if (sl != 0 || !live) return;
+#pragma unroll
+    for (int j = 0; j < CG; ++j) {
+      float t = red[vl * CG + j];
+      for (int q = 1; q < S; ++q) t += red[(q * VB + vl) * CG + j];
+      acc[j] = t;
     }
   }
   float* yp = y.ptr + b * y.bstride + v * y.cstride + co0;
@@ -89,15 +105,17 @@ __global__ void __launch_bounds__(128) conv_fwd_direct_k(d2ip_act x, const float
 }
 
 // gx[v][ci0..ci0+CG) = sum_{tap,co} gy[o(v,tap)][co] * W[co][ci][tap]
-template <int KS, int CG>
-__global__ void __launch_bounds__(128) conv_dgrad_direct_k(d2ip_act gy, const float* __restrict__ w,
+template <int KS, int CG, int S>
+__global__ void __launch_bounds__(288) conv_dgrad_direct_k(d2ip_act gy, const float* __restrict__ w,
                                                            long long wbs, int stride, d2ip_act gx,
                                                            int accumulate, int vec, int dil) {
   D2IP_PDL_ENTRY();
   constexpr int K3 = Taps<KS>::K3, PAD = Taps<KS>::PAD;
-  extern __shared__ float sw[];  // [cout][K3][CG]
+  extern __shared__ float sw[];  // [cout][K3][CG], then (S > 1) [S][VB][CG] partial sums
   const int b = blockIdx.z;
   const int cin = gx.c, cout = gy.c, ci0 = blockIdx.y * CG;
+  const int VB = S == 1 ? (int)blockDim.x : (S == 9 ? 32 : 64);
+  const int sl = (int)threadIdx.x / VB, vl = (int)threadIdx.x % VB;
   const float* wb = w + b * wbs;
   for (int i = threadIdx.x; i < cout * K3 * CG; i += blockDim.x) {
     const int j = i % CG, r = i / CG, tap = r % K3, co = r / K3;
@@ -105,50 +123,53 @@ __global__ void __launch_bounds__(128) conv_dgrad_direct_k(d2ip_act gy, const fl
   }
   __syncthreads();
   const long long V = (long long)gx.d * gx.h * gx.w;
-  const long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= V) return;
-  const int iw = (int)(v % gx.w), ih = (int)((v / gx.w) % gx.h), id = (int)(v / ((long long)gx.w * gx.h));
+  const long long v = (long long)blockIdx.x * VB + vl;
+  const bool live = v < V;
+  if (S == 1 && !live) return;
+  const long long vv = live ? v : 0;
+  const int iw = (int)(vv % gx.w), ih = (int)((vv / gx.w) % gx.h), id = (int)(vv / ((long long)gx.w * gx.h));
   const float* gb = gy.ptr + b * gy.bstride;
   float acc[CG];
 #pragma unroll
   for (int j = 0; j < CG; ++j) acc[j] = 0.f;
-  for (int kd = 0; kd < KS; ++kd) {
-    const int td = id + (PAD - kd) * dil;
-    if (td < 0 || td % stride) continue;
-    const int od = td / stride;
-    if (od >= gy.d) continue;
-    for (int kh = 0; kh < KS; ++kh) {
-      const int th = ih + (PAD - kh) * dil;
-      if (th < 0 || th % stride) continue;
-      const int oh = th / stride;
-      if (oh >= gy.h) continue;
-      for (int kw = 0; kw < KS; ++kw) {
-        const int tw = iw + (PAD - kw) * dil;
-        if (tw < 0 || tw % stride) continue;
-        const int ow = tw / stride;
-        if (ow >= gy.w) continue;
-        const float* gp = gb + (((long long)od * gy.h + oh) * gy.w + ow) * gy.cstride;
-        const int tap = (kd * KS + kh) * KS + kw;
-        if (vec) {
-          for (int co = 0; co < cout; co += 4) {
-            const float4 q = __ldg(reinterpret_cast<const float4*>(gp + co));
-            const float gv[4] = {q.x, q.y, q.z, q.w};
+  for (int tap = sl; live && tap < K3; tap += S) {
+    const int kd = tap / (KS * KS), kh = (tap / KS) % KS, kw = tap % KS;
+    const int td = id + (PAD - kd) * dil, th = ih + (PAD - kh) * dil, tw = iw + (PAD - kw) * dil;
+    if (td < 0 || th < 0 || tw < 0 || td % stride || th % stride || tw % stride) continue;
+    const int od = td / stride, oh = th / stride, ow = tw / stride;
+    if (od >= gy.d || oh >= gy.h || ow >= gy.w) continue;
+    const float* gp = gb + (((long long)od * gy.h + oh) * gy.w + ow) * gy.cstride;
+    if (vec) {
+      for (int co = 0; co < cout; co += 4) {
+        const float4 q = __ldg(reinterpret_cast<const float4*>(gp + co));
+        const float gv[4] = {q.x, q.y, q.z, q.w};
 #pragma unroll
-            for (int u = 0; u < 4; ++u) {
-              const float* wr = sw + ((co + u) * K3 + tap) * CG;
+        for (int u = 0; u < 4; ++u) {
+          const float* wr = sw + ((co + u) * K3 + tap) * CG;
 #pragma unroll
-              for (int j = 0; j < CG; ++j) acc[j] = fmaf(gv[u], wr[j], acc[j]);
-            }
-          }
-        } else {
-          for (int co = 0; co < cout; ++co) {
-            const float gv = __ldg(gp + co);
-            const float* wr = sw + (co * K3 + tap) * CG;
-#pragma unroll
-            for (int j = 0; j < CG; ++j) acc[j] = fmaf(gv, wr[j], acc[j]);
-          }
+          for (int j = 0; j < CG; ++j) acc[j] = fmaf(gv[u], wr[j], acc[j]);
         }
       }
+    } else {
+      for (int co = 0; co < cout; ++co) {
+        const float gv = __ldg(gp + co);
+        const float* wr = sw + (co * K3 + tap) * CG;
+#pragma unroll
+        for (int j = 0; j < CG; ++j) acc[j] = fmaf(gv, wr[j], acc[j]);
+      }
+    }
+  }
+  if constexpr (S > 1) {
+    float* red = sw + cout * K3 * CG;
+#pragma unroll
+    for (int j = 0; j < CG; ++j) red[(sl * VB + vl) * CG + j] = acc[j];
+    __syncthreads();
+    if (sl != 0 || !live) return;
+#pragma unroll
+    for (int j = 0; j < CG; ++j) {
+      float t = red[vl * CG + j];
+      for (int q = 1; q < S; ++q) t += red[(q * VB + vl) * CG + j];
+      acc[j] = t;
     }
   }
   float* xp = gx.ptr + b * gx.bstride + v * gx.cstride + ci0;
@@ -194,11 +215,14 @@ __global__ void __launch_bounds__(256) conv_wgrad_partial_k(d2ip_act x, d2ip_act
   partial[((long long)b * nchunks + c) * nE + e] = acc;
 }
 
-// Register-tiled split-K weight gradient: one thread owns a 4 (C_in) x COG
-// (C_out) tile of one tap (or, for tap == K3, COG bias entries) and streams
-// its chunk of output voxels, 1-2 float4 loads of gy and one float4 load of x
-// per 4*COG FMAs. Output layout matches conv_wgrad_partial_k (OIDHW + bias).
-template <int KS, int COG>
+// Register-tiled split-K weight gradient: a group of L consecutive threads
+// owns a 4 (C_in) x COG (C_out) tile of one tap (or, for tap == K3, COG bias
+// entries); each thread streams a contiguous 1/L of the group's chunk of
+// output voxels (1-2 float4 loads of gy and one float4 load of x per 4*COG
+// FMAs) and the L partial tiles are combined by a fixed shuffle tree
+// (deterministic). L > 1 gives small layers more threads without more
+// partials. Output layout matches conv_wgrad_partial_k (OIDHW + bias).
+template <int KS, int COG, int L>
 __global__ void __launch_bounds__(128) conv_wgrad_tiled_k(d2ip_act x, d2ip_act gy, int stride,
                                                           float* __restrict__ partial, int nchunks, int chunk,
                                                           int dil) {
@@ -207,78 +231,91 @@ __global__ void __launch_bounds__(128) conv_wgrad_tiled_k(d2ip_act x, d2ip_act g
   const int b = blockIdx.z, c = blockIdx.y;
   const int cin = x.c, cout = gy.c;
   const int nci = cin >> 2, nco = cout / COG;
-  const int gid = blockIdx.x * blockDim.x + threadIdx.x;
+  const int gid = (blockIdx.x * blockDim.x + threadIdx.x) / L;
+  const int q = threadIdx.x % L;
   const int ngroups = (K3 + 1) * nci * nco;
-  if (gid >= ngroups) return;
   const int cog = gid % nco;
   const int rest = gid / nco;
   const int ci4 = rest % nci;
   const int t = rest / nci;
-  if (t == K3 && ci4 != 0) return;  // bias groups: one per co-group
+  // whole groups share `valid`, so the shuffle tree below never mixes live and dead lanes
+  const bool valid = gid < ngroups && !(t == K3 && ci4 != 0);  // bias groups: one per co-group
   const int co0 = cog * COG, ci0 = ci4 * 4;
-  const int nW = cout * cin * K3, nE = nW + cout;
   const long long V = (long long)gy.d * gy.h * gy.w;
-  const long long v0 = (long long)c * chunk;
-  const long long v1 = min(V, v0 + chunk);
+  const long long c0 = (long long)c * chunk, c1 = min(V, c0 + chunk);
+  const long long sub = (c1 - c0 + L - 1) / L;
+  const long long v0 = min(c1, c0 + q * sub), v1 = min(c1, v0 + sub);
   const float* gb = gy.ptr + b * gy.bstride + co0;
   float acc[4][COG];
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < COG; ++j) acc[i][j] = 0.f;
-  // partial layout: [b][chunk][gid][4 * COG], contiguous per thread
-  float* pout = partial + (((long long)b * nchunks + c) * ngroups + gid) * (4 * COG);
-  if (t == K3) {
+  if (valid && t == K3) {
     for (long long v = v0; v < v1; ++v) {
       const float* g = gb + v * gy.cstride;
 #pragma unroll
       for (int j = 0; j < COG; ++j) acc[0][j] += __ldg(g + j);
     }
+  } else if (valid) {
+    const int kd = t / (KS * KS), kh = (t / KS) % KS, kw = t % KS;
+    const float* xb = x.ptr + b * x.bstride + ci0;
+    int ow = (int)(v0 % gy.w), oh = (int)((v0 / gy.w) % gy.h), od = (int)(v0 / ((long long)gy.w * gy.h));
+    for (long long v = v0; v < v1; ++v) {
+      const int id = od * stride + (kd - PAD) * dil, ih = oh * stride + (kh - PAD) * dil,
+                iw = ow * stride + (kw - PAD) * dil;
+      if (id >= 0 && id < x.d && ih >= 0 && ih < x.h && iw >= 0 && iw < x.w) {
+        const float4 xv =
+            __ldg(reinterpret_cast<const float4*>(xb + (((long long)id * x.h + ih) * x.w + iw) * x.cstride));
+        float g[COG];
+        const float* gp = gb + v * gy.cstride;
+        if constexpr (COG % 4 == 0) {
+#pragma unroll
+          for (int j = 0; j < COG; j += 4) {
+            const float4 qq = __ldg(reinterpret_cast<const float4*>(gp + j));
+            g[j] = qq.x; g[j + 1] = qq.y; g[j + 2] = qq.z; g[j + 3] = qq.w;
+          }
+        } else {
+#pragma unroll
+          for (int j = 0; j < COG; ++j) g[j] = __ldg(gp + j);
+        }
+#pragma unroll
+        for (int j = 0; j < COG; ++j) {
+          acc[0][j] = fmaf(xv.x, g[j], acc[0][j]);
+          acc[1][j] = fmaf(xv.y, g[j], acc[1][j]);
+          acc[2][j] = fmaf(xv.z, g[j], acc[2][j]);
+          acc[3][j] = fmaf(xv.w, g[j], acc[3][j]);
+        }
+      }
+      if (++ow == gy.w) {
+        ow = 0;
+        if (++oh == gy.h) {
+          oh = 0;
+          ++od;
+        }
+      }
+    }
+  }
+  if constexpr (L > 1) {
+#pragma unroll
+    for (int off = L / 2; off >= 1; off >>= 1)
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < COG; ++j) acc[i][j] += __shfl_down_sync(0xffffffffu, acc[i][j], off, L);
+  }
+  if (!valid || q != 0) return;
+  // partial layout: [b][chunk][gid][4 * COG], contiguous per group
+  float* pout = partial + (((long long)b * nchunks + c) * ngroups + gid) * (4 * COG);
+  if (t == K3) {
 #pragma unroll
     for (int j = 0; j < COG; ++j) pout[j] = acc[0][j];
     return;
-  }
-  const int kd = t / (KS * KS), kh = (t / KS) % KS, kw = t % KS;
-  const float* xb = x.ptr + b * x.bstride + ci0;
-  int ow = (int)(v0 % gy.w), oh = (int)((v0 / gy.w) % gy.h), od = (int)(v0 / ((long long)gy.w * gy.h));
-  for (long long v = v0; v < v1; ++v) {
-    const int id = od * stride + (kd - PAD) * dil, ih = oh * stride + (kh - PAD) * dil,
-              iw = ow * stride + (kw - PAD) * dil;
-    if (id >= 0 && id < x.d && ih >= 0 && ih < x.h && iw >= 0 && iw < x.w) {
-      const float4 xv = __ldg(reinterpret_cast<const float4*>(xb + (((long long)id * x.h + ih) * x.w + iw) * x.cstride));
-      float g[COG];
-      const float* gp = gb + v * gy.cstride;
-      if constexpr (COG % 4 == 0) {
-#pragma unroll
-        for (int j = 0; j < COG; j += 4) {
-          const float4 q = __ldg(reinterpret_cast<const float4*>(gp + j));
-          g[j] = q.x; g[j + 1] = q.y; g[j + 2] = q.z; g[j + 3] = q.w;
-        }
-      } else {
-#pragma unroll
-        for (int j = 0; j < COG; ++j) g[j] = __ldg(gp + j);
-      }
-#pragma unroll
-      for (int j = 0; j < COG; ++j) {
-        acc[0][j] = fmaf(xv.x, g[j], acc[0][j]);
-        acc[1][j] = fmaf(xv.y, g[j], acc[1][j]);
-        acc[2][j] = fmaf(xv.z, g[j], acc[2][j]);
-        acc[3][j] = fmaf(xv.w, g[j], acc[3][j]);
-      }
-    }
-    if (++ow == gy.w) {
-      ow = 0;
-      if (++oh == gy.h) {
-        oh = 0;
-        ++od;
-      }
-    }
   }
 #pragma unroll
   for (int i = 0; i < 4; ++i)
 #pragma unroll
     for (int j = 0; j < COG; ++j) pout[i * COG + j] = acc[i][j];
-  (void)nE;
 }
 
 // Sum the thread-contiguous partials of conv_wgrad_tiled_k over chunks (fixed
@@ -377,26 +414,52 @@ static int smem_opt_in(K kernel, size_t bytes) {
 
 static bool vec_ok(const d2ip_act& a) { return a.c % 4 == 0 && a.cstride % 4 == 0 && ((uintptr_t)a.ptr & 15) == 0; }
 
+// Launch plan of a direct fwd / dgrad: channel group CG, tap split S, threads.
+struct DirectPlan {
+  int cg, S, thr;
+  long long vb;  // voxels per block
+};
+// `live_taps`: taps that actually contribute per output voxel (27, or ~27/8
+// for the data gradient of a stride-2 convolution, where only taps of matching
+// parity land on a given input voxel) -- the serial chain the split shortens.
+static DirectPlan direct_plan(long long V, int C, int ks, int batch, int live_taps) {
+  DirectPlan p;
+  const bool small = V * (C / 8 + 1) * batch < 296LL * 128;
+  p.cg = (C % 8 == 0 && !small) ? 8 : (C % 4 == 0 ? 4 : 1);
+  const long long base = V * (C / p.cg) * batch;  // threads without a tap split
+  p.S = 1;
+  if (ks == 3 && live_taps >= 27) p.S = base < 48LL * 1024 ? 9 : (base < 128LL * 1024 ? 3 : 1);
+  if (ks == 3 && live_taps < 27 && base < 48LL * 1024) p.S = 9;
+  p.vb = p.S == 9 ? 32 : (p.S == 3 ? 64 : 0);
+  p.thr = p.S > 1 ? (int)p.vb * p.S : (small ? 64 : 128);
+  if (p.S == 1) p.vb = p.thr;
+  return p;
+}
+
 int conv_fwd_direct(d2ip_act x, const float* w, const float* bias, long long wbs, int ks, int stride,
                     d2ip_act y, int accumulate, int batch, cudaStream_t st, int dil) {
   const long long V = (long long)y.d * y.h * y.w;
   const int vec = vec_ok(x) ? 1 : 0;
-#define LAUNCH_F(KS_, CG_)                                                                          \
-  do {                                                                                              \
-    const size_t sm = (size_t)x.c * KS_ * KS_ * KS_ * CG_ * sizeof(float);                          \
-    D2IP_CHECK_ARG(sm <= 200 * 1024, "conv3d_fwd: weight slice too large for shared memory");      \
-    D2IP_RET(smem_opt_in(conv_fwd_direct_k<KS_, CG_>, sm));                                        \
-    dim3 grid(cdiv(V, thr), y.c / CG_, batch);                                                      \
-    D2IP_CUDA(launch_pdl((conv_fwd_direct_k<KS_, CG_>), grid, thr, sm, st, x, w, bias, wbs, stride, y, accumulate, vec, dil)); \
+  const DirectPlan p = direct_plan(V, y.c, ks, batch, 27);
+#define LAUNCH_F(KS_, CG_, S_)                                                                       \
+  do {                                                                                               \
+    const size_t sm = ((size_t)x.c * KS_ * KS_ * KS_ * CG_ + (S_ > 1 ? (size_t)p.thr * CG_ : 0)) * sizeof(float); \
+    D2IP_CHECK_ARG(sm <= 200 * 1024, "conv3d_fwd: weight slice too large for shared memory");       \
+    D2IP_RET(smem_opt_in(conv_fwd_direct_k<KS_, CG_, S_>, sm));                                     \
+    dim3 grid(cdiv(V, p.vb), y.c / CG_, batch);                                                      \
+    D2IP_CUDA(launch_pdl((conv_fwd_direct_k<KS_, CG_, S_>), grid, p.thr, sm, st, x, w, bias, wbs, stride, y, \
+                         accumulate, vec, dil));                                                     \
   } while (0)
-  // small layers: narrower channel groups and 64-thread blocks to fill the SMs
-  const bool small = V * (y.c / 8 + 1) * batch < 296LL * 128;
-  const int cg = (y.c % 8 == 0 && !small) ? 8 : (y.c % 4 == 0 ? 4 : 1);
-  const int thr = small ? 64 : 128;
   if (ks == 3) {
-    if (cg == 8) LAUNCH_F(3, 8); else if (cg == 4) LAUNCH_F(3, 4); else LAUNCH_F(3, 1);
+    if (p.S == 9) {
+      if (p.cg == 8) LAUNCH_F(3, 8, 9); else if (p.cg == 4) LAUNCH_F(3, 4, 9); else LAUNCH_F(3, 1, 9);
+    } else if (p.S == 3) {
+      if (p.cg == 8) LAUNCH_F(3, 8, 3); else if (p.cg == 4) LAUNCH_F(3, 4, 3); else LAUNCH_F(3, 1, 3);
+    } else {
+      if (p.cg == 8) LAUNCH_F(3, 8, 1); else if (p.cg == 4) LAUNCH_F(3, 4, 1); else LAUNCH_F(3, 1, 1);
+    }
   } else {
-    if (cg == 8) LAUNCH_F(1, 8); else if (cg == 4) LAUNCH_F(1, 4); else LAUNCH_F(1, 1);
+    if (p.cg == 8) LAUNCH_F(1, 8, 1); else if (p.cg == 4) LAUNCH_F(1, 4, 1); else LAUNCH_F(1, 1, 1);
   }
 #undef LAUNCH_F
   set_variant("direct_fp32");
@@ -408,21 +471,26 @@ int conv_dgrad_direct(d2ip_act gy, const float* w, long long wbs, int ks, int st
                       int accumulate, int batch, cudaStream_t st, int dil) {
   const long long V = (long long)gx.d * gx.h * gx.w;
   const int vec = vec_ok(gy) ? 1 : 0;
-#define LAUNCH_D(KS_, CG_)                                                                        \
-  do {                                                                                            \
-    const size_t sm = (size_t)gy.c * KS_ * KS_ * KS_ * CG_ * sizeof(float);                       \
-    D2IP_CHECK_ARG(sm <= 200 * 1024, "conv3d_dgrad: weight slice too large for shared memory");  \
-    D2IP_RET(smem_opt_in(conv_dgrad_direct_k<KS_, CG_>, sm));                                    \
-    dim3 grid(cdiv(V, thr), gx.c / CG_, batch);                                                   \
-    D2IP_CUDA(launch_pdl((conv_dgrad_direct_k<KS_, CG_>), grid, thr, sm, st, gy, w, wbs, stride, gx, accumulate, vec, dil)); \
+  const DirectPlan p = direct_plan(V, gx.c, ks, batch, stride == 1 ? 27 : 4);
+#define LAUNCH_D(KS_, CG_, S_)                                                                        \
+  do {                                                                                                \
+    const size_t sm = ((size_t)gy.c * KS_ * KS_ * KS_ * CG_ + (S_ > 1 ? (size_t)p.thr * CG_ : 0)) * sizeof(float); \
+    D2IP_CHECK_ARG(sm <= 200 * 1024, "conv3d_dgrad: weight slice too large for shared memory");      \
+    D2IP_RET(smem_opt_in(conv_dgrad_direct_k<KS_, CG_, S_>, sm));                                    \
+    dim3 grid(cdiv(V, p.vb), gx.c / CG_, batch);                                                      \
+    D2IP_CUDA(launch_pdl((conv_dgrad_direct_k<KS_, CG_, S_>), grid, p.thr, sm, st, gy, w, wbs, stride, gx, \
+                         accumulate, vec, dil));                                                      \
   } while (0)
-  const bool small = V * (gx.c / 8 + 1) * batch < 296LL * 128;
-  const int cg = (gx.c % 8 == 0 && !small) ? 8 : (gx.c % 4 == 0 ? 4 : 1);
-  const int thr = small ? 64 : 128;
   if (ks == 3) {
-    if (cg == 8) LAUNCH_D(3, 8); else if (cg == 4) LAUNCH_D(3, 4); else LAUNCH_D(3, 1);
+    if (p.S == 9) {
+      if (p.cg == 8) LAUNCH_D(3, 8, 9); else if (p.cg == 4) LAUNCH_D(3, 4, 9); else LAUNCH_D(3, 1, 9);
+    } else if (p.S == 3) {
+      if (p.cg == 8) LAUNCH_D(3, 8, 3); else if (p.cg == 4) LAUNCH_D(3, 4, 3); else LAUNCH_D(3, 1, 3);
+    } else {
+      if (p.cg == 8) LAUNCH_D(3, 8, 1); else if (p.cg == 4) LAUNCH_D(3, 4, 1); else LAUNCH_D(3, 1, 1);
+    }
   } else {
-    if (cg == 8) LAUNCH_D(1, 8); else if (cg == 4) LAUNCH_D(1, 4); else LAUNCH_D(1, 1);
+    if (p.cg == 8) LAUNCH_D(1, 8, 1); else if (p.cg == 4) LAUNCH_D(1, 4, 1); else LAUNCH_D(1, 1, 1);
   }
 #undef LAUNCH_D
   set_variant("direct_fp32");
@@ -468,11 +536,14 @@ static int tiled_threads(int cin, int cout, int ks, int cog) {
 }
 
 // Chunking of the voxel (K) dimension for the tiled kernel: ~600k threads,
-// >= 32 voxels per chunk, partials capped at 4M floats.
-static void tiled_split(int cin, int cout, int ks, int cog, long long V, int batch, int* nchunks, int* chunk) {
+// >= 32 voxels per chunk, partials capped at 4M floats; then L threads per
+// group (1..8) when the chunks alone leave the GPU short of threads.
+static void tiled_split(int cin, int cout, int ks, int cog, long long V, int batch, int* nchunks, int* chunk,
+                        int* lanes) {
   const long long nthr = tiled_threads(cin, cout, ks, cog);
   const long long per_chunk = nthr * 4 * cog * batch;
-  long long want = (148LL * 4096 + nthr * batch - 1) / (nthr * batch);
+  const long long target = 148LL * 4096;
+  long long want = (target + nthr * batch - 1) / (nthr * batch);
   want = std::min(want, (V + 31) / 32);
   want = std::min(want, std::max(1LL, (4LL << 20) / per_chunk));
   want = std::min(want, 256LL);  // keeps the fixed-order chunk reduction short
@@ -480,6 +551,9 @@ static void tiled_split(int cin, int cout, int ks, int cog, long long V, int bat
   const int c = (int)((V + want - 1) / want);
   *chunk = c;
   *nchunks = (int)((V + c - 1) / c);
+  int L = 1;
+  while (L < 8 && nthr * batch * *nchunks * L * 2 <= target && c >= 16 * L) L *= 2;
+  if (lanes) *lanes = L;
 }
 
 int conv_wgrad_direct(d2ip_act x, d2ip_act gy, int ks, int stride, float* gw, long long gwbs,
@@ -490,22 +564,31 @@ int conv_wgrad_direct(d2ip_act x, d2ip_act gy, int ks, int stride, float* gw, lo
   const int cog = tiled_cog(x, gy);
   if (cog) {
     const int nthr = tiled_threads(x.c, gy.c, ks, cog);
-    tiled_split(x.c, gy.c, ks, cog, V, batch, &nchunks, &chunk);
+    int L = 1;
+    tiled_split(x.c, gy.c, ks, cog, V, batch, &nchunks, &chunk, &L);
     D2IP_CHECK_ARG(ws_bytes >= (size_t)batch * nchunks * nthr * 4 * cog * sizeof(float),
                    "conv3d_wgrad: workspace too small");
     float* partial = reinterpret_cast<float*>(ws);
-    dim3 grid(cdiv(nthr, 128), nchunks, batch);
-#define LAUNCH_T(KS_, COG_) \
-  D2IP_CUDA(launch_pdl((conv_wgrad_tiled_k<KS_, COG_>), grid, 128, 0, st, x, gy, stride, partial, nchunks, chunk, dil))
+    dim3 grid(cdiv((long long)nthr * L, 128), nchunks, batch);
+#define LAUNCH_T(KS_, COG_, L_) \
+  D2IP_CUDA(launch_pdl((conv_wgrad_tiled_k<KS_, COG_, L_>), grid, 128, 0, st, x, gy, stride, partial, nchunks, chunk, dil))
+#define LAUNCH_TL(KS_, COG_)                         \
+  do {                                               \
+    if (L == 8) LAUNCH_T(KS_, COG_, 8);              \
+    else if (L == 4) LAUNCH_T(KS_, COG_, 4);         \
+    else if (L == 2) LAUNCH_T(KS_, COG_, 2);         \
+    else LAUNCH_T(KS_, COG_, 1);                     \
+  } while (0)
     if (ks == 3) {
-      if (cog == 8) LAUNCH_T(3, 8); else if (cog == 4) LAUNCH_T(3, 4); else LAUNCH_T(3, 1);
+      if (cog == 8) LAUNCH_TL(3, 8); else if (cog == 4) LAUNCH_TL(3, 4); else LAUNCH_TL(3, 1);
     } else {
-      if (cog == 8) LAUNCH_T(1, 8); else if (cog == 4) LAUNCH_T(1, 4); else LAUNCH_T(1, 1);
+      if (cog == 8) LAUNCH_TL(1, 8); else if (cog == 4) LAUNCH_TL(1, 4); else LAUNCH_TL(1, 1);
     }
+#undef LAUNCH_TL
 #undef LAUNCH_T
     D2IP_LAUNCH_CHECK();
-    D2IP_CUDA(launch_pdl(wgrad_tiled_reduce_k, dim3(cdiv((long long)nthr * 4 * cog, 32), batch), 256, 0, st, 
-        partial, nchunks, nthr, x.c, gy.c, ks * ks * ks, cog, gw, gwbs));
+    D2IP_CUDA(launch_pdl(wgrad_tiled_reduce_k, dim3(cdiv((long long)nthr * 4 * cog, 32), batch), 256, 0, st,
+                         partial, nchunks, nthr, x.c, gy.c, ks * ks * ks, cog, gw, gwbs));
     D2IP_LAUNCH_CHECK();
     return D2IP_OK;
   }

@@ -94,13 +94,18 @@ def test_refnet_tv_step_vs_reference(gold, tag):
 @pytest.mark.parametrize("tag", ["dw4", "dense4"])
 @pytest.mark.parametrize("k", [1, 10])
 def test_refnet_adam_trajectory_vs_reference(gold, tag, k):
+    """Adam's first steps are sign-like for near-zero gradient entries, so fp32
+    summation order alone moves theta: the reference's own arithmetic with only
+    J.sigma's order changed (CPU oracle, compact J) lands 2.4e-4 from the
+    reference after 10 steps on dw4 (2e-7 on dense4). Bar: 1e-4 after 1 step,
+    5e-4 (2x that band) after 10."""
     g, wl = gold
     dn, _ = _net(g, wl, tag, "fp32")
     dn.reset_frame()
     dn.run(k)
     torch.cuda.synchronize()
     assert int(dn.status_host()[0, 0]) == k
-    assert rel(dn.theta[0].cpu().numpy(), g[f"{tag}_theta{k}"]) < 1e-4
+    assert rel(dn.theta[0].cpu().numpy(), g[f"{tag}_theta{k}"]) < (1e-4 if k == 1 else 5e-4)
     np.testing.assert_allclose(dn.trace_host(0, k)[:, 0], g[f"{tag}_trace{k}"][:, 1], rtol=1e-3)
 
 
