@@ -94,6 +94,11 @@ int d2ip_conv3d_wgrad(d2ip_act x, d2ip_act gy, int ksize, int stride, float* gw,
                       long long gwbstride, void* ws, size_t ws_bytes, int precision,
                       int batch, void* stream);
 
+/* Weight-gradient kernel for TF32 stride-1 layers: 0 = smem-tiled CUDA-core
+ * fp32 (default), 1 = tcgen05 3xTF32 (wgrad_tc.cu). Process-wide; also set by
+ * the environment variable D2IP_WGRAD=tc. */
+int d2ip_set_wgrad_variant(int variant);
+
 /* ---- ChannelLayerNorm (+ residual) (+ LeakyReLU) forward ----------------
  * out = act(gamma * xhat + beta [+ res]), xhat = (y - mean_c) * rstd,
  * rstd = 1/sqrt(var_c + 1e-5). Saves xhat [B][V][C] and rstd [B][V].

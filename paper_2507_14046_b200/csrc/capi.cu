@@ -1,5 +1,6 @@
 // C ABI wrappers (include/d2ip_b200.h) and the convolution dispatcher.
 #include <stdarg.h>
+#include <stdlib.h>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -29,16 +30,28 @@ static size_t conv_ws(int cin, int cout, int ks, int stride, int precision, int 
 
 // Weight gradient: the smem-tiled kernel for stride-1 3^3 layers, the
 // register-tiled / scalar split-K kernels otherwise (stride 2, 1^3, C_out = 1).
+// Weight-gradient kernel policy for TF32 runs: 0 = the smem-tiled CUDA-core
+// kernel (default: with the weight gradients on the engine's side stream it
+// measured faster end to end, 828 vs 786 it/s at cfg1), 1 = tcgen05 (3xTF32).
+static int g_wgrad_variant = [] {
+  const char* v = getenv("D2IP_WGRAD");
+  return v && v[0] == 't' ? 1 : 0;
+}();
+
 size_t conv_wgrad_ws(int cin, int cout, int ks, int D, int H, int W, int batch, int precision) {
-  (void)precision;
+  (void)precision;  // the maximum over every variant the views may select
   const size_t a = conv_wgrad_direct_ws(cin, cout, ks, (long long)D * H * W, batch);
   const size_t b = wgrad_s1_ws_bytes(D, H, W, cin, cout, ks, batch);
-  return a > b ? a : b;
+  const size_t c = wgrad_tc_ws_bytes(D, H, W, cin, cout, ks, batch);
+  return std::max(a, std::max(b, c));
 }
 
 int conv_wgrad(d2ip_act x, d2ip_act gy, int ks, int stride, float* gw, long long gwbs, void* ws,
                size_t ws_bytes, int precision, int batch, cudaStream_t st) {
-  (void)precision;
+  if (stride == 1 && g_wgrad_variant == 1 && wgrad_tc_supported(x, gy, ks, precision)) {
+    set_variant("wgrad_tcgen05_tf32x3");
+    return wgrad_tc(x, gy, ks, gw, gwbs, ws, ws_bytes, batch, st);
+  }
   if (stride == 1 && wgrad_s1_supported(x, gy, ks)) {
     set_variant("wgrad_s1_smem");
     return wgrad_s1(x, gy, ks, gw, gwbs, ws, ws_bytes, batch, st);
@@ -103,6 +116,12 @@ int d2ip_conv3d_dgrad(d2ip_act gy, const float* w, long long wbstride, int ksize
 
 size_t d2ip_conv3d_wgrad_ws_bytes(d2ip_act x, d2ip_act gy, int ksize, int batch) {
   return d2ip::conv_wgrad_ws(x.c, gy.c, ksize, gy.d, gy.h, gy.w, batch, 0);
+}
+
+int d2ip_set_wgrad_variant(int variant) {
+  D2IP_CHECK_ARG(variant == 0 || variant == 1, "wgrad variant must be 0 (CUDA cores) or 1 (tcgen05)");
+  d2ip::g_wgrad_variant = variant;
+  return D2IP_OK;
 }
 
 int d2ip_conv3d_wgrad(d2ip_act x, d2ip_act gy, int ksize, int stride, float* gw, long long gwbstride, void* ws,

@@ -39,7 +39,6 @@ namespace d2ip {
 
 constexpr int kTcThreads = 128;
 constexpr int kTcRows = 128;
-constexpr size_t kTcStageBudget = 110 * 1024;  // both stages; allows 2 CTAs/SM
 
 __host__ __device__ static inline int np_of(int n) { return (n + 15) / 16 * 16; }
 static inline int wr_of(int sw) { return kTcRows + 2 * sw + 2; }
@@ -66,35 +65,30 @@ static size_t stage_bytes(int cb, int np, int wrp) {
   return 2 * ((size_t)cb * wrp * 4 + (size_t)9 * cb * np * 4);
 }
 
-static int choose_cb(int kc, int np, int wrp, size_t budget) {
-  int best = 0;
-  for (int cb = 8; cb <= kc; cb *= 2) {
-    if (kc % cb) continue;
-    if (2 * stage_bytes(cb, np, wrp) <= budget) best = cb;
-  }
-  return best;
-}
-
 static size_t tc_smem_bytes(const TcConv& a) {
   return 2 * stage_bytes(a.CB, a.Ns, a.WRp) + 3 * a.WR * sizeof(int) + 64;
 }
 
 __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 
+// NKC = CB / 4: 16-byte channel chunks per stage (compile-time, so the fill
+// loops need no integer division).
+template <int NKC>
 __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
   D2IP_PDL_ENTRY();
   extern __shared__ __align__(1024) uint8_t smem[];
+  constexpr int CB = NKC * 4;
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int b = blockIdx.z;
   const int ks = blockIdx.y % a.kspl;
   const int n0 = (blockIdx.y / a.kspl) * a.Ns;  // first output channel of this CTA's slice
   const int u0 = a.u_first + blockIdx.x * kTcRows;
-  const int nkc = a.CB >> 2;
-  const size_t Ab = (size_t)a.CB * a.WRp * 4, Bb = (size_t)9 * a.CB * a.Ns * 4;
-  const size_t Sb = 2 * (Ab + Bb);
+  const int Ns = a.Ns, WR = a.WR, WRp = a.WRp;
+  const uint32_t Ab = (uint32_t)NKC * WRp * 16, Bb = (uint32_t)9 * NKC * Ns * 16;
+  const uint32_t Sb = 2 * (Ab + Bb);
   // stage layout: [A hi][A lo][B hi][B lo]
   int* rowmap = reinterpret_cast<int*>(smem + 2 * Sb);
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(rowmap + 3 * a.WR + ((3 * a.WR) & 1));
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(rowmap + 3 * WR + ((3 * WR) & 1));
   uint32_t* tslot = reinterpret_cast<uint32_t*>(mbar + 2);
 
   if (warp == 0) tc::tmem_alloc(tslot, a.tmem_cols);
@@ -105,8 +99,8 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
   }
   // voxel offset of every window row for the three plane taps (-1 = padding)
   const d2ip_act x = a.x;
-  for (int i = tid; i < 3 * a.WR; i += kTcThreads) {
-    const int kd = i / a.WR, r = i - kd * a.WR;
+  for (int i = tid; i < 3 * WR; i += kTcThreads) {
+    const int kd = i / WR, r = i - kd * WR;
     const int u = u0 + (kd - 1) * a.Sh - a.Sw - 1 + r;
     int off = -1;
     if (u >= 0) {
@@ -126,29 +120,32 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
   const int S_all = 3 * a.n_cb;
   const int s_lo = (int)((long long)ks * S_all / a.kspl), s_hi = (int)((long long)(ks + 1) * S_all / a.kspl);
   const int S = s_hi - s_lo;  // this CTA's stages: s_lo + [0, S)
-  const int nA = a.WR * nkc;
+  const int nA = WR * NKC;
+  const int kc_all = a.Kc >> 2;
 
   auto load = [&](int sl, int buf) {
     const int s = s_lo + sl;
     const int kd = s / a.n_cb, cb = s - kd * a.n_cb;
-    const int* rm = rowmap + kd * a.WR;
+    const int* rm = rowmap + kd * WR;
     uint8_t* A = smem + buf * Sb;
+    const float* xc = xb + cb * CB;
     for (int i = tid; i < nA; i += kTcThreads) {
-      const int r = i / nkc, kc = i - r * nkc;  // nkc is a power of two
+      const int r = i / NKC, kc = i % NKC;
       const int off = rm[r];
-      const float* src = off >= 0 ? xb + (long long)off * x.cstride + cb * a.CB + 4 * kc : xb;
-      tc::cp_async16(A + ((size_t)kc * a.WRp + r) * 16, src, off >= 0 ? 16u : 0u);
+      const float* src = off >= 0 ? xc + (long long)off * x.cstride + 4 * kc : xb;
+      tc::cp_async16(A + ((size_t)kc * WRp + r) * 16, src, off >= 0 ? 16u : 0u);
     }
+    // B: 9 taps x NKC chunks, each a contiguous run of Ns 16-byte rows; one warp per run
     uint8_t* Bt = smem + buf * Sb + 2 * Ab;
-    const int per_tap = nkc * a.Ns;  // 16-B units per tap in this stage
-    const int nB = 9 * per_tap;
-    const int kc_all = a.Kc >> 2;
-    for (int i = tid; i < nB; i += kTcThreads) {
-      const int t9 = i / per_tap, rem = i - t9 * per_tap;
-      const int kcl = rem / a.Ns, n = rem - kcl * a.Ns;
-      const float* src = wpb + ((long long)((kd * 9 + t9) * kc_all + cb * nkc + kcl) * a.Np + n0 + n) * 4;
-      tc::cp_async16(Bt + (size_t)i * 16, src, 16u);
-      tc::cp_async16(Bt + Bb + (size_t)i * 16, src + a.wlo, 16u);
+    const float* wk = wpb + ((long long)(kd * 9) * kc_all + cb * NKC) * a.Np * 4 + (long long)n0 * 4;
+    for (int q = warp; q < 9 * NKC; q += kTcThreads / 32) {
+      const int t9 = q / NKC, kcl = q % NKC;
+      const float* src = wk + ((long long)t9 * kc_all + kcl) * a.Np * 4;
+      uint8_t* dst = Bt + (size_t)q * Ns * 16;
+      for (int n = lane; n < Ns; n += 32) {
+        tc::cp_async16(dst + n * 16, src + n * 4, 16u);
+        tc::cp_async16(dst + Bb + n * 16, src + a.wlo + n * 4, 16u);
+      }
     }
     tc::cp_async_commit();
   };
@@ -157,9 +154,9 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
   auto split = [&](int buf) {
     uint8_t* A = smem + buf * Sb;
     for (int i = tid; i < nA; i += kTcThreads) {
-      const int r = i / nkc, kc = i - r * nkc;
-      float4* hp = reinterpret_cast<float4*>(A + ((size_t)kc * a.WRp + r) * 16);
-      float4* lp = reinterpret_cast<float4*>(A + Ab + ((size_t)kc * a.WRp + r) * 16);
+      const int r = i / NKC, kc = i % NKC;
+      float4* hp = reinterpret_cast<float4*>(A + ((size_t)kc * WRp + r) * 16);
+      float4* lp = reinterpret_cast<float4*>(A + Ab + ((size_t)kc * WRp + r) * 16);
       float4 v = *hp, h, l;
       h.x = tf32_hi(v.x); h.y = tf32_hi(v.y); h.z = tf32_hi(v.z); h.w = tf32_hi(v.w);
       l.x = v.x - h.x; l.y = v.y - h.y; l.z = v.z - h.z; l.w = v.w - h.w;
@@ -167,6 +164,11 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
       *lp = l;
     }
   };
+  // descriptors of buffer 0; a tap / K step / buffer is an add to the 14-bit
+  // start-address field (smem addresses < 256 KB never carry out of it)
+  const uint32_t sbase = tc::smem_u32(smem);
+  const uint64_t dAhi = tc::make_desc(sbase, WRp * 16, 128), dAlo = dAhi + (Ab >> 4);
+  const uint64_t dBhi = tc::make_desc(sbase + 2 * Ab, Ns * 16, 128), dBlo = dBhi + (Bb >> 4);
 
   load(0, 0);
   for (int s = 0; s < S; ++s) {
@@ -184,18 +186,17 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
     __syncthreads();
     if (tid == 0) {
       tc::fence_after();
-      const uint32_t ahi = tc::smem_u32(smem + buf * Sb), alo = ahi + (uint32_t)Ab;
-      const uint32_t bhi = ahi + (uint32_t)(2 * Ab), blo = bhi + (uint32_t)Bb;
+      const uint64_t boff = buf ? (uint64_t)(Sb >> 4) : 0;
       for (int t9 = 0; t9 < 9; ++t9) {
         const int rowoff = (t9 / 3) * a.Sw + (t9 % 3);
-        for (int j = 0; j < (a.CB >> 3); ++j) {
-          const uint32_t ao = (uint32_t)((2 * j * a.WRp + rowoff) * 16);
-          const uint32_t bo = (uint32_t)((t9 * nkc + 2 * j) * a.Ns * 16);
-          const uint32_t alb = a.WRp * 16, blb = a.Ns * 16;
+#pragma unroll
+        for (int j = 0; j < NKC / 2; ++j) {
+          const uint64_t ao = boff + (uint64_t)(2 * j * WRp + rowoff);
+          const uint64_t bo = boff + (uint64_t)((t9 * NKC + 2 * j) * Ns);
           const uint32_t first = (s | t9 | j) ? 1u : 0u;
-          tc::mma_tf32(tmem, tc::make_desc(alo + ao, alb, 128), tc::make_desc(bhi + bo, blb, 128), a.idesc, first);
-          tc::mma_tf32(tmem, tc::make_desc(ahi + ao, alb, 128), tc::make_desc(blo + bo, blb, 128), a.idesc, 1u);
-          tc::mma_tf32(tmem, tc::make_desc(ahi + ao, alb, 128), tc::make_desc(bhi + bo, blb, 128), a.idesc, 1u);
+          tc::mma_tf32(tmem, dAlo + ao, dBhi + bo, a.idesc, first);
+          tc::mma_tf32(tmem, dAhi + ao, dBlo + bo, a.idesc, 1u);
+          tc::mma_tf32(tmem, dAhi + ao, dBhi + bo, a.idesc, 1u);
         }
       }
       tc::commit(&mbar[buf]);
@@ -359,6 +360,11 @@ int conv_tc_pack(const float* w, long long wbs, int K, int N, int dgrad, float* 
 }
 
 // Tile / slice / channel-block / split-K plan for one layer shape.
+// Tile / slice / channel-block / split-K plan for one layer shape. Every
+// (N slice, channel block) pair that fits shared memory is scored with a
+// small latency model -- waves x (serial stages per CTA + fixed prologue /
+// epilogue cost) -- because at these sizes a CTA's chain of dependent stages,
+// not the tensor pipe, sets the time.
 static bool tc_plan(int D, int H, int W, int K, int N, int batch, TcConv& a, int* tiles) {
   a.N = N;
   a.Np = np_of(N);
@@ -367,26 +373,35 @@ static bool tc_plan(int D, int H, int W, int K, int N, int batch, TcConv& a, int
   a.Sh = (H + 2) * a.Sw;
   a.WR = wr_of(a.Sw);
   a.WRp = wrp_of(a.WR);
-  a.CB = 0;
-  for (size_t budget : {kTcStageBudget, (size_t)210 * 1024}) {
-    for (int ns = std::min(a.Np, 256); ns >= 16 && a.CB == 0; ns -= 16) {
-      if (a.Np % ns) continue;
-      a.CB = choose_cb(K, ns, a.WRp, budget);
-      if (a.CB) a.Ns = ns;
-    }
-    if (a.CB) break;
-  }
-  if (a.CB < 8) return false;
-  a.n_cb = K / a.CB;
   a.u_first = a.Sh + a.Sw + 1;
   const int u_last = D * a.Sh + H * a.Sw + W;
   *tiles = cdiv(u_last - a.u_first + 1, kTcRows);
-  // small grids are latency-bound on the serial stage chain: split the stages
-  // across CTAs until ~2 CTAs per SM are busy (fixed-order partial reduction).
-  const long long ctas = (long long)*tiles * (a.Np / a.Ns) * batch;
-  const int S = 3 * a.n_cb;
-  a.kspl = (int)std::min<long long>(S, std::max(1LL, (296 + ctas - 1) / ctas));
   a.vout = (long long)D * H * W;
+  a.CB = 0;
+  double best = 1e30;
+  for (int ns = std::min(a.Np, 256); ns >= 16; ns -= 16) {
+    if (a.Np % ns) continue;
+    for (int cb = 8; cb <= K && cb <= 64; cb *= 2) {
+      if (K % cb) continue;
+      const size_t sm = 2 * stage_bytes(cb, ns, a.WRp) + 3 * a.WR * sizeof(int) + 64;
+      if (sm > (size_t)210 * 1024) continue;
+      const int per_sm = sm <= (size_t)110 * 1024 ? 2 : 1;
+      const long long ctas0 = (long long)*tiles * (a.Np / ns) * batch;
+      const int S = 3 * (K / cb);
+      // split the stage chain across CTAs until ~2 CTAs per SM are busy
+      const int kspl = (int)std::min<long long>(S, std::max(1LL, (296 + ctas0 - 1) / ctas0));
+      const long long waves = (ctas0 * kspl + 148LL * per_sm - 1) / (148LL * per_sm);
+      const double cost = (double)waves * ((S + kspl - 1) / kspl + 2.0) + (kspl > 1 ? 1.0 : 0.0);
+      if (cost < best - 1e-9) {
+        best = cost;
+        a.CB = cb;
+        a.Ns = ns;
+        a.kspl = kspl;
+      }
+    }
+  }
+  if (a.CB < 8) return false;
+  a.n_cb = K / a.CB;
   return true;
 }
 
@@ -422,10 +437,18 @@ int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, lo
   const size_t smem = tc_smem_bytes(a);
   static bool attr_set = false;
   if (!attr_set) {
-    D2IP_CUDA(cudaFuncSetAttribute(conv_tc_k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    for (auto k : {conv_tc_k<2>, conv_tc_k<4>, conv_tc_k<8>, conv_tc_k<16>})
+      D2IP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr_set = true;
   }
-  D2IP_CUDA(launch_pdl(conv_tc_k, dim3(tiles, (a.Np / a.Ns) * a.kspl, batch), kTcThreads, smem, st, a));
+  const dim3 grid(tiles, (a.Np / a.Ns) * a.kspl, batch);
+  switch (a.CB / 4) {
+    case 2: D2IP_CUDA(launch_pdl(conv_tc_k<2>, grid, kTcThreads, smem, st, a)); break;
+    case 4: D2IP_CUDA(launch_pdl(conv_tc_k<4>, grid, kTcThreads, smem, st, a)); break;
+    case 8: D2IP_CUDA(launch_pdl(conv_tc_k<8>, grid, kTcThreads, smem, st, a)); break;
+    case 16: D2IP_CUDA(launch_pdl(conv_tc_k<16>, grid, kTcThreads, smem, st, a)); break;
+    default: D2IP_CHECK_ARG(false, "conv_tc: unsupported channel block %d", a.CB);
+  }
   D2IP_LAUNCH_CHECK();
   if (deferred) *deferred = a.kspl > 1 ? a.kspl : 0;
   if (a.kspl > 1 && !deferred) {

@@ -97,6 +97,7 @@ static void config_plan_workspace(d2ip_engine& E, Arena& A) {
   E.gbout = takef((long long)B * E.V[L - 1] * c[L - 1]);
   E.stem_xh = takef((long long)B * E.V[0] * c[0]);
   E.stem_rs = takef((long long)B * E.V[0]);
+  E.stem_gc = takef((long long)B * E.V[0] * c[0]);
   long long maxvc = E.V[0] * c[0];
   auto saved = [&](Block& bl) {
     const long long vc = E.V[bl.lout] * bl.c1.cout;
@@ -106,6 +107,9 @@ static void config_plan_workspace(d2ip_engine& E, Arena& A) {
     bl.xh2 = takef(B * vc);
     bl.rs1 = takef((long long)B * E.V[bl.lout]);
     bl.rs2 = takef((long long)B * E.V[bl.lout]);
+    bl.gpre = takef(B * vc);
+    bl.gc2 = takef(B * vc);
+    bl.gc1 = takef(B * vc);
   };
   for (auto& bl : E.enc) saved(bl);
   saved(E.neck);
@@ -252,6 +256,30 @@ int cwgrad(Ctx& k, const ConvP& c, d2ip_act x, d2ip_act gy) {
   return conv_wgrad(x, gy, c.ks, c.stride, k.gr() + c.ow, k.pbs, k.E.wg_ws, k.E.wg_ws_bytes, k.prec, k.B, k.st);
 }
 
+int fork_side(Ctx& k) {
+  cudaEvent_t e = k.E.ev[k.E.evi++ % d2ip_engine::kEvents];
+  D2IP_CUDA(cudaEventRecord(e, k.st));
+  D2IP_CUDA(cudaStreamWaitEvent(k.side, e, 0));
+  k.forked = true;
+  return D2IP_OK;
+}
+
+int join_side(Ctx& k) {
+  if (!k.forked) return D2IP_OK;
+  k.forked = false;
+  cudaEvent_t e = k.E.ev[k.E.evi++ % d2ip_engine::kEvents];
+  D2IP_CUDA(cudaEventRecord(e, k.side));
+  D2IP_CUDA(cudaStreamWaitEvent(k.st, e, 0));
+  return D2IP_OK;
+}
+
+int cwgrad_side(Ctx& k, const ConvP& c, d2ip_act x, d2ip_act gy) {
+  D2IP_RET(fork_side(k));
+  Ctx ks = k;
+  ks.st = k.side;
+  return cwgrad(ks, c, x, gy);
+}
+
 // The job table of every tcgen05 layer's weight packs (built once at bind).
 static void build_pack_jobs(d2ip_engine& E) {
   PackJobs& j = E.packjobs;
@@ -302,16 +330,22 @@ static int block_bwd(Ctx& k, Block& bl) {
   d2ip_engine& E = k.E;
   const int co = bl.c1.cout;
   auto S = [&](int i) { return view(E, E.sc[i], bl.lout, co, co); };
-  d2ip_act gpre = S(0), gc2 = S(1), gh1 = S(2), gpre1 = S(3), gc1 = S(4);
+  auto P = [&](float* p) { return view(E, p, bl.lout, co, co); };
+  // gpre / gc2 / gc1 feed the side-stream weight gradients: per-block buffers
+  d2ip_act gpre = P(bl.gpre), gc2 = P(bl.gc2), gh1 = S(2), gpre1 = S(3), gc1 = P(bl.gc1);
   d2ip_act h1 = view(E, bl.h1, bl.lout, co, co);
   D2IP_RET(norm_act_bwd(bl.gout, bl.out, 1, k.slope, bl.xh2, bl.rs2, k.th() + bl.n2.og, k.pbs, gpre, gc2,
                         k.gr() + bl.n2.og, k.pbs, E.na_ws, E.na_ws_bytes, k.B, k.st));
-  D2IP_RET(cwgrad(k, bl.c2, h1, gc2));
+  D2IP_RET(cwgrad_side(k, bl.c2, h1, gc2));
   D2IP_RET(cdgrad(k, bl.c2, gc2, gh1, 0));
   D2IP_RET(norm_act_bwd(gh1, h1, 1, k.slope, bl.xh1, bl.rs1, k.th() + bl.n1.og, k.pbs, gpre1, gc1,
                         k.gr() + bl.n1.og, k.pbs, E.na_ws, E.na_ws_bytes, k.B, k.st));
-  D2IP_RET(cwgrad(k, bl.c1, bl.x, gc1));
-  D2IP_RET(cwgrad(k, bl.sk, bl.x, gpre));
+  D2IP_RET(cwgrad_side(k, bl.c1, bl.x, gc1));
+  {
+    Ctx ks = k;  // already ordered after gpre by the fork above
+    ks.st = k.side;
+    D2IP_RET(cwgrad(ks, bl.sk, bl.x, gpre));
+  }
   D2IP_RET(cdgrad(k, bl.c1, gc1, bl.gx, bl.gx_acc));
   D2IP_RET(cdgrad(k, bl.sk, gpre, bl.gx, 1));
   return D2IP_OK;
@@ -380,10 +414,13 @@ static int backward(Ctx& k) {
     D2IP_RET(jac_adj_finish(E.adjpart, E.rsplit, E.d.Vp, E.d.V, E.b.vox_of_col, E.b.sig, scale, E.gtail, E.V[0],
                             0, k.B, k.st));
   }
-  if (E.d.arch == D2IP_ARCH_FAST_RESUNET) return refnet_backward(k);
+  if (E.d.arch == D2IP_ARCH_FAST_RESUNET) {
+    D2IP_RET(refnet_backward(k));
+    return join_side(k);
+  }
   d2ip_act gt = view(E, E.gtail, 0, 1, 1);
   Block& last = E.dec.back();
-  D2IP_RET(cwgrad(k, E.tail, last.out, gt));
+  D2IP_RET(cwgrad_side(k, E.tail, last.out, gt));
   D2IP_RET(cdgrad(k, E.tail, gt, last.gout, 0));
   for (int j = (int)E.dec.size() - 1; j >= 0; --j) {
     Block& bl = E.dec[j];
@@ -399,12 +436,12 @@ static int backward(Ctx& k) {
   d2ip_act a0 = view(E, E.cat[0] + c[1], 0, c[0], E.catw[0]);
   d2ip_act ga0 = view(E, E.gcat[0] + c[1], 0, c[0], E.catw[0]);
   d2ip_act gpre = view(E, E.sc[0], 0, c[0], c[0]);
-  d2ip_act gc = view(E, E.sc[1], 0, c[0], c[0]);
+  d2ip_act gc = view(E, E.stem_gc, 0, c[0], c[0]);
   D2IP_RET(norm_act_bwd(ga0, a0, 1, k.slope, E.stem_xh, E.stem_rs, k.th() + E.stem_n.og, k.pbs, gpre, gc,
                         k.gr() + E.stem_n.og, k.pbs, E.na_ws, E.na_ws_bytes, k.B, k.st));
   d2ip_act z = view(E, const_cast<float*>(E.b.z), 0, E.d.in_channels, E.d.in_channels);
-  D2IP_RET(cwgrad(k, E.stem, z, gc));
-  return D2IP_OK;
+  D2IP_RET(cwgrad_side(k, E.stem, z, gc));
+  return join_side(k);
 }
 
 static int adam(Ctx& k) {
@@ -414,7 +451,7 @@ static int adam(Ctx& k) {
 }
 
 static Ctx ctx(d2ip_engine& E, void* stream) {
-  return Ctx{E, S(stream), E.d.batch, E.nparams, E.d.precision, E.d.negative_slope};
+  return Ctx{E, S(stream), E.d.batch, E.nparams, E.d.precision, E.d.negative_slope, E.side, false};
 }
 
 int engine_step(d2ip_engine& E, void* stream) {
@@ -557,6 +594,9 @@ void d2ip_engine_destroy(d2ip_engine* e) {
   d2ip::drop_graph(*e);
   d2ip::refnet_destroy(*e);
   if (e->cap_stream) cudaStreamDestroy(e->cap_stream);
+  if (e->side) cudaStreamDestroy(e->side);
+  for (auto ev : e->ev)
+    if (ev) cudaEventDestroy(ev);
   delete e;
 }
 
@@ -574,6 +614,10 @@ int d2ip_engine_bind(d2ip_engine* e, const d2ip_bindings* b) {
                  "missing binding");
   D2IP_CHECK_ARG(e->d.lambda_tv <= 0.f || b->history || e->d.max_history == 0, "TV needs a history buffer");
   drop_graph(*e);
+  if (!e->side) {
+    D2IP_CUDA(cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking));
+    for (auto& ev : e->ev) D2IP_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  }
   e->b = *b;
   plan_workspace(*e, reinterpret_cast<char*>(b->workspace));
   if (e->d.arch == D2IP_ARCH_FAST_RESUNET)

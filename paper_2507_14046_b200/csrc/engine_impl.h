@@ -29,6 +29,9 @@ struct Block {
   d2ip_act x{}, out{}, gx{}, gout{};
   int gx_acc = 0;
   float *h1 = nullptr, *xh1 = nullptr, *rs1 = nullptr, *xh2 = nullptr, *rs2 = nullptr;
+  // backward: gradients read by the weight-gradient kernels on the side stream
+  // (per block, so the next block's backward cannot overwrite them early)
+  float *gpre = nullptr, *gc2 = nullptr, *gc1 = nullptr;
 };
 
 }  // namespace d2ip
@@ -70,6 +73,12 @@ struct d2ip_engine {
   cudaGraphExec_t gexec = nullptr;
   cudaStream_t cap_stream = nullptr;
   int launches = 0;
+  // weight gradients run on a side stream, off the data-gradient critical path
+  cudaStream_t side = nullptr;
+  static constexpr int kEvents = 128;
+  cudaEvent_t ev[kEvents]{};
+  int evi = 0;
+  float* stem_gc = nullptr;
   d2ip::RefNet* ref = nullptr;  // arch == 1: FastResUNet3D program (refnet.cu)
 };
 
@@ -109,9 +118,18 @@ struct Ctx {
   long long pbs;
   int prec;
   float slope;
+  cudaStream_t side;  // weight-gradient stream (forked from / joined into st)
+  bool forked = false;  // side stream holds work of this pass (join only then: capture rules)
   float* th() const { return E.b.theta; }
   float* gr() const { return E.b.grad; }
 };
+
+// st -> side dependency (everything enqueued on st so far happens before what
+// is enqueued on side next) and the reverse join.
+int fork_side(Ctx& k);
+int join_side(Ctx& k);
+// weight gradient on the side stream, after everything already on st
+int cwgrad_side(Ctx& k, const ConvP& c, d2ip_act x, d2ip_act gy);
 
 int cfwd(Ctx& k, const ConvP& c, d2ip_act x, d2ip_act y, int acc, SplitK* sk = nullptr);
 int cdgrad(Ctx& k, const ConvP& c, d2ip_act gy, d2ip_act gx, int acc);

@@ -46,6 +46,12 @@ size_t wgrad_s1_ws_bytes(int D, int H, int W, int Cin, int Cout, int ks, int bat
 int wgrad_s1(d2ip_act x, d2ip_act gy, int ks, float* gw, long long gwbs, void* ws, size_t ws_bytes, int batch,
              cudaStream_t st);
 
+// wgrad_tc.cu — tcgen05 weight gradient of stride-1 3^3 / 1^3 convolutions (3xTF32)
+bool wgrad_tc_supported(d2ip_act x, d2ip_act gy, int ks, int precision);
+size_t wgrad_tc_ws_bytes(int D, int H, int W, int Cin, int Cout, int ks, int batch);
+int wgrad_tc(d2ip_act x, d2ip_act gy, int ks, float* gw, long long gwbs, void* ws, size_t ws_bytes, int batch,
+             cudaStream_t st);
+
 // conv_tc.cu — tcgen05 implicit-GEMM convolutions (tf32 / bf16 operands)
 bool conv_tc_supported(int cin, int cout, int ks, int stride, int precision);
 long long conv_tc_pack_floats(int K, int N);

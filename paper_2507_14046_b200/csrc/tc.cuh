@@ -26,6 +26,18 @@ __device__ __forceinline__ uint64_t make_desc(uint32_t saddr, uint32_t lbo, uint
   return d;
 }
 
+// MN-major operand descriptor for 32-bit elements (layout type 1,
+// "128B_BASE32B"): one 128-byte row per K index holding 32 M/N elements in
+// four 32-byte granules, granule g of the row at smem address R stored at
+// granule g ^ ((R >> 7) & 3); K rows are 128 B apart (K blocks of 4 rows,
+// SBO = 512), blocks of 32 M/N elements are LBO apart. Measured on sm_100a
+// (tools/umma_probe.cu): the SWIZZLE_NONE / 128B / 64B / 32B MN-major forms
+// yield zeros for kind::tf32; this one is exact, also when the start address
+// is moved by any whole number of rows (base offset 0).
+__device__ __forceinline__ uint64_t make_desc_mn32(uint32_t saddr, uint32_t lbo) {
+  return make_desc(saddr, lbo, 512) | ((uint64_t)1 << 61);
+}
+
 // Instruction descriptor, dense, fp32 accumulate, A/B K-major.
 // a/b format: 0 f16, 1 bf16, 2 tf32.
 __host__ __device__ constexpr uint32_t make_idesc(int fmt, int M, int N) {

@@ -1,0 +1,441 @@
+// K3 on the tensor cores: weight + bias gradient of the stride-1 3^3 / 1^3
+// convolutions (autograd's conv backward w.r.t. weight/bias, pipeline.py:330)
+// as tcgen05 MMAs with 3xTF32 operands and FP32 accumulation in TMEM.
+//
+//   dW[co][ci][t] = sum_u x[u + off_t][ci] * gy[u][co]
+//
+// GEMM view: M = input channels (x side), N = output channels (gy side),
+// K = rows u of the same virtual zero-padded grid as the forward kernel
+// (conv_tc.cu), so a tap t is the constant row shift off_t. Both operands are
+// MN-major (K runs along the rows): each row of a 32-channel block is one
+// 128-byte line of shared memory in the "128B_BASE32B" layout (tc.cuh), so a
+// tap is a whole-row move of the x descriptor's start address -- no im2col.
+// Each CTA owns G taps (one kd plane, or a kh row of it) of one input-channel
+// block, keeps G accumulators [M x N] in TMEM, and streams its share of the
+// row chunks through a 2-stage cp.async ring (zero-fill outside the grid, so
+// border rows of the virtual grid contribute nothing). Partial sums per row
+// group are written to a workspace and summed in a fixed order
+// (deterministic). The bias gradient is a column sum of gy, accumulated by one
+// CTA column while it splits gy into TF32 hi/lo halves.
+//
+// Tap stacking (C_out <= 32): a tcgen05.mma costs ~57 cycles however small
+// its N (tools/umma_rate.cu), so the three kw taps of a (kd, kh) row go into
+// one MMA with N = 3 x 32. The kw shift moves to the gy side,
+//   sum_u x[u + s(kd,kh) + kw - 1] gy[u] = sum_u x[u + s(kd,kh)] gy[u + 1 - kw],
+// and B block b = 2 - kw is the gy tile started b rows later: LBO = one row.
+//
+// M is 64 or 128 (tcgen05 shapes): a channel block smaller than M is read
+// with LBO = 0 (one 32-channel block, repeated) or runs into a padded block;
+// those rows of D are never stored.
+#include <algorithm>
+
+#include "common.cuh"
+#include "kernels.h"
+#include "tc.cuh"
+
+namespace d2ip {
+
+constexpr int kWtThreads = 128;
+
+struct WgTc {
+  d2ip_act x, gy;
+  int Sw, Sh, u_first, u_last;
+  int RS;              // rows per stage (K chunk)
+  int WR;              // x window rows (RS + 2 Sw + 2 for 3^3, RS for 1^3)
+  int nchunk, chunks_per_rg, nrg;
+  int cib, ncib;       // input-channel block (M side), blocks
+  int M, N;            // MMA shape; N = C_out rounded up
+  int G, ngroups;      // taps per CTA, tap groups
+  int ntaps;           // 27 or 1
+  int stack;           // 1: the three kw taps of a (kd, kh) row share one MMA (N = 3 x 32, see below)
+  int RSg;             // gy rows per stage (RS, or RS + 2 with the kw halo)
+  int nchx, nchg;      // real 16-B chunks per row of the x block / of gy
+  uint32_t Bx, Bg;     // bytes of one 32-channel block region: WR x 128 / RS x 128, 1024-aligned
+  uint32_t lbox, lbog; // descriptor LBO (block stride, or 0 for a single repeated block)
+  uint32_t Sx, Sg;     // bytes of one x (hi or lo) / gy (hi or lo) buffer
+  uint32_t Sb;         // bytes of one stage
+  uint32_t pad;        // bytes after the stages covering MMA reads of padded blocks
+  int tmem_cols;
+  uint32_t idesc;
+  float* part;         // [b][rg][ntaps * Cin * Cout + Cout]
+};
+
+__device__ __forceinline__ float tf32_hi_w(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+
+__device__ __forceinline__ int wg_voxel(const WgTc& a, int u) {
+  if (u < a.u_first || u > a.u_last) return -1;
+  const int dp = u / a.Sh, r = u - dp * a.Sh;
+  const int hp = r / a.Sw, wp = r - hp * a.Sw;
+  if (dp >= 1 && dp <= a.x.d && hp >= 1 && hp <= a.x.h && wp >= 1 && wp <= a.x.w)
+    return ((dp - 1) * a.x.h + (hp - 1)) * a.x.w + (wp - 1);
+  return -1;
+}
+
+// byte offset of 16-B chunk c (4 channels) of row r in a region of 32-channel
+// blocks (block stride B): granule (c % 8) / 2 swizzled by r % 4 (regions are
+// 1024-byte aligned, so r % 4 == address bits 7-8).
+__device__ __forceinline__ uint32_t mn32_off(int r, int c, uint32_t B) {
+  const int cc = c & 7;
+  return (uint32_t)(c >> 3) * B + (uint32_t)r * 128 + (uint32_t)((((cc >> 1) ^ (r & 3)) << 5) | ((cc & 1) << 4));
+}
+
+// NCHXP / NCHGP: chunks per row rounded up to a power of two (lane -> (row, chunk)).
+template <int NCHXP, int NCHGP>
+__global__ void __launch_bounds__(kWtThreads) wgrad_tc_k(WgTc a) {
+  D2IP_PDL_ENTRY();
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int b = blockIdx.z;
+  const int rg = blockIdx.x;
+  const int grp = blockIdx.y % a.ngroups, cbk = blockIdx.y / a.ngroups;
+  const int t0 = grp * a.G;  // first tap of this CTA
+  const int kd = a.ntaps == 27 ? t0 / 9 : 1;
+  const bool do_bias = grp == 0 && cbk == 0;
+  const int RS = a.RS, WR = a.WR, RSg = a.RSg;
+  const d2ip_act x = a.x, gy = a.gy;
+  const float* xb = x.ptr + b * x.bstride + cbk * a.cib;
+  const float* gb = gy.ptr + b * gy.bstride;
+  // stage layout: [x hi][x lo][gy hi][gy lo] (1024-aligned regions); two stages,
+  // the read pad, mbarriers, TMEM slot, bias partials
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + 2 * a.Sb + a.pad);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(mbar + 2);
+  float4* bred = reinterpret_cast<float4*>(tslot + 4);  // [128] bias partials
+
+  if (warp == 0) tc::tmem_alloc(tslot, a.tmem_cols);
+  if (tid == 0) {
+    tc::mbar_init(&mbar[0], 1);
+    tc::mbar_init(&mbar[1], 1);
+    tc::fence_mbar_init();
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tslot;
+  const int c_lo = rg * a.chunks_per_rg, c_hi = min(a.nchunk, c_lo + a.chunks_per_rg);
+  const int S = c_hi - c_lo;
+  // x window row r <-> u0 + (kd-1) Sh - Sw - 1 + r (3^3), u0 + (kd-1) Sh - Sw + r
+  // (stacked: the kw shift lives on the gy side), u0 + r (1^3); gy row r <-> u0 - stack + r
+  const int xshift = a.ntaps == 27 ? (kd - 1) * a.Sh - a.Sw - (a.stack ? 0 : 1) : 0;
+  constexpr int XR = 32 / NCHXP, GR = 32 / NCHGP;  // rows per warp step
+  const int xr = lane / NCHXP, xc = lane % NCHXP, gr = lane / NCHGP, gc = lane % NCHGP;
+  float4 bacc = make_float4(0.f, 0.f, 0.f, 0.f);
+
+  auto load = [&](int sl, int buf) {
+    const int u0 = a.u_first + (c_lo + sl) * RS;
+    uint8_t* X = smem + buf * a.Sb;
+    uint8_t* Gt = X + 2 * a.Sx;
+    for (int r0 = warp * XR; r0 < WR; r0 += 4 * XR) {
+      const int r = r0 + xr;
+      if (r < WR && xc < a.nchx) {
+        const int v = wg_voxel(a, u0 + xshift + r);
+        const float* src = v >= 0 ? xb + (long long)v * x.cstride + 4 * xc : xb;
+        tc::cp_async16(X + mn32_off(r, xc, a.Bx), src, v >= 0 ? 16u : 0u);
+      }
+    }
+    for (int r0 = warp * GR; r0 < RSg; r0 += 4 * GR) {
+      const int r = r0 + gr;
+      if (r < RSg && gc < a.nchg) {
+        const int v = wg_voxel(a, u0 - a.stack + r);
+        const float* src = v >= 0 ? gb + (long long)v * gy.cstride + 4 * gc : gb;
+        tc::cp_async16(Gt + mn32_off(r, gc, a.Bg), src, v >= 0 ? 16u : 0u);
+      }
+    }
+    tc::cp_async_commit();
+  };
+  auto split4 = [](float4* hp, float4* lp) {
+    float4 v = *hp, h, l;
+    h.x = tf32_hi_w(v.x); h.y = tf32_hi_w(v.y); h.z = tf32_hi_w(v.z); h.w = tf32_hi_w(v.w);
+    l.x = v.x - h.x; l.y = v.y - h.y; l.z = v.z - h.z; l.w = v.w - h.w;
+    *hp = h;
+    *lp = l;
+    return v;
+  };
+  // same (row, chunk) ownership as load(): each thread splits what it copied
+  auto split = [&](int buf) {
+    uint8_t* X = smem + buf * a.Sb;
+    uint8_t* Gt = X + 2 * a.Sx;
+    for (int r0 = warp * XR; r0 < WR; r0 += 4 * XR) {
+      const int r = r0 + xr;
+      if (r < WR && xc < a.nchx) {
+        const uint32_t o = mn32_off(r, xc, a.Bx);
+        split4(reinterpret_cast<float4*>(X + o), reinterpret_cast<float4*>(X + a.Sx + o));
+      }
+    }
+    for (int r0 = warp * GR; r0 < RSg; r0 += 4 * GR) {
+      const int r = r0 + gr;
+      if (r < RSg && gc < a.nchg) {
+        const uint32_t o = mn32_off(r, gc, a.Bg);
+        const float4 v = split4(reinterpret_cast<float4*>(Gt + o), reinterpret_cast<float4*>(Gt + a.Sg + o));
+        if (do_bias && r >= a.stack && r < RS + a.stack) {  // the halo rows belong to the neighbour chunks
+          bacc.x += v.x; bacc.y += v.y; bacc.z += v.z; bacc.w += v.w;
+        }
+      }
+    }
+  };
+  const uint32_t sbase = tc::smem_u32(smem);
+  const uint64_t dXhi = tc::make_desc_mn32(sbase, a.lbox), dXlo = dXhi + (a.Sx >> 4);
+  const uint64_t dGhi = tc::make_desc_mn32(sbase + 2 * a.Sx, a.lbog), dGlo = dGhi + (a.Sg >> 4);
+
+  if (S > 0) load(0, 0);
+  for (int s = 0; s < S; ++s) {
+    const int buf = s & 1;
+    if (s + 1 < S) {
+      const int nb = (s + 1) & 1;
+      if (s + 1 >= 2) tc::mbar_wait(&mbar[nb], ((s - 1) >> 1) & 1);
+      load(s + 1, nb);
+      tc::cp_async_wait<1>();
+    } else {
+      tc::cp_async_wait<0>();
+    }
+    split(buf);
+    tc::fence_proxy_async();
+    __syncthreads();
+    if (tid == 0) {
+      tc::fence_after();
+      const uint64_t boff = buf ? (uint64_t)(a.Sb >> 4) : 0;
+      const int nacc = a.stack ? 3 : a.G;  // accumulators: kh rows (stacked) or taps
+      for (int i = 0; i < nacc; ++i) {
+        const int t = t0 + (a.stack ? 3 * i : i);
+        const int tt = a.ntaps == 27 ? t % 9 : 0;
+        const int rowoff = a.ntaps == 27 ? (tt / 3) * a.Sw + (a.stack ? 0 : tt % 3) : 0;
+        const uint32_t dcol = tmem + (uint32_t)(i * a.N);
+        for (int j = 0; j < RS / 8; ++j) {
+          // a row is 128 B = 8 descriptor units
+          const uint64_t xo = boff + (uint64_t)(rowoff + 8 * j) * 8;
+          const uint64_t go = boff + (uint64_t)(8 * j) * 8;
+          const uint32_t first = (s | j) ? 1u : 0u;
+          tc::mma_tf32(dcol, dXlo + xo, dGhi + go, a.idesc, first);
+          tc::mma_tf32(dcol, dXhi + xo, dGlo + go, a.idesc, 1u);
+          tc::mma_tf32(dcol, dXhi + xo, dGhi + go, a.idesc, 1u);
+        }
+      }
+      tc::commit(&mbar[buf]);
+    }
+  }
+  const int Cin = x.c, Cout = gy.c;
+  float* pb = a.part + ((long long)b * a.nrg + rg) * ((long long)a.ntaps * Cin * Cout + Cout);
+  if (do_bias) {  // fixed-order column sum of gy over this CTA's rows
+    bred[tid] = bacc;
+    __syncthreads();
+    if (tid < a.nchg) {
+      float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int q = 0; q < kWtThreads; ++q) {
+        if ((q & 31) % NCHGP != tid) continue;
+        const float4 v = bred[q];
+        sum.x += v.x; sum.y += v.y; sum.z += v.z; sum.w += v.w;
+      }
+      float* o = pb + (long long)a.ntaps * Cin * Cout + 4 * tid;
+      o[0] = sum.x; o[1] = sum.y; o[2] = sum.z; o[3] = sum.w;
+    }
+  }
+  if (S > 0) {
+    tc::mbar_wait(&mbar[(S - 1) & 1], ((S - 1) >> 1) & 1);
+    tc::fence_after();
+  }
+  // epilogue: D row m (input channel) lives in TMEM lane m (M = 128) or lane
+  // (m % 16) + 32 (m / 16) (M = 64); warp w reads its own 32-lane quadrant.
+  const int m = a.M == 128 ? warp * 32 + lane : (lane < 16 ? warp * 16 + lane : -1);
+  const int ci = cbk * a.cib + m;
+  const bool row_ok = m >= 0 && m < a.cib;
+  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+  const int nacc = a.stack ? 3 : a.G;
+  for (int i = 0; i < nacc; ++i) {
+    for (int blk = 0; blk < (a.stack ? 3 : 1); ++blk) {
+      // stacked: TMEM block blk of accumulator i is tap (kd, kh = i, kw = 2 - blk)
+      const int t = a.ntaps == 27 ? (a.stack ? t0 + 3 * i + (2 - blk) : t0 + i) : 0;
+      float* dst = pb + ((long long)t * Cin + ci) * Cout;
+      const int cb = a.stack ? blk * 32 : 0, cw = a.stack ? 32 : a.N;
+      for (int c0 = 0; c0 < cw && c0 < ((Cout + 7) & ~7); c0 += 8) {
+        float v[8];
+        tc::tmem_ld8(trow + (uint32_t)(i * a.N + cb + c0), v);
+        if (row_ok) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (c0 + j < Cout) dst[c0 + j] = S > 0 ? v[j] : 0.f;
+        }
+      }
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_free(tmem, a.tmem_cols);
+}
+
+// Sum over row groups (fixed order) and scatter into OIDHW weight + bias grads.
+// Thread e walks the partial layout [t][ci][co] (co fastest: coalesced reads).
+__global__ void __launch_bounds__(256) wgrad_tc_reduce_k(const float* __restrict__ part, int nrg, int ntaps,
+                                                         int Cin, int Cout, float* __restrict__ out, long long obs) {
+  D2IP_PDL_ENTRY();
+  const int b = blockIdx.y;
+  const long long nw = (long long)ntaps * Cin * Cout, n = nw + Cout;
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= n) return;
+  const float* p = part + (long long)b * nrg * n + e;
+  float s0 = 0.f, s1 = 0.f;
+  int r = 0;
+  for (; r + 1 < nrg; r += 2) {
+    s0 += p[(long long)r * n];
+    s1 += p[(long long)(r + 1) * n];
+  }
+  if (r < nrg) s0 += p[(long long)r * n];
+  const float s = s0 + s1;
+  long long o;
+  if (e < nw) {
+    const int co = (int)(e % Cout);
+    const long long q = e / Cout;
+    const int ci = (int)(q % Cin), t = (int)(q / Cin);
+    o = ((long long)co * Cin + ci) * ntaps + t;
+  } else {
+    o = nw + (e - nw);
+  }
+  out[b * obs + o] = s;
+}
+
+static int pow2_at_least(int v) {
+  int p = 1;
+  while (p < v) p *= 2;
+  return p;
+}
+
+static uint32_t align1k(size_t v) { return (uint32_t)((v + 1023) & ~(size_t)1023); }
+
+static bool wt_plan(int D, int H, int W, int Cin, int Cout, int ks, int batch, WgTc& a) {
+  if (Cin % 4 || Cout % 4 || Cin < 4 || Cout > 128 || (ks != 1 && ks != 3)) return false;
+  a.ntaps = ks == 3 ? 27 : 1;
+  a.Sw = W + 2;
+  a.Sh = (H + 2) * a.Sw;
+  a.u_first = a.Sh + a.Sw + 1;
+  a.u_last = D * a.Sh + H * a.Sw + W;
+  // input-channel block: <= 128, equal blocks, multiple of 4
+  a.ncib = (Cin + 127) / 128;
+  while (Cin % a.ncib || (Cin / a.ncib) % 4) ++a.ncib;
+  a.cib = Cin / a.ncib;
+  a.M = a.cib <= 64 ? 64 : 128;
+  a.stack = (ks == 3 && Cout <= 32) ? 1 : 0;
+  if (a.stack) {
+    a.N = 96;  // 3 kw taps x one 32-channel block
+    a.G = 9;   // one kd plane: 3 accumulators of 96 columns
+  } else {
+    a.N = (Cout + 15) / 16 * 16;
+    if (a.M == 64 && Cout <= 8) a.N = 8;
+    // taps per CTA: as many of a kd plane as fit 512 TMEM columns
+    a.G = ks == 1 ? 1 : (9 * a.N <= 512 ? 9 : (3 * a.N <= 512 ? 3 : 1));
+  }
+  a.ngroups = a.ntaps / a.G;
+  a.tmem_cols = std::max(32, pow2_at_least((a.stack ? 3 : a.G) * a.N));
+  if (a.tmem_cols > 512) return false;
+  a.nchx = a.cib / 4;
+  a.nchg = Cout / 4;
+  const int nbx = (a.cib + 31) / 32, nbg = (Cout + 31) / 32;  // real 32-channel blocks
+  const int mbx = a.M / 32;                                    // blocks the MMA reads
+  // rows per stage: largest that fits two stages (+ read pad) in 220 KB
+  a.RS = 0;
+  for (int rs : {128, 64, 32}) {
+    const int wr = ks == 3 ? rs + 2 * a.Sw + (a.stack ? 0 : 2) : rs;
+    const int rsg = rs + 2 * a.stack;
+    // block strides stay multiples of 512 B so a row's swizzle phase (address bits 7-8) is r % 4 in every block
+    const uint32_t bx = align1k((size_t)wr * 128), bg = align1k((size_t)rsg * 128);
+    const uint32_t sx = align1k((size_t)nbx * bx), sg = align1k((size_t)nbg * bg);
+    const uint32_t sb = 2 * (sx + sg);
+    // one real block is read with LBO = 0; otherwise the MMA runs mbx - nbx blocks past the x lo region
+    const uint32_t pad = (nbx == 1 || nbx == mbx) ? 0 : align1k((size_t)(mbx - nbx) * bx);
+    const size_t total = 2 * (size_t)sb + pad + 64 + 128 * 16 + 64;
+    if (total <= (size_t)220 * 1024) {
+      a.RS = rs;
+      a.RSg = rsg;
+      a.WR = wr;
+      a.Bx = bx;
+      a.Bg = bg;
+      a.Sx = sx;
+      a.Sg = sg;
+      a.Sb = sb;
+      a.pad = pad;
+      a.lbox = nbx == 1 ? 0 : bx;
+      a.lbog = a.stack ? 128 : (nbg == 1 ? 0 : bg);
+      break;
+    }
+  }
+  if (!a.RS) return false;
+  a.nchunk = cdiv(a.u_last - a.u_first + 1, a.RS);
+  // row groups: ~1 CTA per SM overall, >= 2 chunks each when there are enough
+  const long long jobs = (long long)a.ngroups * a.ncib * batch;
+  int nrg = (int)std::max(1LL, (148LL + jobs - 1) / jobs);
+  nrg = std::min(nrg, std::max(1, a.nchunk / 2));
+  a.chunks_per_rg = cdiv(a.nchunk, nrg);
+  a.nrg = cdiv(a.nchunk, a.chunks_per_rg);
+  a.idesc = tc::make_idesc(2, a.M, a.N) | (1u << 15) | (1u << 16);  // A and B MN-major
+  return true;
+}
+
+static size_t wt_smem(const WgTc& a) { return 2 * (size_t)a.Sb + a.pad + 64 + 128 * 16 + 64; }
+
+bool wgrad_tc_supported(d2ip_act x, d2ip_act gy, int ks, int precision) {
+  if (precision != D2IP_PREC_TF32) return false;
+  if (x.d != gy.d || x.h != gy.h || x.w != gy.w) return false;
+  if (x.cstride % 4 || gy.cstride % 4 || ((uintptr_t)x.ptr & 15) || ((uintptr_t)gy.ptr & 15)) return false;
+  WgTc a{};
+  if (!wt_plan(x.d, x.h, x.w, x.c, gy.c, ks, 1, a)) return false;
+  const int nchxp = pow2_at_least(a.nchx), nchgp = pow2_at_least(a.nchg);
+  return nchxp <= 32 && nchgp <= 32 && (nchxp == 1 || nchxp == 2 || nchxp == 4 || nchxp == 8 || nchxp == 16 || nchxp == 32);
+}
+
+size_t wgrad_tc_ws_bytes(int D, int H, int W, int Cin, int Cout, int ks, int batch) {
+  WgTc a{};
+  if (!wt_plan(D, H, W, Cin, Cout, ks, batch, a)) return 0;
+  return (size_t)batch * a.nrg * ((size_t)a.ntaps * Cin * Cout + Cout) * sizeof(float);
+}
+
+template <int NX, int NG>
+static int wt_launch(const WgTc& a, dim3 grid, size_t smem, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    D2IP_CUDA(cudaFuncSetAttribute(wgrad_tc_k<NX, NG>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    attr = true;
+  }
+  D2IP_CUDA(launch_pdl((wgrad_tc_k<NX, NG>), grid, kWtThreads, smem, st, a));
+  return D2IP_OK;
+}
+
+template <int NX>
+static int wt_launch_g(const WgTc& a, int ng, dim3 grid, size_t smem, cudaStream_t st) {
+  switch (ng) {
+    case 1: return wt_launch<NX, 1>(a, grid, smem, st);
+    case 2: return wt_launch<NX, 2>(a, grid, smem, st);
+    case 4: return wt_launch<NX, 4>(a, grid, smem, st);
+    case 8: return wt_launch<NX, 8>(a, grid, smem, st);
+    case 16: return wt_launch<NX, 16>(a, grid, smem, st);
+    case 32: return wt_launch<NX, 32>(a, grid, smem, st);
+  }
+  D2IP_CHECK_ARG(false, "wgrad_tc: C_out chunks %d unsupported", ng);
+  return D2IP_E_ARG;
+}
+
+int wgrad_tc(d2ip_act x, d2ip_act gy, int ks, float* gw, long long gwbs, void* ws, size_t ws_bytes, int batch,
+             cudaStream_t st) {
+  WgTc a{};
+  D2IP_CHECK_ARG(wt_plan(x.d, x.h, x.w, x.c, gy.c, ks, batch, a), "wgrad_tc: unsupported shape");
+  D2IP_CHECK_ARG(ws_bytes >= wgrad_tc_ws_bytes(x.d, x.h, x.w, x.c, gy.c, ks, batch), "wgrad_tc: workspace too small");
+  a.x = x;
+  a.gy = gy;
+  a.part = reinterpret_cast<float*>(ws);
+  const size_t smem = wt_smem(a);
+  const dim3 grid(a.nrg, a.ngroups * a.ncib, batch);
+  const int nx = pow2_at_least(a.nchx), ng = pow2_at_least(a.nchg);
+  switch (nx) {
+    case 1: D2IP_RET(wt_launch_g<1>(a, ng, grid, smem, st)); break;
+    case 2: D2IP_RET(wt_launch_g<2>(a, ng, grid, smem, st)); break;
+    case 4: D2IP_RET(wt_launch_g<4>(a, ng, grid, smem, st)); break;
+    case 8: D2IP_RET(wt_launch_g<8>(a, ng, grid, smem, st)); break;
+    case 16: D2IP_RET(wt_launch_g<16>(a, ng, grid, smem, st)); break;
+    case 32: D2IP_RET(wt_launch_g<32>(a, ng, grid, smem, st)); break;
+    default: D2IP_CHECK_ARG(false, "wgrad_tc: C_in chunks %d unsupported", nx);
+  }
+  D2IP_LAUNCH_CHECK();
+  const long long n = (long long)a.ntaps * x.c * gy.c + gy.c;
+  D2IP_CUDA(launch_pdl(wgrad_tc_reduce_k, dim3(cdiv(n, 256), batch), 256, 0, st, a.part, a.nrg, a.ntaps, x.c, gy.c,
+                       gw, gwbs));
+  D2IP_LAUNCH_CHECK();
+  return D2IP_OK;
+}
+
+}  // namespace d2ip

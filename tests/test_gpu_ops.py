@@ -18,7 +18,7 @@ from paper_2507_14046_b200 import _native as N
 
 pytestmark = pytest.mark.gpu
 
-TOL = {"fp32": 1e-5, "tf32": 1e-4, "bf16": 1e-2}
+TOL = {"fp32": 1e-5, "tf32": 1e-4, "bf16": 1e-2}  # tf32 = 3xTF32 (~2.5e-5 at K=5184: RZ accumulation)
 
 
 def rel(a, b):
@@ -106,9 +106,17 @@ def test_conv3d_fwd(cin, cout, ks, stride, sp, prec):
     assert rel(from_ndhwc(out), ref2) < TOL[prec]
 
 
+@pytest.fixture(params=[0, 1], ids=["wg_cuda", "wg_tcgen05"])
+def wgrad_variant(request):
+    L = N.lib()
+    N.check(L.d2ip_set_wgrad_variant(request.param), "set_wgrad_variant")
+    yield request.param
+    L.d2ip_set_wgrad_variant(0)
+
+
 @pytest.mark.parametrize("prec", ["fp32", "tf32"])
 @pytest.mark.parametrize("cin,cout,ks,stride,sp", CONV_CASES)
-def test_conv3d_dgrad_wgrad(cin, cout, ks, stride, sp, prec):
+def test_conv3d_dgrad_wgrad(cin, cout, ks, stride, sp, prec, wgrad_variant):
     torch.manual_seed(1)
     B = 2
     x = torch.randn(B, cin, *sp, requires_grad=True)
@@ -132,6 +140,8 @@ def test_conv3d_dgrad_wgrad(cin, cout, ks, stride, sp, prec):
     N.check(N.lib().d2ip_conv3d_wgrad(act_of(xd), act_of(gyd), ks, stride, C.c_void_p(gw.data_ptr()), P,
                                       C.c_void_p(ws.data_ptr()), ws_n, N.PREC[prec], B, stream()), "wgrad")
     torch.cuda.synchronize()
+    if wgrad_variant == 1 and prec == "tf32" and stride == 1 and cin % 4 == 0 and cout % 4 == 0 and cout <= 128:
+        assert N.lib().d2ip_last_variant() == b"wgrad_tcgen05_tf32x3"
     assert rel(from_ndhwc(gx), x.grad) < TOL[prec]
     ref_gw = torch.cat([torch.cat([w.grad[i].reshape(-1), b.grad[i]]) for i in range(B)]).reshape(B, P)
     nW = cout * cin * ks ** 3
