@@ -98,6 +98,7 @@ static void config_plan_workspace(d2ip_engine& E, Arena& A) {
   E.stem_xh = takef((long long)B * E.V[0] * c[0]);
   E.stem_rs = takef((long long)B * E.V[0]);
   E.stem_gc = takef((long long)B * E.V[0] * c[0]);
+  E.stem_np = reinterpret_cast<float*>(A.take(norm_act_bwd_ws(E.V[0], c[0], B)));
   long long maxvc = E.V[0] * c[0];
   auto saved = [&](Block& bl) {
     const long long vc = E.V[bl.lout] * bl.c1.cout;
@@ -110,6 +111,8 @@ static void config_plan_workspace(d2ip_engine& E, Arena& A) {
     bl.gpre = takef(B * vc);
     bl.gc2 = takef(B * vc);
     bl.gc1 = takef(B * vc);
+    bl.np1 = reinterpret_cast<float*>(A.take(norm_act_bwd_ws(E.V[bl.lout], bl.c1.cout, B)));
+    bl.np2 = reinterpret_cast<float*>(A.take(norm_act_bwd_ws(E.V[bl.lout], bl.c1.cout, B)));
   };
   for (auto& bl : E.enc) saved(bl);
   saved(E.neck);
@@ -256,10 +259,15 @@ int cwgrad(Ctx& k, const ConvP& c, d2ip_act x, d2ip_act gy) {
   return conv_wgrad(x, gy, c.ks, c.stride, k.gr() + c.ow, k.pbs, k.E.wg_ws, k.E.wg_ws_bytes, k.prec, k.B, k.st);
 }
 
-int fork_side(Ctx& k) {
+int fork_to(Ctx& k, cudaStream_t from, cudaStream_t to) {
   cudaEvent_t e = k.E.ev[k.E.evi++ % d2ip_engine::kEvents];
-  D2IP_CUDA(cudaEventRecord(e, k.st));
-  D2IP_CUDA(cudaStreamWaitEvent(k.side, e, 0));
+  D2IP_CUDA(cudaEventRecord(e, from));
+  D2IP_CUDA(cudaStreamWaitEvent(to, e, 0));
+  return D2IP_OK;
+}
+
+int fork_side(Ctx& k) {
+  D2IP_RET(fork_to(k, k.st, k.side));
   k.forked = true;
   return D2IP_OK;
 }
@@ -315,15 +323,28 @@ static int block_fwd(Ctx& k, Block& bl) {
   d2ip_act raw2 = view(E, E.raw2, bl.lout, co, co);
   d2ip_act h1 = view(E, bl.h1, bl.lout, co, co);
   d2ip_act none{};
+  // 1^3 skip (direct kernel) on side2, beside the conv1 -> norm1 -> conv2 chain
+  D2IP_RET(fork_to(k, k.st, k.side2));
+  {
+    Ctx k2 = k;
+    k2.st = k.side2;
+    D2IP_RET(cfwd(k2, bl.sk, bl.x, raw2, 0));
+  }
   SplitK sk;
   D2IP_RET(cfwd(k, bl.c1, bl.x, raw, 0, &sk));
   D2IP_RET(norm_act_fwd(raw, k.th() + bl.n1.og, k.th() + bl.n1.ob, k.pbs, none, 1, k.slope, h1, bl.xh1, bl.rs1, k.B,
                         k.st, sk));
   D2IP_RET(cfwd(k, bl.c2, h1, raw, 0, &sk));
-  D2IP_RET(cfwd(k, bl.sk, bl.x, raw2, 0));  // 1^3 skip: direct kernel, leaves the split-K partials intact
+  D2IP_RET(fork_to(k, k.side2, k.st));  // join the skip before the residual add
   D2IP_RET(norm_act_fwd(raw, k.th() + bl.n2.og, k.th() + bl.n2.ob, k.pbs, raw2, 1, k.slope, bl.out, bl.xh2, bl.rs2,
                         k.B, k.st, sk));
   return D2IP_OK;
+}
+
+// Side-stream sum of a norm's dgamma/dbeta partials (per-norm buffer `np`).
+static int dgb_side(Ctx& k, const float* np, int nb, int C, long long og) {
+  D2IP_RET(fork_side(k));
+  return reduce_chunks(np, nb, 2 * C, k.gr() + og, k.pbs, k.B, k.side);
 }
 
 static int block_bwd(Ctx& k, Block& bl) {
@@ -331,23 +352,38 @@ static int block_bwd(Ctx& k, Block& bl) {
   const int co = bl.c1.cout;
   auto S = [&](int i) { return view(E, E.sc[i], bl.lout, co, co); };
   auto P = [&](float* p) { return view(E, p, bl.lout, co, co); };
-  // gpre / gc2 / gc1 feed the side-stream weight gradients: per-block buffers
+  // gpre / gc2 / gc1 feed the side-stream kernels: per-block buffers
   d2ip_act gpre = P(bl.gpre), gc2 = P(bl.gc2), gh1 = S(2), gpre1 = S(3), gc1 = P(bl.gc1);
   d2ip_act h1 = view(E, bl.h1, bl.lout, co, co);
+  const size_t npb = norm_act_bwd_ws(E.V[bl.lout], co, k.B);
+  int nb = 0;
   D2IP_RET(norm_act_bwd(bl.gout, bl.out, 1, k.slope, bl.xh2, bl.rs2, k.th() + bl.n2.og, k.pbs, gpre, gc2,
-                        k.gr() + bl.n2.og, k.pbs, E.na_ws, E.na_ws_bytes, k.B, k.st));
-  D2IP_RET(cwgrad_side(k, bl.c2, h1, gc2));
-  D2IP_RET(cdgrad(k, bl.c2, gc2, gh1, 0));
-  D2IP_RET(norm_act_bwd(gh1, h1, 1, k.slope, bl.xh1, bl.rs1, k.th() + bl.n1.og, k.pbs, gpre1, gc1,
-                        k.gr() + bl.n1.og, k.pbs, E.na_ws, E.na_ws_bytes, k.B, k.st));
-  D2IP_RET(cwgrad_side(k, bl.c1, bl.x, gc1));
+                        k.gr() + bl.n2.og, k.pbs, bl.np2, npb, k.B, k.st, &nb));
+  D2IP_RET(dgb_side(k, bl.np2, nb, co, bl.n2.og));
   {
-    Ctx ks = k;  // already ordered after gpre by the fork above
+    Ctx ks = k;  // side: weight gradients (ordered after gpre / gc2 by the fork above)
     ks.st = k.side;
+    D2IP_RET(cwgrad(ks, bl.c2, h1, gc2));
     D2IP_RET(cwgrad(ks, bl.sk, bl.x, gpre));
   }
-  D2IP_RET(cdgrad(k, bl.c1, gc1, bl.gx, bl.gx_acc));
-  D2IP_RET(cdgrad(k, bl.sk, gpre, bl.gx, 1));
+  // side2: the 1^3 skip's data gradient writes gx first; conv1's accumulates after the join
+  D2IP_RET(fork_to(k, k.st, k.side2));
+  {
+    Ctx k2 = k;
+    k2.st = k.side2;
+    D2IP_RET(cdgrad(k2, bl.sk, gpre, bl.gx, bl.gx_acc));
+  }
+  D2IP_RET(cdgrad(k, bl.c2, gc2, gh1, 0));
+  D2IP_RET(norm_act_bwd(gh1, h1, 1, k.slope, bl.xh1, bl.rs1, k.th() + bl.n1.og, k.pbs, gpre1, gc1,
+                        k.gr() + bl.n1.og, k.pbs, bl.np1, npb, k.B, k.st, &nb));
+  D2IP_RET(dgb_side(k, bl.np1, nb, co, bl.n1.og));
+  {
+    Ctx ks = k;  // ordered after gc1 by dgb_side's fork
+    ks.st = k.side;
+    D2IP_RET(cwgrad(ks, bl.c1, bl.x, gc1));
+  }
+  D2IP_RET(fork_to(k, k.side2, k.st));
+  D2IP_RET(cdgrad(k, bl.c1, gc1, bl.gx, 1));
   return D2IP_OK;
 }
 
@@ -437,10 +473,16 @@ static int backward(Ctx& k) {
   d2ip_act ga0 = view(E, E.gcat[0] + c[1], 0, c[0], E.catw[0]);
   d2ip_act gpre = view(E, E.sc[0], 0, c[0], c[0]);
   d2ip_act gc = view(E, E.stem_gc, 0, c[0], c[0]);
+  int nb = 0;
   D2IP_RET(norm_act_bwd(ga0, a0, 1, k.slope, E.stem_xh, E.stem_rs, k.th() + E.stem_n.og, k.pbs, gpre, gc,
-                        k.gr() + E.stem_n.og, k.pbs, E.na_ws, E.na_ws_bytes, k.B, k.st));
+                        k.gr() + E.stem_n.og, k.pbs, E.stem_np, norm_act_bwd_ws(E.V[0], c[0], k.B), k.B, k.st, &nb));
+  D2IP_RET(dgb_side(k, E.stem_np, nb, c[0], E.stem_n.og));
   d2ip_act z = view(E, const_cast<float*>(E.b.z), 0, E.d.in_channels, E.d.in_channels);
-  D2IP_RET(cwgrad_side(k, E.stem, z, gc));
+  {
+    Ctx ks = k;  // ordered after gc by dgb_side's fork
+    ks.st = k.side;
+    D2IP_RET(cwgrad(ks, E.stem, z, gc));
+  }
   return join_side(k);
 }
 
@@ -451,7 +493,7 @@ static int adam(Ctx& k) {
 }
 
 static Ctx ctx(d2ip_engine& E, void* stream) {
-  return Ctx{E, S(stream), E.d.batch, E.nparams, E.d.precision, E.d.negative_slope, E.side, false};
+  return Ctx{E, S(stream), E.d.batch, E.nparams, E.d.precision, E.d.negative_slope, E.side, false, E.side2};
 }
 
 int engine_step(d2ip_engine& E, void* stream) {
@@ -595,6 +637,7 @@ void d2ip_engine_destroy(d2ip_engine* e) {
   d2ip::refnet_destroy(*e);
   if (e->cap_stream) cudaStreamDestroy(e->cap_stream);
   if (e->side) cudaStreamDestroy(e->side);
+  if (e->side2) cudaStreamDestroy(e->side2);
   for (auto ev : e->ev)
     if (ev) cudaEventDestroy(ev);
   delete e;
@@ -616,6 +659,7 @@ int d2ip_engine_bind(d2ip_engine* e, const d2ip_bindings* b) {
   drop_graph(*e);
   if (!e->side) {
     D2IP_CUDA(cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking));
+    D2IP_CUDA(cudaStreamCreateWithFlags(&e->side2, cudaStreamNonBlocking));
     for (auto& ev : e->ev) D2IP_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   }
   e->b = *b;

@@ -32,6 +32,7 @@ struct Block {
   // backward: gradients read by the weight-gradient kernels on the side stream
   // (per block, so the next block's backward cannot overwrite them early)
   float *gpre = nullptr, *gc2 = nullptr, *gc1 = nullptr;
+  float *np1 = nullptr, *np2 = nullptr;  // per-norm dgamma/dbeta partials, reduced on the side stream
 };
 
 }  // namespace d2ip
@@ -75,10 +76,12 @@ struct d2ip_engine {
   int launches = 0;
   // weight gradients run on a side stream, off the data-gradient critical path
   cudaStream_t side = nullptr;
+  cudaStream_t side2 = nullptr;  // short data-gradient branches (1^3 skip) beside the main chain
   static constexpr int kEvents = 128;
   cudaEvent_t ev[kEvents]{};
   int evi = 0;
   float* stem_gc = nullptr;
+  float* stem_np = nullptr;
   d2ip::RefNet* ref = nullptr;  // arch == 1: FastResUNet3D program (refnet.cu)
 };
 
@@ -120,6 +123,7 @@ struct Ctx {
   float slope;
   cudaStream_t side;  // weight-gradient stream (forked from / joined into st)
   bool forked = false;  // side stream holds work of this pass (join only then: capture rules)
+  cudaStream_t side2;
   float* th() const { return E.b.theta; }
   float* gr() const { return E.b.grad; }
 };
@@ -128,6 +132,8 @@ struct Ctx {
 // is enqueued on side next) and the reverse join.
 int fork_side(Ctx& k);
 int join_side(Ctx& k);
+// generic fork / join between two streams (graph-capture safe)
+int fork_to(Ctx& k, cudaStream_t from, cudaStream_t to);
 // weight gradient on the side stream, after everything already on st
 int cwgrad_side(Ctx& k, const ConvP& c, d2ip_act x, d2ip_act gy);
 

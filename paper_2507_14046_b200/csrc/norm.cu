@@ -245,7 +245,7 @@ size_t norm_act_bwd_ws(long long V, int C, int batch) {
 
 int norm_act_bwd(d2ip_act gout, d2ip_act out, int act, float slope, const float* xhat, const float* rstd,
                  const float* gamma, long long pbs, d2ip_act gpre, d2ip_act gc, float* dgb, long long dgbs, void* ws,
-                 size_t ws_bytes, int batch, cudaStream_t st) {
+                 size_t ws_bytes, int batch, cudaStream_t st, int* deferred) {
   const int C = gout.c;
   D2IP_CHECK_ARG(C % 4 == 0 && C <= 256, "norm_act_bwd: C=%d must be a multiple of 4, <= 256", C);
   D2IP_CHECK_ARG(gout.cstride % 4 == 0 && gc.cstride % 4 == 0 && (!act || out.cstride % 4 == 0) &&
@@ -265,6 +265,10 @@ int norm_act_bwd(d2ip_act gout, d2ip_act out, int act, float slope, const float*
     D2IP_CUDA(launch_pdl(norm_act_bwd_k<8>, grid, kNormThreads, smem, st, gout, out, act, slope, xhat, rstd, gamma, pbs, gpre, gc,
                                                         partial, g.G));
   D2IP_LAUNCH_CHECK();
+  if (deferred) {  // the caller sums the dgamma / dbeta partials (reduce_chunks) where it likes
+    *deferred = nb;
+    return D2IP_OK;
+  }
   return reduce_chunks(partial, nb, 2 * C, dgb, dgbs, batch, st);
 }
 
