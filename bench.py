@@ -184,6 +184,22 @@ def run_gpu(args):
             dn.set_theta(kaiming_flat(net, seed=s + 1), b=b)
             dn.set_dv(wl.voltages.frames[0].values, b=b)
         units_per_step = len(mine)
+    elif spec.n_measurements * int(np.prod(spec.grid)) > 64 * 1024 * 1024:
+        # cfg2 / cfg4: J (GB-sized) synthesised on the GPU, never on the host
+        J_dev, mask, dv_dev, omap = W.device_frame(spec, seed)
+        wl = None
+        net = spec.network(seed=seed + 1)
+        grid = spec.geometry()
+        noise = sample_noise_input(grid, seed, spec.in_channels, 0.1)
+        dn = DeviceNet(net, grid.shape, J_dev.shape[0], mask, data_norm="l2sq", output_map=omap,
+                       lr=spec.learning_rate, precision=args.precision or spec.precision,
+                       max_iters=args.warmup + args.steps + 8)
+        dn.set_noise(noise.values)
+        dn.set_J_device(J_dev)
+        del J_dev
+        dn.set_theta(kaiming_flat(net))
+        dn.dv[0, 0].copy_(dv_dev)
+        units_per_step = 1
     else:
         wl = W.make_workload(spec, seed=seed, frames=min(spec.frames, 20))
         net = spec.network(seed=seed + 1)
@@ -273,7 +289,7 @@ def run_gpu(args):
 
     # --- e2e through the public API (rank-local, one full sequence)
     e2e = None
-    if not args.skip_e2e and units_per_step == 1:
+    if not args.skip_e2e and units_per_step == 1 and wl is not None:
         e2e = run_e2e(spec, wl, args, ws)
 
     out = {
@@ -309,6 +325,11 @@ def run_gpu(args):
         dist.destroy_process_group()
 
 
+# dense TF32 tensor peak measured with tools/umma_rate.cu (148 SMs x 2 CTAs,
+# M=128 N=256 kind::tf32 MMAs): 1104.5 TFLOP/s (profiles/r1_umma_rate.txt)
+TF32_PEAK_TFLOPS = 1104.5
+
+
 def conv_probe(L, N, C, st, pk, pk_kind, flush, t_flush):
     """One launch of the tcgen05 conv on cfg1's dec0.conv1 shape (48 -> 16 @ 32^3),
     timed with CUDA events; algorithmic FLOPs = 2*27*Cin*Cout*V."""
@@ -335,12 +356,13 @@ def conv_probe(L, N, C, st, pk, pk_kind, flush, t_flush):
                                   3, 1, ya, 0, N.PREC["tf32"], C.c_void_p(ws.data_ptr()), wsn, 1, st), "conv")
     t = max(time_kernel(run) - t_flush, 1e-9)
     flops = 2.0 * 27 * cin * cout * D ** 3
-    peak = pk.get("bf16_tflops", 1590.0) / 2  # dense TF32 = 1/2 bf16 (no measured TF32 peak)
+    peak = TF32_PEAK_TFLOPS
     return {"bound": "tensor", "kernel": "conv_tc_k (K1, tcgen05 3xTF32 implicit GEMM) incl. weight pack",
             "layer": "dec0.conv1 48->16 @ 32^3", "achieved": round(flops / t / 1e12, 2), "peak": peak,
             "unit": "TFLOP/s", "frac": round(flops / t / 1e12 / peak, 4), "traffic": None,
             "algorithmic_flops_per_launch": flops, "avg_launch_s": t,
-            "peak_source": f"{pk_kind} bf16 burst / 2 (TF32 dense); 3xTF32 issues 3 MMAs per product"}
+            "peak_source": "measured dense kind::tf32 tcgen05.mma peak on this pool's B200 (profiles/r1_umma_rate.txt); "
+                           "3xTF32 issues 3 MMAs per product"}
 
 
 def run_e2e(spec, wl, args, ws):

@@ -145,6 +145,21 @@ size_t d2ip_jac_adj_ws_bytes(int m, int vp, int batch);
 int d2ip_adam(float* p, const float* g, float* m, float* v, long long n, float lr, float beta1,
               float beta2, float eps, const int* step, void* stream);
 
+/* ---- Sensitivity operator assembly ---------------------
+ * Replaces assemble_sensitivity + normalize_sensitivity
+ * (pkg/src/d2ip/forward.py:58-112) on the device, fp64:
+ *   out[m][q] = -(f_d+ - f_d-).(f_m+ - f_m-) * voxel_volume,
+ *   f_e(q) = -(c_q - p_e) / (4 pi max(|c_q - p_e|, min_dist)^3),
+ * centers [Q][3] (canonical q order), electrodes [E][3], quads int32 [M][4]
+ * (16-byte aligned), norms[m] = ||out[m]||_2. normalize != 0 divides every row
+ * by its norm in place (the caller rejects zero rows, forward.py:103-106).
+ * J_masked (optional): fp32 [M][Vp] block, column j = voxel q_of_col[j] (the
+ * engine's memory column order), zero padded -- the fp64 operator never needs
+ * to visit the host. */
+int d2ip_assemble_sensitivity(const double* centers, int Q, const double* electrodes, int E, const int* quads, int M,
+                              double min_dist, double voxel_volume, int normalize, double* out, double* norms,
+                              float* J_masked, int V, int Vp, const int* q_of_col, void* stream);
+
 /* ---- Engine: one whole DIP iteration, graph-captured --------------------
  * Owns the launch plan of one network program (`arch`: the canonical config
  * ResUNet of SURVEY §7.1, or the reference's FastResUNet3D with levels = 4,

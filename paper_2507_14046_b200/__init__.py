@@ -33,6 +33,16 @@ from .priornet import (  # noqa: F401
     save_checkpoint,
 )
 from .regularizers import FrameHistory, TVWeights, decay_weight  # noqa: F401
+from .sensitivity import (  # noqa: F401
+    assemble_masked_device,
+    assemble_sensitivity,
+    load_matrix,
+    load_matrix_device,
+    load_voltages,
+    normalize_sensitivity,
+    save_matrix,
+    save_voltages,
+)
 from .pipeline import (  # noqa: F401
     LossTrace,
     ReconstructionResult,

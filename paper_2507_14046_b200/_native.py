@@ -100,6 +100,9 @@ _SIGS = {
     "d2ip_last_error": (C.c_char_p, []),
     "d2ip_last_variant": (C.c_char_p, []),
     "d2ip_set_wgrad_variant": (C.c_int, [C.c_int]),
+    "d2ip_assemble_sensitivity": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_int,
+                                            C.c_double, C.c_double, C.c_int, C.c_void_p, C.c_void_p, C.c_void_p,
+                                            C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
     "d2ip_conv3d_ws_bytes": (C.c_size_t, [C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int]),
     "d2ip_conv3d_fwd": (C.c_int, [Act, C.c_void_p, C.c_void_p, C.c_longlong, C.c_int, C.c_int, Act, C.c_int,
                                   C.c_int, C.c_void_p, C.c_size_t, C.c_int, C.c_void_p]),

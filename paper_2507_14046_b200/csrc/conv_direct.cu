@@ -422,10 +422,13 @@ struct DirectPlan {
 // `live_taps`: taps that actually contribute per output voxel (27, or ~27/8
 // for the data gradient of a stride-2 convolution, where only taps of matching
 // parity land on a given input voxel) -- the serial chain the split shortens.
-static DirectPlan direct_plan(long long V, int C, int ks, int batch, int live_taps) {
+static DirectPlan direct_plan(long long V, int C, int ks, int batch, int live_taps, int Cred) {
   DirectPlan p;
   const bool small = V * (C / 8 + 1) * batch < 296LL * 128;
   p.cg = (C % 8 == 0 && !small) ? 8 : (C % 4 == 0 ? 4 : 1);
+  // the Cred x k^3 x CG weight slice must fit shared memory (wide decoder inputs at cfg4)
+  const long long k3 = (long long)ks * ks * ks;
+  while (p.cg > 1 && Cred * k3 * p.cg * 4 + 288LL * p.cg * 4 > 200LL * 1024) p.cg = p.cg == 8 ? 4 : 1;
   const long long base = V * (C / p.cg) * batch;  // threads without a tap split
   p.S = 1;
   if (ks == 3 && live_taps >= 27) p.S = base < 48LL * 1024 ? 9 : (base < 128LL * 1024 ? 3 : 1);
@@ -440,7 +443,7 @@ int conv_fwd_direct(d2ip_act x, const float* w, const float* bias, long long wbs
                     d2ip_act y, int accumulate, int batch, cudaStream_t st, int dil) {
   const long long V = (long long)y.d * y.h * y.w;
   const int vec = vec_ok(x) ? 1 : 0;
-  const DirectPlan p = direct_plan(V, y.c, ks, batch, 27);
+  const DirectPlan p = direct_plan(V, y.c, ks, batch, 27, x.c);
 #define LAUNCH_F(KS_, CG_, S_)                                                                       \
   do {                                                                                               \
     const size_t sm = ((size_t)x.c * KS_ * KS_ * KS_ * CG_ + (S_ > 1 ? (size_t)p.thr * CG_ : 0)) * sizeof(float); \
@@ -471,7 +474,7 @@ int conv_dgrad_direct(d2ip_act gy, const float* w, long long wbs, int ks, int st
                       int accumulate, int batch, cudaStream_t st, int dil) {
   const long long V = (long long)gx.d * gx.h * gx.w;
   const int vec = vec_ok(gy) ? 1 : 0;
-  const DirectPlan p = direct_plan(V, gx.c, ks, batch, stride == 1 ? 27 : 4);
+  const DirectPlan p = direct_plan(V, gx.c, ks, batch, stride == 1 ? 27 : 4, gy.c);
 #define LAUNCH_D(KS_, CG_, S_)                                                                        \
   do {                                                                                                \
     const size_t sm = ((size_t)gy.c * KS_ * KS_ * KS_ * CG_ + (S_ > 1 ? (size_t)p.thr * CG_ : 0)) * sizeof(float); \

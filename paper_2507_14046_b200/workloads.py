@@ -136,6 +136,27 @@ def jacobian_device(spec: WorkloadSpec, seed: int = 0):
     return J, mask
 
 
+def device_frame(spec: WorkloadSpec, seed: int = 0, t: int = 0):
+    """One frame of the large configs (cfg2 / cfg4) built on the GPU: J from
+    `jacobian_device`, dv = J sigma_true(t) + 1 % RMS noise (torch RNG, seeded),
+    output_map = (min, max) of sigma_true. Returns (J [M][V] cuda, mask, dv
+    [M] cuda fp32, output_map)."""
+    import torch
+
+    J, mask = jacobian_device(spec, seed)
+    grid = spec.geometry()
+    truth = sigma_true(spec, t)
+    cols = torch.from_numpy(np.ascontiguousarray(vectorize(truth)[np.flatnonzero(vectorize(mask))])).cuda().float()
+    clean = J @ cols
+    g = torch.Generator(device="cuda").manual_seed(int(seed) + 7919)
+    rms = float(clean.pow(2).mean().sqrt())
+    dv = clean + torch.randn(clean.shape, generator=g, device="cuda") * (spec.noise_rel * rms)
+    lo, hi = float(truth.min()), float(truth.max())
+    if lo == hi:
+        lo, hi = lo - 0.5, hi + 0.5
+    return J, mask, dv, (lo, hi)
+
+
 def _ellipsoid(grid: GridGeometry, centre, axes) -> np.ndarray:
     ys, xs, zs = grid.axis_centers()
     u = ((xs[None, :, None] - centre[0]) / axes[0]) ** 2
