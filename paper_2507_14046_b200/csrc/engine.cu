@@ -190,6 +190,7 @@ static size_t plan_workspace(d2ip_engine& E, char* base) {
   E.n_reg = tv_nblocks(E.V[0]);
   E.regpart = A.f((long long)B * E.n_reg);
   E.wg_ws = A.take(E.wg_ws_bytes);
+  for (auto& w : E.lane_ws) w = A.take(E.wg_ws_bytes);
   E.na_ws = A.take(E.na_ws_bytes);
   E.tc_ws = E.tc_ws_bytes ? reinterpret_cast<float*>(A.take(E.tc_ws_bytes)) : nullptr;
   return A.total();
@@ -255,8 +256,8 @@ int cdgrad(Ctx& k, const ConvP& c, d2ip_act gy, d2ip_act gx, int acc) {
 
 int cwgrad(Ctx& k, const ConvP& c, d2ip_act x, d2ip_act gy) {
   if (c.dil != 1)
-    return conv_wgrad_direct(x, gy, c.ks, c.stride, k.gr() + c.ow, k.pbs, k.E.wg_ws, k.E.wg_ws_bytes, k.B, k.st, c.dil);
-  return conv_wgrad(x, gy, c.ks, c.stride, k.gr() + c.ow, k.pbs, k.E.wg_ws, k.E.wg_ws_bytes, k.prec, k.B, k.st);
+    return conv_wgrad_direct(x, gy, c.ks, c.stride, k.gr() + c.ow, k.pbs, k.wgws, k.E.wg_ws_bytes, k.B, k.st, c.dil);
+  return conv_wgrad(x, gy, c.ks, c.stride, k.gr() + c.ow, k.pbs, k.wgws, k.E.wg_ws_bytes, k.prec, k.B, k.st);
 }
 
 int fork_to(Ctx& k, cudaStream_t from, cudaStream_t to) {
@@ -266,25 +267,26 @@ int fork_to(Ctx& k, cudaStream_t from, cudaStream_t to) {
   return D2IP_OK;
 }
 
-int fork_side(Ctx& k) {
-  D2IP_RET(fork_to(k, k.st, k.side));
-  k.forked = true;
+int side_ctx(Ctx& k, Ctx& ks) {
+  d2ip_engine& E = k.E;
+  const int i = E.lane_next++ % d2ip_engine::kLanes;
+  D2IP_RET(fork_to(k, k.st, E.lane[i]));
+  k.lanes |= 1u << i;
+  ks.st = E.lane[i];  // ks: a copy of k made by the caller
+  ks.wgws = E.lane_ws[i];
   return D2IP_OK;
 }
 
 int join_side(Ctx& k) {
-  if (!k.forked) return D2IP_OK;
-  k.forked = false;
-  cudaEvent_t e = k.E.ev[k.E.evi++ % d2ip_engine::kEvents];
-  D2IP_CUDA(cudaEventRecord(e, k.side));
-  D2IP_CUDA(cudaStreamWaitEvent(k.st, e, 0));
+  for (int i = 0; i < d2ip_engine::kLanes; ++i)
+    if (k.lanes & (1u << i)) D2IP_RET(fork_to(k, k.E.lane[i], k.st));
+  k.lanes = 0;
   return D2IP_OK;
 }
 
 int cwgrad_side(Ctx& k, const ConvP& c, d2ip_act x, d2ip_act gy) {
-  D2IP_RET(fork_side(k));
   Ctx ks = k;
-  ks.st = k.side;
+  D2IP_RET(side_ctx(k, ks));
   return cwgrad(ks, c, x, gy);
 }
 
@@ -343,8 +345,9 @@ static int block_fwd(Ctx& k, Block& bl) {
 
 // Side-stream sum of a norm's dgamma/dbeta partials (per-norm buffer `np`).
 static int dgb_side(Ctx& k, const float* np, int nb, int C, long long og) {
-  D2IP_RET(fork_side(k));
-  return reduce_chunks(np, nb, 2 * C, k.gr() + og, k.pbs, k.B, k.side);
+  Ctx ks = k;
+  D2IP_RET(side_ctx(k, ks));
+  return reduce_chunks(np, nb, 2 * C, k.gr() + og, k.pbs, k.B, ks.st);
 }
 
 static int block_bwd(Ctx& k, Block& bl) {
@@ -360,12 +363,8 @@ static int block_bwd(Ctx& k, Block& bl) {
   D2IP_RET(norm_act_bwd(bl.gout, bl.out, 1, k.slope, bl.xh2, bl.rs2, k.th() + bl.n2.og, k.pbs, gpre, gc2,
                         k.gr() + bl.n2.og, k.pbs, bl.np2, npb, k.B, k.st, &nb));
   D2IP_RET(dgb_side(k, bl.np2, nb, co, bl.n2.og));
-  {
-    Ctx ks = k;  // side: weight gradients (ordered after gpre / gc2 by the fork above)
-    ks.st = k.side;
-    D2IP_RET(cwgrad(ks, bl.c2, h1, gc2));
-    D2IP_RET(cwgrad(ks, bl.sk, bl.x, gpre));
-  }
+  D2IP_RET(cwgrad_side(k, bl.c2, h1, gc2));
+  D2IP_RET(cwgrad_side(k, bl.sk, bl.x, gpre));
   // side2: the 1^3 skip's data gradient writes gx first; conv1's accumulates after the join
   D2IP_RET(fork_to(k, k.st, k.side2));
   {
@@ -377,11 +376,7 @@ static int block_bwd(Ctx& k, Block& bl) {
   D2IP_RET(norm_act_bwd(gh1, h1, 1, k.slope, bl.xh1, bl.rs1, k.th() + bl.n1.og, k.pbs, gpre1, gc1,
                         k.gr() + bl.n1.og, k.pbs, bl.np1, npb, k.B, k.st, &nb));
   D2IP_RET(dgb_side(k, bl.np1, nb, co, bl.n1.og));
-  {
-    Ctx ks = k;  // ordered after gc1 by dgb_side's fork
-    ks.st = k.side;
-    D2IP_RET(cwgrad(ks, bl.c1, bl.x, gc1));
-  }
+  D2IP_RET(cwgrad_side(k, bl.c1, bl.x, gc1));
   D2IP_RET(fork_to(k, k.side2, k.st));
   D2IP_RET(cdgrad(k, bl.c1, gc1, bl.gx, 1));
   return D2IP_OK;
@@ -478,11 +473,7 @@ static int backward(Ctx& k) {
                         k.gr() + E.stem_n.og, k.pbs, E.stem_np, norm_act_bwd_ws(E.V[0], c[0], k.B), k.B, k.st, &nb));
   D2IP_RET(dgb_side(k, E.stem_np, nb, c[0], E.stem_n.og));
   d2ip_act z = view(E, const_cast<float*>(E.b.z), 0, E.d.in_channels, E.d.in_channels);
-  {
-    Ctx ks = k;  // ordered after gc by dgb_side's fork
-    ks.st = k.side;
-    D2IP_RET(cwgrad(ks, E.stem, z, gc));
-  }
+  D2IP_RET(cwgrad_side(k, E.stem, z, gc));
   return join_side(k);
 }
 
@@ -493,7 +484,7 @@ static int adam(Ctx& k) {
 }
 
 static Ctx ctx(d2ip_engine& E, void* stream) {
-  return Ctx{E, S(stream), E.d.batch, E.nparams, E.d.precision, E.d.negative_slope, E.side, false, E.side2};
+  return Ctx{E, S(stream), E.d.batch, E.nparams, E.d.precision, E.d.negative_slope, E.side2, E.wg_ws, 0u};
 }
 
 int engine_step(d2ip_engine& E, void* stream) {
@@ -636,7 +627,8 @@ void d2ip_engine_destroy(d2ip_engine* e) {
   d2ip::drop_graph(*e);
   d2ip::refnet_destroy(*e);
   if (e->cap_stream) cudaStreamDestroy(e->cap_stream);
-  if (e->side) cudaStreamDestroy(e->side);
+  for (auto l : e->lane)
+    if (l) cudaStreamDestroy(l);
   if (e->side2) cudaStreamDestroy(e->side2);
   for (auto ev : e->ev)
     if (ev) cudaEventDestroy(ev);
@@ -657,8 +649,8 @@ int d2ip_engine_bind(d2ip_engine* e, const d2ip_bindings* b) {
                  "missing binding");
   D2IP_CHECK_ARG(e->d.lambda_tv <= 0.f || b->history || e->d.max_history == 0, "TV needs a history buffer");
   drop_graph(*e);
-  if (!e->side) {
-    D2IP_CUDA(cudaStreamCreateWithFlags(&e->side, cudaStreamNonBlocking));
+  if (!e->side2) {
+    for (auto& l : e->lane) D2IP_CUDA(cudaStreamCreateWithFlags(&l, cudaStreamNonBlocking));
     D2IP_CUDA(cudaStreamCreateWithFlags(&e->side2, cudaStreamNonBlocking));
     for (auto& ev : e->ev) D2IP_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   }

@@ -74,8 +74,12 @@ struct d2ip_engine {
   cudaGraphExec_t gexec = nullptr;
   cudaStream_t cap_stream = nullptr;
   int launches = 0;
-  // weight gradients run on a side stream, off the data-gradient critical path
-  cudaStream_t side = nullptr;
+  // weight gradients (and dgamma/dbeta sums) run on a pool of side lanes, off the
+  // data-gradient critical path; each lane has its own reduction workspace
+  static constexpr int kLanes = 3;
+  cudaStream_t lane[kLanes]{};
+  void* lane_ws[kLanes]{};
+  int lane_next = 0;
   cudaStream_t side2 = nullptr;  // short data-gradient branches (1^3 skip) beside the main chain
   static constexpr int kEvents = 128;
   cudaEvent_t ev[kEvents]{};
@@ -121,20 +125,20 @@ struct Ctx {
   long long pbs;
   int prec;
   float slope;
-  cudaStream_t side;  // weight-gradient stream (forked from / joined into st)
-  bool forked = false;  // side stream holds work of this pass (join only then: capture rules)
   cudaStream_t side2;
+  void* wgws;          // weight-gradient reduction workspace of the stream this context launches on
+  unsigned lanes = 0;  // side lanes holding work of this pass (join only those: capture rules)
   float* th() const { return E.b.theta; }
   float* gr() const { return E.b.grad; }
 };
 
-// st -> side dependency (everything enqueued on st so far happens before what
-// is enqueued on side next) and the reverse join.
-int fork_side(Ctx& k);
+// A context on the next side lane, ordered after everything already on k.st
+// (k records the lane for the join); join_side makes k.st wait for every lane used.
+int side_ctx(Ctx& k, Ctx& ks);
 int join_side(Ctx& k);
 // generic fork / join between two streams (graph-capture safe)
 int fork_to(Ctx& k, cudaStream_t from, cudaStream_t to);
-// weight gradient on the side stream, after everything already on st
+// weight gradient on a side lane, after everything already on st
 int cwgrad_side(Ctx& k, const ConvP& c, d2ip_act x, d2ip_act gy);
 
 int cfwd(Ctx& k, const ConvP& c, d2ip_act x, d2ip_act y, int acc, SplitK* sk = nullptr);

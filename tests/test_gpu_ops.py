@@ -66,6 +66,9 @@ CONV_CASES = [
     (8, 16, 3, 1, (32, 32, 32)),
     (128, 128, 3, 1, (8, 8, 4)),
     (192, 64, 3, 1, (16, 16, 8)),
+    # large grids (cfg2 / cfg4 scale tiles)
+    (16, 32, 3, 1, (64, 64, 32)),
+    (32, 16, 3, 1, (48, 48, 32)),
 ]
 
 
