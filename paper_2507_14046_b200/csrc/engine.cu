@@ -248,9 +248,17 @@ int cfwd(Ctx& k, const ConvP& c, d2ip_act x, d2ip_act y, int acc, SplitK* sk) {
   return conv_fwd_direct(x, k.th() + c.ow, k.th() + c.ob, k.pbs, c.ks, c.stride, y, acc, k.B, k.st, c.dil);
 }
 
-int cdgrad(Ctx& k, const ConvP& c, d2ip_act gy, d2ip_act gx, int acc) {
-  if (c.tcd)
-    return conv_tc_run(gy, c.pkd, c.cout, c.cin, nullptr, 0, gx, acc, k.E.tc_ws, k.E.tc_ws_bytes, k.B, k.st);
+// With `sk`, a split-K tcgen05 data gradient is left as partials for the
+// consuming LayerNorm backward to reduce (as the forward does).
+int cdgrad(Ctx& k, const ConvP& c, d2ip_act gy, d2ip_act gx, int acc, SplitK* sk) {
+  if (c.tcd) {
+    int kspl = 0;
+    D2IP_RET(conv_tc_run(gy, c.pkd, c.cout, c.cin, nullptr, 0, gx, acc, k.E.tc_ws, k.E.tc_ws_bytes, k.B, k.st,
+                         sk && !acc ? &kspl : nullptr));
+    if (sk) *sk = kspl ? SplitK{k.E.tc_ws, kspl, nullptr, 0} : SplitK{};
+    return D2IP_OK;
+  }
+  if (sk) *sk = SplitK{};
   return conv_dgrad_direct(gy, k.th() + c.ow, k.pbs, c.ks, c.stride, gx, acc, k.B, k.st, c.dil);
 }
 
@@ -372,9 +380,10 @@ static int block_bwd(Ctx& k, Block& bl) {
     k2.st = k.side2;
     D2IP_RET(cdgrad(k2, bl.sk, gpre, bl.gx, bl.gx_acc));
   }
-  D2IP_RET(cdgrad(k, bl.c2, gc2, gh1, 0));
+  SplitK skd;
+  D2IP_RET(cdgrad(k, bl.c2, gc2, gh1, 0, &skd));
   D2IP_RET(norm_act_bwd(gh1, h1, 1, k.slope, bl.xh1, bl.rs1, k.th() + bl.n1.og, k.pbs, gpre1, gc1,
-                        k.gr() + bl.n1.og, k.pbs, bl.np1, npb, k.B, k.st, &nb));
+                        k.gr() + bl.n1.og, k.pbs, bl.np1, npb, k.B, k.st, &nb, skd));
   D2IP_RET(dgb_side(k, bl.np1, nb, co, bl.n1.og));
   D2IP_RET(cwgrad_side(k, bl.c1, bl.x, gc1));
   D2IP_RET(fork_to(k, k.side2, k.st));

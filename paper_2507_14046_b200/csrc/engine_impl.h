@@ -142,7 +142,7 @@ int fork_to(Ctx& k, cudaStream_t from, cudaStream_t to);
 int cwgrad_side(Ctx& k, const ConvP& c, d2ip_act x, d2ip_act gy);
 
 int cfwd(Ctx& k, const ConvP& c, d2ip_act x, d2ip_act y, int acc, SplitK* sk = nullptr);
-int cdgrad(Ctx& k, const ConvP& c, d2ip_act gy, d2ip_act gx, int acc);
+int cdgrad(Ctx& k, const ConvP& c, d2ip_act gy, d2ip_act gx, int acc, SplitK* sk = nullptr);
 int cwgrad(Ctx& k, const ConvP& c, d2ip_act x, d2ip_act gy);
 
 // refnet.cu

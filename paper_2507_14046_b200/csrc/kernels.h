@@ -99,7 +99,8 @@ size_t norm_act_bwd_ws(long long V, int C, int batch);
 int norm_act_bwd(d2ip_act gout, d2ip_act out, int act, float slope, const float* xhat,
                  const float* rstd, const float* gamma, long long pbs, d2ip_act gpre, d2ip_act gc,
                  float* dgb, long long dgbs, void* ws, size_t ws_bytes, int batch, cudaStream_t st,
-                 int* deferred = nullptr);  // deferred: skip the dgamma/dbeta reduce, *deferred = partial chunks
+                 int* deferred = nullptr,   // deferred: skip the dgamma/dbeta reduce, *deferred = partial chunks
+                 SplitK sk = SplitK{});     // sk: gout = sum of the producing conv's split-K partials
 int upsample2x_fwd(d2ip_act x, d2ip_act y, int batch, cudaStream_t st);
 int upsample2x_bwd(d2ip_act gy, d2ip_act gx, int accumulate, int batch, cudaStream_t st);
 int tail_fwd(d2ip_act x, const float* w, const float* bias, long long wbs, float lo, float scale,

@@ -163,7 +163,7 @@ __global__ void __launch_bounds__(kNormThreads) norm_act_bwd_k(d2ip_act gout, d2
                                                                const float* __restrict__ rstd,
                                                                const float* __restrict__ gamma, long long pbs,
                                                                d2ip_act gpre, d2ip_act gc,
-                                                               float* __restrict__ partial, int G) {
+                                                               float* __restrict__ partial, int G, SplitK sk) {
   D2IP_PDL_ENTRY();
   extern __shared__ float red[];  // [groups][2C]
   const int b = blockIdx.y;
@@ -186,7 +186,17 @@ __global__ void __launch_bounds__(kNormThreads) norm_act_bwd_k(d2ip_act gout, d2
 #pragma unroll
     for (int i = 0; i < VPL; ++i) g[i] = xh[i] = 0.f;
     if (ok) {
-      ld<VPL>(gout.ptr + b * gout.bstride + v * gout.cstride + c0, g);
+      if (sk.part) {  // the producing data-gradient convolution's split-K partials (fixed order, no bias)
+        const float* p = sk.part + ((long long)b * sk.kspl * V + v) * C + c0;
+        for (int k = 0; k < sk.kspl; ++k) {
+          float t[VPL];
+          ld<VPL>(p + (long long)k * V * C, t);
+#pragma unroll
+          for (int i = 0; i < VPL; ++i) g[i] += t[i];
+        }
+      } else {
+        ld<VPL>(gout.ptr + b * gout.bstride + v * gout.cstride + c0, g);
+      }
       ld<VPL>(xhat + ((long long)b * V + v) * C + c0, xh);
       if (act) {
         float o[VPL];
@@ -245,7 +255,7 @@ size_t norm_act_bwd_ws(long long V, int C, int batch) {
 
 int norm_act_bwd(d2ip_act gout, d2ip_act out, int act, float slope, const float* xhat, const float* rstd,
                  const float* gamma, long long pbs, d2ip_act gpre, d2ip_act gc, float* dgb, long long dgbs, void* ws,
-                 size_t ws_bytes, int batch, cudaStream_t st, int* deferred) {
+                 size_t ws_bytes, int batch, cudaStream_t st, int* deferred, SplitK sk) {
   const int C = gout.c;
   D2IP_CHECK_ARG(C % 4 == 0 && C <= 256, "norm_act_bwd: C=%d must be a multiple of 4, <= 256", C);
   D2IP_CHECK_ARG(gout.cstride % 4 == 0 && gc.cstride % 4 == 0 && (!act || out.cstride % 4 == 0) &&
@@ -260,10 +270,10 @@ int norm_act_bwd(d2ip_act gout, d2ip_act out, int act, float slope, const float*
   dim3 grid(nb, batch);
   if (g.vpl == 4)
     D2IP_CUDA(launch_pdl(norm_act_bwd_k<4>, grid, kNormThreads, smem, st, gout, out, act, slope, xhat, rstd, gamma, pbs, gpre, gc,
-                                                        partial, g.G));
+                                                        partial, g.G, sk));
   else
     D2IP_CUDA(launch_pdl(norm_act_bwd_k<8>, grid, kNormThreads, smem, st, gout, out, act, slope, xhat, rstd, gamma, pbs, gpre, gc,
-                                                        partial, g.G));
+                                                        partial, g.G, sk));
   D2IP_LAUNCH_CHECK();
   if (deferred) {  // the caller sums the dgamma / dbeta partials (reduce_chunks) where it likes
     *deferred = nb;
