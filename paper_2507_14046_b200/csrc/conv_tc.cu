@@ -37,7 +37,7 @@
 
 namespace d2ip {
 
-constexpr int kTcThreads = 128;
+constexpr int kTcThreads = 256;  // 8 warps: fills / splits spread wider; epilogue = 2 threads per row
 constexpr int kTcRows = 128;
 
 __host__ __device__ static inline int np_of(int n) { return (n + 15) / 16 * 16; }
@@ -206,7 +206,9 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
   tc::fence_after();
 
   // epilogue: TMEM lane = GEMM row; each thread owns one row / voxel.
-  const int row = warp * 32 + lane;
+  // warp w reads TMEM lane quadrant w % 4 (rows) and column half w / 4
+  const int row = (warp & 3) * 32 + lane;
+  const int chalf = a.Ns / 2, cbeg = (warp >> 2) * chalf, cend = cbeg + chalf;
   const int u = u0 + row;
   int v = -1;
   {
@@ -216,10 +218,10 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
       v = ((dp - 1) * x.h + (hp - 1)) * x.w + (wp - 1);
   }
   const d2ip_act y = a.y;
-  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
+  const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16);
   if (a.kspl > 1) {  // raw partial sums; conv_tc_splitk_reduce_k adds bias / accumulates
     float* pp = v >= 0 ? a.part + (((long long)b * a.kspl + ks) * a.vout + v) * a.N : nullptr;
-    for (int c0 = 0; c0 < a.Ns; c0 += 8) {
+    for (int c0 = cbeg; c0 < cend; c0 += 8) {
       float vals[8];
       tc::tmem_ld8(trow + c0, vals);
       if (pp) {
@@ -235,7 +237,7 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
   }
   float* yp = v >= 0 ? y.ptr + b * y.bstride + (long long)v * y.cstride : nullptr;
   const float* bias = a.bias ? a.bias + b * a.bbs : nullptr;
-  for (int c0 = 0; c0 < a.Ns; c0 += 8) {
+  for (int c0 = cbeg; c0 < cend; c0 += 8) {
     float vals[8];
     tc::tmem_ld8(trow + c0, vals);
     if (yp) {
