@@ -53,11 +53,52 @@ __global__ void __launch_bounds__(256) upsample2x_fwd_k(d2ip_act x, d2ip_act y) 
   y.ptr[b * y.bstride + v * y.cstride + c] = r;
 }
 
+// float4 variant: one thread per (voxel, 4 channels) -- a quarter of the index
+// arithmetic and 128-bit loads / stores (C, strides and bases 16-byte aligned).
+__global__ void __launch_bounds__(256) upsample2x_fwd4_k(d2ip_act x, d2ip_act y) {
+  D2IP_PDL_ENTRY();
+  const int b = blockIdx.y;
+  const int C4 = x.c >> 2;
+  const long long total = (long long)y.d * y.h * y.w * C4;
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= total) return;
+  const int c = (int)(idx % C4) * 4;
+  const long long v = idx / C4;
+  const int ow = (int)(v % y.w), oh = (int)((v / y.w) % y.h), od = (int)(v / ((long long)y.w * y.h));
+  const Lin ld = lin_src(od, x.d), lh = lin_src(oh, x.h), lw = lin_src(ow, x.w);
+  const float* xb = x.ptr + b * x.bstride + c;
+  auto at = [&](int d, int h, int w) {
+    return *reinterpret_cast<const float4*>(xb + (((long long)d * x.h + h) * x.w + w) * x.cstride);
+  };
+  auto lerp2 = [](float a, float p, float bb, float q) { return a * p + bb * q; };
+  const float4 p00 = at(ld.i0, lh.i0, lw.i0), p01 = at(ld.i0, lh.i0, lw.i1);
+  const float4 p10 = at(ld.i0, lh.i1, lw.i0), p11 = at(ld.i0, lh.i1, lw.i1);
+  const float4 q00 = at(ld.i1, lh.i0, lw.i0), q01 = at(ld.i1, lh.i0, lw.i1);
+  const float4 q10 = at(ld.i1, lh.i1, lw.i0), q11 = at(ld.i1, lh.i1, lw.i1);
+  float4 r;
+#define D2IP_UP(comp)                                                                        \
+  {                                                                                          \
+    const float v00 = lerp2(lw.l0, p00.comp, lw.l1, p01.comp);                                \
+    const float v01 = lerp2(lw.l0, p10.comp, lw.l1, p11.comp);                                \
+    const float v10 = lerp2(lw.l0, q00.comp, lw.l1, q01.comp);                                \
+    const float v11 = lerp2(lw.l0, q10.comp, lw.l1, q11.comp);                                \
+    r.comp = ld.l0 * (lh.l0 * v00 + lh.l1 * v01) + ld.l1 * (lh.l0 * v10 + lh.l1 * v11);       \
+  }
+  D2IP_UP(x) D2IP_UP(y) D2IP_UP(z) D2IP_UP(w)
+#undef D2IP_UP
+  *reinterpret_cast<float4*>(y.ptr + b * y.bstride + v * y.cstride + c) = r;
+}
+
+static bool aligned4(const d2ip_act& a) { return a.c % 4 == 0 && a.cstride % 4 == 0 && ((uintptr_t)a.ptr & 15) == 0; }
+
 int upsample2x_fwd(d2ip_act x, d2ip_act y, int batch, cudaStream_t st) {
   D2IP_CHECK_ARG(y.d == 2 * x.d && y.h == 2 * x.h && y.w == 2 * x.w && y.c == x.c,
                  "upsample2x: shape mismatch");
   const long long total = (long long)y.d * y.h * y.w * y.c;
-  D2IP_CUDA(launch_pdl(upsample2x_fwd_k, dim3(cdiv(total, 256), batch), 256, 0, st, x, y));
+  if (aligned4(x) && aligned4(y))
+    D2IP_CUDA(launch_pdl(upsample2x_fwd4_k, dim3(cdiv(total / 4, 256), batch), 256, 0, st, x, y));
+  else
+    D2IP_CUDA(launch_pdl(upsample2x_fwd_k, dim3(cdiv(total, 256), batch), 256, 0, st, x, y));
   D2IP_LAUNCH_CHECK();
   return D2IP_OK;
 }
@@ -98,11 +139,55 @@ __global__ void __launch_bounds__(256) upsample2x_bwd_k(d2ip_act gy, d2ip_act gx
   *o = accumulate ? *o + acc : acc;
 }
 
+// float4 variant of the gather (same per-channel summation order)
+__global__ void __launch_bounds__(256) upsample2x_bwd4_k(d2ip_act gy, d2ip_act gx, int accumulate) {
+  D2IP_PDL_ENTRY();
+  const int b = blockIdx.y;
+  const int C4 = gx.c >> 2;
+  const long long total = (long long)gx.d * gx.h * gx.w * C4;
+  const long long idx = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= total) return;
+  const int c = (int)(idx % C4) * 4;
+  const long long v = idx / C4;
+  const int iw = (int)(v % gx.w), ih = (int)((v / gx.w) % gx.h), id = (int)(v / ((long long)gx.w * gx.h));
+  int hd[4], hh[4], hw[4];
+  float wd[4], wh[4], ww[4];
+  const int nd = lin_adj(id, gx.d, hd, wd), nh = lin_adj(ih, gx.h, hh, wh), nw = lin_adj(iw, gx.w, hw, ww);
+  const float* gb = gy.ptr + b * gy.bstride + c;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int a = 0; a < nd; ++a)
+    for (int e = 0; e < nh; ++e) {
+      float4 row = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int f = 0; f < nw; ++f) {
+        const float4 g =
+            *reinterpret_cast<const float4*>(gb + (((long long)hd[a] * gy.h + hh[e]) * gy.w + hw[f]) * gy.cstride);
+        row.x = fmaf(ww[f], g.x, row.x);
+        row.y = fmaf(ww[f], g.y, row.y);
+        row.z = fmaf(ww[f], g.z, row.z);
+        row.w = fmaf(ww[f], g.w, row.w);
+      }
+      const float wde = wd[a] * wh[e];
+      acc.x = fmaf(wde, row.x, acc.x);
+      acc.y = fmaf(wde, row.y, acc.y);
+      acc.z = fmaf(wde, row.z, acc.z);
+      acc.w = fmaf(wde, row.w, acc.w);
+    }
+  float4* o = reinterpret_cast<float4*>(gx.ptr + b * gx.bstride + v * gx.cstride + c);
+  if (accumulate) {
+    const float4 p = *o;
+    acc.x += p.x; acc.y += p.y; acc.z += p.z; acc.w += p.w;
+  }
+  *o = acc;
+}
+
 int upsample2x_bwd(d2ip_act gy, d2ip_act gx, int accumulate, int batch, cudaStream_t st) {
   D2IP_CHECK_ARG(gy.d == 2 * gx.d && gy.h == 2 * gx.h && gy.w == 2 * gx.w && gy.c == gx.c,
                  "upsample2x_bwd: shape mismatch");
   const long long total = (long long)gx.d * gx.h * gx.w * gx.c;
-  D2IP_CUDA(launch_pdl(upsample2x_bwd_k, dim3(cdiv(total, 256), batch), 256, 0, st, gy, gx, accumulate));
+  if (aligned4(gy) && aligned4(gx))
+    D2IP_CUDA(launch_pdl(upsample2x_bwd4_k, dim3(cdiv(total / 4, 256), batch), 256, 0, st, gy, gx, accumulate));
+  else
+    D2IP_CUDA(launch_pdl(upsample2x_bwd_k, dim3(cdiv(total, 256), batch), 256, 0, st, gy, gx, accumulate));
   D2IP_LAUNCH_CHECK();
   return D2IP_OK;
 }
@@ -128,7 +213,8 @@ __global__ void __launch_bounds__(128) tail_fwd_k(d2ip_act x, const float* __res
   const int ow = (int)(v % x.w), oh = (int)((v / x.w) % x.h), od = (int)(v / ((long long)x.w * x.h));
   const float* xb = x.ptr + b * x.bstride;
   const bool vec = (cin % 4 == 0) && (x.cstride % 4 == 0) && (((uintptr_t)x.ptr & 15) == 0);
-  float acc = __ldg(bias + b * wbs);
+  // four independent partial sums (one per float4 lane): a 4x shorter FMA chain
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
   for (int kd = 0; kd < 3; ++kd) {
     const int id = od + kd - 1;
     if (id < 0 || id >= x.d) continue;
@@ -143,17 +229,18 @@ __global__ void __launch_bounds__(128) tail_fwd_k(d2ip_act x, const float* __res
         if (vec) {
           for (int ci = 0; ci < cin; ci += 4) {
             const float4 q = __ldg(reinterpret_cast<const float4*>(xp + ci));
-            acc = fmaf(q.x, wr[ci], acc);
-            acc = fmaf(q.y, wr[ci + 1], acc);
-            acc = fmaf(q.z, wr[ci + 2], acc);
-            acc = fmaf(q.w, wr[ci + 3], acc);
+            a0 = fmaf(q.x, wr[ci], a0);
+            a1 = fmaf(q.y, wr[ci + 1], a1);
+            a2 = fmaf(q.z, wr[ci + 2], a2);
+            a3 = fmaf(q.w, wr[ci + 3], a3);
           }
         } else {
-          for (int ci = 0; ci < cin; ++ci) acc = fmaf(xp[ci], wr[ci], acc);
+          for (int ci = 0; ci < cin; ++ci) a0 = fmaf(xp[ci], wr[ci], a0);
         }
       }
     }
   }
+  const float acc = __ldg(bias + b * wbs) + ((a0 + a1) + (a2 + a3));
   const float s = 1.0f / (1.0f + expf(-acc));
   const float mp = lo + scale * s;
   sig[b * V + v] = s;
