@@ -160,29 +160,32 @@ int dw_conv_wgrad(d2ip_act x, d2ip_act gy, int stride, float* gw, long long gwbs
 }
 
 // ---- SqueezeExcite -----------------------------------------------------------
-// column sums: partial[b][blk][c] = sum over the block's voxels of a[v][c] (* m[v][c])
-__global__ void __launch_bounds__(256) colsum_k(d2ip_act a, d2ip_act m, float* __restrict__ partial, int chunk,
+// column sums: partial[b][blk][c] = sum over the block's voxels of a[v][c] (* m[v][c]).
+// Accumulated in fp64: the SE gate gradient sum_v gs*x cancels heavily, and an
+// fp32 running sum over 32K voxels loses ~1e-3 of it (the reference's CPU
+// reductions are pairwise).
+__global__ void __launch_bounds__(256) colsum_k(d2ip_act a, d2ip_act m, double* __restrict__ partial, int chunk,
                                                 int nchunks) {
   D2IP_PDL_ENTRY();
-  __shared__ float red[256];
+  __shared__ double red[256];
   const int b = blockIdx.y, blk = blockIdx.x;
   const int C = a.c;
   const long long V = (long long)a.d * a.h * a.w;
   const int rows = 256 / C;  // C <= 256
   const int c = threadIdx.x % C, r = threadIdx.x / C;
-  float acc = 0.f;
+  double acc = 0.0;
   if (r < rows) {
     const long long v0 = (long long)blk * chunk, v1 = min(V, v0 + chunk);
     for (long long v = v0 + r; v < v1; v += rows) {
-      float t = a.ptr[b * a.bstride + v * a.cstride + c];
-      if (m.ptr) t *= m.ptr[b * m.bstride + v * m.cstride + c];
+      double t = a.ptr[b * a.bstride + v * a.cstride + c];
+      if (m.ptr) t *= (double)m.ptr[b * m.bstride + v * m.cstride + c];
       acc += t;
     }
   }
   red[threadIdx.x] = acc;
   __syncthreads();
   if (threadIdx.x < C) {
-    float s = 0.f;
+    double s = 0.0;
     for (int q = 0; q < rows; ++q) s += red[q * C + threadIdx.x];
     partial[((long long)b * nchunks + blk) * C + threadIdx.x] = s;
   }
@@ -197,15 +200,15 @@ static void col_split(long long V, int batch, int* n, int* chunk) {
 size_t colsum_ws(int C, long long V, int batch) {
   int n, c;
   col_split(V, batch, &n, &c);
-  return (size_t)batch * n * C * sizeof(float);
+  return (size_t)batch * n * C * sizeof(double);
 }
 
-int colsum(d2ip_act a, d2ip_act m, float* partial, size_t ws_bytes, int batch, int* nchunks, cudaStream_t st) {
+int colsum(d2ip_act a, d2ip_act m, double* partial, size_t ws_bytes, int batch, int* nchunks, cudaStream_t st) {
   D2IP_CHECK_ARG(a.c <= 256, "colsum: C > 256");
   const long long V = (long long)a.d * a.h * a.w;
   int chunk;
   col_split(V, batch, nchunks, &chunk);
-  D2IP_CHECK_ARG(ws_bytes >= (size_t)batch * *nchunks * a.c * sizeof(float), "colsum: workspace too small");
+  D2IP_CHECK_ARG(ws_bytes >= (size_t)batch * *nchunks * a.c * sizeof(double), "colsum: workspace too small");
   D2IP_CUDA(launch_pdl(colsum_k, dim3(*nchunks, batch), 256, 0, st, a, m, partial, chunk, *nchunks));
   return D2IP_OK;
 }
@@ -213,7 +216,7 @@ int colsum(d2ip_act a, d2ip_act m, float* partial, size_t ws_bytes, int batch, i
 // One block per sequence: pooled = colsum / V; z1 = W1 pooled + b1; h = silu(z1);
 // z2 = W2 h + b2; g = sigmoid(z2). Saves pooled, z1, g (fwd_state layout:
 // [pooled C][z1 hid][g C]).
-__global__ void se_mlp_fwd_k(const float* __restrict__ partial, int nchunks, long long V, int C, int hid,
+__global__ void se_mlp_fwd_k(const double* __restrict__ partial, int nchunks, long long V, int C, int hid,
                              const float* __restrict__ w1, const float* __restrict__ b1, const float* __restrict__ w2,
                              const float* __restrict__ b2, long long pbs, float* __restrict__ state, int sbs) {
   D2IP_PDL_ENTRY();
@@ -223,9 +226,9 @@ __global__ void se_mlp_fwd_k(const float* __restrict__ partial, int nchunks, lon
   float* hv = sm + C;
   float* S = state + (long long)b * sbs;
   for (int c = threadIdx.x; c < C; c += blockDim.x) {
-    float s = 0.f;
+    double s = 0.0;
     for (int k = 0; k < nchunks; ++k) s += partial[((long long)b * nchunks + k) * C + c];
-    pooled[c] = s / (float)V;
+    pooled[c] = (float)(s / (double)V);
     S[c] = pooled[c];
   }
   __syncthreads();
@@ -262,7 +265,7 @@ __global__ void __launch_bounds__(256) chan_gate_k(d2ip_act x, const float* __re
 // gs[v][c] x[v][c] (colsum partials). Writes dW1, db1, dW2, db2 (adjacent in
 // the flat gradient like the reference's fc1.weight, fc1.bias, fc2.weight,
 // fc2.bias) and gpool[c] = (W1^T gz1)[c] / V into the state's scratch slot.
-__global__ void se_mlp_bwd_k(const float* __restrict__ partial, int nchunks, long long V, int C, int hid,
+__global__ void se_mlp_bwd_k(const double* __restrict__ partial, int nchunks, long long V, int C, int hid,
                              const float* __restrict__ w1, const float* __restrict__ b1, const float* __restrict__ w2,
                              long long pbs, float* __restrict__ state, int sbs, float* __restrict__ g1,
                              float* __restrict__ g2) {
@@ -279,9 +282,9 @@ __global__ void se_mlp_bwd_k(const float* __restrict__ partial, int nchunks, lon
   float* gpool = S + C + hid + C;
   for (int j = threadIdx.x; j < hid; j += blockDim.x) hv[j] = silu(z1[j]);
   for (int c = threadIdx.x; c < C; c += blockDim.x) {
-    float s = 0.f;
+    double s = 0.0;
     for (int k = 0; k < nchunks; ++k) s += partial[((long long)b * nchunks + k) * C + c];
-    gz2[c] = s * g[c] * (1.f - g[c]);
+    gz2[c] = (float)s * g[c] * (1.f - g[c]);
   }
   __syncthreads();
   float* gw2 = g2 + b * pbs;  // fc2.weight [C][hid], then fc2.bias [C]
@@ -326,7 +329,7 @@ int se_forward(d2ip_act x, const float* w1, const float* b1, const float* w2, co
   const int C = x.c;
   const long long V = (long long)x.d * x.h * x.w;
   int nchunks;
-  float* partial = reinterpret_cast<float*>(ws);
+  double* partial = reinterpret_cast<double*>(ws);
   D2IP_RET(colsum(x, d2ip_act{}, partial, ws_bytes, batch, &nchunks, st));
   D2IP_CUDA(launch_pdl(se_mlp_fwd_k, dim3(batch), 256, (size_t)(C + hid) * sizeof(float), st, partial, nchunks, V,
                        C, hid, w1, b1, w2, b2, pbs, state, sbs));
@@ -340,7 +343,7 @@ int se_backward(d2ip_act x, d2ip_act gs, const float* w1, const float* b1, const
   const int C = x.c;
   const long long V = (long long)x.d * x.h * x.w;
   int nchunks;
-  float* partial = reinterpret_cast<float*>(ws);
+  double* partial = reinterpret_cast<double*>(ws);
   D2IP_RET(colsum(gs, x, partial, ws_bytes, batch, &nchunks, st));
   D2IP_CUDA(launch_pdl(se_mlp_bwd_k, dim3(batch), 256, (size_t)(C + 2 * hid) * sizeof(float), st, partial, nchunks,
                        V, C, hid, w1, b1, w2, pbs, state, sbs, g1, g2));
