@@ -149,19 +149,18 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
     }
     tc::cp_async_commit();
   };
-  // split the landed activation window into hi (in place) and lo; every thread
-  // touches exactly the 16-B elements its own cp.async wrote.
+  // write the lo half of the landed activation window; the raw fp32 window
+  // itself is the hi operand, because the tensor core truncates fp32 operands
+  // to TF32 (measured: tools/tf32_round_probe.cu). Every thread touches exactly
+  // the 16-B elements its own cp.async wrote.
   auto split = [&](int buf) {
     uint8_t* A = smem + buf * Sb;
     for (int i = tid; i < nA; i += kTcThreads) {
       const int r = i / NKC, kc = i % NKC;
-      float4* hp = reinterpret_cast<float4*>(A + ((size_t)kc * WRp + r) * 16);
-      float4* lp = reinterpret_cast<float4*>(A + Ab + ((size_t)kc * WRp + r) * 16);
-      float4 v = *hp, h, l;
-      h.x = tf32_hi(v.x); h.y = tf32_hi(v.y); h.z = tf32_hi(v.z); h.w = tf32_hi(v.w);
-      l.x = v.x - h.x; l.y = v.y - h.y; l.z = v.z - h.z; l.w = v.w - h.w;
-      *hp = h;
-      *lp = l;
+      const float4 v = *reinterpret_cast<const float4*>(A + ((size_t)kc * WRp + r) * 16);
+      float4 l;
+      l.x = v.x - tf32_hi(v.x); l.y = v.y - tf32_hi(v.y); l.z = v.z - tf32_hi(v.z); l.w = v.w - tf32_hi(v.w);
+      *reinterpret_cast<float4*>(A + Ab + ((size_t)kc * WRp + r) * 16) = l;
     }
   };
   // descriptors of buffer 0; a tap / K step / buffer is an add to the 14-bit

@@ -142,11 +142,11 @@ __global__ void __launch_bounds__(kWtThreads) wgrad_tc_k(WgTc a) {
     }
     tc::cp_async_commit();
   };
+  // lo half only: the raw fp32 operand is the hi half (the tensor core truncates to TF32)
   auto split4 = [](float4* hp, float4* lp) {
-    float4 v = *hp, h, l;
-    h.x = tf32_hi_w(v.x); h.y = tf32_hi_w(v.y); h.z = tf32_hi_w(v.z); h.w = tf32_hi_w(v.w);
-    l.x = v.x - h.x; l.y = v.y - h.y; l.z = v.z - h.z; l.w = v.w - h.w;
-    *hp = h;
+    const float4 v = *hp;
+    float4 l;
+    l.x = v.x - tf32_hi_w(v.x); l.y = v.y - tf32_hi_w(v.y); l.z = v.z - tf32_hi_w(v.z); l.w = v.w - tf32_hi_w(v.w);
     *lp = l;
     return v;
   };
