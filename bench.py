@@ -204,6 +204,10 @@ def run_gpu(args):
         wl = W.make_workload(spec, seed=seed, frames=min(spec.frames, 20))
         net = spec.network(seed=seed + 1)
         noise = sample_noise_input(wl.grid, seed, spec.in_channels, 0.1)
+        if args.net == "fast":  # the reference's own backbone on this workload (1-channel U[0,1) noise)
+            from paper_2507_14046_b200.priornet import NetworkConfig
+            net = NetworkConfig(base_channels=args.base_channels, use_depthwise=not args.dense, seed=seed + 1)
+            noise = sample_noise_input(wl.grid, seed)
         dn = DeviceNet(net, wl.grid.shape, wl.matrix.n_measurements, wl.matrix.mask, data_norm="l2sq",
                        output_map=wl.output_map, lr=spec.learning_rate,
                        precision=args.precision or spec.precision, max_iters=args.warmup + args.steps + 8)
@@ -251,7 +255,8 @@ def run_gpu(args):
 
     # --- roofline of the dominant kernels, timed live on this stream
     pk, pk_kind = peaks()
-    units = algorithmic_units(spec, net, dn.M, dn.Vp)
+    units = algorithmic_units(spec, net, dn.M, dn.Vp) if args.net == "config" else {
+        "conv_flops": float("nan"), "n_params": dn.n_params}
     L = N.lib()
     st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
     t_flush = time_kernel(lambda: flush.zero_())
@@ -284,14 +289,14 @@ def run_gpu(args):
         del J2
     # dominant kernel: the tcgen05 conv on cfg1's largest layer (dec0.conv1,
     # 48 -> 16 channels at 32^3), one launch timed live through the C ABI
-    conv_roof = conv_probe(L, N, C, st, pk, pk_kind, flush, t_flush) if spec.channels[0] == 16 else None
+    conv_roof = conv_probe(L, N, C, st, pk, pk_kind, flush, t_flush) if spec.channels[0] == 16 and args.net == "config" else None
     # whole-iteration tensor-throughput view of the convolutions
     conv_tflops = units["conv_flops"] * units_per_step / (t_dev / args.steps) / 1e12
     roofline = conv_roof or jac_cfg
 
     # --- e2e through the public API (rank-local, one full sequence)
     e2e = None
-    if not args.skip_e2e and units_per_step == 1 and wl is not None:
+    if not args.skip_e2e and units_per_step == 1 and wl is not None and args.net == "config":
         e2e = run_e2e(spec, wl, args, ws)
 
     out = {
@@ -299,7 +304,9 @@ def run_gpu(args):
         "warmup": args.warmup, "ms_per_step": round(1e3 * t_dev / args.steps, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": "f32 (TF32 conv operands)" if (args.precision or spec.precision) == "tf32" else "f32",
         "data": "synthetic (seeded BASELINE cfg generator; random-init weights)",
-        "config": {"workload": args.workload, "grid": list(spec.grid), "channels": list(spec.channels),
+        "config": {"workload": args.workload + ("" if args.net == "config" else
+                                                f"+FastResUNet3D(b={args.base_channels},{'dense' if args.dense else 'depthwise'})"),
+                   "grid": list(spec.grid), "channels": list(spec.channels),
                    "C_z": spec.in_channels, "M": dn.M, "V": dn.V, "n_params": units["n_params"],
                    "precision": args.precision or spec.precision,
                    "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
@@ -470,7 +477,9 @@ def run_reference(args):
            "warmup": args.warmup, "ms_per_step": round(1e3 * t / args.steps, 3), "higher_is_better": True,
            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "impl": "reference",
            "data": "synthetic (seeded BASELINE cfg generator)",
-           "config": {"workload": args.workload, "grid": list(spec.grid), "channels": list(spec.channels),
+           "config": {"workload": args.workload + ("" if args.net == "config" else
+                                                f"+FastResUNet3D(b={args.base_channels},{'dense' if args.dense else 'depthwise'})"),
+                   "grid": list(spec.grid), "channels": list(spec.channels),
                       "C_z": spec.in_channels, "M": int(wl.matrix.n_measurements), "V": int(wl.matrix.n_masked),
                       "parallelism": "CPU, rank 0 only"},
            "cpu_baseline": {"value": round(v, 4), "unit": "it/s", "cores": threads, "kind": "port",
@@ -486,6 +495,10 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--workload", default="cfg1")
     ap.add_argument("--precision", default=None)
+    ap.add_argument("--net", default="config", choices=["config", "fast"],
+                    help="config: the BASELINE config ResUNet; fast: the reference's FastResUNet3D (NetworkConfig)")
+    ap.add_argument("--base-channels", type=int, default=8)
+    ap.add_argument("--dense", action="store_true", help="FastResUNet3D with dense 3^3 convs (use_depthwise=False)")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--skip-e2e", action="store_true")
     ap.add_argument("--skip-cpu", action="store_true")

@@ -30,6 +30,7 @@ struct RBlock {  // ResConv3d (priornet.py:134-148)
   int gx_acc = 0;
   float *t1 = nullptr, *h1 = nullptr, *p1 = nullptr, *xh1 = nullptr, *rs1 = nullptr;
   float *t2 = nullptr, *p2 = nullptr, *xh2 = nullptr, *rs2 = nullptr;
+  float* sb[7]{};  // backward scratch of this block (side-lane weight gradients read it: not shared)
 };
 
 struct SEP {  // SqueezeExcite (priornet.py:120-131)
@@ -42,6 +43,7 @@ struct AttP {  // AttentionGate3d (priornet.py:167-180), skip level l, gate leve
   ConvP key, query, score;
   int l = 0, inter = 0;
   float *k = nullptr, *q = nullptr, *pre = nullptr, *a = nullptr, *att_c = nullptr, *att_f = nullptr;
+  float* sb[4]{};  // backward: gatt_f, gatt_c, ga, gpre
 };
 
 struct RefNet {
@@ -66,6 +68,7 @@ struct RefNet {
   float *cat[3]{}, *gcat[3]{};           // decoder input at level l: [x_up (c_l+1) | gated (c_l)]
   float *d[3]{}, *gd[3]{};               // decoder output at level l
   float *raw = nullptr, *raw2 = nullptr, *sc[7]{};
+  float *asb[2]{}, *ssb[2]{};  // backward scratch of the ASPP norm and the stem norm
   long long maxvc = 0;
 };
 
@@ -223,6 +226,7 @@ void refnet_plan_workspace(d2ip_engine& E, Arena& A) {
     r.p2 = act(l, r.cout);
     r.xh2 = act(l, r.cout);
     r.rs2 = vox(l);
+    for (auto& p : r.sb) p = act(l, std::max(r.cin, r.cout));
     grow(l, std::max(r.cin, r.cout));
   };
   for (auto& r : N.enc) saved(r);
@@ -234,6 +238,10 @@ void refnet_plan_workspace(d2ip_engine& E, Arena& A) {
   N.b_rs = vox(3);
   N.xb = act(3, ch[3]);
   N.gxb = act(3, ch[3]);
+  N.asb[0] = act(3, ch[3]);
+  N.asb[1] = act(3, ch[3]);
+  N.ssb[0] = act(0, ch[0]);
+  N.ssb[1] = act(0, ch[0]);
   for (auto& a : N.att) {
     const int lg = a.l + 1;
     a.k = act(lg, a.inter);
@@ -242,6 +250,10 @@ void refnet_plan_workspace(d2ip_engine& E, Arena& A) {
     a.a = act(lg, a.inter);
     a.att_c = vox(lg);
     a.att_f = vox(a.l);
+    a.sb[0] = vox(a.l);
+    a.sb[1] = vox(lg);
+    a.sb[2] = act(lg, a.inter);
+    a.sb[3] = act(lg, a.inter);
     grow(lg, a.inter);
   }
   for (int l = 0; l < 3; ++l) {
@@ -457,12 +469,18 @@ int refnet_forward(Ctx& k) {
 // ---------------------------------------------------------------------------
 // backward
 
+// depthwise weight gradient on a side lane (its own reduction workspace)
+static int dw_wgrad_side(Ctx& k, d2ip_act x, d2ip_act gy, int stride, float* gw) {
+  Ctx ks = k;
+  D2IP_RET(side_ctx(k, ks));
+  return dw_conv_wgrad(x, gy, stride, gw, k.pbs, ks.wgws, k.E.wg_ws_bytes, k.B, ks.st);
+}
+
 static int rblock_bwd(Ctx& k, RBlock& r) {
   d2ip_engine& E = k.E;
-  RefNet& N = *E.ref;
   const int l = r.lout;
   const int co = r.cout;
-  auto S = [&](int i, int c) { return scratch(E, N.sc[i], l, c); };
+  auto S = [&](int i, int c) { return scratch(E, r.sb[i], l, c); };
   d2ip_act gpre = S(0, co), gc2 = S(1, co), gh1 = S(2, co), gpre1 = S(3, co), gc1 = S(4, co);
   d2ip_act h1 = scratch(E, r.h1, l, co), p1 = scratch(E, r.p1, l, co), p2 = scratch(E, r.p2, l, co);
   // norm2 (+ skip residual) + SiLU; `out` slot carries the saved pre-activation
@@ -470,27 +488,27 @@ static int rblock_bwd(Ctx& k, RBlock& r) {
                         E.na_ws, E.na_ws_bytes, k.B, k.st));
   if (r.dw) {
     d2ip_act t2 = scratch(E, r.t2, l, co), gt2 = S(5, co);
-    D2IP_RET(cwgrad(k, r.c2p, t2, gc2));
+    D2IP_RET(cwgrad_side(k, r.c2p, t2, gc2));
     D2IP_RET(cdgrad(k, r.c2p, gc2, gt2, 0));
-    D2IP_RET(dw_conv_wgrad(h1, gt2, 1, k.gr() + r.c2d.ow, k.pbs, E.wg_ws, E.wg_ws_bytes, k.B, k.st));
+    D2IP_RET(dw_wgrad_side(k, h1, gt2, 1, k.gr() + r.c2d.ow));
     D2IP_RET(dw_conv_dgrad(gt2, k.th() + r.c2d.ow, k.pbs, 1, gh1, 0, k.B, k.st));
   } else {
-    D2IP_RET(cwgrad(k, r.c2, h1, gc2));
+    D2IP_RET(cwgrad_side(k, r.c2, h1, gc2));
     D2IP_RET(cdgrad(k, r.c2, gc2, gh1, 0));
   }
   D2IP_RET(norm_act_bwd(gh1, p1, 2, 0.f, r.xh1, r.rs1, k.th() + r.n1.og, k.pbs, gpre1, gc1, k.gr() + r.n1.og, k.pbs,
                         E.na_ws, E.na_ws_bytes, k.B, k.st));
   if (r.dw) {
     d2ip_act t1 = scratch(E, r.t1, l, r.cin), gt1 = S(6, r.cin);
-    D2IP_RET(cwgrad(k, r.c1p, t1, gc1));
+    D2IP_RET(cwgrad_side(k, r.c1p, t1, gc1));
     D2IP_RET(cdgrad(k, r.c1p, gc1, gt1, 0));
-    D2IP_RET(dw_conv_wgrad(r.x, gt1, r.stride, k.gr() + r.c1d.ow, k.pbs, E.wg_ws, E.wg_ws_bytes, k.B, k.st));
+    D2IP_RET(dw_wgrad_side(k, r.x, gt1, r.stride, k.gr() + r.c1d.ow));
     D2IP_RET(dw_conv_dgrad(gt1, k.th() + r.c1d.ow, k.pbs, r.stride, r.gx, r.gx_acc, k.B, k.st));
   } else {
-    D2IP_RET(cwgrad(k, r.c1, r.x, gc1));
+    D2IP_RET(cwgrad_side(k, r.c1, r.x, gc1));
     D2IP_RET(cdgrad(k, r.c1, gc1, r.gx, r.gx_acc));
   }
-  D2IP_RET(cwgrad(k, r.sk, r.x, gpre));
+  D2IP_RET(cwgrad_side(k, r.sk, r.x, gpre));
   D2IP_RET(cdgrad(k, r.sk, gpre, r.gx, 1));
   return D2IP_OK;
 }
@@ -499,22 +517,21 @@ static int rblock_bwd(Ctx& k, RBlock& r) {
 // accumulates the gate gradient into ggate (already holding the upsample part).
 static int att_bwd(Ctx& k, AttP& a, d2ip_act skip, d2ip_act gate, d2ip_act gg, d2ip_act gs, d2ip_act ggate) {
   d2ip_engine& E = k.E;
-  RefNet& N = *E.ref;
   const int lg = a.l + 1;
-  float* gatt_f = N.sc[0];
-  float* gatt_c = N.sc[1];
+  float* gatt_f = a.sb[0];
+  float* gatt_c = a.sb[1];
   D2IP_RET(att_gate_bwd(gg, skip, a.att_f, gs, 0, gatt_f, k.B, k.st));
   d2ip_act gc = scratch(E, gatt_c, lg, 1);
   D2IP_RET(upsample2x_bwd(scratch(E, gatt_f, a.l, 1), gc, 0, k.B, k.st));
   D2IP_RET(sigmoid_bwd(gatt_c, a.att_c, (long long)k.B * E.V[lg], k.st));
   d2ip_act aa = scratch(E, a.a, lg, a.inter);
-  d2ip_act ga = scratch(E, N.sc[2], lg, a.inter), gpre = scratch(E, N.sc[3], lg, a.inter);
-  D2IP_RET(cwgrad(k, a.score, aa, gc));
+  d2ip_act ga = scratch(E, a.sb[2], lg, a.inter), gpre = scratch(E, a.sb[3], lg, a.inter);
+  D2IP_RET(cwgrad_side(k, a.score, aa, gc));
   D2IP_RET(cdgrad(k, a.score, gc, ga, 0));
   D2IP_RET(silu_bwd(ga, a.pre, gpre, k.B, k.st));
-  D2IP_RET(cwgrad(k, a.key, skip, gpre));
+  D2IP_RET(cwgrad_side(k, a.key, skip, gpre));
   D2IP_RET(cdgrad(k, a.key, gpre, gs, 1));
-  D2IP_RET(cwgrad(k, a.query, gate, gpre));
+  D2IP_RET(cwgrad_side(k, a.query, gate, gpre));
   D2IP_RET(cdgrad(k, a.query, gpre, ggate, 1));
   return D2IP_OK;
 }
@@ -524,16 +541,16 @@ static int aspp_bwd(Ctx& k) {
   RefNet& N = *E.ref;
   const int C = N.ch[3];
   const int W = N.nd * C;
-  d2ip_act gpre = scratch(E, N.sc[0], 3, C), gc = scratch(E, N.sc[1], 3, C);
+  d2ip_act gpre = scratch(E, N.asb[0], 3, C), gc = scratch(E, N.asb[1], 3, C);
   D2IP_RET(norm_act_bwd(view(E, N.gxb, 3, C, C), view(E, N.b_p, 3, C, C), 2, 0.f, N.b_xh, N.b_rs, k.th() + N.bn.og,
                         k.pbs, gpre, gc, k.gr() + N.bn.og, k.pbs, E.na_ws, E.na_ws_bytes, k.B, k.st));
   d2ip_act cat = view(E, N.acat, 3, W, W), gcat = view(E, N.gacat, 3, W, W);
-  D2IP_RET(cwgrad(k, N.proj, cat, gc));
+  D2IP_RET(cwgrad_side(k, N.proj, cat, gc));
   D2IP_RET(cdgrad(k, N.proj, gc, gcat, 0));
   d2ip_act x3 = view(E, N.x[3], 3, C, C), gx3 = view(E, N.gx[3], 3, C, C);
   for (int j = 0; j < N.nd; ++j) {
     d2ip_act gj = view(E, N.gacat + j * C, 3, C, W);
-    D2IP_RET(cwgrad(k, N.br[j], x3, gj));
+    D2IP_RET(cwgrad_side(k, N.br[j], x3, gj));
     D2IP_RET(cdgrad(k, N.br[j], gj, gx3, j > 0));
   }
   return D2IP_OK;
@@ -544,7 +561,7 @@ int refnet_backward(Ctx& k) {
   RefNet& N = *E.ref;
   const int* ch = N.ch;
   d2ip_act gt = view(E, E.gtail, 0, 1, 1);
-  D2IP_RET(cwgrad(k, N.tail, N.dec[2].out, gt));
+  D2IP_RET(cwgrad_side(k, N.tail, N.dec[2].out, gt));
   D2IP_RET(cdgrad(k, N.tail, gt, N.dec[2].gout, 0));
   for (int j = 2; j >= 0; --j) {
     const int l = 2 - j;
@@ -564,12 +581,12 @@ int refnet_backward(Ctx& k) {
                          k.th() + s.fc1.ob, k.th() + s.fc2.ow, k.pbs, s.hid, s.state, s.sbs, k.gr() + s.fc1.ow,
                          k.gr() + s.fc2.ow, view(E, N.gx[i], i, ch[i], ch[i]), 0, E.wg_ws, E.wg_ws_bytes, k.B, k.st));
   }
-  d2ip_act gpre = scratch(E, N.sc[0], 0, ch[0]), gc = scratch(E, N.sc[1], 0, ch[0]);
+  d2ip_act gpre = scratch(E, N.ssb[0], 0, ch[0]), gc = scratch(E, N.ssb[1], 0, ch[0]);
   D2IP_RET(norm_act_bwd(view(E, N.gx[0], 0, ch[0], ch[0]), view(E, N.stem_p, 0, ch[0], ch[0]), 2, 0.f, N.stem_xh,
                         N.stem_rs, k.th() + N.stem_n.og, k.pbs, gpre, gc, k.gr() + N.stem_n.og, k.pbs, E.na_ws,
                         E.na_ws_bytes, k.B, k.st));
   d2ip_act z = view(E, const_cast<float*>(E.b.z), 0, 1, 1);
-  return cwgrad(k, N.stem, z, gc);
+  return cwgrad_side(k, N.stem, z, gc);
 }
 
 }  // namespace d2ip

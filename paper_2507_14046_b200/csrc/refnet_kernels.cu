@@ -89,38 +89,64 @@ __global__ void __launch_bounds__(256) dw_dgrad_k(d2ip_act gy, const float* __re
 }
 
 // partial[b][chunk][c*27 + t] = sum_v gy[v][c] x[in(v,t)][c];  [27C + c] = sum_v gy[v][c]
+// One thread per (channel, voxel chunk) keeps all 27 taps + the bias in
+// registers and walks its chunk in order with incremental coordinates (each
+// gy value is read once; neighbouring x rows stay in L1).
 __global__ void __launch_bounds__(256) dw_wgrad_k(d2ip_act x, d2ip_act gy, int stride, float* __restrict__ partial,
                                                   int nchunks, int chunk) {
   D2IP_PDL_ENTRY();
-  const int b = blockIdx.z, ch = blockIdx.y;
+  const int b = blockIdx.y;
   const int C = x.c;
-  const int e = blockIdx.x * blockDim.x + threadIdx.x;  // (t, c) with c fastest; t == 27: bias
-  if (e >= 28 * C) return;
-  const int c = e % C, t = e / C;
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;  // (chunk, c), c fastest
+  if (e >= nchunks * C) return;
+  const int c = e % C, ch = e / C;
   const long long V = (long long)gy.d * gy.h * gy.w;
   const long long v0 = (long long)ch * chunk, v1 = min(V, v0 + chunk);
   const float* gb = gy.ptr + b * gy.bstride + c;
   const float* xb = x.ptr + b * x.bstride + c;
-  float acc = 0.f;
-  if (t == 27) {
-    for (long long v = v0; v < v1; ++v) acc += gb[v * gy.cstride];
-  } else {
-    const int kd = t / 9, kh = (t / 3) % 3, kw = t % 3;
-    for (long long v = v0; v < v1; ++v) {
-      const int ow = (int)(v % gy.w), oh = (int)((v / gy.w) % gy.h), od = (int)(v / ((long long)gy.w * gy.h));
-      const int id = od * stride + kd - 1, ih = oh * stride + kh - 1, iw = ow * stride + kw - 1;
-      if (id < 0 || id >= x.d || ih < 0 || ih >= x.h || iw < 0 || iw >= x.w) continue;
-      acc = fmaf(gb[v * gy.cstride], xb[(((long long)id * x.h + ih) * x.w + iw) * x.cstride], acc);
+  float acc[27], bacc = 0.f;
+#pragma unroll
+  for (int t = 0; t < 27; ++t) acc[t] = 0.f;
+  int ow = (int)(v0 % gy.w), oh = (int)((v0 / gy.w) % gy.h), od = (int)(v0 / ((long long)gy.w * gy.h));
+  for (long long v = v0; v < v1; ++v) {
+    const float g = gb[v * gy.cstride];
+    bacc += g;
+#pragma unroll
+    for (int kd = 0; kd < 3; ++kd) {
+      const int id = od * stride + kd - 1;
+      const bool okd = id >= 0 && id < x.d;
+#pragma unroll
+      for (int kh = 0; kh < 3; ++kh) {
+        const int ih = oh * stride + kh - 1;
+        const bool okh = okd && ih >= 0 && ih < x.h;
+#pragma unroll
+        for (int kw = 0; kw < 3; ++kw) {
+          const int iw = ow * stride + kw - 1;
+          if (okh && iw >= 0 && iw < x.w)
+            acc[(kd * 3 + kh) * 3 + kw] =
+                fmaf(g, xb[(((long long)id * x.h + ih) * x.w + iw) * x.cstride], acc[(kd * 3 + kh) * 3 + kw]);
+        }
+      }
+    }
+    if (++ow == gy.w) {
+      ow = 0;
+      if (++oh == gy.h) {
+        oh = 0;
+        ++od;
+      }
     }
   }
   float* p = partial + ((long long)b * nchunks + ch) * 28 * C;
-  p[t < 27 ? c * 27 + t : 27 * C + c] = acc;
+#pragma unroll
+  for (int t = 0; t < 27; ++t) p[c * 27 + t] = acc[t];
+  p[27 * C + c] = bacc;
 }
 
 static void dw_split(int C, long long V, int batch, int* nchunks, int* chunk) {
-  long long want = (148LL * 2048 + 28LL * C * batch - 1) / (28LL * C * batch);
-  want = std::min(want, std::max(1LL, V / 64));
-  want = std::min(want, 512LL);
+  // ~64K threads of (channel, chunk), >= 16 voxels per chunk, <= 1024 chunks (the reduce is per chunk)
+  long long want = (64LL * 1024 + (long long)C * batch - 1) / ((long long)C * batch);
+  want = std::min(want, std::max(1LL, V / 16));
+  want = std::min(want, 1024LL);
   if (want < 1) want = 1;
   *chunk = (int)((V + want - 1) / want);
   *nchunks = (int)((V + *chunk - 1) / *chunk);
@@ -154,8 +180,8 @@ int dw_conv_wgrad(d2ip_act x, d2ip_act gy, int stride, float* gw, long long gwbs
   dw_split(C, V, batch, &nchunks, &chunk);
   D2IP_CHECK_ARG(ws_bytes >= (size_t)batch * nchunks * 28 * C * sizeof(float), "dw_wgrad: workspace too small");
   float* partial = reinterpret_cast<float*>(ws);
-  D2IP_CUDA(launch_pdl(dw_wgrad_k, dim3(cdiv(28 * C, 256), nchunks, batch), 256, 0, st, x, gy, stride, partial,
-                       nchunks, chunk));
+  D2IP_CUDA(launch_pdl(dw_wgrad_k, dim3(cdiv((long long)nchunks * C, 256), batch), 256, 0, st, x, gy, stride,
+                       partial, nchunks, chunk));
   return reduce_chunks(partial, nchunks, 28 * C, gw, gwbs, batch, st);
 }
 
