@@ -9,6 +9,8 @@
 // The step t is read from device memory (graph-replay safe). An iteration
 // whose loss was non-finite (bad flag set) skips the update, mirroring the
 // reference raising before `optimizer.step()` (pipeline.py:312-317).
+#include <algorithm>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -24,8 +26,10 @@ __device__ __forceinline__ void adam_one(float& p, float g, float& m, float& v, 
   p = p + (-step_size) * (m / denom);
 }
 
-__global__ void __launch_bounds__(256) adam_k(float4* __restrict__ p, const float4* __restrict__ g,
-                                              float4* __restrict__ m, float4* __restrict__ v, long long n4,
+// One launch: float4 body over the 16-byte-aligned prefix, scalar remainder
+// (n % 4 elements, or everything when a pointer is misaligned) in the same grid.
+__global__ void __launch_bounds__(256) adam_k(float* __restrict__ p, const float* __restrict__ g,
+                                              float* __restrict__ m, float* __restrict__ v, long long n4, long long n,
                                               float lr, float b1, float b2, float eps,
                                               const int* __restrict__ step, const int* __restrict__ bad) {
   D2IP_PDL_ENTRY();
@@ -36,49 +40,33 @@ __global__ void __launch_bounds__(256) adam_k(float4* __restrict__ p, const floa
   const float step_size = (float)((double)lr / bc1);
   const float bc2s = (float)sqrt(bc2);
   const float w1 = (float)(1.0 - (double)b1), omb2 = (float)(1.0 - (double)b2);
-  for (long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x; i < n4;
-       i += (long long)gridDim.x * blockDim.x) {
-    float4 pp = p[i], gg = g[i], mm = m[i], vv = v[i];
+  const long long tid = (long long)blockIdx.x * blockDim.x + threadIdx.x, nth = (long long)gridDim.x * blockDim.x;
+  float4* p4 = reinterpret_cast<float4*>(p);
+  const float4* g4 = reinterpret_cast<const float4*>(g);
+  float4* m4 = reinterpret_cast<float4*>(m);
+  float4* v4 = reinterpret_cast<float4*>(v);
+  for (long long i = tid; i < n4; i += nth) {
+    float4 pp = p4[i], gg = g4[i], mm = m4[i], vv = v4[i];
     adam_one(pp.x, gg.x, mm.x, vv.x, w1, b2, omb2, step_size, bc2s, eps);
     adam_one(pp.y, gg.y, mm.y, vv.y, w1, b2, omb2, step_size, bc2s, eps);
     adam_one(pp.z, gg.z, mm.z, vv.z, w1, b2, omb2, step_size, bc2s, eps);
     adam_one(pp.w, gg.w, mm.w, vv.w, w1, b2, omb2, step_size, bc2s, eps);
-    p[i] = pp;
-    m[i] = mm;
-    v[i] = vv;
+    p4[i] = pp;
+    m4[i] = mm;
+    v4[i] = vv;
   }
-}
-
-__global__ void adam_tail_k(float* p, const float* g, float* m, float* v, long long start, long long n,
-                            float lr, float b1, float b2, float eps, const int* step, const int* bad) {
-  D2IP_PDL_ENTRY();
-  if (bad && *bad) return;
-  const long long i = start + blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= n) return;
-  const int t = *step;
-  const double bc1 = 1.0 - pow((double)b1, (double)t);
-  const double bc2 = 1.0 - pow((double)b2, (double)t);
-  adam_one(p[i], g[i], m[i], v[i], (float)(1.0 - (double)b1), b2, (float)(1.0 - (double)b2),
-           (float)((double)lr / bc1), (float)sqrt(bc2), eps);
+  for (long long i = 4 * n4 + tid; i < n; i += nth) adam_one(p[i], g[i], m[i], v[i], w1, b2, omb2, step_size, bc2s, eps);
 }
 
 int adam_flat(float* p, const float* g, float* m, float* v, long long n, float lr, float b1, float b2,
               float eps, const int* step, const int* bad, cudaStream_t st) {
   const bool aligned = (((uintptr_t)p | (uintptr_t)g | (uintptr_t)m | (uintptr_t)v) & 15) == 0;
   const long long n4 = aligned ? n / 4 : 0;
-  if (n4 > 0) {
-    long long blocks = (n4 + 255) / 256;
-    if (blocks > 148LL * 16) blocks = 148LL * 16;
-    D2IP_CUDA(launch_pdl(adam_k, (int)blocks, 256, 0, st, reinterpret_cast<float4*>(p), reinterpret_cast<const float4*>(g),
-                                        reinterpret_cast<float4*>(m), reinterpret_cast<float4*>(v), n4, lr,
-                                        b1, b2, eps, step, bad));
-    D2IP_LAUNCH_CHECK();
-  }
-  const long long rest = n - n4 * 4;
-  if (rest > 0) {
-    D2IP_CUDA(launch_pdl(adam_tail_k, cdiv(rest, 256), 256, 0, st, p, g, m, v, n4 * 4, n, lr, b1, b2, eps, step, bad));
-    D2IP_LAUNCH_CHECK();
-  }
+  long long blocks = (std::max(n4, n - 4 * n4) + 255) / 256;
+  if (blocks > 148LL * 16) blocks = 148LL * 16;
+  if (blocks < 1) blocks = 1;
+  D2IP_CUDA(launch_pdl(adam_k, (int)blocks, 256, 0, st, p, g, m, v, n4, n, lr, b1, b2, eps, step, bad));
+  D2IP_LAUNCH_CHECK();
   return D2IP_OK;
 }
 

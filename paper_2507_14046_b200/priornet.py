@@ -28,7 +28,7 @@ from __future__ import annotations
 
 import hashlib
 import json
-from dataclasses import dataclass
+from dataclasses import dataclass, field
 
 import numpy as np
 import torch
@@ -271,43 +271,70 @@ class ParameterState:
     tensors: dict
     iteration_counter: int = 0
     provenance: str = "kaiming_init"
+    # host-side caches (not part of the value): the sha256 of the tensors, and
+    # the flat fp32 buffer the state was exported from (same bytes)
+    _sha: str | None = field(default=None, repr=False, compare=False)
+    _flat: torch.Tensor | None = field(default=None, repr=False, compare=False)
 
     def __post_init__(self):
         if self.provenance not in PROVENANCES:
             raise ValueError(f"unknown provenance {self.provenance!r}")
+        if self._flat is not None:  # exported from one flat buffer: one vectorised finiteness check
+            if not bool(torch.isfinite(self._flat).all()):
+                for name, t in self.tensors.items():
+                    if not torch.isfinite(t).all():
+                        raise ValueError(f"parameter tensor {name} contains non-finite values")
+            return
         for name, t in self.tensors.items():
             if not torch.isfinite(t).all():
                 raise ValueError(f"parameter tensor {name} contains non-finite values")
 
     def clone(self, provenance=None, iteration_counter=None) -> "ParameterState":
+        flat = self._flat.clone() if self._flat is not None else None
+        if flat is not None:  # the clones are views of one new flat buffer, like the original
+            tensors, o = {}, 0
+            for k, v in self.tensors.items():
+                tensors[k] = flat[o:o + v.numel()].view(v.shape)
+                o += v.numel()
+        else:
+            tensors = {k: v.detach().clone() for k, v in self.tensors.items()}
         return ParameterState(
-            tensors={k: v.detach().clone() for k, v in self.tensors.items()},
+            tensors=tensors,
             iteration_counter=self.iteration_counter if iteration_counter is None else iteration_counter,
             provenance=self.provenance if provenance is None else provenance,
+            _sha=self._sha, _flat=flat,
         )
 
     def checksum(self) -> str:
+        if self._sha is not None:
+            return self._sha
         digest = hashlib.sha256()
         for name, t in self.tensors.items():
             digest.update(name.encode())
             digest.update(t.detach().cpu().contiguous().numpy().tobytes())
-        return digest.hexdigest()
+        # cached: the tensors are detached clones handed between stages, never mutated in place
+        object.__setattr__(self, "_sha", digest.hexdigest())
+        return self._sha
 
     def flat(self, schema=None) -> torch.Tensor:
         """Concatenate into the engine's flat fp32 layout (state-dict order)."""
         names = [e.name for e in schema] if schema is not None else list(self.tensors)
+        if self._flat is not None and names == list(self.tensors):
+            return self._flat
         return torch.cat([self.tensors[n].detach().reshape(-1).to(torch.float32).cpu() for n in names])
 
 
 def state_from_flat(flat: torch.Tensor, schema, iteration_counter=0, provenance="kaiming_init") -> ParameterState:
-    flat = flat.detach().to("cpu", torch.float32).contiguous()
+    """Tensors are views of one private host copy of `flat` (one D2H copy, one
+    finiteness check, and `flat()` can hand the buffer back without a cat)."""
+    flat = flat.detach().to("cpu", torch.float32).contiguous().clone()
     tensors, o = {}, 0
     for e in schema:
-        tensors[e.name] = flat[o:o + e.numel].reshape(e.shape).clone()
+        tensors[e.name] = flat[o:o + e.numel].view(e.shape)
         o += e.numel
     if o != flat.numel():
         raise ValueError(f"flat buffer has {flat.numel()} values, schema needs {o}")
-    return ParameterState(tensors, iteration_counter, provenance)
+    return ParameterState(tensors, iteration_counter, provenance, _flat=flat)
 
 
 def kaiming_flat(cfg, seed: int | None = None) -> torch.Tensor:
