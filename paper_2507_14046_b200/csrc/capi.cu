@@ -52,7 +52,9 @@ int conv_wgrad(d2ip_act x, d2ip_act gy, int ks, int stride, float* gw, long long
     set_variant("wgrad_tcgen05_tf32x3");
     return wgrad_tc(x, gy, ks, gw, gwbs, ws, ws_bytes, batch, st);
   }
-  if (stride == 1 && wgrad_s1_supported(x, gy, ks)) {
+  // 1^3 (skip) layers: the lane-split tiled kernel; the smem-tiled s1 kernel would
+  // run one warp per CTA there (centre tap only; measured 30-40 us vs ~10 us)
+  if (stride == 1 && ks == 3 && wgrad_s1_supported(x, gy, ks)) {
     set_variant("wgrad_s1_smem");
     return wgrad_s1(x, gy, ks, gw, gwbs, ws, ws_bytes, batch, st);
   }
