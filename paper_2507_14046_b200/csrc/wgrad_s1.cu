@@ -195,8 +195,21 @@ static int pick_block(int c, std::initializer_list<int> opts) {
 static bool wg_plan(int D, int H, int W, int Cin, int Cout, int ks, int batch, WgS1& a) {
   a.ks = ks;
   if (Cin % 4 || Cout % 8) return false;
-  a.CIB = pick_block(Cin, {32, 16, 8, 4});
+  // channel tiles: 9 taps x CIB/4 x COB/8 threads per CTA; prefer tiles that
+  // fill whole warps (e.g. C_in = 48: CIB = 48 -> 216 threads, not 16 -> 72 of 96)
   a.COB = pick_block(Cout, {32, 16, 8});
+  a.CIB = 0;
+  if (a.COB)
+    for (int cib : {32, 48, 24, 16, 8, 4}) {
+      if (cib > Cin || Cin % cib) continue;
+      const int thr = (ks == 3 ? 9 : 1) * (cib / 4) * (a.COB / 8);
+      if (thr > 288) continue;
+      if (!a.CIB) a.CIB = cib;                 // largest-first fallback
+      if (thr % 32 == 0 || thr >= 192) {       // whole warps, or big enough that the tail warp matters little
+        a.CIB = cib;
+        break;
+      }
+    }
   if (!a.CIB || !a.COB) return false;
   a.ncib = Cin / a.CIB;
   a.ncob = Cout / a.COB;
