@@ -41,7 +41,7 @@ constexpr int kTcThreads = 256;  // 8 warps: fills / splits spread wider; epilog
 constexpr int kTcRows = 128;
 
 __host__ __device__ static inline int np_of(int n) { return (n + 15) / 16 * 16; }
-static inline int wr_of(int sw) { return kTcRows + 2 * sw + 2; }
+static inline int wr_of(int sw, int T = 1) { return T * kTcRows + 2 * sw + 2; }
 static inline int wrp_of(int wr) { return wr + ((1 - wr) % 8 + 8) % 8; }  // = 1 mod 8: conflict-free fills
 
 struct TcConv {
@@ -54,6 +54,7 @@ struct TcConv {
   d2ip_act y;
   int accumulate;
   int N, Np, Ns, Kc, CB, n_cb, WR, WRp, Sw, Sh, u_first, tmem_cols;  // Ns: N columns per CTA (slice)
+  int T;        // 128-row tiles per CTA: T TMEM accumulators share every stage's weight tile
   uint32_t idesc;
   int kspl;     // split-K factor over the (plane tap, channel block) stages
   float* part;  // kspl > 1: partial sums [b][kspl][V][N]
@@ -73,7 +74,7 @@ __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__flo
 
 // NKC = CB / 4: 16-byte channel chunks per stage (compile-time, so the fill
 // loops need no integer division).
-template <int NKC>
+template <int NKC, int T>
 __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
   D2IP_PDL_ENTRY();
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -82,7 +83,7 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
   const int b = blockIdx.z;
   const int ks = blockIdx.y % a.kspl;
   const int n0 = (blockIdx.y / a.kspl) * a.Ns;  // first output channel of this CTA's slice
-  const int u0 = a.u_first + blockIdx.x * kTcRows;
+  const int u0 = a.u_first + blockIdx.x * T * kTcRows;
   const int Ns = a.Ns, WR = a.WR, WRp = a.WRp;
   const uint32_t Ab = (uint32_t)NKC * WRp * 16, Bb = (uint32_t)9 * NKC * Ns * 16;
   const uint32_t Sb = 2 * (Ab + Bb);
@@ -190,12 +191,16 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
         const int rowoff = (t9 / 3) * a.Sw + (t9 % 3);
 #pragma unroll
         for (int j = 0; j < NKC / 2; ++j) {
-          const uint64_t ao = boff + (uint64_t)(2 * j * WRp + rowoff);
           const uint64_t bo = boff + (uint64_t)((t9 * NKC + 2 * j) * Ns);
           const uint32_t first = (s | t9 | j) ? 1u : 0u;
-          tc::mma_tf32(tmem, dAlo + ao, dBhi + bo, a.idesc, first);
-          tc::mma_tf32(tmem, dAhi + ao, dBlo + bo, a.idesc, 1u);
-          tc::mma_tf32(tmem, dAhi + ao, dBhi + bo, a.idesc, 1u);
+#pragma unroll
+          for (int tt = 0; tt < T; ++tt) {  // sub-tile tt: rows + 128 tt, accumulator columns + tt Ns
+            const uint64_t ao = boff + (uint64_t)(2 * j * WRp + rowoff + tt * kTcRows);
+            const uint32_t d = tmem + (uint32_t)(tt * Ns);
+            tc::mma_tf32(d, dAlo + ao, dBhi + bo, a.idesc, first);
+            tc::mma_tf32(d, dAhi + ao, dBlo + bo, a.idesc, 1u);
+            tc::mma_tf32(d, dAhi + ao, dBhi + bo, a.idesc, 1u);
+          }
         }
       }
       tc::commit(&mbar[buf]);
@@ -204,49 +209,49 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
   tc::mbar_wait(&mbar[(S - 1) & 1], ((S - 1) >> 1) & 1);
   tc::fence_after();
 
-  // epilogue: TMEM lane = GEMM row; each thread owns one row / voxel.
+  // epilogue: TMEM lane = GEMM row; each thread owns one row / voxel per sub-tile.
   // warp w reads TMEM lane quadrant w % 4 (rows) and column half w / 4
   const int row = (warp & 3) * 32 + lane;
   const int chalf = a.Ns / 2, cbeg = (warp >> 2) * chalf, cend = cbeg + chalf;
-  const int u = u0 + row;
-  int v = -1;
-  {
-    const int dp = u / a.Sh, rem = u - dp * a.Sh;
-    const int hp = rem / a.Sw, wp = rem - hp * a.Sw;
-    if (dp >= 1 && dp <= x.d && hp >= 1 && hp <= x.h && wp >= 1 && wp <= x.w)
-      v = ((dp - 1) * x.h + (hp - 1)) * x.w + (wp - 1);
-  }
   const d2ip_act y = a.y;
   const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16);
-  if (a.kspl > 1) {  // raw partial sums; conv_tc_splitk_reduce_k adds bias / accumulates
-    float* pp = v >= 0 ? a.part + (((long long)b * a.kspl + ks) * a.vout + v) * a.N : nullptr;
+  const float* bias = a.bias ? a.bias + b * a.bbs : nullptr;
+  for (int tt = 0; tt < T; ++tt) {
+    const int u = u0 + tt * kTcRows + row;
+    int v = -1;
+    {
+      const int dp = u / a.Sh, rem = u - dp * a.Sh;
+      const int hp = rem / a.Sw, wp = rem - hp * a.Sw;
+      if (dp >= 1 && dp <= x.d && hp >= 1 && hp <= x.h && wp >= 1 && wp <= x.w)
+        v = ((dp - 1) * x.h + (hp - 1)) * x.w + (wp - 1);
+    }
+    const uint32_t tcol = trow + (uint32_t)(tt * Ns);
+    if (a.kspl > 1) {  // raw partial sums; the consumer adds bias / accumulates
+      float* pp = v >= 0 ? a.part + (((long long)b * a.kspl + ks) * a.vout + v) * a.N : nullptr;
+      for (int c0 = cbeg; c0 < cend; c0 += 8) {
+        float vals[8];
+        tc::tmem_ld8(tcol + c0, vals);
+        if (pp) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (n0 + c0 + j < a.N) pp[n0 + c0 + j] = vals[j];
+        }
+      }
+      continue;
+    }
+    float* yp = v >= 0 ? y.ptr + b * y.bstride + (long long)v * y.cstride : nullptr;
     for (int c0 = cbeg; c0 < cend; c0 += 8) {
       float vals[8];
-      tc::tmem_ld8(trow + c0, vals);
-      if (pp) {
+      tc::tmem_ld8(tcol + c0, vals);
+      if (yp) {
 #pragma unroll
-        for (int j = 0; j < 8; ++j)
-          if (n0 + c0 + j < a.N) pp[n0 + c0 + j] = vals[j];
-      }
-    }
-    tc::fence_before();
-    __syncthreads();
-    if (warp == 0) tc::tmem_free(tmem, a.tmem_cols);
-    return;
-  }
-  float* yp = v >= 0 ? y.ptr + b * y.bstride + (long long)v * y.cstride : nullptr;
-  const float* bias = a.bias ? a.bias + b * a.bbs : nullptr;
-  for (int c0 = cbeg; c0 < cend; c0 += 8) {
-    float vals[8];
-    tc::tmem_ld8(trow + c0, vals);
-    if (yp) {
-#pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        const int n = n0 + c0 + j;
-        if (n < a.N) {
-          float o = vals[j] + (bias ? __ldg(bias + n) : 0.f);
-          if (a.accumulate) o += yp[n];
-          yp[n] = o;
+        for (int j = 0; j < 8; ++j) {
+          const int n = n0 + c0 + j;
+          if (n < a.N) {
+            float o = vals[j] + (bias ? __ldg(bias + n) : 0.f);
+            if (a.accumulate) o += yp[n];
+            yp[n] = o;
+          }
         }
       }
     }
@@ -372,32 +377,52 @@ static bool tc_plan(int D, int H, int W, int K, int N, int batch, TcConv& a, int
   a.Kc = K;
   a.Sw = W + 2;
   a.Sh = (H + 2) * a.Sw;
-  a.WR = wr_of(a.Sw);
-  a.WRp = wrp_of(a.WR);
   a.u_first = a.Sh + a.Sw + 1;
   const int u_last = D * a.Sh + H * a.Sw + W;
-  *tiles = cdiv(u_last - a.u_first + 1, kTcRows);
+  const int tiles1 = cdiv(u_last - a.u_first + 1, kTcRows);
   a.vout = (long long)D * H * W;
   a.CB = 0;
+  a.T = 1;
   double best = 1e30;
-  for (int ns = std::min(a.Np, 256); ns >= 16; ns -= 16) {
-    if (a.Np % ns) continue;
-    for (int cb = 8; cb <= K && cb <= 64; cb *= 2) {
-      if (K % cb) continue;
-      const size_t sm = 2 * stage_bytes(cb, ns, a.WRp) + 3 * a.WR * sizeof(int) + 64;
-      if (sm > (size_t)210 * 1024) continue;
-      const int per_sm = sm <= (size_t)110 * 1024 ? 2 : 1;
-      const long long ctas0 = (long long)*tiles * (a.Np / ns) * batch;
-      const int S = 3 * (K / cb);
-      // split the stage chain across CTAs until ~2 CTAs per SM are busy
-      const int kspl = (int)std::min<long long>(S, std::max(1LL, (296 + ctas0 - 1) / ctas0));
-      const long long waves = (ctas0 * kspl + 148LL * per_sm - 1) / (148LL * per_sm);
-      const double cost = (double)waves * ((S + kspl - 1) / kspl + 2.0) + (kspl > 1 ? 1.0 : 0.0);
-      if (cost < best - 1e-9) {
-        best = cost;
-        a.CB = cb;
-        a.Ns = ns;
-        a.kspl = kspl;
+  // Large layers (>= 4 waves of single tiles): T tiles per CTA share each
+  // stage's weight tile and per-CTA overhead; scored by a latency model in us:
+  // a stage costs max(cp.async landing ~1.5, its MMAs: 27/8 CB T x 57 cycles).
+  const bool large = (long long)tiles1 * batch >= 4LL * 296;
+  for (int T : {1, 2, 4}) {
+    if (T > 1 && !large) break;
+    const int wr = wr_of(a.Sw, T), wrp = wrp_of(wr);
+    const int tl = cdiv(tiles1, T);
+    for (int ns = std::min(a.Np, 256); ns >= 16; ns -= 16) {
+      if (a.Np % ns) continue;
+      if (T * ns > 512) continue;  // TMEM columns
+      for (int cb = 8; cb <= K && cb <= 64; cb *= 2) {
+        if (K % cb) continue;
+        const size_t sm = 2 * stage_bytes(cb, ns, wrp) + 3 * wr * sizeof(int) + 64;
+        if (sm > (size_t)210 * 1024) continue;
+        const int per_sm = sm <= (size_t)110 * 1024 ? 2 : 1;
+        const long long ctas0 = (long long)tl * (a.Np / ns) * batch;
+        const int S = 3 * (K / cb);
+        // split the stage chain across CTAs until ~2 CTAs per SM are busy
+        const int kspl = (int)std::min<long long>(S, std::max(1LL, (296 + ctas0 - 1) / ctas0));
+        const long long waves = (ctas0 * kspl + 148LL * per_sm - 1) / (148LL * per_sm);
+        double cost;
+        if (!large) {
+          cost = (double)waves * ((S + kspl - 1) / kspl + 2.0) + (kspl > 1 ? 1.0 : 0.0);
+        } else {
+          const double mma_us = 27.0 / 8.0 * cb * T * 57.0 / 1900.0 * (per_sm == 2 ? 1.4 : 1.0);
+          const double stage_us = std::max(1.5, mma_us);
+          cost = (double)waves * ((S + kspl - 1) / kspl * stage_us + 2.0 + 0.5 * T) + (kspl > 1 ? 3.0 : 0.0);
+        }
+        if (cost < best - 1e-9) {
+          best = cost;
+          a.CB = cb;
+          a.Ns = ns;
+          a.kspl = kspl;
+          a.T = T;
+          a.WR = wr;
+          a.WRp = wrp;
+          *tiles = tl;
+        }
       }
     }
   }
@@ -432,24 +457,33 @@ int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, lo
   a.y = y;
   a.accumulate = accumulate;
   int cols = 32;
-  while (cols < a.Ns) cols *= 2;
+  while (cols < a.T * a.Ns) cols *= 2;
   a.tmem_cols = cols;
   a.idesc = tc::make_idesc(2, kTcRows, a.Ns);
   const size_t smem = tc_smem_bytes(a);
   static bool attr_set = false;
   if (!attr_set) {
-    for (auto k : {conv_tc_k<2>, conv_tc_k<4>, conv_tc_k<8>, conv_tc_k<16>})
+    for (auto k : {conv_tc_k<2, 1>, conv_tc_k<4, 1>, conv_tc_k<8, 1>, conv_tc_k<16, 1>, conv_tc_k<2, 2>,
+                   conv_tc_k<4, 2>, conv_tc_k<8, 2>, conv_tc_k<16, 2>, conv_tc_k<2, 4>, conv_tc_k<4, 4>,
+                   conv_tc_k<8, 4>, conv_tc_k<16, 4>})
       D2IP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr_set = true;
   }
   const dim3 grid(tiles, (a.Np / a.Ns) * a.kspl, batch);
+#define D2IP_TC_LAUNCH(NKC_)                                                                              \
+  do {                                                                                                    \
+    if (a.T == 4) D2IP_CUDA(launch_pdl((conv_tc_k<NKC_, 4>), grid, kTcThreads, smem, st, a));            \
+    else if (a.T == 2) D2IP_CUDA(launch_pdl((conv_tc_k<NKC_, 2>), grid, kTcThreads, smem, st, a));       \
+    else D2IP_CUDA(launch_pdl((conv_tc_k<NKC_, 1>), grid, kTcThreads, smem, st, a));                     \
+  } while (0)
   switch (a.CB / 4) {
-    case 2: D2IP_CUDA(launch_pdl(conv_tc_k<2>, grid, kTcThreads, smem, st, a)); break;
-    case 4: D2IP_CUDA(launch_pdl(conv_tc_k<4>, grid, kTcThreads, smem, st, a)); break;
-    case 8: D2IP_CUDA(launch_pdl(conv_tc_k<8>, grid, kTcThreads, smem, st, a)); break;
-    case 16: D2IP_CUDA(launch_pdl(conv_tc_k<16>, grid, kTcThreads, smem, st, a)); break;
+    case 2: D2IP_TC_LAUNCH(2); break;
+    case 4: D2IP_TC_LAUNCH(4); break;
+    case 8: D2IP_TC_LAUNCH(8); break;
+    case 16: D2IP_TC_LAUNCH(16); break;
     default: D2IP_CHECK_ARG(false, "conv_tc: unsupported channel block %d", a.CB);
   }
+#undef D2IP_TC_LAUNCH
   D2IP_LAUNCH_CHECK();
   if (deferred) *deferred = a.kspl > 1 ? a.kspl : 0;
   if (a.kspl > 1 && !deferred) {
