@@ -98,22 +98,34 @@ __device__ __forceinline__ void mbar_init(uint64_t* mbar, uint32_t count) {
   asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(mbar)), "r"(count) : "memory");
 }
 
-// Bounded wait: a phase that never completes (a bug) traps after ~seconds
-// instead of hanging the GPU.
+// Bounded wait: a phase that never completes (a bug) traps after ~2 s of
+// global time instead of hanging the GPU. No suspend-time hint: a hinted
+// try_wait compiles to NANOSLEEP.SYNCS sleeps, which cost warp-specialised
+// pipelines (long producer / consumer waits) up to 100x.
 __device__ __forceinline__ void mbar_wait(uint64_t* mbar, uint32_t parity) {
   const uint32_t a = smem_u32(mbar);
+  uint64_t t0 = 0;
   for (uint32_t n = 0;; ++n) {
     uint32_t done;
     asm volatile(
         "{\n\t.reg .pred P1;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2, %3;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 P1, [%1], %2;\n\t"
         "selp.b32 %0, 1, 0, P1;\n\t}"
         : "=r"(done)
-        : "r"(a), "r"(parity), "r"(0x100000u)
+        : "r"(a), "r"(parity)
         : "memory");
     if (done) return;
-    if (n > 4000) asm volatile("trap;");
+    if ((n & 1023) == 1023) {
+      uint64_t t;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+      if (!t0) t0 = t;
+      else if (t - t0 > 2000000000ull) asm volatile("trap;");
+    }
   }
+}
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* mbar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(mbar)) : "memory");
 }
 
 __device__ __forceinline__ void fence_mbar_init() {

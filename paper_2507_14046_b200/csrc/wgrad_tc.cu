@@ -35,7 +35,8 @@
 
 namespace d2ip {
 
-constexpr int kWtThreads = 128;
+constexpr int kWtThreads = 160;  // warp 0: MMA issue; warps 1-4: producers (loads, splits, epilogue)
+constexpr int kWtProd = 128;
 
 struct WgTc {
   d2ip_act x, gy;
@@ -55,6 +56,7 @@ struct WgTc {
   uint32_t Sx, Sg;     // bytes of one x (hi or lo) / gy (hi or lo) buffer
   uint32_t Sb;         // bytes of one stage
   uint32_t pad;        // bytes after the stages covering MMA reads of padded blocks
+  int NSTG;            // stages in the ring
   int tmem_cols;
   uint32_t idesc;
   float* part;         // [b][rg][ntaps * Cin * Cout + Cout]
@@ -80,6 +82,10 @@ __device__ __forceinline__ uint32_t mn32_off(int r, int c, uint32_t B) {
 }
 
 // NCHXP / NCHGP: chunks per row rounded up to a power of two (lane -> (row, chunk)).
+// Warp-specialised: warp 0 (one elected lane) issues the MMAs of a stage as
+// soon as the four producer warps have landed and split it (`full` barrier),
+// and hands the slot back through `tcgen05.commit` (`empty`); producers run
+// up to NSTG stages ahead, so loads and splits overlap the tensor pipe.
 template <int NCHXP, int NCHGP>
 __global__ void __launch_bounds__(kWtThreads) wgrad_tc_k(WgTc a) {
   D2IP_PDL_ENTRY();
@@ -91,20 +97,26 @@ __global__ void __launch_bounds__(kWtThreads) wgrad_tc_k(WgTc a) {
   const int t0 = grp * a.G;  // first tap of this CTA
   const int kd = a.ntaps == 27 ? t0 / 9 : 1;
   const bool do_bias = grp == 0 && cbk == 0;
-  const int RS = a.RS, WR = a.WR, RSg = a.RSg;
+  const int RS = a.RS, WR = a.WR, RSg = a.RSg, NSTG = a.NSTG;
   const d2ip_act x = a.x, gy = a.gy;
   const float* xb = x.ptr + b * x.bstride + cbk * a.cib;
   const float* gb = gy.ptr + b * gy.bstride;
-  // stage layout: [x hi][x lo][gy hi][gy lo] (1024-aligned regions); two stages,
-  // the read pad, mbarriers, TMEM slot, bias partials
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + 2 * a.Sb + a.pad);
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(mbar + 2);
-  float4* bred = reinterpret_cast<float4*>(tslot + 4);  // [128] bias partials
+  // layout: NSTG stages of [x hi][x lo][gy hi][gy lo] (1024-aligned regions), the
+  // read pad, barriers full[NSTG] empty[NSTG] done, TMEM slot, bias partials
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)NSTG * a.Sb + a.pad);
+  uint64_t* empty = full + NSTG;
+  uint64_t* done = empty + NSTG;
+  uint8_t* tail = smem + (size_t)NSTG * a.Sb + a.pad + (((2 * NSTG + 1) * 8 + 15) & ~15);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tail);
+  float4* bred = reinterpret_cast<float4*>(tail + 16);  // [kWtProd] bias partials (layout: see wt_smem)
 
   if (warp == 0) tc::tmem_alloc(tslot, a.tmem_cols);
   if (tid == 0) {
-    tc::mbar_init(&mbar[0], 1);
-    tc::mbar_init(&mbar[1], 1);
+    for (int i = 0; i < NSTG; ++i) {
+      tc::mbar_init(&full[i], kWtProd);
+      tc::mbar_init(&empty[i], 1);
+    }
+    tc::mbar_init(done, 1);
     tc::fence_mbar_init();
   }
   tc::fence_before();
@@ -113,145 +125,139 @@ __global__ void __launch_bounds__(kWtThreads) wgrad_tc_k(WgTc a) {
   const uint32_t tmem = *tslot;
   const int c_lo = rg * a.chunks_per_rg, c_hi = min(a.nchunk, c_lo + a.chunks_per_rg);
   const int S = c_hi - c_lo;
-  // x window row r <-> u0 + (kd-1) Sh - Sw - 1 + r (3^3), u0 + (kd-1) Sh - Sw + r
-  // (stacked: the kw shift lives on the gy side), u0 + r (1^3); gy row r <-> u0 - stack + r
-  const int xshift = a.ntaps == 27 ? (kd - 1) * a.Sh - a.Sw - (a.stack ? 0 : 1) : 0;
-  constexpr int XR = 32 / NCHXP, GR = 32 / NCHGP;  // rows per warp step
-  const int xr = lane / NCHXP, xc = lane % NCHXP, gr = lane / NCHGP, gc = lane % NCHGP;
-  float4 bacc = make_float4(0.f, 0.f, 0.f, 0.f);
-
-  auto load = [&](int sl, int buf) {
-    const int u0 = a.u_first + (c_lo + sl) * RS;
-    uint8_t* X = smem + buf * a.Sb;
-    uint8_t* Gt = X + 2 * a.Sx;
-    for (int r0 = warp * XR; r0 < WR; r0 += 4 * XR) {
-      const int r = r0 + xr;
-      if (r < WR && xc < a.nchx) {
-        const int v = wg_voxel(a, u0 + xshift + r);
-        const float* src = v >= 0 ? xb + (long long)v * x.cstride + 4 * xc : xb;
-        tc::cp_async16(X + mn32_off(r, xc, a.Bx), src, v >= 0 ? 16u : 0u);
-      }
-    }
-    for (int r0 = warp * GR; r0 < RSg; r0 += 4 * GR) {
-      const int r = r0 + gr;
-      if (r < RSg && gc < a.nchg) {
-        const int v = wg_voxel(a, u0 - a.stack + r);
-        const float* src = v >= 0 ? gb + (long long)v * gy.cstride + 4 * gc : gb;
-        tc::cp_async16(Gt + mn32_off(r, gc, a.Bg), src, v >= 0 ? 16u : 0u);
-      }
-    }
-    tc::cp_async_commit();
-  };
-  // lo half only: the raw fp32 operand is the hi half (the tensor core truncates to TF32)
-  auto split4 = [](float4* hp, float4* lp) {
-    const float4 v = *hp;
-    float4 l;
-    l.x = v.x - tf32_hi_w(v.x); l.y = v.y - tf32_hi_w(v.y); l.z = v.z - tf32_hi_w(v.z); l.w = v.w - tf32_hi_w(v.w);
-    *lp = l;
-    return v;
-  };
-  // same (row, chunk) ownership as load(): each thread splits what it copied
-  auto split = [&](int buf) {
-    uint8_t* X = smem + buf * a.Sb;
-    uint8_t* Gt = X + 2 * a.Sx;
-    for (int r0 = warp * XR; r0 < WR; r0 += 4 * XR) {
-      const int r = r0 + xr;
-      if (r < WR && xc < a.nchx) {
-        const uint32_t o = mn32_off(r, xc, a.Bx);
-        split4(reinterpret_cast<float4*>(X + o), reinterpret_cast<float4*>(X + a.Sx + o));
-      }
-    }
-    for (int r0 = warp * GR; r0 < RSg; r0 += 4 * GR) {
-      const int r = r0 + gr;
-      if (r < RSg && gc < a.nchg) {
-        const uint32_t o = mn32_off(r, gc, a.Bg);
-        const float4 v = split4(reinterpret_cast<float4*>(Gt + o), reinterpret_cast<float4*>(Gt + a.Sg + o));
-        if (do_bias && r >= a.stack && r < RS + a.stack) {  // the halo rows belong to the neighbour chunks
-          bacc.x += v.x; bacc.y += v.y; bacc.z += v.z; bacc.w += v.w;
-        }
-      }
-    }
-  };
-  const uint32_t sbase = tc::smem_u32(smem);
-  const uint64_t dXhi = tc::make_desc_mn32(sbase, a.lbox), dXlo = dXhi + (a.Sx >> 4);
-  const uint64_t dGhi = tc::make_desc_mn32(sbase + 2 * a.Sx, a.lbog), dGlo = dGhi + (a.Sg >> 4);
-
-  if (S > 0) load(0, 0);
-  for (int s = 0; s < S; ++s) {
-    const int buf = s & 1;
-    if (s + 1 < S) {
-      const int nb = (s + 1) & 1;
-      if (s + 1 >= 2) tc::mbar_wait(&mbar[nb], ((s - 1) >> 1) & 1);
-      load(s + 1, nb);
-      tc::cp_async_wait<1>();
-    } else {
-      tc::cp_async_wait<0>();
-    }
-    split(buf);
-    tc::fence_proxy_async();
-    __syncthreads();
-    if (tid == 0) {
-      tc::fence_after();
-      const uint64_t boff = buf ? (uint64_t)(a.Sb >> 4) : 0;
-      const int nacc = a.stack ? 3 : a.G;  // accumulators: kh rows (stacked) or taps
-      for (int i = 0; i < nacc; ++i) {
-        const int t = t0 + (a.stack ? 3 * i : i);
-        const int tt = a.ntaps == 27 ? t % 9 : 0;
-        const int rowoff = a.ntaps == 27 ? (tt / 3) * a.Sw + (a.stack ? 0 : tt % 3) : 0;
-        const uint32_t dcol = tmem + (uint32_t)(i * a.N);
-        for (int j = 0; j < RS / 8; ++j) {
-          // a row is 128 B = 8 descriptor units
-          const uint64_t xo = boff + (uint64_t)(rowoff + 8 * j) * 8;
-          const uint64_t go = boff + (uint64_t)(8 * j) * 8;
-          const uint32_t first = (s | j) ? 1u : 0u;
-          tc::mma_tf32(dcol, dXlo + xo, dGhi + go, a.idesc, first);
-          tc::mma_tf32(dcol, dXhi + xo, dGlo + go, a.idesc, 1u);
-          tc::mma_tf32(dcol, dXhi + xo, dGhi + go, a.idesc, 1u);
-        }
-      }
-      tc::commit(&mbar[buf]);
-    }
-  }
   const int Cin = x.c, Cout = gy.c;
   float* pb = a.part + ((long long)b * a.nrg + rg) * ((long long)a.ntaps * Cin * Cout + Cout);
-  if (do_bias) {  // fixed-order column sum of gy over this CTA's rows
-    bred[tid] = bacc;
-    __syncthreads();
-    if (tid < a.nchg) {
+
+  if (warp == 0) {
+    // ---- MMA issue
+    if (lane == 0) {
+      const uint32_t sbase = tc::smem_u32(smem);
+      const uint64_t dXhi = tc::make_desc_mn32(sbase, a.lbox), dXlo = dXhi + (a.Sx >> 4);
+      const uint64_t dGhi = tc::make_desc_mn32(sbase + 2 * a.Sx, a.lbog), dGlo = dGhi + (a.Sg >> 4);
+      for (int s = 0; s < S; ++s) {
+        const int slot = s % NSTG;
+        tc::mbar_wait(&full[slot], (uint32_t)((s / NSTG) & 1));
+        tc::fence_after();
+        const uint64_t boff = (uint64_t)(slot * a.Sb) >> 4;
+        const int nacc = a.stack ? 3 : a.G;  // accumulators: kh rows (stacked) or taps
+        for (int i = 0; i < nacc; ++i) {
+          const int t = t0 + (a.stack ? 3 * i : i);
+          const int tt = a.ntaps == 27 ? t % 9 : 0;
+          const int rowoff = a.ntaps == 27 ? (tt / 3) * a.Sw + (a.stack ? 0 : tt % 3) : 0;
+          const uint32_t dcol = tmem + (uint32_t)(i * a.N);
+          for (int j = 0; j < RS / 8; ++j) {
+            // a row is 128 B = 8 descriptor units
+            const uint64_t xo = boff + (uint64_t)(rowoff + 8 * j) * 8;
+            const uint64_t go = boff + (uint64_t)(8 * j) * 8;
+            const uint32_t first = (s | j) ? 1u : 0u;
+            tc::mma_tf32(dcol, dXlo + xo, dGhi + go, a.idesc, first);
+            tc::mma_tf32(dcol, dXhi + xo, dGlo + go, a.idesc, 1u);
+            tc::mma_tf32(dcol, dXhi + xo, dGhi + go, a.idesc, 1u);
+          }
+        }
+        tc::commit(&empty[slot]);
+      }
+      if (S > 0) tc::commit(done);
+    }
+  } else {
+    // ---- producers: 4 warps, (row, chunk) ownership fixed per thread across load and split
+    const int pw = warp - 1, ptid = tid - 32;
+    const int xshift = a.ntaps == 27 ? (kd - 1) * a.Sh - a.Sw - (a.stack ? 0 : 1) : 0;
+    constexpr int XR = 32 / NCHXP, GR = 32 / NCHGP;  // rows per warp step
+    const int xr = lane / NCHXP, xc = lane % NCHXP, gr = lane / NCHGP, gc = lane % NCHGP;
+    float4 bacc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s = 0; s < S; ++s) {
+      const int slot = s % NSTG;
+      if (s >= NSTG) tc::mbar_wait(&empty[slot], (uint32_t)((s / NSTG - 1) & 1));
+      const int u0 = a.u_first + (c_lo + s) * RS;
+      uint8_t* X = smem + (size_t)slot * a.Sb;
+      uint8_t* Gt = X + 2 * a.Sx;
+      for (int r0 = pw * XR; r0 < WR; r0 += 4 * XR) {
+        const int r = r0 + xr;
+        if (r < WR && xc < a.nchx) {
+          const int v = wg_voxel(a, u0 + xshift + r);
+          const float* src = v >= 0 ? xb + (long long)v * x.cstride + 4 * xc : xb;
+          tc::cp_async16(X + mn32_off(r, xc, a.Bx), src, v >= 0 ? 16u : 0u);
+        }
+      }
+      for (int r0 = pw * GR; r0 < RSg; r0 += 4 * GR) {
+        const int r = r0 + gr;
+        if (r < RSg && gc < a.nchg) {
+          const int v = wg_voxel(a, u0 - a.stack + r);
+          const float* src = v >= 0 ? gb + (long long)v * gy.cstride + 4 * gc : gb;
+          tc::cp_async16(Gt + mn32_off(r, gc, a.Bg), src, v >= 0 ? 16u : 0u);
+        }
+      }
+      tc::cp_async_commit();
+      tc::cp_async_wait<0>();
+      // lo halves (the raw fp32 operand is the hi half: the tensor core truncates to TF32)
+      for (int r0 = pw * XR; r0 < WR; r0 += 4 * XR) {
+        const int r = r0 + xr;
+        if (r < WR && xc < a.nchx) {
+          const uint32_t o = mn32_off(r, xc, a.Bx);
+          const float4 v = *reinterpret_cast<const float4*>(X + o);
+          float4 l;
+          l.x = v.x - tf32_hi_w(v.x); l.y = v.y - tf32_hi_w(v.y); l.z = v.z - tf32_hi_w(v.z); l.w = v.w - tf32_hi_w(v.w);
+          *reinterpret_cast<float4*>(X + a.Sx + o) = l;
+        }
+      }
+      for (int r0 = pw * GR; r0 < RSg; r0 += 4 * GR) {
+        const int r = r0 + gr;
+        if (r < RSg && gc < a.nchg) {
+          const uint32_t o = mn32_off(r, gc, a.Bg);
+          const float4 v = *reinterpret_cast<const float4*>(Gt + o);
+          float4 l;
+          l.x = v.x - tf32_hi_w(v.x); l.y = v.y - tf32_hi_w(v.y); l.z = v.z - tf32_hi_w(v.z); l.w = v.w - tf32_hi_w(v.w);
+          *reinterpret_cast<float4*>(Gt + a.Sg + o) = l;
+          if (do_bias && r >= a.stack && r < RS + a.stack) {  // the halo rows belong to the neighbour chunks
+            bacc.x += v.x; bacc.y += v.y; bacc.z += v.z; bacc.w += v.w;
+          }
+        }
+      }
+      tc::fence_proxy_async();
+      tc::mbar_arrive(&full[slot]);
+    }
+    if (do_bias) bred[ptid] = bacc;
+  }
+  __syncthreads();
+  if (warp != 0) {
+    const int ptid = tid - 32;
+    if (do_bias && ptid < a.nchg) {  // fixed-order column sum of gy over this CTA's rows
       float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
-      for (int q = 0; q < kWtThreads; ++q) {
-        if ((q & 31) % NCHGP != tid) continue;
+      for (int q = 0; q < kWtProd; ++q) {
+        if ((q & 31) % NCHGP != ptid) continue;
         const float4 v = bred[q];
         sum.x += v.x; sum.y += v.y; sum.z += v.z; sum.w += v.w;
       }
-      float* o = pb + (long long)a.ntaps * Cin * Cout + 4 * tid;
+      float* o = pb + (long long)a.ntaps * Cin * Cout + 4 * ptid;
       o[0] = sum.x; o[1] = sum.y; o[2] = sum.z; o[3] = sum.w;
     }
-  }
-  if (S > 0) {
-    tc::mbar_wait(&mbar[(S - 1) & 1], ((S - 1) >> 1) & 1);
-    tc::fence_after();
-  }
-  // epilogue: D row m (input channel) lives in TMEM lane m (M = 128) or lane
-  // (m % 16) + 32 (m / 16) (M = 64); warp w reads its own 32-lane quadrant.
-  const int m = a.M == 128 ? warp * 32 + lane : (lane < 16 ? warp * 16 + lane : -1);
-  const int ci = cbk * a.cib + m;
-  const bool row_ok = m >= 0 && m < a.cib;
-  const uint32_t trow = tmem + ((uint32_t)(warp * 32) << 16);
-  const int nacc = a.stack ? 3 : a.G;
-  for (int i = 0; i < nacc; ++i) {
-    for (int blk = 0; blk < (a.stack ? 3 : 1); ++blk) {
-      // stacked: TMEM block blk of accumulator i is tap (kd, kh = i, kw = 2 - blk)
-      const int t = a.ntaps == 27 ? (a.stack ? t0 + 3 * i + (2 - blk) : t0 + i) : 0;
-      float* dst = pb + ((long long)t * Cin + ci) * Cout;
-      const int cb = a.stack ? blk * 32 : 0, cw = a.stack ? 32 : a.N;
-      for (int c0 = 0; c0 < cw && c0 < ((Cout + 7) & ~7); c0 += 8) {
-        float v[8];
-        tc::tmem_ld8(trow + (uint32_t)(i * a.N + cb + c0), v);
-        if (row_ok) {
+    if (S > 0) {
+      tc::mbar_wait(done, 0);
+      tc::fence_after();
+    }
+    // epilogue: D row m (input channel) lives in TMEM lane m (M = 128) or lane
+    // (m % 16) + 32 (m / 16) (M = 64); warp w reads lane quadrant w % 4.
+    const int q = warp & 3;
+    const int m = a.M == 128 ? q * 32 + lane : (lane < 16 ? q * 16 + lane : -1);
+    const int ci = cbk * a.cib + m;
+    const bool row_ok = m >= 0 && m < a.cib;
+    const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
+    const int nacc = a.stack ? 3 : a.G;
+    for (int i = 0; i < nacc; ++i) {
+      for (int blk = 0; blk < (a.stack ? 3 : 1); ++blk) {
+        // stacked: TMEM block blk of accumulator i is tap (kd, kh = i, kw = 2 - blk)
+        const int t = a.ntaps == 27 ? (a.stack ? t0 + 3 * i + (2 - blk) : t0 + i) : 0;
+        float* dst = pb + ((long long)t * Cin + ci) * Cout;
+        const int cb = a.stack ? blk * 32 : 0, cw = a.stack ? 32 : a.N;
+        for (int c0 = 0; c0 < cw && c0 < ((Cout + 7) & ~7); c0 += 8) {
+          float v[8];
+          tc::tmem_ld8(trow + (uint32_t)(i * a.N + cb + c0), v);
+          if (row_ok) {
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
-            if (c0 + j < Cout) dst[c0 + j] = S > 0 ? v[j] : 0.f;
+            for (int j = 0; j < 8; ++j)
+              if (c0 + j < Cout) dst[c0 + j] = S > 0 ? v[j] : 0.f;
+          }
         }
       }
     }
@@ -328,7 +334,8 @@ static bool wt_plan(int D, int H, int W, int Cin, int Cout, int ks, int batch, W
   a.nchg = Cout / 4;
   const int nbx = (a.cib + 31) / 32, nbg = (Cout + 31) / 32;  // real 32-channel blocks
   const int mbx = a.M / 32;                                    // blocks the MMA reads
-  // rows per stage: largest that fits two stages (+ read pad) in 220 KB
+  // rows per stage and ring depth: the largest rows per stage with >= 2 stages
+  // (+ read pad) in 220 KB, then as many stages (<= 4) as fit
   a.RS = 0;
   for (int rs : {128, 64, 32}) {
     const int wr = ks == 3 ? rs + 2 * a.Sw + (a.stack ? 0 : 2) : rs;
@@ -339,8 +346,10 @@ static bool wt_plan(int D, int H, int W, int Cin, int Cout, int ks, int batch, W
     const uint32_t sb = 2 * (sx + sg);
     // one real block is read with LBO = 0; otherwise the MMA runs mbx - nbx blocks past the x lo region
     const uint32_t pad = (nbx == 1 || nbx == mbx) ? 0 : align1k((size_t)(mbx - nbx) * bx);
-    const size_t total = 2 * (size_t)sb + pad + 64 + 128 * 16 + 64;
+    const size_t total = 2 * (size_t)sb + pad + 64 + kWtProd * 16 + 64;
     if (total <= (size_t)220 * 1024) {
+      a.NSTG = 2;
+      while (a.NSTG < 4 && (size_t)(a.NSTG + 1) * sb + pad + 128 + kWtProd * 16 + 64 <= (size_t)220 * 1024) ++a.NSTG;
       a.RS = rs;
       a.RSg = rsg;
       a.WR = wr;
@@ -367,7 +376,10 @@ static bool wt_plan(int D, int H, int W, int Cin, int Cout, int ks, int batch, W
   return true;
 }
 
-static size_t wt_smem(const WgTc& a) { return 2 * (size_t)a.Sb + a.pad + 64 + 128 * 16 + 64; }
+// stages, pad, barriers (2 NSTG + 1, padded to 16 B), TMEM slot (16 B), bias partials
+static size_t wt_smem(const WgTc& a) {
+  return (size_t)a.NSTG * a.Sb + a.pad + (((2 * a.NSTG + 1) * 8 + 15) & ~15) + 16 + kWtProd * 16 + 64;
+}
 
 bool wgrad_tc_supported(d2ip_act x, d2ip_act gy, int ks, int precision) {
   if (precision != D2IP_PREC_TF32) return false;
