@@ -403,8 +403,11 @@ def run_e2e(spec, wl, args, ws):
     iters = cfg.iters_warm + sum(f.iterations for f in res.frame_records)
     h2d = matrix.values.nbytes + 4 * np.prod(wl.grid.shape) * spec.in_channels + frames * 4 * wl.matrix.n_measurements
     nparam = res.states["init"].flat().numel()
-    h2d += 4 * nparam * (frames + 1)  # theta upload per stage
-    d2h = frames * (8 * np.prod(wl.grid.shape) + 4 * nparam) + 4 * iters * 4
+    # theta0 is uploaded once: every later stage starts from the theta the device already
+    # holds (UPWS -> frame 1 -> TPP hand-off, pipeline.py:529)
+    h2d += 4 * nparam
+    # per stage: sigmoid volume (fp32) + exported theta + status; per iteration: trace row (4 fp32)
+    d2h = (frames + 1) * (4 * np.prod(wl.grid.shape) + 4 * nparam + 16) + 4 * iters * 4
     return {"value": round(iters / secs, 2), "unit": "it/s", "h2d_bytes_per_step": int(h2d / iters),
             "d2h_bytes_per_step": int(d2h / iters), "call": "reconstruct_sequence",
             "iterations": int(iters), "frames": frames, "seconds": round(secs, 3),
