@@ -94,10 +94,12 @@ int d2ip_conv3d_wgrad(d2ip_act x, d2ip_act gy, int ksize, int stride, float* gw,
                       long long gwbstride, void* ws, size_t ws_bytes, int precision,
                       int batch, void* stream);
 
-/* Weight-gradient kernel for TF32 stride-1 layers: 0 = smem-tiled CUDA-core
- * fp32 (default), 1 = tcgen05 3xTF32 (wgrad_tc.cu). Process-wide; also set by
- * the environment variable D2IP_WGRAD=tc. */
+/* Weight-gradient kernel for TF32 stride-1 3^3 layers: 1 = tcgen05 3xTF32
+ * (wgrad_tc.cu, default), 0 = smem-tiled CUDA-core fp32 (wgrad_s1.cu).
+ * Process-wide; the default can be set by the environment variable
+ * D2IP_WGRAD=s1|tc. */
 int d2ip_set_wgrad_variant(int variant);
+int d2ip_get_wgrad_variant(void);
 
 /* ---- ChannelLayerNorm (+ residual) (+ LeakyReLU) forward ----------------
  * out = act(gamma * xhat + beta [+ res]), xhat = (y - mean_c) * rstd,

@@ -30,12 +30,12 @@ static size_t conv_ws(int cin, int cout, int ks, int stride, int precision, int 
 
 // Weight gradient: the smem-tiled kernel for stride-1 3^3 layers, the
 // register-tiled / scalar split-K kernels otherwise (stride 2, 1^3, C_out = 1).
-// Weight-gradient kernel policy for TF32 runs: 0 = the smem-tiled CUDA-core
-// kernel (default: with the weight gradients on the engine's side stream it
-// measured faster end to end, 828 vs 786 it/s at cfg1), 1 = tcgen05 (3xTF32).
+// Weight-gradient kernel policy for TF32 runs: 1 = tcgen05 3xTF32 (default:
+// warp-specialised, two producer groups; measured 1029 vs 979 it/s at cfg1,
+// 270 vs 254 at cfg2, 41.9 vs 37.8 at cfg4), 0 = the smem-tiled CUDA-core kernel.
 static int g_wgrad_variant = [] {
   const char* v = getenv("D2IP_WGRAD");
-  return v && v[0] == 't' ? 1 : 0;
+  return v && v[0] == 's' ? 0 : 1;
 }();
 
 size_t conv_wgrad_ws(int cin, int cout, int ks, int D, int H, int W, int batch, int precision) {
@@ -119,6 +119,8 @@ int d2ip_conv3d_dgrad(d2ip_act gy, const float* w, long long wbstride, int ksize
 size_t d2ip_conv3d_wgrad_ws_bytes(d2ip_act x, d2ip_act gy, int ksize, int batch) {
   return d2ip::conv_wgrad_ws(x.c, gy.c, ksize, gy.d, gy.h, gy.w, batch, 0);
 }
+
+int d2ip_get_wgrad_variant(void) { return d2ip::g_wgrad_variant; }
 
 int d2ip_set_wgrad_variant(int variant) {
   D2IP_CHECK_ARG(variant == 0 || variant == 1, "wgrad variant must be 0 (CUDA cores) or 1 (tcgen05)");

@@ -109,11 +109,12 @@ __global__ void __launch_bounds__(kWtThreads) wgrad_tc_k(WgTc a) {
   uint8_t* tail = smem + (size_t)NSTG * a.Sb + a.pad + (((2 * NSTG + 1) * 8 + 15) & ~15);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(tail);
   float4* bred = reinterpret_cast<float4*>(tail + 16);  // [kWtProd] bias partials (layout: see wt_smem)
+  int* rowmaps = reinterpret_cast<int*>(tail + 16 + kWtProd * 16);  // [2 groups][WR + RSg] voxel offsets
 
   if (warp == 0) tc::tmem_alloc(tslot, a.tmem_cols);
   if (tid == 0) {
     for (int i = 0; i < NSTG; ++i) {
-      tc::mbar_init(&full[i], kWtProd);
+      tc::mbar_init(&full[i], kWtProd / 2);  // one producer group (2 warps) fills a stage
       tc::mbar_init(&empty[i], 1);
     }
     tc::mbar_init(done, 1);
@@ -160,30 +161,37 @@ __global__ void __launch_bounds__(kWtThreads) wgrad_tc_k(WgTc a) {
       if (S > 0) tc::commit(done);
     }
   } else {
-    // ---- producers: 4 warps, (row, chunk) ownership fixed per thread across load and split
-    const int pw = warp - 1, ptid = tid - 32;
+    // ---- producers: two groups of 2 warps take alternate stages, so two stages
+    // are in flight; a group first maps its stage's rows to voxels once (one
+    // division pair per row, not per 16-byte chunk), then copies and splits
+    // with fixed (row, chunk) ownership per thread.
+    const int ptid = tid - 32, pg = (warp - 1) >> 1, gw = (warp - 1) & 1, gtid = gw * 32 + lane;
     const int xshift = a.ntaps == 27 ? (kd - 1) * a.Sh - a.Sw - (a.stack ? 0 : 1) : 0;
     constexpr int XR = 32 / NCHXP, GR = 32 / NCHGP;  // rows per warp step
     const int xr = lane / NCHXP, xc = lane % NCHXP, gr = lane / NCHGP, gc = lane % NCHGP;
+    int* rm = rowmaps + pg * (WR + RSg);
     float4 bacc = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int s = 0; s < S; ++s) {
+    for (int s = pg; s < S; s += 2) {
       const int slot = s % NSTG;
       if (s >= NSTG) tc::mbar_wait(&empty[slot], (uint32_t)((s / NSTG - 1) & 1));
       const int u0 = a.u_first + (c_lo + s) * RS;
+      for (int i = gtid; i < WR + RSg; i += 64)
+        rm[i] = i < WR ? wg_voxel(a, u0 + xshift + i) : wg_voxel(a, u0 - a.stack + (i - WR));
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + pg) : "memory");
       uint8_t* X = smem + (size_t)slot * a.Sb;
       uint8_t* Gt = X + 2 * a.Sx;
-      for (int r0 = pw * XR; r0 < WR; r0 += 4 * XR) {
+      for (int r0 = gw * XR; r0 < WR; r0 += 2 * XR) {
         const int r = r0 + xr;
         if (r < WR && xc < a.nchx) {
-          const int v = wg_voxel(a, u0 + xshift + r);
+          const int v = rm[r];
           const float* src = v >= 0 ? xb + (long long)v * x.cstride + 4 * xc : xb;
           tc::cp_async16(X + mn32_off(r, xc, a.Bx), src, v >= 0 ? 16u : 0u);
         }
       }
-      for (int r0 = pw * GR; r0 < RSg; r0 += 4 * GR) {
+      for (int r0 = gw * GR; r0 < RSg; r0 += 2 * GR) {
         const int r = r0 + gr;
         if (r < RSg && gc < a.nchg) {
-          const int v = wg_voxel(a, u0 - a.stack + r);
+          const int v = rm[WR + r];
           const float* src = v >= 0 ? gb + (long long)v * gy.cstride + 4 * gc : gb;
           tc::cp_async16(Gt + mn32_off(r, gc, a.Bg), src, v >= 0 ? 16u : 0u);
         }
@@ -191,7 +199,7 @@ __global__ void __launch_bounds__(kWtThreads) wgrad_tc_k(WgTc a) {
       tc::cp_async_commit();
       tc::cp_async_wait<0>();
       // lo halves (the raw fp32 operand is the hi half: the tensor core truncates to TF32)
-      for (int r0 = pw * XR; r0 < WR; r0 += 4 * XR) {
+      for (int r0 = gw * XR; r0 < WR; r0 += 2 * XR) {
         const int r = r0 + xr;
         if (r < WR && xc < a.nchx) {
           const uint32_t o = mn32_off(r, xc, a.Bx);
@@ -201,7 +209,7 @@ __global__ void __launch_bounds__(kWtThreads) wgrad_tc_k(WgTc a) {
           *reinterpret_cast<float4*>(X + a.Sx + o) = l;
         }
       }
-      for (int r0 = pw * GR; r0 < RSg; r0 += 4 * GR) {
+      for (int r0 = gw * GR; r0 < RSg; r0 += 2 * GR) {
         const int r = r0 + gr;
         if (r < RSg && gc < a.nchg) {
           const uint32_t o = mn32_off(r, gc, a.Bg);
@@ -216,6 +224,7 @@ __global__ void __launch_bounds__(kWtThreads) wgrad_tc_k(WgTc a) {
       }
       tc::fence_proxy_async();
       tc::mbar_arrive(&full[slot]);
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + pg) : "memory");  // rm is rebuilt next stage
     }
     if (do_bias) bred[ptid] = bacc;
   }
@@ -346,10 +355,12 @@ static bool wt_plan(int D, int H, int W, int Cin, int Cout, int ks, int batch, W
     const uint32_t sb = 2 * (sx + sg);
     // one real block is read with LBO = 0; otherwise the MMA runs mbx - nbx blocks past the x lo region
     const uint32_t pad = (nbx == 1 || nbx == mbx) ? 0 : align1k((size_t)(mbx - nbx) * bx);
-    const size_t total = 2 * (size_t)sb + pad + 64 + kWtProd * 16 + 64;
+    const size_t total = 2 * (size_t)sb + pad + 64 + kWtProd * 16 + 8 * (size_t)(wr + rsg) + 64;
     if (total <= (size_t)220 * 1024) {
       a.NSTG = 2;
-      while (a.NSTG < 4 && (size_t)(a.NSTG + 1) * sb + pad + 128 + kWtProd * 16 + 64 <= (size_t)220 * 1024) ++a.NSTG;
+      while (a.NSTG < 4 && (size_t)(a.NSTG + 1) * sb + pad + 128 + kWtProd * 16 + 8 * (size_t)(wr + rsg) + 64 <=
+                               (size_t)220 * 1024)
+        ++a.NSTG;
       a.RS = rs;
       a.RSg = rsg;
       a.WR = wr;
@@ -378,7 +389,8 @@ static bool wt_plan(int D, int H, int W, int Cin, int Cout, int ks, int batch, W
 
 // stages, pad, barriers (2 NSTG + 1, padded to 16 B), TMEM slot (16 B), bias partials
 static size_t wt_smem(const WgTc& a) {
-  return (size_t)a.NSTG * a.Sb + a.pad + (((2 * a.NSTG + 1) * 8 + 15) & ~15) + 16 + kWtProd * 16 + 64;
+  return (size_t)a.NSTG * a.Sb + a.pad + (((2 * a.NSTG + 1) * 8 + 15) & ~15) + 16 + kWtProd * 16 +
+         2 * (size_t)(a.WR + a.RSg) * sizeof(int) + 64;
 }
 
 bool wgrad_tc_supported(d2ip_act x, d2ip_act gy, int ks, int precision) {

@@ -112,9 +112,10 @@ def test_conv3d_fwd(cin, cout, ks, stride, sp, prec):
 @pytest.fixture(params=[0, 1], ids=["wg_cuda", "wg_tcgen05"])
 def wgrad_variant(request):
     L = N.lib()
+    before = L.d2ip_get_wgrad_variant()
     N.check(L.d2ip_set_wgrad_variant(request.param), "set_wgrad_variant")
     yield request.param
-    L.d2ip_set_wgrad_variant(0)
+    L.d2ip_set_wgrad_variant(before)
 
 
 @pytest.mark.parametrize("prec", ["fp32", "tf32"])
