@@ -30,6 +30,7 @@
 // grid) by all 128 threads; thread 0 issues the MMAs of a stage and commits
 // them to that stage's mbarrier, which gates the refill of the buffer.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -37,7 +38,8 @@
 
 namespace d2ip {
 
-constexpr int kTcThreads = 256;  // 8 warps: fills / splits spread wider; epilogue = 2 threads per row
+constexpr int kTcThreads = 288;  // warp 0: MMA issue; warps 1-8: two producer groups, then the epilogue
+constexpr int kTcProd = 256;
 constexpr int kTcRows = 128;
 
 __host__ __device__ static inline int np_of(int n) { return (n + 15) / 16 * 16; }
@@ -67,14 +69,16 @@ static size_t stage_bytes(int cb, int np, int wrp) {
 }
 
 static size_t tc_smem_bytes(const TcConv& a) {
-  return 2 * stage_bytes(a.CB, a.Ns, a.WRp) + 3 * a.WR * sizeof(int) + 64;
+  return 2 * stage_bytes(a.CB, a.Ns, a.WRp) + 3 * a.WR * sizeof(int) + 8 + 5 * 8 + 16;
 }
 
 __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 
 // NKC = CB / 4: 16-byte channel chunks per stage (compile-time, so the fill
 // loops need no integer division).
-template <int NKC, int T>
+// PG: producer groups (1: all eight producer warps fill each stage; 2: two
+// groups of four fill alternate stages, two stages in flight).
+template <int NKC, int T, int PG>
 __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
   D2IP_PDL_ENTRY();
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -87,15 +91,20 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
   const int Ns = a.Ns, WR = a.WR, WRp = a.WRp;
   const uint32_t Ab = (uint32_t)NKC * WRp * 16, Bb = (uint32_t)9 * NKC * Ns * 16;
   const uint32_t Sb = 2 * (Ab + Bb);
-  // stage layout: [A hi][A lo][B hi][B lo]
+  // layout: 2 stages of [A hi][A lo][B hi][B lo], row map, barriers full[2] empty[2] done, TMEM slot
   int* rowmap = reinterpret_cast<int*>(smem + 2 * Sb);
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(rowmap + 3 * WR + ((3 * WR) & 1));
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(mbar + 2);
+  uint64_t* full = reinterpret_cast<uint64_t*>(rowmap + 3 * WR + ((3 * WR) & 1));
+  uint64_t* empty = full + 2;
+  uint64_t* done = empty + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
 
   if (warp == 0) tc::tmem_alloc(tslot, a.tmem_cols);
   if (tid == 0) {
-    tc::mbar_init(&mbar[0], 1);
-    tc::mbar_init(&mbar[1], 1);
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&full[i], kTcProd / PG);  // one producer group fills a stage
+      tc::mbar_init(&empty[i], 1);
+    }
+    tc::mbar_init(done, 1);
     tc::fence_mbar_init();
   }
   // voxel offset of every window row for the three plane taps (-1 = padding)
@@ -124,133 +133,133 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
   const int nA = WR * NKC;
   const int kc_all = a.Kc >> 2;
 
-  auto load = [&](int sl, int buf) {
-    const int s = s_lo + sl;
-    const int kd = s / a.n_cb, cb = s - kd * a.n_cb;
-    const int* rm = rowmap + kd * WR;
-    uint8_t* A = smem + buf * Sb;
-    const float* xc = xb + cb * CB;
-    for (int i = tid; i < nA; i += kTcThreads) {
-      const int r = i / NKC, kc = i % NKC;
-      const int off = rm[r];
-      const float* src = off >= 0 ? xc + (long long)off * x.cstride + 4 * kc : xb;
-      tc::cp_async16(A + ((size_t)kc * WRp + r) * 16, src, off >= 0 ? 16u : 0u);
-    }
-    // B: 9 taps x NKC chunks, each a contiguous run of Ns 16-byte rows; one warp per run
-    uint8_t* Bt = smem + buf * Sb + 2 * Ab;
-    const float* wk = wpb + ((long long)(kd * 9) * kc_all + cb * NKC) * a.Np * 4 + (long long)n0 * 4;
-    for (int q = warp; q < 9 * NKC; q += kTcThreads / 32) {
-      const int t9 = q / NKC, kcl = q % NKC;
-      const float* src = wk + ((long long)t9 * kc_all + kcl) * a.Np * 4;
-      uint8_t* dst = Bt + (size_t)q * Ns * 16;
-      for (int n = lane; n < Ns; n += 32) {
-        tc::cp_async16(dst + n * 16, src + n * 4, 16u);
-        tc::cp_async16(dst + Bb + n * 16, src + a.wlo + n * 4, 16u);
-      }
-    }
-    tc::cp_async_commit();
-  };
-  // write the lo half of the landed activation window; the raw fp32 window
-  // itself is the hi operand, because the tensor core truncates fp32 operands
-  // to TF32 (measured: tools/tf32_round_probe.cu). Every thread touches exactly
-  // the 16-B elements its own cp.async wrote.
-  auto split = [&](int buf) {
-    uint8_t* A = smem + buf * Sb;
-    for (int i = tid; i < nA; i += kTcThreads) {
-      const int r = i / NKC, kc = i % NKC;
-      const float4 v = *reinterpret_cast<const float4*>(A + ((size_t)kc * WRp + r) * 16);
-      float4 l;
-      l.x = v.x - tf32_hi(v.x); l.y = v.y - tf32_hi(v.y); l.z = v.z - tf32_hi(v.z); l.w = v.w - tf32_hi(v.w);
-      *reinterpret_cast<float4*>(A + Ab + ((size_t)kc * WRp + r) * 16) = l;
-    }
-  };
-  // descriptors of buffer 0; a tap / K step / buffer is an add to the 14-bit
-  // start-address field (smem addresses < 256 KB never carry out of it)
-  const uint32_t sbase = tc::smem_u32(smem);
-  const uint64_t dAhi = tc::make_desc(sbase, WRp * 16, 128), dAlo = dAhi + (Ab >> 4);
-  const uint64_t dBhi = tc::make_desc(sbase + 2 * Ab, Ns * 16, 128), dBlo = dBhi + (Bb >> 4);
-
-  load(0, 0);
-  for (int s = 0; s < S; ++s) {
-    const int buf = s & 1;
-    if (s + 1 < S) {
-      const int nb = (s + 1) & 1;
-      if (s + 1 >= 2) tc::mbar_wait(&mbar[nb], ((s - 1) >> 1) & 1);  // MMAs of stage s-1 done with nb
-      load(s + 1, nb);
-      tc::cp_async_wait<1>();
-    } else {
-      tc::cp_async_wait<0>();
-    }
-    split(buf);
-    tc::fence_proxy_async();
-    __syncthreads();
-    if (tid == 0) {
-      tc::fence_after();
-      const uint64_t boff = buf ? (uint64_t)(Sb >> 4) : 0;
-      for (int t9 = 0; t9 < 9; ++t9) {
-        const int rowoff = (t9 / 3) * a.Sw + (t9 % 3);
+  if (warp == 0) {
+    // ---- MMA issue (one elected thread); stage s lives in slot s & 1
+    if (lane == 0) {
+      // descriptors of slot 0; a tap / K step / slot is an add to the 14-bit
+      // start-address field (smem addresses < 256 KB never carry out of it)
+      const uint32_t sbase = tc::smem_u32(smem);
+      const uint64_t dAhi = tc::make_desc(sbase, WRp * 16, 128), dAlo = dAhi + (Ab >> 4);
+      const uint64_t dBhi = tc::make_desc(sbase + 2 * Ab, Ns * 16, 128), dBlo = dBhi + (Bb >> 4);
+      for (int s = 0; s < S; ++s) {
+        const int slot = s & 1;
+        tc::mbar_wait(&full[slot], (uint32_t)((s >> 1) & 1));
+        tc::fence_after();
+        const uint64_t boff = slot ? (uint64_t)(Sb >> 4) : 0;
+        for (int t9 = 0; t9 < 9; ++t9) {
+          const int rowoff = (t9 / 3) * a.Sw + (t9 % 3);
 #pragma unroll
-        for (int j = 0; j < NKC / 2; ++j) {
-          const uint64_t bo = boff + (uint64_t)((t9 * NKC + 2 * j) * Ns);
-          const uint32_t first = (s | t9 | j) ? 1u : 0u;
+          for (int j = 0; j < NKC / 2; ++j) {
+            const uint64_t bo = boff + (uint64_t)((t9 * NKC + 2 * j) * Ns);
+            const uint32_t first = (s | t9 | j) ? 1u : 0u;
 #pragma unroll
-          for (int tt = 0; tt < T; ++tt) {  // sub-tile tt: rows + 128 tt, accumulator columns + tt Ns
-            const uint64_t ao = boff + (uint64_t)(2 * j * WRp + rowoff + tt * kTcRows);
-            const uint32_t d = tmem + (uint32_t)(tt * Ns);
-            tc::mma_tf32(d, dAlo + ao, dBhi + bo, a.idesc, first);
-            tc::mma_tf32(d, dAhi + ao, dBlo + bo, a.idesc, 1u);
-            tc::mma_tf32(d, dAhi + ao, dBhi + bo, a.idesc, 1u);
+            for (int tt = 0; tt < T; ++tt) {  // sub-tile tt: rows + 128 tt, accumulator columns + tt Ns
+              const uint64_t ao = boff + (uint64_t)(2 * j * WRp + rowoff + tt * kTcRows);
+              const uint32_t d = tmem + (uint32_t)(tt * Ns);
+              tc::mma_tf32(d, dAlo + ao, dBhi + bo, a.idesc, first);
+              tc::mma_tf32(d, dAhi + ao, dBlo + bo, a.idesc, 1u);
+              tc::mma_tf32(d, dAhi + ao, dBhi + bo, a.idesc, 1u);
+            }
           }
         }
+        tc::commit(&empty[slot]);
       }
-      tc::commit(&mbar[buf]);
+      if (S > 0) tc::commit(done);
     }
-  }
-  tc::mbar_wait(&mbar[(S - 1) & 1], ((S - 1) >> 1) & 1);
-  tc::fence_after();
+  } else {
+    // ---- producers: PG groups fill alternate stages; a thread copies and splits
+    // the same 16-byte elements
+    constexpr int GT = kTcProd / PG;
+    const int pg = PG == 2 ? (warp - 1) >> 2 : 0, gtid = tid - 32 - pg * GT;
+    for (int s = pg; s < S; s += PG) {
+      const int slot = s & 1;
+      if (s >= 2) tc::mbar_wait(&empty[slot], (uint32_t)(((s >> 1) - 1) & 1));
+      const int sg = s_lo + s;
+      const int kd = sg / a.n_cb, cb = sg - kd * a.n_cb;
+      const int* rm = rowmap + kd * WR;
+      uint8_t* A = smem + slot * Sb;
+      const float* xc = xb + cb * CB;
+      for (int i = gtid; i < nA; i += GT) {
+        const int r = i / NKC, kc = i % NKC;
+        const int off = rm[r];
+        const float* src = off >= 0 ? xc + (long long)off * x.cstride + 4 * kc : xb;
+        tc::cp_async16(A + ((size_t)kc * WRp + r) * 16, src, off >= 0 ? 16u : 0u);
+      }
+      // B: 9 taps x NKC chunks, each a contiguous run of Ns 16-byte rows; one warp per run
+      uint8_t* Bt = A + 2 * Ab;
+      const float* wk = wpb + ((long long)(kd * 9) * kc_all + cb * NKC) * a.Np * 4 + (long long)n0 * 4;
+      const int gwarp = gtid >> 5;
+      for (int q = gwarp; q < 9 * NKC; q += GT / 32) {
+        const int t9 = q / NKC, kcl = q % NKC;
+        const float* src = wk + ((long long)t9 * kc_all + kcl) * a.Np * 4;
+        uint8_t* dst = Bt + (size_t)q * Ns * 16;
+        for (int n = lane; n < Ns; n += 32) {
+          tc::cp_async16(dst + n * 16, src + n * 4, 16u);
+          tc::cp_async16(dst + Bb + n * 16, src + a.wlo + n * 4, 16u);
+        }
+      }
+      tc::cp_async_commit();
+      tc::cp_async_wait<0>();
+      // lo half of the landed activation window; the raw fp32 window is the hi
+      // operand (the tensor core truncates fp32 to TF32: tools/tf32_round_probe.cu)
+      for (int i = gtid; i < nA; i += GT) {
+        const int r = i / NKC, kc = i % NKC;
+        const float4 v = *reinterpret_cast<const float4*>(A + ((size_t)kc * WRp + r) * 16);
+        float4 l;
+        l.x = v.x - tf32_hi(v.x); l.y = v.y - tf32_hi(v.y); l.z = v.z - tf32_hi(v.z); l.w = v.w - tf32_hi(v.w);
+        *reinterpret_cast<float4*>(A + Ab + ((size_t)kc * WRp + r) * 16) = l;
+      }
+      tc::fence_proxy_async();
+      tc::mbar_arrive(&full[slot]);
+    }
 
-  // epilogue: TMEM lane = GEMM row; each thread owns one row / voxel per sub-tile.
-  // warp w reads TMEM lane quadrant w % 4 (rows) and column half w / 4
-  const int row = (warp & 3) * 32 + lane;
-  const int chalf = a.Ns / 2, cbeg = (warp >> 2) * chalf, cend = cbeg + chalf;
-  const d2ip_act y = a.y;
-  const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16);
-  const float* bias = a.bias ? a.bias + b * a.bbs : nullptr;
-  for (int tt = 0; tt < T; ++tt) {
-    const int u = u0 + tt * kTcRows + row;
-    int v = -1;
-    {
-      const int dp = u / a.Sh, rem = u - dp * a.Sh;
-      const int hp = rem / a.Sw, wp = rem - hp * a.Sw;
-      if (dp >= 1 && dp <= x.d && hp >= 1 && hp <= x.h && wp >= 1 && wp <= x.w)
-        v = ((dp - 1) * x.h + (hp - 1)) * x.w + (wp - 1);
+    // ---- epilogue (producer warps): TMEM lane = GEMM row; warp w reads lane
+    // quadrant w % 4 and column half (w - 1) / 4; one row / voxel per sub-tile
+    if (S > 0) {
+      tc::mbar_wait(done, 0);
+      tc::fence_after();
     }
-    const uint32_t tcol = trow + (uint32_t)(tt * Ns);
-    if (a.kspl > 1) {  // raw partial sums; the consumer adds bias / accumulates
-      float* pp = v >= 0 ? a.part + (((long long)b * a.kspl + ks) * a.vout + v) * a.N : nullptr;
+    const int row = (warp & 3) * 32 + lane;
+    const int chalf = a.Ns / 2, cbeg = ((warp - 1) >> 2) * chalf, cend = cbeg + chalf;
+    const d2ip_act y = a.y;
+    const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+    const float* bias = a.bias ? a.bias + b * a.bbs : nullptr;
+    for (int tt = 0; tt < T; ++tt) {
+      const int u = u0 + tt * kTcRows + row;
+      int v = -1;
+      {
+        const int dp = u / a.Sh, rem = u - dp * a.Sh;
+        const int hp = rem / a.Sw, wp = rem - hp * a.Sw;
+        if (dp >= 1 && dp <= x.d && hp >= 1 && hp <= x.h && wp >= 1 && wp <= x.w)
+          v = ((dp - 1) * x.h + (hp - 1)) * x.w + (wp - 1);
+      }
+      const uint32_t tcol = trow + (uint32_t)(tt * Ns);
+      if (a.kspl > 1) {  // raw partial sums; the consumer adds bias / accumulates
+        float* pp = v >= 0 ? a.part + (((long long)b * a.kspl + ks) * a.vout + v) * a.N : nullptr;
+        for (int c0 = cbeg; c0 < cend; c0 += 8) {
+          float vals[8];
+          tc::tmem_ld8(tcol + c0, vals);
+          if (pp) {
+#pragma unroll
+            for (int j = 0; j < 8; ++j)
+              if (n0 + c0 + j < a.N) pp[n0 + c0 + j] = S > 0 ? vals[j] : 0.f;
+          }
+        }
+        continue;
+      }
+      float* yp = v >= 0 ? y.ptr + b * y.bstride + (long long)v * y.cstride : nullptr;
       for (int c0 = cbeg; c0 < cend; c0 += 8) {
         float vals[8];
         tc::tmem_ld8(tcol + c0, vals);
-        if (pp) {
+        if (yp) {
 #pragma unroll
-          for (int j = 0; j < 8; ++j)
-            if (n0 + c0 + j < a.N) pp[n0 + c0 + j] = vals[j];
-        }
-      }
-      continue;
-    }
-    float* yp = v >= 0 ? y.ptr + b * y.bstride + (long long)v * y.cstride : nullptr;
-    for (int c0 = cbeg; c0 < cend; c0 += 8) {
-      float vals[8];
-      tc::tmem_ld8(tcol + c0, vals);
-      if (yp) {
-#pragma unroll
-        for (int j = 0; j < 8; ++j) {
-          const int n = n0 + c0 + j;
-          if (n < a.N) {
-            float o = vals[j] + (bias ? __ldg(bias + n) : 0.f);
-            if (a.accumulate) o += yp[n];
-            yp[n] = o;
+          for (int j = 0; j < 8; ++j) {
+            const int n = n0 + c0 + j;
+            if (n < a.N) {
+              float o = (S > 0 ? vals[j] : 0.f) + (bias ? __ldg(bias + n) : 0.f);
+              if (a.accumulate) o += yp[n];
+              yp[n] = o;
+            }
           }
         }
       }
@@ -463,18 +472,30 @@ int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, lo
   const size_t smem = tc_smem_bytes(a);
   static bool attr_set = false;
   if (!attr_set) {
-    for (auto k : {conv_tc_k<2, 1>, conv_tc_k<4, 1>, conv_tc_k<8, 1>, conv_tc_k<16, 1>, conv_tc_k<2, 2>,
-                   conv_tc_k<4, 2>, conv_tc_k<8, 2>, conv_tc_k<16, 2>, conv_tc_k<2, 4>, conv_tc_k<4, 4>,
-                   conv_tc_k<8, 4>, conv_tc_k<16, 4>})
+    for (auto k : {conv_tc_k<2, 1, 1>, conv_tc_k<4, 1, 1>, conv_tc_k<8, 1, 1>, conv_tc_k<16, 1, 1>,
+                   conv_tc_k<2, 1, 2>, conv_tc_k<4, 1, 2>, conv_tc_k<8, 1, 2>, conv_tc_k<16, 1, 2>,
+                   conv_tc_k<2, 2, 1>, conv_tc_k<4, 2, 1>, conv_tc_k<8, 2, 1>, conv_tc_k<16, 2, 1>,
+                   conv_tc_k<2, 2, 2>, conv_tc_k<4, 2, 2>, conv_tc_k<8, 2, 2>, conv_tc_k<16, 2, 2>,
+                   conv_tc_k<2, 4, 1>, conv_tc_k<4, 4, 1>, conv_tc_k<8, 4, 1>, conv_tc_k<16, 4, 1>,
+                   conv_tc_k<2, 4, 2>, conv_tc_k<4, 4, 2>, conv_tc_k<8, 4, 2>, conv_tc_k<16, 4, 2>})
       D2IP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr_set = true;
   }
   const dim3 grid(tiles, (a.Np / a.Ns) * a.kspl, batch);
+  // one producer group (all eight warps per stage) measured faster than two on
+  // cfg1 (1029 vs 1013 it/s) and cfg2 (280 vs 274); D2IP_TC_PG=2 selects two
+  static const bool pg2 = [] {
+    const char* v = getenv("D2IP_TC_PG");
+    return v && atoi(v) == 2;
+  }();
 #define D2IP_TC_LAUNCH(NKC_)                                                                              \
   do {                                                                                                    \
-    if (a.T == 4) D2IP_CUDA(launch_pdl((conv_tc_k<NKC_, 4>), grid, kTcThreads, smem, st, a));            \
-    else if (a.T == 2) D2IP_CUDA(launch_pdl((conv_tc_k<NKC_, 2>), grid, kTcThreads, smem, st, a));       \
-    else D2IP_CUDA(launch_pdl((conv_tc_k<NKC_, 1>), grid, kTcThreads, smem, st, a));                     \
+    if (a.T == 4 && pg2) D2IP_CUDA(launch_pdl((conv_tc_k<NKC_, 4, 2>), grid, kTcThreads, smem, st, a));  \
+    else if (a.T == 4) D2IP_CUDA(launch_pdl((conv_tc_k<NKC_, 4, 1>), grid, kTcThreads, smem, st, a));    \
+    else if (a.T == 2 && pg2) D2IP_CUDA(launch_pdl((conv_tc_k<NKC_, 2, 2>), grid, kTcThreads, smem, st, a)); \
+    else if (a.T == 2) D2IP_CUDA(launch_pdl((conv_tc_k<NKC_, 2, 1>), grid, kTcThreads, smem, st, a));    \
+    else if (pg2) D2IP_CUDA(launch_pdl((conv_tc_k<NKC_, 1, 2>), grid, kTcThreads, smem, st, a));         \
+    else D2IP_CUDA(launch_pdl((conv_tc_k<NKC_, 1, 1>), grid, kTcThreads, smem, st, a));                  \
   } while (0)
   switch (a.CB / 4) {
     case 2: D2IP_TC_LAUNCH(2); break;
