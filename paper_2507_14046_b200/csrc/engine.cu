@@ -277,7 +277,7 @@ int fork_to(Ctx& k, cudaStream_t from, cudaStream_t to) {
 
 int side_ctx(Ctx& k, Ctx& ks) {
   d2ip_engine& E = k.E;
-  const int i = E.lane_next++ % d2ip_engine::kLanes;
+  const int i = E.lane_next++ % E.nlanes;
   D2IP_RET(fork_to(k, k.st, E.lane[i]));
   k.lanes |= 1u << i;
   ks.st = E.lane[i];  // ks: a copy of k made by the caller
@@ -616,6 +616,7 @@ int d2ip_engine_create(const d2ip_net_desc* desc, d2ip_engine** out) {
     E->W[l] = d.P >> l;
     E->V[l] = (long long)E->D[l] * E->H[l] * E->W[l];
   }
+  E->nlanes = d.arch == D2IP_ARCH_FAST_RESUNET ? 3 : 2;
   if (d.arch == D2IP_ARCH_FAST_RESUNET) {
     int rc = refnet_plan_params(*E);
     if (rc != D2IP_OK) {

@@ -77,6 +77,7 @@ struct d2ip_engine {
   // weight gradients (and dgamma/dbeta sums) run on a pool of side lanes, off the
   // data-gradient critical path; each lane has its own reduction workspace
   static constexpr int kLanes = 3;
+  int nlanes = 2;  // lanes in use: 2 for the config ResUNet, 3 for FastResUNet3D (measured best)
   cudaStream_t lane[kLanes]{};
   void* lane_ws[kLanes]{};
   int lane_next = 0;
