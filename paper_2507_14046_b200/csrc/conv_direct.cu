@@ -435,6 +435,9 @@ static DirectPlan direct_plan(long long V, int C, int ks, int batch, int live_ta
   if (ks == 3 && live_taps < 27 && base < 48LL * 1024) p.S = 9;
   p.vb = p.S == 9 ? 32 : (p.S == 3 ? 64 : 0);
   p.thr = p.S > 1 ? (int)p.vb * p.S : (small ? 64 : 128);
+  // a large weight slice per block (e.g. a stride-2 data gradient, 32 x 27 x 8
+  // floats) is amortised over more voxels when there is parallelism to spare
+  if (p.S == 1 && !small && Cred * (long long)ks * ks * ks * p.cg >= 2048 && base >= 64LL * 1024) p.thr = 256;
   if (p.S == 1) p.vb = p.thr;
   return p;
 }
