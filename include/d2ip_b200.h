@@ -66,12 +66,21 @@ const char* d2ip_last_error(void);
 /* Name of the kernel variant the last conv call dispatched to (diagnostics). */
 const char* d2ip_last_variant(void);
 
+/* Debug launch tracing (no reference counterpart): events around every kernel
+ * launch from d2ip_trace_begin until d2ip_trace_dump, which synchronises and
+ * writes "<start_us> <end_us> <stream> <kernel>" lines (relative to the first
+ * launch) into buf; returns the full text length. Eager launches only. */
+int d2ip_trace_begin(void);
+int d2ip_trace_dump(char* buf, size_t n);
+
 /* ---- K1: 3^3 / 1^3 convolution forward ---------------------------------
  * y = conv3d(x, W, b) (+ y if accumulate). ksize 3 -> padding 1, ksize 1 ->
  * padding 0; stride 1 or 2. Replaces `nn.Conv3d` forward
  * (priornet.py:117,143,200,215 / oracle ConfigResUNet). precision TF32 on a
- * stride-1 3^3 layer runs the tcgen05 implicit GEMM, whose packed weights
- * need `d2ip_conv3d_ws_bytes()` of workspace (0 for the direct kernels). */
+ * 3^3 layer (stride 1, or stride 2 by parity decomposition) runs the tcgen05
+ * implicit GEMM, whose packed weights need `d2ip_conv3d_ws_bytes()` of
+ * workspace (0 for the direct kernels); workspace beyond that, when large
+ * enough, holds split-K partial sums (more CTAs on small grids). */
 size_t d2ip_conv3d_ws_bytes(int cin, int cout, int ksize, int stride, int precision, int batch);
 int d2ip_conv3d_fwd(d2ip_act x, const float* w, const float* bias, long long wbstride,
                     int ksize, int stride, d2ip_act y, int accumulate, int precision,

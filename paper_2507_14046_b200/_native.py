@@ -99,6 +99,8 @@ _SIGS = {
     "d2ip_abi_version": (C.c_int, []),
     "d2ip_last_error": (C.c_char_p, []),
     "d2ip_last_variant": (C.c_char_p, []),
+    "d2ip_trace_begin": (C.c_int, []),
+    "d2ip_trace_dump": (C.c_int, [C.c_char_p, C.c_size_t]),
     "d2ip_set_wgrad_variant": (C.c_int, [C.c_int]),
     "d2ip_get_wgrad_variant": (C.c_int, []),
     "d2ip_assemble_sensitivity": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p, C.c_int, C.c_void_p, C.c_int,

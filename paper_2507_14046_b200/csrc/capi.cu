@@ -1,3 +1,6 @@
+#include <string>
+#include <vector>
+#include <cstring>
 // C ABI wrappers (include/d2ip_b200.h) and the convolution dispatcher.
 #include <stdarg.h>
 #include <stdlib.h>
@@ -20,12 +23,12 @@ void set_variant(const char* name) { g_variant = name; }
 
 // Convolution dispatch for the standalone ABI: tcgen05 implicit GEMM where the
 // shape and precision allow it (weights packed into the caller's workspace),
-// the exact-fp32 direct kernel otherwise (C_out = 1 tail, stride 2, 1^3,
-// C_in not a multiple of 8, or precision FP32).
+// the exact-fp32 direct kernel otherwise (C_out = 1 tail, 1^3, channel
+// counts the GEMM views cannot tile, or precision FP32).
 static size_t conv_ws(int cin, int cout, int ks, int stride, int precision, int batch, int dgrad) {
-  const int K = dgrad ? cout : cin, N = dgrad ? cin : cout;
-  if (!conv_tc_supported(K, N, ks, stride, precision)) return 0;
-  return (size_t)batch * conv_tc_pack_floats(K, N) * sizeof(float);
+  TcDims t;
+  if (!conv_tc_layer(cin, cout, ks, stride, dgrad, precision, -1, &t)) return 0;
+  return (size_t)batch * conv_tc_pack_floats(t.K, t.N) * sizeof(float);
 }
 
 // Weight gradient: the smem-tiled kernel for stride-1 3^3 layers, the
@@ -75,11 +78,80 @@ static int check_conv_shapes(const d2ip_act& x, const d2ip_act& y, int ks, int s
 
 }  // namespace d2ip
 
+// ---- launch tracing (debug only; not used on the product path)
+namespace d2ip {
+int g_trace_on = 0;
+struct TraceRec {
+  const void* fn;
+  cudaStream_t st;
+  cudaEvent_t a, b;
+};
+static std::vector<TraceRec> g_trace;
+static std::vector<cudaEvent_t> g_trace_pool;
+static size_t g_trace_used = 0;
+static cudaEvent_t trace_event() {
+  if (g_trace_used == g_trace_pool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    g_trace_pool.push_back(e);
+  }
+  return g_trace_pool[g_trace_used++];
+}
+void trace_pre(cudaStream_t st, const void* fn) {
+  TraceRec r{fn, st, trace_event(), nullptr};
+  cudaEventRecord(r.a, st);
+  g_trace.push_back(r);
+}
+void trace_post(cudaStream_t st) {
+  if (g_trace.empty()) return;
+  g_trace.back().b = trace_event();
+  cudaEventRecord(g_trace.back().b, st);
+}
+}  // namespace d2ip
+
 extern "C" {
 
 int d2ip_abi_version(void) { return D2IP_ABI_VERSION; }
 const char* d2ip_last_error(void) { return d2ip::g_err; }
 const char* d2ip_last_variant(void) { return d2ip::g_variant; }
+
+
+
+int d2ip_trace_begin(void) {
+  d2ip::g_trace.clear();
+  d2ip::g_trace_used = 0;
+  d2ip::g_trace_on = 1;
+  return D2IP_OK;
+}
+
+// Stops tracing, synchronises, and writes one line per launch:
+// "<start_us> <end_us> <stream> <kernel name>\n" relative to the first launch.
+int d2ip_trace_dump(char* buf, size_t n) {
+  using namespace d2ip;
+  g_trace_on = 0;
+  D2IP_CUDA(cudaDeviceSynchronize());
+  std::string out;
+  if (!g_trace.empty()) {
+    const cudaEvent_t t0 = g_trace.front().a;
+    char line[512];
+    for (const TraceRec& r : g_trace) {
+      float s = 0.f, e = 0.f;
+      cudaEventElapsedTime(&s, t0, r.a);
+      cudaEventElapsedTime(&e, t0, r.b);
+      const char* name = "?";
+      cudaFuncGetName(&name, r.fn);
+      snprintf(line, sizeof line, "%.2f %.2f %p %s\n", 1000.0 * s, 1000.0 * e, (void*)r.st, name);
+      out += line;
+    }
+  }
+  g_trace.clear();
+  if (buf && n) {
+    const size_t k = out.size() < n - 1 ? out.size() : n - 1;
+    memcpy(buf, out.data(), k);
+    buf[k] = 0;
+  }
+  return (int)out.size();
+}
 
 size_t d2ip_conv3d_ws_bytes(int cin, int cout, int ksize, int stride, int precision, int batch) {
   const size_t a = d2ip::conv_ws(cin, cout, ksize, stride, precision, batch, 0);
@@ -92,12 +164,16 @@ int d2ip_conv3d_fwd(d2ip_act x, const float* w, const float* bias, long long wbs
                     void* stream) {
   using namespace d2ip;
   D2IP_RET(check_conv_shapes(x, y, ksize, stride));
-  if (conv_tc_supported(x.c, y.c, ksize, stride, precision)) {
+  TcDims t;
+  if (conv_tc_layer(x.c, y.c, ksize, stride, 0, precision, (long long)y.d * y.h * y.w, &t)) {
     D2IP_CHECK_ARG(ws && ws_bytes >= conv_ws(x.c, y.c, ksize, stride, precision, batch, 0),
                    "conv3d_fwd: workspace too small for the packed weights");
     float* pk = reinterpret_cast<float*>(ws);
-    D2IP_RET(conv_tc_pack(w, wbstride, x.c, y.c, 0, pk, batch, S(stream)));
-    return conv_tc_run(x, pk, x.c, y.c, bias, wbstride, y, accumulate, nullptr, 0, batch, S(stream));
+    D2IP_RET(conv_tc_pack(w, wbstride, t.K, t.N, t.pack, pk, batch, S(stream)));
+    const size_t pkb = conv_ws(x.c, y.c, ksize, stride, precision, batch, 0);
+    // workspace beyond the packed weights holds split-K partials (used when large enough)
+    return conv_tc_run(x, pk, t.K, t.N, bias, wbstride, y, accumulate, reinterpret_cast<float*>((char*)ws + pkb),
+                       ws_bytes - pkb, batch, S(stream), nullptr, t.mode);
   }
   return conv_fwd_direct(x, w, bias, wbstride, ksize, stride, y, accumulate, batch, S(stream));
 }
@@ -106,12 +182,15 @@ int d2ip_conv3d_dgrad(d2ip_act gy, const float* w, long long wbstride, int ksize
                       int accumulate, int precision, void* ws, size_t ws_bytes, int batch, void* stream) {
   using namespace d2ip;
   D2IP_RET(check_conv_shapes(gx, gy, ksize, stride));
-  if (conv_tc_supported(gy.c, gx.c, ksize, stride, precision)) {
+  TcDims t;
+  if (conv_tc_layer(gx.c, gy.c, ksize, stride, 1, precision, (long long)gy.d * gy.h * gy.w, &t)) {
     D2IP_CHECK_ARG(ws && ws_bytes >= conv_ws(gx.c, gy.c, ksize, stride, precision, batch, 1),
                    "conv3d_dgrad: workspace too small for the packed weights");
     float* pk = reinterpret_cast<float*>(ws);
-    D2IP_RET(conv_tc_pack(w, wbstride, gy.c, gx.c, 1, pk, batch, S(stream)));
-    return conv_tc_run(gy, pk, gy.c, gx.c, nullptr, 0, gx, accumulate, nullptr, 0, batch, S(stream));
+    D2IP_RET(conv_tc_pack(w, wbstride, t.K, t.N, t.pack, pk, batch, S(stream)));
+    const size_t pkb = conv_ws(gx.c, gy.c, ksize, stride, precision, batch, 1);
+    return conv_tc_run(gy, pk, t.K, t.N, nullptr, 0, gx, accumulate, reinterpret_cast<float*>((char*)ws + pkb),
+                       ws_bytes - pkb, batch, S(stream), nullptr, t.mode);
   }
   return conv_dgrad_direct(gy, w, wbstride, ksize, stride, gx, accumulate, batch, S(stream));
 }

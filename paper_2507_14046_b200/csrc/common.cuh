@@ -54,6 +54,12 @@ inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
     asm volatile("griddepcontrol.wait;" ::: "memory");                \
   } while (0)
 
+// Launch tracing (debug: d2ip_trace_begin / d2ip_trace_dump): events around
+// every launch, so a step's real concurrent timeline can be read back.
+extern int g_trace_on;
+void trace_pre(cudaStream_t st, const void* fn);
+void trace_post(cudaStream_t st);
+
 template <typename... KArgs, typename... Args>
 inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
                               Args&&... args) {
@@ -67,7 +73,10 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+  if (g_trace_on) trace_pre(st, reinterpret_cast<const void*>(kernel));
+  const cudaError_t e = cudaLaunchKernelEx(&cfg, kernel, static_cast<KArgs>(args)...);
+  if (g_trace_on) trace_post(st);
+  return e;
 }
 
 inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }

@@ -26,6 +26,17 @@
 // Weights are split once per iteration by the pack kernel; the activation
 // window is split in shared memory after it lands.
 //
+// Stride 2 (mode 1 / 2) by parity decomposition: with x = 2o + k - 1, tap
+// k = 0 reads parity 1 of voxel o - 1, k = 1 parity 0 of o, k = 2 parity 1 of
+// o, so a stride-2 3^3 conv is a stride-1 conv over the output grid whose
+// input channels are the 8 parity classes x input channels ("space to depth",
+// gathered by the producers, never materialised) and whose taps per axis are
+// the offsets {-1, 0} only (t0 = 0, nt = 2: 8 of 27 taps, 2 of 3 planes).
+// Its data gradient is the mirror image: a stride-1 conv over the gy grid with
+// offsets {0, +1} (t0 = 1) and 8 x C_in output columns, each column block
+// scattered by the epilogue to its parity voxel 2o + p of gx. The pack kernel
+// lays out the parity weights (zeros where a parity has no tap).
+//
 // Pipeline: 2 smem stages filled with cp.async (16 B, zero-fill outside the
 // grid) by all 128 threads; thread 0 issues the MMAs of a stage and commits
 // them to that stage's mbarrier, which gates the refill of the buffer.
@@ -59,17 +70,20 @@ struct TcConv {
   int T;        // 128-row tiles per CTA: T TMEM accumulators share every stage's weight tile
   uint32_t idesc;
   int kspl;     // split-K factor over the (plane tap, channel block) stages
-  float* part;  // kspl > 1: partial sums [b][kspl][V][N]
+  float* part;  // kspl > 1: partial sums [b][kspl][V][N] (mode 2: [b][kspl][V_gx][C_gx])
   long long vout;
+  int mode;     // 0: stride 1; 1: stride-2 forward (parity-gathered input); 2: stride-2 dgrad (parity-scattered output)
+  int t0, nt;   // taps per axis used: t0 .. t0 + nt - 1 (offsets t - 1)
+  int gd, gh, gw;  // row-space grid (stride 1: x; mode 1: y; mode 2: gy)
 };
 
-// Per stage: A hi + A lo windows, B hi + B lo tiles.
-static size_t stage_bytes(int cb, int np, int wrp) {
-  return 2 * ((size_t)cb * wrp * 4 + (size_t)9 * cb * np * 4);
+// Per stage: A hi + A lo windows, B hi + B lo tiles (nt^2 taps).
+static size_t stage_bytes(int cb, int np, int wrp, int nt = 3) {
+  return 2 * ((size_t)cb * wrp * 4 + (size_t)nt * nt * cb * np * 4);
 }
 
 static size_t tc_smem_bytes(const TcConv& a) {
-  return 2 * stage_bytes(a.CB, a.Ns, a.WRp) + 3 * a.WR * sizeof(int) + 8 + 5 * 8 + 16;
+  return 2 * stage_bytes(a.CB, a.Ns, a.WRp, a.nt) + 3 * a.WR * sizeof(int) + 8 + 5 * 8 + 16;
 }
 
 __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
@@ -78,7 +92,9 @@ __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__flo
 // loops need no integer division).
 // PG: producer groups (1: all eight producer warps fill each stage; 2: two
 // groups of four fill alternate stages, two stages in flight).
-template <int NKC, int T, int PG>
+// MODE: 0 stride 1, 1 / 2 stride-2 forward / data gradient (compile-time, so
+// the stride-1 issue loop keeps its constant tap arithmetic).
+template <int NKC, int T, int PG, int MODE>
 __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
   D2IP_PDL_ENTRY();
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -89,7 +105,10 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
   const int n0 = (blockIdx.y / a.kspl) * a.Ns;  // first output channel of this CTA's slice
   const int u0 = a.u_first + blockIdx.x * T * kTcRows;
   const int Ns = a.Ns, WR = a.WR, WRp = a.WRp;
-  const uint32_t Ab = (uint32_t)NKC * WRp * 16, Bb = (uint32_t)9 * NKC * Ns * 16;
+  constexpr int nt = MODE ? 2 : 3, t0 = MODE == 2 ? 1 : 0, ntap = nt * nt;
+  // (kh, kw) of the q-th live tap as a 3x3 index: nt = 3 -> q; nt = 2 -> the 2x2 block at (t0, t0)
+  auto tap9 = [&](int q) { return nt == 3 ? q : (t0 + (q >> 1)) * 3 + (t0 + (q & 1)); };
+  const uint32_t Ab = (uint32_t)NKC * WRp * 16, Bb = (uint32_t)ntap * NKC * Ns * 16;
   const uint32_t Sb = 2 * (Ab + Bb);
   // layout: 2 stages of [A hi][A lo][B hi][B lo], row map, barriers full[2] empty[2] done, TMEM slot
   int* rowmap = reinterpret_cast<int*>(smem + 2 * Sb);
@@ -107,7 +126,8 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
     tc::mbar_init(done, 1);
     tc::fence_mbar_init();
   }
-  // voxel offset of every window row for the three plane taps (-1 = padding)
+  // voxel offset of every window row for the three plane taps (-1 = padding);
+  // mode 1: (even-corner input voxel << 3) | which odd parities exist per axis
   const d2ip_act x = a.x;
   for (int i = tid; i < 3 * WR; i += kTcThreads) {
     const int kd = i / WR, r = i - kd * WR;
@@ -116,8 +136,15 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
     if (u >= 0) {
       const int dp = u / a.Sh, rem = u - dp * a.Sh;
       const int hp = rem / a.Sw, wp = rem - hp * a.Sw;
-      if (dp >= 1 && dp <= x.d && hp >= 1 && hp <= x.h && wp >= 1 && wp <= x.w)
-        off = ((dp - 1) * x.h + (hp - 1)) * x.w + (wp - 1);
+      if (dp >= 1 && dp <= a.gd && hp >= 1 && hp <= a.gh && wp >= 1 && wp <= a.gw) {
+        if (MODE == 1) {
+          const int d2 = 2 * (dp - 1), h2 = 2 * (hp - 1), w2 = 2 * (wp - 1);
+          off = (((d2 * x.h + h2) * x.w + w2) << 3) | ((d2 + 1 < x.d) << 2) | ((h2 + 1 < x.h) << 1) |
+                (w2 + 1 < x.w);
+        } else {
+          off = ((dp - 1) * a.gh + (hp - 1)) * a.gw + (wp - 1);
+        }
+      }
     }
     rowmap[i] = off;
   }
@@ -127,7 +154,7 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
   const uint32_t tmem = *tslot;
   const float* xb = x.ptr + b * x.bstride;
   const float* wpb = a.wp + b * a.wpbs;
-  const int S_all = 3 * a.n_cb;
+  const int S_all = nt * a.n_cb;
   const int s_lo = (int)((long long)ks * S_all / a.kspl), s_hi = (int)((long long)(ks + 1) * S_all / a.kspl);
   const int S = s_hi - s_lo;  // this CTA's stages: s_lo + [0, S)
   const int nA = WR * NKC;
@@ -146,12 +173,13 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
         tc::mbar_wait(&full[slot], (uint32_t)((s >> 1) & 1));
         tc::fence_after();
         const uint64_t boff = slot ? (uint64_t)(Sb >> 4) : 0;
-        for (int t9 = 0; t9 < 9; ++t9) {
-          const int rowoff = (t9 / 3) * a.Sw + (t9 % 3);
+        for (int tq = 0; tq < ntap; ++tq) {
+          const int t9 = tap9(tq);
+          const int rowoff = (t9 >= 6 ? 2 : t9 >= 3 ? 1 : 0) * a.Sw + (t9 % 3);
 #pragma unroll
           for (int j = 0; j < NKC / 2; ++j) {
-            const uint64_t bo = boff + (uint64_t)((t9 * NKC + 2 * j) * Ns);
-            const uint32_t first = (s | t9 | j) ? 1u : 0u;
+            const uint64_t bo = boff + (uint64_t)((tq * NKC + 2 * j) * Ns);
+            const uint32_t first = (s | tq | j) ? 1u : 0u;
 #pragma unroll
             for (int tt = 0; tt < T; ++tt) {  // sub-tile tt: rows + 128 tt, accumulator columns + tt Ns
               const uint64_t ao = boff + (uint64_t)(2 * j * WRp + rowoff + tt * kTcRows);
@@ -175,22 +203,39 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
       const int slot = s & 1;
       if (s >= 2) tc::mbar_wait(&empty[slot], (uint32_t)(((s >> 1) - 1) & 1));
       const int sg = s_lo + s;
-      const int kd = sg / a.n_cb, cb = sg - kd * a.n_cb;
+      const int kdi = sg / a.n_cb, cb = sg - kdi * a.n_cb;
+      const int kd = t0 + kdi;
       const int* rm = rowmap + kd * WR;
       uint8_t* A = smem + slot * Sb;
-      const float* xc = xb + cb * CB;
-      for (int i = gtid; i < nA; i += GT) {
-        const int r = i / NKC, kc = i % NKC;
-        const int off = rm[r];
-        const float* src = off >= 0 ? xc + (long long)off * x.cstride + 4 * kc : xb;
-        tc::cp_async16(A + ((size_t)kc * WRp + r) * 16, src, off >= 0 ? 16u : 0u);
+      if (MODE == 1) {
+        // parity gather: virtual channel c = p * C_x + ci reads input voxel 2o + p
+        const long long plane = (long long)x.h * x.w;
+        for (int i = gtid; i < nA; i += GT) {
+          const int r = i / NKC, kc = i % NKC;
+          const int off = rm[r];
+          const int c = cb * CB + 4 * kc, p = c / x.c, ci = c - p * x.c;
+          const int pd = p >> 2, ph = (p >> 1) & 1, pw = p & 1;
+          const bool ok = off >= 0 && (!pd || (off & 4)) && (!ph || (off & 2)) && (!pw || (off & 1));
+          const float* src =
+              ok ? xb + ((off >> 3) + pd * plane + ph * x.w + pw) * (long long)x.cstride + ci : xb;
+          tc::cp_async16(A + ((size_t)kc * WRp + r) * 16, src, ok ? 16u : 0u);
+        }
+      } else {
+        const float* xc = xb + cb * CB;
+        for (int i = gtid; i < nA; i += GT) {
+          const int r = i / NKC, kc = i % NKC;
+          const int off = rm[r];
+          const float* src = off >= 0 ? xc + (long long)off * x.cstride + 4 * kc : xb;
+          tc::cp_async16(A + ((size_t)kc * WRp + r) * 16, src, off >= 0 ? 16u : 0u);
+        }
       }
-      // B: 9 taps x NKC chunks, each a contiguous run of Ns 16-byte rows; one warp per run
+      // B: nt^2 taps x NKC chunks, each a contiguous run of Ns 16-byte rows; one warp per run
       uint8_t* Bt = A + 2 * Ab;
       const float* wk = wpb + ((long long)(kd * 9) * kc_all + cb * NKC) * a.Np * 4 + (long long)n0 * 4;
       const int gwarp = gtid >> 5;
-      for (int q = gwarp; q < 9 * NKC; q += GT / 32) {
-        const int t9 = q / NKC, kcl = q % NKC;
+      for (int q = gwarp; q < ntap * NKC; q += GT / 32) {
+        const int tq = q / NKC, kcl = q % NKC;
+        const int t9 = tap9(tq);
         const float* src = wk + ((long long)t9 * kc_all + kcl) * a.Np * 4;
         uint8_t* dst = Bt + (size_t)q * Ns * 16;
         for (int n = lane; n < Ns; n += 32) {
@@ -226,14 +271,43 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
     const float* bias = a.bias ? a.bias + b * a.bbs : nullptr;
     for (int tt = 0; tt < T; ++tt) {
       const int u = u0 + tt * kTcRows + row;
-      int v = -1;
+      int v = -1, dq = 0, hq = 0, wq = 0;
       {
         const int dp = u / a.Sh, rem = u - dp * a.Sh;
         const int hp = rem / a.Sw, wp = rem - hp * a.Sw;
-        if (dp >= 1 && dp <= x.d && hp >= 1 && hp <= x.h && wp >= 1 && wp <= x.w)
-          v = ((dp - 1) * x.h + (hp - 1)) * x.w + (wp - 1);
+        if (dp >= 1 && dp <= a.gd && hp >= 1 && hp <= a.gh && wp >= 1 && wp <= a.gw) {
+          v = ((dp - 1) * a.gh + (hp - 1)) * a.gw + (wp - 1);
+          dq = dp - 1; hq = hp - 1; wq = wp - 1;
+        }
       }
       const uint32_t tcol = trow + (uint32_t)(tt * Ns);
+      if (MODE == 2) {  // column n = p * C_gx + ci -> gx voxel 2o + p (8 columns share p)
+        const int cy = y.c;
+        for (int c0 = cbeg; c0 < cend; c0 += 8) {
+          float vals[8];
+          tc::tmem_ld8(tcol + c0, vals);
+          const int n = n0 + c0;
+          if (v < 0 || n >= a.N) continue;
+          const int p = n / cy, ci = n - p * cy;
+          const int d2 = 2 * dq + (p >> 2), h2 = 2 * hq + ((p >> 1) & 1), w2 = 2 * wq + (p & 1);
+          if (d2 >= y.d || h2 >= y.h || w2 >= y.w) continue;
+          const long long vf = ((long long)d2 * y.h + h2) * y.w + w2;
+          if (a.kspl > 1) {
+            float* pp = a.part + (((long long)b * a.kspl + ks) * a.vout + vf) * cy + ci;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) pp[j] = S > 0 ? vals[j] : 0.f;
+          } else {
+            float* yp = y.ptr + b * y.bstride + vf * y.cstride + ci;
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              float o = S > 0 ? vals[j] : 0.f;
+              if (a.accumulate) o += yp[j];
+              yp[j] = o;
+            }
+          }
+        }
+        continue;
+      }
       if (a.kspl > 1) {  // raw partial sums; the consumer adds bias / accumulates
         float* pp = v >= 0 ? a.part + (((long long)b * a.kspl + ks) * a.vout + v) * a.N : nullptr;
         for (int c0 = cbeg; c0 < cend; c0 += 8) {
@@ -287,9 +361,33 @@ __global__ void conv_tc_splitk_reduce_k(const float* __restrict__ part, int kspl
   *yp = accumulate ? *yp + s : s;
 }
 
+// Stride-2 parity taps: the original tap index along one axis that pairs GEMM
+// tap ta (offset ta - 1) with parity pa, or -1 (no such tap; weight 0).
+__device__ __forceinline__ int s2_axis(int ta, int pa, int dgrad) {
+  if (ta == 1) return pa ? 2 : 1;  // offset 0: x = 2o (k = 1) or 2o + 1 (k = 2)
+  if (!dgrad) return (ta == 0 && pa) ? 0 : -1;  // forward offset -1: x = 2(o - 1) + 1 (k = 0)
+  return (ta == 2 && pa) ? 0 : -1;              // dgrad offset +1: gx 2o + 1 <- gy o + 1 (k = 0)
+}
+
+// One packed weight: code 0 forward, 1 stride-1 dgrad, 2 stride-2 forward
+// (k = p C_in + ci), 3 stride-2 dgrad (n = p C_in + ci).
+__device__ __forceinline__ float pack_val(const float* wb, int K, int N, int code, int t, int k, int n) {
+  if (code == 0) return wb[((long long)n * K + k) * 27 + t];
+  if (code == 1) return wb[((long long)k * N + n) * 27 + (26 - t)];
+  const int cin = code == 2 ? K >> 3 : N >> 3;
+  const int pc = code == 2 ? k : n;
+  const int p = pc / cin, ci = pc - p * cin;
+  const int kd = s2_axis(t / 9, p >> 2, code == 3), kh = s2_axis((t / 3) % 3, (p >> 1) & 1, code == 3),
+            kw = s2_axis(t % 3, p & 1, code == 3);
+  if (kd < 0 || kh < 0 || kw < 0) return 0.f;
+  const int co = code == 2 ? n : k;
+  return wb[((long long)co * cin + ci) * 27 + kd * 9 + kh * 3 + kw];
+}
+
 // Pack OIDHW weights into [b][hi|lo][tap][K/4][Np][4] (K-major B tiles).
 //   forward: K = C_in,  N = C_out:  P[t][k][n] = W[n][k][t]
 //   dgrad  : K = C_out, N = C_in :  P[t][k][n] = W[k][n][26 - t]
+//   stride 2: the parity layouts of pack_val (codes 2, 3)
 __global__ void conv_tc_pack_k(const float* __restrict__ w, long long wbs, int K, int N, int Np, int dgrad,
                                float* __restrict__ out, long long half, long long obs) {
   D2IP_PDL_ENTRY();
@@ -303,11 +401,7 @@ __global__ void conv_tc_pack_k(const float* __restrict__ w, long long wbs, int K
   const int kc = (int)(q2 % (K / 4));
   const int t = (int)(q2 / (K / 4));
   const int k = 4 * kc + j;
-  float val = 0.f;
-  if (n < N) {
-    const float* wb = w + b * wbs;
-    val = dgrad ? wb[((long long)k * N + n) * 27 + (26 - t)] : wb[((long long)n * K + k) * 27 + t];
-  }
+  const float val = n < N ? pack_val(w + b * wbs, K, N, dgrad, t, k, n) : 0.f;
   const float hi = tf32_hi(val);
   out[b * obs + i] = hi;
   out[b * obs + half + i] = val - hi;
@@ -330,11 +424,7 @@ __global__ void conv_tc_pack_multi_k(PackJobs j) {
   const int kc = (int)(q2 % (K / 4));
   const int t = (int)(q2 / (K / 4));
   const int k = 4 * kc + jj;
-  float val = 0.f;
-  if (n < N) {
-    const float* wb = j.w[q] + b * j.wbs;
-    val = j.dgrad[q] ? wb[((long long)k * N + n) * 27 + (26 - t)] : wb[((long long)n * K + k) * 27 + t];
-  }
+  const float val = n < N ? pack_val(j.w[q] + b * j.wbs, K, N, j.dgrad[q], t, k, n) : 0.f;
   const float hi = tf32_hi(val);
   float* out = j.out[q] + b * 2 * half;
   out[i] = hi;
@@ -365,6 +455,37 @@ bool conv_tc_supported(int cin, int cout, int ks, int stride, int precision) {
   return true;
 }
 
+bool conv_tc_layer(int cin, int cout, int ks, int stride, int dgrad, int precision, long long vout, TcDims* d) {
+  TcDims r{};
+  if (stride == 1) {
+    r.K = dgrad ? cout : cin;
+    r.N = dgrad ? cin : cout;
+    r.mode = 0;
+    r.pack = dgrad;
+    if (!conv_tc_supported(r.K, r.N, ks, 1, precision)) return false;
+  } else {
+    // Below ~4M output-voxel x channel-pair products the direct CUDA-core kernel
+    // is faster (tools/conv_bench.py: 16->32 at 16^3 out 24 vs 29 us; 32->64 at
+    // 16^3 out 110 vs 50 us, at 32^3 out 98 vs 73 us). D2IP_TC_S2=0 / 2 forces
+    // the direct / tcgen05 kernel.
+    static const int s2 = [] {
+      const char* v = getenv("D2IP_TC_S2");
+      return v ? atoi(v) : 1;
+    }();
+    if (!s2 || precision != D2IP_PREC_TF32 || ks != 3 || stride != 2) return false;
+    if (s2 == 1 && vout >= 0 && vout * cin * cout < 4LL * 1024 * 1024) return false;
+    if (!dgrad) {  // K = 8 C_in: a 16-byte chunk must not straddle two parities
+      if (cin % 4 || cout < 1 || np_of(cout) > 1024) return false;
+      r = TcDims{8 * cin, cout, 1, 2};
+    } else {       // 8 epilogue columns share one parity
+      if (cout % 8 || cin % 8 || np_of(8 * cin) > 1024) return false;
+      r = TcDims{cout, 8 * cin, 2, 3};
+    }
+  }
+  if (d) *d = r;
+  return true;
+}
+
 long long conv_tc_pack_floats(int K, int N) { return 2 * 27LL * K * np_of(N); }
 
 int conv_tc_pack(const float* w, long long wbs, int K, int N, int dgrad, float* out, int batch, cudaStream_t st) {
@@ -380,7 +501,7 @@ int conv_tc_pack(const float* w, long long wbs, int K, int N, int dgrad, float* 
 // small latency model -- waves x (serial stages per CTA + fixed prologue /
 // epilogue cost) -- because at these sizes a CTA's chain of dependent stages,
 // not the tensor pipe, sets the time.
-static bool tc_plan(int D, int H, int W, int K, int N, int batch, TcConv& a, int* tiles) {
+static bool tc_plan(int D, int H, int W, int K, int N, int batch, TcConv& a, int* tiles, int nt = 3) {
   a.N = N;
   a.Np = np_of(N);
   a.Kc = K;
@@ -398,7 +519,7 @@ static bool tc_plan(int D, int H, int W, int K, int N, int batch, TcConv& a, int
   // a stage costs max(cp.async landing ~1.5, its MMAs: 27/8 CB T x 57 cycles).
   const bool large = (long long)tiles1 * batch >= 4LL * 296;
   for (int T : {1, 2, 4}) {
-    if (T > 1 && !large) break;
+    if (T > 1 && (!large || nt != 3)) break;
     const int wr = wr_of(a.Sw, T), wrp = wrp_of(wr);
     const int tl = cdiv(tiles1, T);
     for (int ns = std::min(a.Np, 256); ns >= 16; ns -= 16) {
@@ -406,11 +527,11 @@ static bool tc_plan(int D, int H, int W, int K, int N, int batch, TcConv& a, int
       if (T * ns > 512) continue;  // TMEM columns
       for (int cb = 8; cb <= K && cb <= 64; cb *= 2) {
         if (K % cb) continue;
-        const size_t sm = 2 * stage_bytes(cb, ns, wrp) + 3 * wr * sizeof(int) + 64;
+        const size_t sm = 2 * stage_bytes(cb, ns, wrp, nt) + 3 * wr * sizeof(int) + 64;
         if (sm > (size_t)210 * 1024) continue;
         const int per_sm = sm <= (size_t)110 * 1024 ? 2 : 1;
         const long long ctas0 = (long long)tl * (a.Np / ns) * batch;
-        const int S = 3 * (K / cb);
+        const int S = nt * (K / cb);
         // split the stage chain across CTAs until ~2 CTAs per SM are busy
         const int kspl = (int)std::min<long long>(S, std::max(1LL, (296 + ctas0 - 1) / ctas0));
         const long long waves = (ctas0 * kspl + 148LL * per_sm - 1) / (148LL * per_sm);
@@ -418,7 +539,7 @@ static bool tc_plan(int D, int H, int W, int K, int N, int batch, TcConv& a, int
         if (!large) {
           cost = (double)waves * ((S + kspl - 1) / kspl + 2.0) + (kspl > 1 ? 1.0 : 0.0);
         } else {
-          const double mma_us = 27.0 / 8.0 * cb * T * 57.0 / 1900.0 * (per_sm == 2 ? 1.4 : 1.0);
+          const double mma_us = 3.0 * nt * nt / 8.0 * cb * T * 57.0 / 1900.0 * (per_sm == 2 ? 1.4 : 1.0);
           const double stage_us = std::max(1.5, mma_us);
           cost = (double)waves * ((S + kspl - 1) / kspl * stage_us + 2.0 + 0.5 * T) + (kspl > 1 ? 3.0 : 0.0);
         }
@@ -440,22 +561,36 @@ static bool tc_plan(int D, int H, int W, int K, int N, int batch, TcConv& a, int
   return true;
 }
 
-size_t conv_tc_ws_bytes(int D, int H, int W, int K, int N, int batch) {
+size_t conv_tc_ws_bytes(int D, int H, int W, int K, int N, int batch, int mode) {
   TcConv a{};
   int tiles;
-  if (!tc_plan(D, H, W, K, N, batch, a, &tiles) || a.kspl <= 1) return 0;
+  if (!tc_plan(D, H, W, K, N, batch, a, &tiles, mode ? 2 : 3) || a.kspl <= 1) return 0;
+  // mode 2 partials are [V_gx][C_gx]: V_gx C_gx <= 8 V N / 8 (gx dims <= 2 x the row grid)
   return (size_t)batch * a.kspl * a.vout * N * sizeof(float);
 }
 
 int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, long long bbs, d2ip_act y,
-                int accumulate, float* ws, size_t ws_bytes, int batch, cudaStream_t st, int* deferred) {
-  D2IP_CHECK_ARG(x.c == K && y.c == N, "conv_tc: channel mismatch");
+                int accumulate, float* ws, size_t ws_bytes, int batch, cudaStream_t st, int* deferred, int mode) {
+  D2IP_CHECK_ARG((mode == 1 ? 8 * x.c : x.c) == K && (mode == 2 ? 8 * y.c : y.c) == N, "conv_tc: channel mismatch");
   D2IP_CHECK_ARG(x.cstride % 4 == 0 && ((uintptr_t)x.ptr & 15) == 0, "conv_tc: input view must be 16B aligned");
+  D2IP_CHECK_ARG(mode != 2 || (y.cstride % 4 == 0 && ((uintptr_t)y.ptr & 15) == 0 && y.c % 8 == 0),
+                 "conv_tc: stride-2 dgrad output view must be 16B aligned with C %% 8 == 0");
+  const d2ip_act& g = mode == 1 ? y : x;  // the row-space grid
+  if (mode == 1) D2IP_CHECK_ARG(g.d == (x.d + 1) / 2 && g.h == (x.h + 1) / 2 && g.w == (x.w + 1) / 2, "conv_tc: stride-2 shape");
+  if (mode == 2) D2IP_CHECK_ARG(g.d == (y.d + 1) / 2 && g.h == (y.h + 1) / 2 && g.w == (y.w + 1) / 2, "conv_tc: stride-2 shape");
   TcConv a{};
   int tiles = 0;
-  D2IP_CHECK_ARG(tc_plan(x.d, x.h, x.w, K, N, batch, a, &tiles),
-                 "conv_tc: no channel blocking fits shared memory (K=%d N=%d W=%d)", K, N, x.w);
-  if (a.kspl > 1 && (!ws || ws_bytes < (size_t)batch * a.kspl * a.vout * N * sizeof(float))) a.kspl = 1;
+  D2IP_CHECK_ARG(tc_plan(g.d, g.h, g.w, K, N, batch, a, &tiles, mode ? 2 : 3),
+                 "conv_tc: no channel blocking fits shared memory (K=%d N=%d W=%d)", K, N, g.w);
+  a.mode = mode;
+  a.t0 = mode == 2 ? 1 : 0;
+  a.nt = mode ? 2 : 3;
+  a.gd = g.d;
+  a.gh = g.h;
+  a.gw = g.w;
+  const int Nout = mode == 2 ? y.c : N;  // channels of the stored result (partials too)
+  if (mode == 2) a.vout = (long long)y.d * y.h * y.w;
+  if (a.kspl > 1 && (!ws || ws_bytes < (size_t)batch * a.kspl * a.vout * Nout * sizeof(float))) a.kspl = 1;
   a.part = ws;
   a.x = x;
   a.wp = wp;
@@ -472,12 +607,14 @@ int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, lo
   const size_t smem = tc_smem_bytes(a);
   static bool attr_set = false;
   if (!attr_set) {
-    for (auto k : {conv_tc_k<2, 1, 1>, conv_tc_k<4, 1, 1>, conv_tc_k<8, 1, 1>, conv_tc_k<16, 1, 1>,
-                   conv_tc_k<2, 1, 2>, conv_tc_k<4, 1, 2>, conv_tc_k<8, 1, 2>, conv_tc_k<16, 1, 2>,
-                   conv_tc_k<2, 2, 1>, conv_tc_k<4, 2, 1>, conv_tc_k<8, 2, 1>, conv_tc_k<16, 2, 1>,
-                   conv_tc_k<2, 2, 2>, conv_tc_k<4, 2, 2>, conv_tc_k<8, 2, 2>, conv_tc_k<16, 2, 2>,
-                   conv_tc_k<2, 4, 1>, conv_tc_k<4, 4, 1>, conv_tc_k<8, 4, 1>, conv_tc_k<16, 4, 1>,
-                   conv_tc_k<2, 4, 2>, conv_tc_k<4, 4, 2>, conv_tc_k<8, 4, 2>, conv_tc_k<16, 4, 2>})
+    for (auto k : {conv_tc_k<2, 1, 1, 0>, conv_tc_k<4, 1, 1, 0>, conv_tc_k<8, 1, 1, 0>, conv_tc_k<16, 1, 1, 0>,
+                   conv_tc_k<2, 1, 2, 0>, conv_tc_k<4, 1, 2, 0>, conv_tc_k<8, 1, 2, 0>, conv_tc_k<16, 1, 2, 0>,
+                   conv_tc_k<2, 2, 1, 0>, conv_tc_k<4, 2, 1, 0>, conv_tc_k<8, 2, 1, 0>, conv_tc_k<16, 2, 1, 0>,
+                   conv_tc_k<2, 2, 2, 0>, conv_tc_k<4, 2, 2, 0>, conv_tc_k<8, 2, 2, 0>, conv_tc_k<16, 2, 2, 0>,
+                   conv_tc_k<2, 4, 1, 0>, conv_tc_k<4, 4, 1, 0>, conv_tc_k<8, 4, 1, 0>, conv_tc_k<16, 4, 1, 0>,
+                   conv_tc_k<2, 4, 2, 0>, conv_tc_k<4, 4, 2, 0>, conv_tc_k<8, 4, 2, 0>, conv_tc_k<16, 4, 2, 0>,
+                   conv_tc_k<2, 1, 1, 1>, conv_tc_k<4, 1, 1, 1>, conv_tc_k<8, 1, 1, 1>, conv_tc_k<16, 1, 1, 1>,
+                   conv_tc_k<2, 1, 1, 2>, conv_tc_k<4, 1, 1, 2>, conv_tc_k<8, 1, 1, 2>, conv_tc_k<16, 1, 1, 2>})
       D2IP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr_set = true;
   }
@@ -488,14 +625,16 @@ int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, lo
     const char* v = getenv("D2IP_TC_PG");
     return v && atoi(v) == 2;
   }();
-#define D2IP_TC_LAUNCH(NKC_)                                                                              \
-  do {                                                                                                    \
-    if (a.T == 4 && pg2) D2IP_CUDA(launch_pdl((conv_tc_k<NKC_, 4, 2>), grid, kTcThreads, smem, st, a));  \
-    else if (a.T == 4) D2IP_CUDA(launch_pdl((conv_tc_k<NKC_, 4, 1>), grid, kTcThreads, smem, st, a));    \
-    else if (a.T == 2 && pg2) D2IP_CUDA(launch_pdl((conv_tc_k<NKC_, 2, 2>), grid, kTcThreads, smem, st, a)); \
-    else if (a.T == 2) D2IP_CUDA(launch_pdl((conv_tc_k<NKC_, 2, 1>), grid, kTcThreads, smem, st, a));    \
-    else if (pg2) D2IP_CUDA(launch_pdl((conv_tc_k<NKC_, 1, 2>), grid, kTcThreads, smem, st, a));         \
-    else D2IP_CUDA(launch_pdl((conv_tc_k<NKC_, 1, 1>), grid, kTcThreads, smem, st, a));                  \
+#define D2IP_TC_LAUNCH(NKC_)                                                                                 \
+  do {                                                                                                       \
+    if (mode == 1) D2IP_CUDA(launch_pdl((conv_tc_k<NKC_, 1, 1, 1>), grid, kTcThreads, smem, st, a));        \
+    else if (mode == 2) D2IP_CUDA(launch_pdl((conv_tc_k<NKC_, 1, 1, 2>), grid, kTcThreads, smem, st, a));   \
+    else if (a.T == 4 && pg2) D2IP_CUDA(launch_pdl((conv_tc_k<NKC_, 4, 2, 0>), grid, kTcThreads, smem, st, a)); \
+    else if (a.T == 4) D2IP_CUDA(launch_pdl((conv_tc_k<NKC_, 4, 1, 0>), grid, kTcThreads, smem, st, a));    \
+    else if (a.T == 2 && pg2) D2IP_CUDA(launch_pdl((conv_tc_k<NKC_, 2, 2, 0>), grid, kTcThreads, smem, st, a)); \
+    else if (a.T == 2) D2IP_CUDA(launch_pdl((conv_tc_k<NKC_, 2, 1, 0>), grid, kTcThreads, smem, st, a));    \
+    else if (pg2) D2IP_CUDA(launch_pdl((conv_tc_k<NKC_, 1, 2, 0>), grid, kTcThreads, smem, st, a));         \
+    else D2IP_CUDA(launch_pdl((conv_tc_k<NKC_, 1, 1, 0>), grid, kTcThreads, smem, st, a));                  \
   } while (0)
   switch (a.CB / 4) {
     case 2: D2IP_TC_LAUNCH(2); break;
@@ -508,8 +647,8 @@ int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, lo
   D2IP_LAUNCH_CHECK();
   if (deferred) *deferred = a.kspl > 1 ? a.kspl : 0;
   if (a.kspl > 1 && !deferred) {
-    D2IP_CUDA(launch_pdl(conv_tc_splitk_reduce_k, dim3(cdiv(a.vout * N, 256), batch), 256, 0, st, ws, a.kspl,
-                         a.vout, N, bias, bbs, y, accumulate));
+    D2IP_CUDA(launch_pdl(conv_tc_splitk_reduce_k, dim3(cdiv(a.vout * Nout, 256), batch), 256, 0, st, ws, a.kspl,
+                         a.vout, Nout, bias, bbs, y, accumulate));
     D2IP_LAUNCH_CHECK();
   }
   set_variant(a.kspl > 1 ? "tcgen05_tf32x3_splitk" : "tcgen05_tf32x3");

@@ -194,53 +194,61 @@ int upsample2x_bwd(d2ip_act gy, d2ip_act gx, int accumulate, int batch, cudaStre
 
 // ---------------------------------------------------------------------------
 // Tail: conv3(c0 -> 1) + bias -> sigmoid -> lo + scale * s, and the gather of
-// the mapped value into J's column order (sigma_c[col_of_vox[v]]).
-__global__ void __launch_bounds__(128) tail_fwd_k(d2ip_act x, const float* __restrict__ w,
-                                                  const float* __restrict__ bias, long long wbs,
-                                                  float lo, float scale, float* __restrict__ sig,
-                                                  float* __restrict__ mapped, float* __restrict__ sigma_c,
-                                                  long long sc_bs, const int* __restrict__ col_of_vox) {
+// the mapped value into J's column order (sigma_c[col_of_vox[v]]). The three
+// kd planes of taps are split over three thread slices (32 voxels x 3 per
+// block; plane sums added in order through shared memory), each slice keeping
+// four independent partial sums -- a 12x shorter FMA chain than one thread per
+// voxel.
+__global__ void __launch_bounds__(96) tail_fwd_k(d2ip_act x, const float* __restrict__ w,
+                                                 const float* __restrict__ bias, long long wbs,
+                                                 float lo, float scale, float* __restrict__ sig,
+                                                 float* __restrict__ mapped, float* __restrict__ sigma_c,
+                                                 long long sc_bs, const int* __restrict__ col_of_vox) {
   D2IP_PDL_ENTRY();
-  extern __shared__ float sw[];  // [tap][cin]
+  extern __shared__ float sw[];  // [tap][cin], then [3][32] plane sums
   const int b = blockIdx.y;
   const int cin = x.c;
   const float* wb = w + b * wbs;
   for (int i = threadIdx.x; i < 27 * cin; i += blockDim.x) sw[i] = __ldg(wb + (i % cin) * 27 + i / cin);
+  float* red = sw + 27 * cin;
   __syncthreads();
   const long long V = (long long)x.d * x.h * x.w;
-  const long long v = (long long)blockIdx.x * blockDim.x + threadIdx.x;
-  if (v >= V) return;
-  const int ow = (int)(v % x.w), oh = (int)((v / x.w) % x.h), od = (int)(v / ((long long)x.w * x.h));
-  const float* xb = x.ptr + b * x.bstride;
-  const bool vec = (cin % 4 == 0) && (x.cstride % 4 == 0) && (((uintptr_t)x.ptr & 15) == 0);
-  // four independent partial sums (one per float4 lane): a 4x shorter FMA chain
+  const int kd = threadIdx.x / 32, vl = threadIdx.x % 32;
+  const long long v = (long long)blockIdx.x * 32 + vl;
   float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-  for (int kd = 0; kd < 3; ++kd) {
+  if (v < V) {
+    const int ow = (int)(v % x.w), oh = (int)((v / x.w) % x.h), od = (int)(v / ((long long)x.w * x.h));
+    const float* xb = x.ptr + b * x.bstride;
+    const bool vec = (cin % 4 == 0) && (x.cstride % 4 == 0) && (((uintptr_t)x.ptr & 15) == 0);
     const int id = od + kd - 1;
-    if (id < 0 || id >= x.d) continue;
-    for (int kh = 0; kh < 3; ++kh) {
-      const int ih = oh + kh - 1;
-      if (ih < 0 || ih >= x.h) continue;
-      for (int kw = 0; kw < 3; ++kw) {
-        const int iw = ow + kw - 1;
-        if (iw < 0 || iw >= x.w) continue;
-        const float* xp = xb + (((long long)id * x.h + ih) * x.w + iw) * x.cstride;
-        const float* wr = sw + ((kd * 3 + kh) * 3 + kw) * cin;
-        if (vec) {
-          for (int ci = 0; ci < cin; ci += 4) {
-            const float4 q = __ldg(reinterpret_cast<const float4*>(xp + ci));
-            a0 = fmaf(q.x, wr[ci], a0);
-            a1 = fmaf(q.y, wr[ci + 1], a1);
-            a2 = fmaf(q.z, wr[ci + 2], a2);
-            a3 = fmaf(q.w, wr[ci + 3], a3);
+    if (id >= 0 && id < x.d) {
+      for (int kh = 0; kh < 3; ++kh) {
+        const int ih = oh + kh - 1;
+        if (ih < 0 || ih >= x.h) continue;
+        for (int kw = 0; kw < 3; ++kw) {
+          const int iw = ow + kw - 1;
+          if (iw < 0 || iw >= x.w) continue;
+          const float* xp = xb + (((long long)id * x.h + ih) * x.w + iw) * x.cstride;
+          const float* wr = sw + ((kd * 3 + kh) * 3 + kw) * cin;
+          if (vec) {
+            for (int ci = 0; ci < cin; ci += 4) {
+              const float4 q = __ldg(reinterpret_cast<const float4*>(xp + ci));
+              a0 = fmaf(q.x, wr[ci], a0);
+              a1 = fmaf(q.y, wr[ci + 1], a1);
+              a2 = fmaf(q.z, wr[ci + 2], a2);
+              a3 = fmaf(q.w, wr[ci + 3], a3);
+            }
+          } else {
+            for (int ci = 0; ci < cin; ++ci) a0 = fmaf(xp[ci], wr[ci], a0);
           }
-        } else {
-          for (int ci = 0; ci < cin; ++ci) a0 = fmaf(xp[ci], wr[ci], a0);
         }
       }
     }
   }
-  const float acc = __ldg(bias + b * wbs) + ((a0 + a1) + (a2 + a3));
+  red[kd * 32 + vl] = (a0 + a1) + (a2 + a3);
+  __syncthreads();
+  if (kd != 0 || v >= V) return;
+  const float acc = __ldg(bias + b * wbs) + ((red[vl] + red[32 + vl]) + red[64 + vl]);
   const float s = 1.0f / (1.0f + expf(-acc));
   const float mp = lo + scale * s;
   sig[b * V + v] = s;
@@ -253,9 +261,9 @@ int tail_fwd(d2ip_act x, const float* w, const float* bias, long long wbs, float
              float* sig, float* mapped, float* sigma_c, long long sc_bs, const int* col_of_vox,
              int batch, cudaStream_t st) {
   const long long V = (long long)x.d * x.h * x.w;
-  D2IP_CHECK_ARG(27 * x.c * sizeof(float) <= 48 * 1024, "tail: C_in too large");
-  D2IP_CUDA(launch_pdl(tail_fwd_k, dim3(cdiv(V, 128), batch), 128, 27 * x.c * sizeof(float), st, x, w, bias, wbs, lo, scale, sig, mapped,
-                                                         sigma_c, sc_bs, col_of_vox));
+  D2IP_CHECK_ARG(27 * x.c * sizeof(float) <= 40 * 1024, "tail: C_in too large");
+  D2IP_CUDA(launch_pdl(tail_fwd_k, dim3(cdiv(V, 32), batch), 96, (27 * x.c + 96) * sizeof(float), st, x, w, bias,
+                       wbs, lo, scale, sig, mapped, sigma_c, sc_bs, col_of_vox));
   D2IP_LAUNCH_CHECK();
   return D2IP_OK;
 }

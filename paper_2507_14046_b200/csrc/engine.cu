@@ -148,12 +148,14 @@ static void config_plan_workspace(d2ip_engine& E, Arena& A) {
   // packed tcgen05 weight tiles, refreshed from theta at the start of every forward
   size_t tcws = 0;  // split-K partials of the tcgen05 convs (max over layers)
   auto packs = [&](ConvP& cv, bool need_dgrad, int lvl) {
-    cv.tcf = conv_tc_supported(cv.cin, cv.cout, cv.ks, cv.stride, E.d.precision);
-    cv.tcd = need_dgrad && conv_tc_supported(cv.cout, cv.cin, cv.ks, cv.stride, E.d.precision);
-    cv.pkf = cv.tcf ? takef((long long)B * conv_tc_pack_floats(cv.cin, cv.cout)) : nullptr;
-    cv.pkd = cv.tcd ? takef((long long)B * conv_tc_pack_floats(cv.cout, cv.cin)) : nullptr;
-    if (cv.tcf) tcws = std::max(tcws, conv_tc_ws_bytes(E.D[lvl], E.H[lvl], E.W[lvl], cv.cin, cv.cout, B));
-    if (cv.tcd) tcws = std::max(tcws, conv_tc_ws_bytes(E.D[lvl], E.H[lvl], E.W[lvl], cv.cout, cv.cin, B));
+    cv.tcf = conv_tc_layer(cv.cin, cv.cout, cv.ks, cv.stride, 0, E.d.precision, E.V[lvl], &cv.tdf);
+    cv.tcd = need_dgrad && conv_tc_layer(cv.cin, cv.cout, cv.ks, cv.stride, 1, E.d.precision, E.V[lvl], &cv.tdd);
+    cv.pkf = cv.tcf ? takef((long long)B * conv_tc_pack_floats(cv.tdf.K, cv.tdf.N)) : nullptr;
+    cv.pkd = cv.tcd ? takef((long long)B * conv_tc_pack_floats(cv.tdd.K, cv.tdd.N)) : nullptr;
+    if (cv.tcf)
+      tcws = std::max(tcws, conv_tc_ws_bytes(E.D[lvl], E.H[lvl], E.W[lvl], cv.tdf.K, cv.tdf.N, B, cv.tdf.mode));
+    if (cv.tcd)
+      tcws = std::max(tcws, conv_tc_ws_bytes(E.D[lvl], E.H[lvl], E.W[lvl], cv.tdd.K, cv.tdd.N, B, cv.tdd.mode));
   };
   packs(E.stem, false, 0);
   packs(E.tail, true, 0);
@@ -239,8 +241,8 @@ static void plan_views(d2ip_engine& E) {
 int cfwd(Ctx& k, const ConvP& c, d2ip_act x, d2ip_act y, int acc, SplitK* sk) {
   if (c.tcf) {
     int kspl = 0;
-    D2IP_RET(conv_tc_run(x, c.pkf, c.cin, c.cout, k.th() + c.ob, k.pbs, y, acc, k.E.tc_ws, k.E.tc_ws_bytes, k.B, k.st,
-                         sk && !acc ? &kspl : nullptr));
+    D2IP_RET(conv_tc_run(x, c.pkf, c.tdf.K, c.tdf.N, k.th() + c.ob, k.pbs, y, acc, k.E.tc_ws, k.E.tc_ws_bytes, k.B,
+                         k.st, sk && !acc ? &kspl : nullptr, c.tdf.mode));
     if (sk) *sk = kspl ? SplitK{k.E.tc_ws, kspl, k.th() + c.ob, k.pbs} : SplitK{};
     return D2IP_OK;
   }
@@ -253,8 +255,8 @@ int cfwd(Ctx& k, const ConvP& c, d2ip_act x, d2ip_act y, int acc, SplitK* sk) {
 int cdgrad(Ctx& k, const ConvP& c, d2ip_act gy, d2ip_act gx, int acc, SplitK* sk) {
   if (c.tcd) {
     int kspl = 0;
-    D2IP_RET(conv_tc_run(gy, c.pkd, c.cout, c.cin, nullptr, 0, gx, acc, k.E.tc_ws, k.E.tc_ws_bytes, k.B, k.st,
-                         sk && !acc ? &kspl : nullptr));
+    D2IP_RET(conv_tc_run(gy, c.pkd, c.tdd.K, c.tdd.N, nullptr, 0, gx, acc, k.E.tc_ws, k.E.tc_ws_bytes, k.B, k.st,
+                         sk && !acc ? &kspl : nullptr, c.tdd.mode));
     if (sk) *sk = kspl ? SplitK{k.E.tc_ws, kspl, nullptr, 0} : SplitK{};
     return D2IP_OK;
   }
@@ -304,8 +306,8 @@ static void build_pack_jobs(d2ip_engine& E) {
   j = PackJobs{};
   j.wbs = E.nparams;
   auto add = [&](const ConvP& c) {
-    if (c.tcf) pack_jobs_add(j, E.b.theta + c.ow, c.cin, c.cout, 0, c.pkf);
-    if (c.tcd) pack_jobs_add(j, E.b.theta + c.ow, c.cout, c.cin, 1, c.pkd);
+    if (c.tcf) pack_jobs_add(j, E.b.theta + c.ow, c.tdf.K, c.tdf.N, c.tdf.pack, c.pkf);
+    if (c.tcd) pack_jobs_add(j, E.b.theta + c.ow, c.tdd.K, c.tdd.N, c.tdd.pack, c.pkd);
   };
   if (E.d.arch == D2IP_ARCH_FAST_RESUNET) {
     refnet_pack_jobs(E);

@@ -15,6 +15,7 @@ struct ConvP {
   long long ow = 0, ob = 0;
   int cin = 0, cout = 0, ks = 3, stride = 1, dil = 1;
   bool tcf = false, tcd = false;  // tcgen05 forward / data-gradient path
+  d2ip::TcDims tdf{}, tdd{};      // their GEMM views (K, N, mode, pack code)
   float* pkf = nullptr;           // packed weights [B][27][cin/4][Np][4] (forward)
   float* pkd = nullptr;           // packed flipped W^T (data gradient)
 };

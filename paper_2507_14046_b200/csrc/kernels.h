@@ -54,6 +54,13 @@ int wgrad_tc(d2ip_act x, d2ip_act gy, int ks, float* gw, long long gwbs, void* w
 
 // conv_tc.cu — tcgen05 implicit-GEMM convolutions (tf32 / bf16 operands)
 bool conv_tc_supported(int cin, int cout, int ks, int stride, int precision);
+// GEMM view of a layer's tcgen05 forward (dgrad = 0) or data gradient: K, N,
+// kernel mode (0 stride 1, 1 stride-2 forward, 2 stride-2 dgrad) and pack code.
+struct TcDims {
+  int K, N, mode, pack;
+};
+// vout: the layer's output voxels (-1: unknown) -- small stride-2 layers stay on the direct kernel
+bool conv_tc_layer(int cin, int cout, int ks, int stride, int dgrad, int precision, long long vout, TcDims* d);
 long long conv_tc_pack_floats(int K, int N);
 int conv_tc_pack(const float* w, long long wbs, int K, int N, int dgrad, float* out, int batch, cudaStream_t st);
 // One launch packing every tcgen05 layer of the network (weights change each step).
@@ -70,11 +77,13 @@ struct PackJobs {
 void pack_jobs_add(PackJobs& j, const float* w, int K, int N, int dgrad, float* out);
 int conv_tc_pack_multi(const PackJobs& jobs, int batch, cudaStream_t st);
 // ws (optional): split-K partials, conv_tc_ws_bytes() of them; null -> no split-K
-size_t conv_tc_ws_bytes(int D, int H, int W, int K, int N, int batch);
+// (D, H, W: the row-space grid = the layer's output grid, or gy's for a dgrad)
+size_t conv_tc_ws_bytes(int D, int H, int W, int K, int N, int batch, int mode = 0);
 // deferred != null: a split-K result is left as partials in ws (*deferred =
 // kspl, 0 if not split) for the consumer to reduce (norm_act_fwd's `part`).
 int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, long long bbs, d2ip_act y,
-                int accumulate, float* ws, size_t ws_bytes, int batch, cudaStream_t st, int* deferred = nullptr);
+                int accumulate, float* ws, size_t ws_bytes, int batch, cudaStream_t st, int* deferred = nullptr,
+                int mode = 0);
 
 // Split-K partial sums handed from a convolution to its consumer:
 // y[v][n] = bias[n] + sum_k part[b][k][v][n].

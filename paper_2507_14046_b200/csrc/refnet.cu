@@ -306,12 +306,12 @@ void refnet_plan_workspace(d2ip_engine& E, Arena& A) {
   // tcgen05 weight packs for the dense stride-1 3^3 layers
   size_t tcws = 0;
   auto packs = [&](ConvP& c, bool need_dgrad, int l) {
-    c.tcf = c.dil == 1 && conv_tc_supported(c.cin, c.cout, c.ks, c.stride, E.d.precision);
-    c.tcd = need_dgrad && c.dil == 1 && conv_tc_supported(c.cout, c.cin, c.ks, c.stride, E.d.precision);
-    c.pkf = c.tcf ? A.f((long long)B * conv_tc_pack_floats(c.cin, c.cout)) : nullptr;
-    c.pkd = c.tcd ? A.f((long long)B * conv_tc_pack_floats(c.cout, c.cin)) : nullptr;
-    if (c.tcf) tcws = std::max(tcws, conv_tc_ws_bytes(E.D[l], E.H[l], E.W[l], c.cin, c.cout, B));
-    if (c.tcd) tcws = std::max(tcws, conv_tc_ws_bytes(E.D[l], E.H[l], E.W[l], c.cout, c.cin, B));
+    c.tcf = c.dil == 1 && conv_tc_layer(c.cin, c.cout, c.ks, c.stride, 0, E.d.precision, E.V[l], &c.tdf);
+    c.tcd = need_dgrad && c.dil == 1 && conv_tc_layer(c.cin, c.cout, c.ks, c.stride, 1, E.d.precision, E.V[l], &c.tdd);
+    c.pkf = c.tcf ? A.f((long long)B * conv_tc_pack_floats(c.tdf.K, c.tdf.N)) : nullptr;
+    c.pkd = c.tcd ? A.f((long long)B * conv_tc_pack_floats(c.tdd.K, c.tdd.N)) : nullptr;
+    if (c.tcf) tcws = std::max(tcws, conv_tc_ws_bytes(E.D[l], E.H[l], E.W[l], c.tdf.K, c.tdf.N, B, c.tdf.mode));
+    if (c.tcd) tcws = std::max(tcws, conv_tc_ws_bytes(E.D[l], E.H[l], E.W[l], c.tdd.K, c.tdd.N, B, c.tdd.mode));
   };
   packs(N.stem, false, 0);
   packs(N.tail, true, 0);
@@ -330,8 +330,8 @@ void refnet_pack_jobs(d2ip_engine& E) {
   RefNet& N = *E.ref;
   PackJobs& j = E.packjobs;
   auto add = [&](const ConvP& c) {
-    if (c.tcf) pack_jobs_add(j, E.b.theta + c.ow, c.cin, c.cout, 0, c.pkf);
-    if (c.tcd) pack_jobs_add(j, E.b.theta + c.ow, c.cout, c.cin, 1, c.pkd);
+    if (c.tcf) pack_jobs_add(j, E.b.theta + c.ow, c.tdf.K, c.tdf.N, c.tdf.pack, c.pkf);
+    if (c.tcd) pack_jobs_add(j, E.b.theta + c.ow, c.tdd.K, c.tdd.N, c.tdd.pack, c.pkd);
   };
   add(N.stem);
   add(N.tail);

@@ -24,10 +24,20 @@
 //   sum_u x[u + s(kd,kh) + kw - 1] gy[u] = sum_u x[u + s(kd,kh)] gy[u + 1 - kw],
 // and B block b = 2 - kw is the gy tile started b rows later: LBO = one row.
 //
+// Tap packing (C_in, C_out <= 16, the 32^3 levels): two 16-channel rows share
+// one 128-byte line, so the producers bake the kh shift into the x operand
+// and the kw shift into gy:
+//   x block 0 row w = [x[w + A] | x[w + A + Sw]], block 1 = [x[w + A + 2 Sw] | -]
+//   gy line j       = [gy[w0 + j - 1] | gy[w0 + j - 2]], N block 1 = 2 lines on
+// (A = (kd - 1) Sh - Sw). One M = 64, N = 64 MMA per K step then covers the
+// nine (kh, kw) taps of a kd plane (D rows 16 kh + ci, columns: block 0 =
+// [kw 2 | -], block 1 = [kw 0 | kw 1]) -- a third of the stacked MMA count.
+//
 // M is 64 or 128 (tcgen05 shapes): a channel block smaller than M is read
 // with LBO = 0 (one 32-channel block, repeated) or runs into a padded block;
 // those rows of D are never stored.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -49,6 +59,7 @@ struct WgTc {
   int G, ngroups;      // taps per CTA, tap groups
   int ntaps;           // 27 or 1
   int stack;           // 1: the three kw taps of a (kd, kh) row share one MMA (N = 3 x 32, see below)
+  int pack;            // 1: C_in, C_out <= 16 -- all nine taps of a kd plane in one 64 x 64 MMA (see below)
   int RSg;             // gy rows per stage (RS, or RS + 2 with the kw halo)
   int nchx, nchg;      // real 16-B chunks per row of the x block / of gy
   uint32_t Bx, Bg;     // bytes of one 32-channel block region: WR x 128 / RS x 128, 1024-aligned
@@ -276,6 +287,173 @@ __global__ void __launch_bounds__(kWtThreads) wgrad_tc_k(WgTc a) {
   if (warp == 0) tc::tmem_free(tmem, a.tmem_cols);
 }
 
+// Packed variant (a.pack): see the header. Same ring / barrier protocol as
+// wgrad_tc_k; the producers gather 16-channel half lines.
+__global__ void __launch_bounds__(kWtThreads) wgrad_tc_pack_k(WgTc a) {
+  D2IP_PDL_ENTRY();
+  extern __shared__ __align__(1024) uint8_t smem[];
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int b = blockIdx.z;
+  const int rg = blockIdx.x;
+  const int kd = blockIdx.y;  // one kd plane per CTA
+  const bool do_bias = kd == 0;
+  const int RS = a.RS, NSTG = a.NSTG;
+  const int NX = RS + 2 * a.Sw, NG = RS + 3;  // rowmap entries: x window, gy window
+  const d2ip_act x = a.x, gy = a.gy;
+  const float* xb = x.ptr + b * x.bstride;
+  const float* gb = gy.ptr + b * gy.bstride;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)NSTG * a.Sb);
+  uint64_t* empty = full + NSTG;
+  uint64_t* done = empty + NSTG;
+  uint8_t* tail = smem + (size_t)NSTG * a.Sb + (((2 * NSTG + 1) * 8 + 15) & ~15);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tail);
+  float4* bred = reinterpret_cast<float4*>(tail + 16);
+  int* rowmaps = reinterpret_cast<int*>(tail + 16 + kWtProd * 16);
+
+  if (warp == 0) tc::tmem_alloc(tslot, a.tmem_cols);
+  if (tid == 0) {
+    for (int i = 0; i < NSTG; ++i) {
+      tc::mbar_init(&full[i], kWtProd / 2);
+      tc::mbar_init(&empty[i], 1);
+    }
+    tc::mbar_init(done, 1);
+    tc::fence_mbar_init();
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tslot;
+  const int c_lo = rg * a.chunks_per_rg, c_hi = min(a.nchunk, c_lo + a.chunks_per_rg);
+  const int S = c_hi - c_lo;
+  const int Cin = x.c, Cout = gy.c;
+  float* pb = a.part + ((long long)b * a.nrg + rg) * ((long long)27 * Cin * Cout + Cout);
+
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint32_t sbase = tc::smem_u32(smem);
+      const uint64_t dXhi = tc::make_desc_mn32(sbase, a.lbox), dXlo = dXhi + (a.Sx >> 4);
+      const uint64_t dGhi = tc::make_desc_mn32(sbase + 2 * a.Sx, a.lbog), dGlo = dGhi + (a.Sg >> 4);
+      for (int s = 0; s < S; ++s) {
+        const int slot = s % NSTG;
+        tc::mbar_wait(&full[slot], (uint32_t)((s / NSTG) & 1));
+        tc::fence_after();
+        const uint64_t boff = (uint64_t)(slot * a.Sb) >> 4;
+        for (int j = 0; j < RS / 8; ++j) {
+          const uint64_t o = boff + (uint64_t)(8 * j) * 8;
+          const uint32_t first = (s | j) ? 1u : 0u;
+          tc::mma_tf32(tmem, dXlo + o, dGhi + o, a.idesc, first);
+          tc::mma_tf32(tmem, dXhi + o, dGlo + o, a.idesc, 1u);
+          tc::mma_tf32(tmem, dXhi + o, dGhi + o, a.idesc, 1u);
+        }
+        tc::commit(&empty[slot]);
+      }
+      if (S > 0) tc::commit(done);
+    }
+  } else {
+    const int ptid = tid - 32, pg = (warp - 1) >> 1, gtid = ((warp - 1) & 1) * 32 + lane;
+    const int xshift = (kd - 1) * a.Sh - a.Sw;
+    int* rm = rowmaps + pg * (NX + NG);
+    const int nchx = Cin / 4, nchg = Cout / 4;
+    float4 bacc = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int s = pg; s < S; s += 2) {
+      const int slot = s % NSTG;
+      if (s >= NSTG) tc::mbar_wait(&empty[slot], (uint32_t)((s / NSTG - 1) & 1));
+      const int u0 = a.u_first + (c_lo + s) * RS;
+      for (int i = gtid; i < NX + NG; i += 64)
+        rm[i] = i < NX ? wg_voxel(a, u0 + xshift + i) : wg_voxel(a, u0 - 2 + (i - NX));
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + pg) : "memory");
+      uint8_t* X = smem + (size_t)slot * a.Sb;
+      uint8_t* Gt = X + 2 * a.Sx;
+      // x: slot c = 4 (3 halves: block 0 lo / hi half, block 1 lo half) x chunk; kh = c / 4
+      for (int i = gtid; i < RS * 16; i += 64) {
+        const int r = i >> 4, c = i & 15, kh = c >> 2, cc = c & 3;
+        if (kh < 3 && cc < nchx) {
+          const int v = rm[r + kh * a.Sw];
+          const float* src = v >= 0 ? xb + (long long)v * x.cstride + 4 * cc : xb;
+          tc::cp_async16(X + mn32_off(r, (kh & 1) * 4 + cc + (kh >> 1) * 8, a.Bx), src, v >= 0 ? 16u : 0u);
+        }
+      }
+      // gy line j = [gy(u0 - 1 + j) | gy(u0 - 2 + j)]
+      for (int i = gtid; i < (RS + 2) * 8; i += 64) {
+        const int j = i >> 3, h = (i >> 2) & 1, cc = i & 3;
+        if (cc < nchg) {
+          const int v = rm[NX + j + 1 - h];
+          const float* src = v >= 0 ? gb + (long long)v * gy.cstride + 4 * cc : gb;
+          tc::cp_async16(Gt + mn32_off(j, h * 4 + cc, a.Bg), src, v >= 0 ? 16u : 0u);
+        }
+      }
+      tc::cp_async_commit();
+      tc::cp_async_wait<0>();
+      for (int i = gtid; i < RS * 16; i += 64) {
+        const int r = i >> 4, c = i & 15, kh = c >> 2, cc = c & 3;
+        if (kh < 3 && cc < nchx) {
+          const uint32_t o = mn32_off(r, (kh & 1) * 4 + cc + (kh >> 1) * 8, a.Bx);
+          const float4 v = *reinterpret_cast<const float4*>(X + o);
+          float4 l;
+          l.x = v.x - tf32_hi_w(v.x); l.y = v.y - tf32_hi_w(v.y); l.z = v.z - tf32_hi_w(v.z); l.w = v.w - tf32_hi_w(v.w);
+          *reinterpret_cast<float4*>(X + a.Sx + o) = l;
+        }
+      }
+      for (int i = gtid; i < (RS + 2) * 8; i += 64) {
+        const int j = i >> 3, h = (i >> 2) & 1, cc = i & 3;
+        if (cc < nchg) {
+          const uint32_t o = mn32_off(j, h * 4 + cc, a.Bg);
+          const float4 v = *reinterpret_cast<const float4*>(Gt + o);
+          float4 l;
+          l.x = v.x - tf32_hi_w(v.x); l.y = v.y - tf32_hi_w(v.y); l.z = v.z - tf32_hi_w(v.z); l.w = v.w - tf32_hi_w(v.w);
+          *reinterpret_cast<float4*>(Gt + a.Sg + o) = l;
+          if (do_bias && h == 0 && j >= 1 && j <= RS) {  // gy rows u0 .. u0 + RS - 1, once each
+            bacc.x += v.x; bacc.y += v.y; bacc.z += v.z; bacc.w += v.w;
+          }
+        }
+      }
+      tc::fence_proxy_async();
+      tc::mbar_arrive(&full[slot]);
+      asm volatile("bar.sync %0, 64;" ::"r"(1 + pg) : "memory");
+    }
+    if (do_bias) bred[ptid] = bacc;
+  }
+  __syncthreads();
+  if (warp != 0) {
+    const int ptid = tid - 32;
+    if (do_bias && ptid < Cout / 4) {  // fixed-order column sum: thread q held chunk q % 4 (h == 0 slots)
+      float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
+      for (int q = 0; q < kWtProd; ++q) {
+        if ((q & 7) != ptid) continue;  // gtid % 8 == h * 4 + cc with h == 0
+        const float4 v = bred[q];
+        sum.x += v.x; sum.y += v.y; sum.z += v.z; sum.w += v.w;
+      }
+      float* o = pb + (long long)27 * Cin * Cout + 4 * ptid;
+      o[0] = sum.x; o[1] = sum.y; o[2] = sum.z; o[3] = sum.w;
+    }
+    if (S > 0) {
+      tc::mbar_wait(done, 0);
+      tc::fence_after();
+    }
+    // D row m = 16 kh + ci in TMEM lane (m % 16) + 32 (m / 16): quadrant q = kh
+    const int q = warp & 3, ci = lane;
+    if (q < 3) {
+      const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
+      for (int c0 = 0; c0 < 64; c0 += 8) {
+        const int blk = c0 >> 4 >> 1, h = (c0 >> 4) & 1, co0 = c0 & 15;
+        if ((blk == 0 && h == 1) || co0 >= Cout) continue;
+        const int kw = blk == 0 ? 2 : h;
+        float v[8];
+        tc::tmem_ld8(trow + (uint32_t)c0, v);
+        if (ci < Cin && lane < 16) {
+          float* dst = pb + ((long long)(kd * 9 + q * 3 + kw) * Cin + ci) * Cout + co0;
+#pragma unroll
+          for (int jj = 0; jj < 8; ++jj)
+            if (co0 + jj < Cout) dst[jj] = S > 0 ? v[jj] : 0.f;
+        }
+      }
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_free(tmem, a.tmem_cols);
+}
+
 // Sum over row groups (fixed order) and scatter into OIDHW weight + bias grads.
 // Thread e walks the partial layout [t][ci][co] (co fastest: coalesced reads).
 __global__ void __launch_bounds__(256) wgrad_tc_reduce_k(const float* __restrict__ part, int nrg, int ntaps,
@@ -314,6 +492,14 @@ static int pow2_at_least(int v) {
 
 static uint32_t align1k(size_t v) { return (uint32_t)((v + 1023) & ~(size_t)1023); }
 
+static bool wt_nopack() {
+  static const int v = [] {
+    const char* e = getenv("D2IP_WGRAD_NOPACK");
+    return e && *e == '1' ? 1 : 0;
+  }();
+  return v;
+}
+
 static bool wt_plan(int D, int H, int W, int Cin, int Cout, int ks, int batch, WgTc& a) {
   if (Cin % 4 || Cout % 4 || Cin < 4 || Cout > 128 || (ks != 1 && ks != 3)) return false;
   a.ntaps = ks == 3 ? 27 : 1;
@@ -326,6 +512,41 @@ static bool wt_plan(int D, int H, int W, int Cin, int Cout, int ks, int batch, W
   while (Cin % a.ncib || (Cin / a.ncib) % 4) ++a.ncib;
   a.cib = Cin / a.ncib;
   a.M = a.cib <= 64 ? 64 : 128;
+  a.pack = (ks == 3 && Cin <= 16 && Cout <= 16 && !wt_nopack()) ? 1 : 0;
+  if (a.pack) {
+    a.stack = 0;
+    a.M = a.N = 64;
+    a.G = 9;
+    a.ngroups = 3;
+    a.tmem_cols = 64;
+    a.nchx = Cin / 4;
+    a.nchg = Cout / 4;
+    a.RS = 0;
+    for (int rs : {128, 64, 32}) {
+      const uint32_t bx = align1k((size_t)rs * 128), bg = align1k((size_t)(rs + 2) * 128);
+      const uint32_t sx = 2 * bx, sg = bg, sb = 2 * (sx + sg);
+      const int nx = rs + 2 * a.Sw, ng = rs + 3;
+      auto total = [&](int nst) {
+        return (size_t)nst * sb + (((2 * nst + 1) * 8 + 15) & ~15) + 16 + kWtProd * 16 + 8 * (size_t)(nx + ng) + 64;
+      };
+      if (total(2) > (size_t)220 * 1024) continue;
+      a.NSTG = 2;
+      while (a.NSTG < 4 && total(a.NSTG + 1) <= (size_t)220 * 1024) ++a.NSTG;
+      a.RS = rs;
+      a.WR = nx;
+      a.RSg = ng;
+      a.Bx = bx;
+      a.Bg = bg;
+      a.Sx = sx;
+      a.Sg = sg;
+      a.Sb = sb;
+      a.pad = 0;
+      a.lbox = bx;
+      a.lbog = 256;  // N block 1 = two gy lines on
+      break;
+    }
+    if (!a.RS) return false;
+  } else {
   a.stack = (ks == 3 && Cout <= 32) ? 1 : 0;
   if (a.stack) {
     a.N = 96;  // 3 kw taps x one 32-channel block
@@ -376,6 +597,7 @@ static bool wt_plan(int D, int H, int W, int Cin, int Cout, int ks, int batch, W
     }
   }
   if (!a.RS) return false;
+  }
   a.nchunk = cdiv(a.u_last - a.u_first + 1, a.RS);
   // row groups: ~1 CTA per SM overall, >= 2 chunks each when there are enough
   const long long jobs = (long long)a.ngroups * a.ncib * batch;
@@ -444,6 +666,14 @@ int wgrad_tc(d2ip_act x, d2ip_act gy, int ks, float* gw, long long gwbs, void* w
   a.part = reinterpret_cast<float*>(ws);
   const size_t smem = wt_smem(a);
   const dim3 grid(a.nrg, a.ngroups * a.ncib, batch);
+  if (a.pack) {
+    static bool attr = false;
+    if (!attr) {
+      D2IP_CUDA(cudaFuncSetAttribute(wgrad_tc_pack_k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+      attr = true;
+    }
+    D2IP_CUDA(launch_pdl(wgrad_tc_pack_k, grid, kWtThreads, smem, st, a));
+  } else {
   const int nx = pow2_at_least(a.nchx), ng = pow2_at_least(a.nchg);
   switch (nx) {
     case 1: D2IP_RET(wt_launch_g<1>(a, ng, grid, smem, st)); break;
@@ -453,6 +683,7 @@ int wgrad_tc(d2ip_act x, d2ip_act gy, int ks, float* gw, long long gwbs, void* w
     case 16: D2IP_RET(wt_launch_g<16>(a, ng, grid, smem, st)); break;
     case 32: D2IP_RET(wt_launch_g<32>(a, ng, grid, smem, st)); break;
     default: D2IP_CHECK_ARG(false, "wgrad_tc: C_in chunks %d unsupported", nx);
+  }
   }
   D2IP_LAUNCH_CHECK();
   const long long n = (long long)a.ntaps * x.c * gy.c + gy.c;

@@ -64,12 +64,24 @@ CONV_CASES = [
     (48, 16, 3, 1, (32, 32, 32)),
     (32, 32, 3, 1, (16, 16, 16)),
     (8, 16, 3, 1, (32, 32, 32)),
+    (16, 16, 3, 1, (32, 32, 32)),
+    (12, 8, 3, 1, (6, 10, 12)),
+    # stride 2 on the tensor cores (parity decomposition), odd extents included
+    (16, 32, 3, 2, (9, 10, 7)),
+    (32, 64, 3, 2, (32, 32, 32)),
+    (32, 32, 3, 2, (65, 34, 17)),
+    (4, 8, 3, 2, (6, 6, 6)),
     (128, 128, 3, 1, (8, 8, 4)),
     (192, 64, 3, 1, (16, 16, 8)),
     # large grids (cfg2 / cfg4 scale tiles)
     (16, 32, 3, 1, (64, 64, 32)),
     (32, 16, 3, 1, (48, 48, 32)),
 ]
+
+
+def s2_big(cin, cout, sp):
+    """Stride-2 layers run on the tensor cores from 4M output-voxel x channel-pair products (conv_tc_layer)."""
+    return int(np.prod([(n + 1) // 2 for n in sp])) * cin * cout >= 4 * 1024 * 1024
 
 
 @pytest.mark.parametrize("prec", ["fp32", "tf32"])
@@ -98,8 +110,8 @@ def test_conv3d_fwd(cin, cout, ks, stride, sp, prec):
                            P, ks, stride, ya, 0, N.PREC[prec], C.c_void_p(ws.data_ptr()), wsn, B, stream())
     N.check(rc, "conv3d_fwd")
     torch.cuda.synchronize()
-    if prec == "tf32" and ks == 3 and stride == 1 and cin % 8 == 0:
-        assert L.d2ip_last_variant() == b"tcgen05_tf32x3"
+    if prec == "tf32" and ks == 3 and ((stride == 1 and cin % 8 == 0) or (stride == 2 and cin % 4 == 0 and s2_big(cin, cout, sp))):
+        assert L.d2ip_last_variant().startswith(b"tcgen05_tf32x3")
     assert rel(from_ndhwc(out), ref) < TOL[prec]
     # accumulate mode adds on top
     N.check(L.d2ip_conv3d_fwd(xa, C.c_void_p(params.data_ptr()), None, P, ks, stride, ya, 1, N.PREC[prec],
@@ -137,6 +149,8 @@ def test_conv3d_dgrad_wgrad(cin, cout, ks, stride, sp, prec, wgrad_variant):
     wsd = torch.empty(max(wsn, 16), dtype=torch.uint8, device="cuda")
     N.check(N.lib().d2ip_conv3d_dgrad(act_of(gyd), C.c_void_p(params.data_ptr()), P, ks, stride, act_of(gx), 0,
                                       N.PREC[prec], C.c_void_p(wsd.data_ptr()), wsn, B, stream()), "dgrad")
+    if prec == "tf32" and ks == 3 and cout % 8 == 0 and cin % 8 == 0 and (stride == 1 or s2_big(cin, cout, sp)):
+        assert N.lib().d2ip_last_variant().startswith(b"tcgen05_tf32x3")
     xd = to_ndhwc(x.detach())
     gw = torch.zeros(B, P, device="cuda")
     ws_n = N.lib().d2ip_conv3d_wgrad_ws_bytes(act_of(xd), act_of(gyd), ks, B)
