@@ -37,11 +37,23 @@
 // scattered by the epilogue to its parity voxel 2o + p of gx. The pack kernel
 // lays out the parity weights (zeros where a parity has no tap).
 //
+// bf16 operands (precision D2IP_PREC_BF16, mode bit kTcBf16): one kind::f16
+// MMA per 16-channel K step instead of three kind::tf32 MMAs per 8 channels.
+// The producers load the fp32 activation window through registers and store
+// it as bf16 (round to nearest), the pack kernel writes bf16 weights; the
+// accumulator stays FP32 in TMEM. Measured on sm_100a (tools/umma_chains.cu):
+// an M = 128 MMA reads its A tile (128 rows x 32 B) and B tile (N x 32 B) from
+// shared memory at ~128 B/cycle, so it costs max(N / 2, (4096 + 32 N) / 128)
+// cycles -- 40 at N = 32, 48 at N = 64 -- whatever the operand type: at these
+// channel counts bf16 moves 6x more products per MMA cycle than 3xTF32.
+//
 // Pipeline: 2 smem stages filled with cp.async (16 B, zero-fill outside the
 // grid) by all 128 threads; thread 0 issues the MMAs of a stage and commits
 // them to that stage's mbarrier, which gates the refill of the buffer.
 #include <algorithm>
 #include <cstdlib>
+
+#include <cuda_bf16.h>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -75,30 +87,40 @@ struct TcConv {
   int mode;     // 0: stride 1; 1: stride-2 forward (parity-gathered input); 2: stride-2 dgrad (parity-scattered output)
   int t0, nt;   // taps per axis used: t0 .. t0 + nt - 1 (offsets t - 1)
   int gd, gh, gw;  // row-space grid (stride 1: x; mode 1: y; mode 2: gy)
+  int bf;          // bf16 operands (kind::f16)
+  int vec;         // y rows (and bias) 16-byte aligned: float4 epilogue stores
 };
 
-// Per stage: A hi + A lo windows, B hi + B lo tiles (nt^2 taps).
-static size_t stage_bytes(int cb, int np, int wrp, int nt = 3) {
+// Per stage: A hi + A lo windows, B hi + B lo tiles (nt^2 taps); bf16: one
+// A window and one B tile of 2-byte elements.
+static size_t stage_bytes(int cb, int np, int wrp, int nt = 3, bool bf = false) {
+  if (bf) return (size_t)cb * wrp * 2 + (size_t)nt * nt * cb * np * 2;
   return 2 * ((size_t)cb * wrp * 4 + (size_t)nt * nt * cb * np * 4);
 }
 
 static size_t tc_smem_bytes(const TcConv& a) {
-  return 2 * stage_bytes(a.CB, a.Ns, a.WRp, a.nt) + 3 * a.WR * sizeof(int) + 8 + 5 * 8 + 16;
+  return 2 * stage_bytes(a.CB, a.Ns, a.WRp, a.nt, a.bf) + 3 * a.WR * sizeof(int) + 8 + 5 * 8 + 16;
+}
+
+__device__ __forceinline__ uint32_t bf2(float a, float b) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
 }
 
 __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
 
-// NKC = CB / 4: 16-byte channel chunks per stage (compile-time, so the fill
-// loops need no integer division).
+// NKC: 16-byte channel chunks per row and stage (CB / 4 for tf32, CB / 8 for
+// bf16; compile-time, so the fill loops need no integer division).
 // PG: producer groups (1: all eight producer warps fill each stage; 2: two
 // groups of four fill alternate stages, two stages in flight).
 // MODE: 0 stride 1, 1 / 2 stride-2 forward / data gradient (compile-time, so
 // the stride-1 issue loop keeps its constant tap arithmetic).
-template <int NKC, int T, int PG, int MODE>
+template <int NKC, int T, int PG, int MODE, bool BF = false>
 __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
   D2IP_PDL_ENTRY();
   extern __shared__ __align__(1024) uint8_t smem[];
-  constexpr int CB = NKC * 4;
+  constexpr int CB = NKC * (BF ? 8 : 4);
+  constexpr int NH = BF ? 1 : 2;  // operand halves per stage (3xTF32: hi, lo)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int b = blockIdx.z;
   const int ks = blockIdx.y % a.kspl;
@@ -109,8 +131,8 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
   // (kh, kw) of the q-th live tap as a 3x3 index: nt = 3 -> q; nt = 2 -> the 2x2 block at (t0, t0)
   auto tap9 = [&](int q) { return nt == 3 ? q : (t0 + (q >> 1)) * 3 + (t0 + (q & 1)); };
   const uint32_t Ab = (uint32_t)NKC * WRp * 16, Bb = (uint32_t)ntap * NKC * Ns * 16;
-  const uint32_t Sb = 2 * (Ab + Bb);
-  // layout: 2 stages of [A hi][A lo][B hi][B lo], row map, barriers full[2] empty[2] done, TMEM slot
+  const uint32_t Sb = NH * (Ab + Bb);
+  // layout: 2 stages of [A hi][A lo][B hi][B lo] (bf16: [A][B]), row map, barriers full[2] empty[2] done, TMEM slot
   int* rowmap = reinterpret_cast<int*>(smem + 2 * Sb);
   uint64_t* full = reinterpret_cast<uint64_t*>(rowmap + 3 * WR + ((3 * WR) & 1));
   uint64_t* empty = full + 2;
@@ -158,7 +180,7 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
   const int s_lo = (int)((long long)ks * S_all / a.kspl), s_hi = (int)((long long)(ks + 1) * S_all / a.kspl);
   const int S = s_hi - s_lo;  // this CTA's stages: s_lo + [0, S)
   const int nA = WR * NKC;
-  const int kc_all = a.Kc >> 2;
+  const int kc_all = BF ? a.Kc >> 3 : a.Kc >> 2;  // 16-byte chunks per K
 
   if (warp == 0) {
     // ---- MMA issue (one elected thread); stage s lives in slot s & 1
@@ -167,7 +189,7 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
       // start-address field (smem addresses < 256 KB never carry out of it)
       const uint32_t sbase = tc::smem_u32(smem);
       const uint64_t dAhi = tc::make_desc(sbase, WRp * 16, 128), dAlo = dAhi + (Ab >> 4);
-      const uint64_t dBhi = tc::make_desc(sbase + 2 * Ab, Ns * 16, 128), dBlo = dBhi + (Bb >> 4);
+      const uint64_t dBhi = tc::make_desc(sbase + NH * Ab, Ns * 16, 128), dBlo = dBhi + (Bb >> 4);
       for (int s = 0; s < S; ++s) {
         const int slot = s & 1;
         tc::mbar_wait(&full[slot], (uint32_t)((s >> 1) & 1));
@@ -184,9 +206,13 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
             for (int tt = 0; tt < T; ++tt) {  // sub-tile tt: rows + 128 tt, accumulator columns + tt Ns
               const uint64_t ao = boff + (uint64_t)(2 * j * WRp + rowoff + tt * kTcRows);
               const uint32_t d = tmem + (uint32_t)(tt * Ns);
-              tc::mma_tf32(d, dAlo + ao, dBhi + bo, a.idesc, first);
-              tc::mma_tf32(d, dAhi + ao, dBlo + bo, a.idesc, 1u);
-              tc::mma_tf32(d, dAhi + ao, dBhi + bo, a.idesc, 1u);
+              if (BF) {
+                tc::mma_f16(d, dAhi + ao, dBhi + bo, a.idesc, first);
+              } else {
+                tc::mma_tf32(d, dAlo + ao, dBhi + bo, a.idesc, first);
+                tc::mma_tf32(d, dAhi + ao, dBlo + bo, a.idesc, 1u);
+                tc::mma_tf32(d, dAhi + ao, dBhi + bo, a.idesc, 1u);
+              }
             }
           }
         }
@@ -207,7 +233,44 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
       const int kd = t0 + kdi;
       const int* rm = rowmap + kd * WR;
       uint8_t* A = smem + slot * Sb;
-      if (MODE == 1) {
+      if (BF) {
+        // fp32 window -> registers -> bf16 rows. A work item is one float4 (4
+        // channels; consecutive threads read consecutive 16 B of a voxel row) that
+        // lands as 8 bytes, half of a 16-byte chunk; eight loads in flight per thread.
+        constexpr int PPR = 2 * NKC;  // float4 pieces per window row
+        const int nP = WR * PPR;
+        const long long plane = (long long)x.h * x.w;
+        for (int i0 = gtid; i0 < nP; i0 += 8 * GT) {
+          float4 v[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int i = i0 + q * GT;
+            v[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (i >= nP) continue;
+            const int r = i / PPR, pc = i % PPR;
+            const int off = rm[r];
+            if (MODE == 1) {
+              const int c = cb * CB + 4 * pc, p = c / x.c, ci = c - p * x.c;
+              const int pd = p >> 2, ph = (p >> 1) & 1, pw = p & 1;
+              if (off >= 0 && (!pd || (off & 4)) && (!ph || (off & 2)) && (!pw || (off & 1)))
+                v[q] = *reinterpret_cast<const float4*>(
+                    xb + ((off >> 3) + pd * plane + ph * x.w + pw) * (long long)x.cstride + ci);
+            } else if (off >= 0) {
+              v[q] = *reinterpret_cast<const float4*>(xb + (long long)off * x.cstride + cb * CB + 4 * pc);
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int i = i0 + q * GT;
+            if (i >= nP) continue;
+            const int r = i / PPR, pc = i % PPR;
+            uint2 o;
+            o.x = bf2(v[q].x, v[q].y);
+            o.y = bf2(v[q].z, v[q].w);
+            *reinterpret_cast<uint2*>(A + ((size_t)(pc >> 1) * WRp + r) * 16 + (pc & 1) * 8) = o;
+          }
+        }
+      } else if (MODE == 1) {
         // parity gather: virtual channel c = p * C_x + ci reads input voxel 2o + p
         const long long plane = (long long)x.h * x.w;
         for (int i = gtid; i < nA; i += GT) {
@@ -230,7 +293,8 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
         }
       }
       // B: nt^2 taps x NKC chunks, each a contiguous run of Ns 16-byte rows; one warp per run
-      uint8_t* Bt = A + 2 * Ab;
+      // (16-byte rows: 4 floats, or 8 bf16 = 4 float slots of the pack buffer)
+      uint8_t* Bt = A + NH * Ab;
       const float* wk = wpb + ((long long)(kd * 9) * kc_all + cb * NKC) * a.Np * 4 + (long long)n0 * 4;
       const int gwarp = gtid >> 5;
       for (int q = gwarp; q < ntap * NKC; q += GT / 32) {
@@ -240,13 +304,14 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
         uint8_t* dst = Bt + (size_t)q * Ns * 16;
         for (int n = lane; n < Ns; n += 32) {
           tc::cp_async16(dst + n * 16, src + n * 4, 16u);
-          tc::cp_async16(dst + Bb + n * 16, src + a.wlo + n * 4, 16u);
+          if (!BF) tc::cp_async16(dst + Bb + n * 16, src + a.wlo + n * 4, 16u);
         }
       }
       tc::cp_async_commit();
       tc::cp_async_wait<0>();
       // lo half of the landed activation window; the raw fp32 window is the hi
       // operand (the tensor core truncates fp32 to TF32: tools/tf32_round_probe.cu)
+      if (!BF)
       for (int i = gtid; i < nA; i += GT) {
         const int r = i / NKC, kc = i % NKC;
         const float4 v = *reinterpret_cast<const float4*>(A + ((size_t)kc * WRp + r) * 16);
@@ -325,7 +390,24 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
       for (int c0 = cbeg; c0 < cend; c0 += 8) {
         float vals[8];
         tc::tmem_ld8(tcol + c0, vals);
-        if (yp) {
+        if (yp && a.vec && n0 + c0 + 8 <= a.N) {
+          // 8 consecutive channels of one voxel: two 16-byte stores (one 32-byte sector)
+          float4* y4 = reinterpret_cast<float4*>(yp + n0 + c0);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            float4 o = make_float4(S > 0 ? vals[4 * h] : 0.f, S > 0 ? vals[4 * h + 1] : 0.f,
+                                   S > 0 ? vals[4 * h + 2] : 0.f, S > 0 ? vals[4 * h + 3] : 0.f);
+            if (bias) {
+              const float* bb = bias + n0 + c0 + 4 * h;
+              o.x += __ldg(bb); o.y += __ldg(bb + 1); o.z += __ldg(bb + 2); o.w += __ldg(bb + 3);
+            }
+            if (a.accumulate) {
+              const float4 yo = y4[h];
+              o.x += yo.x; o.y += yo.y; o.z += yo.z; o.w += yo.w;
+            }
+            y4[h] = o;
+          }
+        } else if (yp) {
 #pragma unroll
           for (int j = 0; j < 8; ++j) {
             const int n = n0 + c0 + j;
@@ -370,8 +452,9 @@ __device__ __forceinline__ int s2_axis(int ta, int pa, int dgrad) {
 }
 
 // One packed weight: code 0 forward, 1 stride-1 dgrad, 2 stride-2 forward
-// (k = p C_in + ci), 3 stride-2 dgrad (n = p C_in + ci).
+// (k = p C_in + ci), 3 stride-2 dgrad (n = p C_in + ci); + kTcBf16: bf16 layout.
 __device__ __forceinline__ float pack_val(const float* wb, int K, int N, int code, int t, int k, int n) {
+  code &= 3;
   if (code == 0) return wb[((long long)n * K + k) * 27 + t];
   if (code == 1) return wb[((long long)k * N + n) * 27 + (26 - t)];
   const int cin = code == 2 ? K >> 3 : N >> 3;
@@ -388,12 +471,29 @@ __device__ __forceinline__ float pack_val(const float* wb, int K, int N, int cod
 //   forward: K = C_in,  N = C_out:  P[t][k][n] = W[n][k][t]
 //   dgrad  : K = C_out, N = C_in :  P[t][k][n] = W[k][n][26 - t]
 //   stride 2: the parity layouts of pack_val (codes 2, 3)
+// bf16 (code & kTcBf16): [b][tap][K/8][Np][8] bf16, element i of `half`.
+__device__ __forceinline__ void pack_bf16(const float* wb, int K, int N, int Np, int code, long long i,
+                                          __nv_bfloat16* out) {
+  const int j = (int)(i & 7);
+  const long long q = i >> 3;
+  const int n = (int)(q % Np);
+  const long long q2 = q / Np;
+  const int kc = (int)(q2 % (K / 8));
+  const int t = (int)(q2 / (K / 8));
+  const float val = n < N ? pack_val(wb, K, N, code, t, 8 * kc + j, n) : 0.f;
+  out[i] = __float2bfloat16_rn(val);
+}
+
 __global__ void conv_tc_pack_k(const float* __restrict__ w, long long wbs, int K, int N, int Np, int dgrad,
                                float* __restrict__ out, long long half, long long obs) {
   D2IP_PDL_ENTRY();
   const int b = blockIdx.y;
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= half) return;
+  if (dgrad & kTcBf16) {
+    pack_bf16(w + b * wbs, K, N, Np, dgrad, i, reinterpret_cast<__nv_bfloat16*>(out + b * obs));
+    return;
+  }
   const int j = (int)(i & 3);
   const long long q = i >> 2;
   const int n = (int)(q % Np);
@@ -417,6 +517,11 @@ __global__ void conv_tc_pack_multi_k(PackJobs j) {
   const long long i = (long long)(blockIdx.x - j.block0[q]) * blockDim.x + threadIdx.x;
   if (i >= half) return;
   const int K = j.K[q], N = j.N[q], Np = np_of(N);
+  if (j.dgrad[q] & kTcBf16) {
+    pack_bf16(j.w[q] + b * j.wbs, K, N, Np, j.dgrad[q], i,
+              reinterpret_cast<__nv_bfloat16*>(j.out[q] + b * 2 * half));
+    return;
+  }
   const int jj = (int)(i & 3);
   const long long qq = i >> 2;
   const int n = (int)(qq % Np);
@@ -450,7 +555,7 @@ void pack_jobs_add(PackJobs& j, const float* w, int K, int N, int dgrad, float* 
 }
 
 bool conv_tc_supported(int cin, int cout, int ks, int stride, int precision) {
-  if (precision != D2IP_PREC_TF32 || ks != 3 || stride != 1) return false;
+  if ((precision != D2IP_PREC_TF32 && precision != D2IP_PREC_BF16) || ks != 3 || stride != 1) return false;
   if (cin % 8 || cin < 8 || cout < 1 || np_of(cout) > 1024) return false;
   return true;
 }
@@ -463,6 +568,11 @@ bool conv_tc_layer(int cin, int cout, int ks, int stride, int dgrad, int precisi
     r.mode = 0;
     r.pack = dgrad;
     if (!conv_tc_supported(r.K, r.N, ks, 1, precision)) return false;
+    // bf16: 16-channel K steps; K % 16 != 0 (e.g. the 8-channel stem) keeps 3xTF32
+    if (precision == D2IP_PREC_BF16 && r.K % 16 == 0) {
+      r.mode |= kTcBf16;
+      r.pack |= kTcBf16;
+    }
   } else {
     // Below ~4M output-voxel x channel-pair products the direct CUDA-core kernel
     // is faster (tools/conv_bench.py: 16->32 at 16^3 out 24 vs 29 us; 32->64 at
@@ -472,7 +582,7 @@ bool conv_tc_layer(int cin, int cout, int ks, int stride, int dgrad, int precisi
       const char* v = getenv("D2IP_TC_S2");
       return v ? atoi(v) : 1;
     }();
-    if (!s2 || precision != D2IP_PREC_TF32 || ks != 3 || stride != 2) return false;
+    if (!s2 || (precision != D2IP_PREC_TF32 && precision != D2IP_PREC_BF16) || ks != 3 || stride != 2) return false;
     if (s2 == 1 && vout >= 0 && vout * cin * cout < 4LL * 1024 * 1024) return false;
     if (!dgrad) {  // K = 8 C_in: a 16-byte chunk must not straddle two parities
       if (cin % 4 || cout < 1 || np_of(cout) > 1024) return false;
@@ -480,6 +590,11 @@ bool conv_tc_layer(int cin, int cout, int ks, int stride, int dgrad, int precisi
     } else {       // 8 epilogue columns share one parity
       if (cout % 8 || cin % 8 || np_of(8 * cin) > 1024) return false;
       r = TcDims{cout, 8 * cin, 2, 3};
+    }
+    // bf16: 8-channel chunks must not straddle two parities (mode 1: C_in % 8)
+    if (precision == D2IP_PREC_BF16 && r.K % 16 == 0 && (dgrad || cin % 8 == 0)) {
+      r.mode |= kTcBf16;
+      r.pack |= kTcBf16;
     }
   }
   if (d) *d = r;
@@ -501,7 +616,8 @@ int conv_tc_pack(const float* w, long long wbs, int K, int N, int dgrad, float* 
 // small latency model -- waves x (serial stages per CTA + fixed prologue /
 // epilogue cost) -- because at these sizes a CTA's chain of dependent stages,
 // not the tensor pipe, sets the time.
-static bool tc_plan(int D, int H, int W, int K, int N, int batch, TcConv& a, int* tiles, int nt = 3) {
+static bool tc_plan(int D, int H, int W, int K, int N, int batch, TcConv& a, int* tiles, int nt = 3,
+                    bool bf = false) {
   a.N = N;
   a.Np = np_of(N);
   a.Kc = K;
@@ -525,9 +641,9 @@ static bool tc_plan(int D, int H, int W, int K, int N, int batch, TcConv& a, int
     for (int ns = std::min(a.Np, 256); ns >= 16; ns -= 16) {
       if (a.Np % ns) continue;
       if (T * ns > 512) continue;  // TMEM columns
-      for (int cb = 8; cb <= K && cb <= 64; cb *= 2) {
+      for (int cb = bf ? 16 : 8; cb <= K && cb <= (bf ? 128 : 64); cb *= 2) {
         if (K % cb) continue;
-        const size_t sm = 2 * stage_bytes(cb, ns, wrp, nt) + 3 * wr * sizeof(int) + 64;
+        const size_t sm = 2 * stage_bytes(cb, ns, wrp, nt, bf) + 3 * wr * sizeof(int) + 64;
         if (sm > (size_t)210 * 1024) continue;
         const int per_sm = sm <= (size_t)110 * 1024 ? 2 : 1;
         const long long ctas0 = (long long)tl * (a.Np / ns) * batch;
@@ -539,7 +655,11 @@ static bool tc_plan(int D, int H, int W, int K, int N, int batch, TcConv& a, int
         if (!large) {
           cost = (double)waves * ((S + kspl - 1) / kspl + 2.0) + (kspl > 1 ? 1.0 : 0.0);
         } else {
-          const double mma_us = 3.0 * nt * nt / 8.0 * cb * T * 57.0 / 1900.0 * (per_sm == 2 ? 1.4 : 1.0);
+          // bf16: one MMA per 16 channels at max(N/2, (4096 + 32 N)/128) + issue cycles
+          const double mma_us =
+              bf ? nt * nt * (cb / 16.0) * T * (std::max(ns / 2.0, (4096.0 + 32.0 * ns) / 128.0) + 6.0) / 1900.0 *
+                       (per_sm == 2 ? 1.4 : 1.0)
+                 : 3.0 * nt * nt / 8.0 * cb * T * 57.0 / 1900.0 * (per_sm == 2 ? 1.4 : 1.0);
           const double stage_us = std::max(1.5, mma_us);
           cost = (double)waves * ((S + kspl - 1) / kspl * stage_us + 2.0 + 0.5 * T) + (kspl > 1 ? 3.0 : 0.0);
         }
@@ -558,19 +678,64 @@ static bool tc_plan(int D, int H, int W, int K, int N, int batch, TcConv& a, int
   }
   if (a.CB < 8) return false;
   a.n_cb = K / a.CB;
+  a.bf = bf;
   return true;
 }
 
 size_t conv_tc_ws_bytes(int D, int H, int W, int K, int N, int batch, int mode) {
   TcConv a{};
   int tiles;
-  if (!tc_plan(D, H, W, K, N, batch, a, &tiles, mode ? 2 : 3) || a.kspl <= 1) return 0;
+  if (!tc_plan(D, H, W, K, N, batch, a, &tiles, (mode & 3) ? 2 : 3, (mode & kTcBf16) != 0) || a.kspl <= 1)
+    return 0;
   // mode 2 partials are [V_gx][C_gx]: V_gx C_gx <= 8 V N / 8 (gx dims <= 2 x the row grid)
   return (size_t)batch * a.kspl * a.vout * N * sizeof(float);
 }
 
+// Launch one instantiation (the >48 KB shared-memory opt-in is set on first use).
+template <int NKC, int T, int PG, int MODE, bool BF>
+static int tc_launch(const TcConv& a, dim3 grid, size_t smem, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    D2IP_CUDA(cudaFuncSetAttribute(conv_tc_k<NKC, T, PG, MODE, BF>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   227 * 1024));
+    attr = true;
+  }
+  D2IP_CUDA(launch_pdl((conv_tc_k<NKC, T, PG, MODE, BF>), grid, kTcThreads, smem, st, a));
+  return D2IP_OK;
+}
+
+template <int NKC, bool BF>
+static int tc_dispatch(const TcConv& a, dim3 grid, size_t smem, cudaStream_t st, int mode, bool pg2) {
+  if (mode == 1) return tc_launch<NKC, 1, 1, 1, BF>(a, grid, smem, st);
+  if (mode == 2) return tc_launch<NKC, 1, 1, 2, BF>(a, grid, smem, st);
+  if (!BF && pg2) {
+    if (a.T == 4) return tc_launch<NKC, 4, 2, 0, BF>(a, grid, smem, st);
+    if (a.T == 2) return tc_launch<NKC, 2, 2, 0, BF>(a, grid, smem, st);
+    return tc_launch<NKC, 1, 2, 0, BF>(a, grid, smem, st);
+  }
+  if (a.T == 4) return tc_launch<NKC, 4, 1, 0, BF>(a, grid, smem, st);
+  if (a.T == 2) return tc_launch<NKC, 2, 1, 0, BF>(a, grid, smem, st);
+  return tc_launch<NKC, 1, 1, 0, BF>(a, grid, smem, st);
+}
+
+// NKC = 16-byte chunks per row: CB / 4 (tf32, CB 8..64) or CB / 8 (bf16, CB 16..128)
+template <bool BF>
+static int tc_dispatch_nkc(const TcConv& a, dim3 grid, size_t smem, cudaStream_t st, int mode, bool pg2) {
+  switch (a.CB / (BF ? 8 : 4)) {
+    case 2: return tc_dispatch<2, BF>(a, grid, smem, st, mode, pg2);
+    case 4: return tc_dispatch<4, BF>(a, grid, smem, st, mode, pg2);
+    case 8: return tc_dispatch<8, BF>(a, grid, smem, st, mode, pg2);
+    case 16: return tc_dispatch<16, BF>(a, grid, smem, st, mode, pg2);
+    default: D2IP_CHECK_ARG(false, "conv_tc: unsupported channel block %d", a.CB);
+  }
+  return D2IP_OK;
+}
+
 int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, long long bbs, d2ip_act y,
                 int accumulate, float* ws, size_t ws_bytes, int batch, cudaStream_t st, int* deferred, int mode) {
+  const bool bf = (mode & kTcBf16) != 0;
+  mode &= 3;
+  D2IP_CHECK_ARG(!bf || K % 16 == 0, "conv_tc: bf16 needs K %% 16 == 0 (K=%d)", K);
   D2IP_CHECK_ARG((mode == 1 ? 8 * x.c : x.c) == K && (mode == 2 ? 8 * y.c : y.c) == N, "conv_tc: channel mismatch");
   D2IP_CHECK_ARG(x.cstride % 4 == 0 && ((uintptr_t)x.ptr & 15) == 0, "conv_tc: input view must be 16B aligned");
   D2IP_CHECK_ARG(mode != 2 || (y.cstride % 4 == 0 && ((uintptr_t)y.ptr & 15) == 0 && y.c % 8 == 0),
@@ -580,7 +745,7 @@ int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, lo
   if (mode == 2) D2IP_CHECK_ARG(g.d == (y.d + 1) / 2 && g.h == (y.h + 1) / 2 && g.w == (y.w + 1) / 2, "conv_tc: stride-2 shape");
   TcConv a{};
   int tiles = 0;
-  D2IP_CHECK_ARG(tc_plan(g.d, g.h, g.w, K, N, batch, a, &tiles, mode ? 2 : 3),
+  D2IP_CHECK_ARG(tc_plan(g.d, g.h, g.w, K, N, batch, a, &tiles, mode ? 2 : 3, bf),
                  "conv_tc: no channel blocking fits shared memory (K=%d N=%d W=%d)", K, N, g.w);
   a.mode = mode;
   a.t0 = mode == 2 ? 1 : 0;
@@ -600,24 +765,12 @@ int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, lo
   a.bbs = bbs;
   a.y = y;
   a.accumulate = accumulate;
+  a.vec = y.cstride % 4 == 0 && ((uintptr_t)y.ptr & 15) == 0;
   int cols = 32;
   while (cols < a.T * a.Ns) cols *= 2;
   a.tmem_cols = cols;
-  a.idesc = tc::make_idesc(2, kTcRows, a.Ns);
+  a.idesc = tc::make_idesc(bf ? 1 : 2, kTcRows, a.Ns);
   const size_t smem = tc_smem_bytes(a);
-  static bool attr_set = false;
-  if (!attr_set) {
-    for (auto k : {conv_tc_k<2, 1, 1, 0>, conv_tc_k<4, 1, 1, 0>, conv_tc_k<8, 1, 1, 0>, conv_tc_k<16, 1, 1, 0>,
-                   conv_tc_k<2, 1, 2, 0>, conv_tc_k<4, 1, 2, 0>, conv_tc_k<8, 1, 2, 0>, conv_tc_k<16, 1, 2, 0>,
-                   conv_tc_k<2, 2, 1, 0>, conv_tc_k<4, 2, 1, 0>, conv_tc_k<8, 2, 1, 0>, conv_tc_k<16, 2, 1, 0>,
-                   conv_tc_k<2, 2, 2, 0>, conv_tc_k<4, 2, 2, 0>, conv_tc_k<8, 2, 2, 0>, conv_tc_k<16, 2, 2, 0>,
-                   conv_tc_k<2, 4, 1, 0>, conv_tc_k<4, 4, 1, 0>, conv_tc_k<8, 4, 1, 0>, conv_tc_k<16, 4, 1, 0>,
-                   conv_tc_k<2, 4, 2, 0>, conv_tc_k<4, 4, 2, 0>, conv_tc_k<8, 4, 2, 0>, conv_tc_k<16, 4, 2, 0>,
-                   conv_tc_k<2, 1, 1, 1>, conv_tc_k<4, 1, 1, 1>, conv_tc_k<8, 1, 1, 1>, conv_tc_k<16, 1, 1, 1>,
-                   conv_tc_k<2, 1, 1, 2>, conv_tc_k<4, 1, 1, 2>, conv_tc_k<8, 1, 1, 2>, conv_tc_k<16, 1, 1, 2>})
-      D2IP_CUDA(cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    attr_set = true;
-  }
   const dim3 grid(tiles, (a.Np / a.Ns) * a.kspl, batch);
   // one producer group (all eight warps per stage) measured faster than two on
   // cfg1 (1029 vs 1013 it/s) and cfg2 (280 vs 274); D2IP_TC_PG=2 selects two
@@ -625,25 +778,12 @@ int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, lo
     const char* v = getenv("D2IP_TC_PG");
     return v && atoi(v) == 2;
   }();
-#define D2IP_TC_LAUNCH(NKC_)                                                                                 \
-  do {                                                                                                       \
-    if (mode == 1) D2IP_CUDA(launch_pdl((conv_tc_k<NKC_, 1, 1, 1>), grid, kTcThreads, smem, st, a));        \
-    else if (mode == 2) D2IP_CUDA(launch_pdl((conv_tc_k<NKC_, 1, 1, 2>), grid, kTcThreads, smem, st, a));   \
-    else if (a.T == 4 && pg2) D2IP_CUDA(launch_pdl((conv_tc_k<NKC_, 4, 2, 0>), grid, kTcThreads, smem, st, a)); \
-    else if (a.T == 4) D2IP_CUDA(launch_pdl((conv_tc_k<NKC_, 4, 1, 0>), grid, kTcThreads, smem, st, a));    \
-    else if (a.T == 2 && pg2) D2IP_CUDA(launch_pdl((conv_tc_k<NKC_, 2, 2, 0>), grid, kTcThreads, smem, st, a)); \
-    else if (a.T == 2) D2IP_CUDA(launch_pdl((conv_tc_k<NKC_, 2, 1, 0>), grid, kTcThreads, smem, st, a));    \
-    else if (pg2) D2IP_CUDA(launch_pdl((conv_tc_k<NKC_, 1, 2, 0>), grid, kTcThreads, smem, st, a));         \
-    else D2IP_CUDA(launch_pdl((conv_tc_k<NKC_, 1, 1, 0>), grid, kTcThreads, smem, st, a));                  \
-  } while (0)
-  switch (a.CB / 4) {
-    case 2: D2IP_TC_LAUNCH(2); break;
-    case 4: D2IP_TC_LAUNCH(4); break;
-    case 8: D2IP_TC_LAUNCH(8); break;
-    case 16: D2IP_TC_LAUNCH(16); break;
-    default: D2IP_CHECK_ARG(false, "conv_tc: unsupported channel block %d", a.CB);
-  }
-#undef D2IP_TC_LAUNCH
+  int rc;
+  if (bf)
+    rc = tc_dispatch_nkc<true>(a, grid, smem, st, mode, false);
+  else
+    rc = tc_dispatch_nkc<false>(a, grid, smem, st, mode, pg2);
+  D2IP_RET(rc);
   D2IP_LAUNCH_CHECK();
   if (deferred) *deferred = a.kspl > 1 ? a.kspl : 0;
   if (a.kspl > 1 && !deferred) {
@@ -651,7 +791,8 @@ int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, lo
                          a.vout, Nout, bias, bbs, y, accumulate));
     D2IP_LAUNCH_CHECK();
   }
-  set_variant(a.kspl > 1 ? "tcgen05_tf32x3_splitk" : "tcgen05_tf32x3");
+  set_variant(bf ? (a.kspl > 1 ? "tcgen05_bf16_splitk" : "tcgen05_bf16")
+                 : (a.kspl > 1 ? "tcgen05_tf32x3_splitk" : "tcgen05_tf32x3"));
   return D2IP_OK;
 }
 

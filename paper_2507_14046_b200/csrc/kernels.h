@@ -55,7 +55,9 @@ int wgrad_tc(d2ip_act x, d2ip_act gy, int ks, float* gw, long long gwbs, void* w
 // conv_tc.cu — tcgen05 implicit-GEMM convolutions (tf32 / bf16 operands)
 bool conv_tc_supported(int cin, int cout, int ks, int stride, int precision);
 // GEMM view of a layer's tcgen05 forward (dgrad = 0) or data gradient: K, N,
-// kernel mode (0 stride 1, 1 stride-2 forward, 2 stride-2 dgrad) and pack code.
+// kernel mode (0 stride 1, 1 stride-2 forward, 2 stride-2 dgrad) and pack code;
+// both carry kTcBf16 when the layer runs with bf16 operands (kind::f16).
+constexpr int kTcBf16 = 4;
 struct TcDims {
   int K, N, mode, pack;
 };

@@ -615,8 +615,10 @@ static size_t wt_smem(const WgTc& a) {
          2 * (size_t)(a.WR + a.RSg) * sizeof(int) + 64;
 }
 
+// bf16 layers use it too until a kind::f16 weight-gradient kernel exists: 3xTF32
+// is more accurate than the bf16 bar asks for.
 bool wgrad_tc_supported(d2ip_act x, d2ip_act gy, int ks, int precision) {
-  if (precision != D2IP_PREC_TF32) return false;
+  if (precision != D2IP_PREC_TF32 && precision != D2IP_PREC_BF16) return false;
   if (x.d != gy.d || x.h != gy.h || x.w != gy.w) return false;
   if (x.cstride % 4 || gy.cstride % 4 || ((uintptr_t)x.ptr & 15) || ((uintptr_t)gy.ptr & 15)) return false;
   WgTc a{};

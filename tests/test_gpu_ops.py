@@ -84,7 +84,17 @@ def s2_big(cin, cout, sp):
     return int(np.prod([(n + 1) // 2 for n in sp])) * cin * cout >= 4 * 1024 * 1024
 
 
-@pytest.mark.parametrize("prec", ["fp32", "tf32"])
+def bf16_tc(cin, cout, ks, stride, sp, dgrad):
+    """bf16 operands on the tensor cores (conv_tc_layer): 16-channel K steps, 8-channel parity chunks."""
+    if ks != 3:
+        return False
+    K = cout if dgrad else cin
+    if stride == 1:
+        return K % 16 == 0
+    return s2_big(cin, cout, sp) and cin % 8 == 0 and (8 * cin if not dgrad else cout) % 16 == 0 and (not dgrad or cout % 8 == 0)
+
+
+@pytest.mark.parametrize("prec", ["fp32", "tf32", "bf16"])
 @pytest.mark.parametrize("cin,cout,ks,stride,sp", CONV_CASES)
 def test_conv3d_fwd(cin, cout, ks, stride, sp, prec):
     torch.manual_seed(0)
@@ -112,6 +122,8 @@ def test_conv3d_fwd(cin, cout, ks, stride, sp, prec):
     torch.cuda.synchronize()
     if prec == "tf32" and ks == 3 and ((stride == 1 and cin % 8 == 0) or (stride == 2 and cin % 4 == 0 and s2_big(cin, cout, sp))):
         assert L.d2ip_last_variant().startswith(b"tcgen05_tf32x3")
+    if prec == "bf16" and bf16_tc(cin, cout, ks, stride, sp, False):
+        assert L.d2ip_last_variant().startswith(b"tcgen05_bf16")
     assert rel(from_ndhwc(out), ref) < TOL[prec]
     # accumulate mode adds on top
     N.check(L.d2ip_conv3d_fwd(xa, C.c_void_p(params.data_ptr()), None, P, ks, stride, ya, 1, N.PREC[prec],
@@ -130,7 +142,7 @@ def wgrad_variant(request):
     L.d2ip_set_wgrad_variant(before)
 
 
-@pytest.mark.parametrize("prec", ["fp32", "tf32"])
+@pytest.mark.parametrize("prec", ["fp32", "tf32", "bf16"])
 @pytest.mark.parametrize("cin,cout,ks,stride,sp", CONV_CASES)
 def test_conv3d_dgrad_wgrad(cin, cout, ks, stride, sp, prec, wgrad_variant):
     torch.manual_seed(1)
@@ -151,6 +163,8 @@ def test_conv3d_dgrad_wgrad(cin, cout, ks, stride, sp, prec, wgrad_variant):
                                       N.PREC[prec], C.c_void_p(wsd.data_ptr()), wsn, B, stream()), "dgrad")
     if prec == "tf32" and ks == 3 and cout % 8 == 0 and cin % 8 == 0 and (stride == 1 or s2_big(cin, cout, sp)):
         assert N.lib().d2ip_last_variant().startswith(b"tcgen05_tf32x3")
+    if prec == "bf16" and bf16_tc(cin, cout, ks, stride, sp, True):
+        assert N.lib().d2ip_last_variant().startswith(b"tcgen05_bf16")
     xd = to_ndhwc(x.detach())
     gw = torch.zeros(B, P, device="cuda")
     ws_n = N.lib().d2ip_conv3d_wgrad_ws_bytes(act_of(xd), act_of(gyd), ks, B)
