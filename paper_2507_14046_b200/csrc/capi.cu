@@ -46,11 +46,16 @@ size_t conv_wgrad_ws(int cin, int cout, int ks, int D, int H, int W, int batch, 
   const size_t a = conv_wgrad_direct_ws(cin, cout, ks, (long long)D * H * W, batch);
   const size_t b = wgrad_s1_ws_bytes(D, H, W, cin, cout, ks, batch);
   const size_t c = wgrad_tc_ws_bytes(D, H, W, cin, cout, ks, batch);
-  return std::max(a, std::max(b, c));
+  const size_t d = wgrad_bf_ws_bytes(D, H, W, cin, cout, ks, batch);
+  return std::max(std::max(a, d), std::max(b, c));
 }
 
 int conv_wgrad(d2ip_act x, d2ip_act gy, int ks, int stride, float* gw, long long gwbs, void* ws,
                size_t ws_bytes, int precision, int batch, cudaStream_t st) {
+  if (stride == 1 && precision == D2IP_PREC_BF16 && g_wgrad_variant == 1 && wgrad_bf_supported(x, gy, ks)) {
+    set_variant("wgrad_tcgen05_bf16");
+    return wgrad_bf(x, gy, ks, gw, gwbs, ws, ws_bytes, batch, st);
+  }
   if (stride == 1 && g_wgrad_variant == 1 && wgrad_tc_supported(x, gy, ks, precision)) {
     set_variant("wgrad_tcgen05_tf32x3");
     return wgrad_tc(x, gy, ks, gw, gwbs, ws, ws_bytes, batch, st);

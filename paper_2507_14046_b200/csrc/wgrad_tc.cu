@@ -695,4 +695,14 @@ int wgrad_tc(d2ip_act x, d2ip_act gy, int ks, float* gw, long long gwbs, void* w
   return D2IP_OK;
 }
 
+// Fixed-order sum of per-row-group partials [b][rg][ntaps][Cin][Cout] + [Cout]
+// into OIDHW weight gradients + bias (also used by wgrad_bf.cu).
+int wgrad_reduce(const float* part, int nrg, int ntaps, int Cin, int Cout, float* gw, long long gwbs, int batch,
+                 cudaStream_t st) {
+  const long long n = (long long)ntaps * Cin * Cout + Cout;
+  D2IP_CUDA(launch_pdl(wgrad_tc_reduce_k, dim3(cdiv(n, 256), batch), 256, 0, st, part, nrg, ntaps, Cin, Cout, gw, gwbs));
+  D2IP_LAUNCH_CHECK();
+  return D2IP_OK;
+}
+
 }  // namespace d2ip

@@ -142,6 +142,16 @@ def wgrad_variant(request):
     L.d2ip_set_wgrad_variant(before)
 
 
+def bf16_wgrad_tc(cin, cout, stride):
+    """Stride-1 weight gradients of bf16 layers on kind::f16 MMAs (wgrad_bf.cu plan)."""
+    if stride != 1 or cin % 8 or cout < 16 or cout > 256 or cout & (cout - 1):
+        return False
+    nb = 1
+    while cin // nb > 128 or cin % nb or (cin // nb) % 8:
+        nb += 1
+    return cin // nb // 4 in (2, 4, 8, 12, 16, 24, 32)
+
+
 @pytest.mark.parametrize("prec", ["fp32", "tf32", "bf16"])
 @pytest.mark.parametrize("cin,cout,ks,stride,sp", CONV_CASES)
 def test_conv3d_dgrad_wgrad(cin, cout, ks, stride, sp, prec, wgrad_variant):
@@ -174,6 +184,8 @@ def test_conv3d_dgrad_wgrad(cin, cout, ks, stride, sp, prec, wgrad_variant):
     torch.cuda.synchronize()
     if wgrad_variant == 1 and prec == "tf32" and stride == 1 and cin % 4 == 0 and cout % 4 == 0 and cout <= 128:
         assert N.lib().d2ip_last_variant() == b"wgrad_tcgen05_tf32x3"
+    if wgrad_variant == 1 and prec == "bf16" and bf16_wgrad_tc(cin, cout, stride):
+        assert N.lib().d2ip_last_variant() == b"wgrad_tcgen05_bf16"
     assert rel(from_ndhwc(gx), x.grad) < TOL[prec]
     ref_gw = torch.cat([torch.cat([w.grad[i].reshape(-1), b.grad[i]]) for i in range(B)]).reshape(B, P)
     nW = cout * cin * ks ** 3

@@ -52,7 +52,16 @@ for prec in precs:
                                     act(gx, cin, (Dd, Hd, Wd)), 0,
                                     N.PREC[prec], C.c_void_p(ws.data_ptr()), wsn, 1, st), "dgrad")
 
-    for name, fn in (("fwd", fwd), ("dgrad", dgrad)):
+    gw = torch.zeros(P, device="cuda")
+    wgn = max(16, L.d2ip_conv3d_wgrad_ws_bytes(act(x, cin, (Dd, Hd, Wd)), act(y, cout, (Do, Ho, Wo)), 3, 1))
+    wgs = torch.empty(wgn, dtype=torch.uint8, device="cuda")
+
+    def wgrad():
+        N.check(L.d2ip_conv3d_wgrad(act(x, cin, (Dd, Hd, Wd)), act(y, cout, (Do, Ho, Wo)), 3, stride,
+                                    C.c_void_p(gw.data_ptr()), P, C.c_void_p(wgs.data_ptr()), wgn, N.PREC[prec], 1,
+                                    st), "wgrad")
+
+    for name, fn in (("fwd", fwd), ("dgrad", dgrad), ("wgrad", wgrad)):
         for _ in range(5):
             fn()
         torch.cuda.synchronize()

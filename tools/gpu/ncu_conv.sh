@@ -1,6 +1,6 @@
 # usage: bash tools/gpu/ncu_conv.sh TAG "cin cout dims stride" prec
 TAG=$1; ARGS=$2; PREC=$3
-timeout 300 ncu --set full --import-source on --clock-control none -k regex:conv_tc_k -c 1 -o gpurun_out/ncu_$TAG python tools/conv_bench.py $ARGS 1 $PREC > gpurun_out/ncu_$TAG.log 2>&1
+timeout 300 ncu --set full --import-source on --clock-control none -k regex:${KREGEX:-conv_tc_k} -c 1 -o gpurun_out/ncu_$TAG python tools/conv_bench.py $ARGS 1 $PREC > gpurun_out/ncu_$TAG.log 2>&1
 echo ncu rc $?
 ncu -i gpurun_out/ncu_$TAG.ncu-rep --page details --csv > gpurun_out/ncu_$TAG.details.csv 2>/dev/null
 ncu -i gpurun_out/ncu_$TAG.ncu-rep --page raw --csv > gpurun_out/ncu_$TAG.raw.csv 2>/dev/null

@@ -30,7 +30,7 @@ __device__ __forceinline__ void mma_elect(uint32_t d, uint64_t a, uint64_t b, ui
 // issues (divergent branch), MODE 1: the whole warp runs the loop and an
 // elect.sync inside the asm picks the issuing lane.
 template <bool F16, int NACC, int MODE>
-__global__ void chains_k(int M, int N, int nmma, int nw, long long* cycles) {
+__global__ void chains_k(int M, int N, int nmma, int nw, long long* cycles, int mn) {
   extern __shared__ __align__(1024) uint8_t smem[];
   uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + 65536);
   uint32_t* tslot = reinterpret_cast<uint32_t*>(mbar + 4);
@@ -46,10 +46,11 @@ __global__ void chains_k(int M, int N, int nmma, int nw, long long* cycles) {
   long long t0 = clock64();
   const bool issuer = MODE == 1 ? warp < nw : (warp < nw && (threadIdx.x & 31) == 0);
   if (issuer) {
-    const uint32_t idesc = tc::make_idesc(F16 ? 1 : 2, M, N);
+    // mn: operands MN-major (LBO = 128 B between 8-row K blocks, SBO = 2 KB between 8-element groups)
+    const uint32_t idesc = tc::make_idesc(F16 ? 1 : 2, M, N) | (mn ? (1u << 15) | (1u << 16) : 0u);
     const uint32_t sb = tc::smem_u32(smem);
-    const uint64_t da = tc::make_desc(sb, 2048, 128);
-    const uint64_t db = tc::make_desc(sb + 32768, 2048, 128);
+    const uint64_t da = mn ? tc::make_desc(sb, 128, 2048) : tc::make_desc(sb, 2048, 128);
+    const uint64_t db = mn ? tc::make_desc(sb + 32768, 128, 2048) : tc::make_desc(sb + 32768, 2048, 128);
     const uint32_t dbase = tmem + (uint32_t)(warp * NACC * N);
 #pragma unroll
     for (int a = 0; a < NACC; ++a) {
@@ -84,14 +85,14 @@ __global__ void chains_k(int M, int N, int nmma, int nw, long long* cycles) {
 }
 
 template <bool F16, int NACC, int MODE>
-static void run(int M, int N, int nw, long long* d, cudaEvent_t e0, cudaEvent_t e1) {
+static void run(int M, int N, int nw, long long* d, cudaEvent_t e0, cudaEvent_t e1, int mn = 0) {
   if (nw * NACC * N > 512) return;
   auto k = chains_k<F16, NACC, MODE>;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, 100 * 1024);
   const int nmma = 4096, blocks = 148;
-  k<<<blocks, 128, 70 * 1024>>>(M, N, nmma, nw, d);
+  k<<<blocks, 128, 70 * 1024>>>(M, N, nmma, nw, d, mn);
   cudaEventRecord(e0);
-  k<<<blocks, 128, 70 * 1024>>>(M, N, nmma, nw, d);
+  k<<<blocks, 128, 70 * 1024>>>(M, N, nmma, nw, d, mn);
   cudaEventRecord(e1);
   cudaError_t e = cudaDeviceSynchronize();
   if (e != cudaSuccess) { printf("err %s\n", cudaGetErrorString(e)); exit(1); }
@@ -101,17 +102,23 @@ static void run(int M, int N, int nw, long long* d, cudaEvent_t e0, cudaEvent_t 
   cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
   const double K = F16 ? 16 : 8;
   const double flops = 2.0 * M * N * K * nmma * blocks;
-  printf("%s %s M=%3d N=%3d issuers=%d nacc=%d: %.1f cyc/mma per CTA, device %.1f TFLOP/s\n",
-         MODE ? "elect" : "lane0", F16 ? "f16 " : "tf32", M, N, nw, NACC, (double)h / nmma,
+  printf("%s %s %s M=%3d N=%3d issuers=%d nacc=%d: %.1f cyc/mma per CTA, device %.1f TFLOP/s\n",
+         MODE ? "elect" : "lane0", F16 ? "f16 " : "tf32", mn ? "MN-major" : "K-major ", M, N, nw, NACC, (double)h / nmma,
          flops / (ms * 1e-3) / 1e12);
 }
 
-int main() {
+int main(int argc, char**) {
   long long* d;
   cudaMalloc(&d, 16);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
+  if (argc > 1) {  // operand-major comparison at the weight-gradient shapes
+    for (int M : {64, 128})
+      for (int N : {16, 32, 64, 128, 256})
+        for (int mn : {0, 1}) run<true, 2, 1>(M, N, 1, d, e0, e1, mn);
+    return 0;
+  }
   for (int N : {16, 32, 64, 128, 256})
     for (int nw : {1, 2, 4}) {
       run<true, 1, 0>(128, N, nw, d, e0, e1);
