@@ -37,6 +37,10 @@
 // scattered by the epilogue to its parity voxel 2o + p of gx. The pack kernel
 // lays out the parity weights (zeros where a parity has no tap).
 //
+// 1^3 layers (mode 3, "pointwise"): one tap, one plane, a window of exactly
+// the tile's 128 T rows (no halo) per channel block -- a plain GEMM over voxels
+// (the decoder / bottleneck skip convolutions, priornet.py:145-148 restated).
+//
 // bf16 operands (precision D2IP_PREC_BF16, mode bit kTcBf16): one kind::f16
 // MMA per 16-channel K step instead of three kind::tf32 MMAs per 8 channels.
 // The producers load the fp32 activation window through registers and store
@@ -84,7 +88,7 @@ struct TcConv {
   int kspl;     // split-K factor over the (plane tap, channel block) stages
   float* part;  // kspl > 1: partial sums [b][kspl][V][N] (mode 2: [b][kspl][V_gx][C_gx])
   long long vout;
-  int mode;     // 0: stride 1; 1: stride-2 forward (parity-gathered input); 2: stride-2 dgrad (parity-scattered output)
+  int mode;     // 0: stride 1; 1: stride-2 forward (parity-gathered input); 2: stride-2 dgrad (parity-scattered output); 3: 1^3
   int t0, nt;   // taps per axis used: t0 .. t0 + nt - 1 (offsets t - 1)
   int gd, gh, gw;  // row-space grid (stride 1: x; mode 1: y; mode 2: gy)
   int bf;          // bf16 operands (kind::f16)
@@ -127,7 +131,8 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
   const int n0 = (blockIdx.y / a.kspl) * a.Ns;  // first output channel of this CTA's slice
   const int u0 = a.u_first + blockIdx.x * T * kTcRows;
   const int Ns = a.Ns, WR = a.WR, WRp = a.WRp;
-  constexpr int nt = MODE ? 2 : 3, t0 = MODE == 2 ? 1 : 0, ntap = nt * nt;
+  constexpr bool PW = MODE == 3;  // 1^3: one tap, window = the tile rows
+  constexpr int nt = PW ? 1 : MODE ? 2 : 3, t0 = MODE == 2 ? 1 : 0, ntap = nt * nt;
   // (kh, kw) of the q-th live tap as a 3x3 index: nt = 3 -> q; nt = 2 -> the 2x2 block at (t0, t0)
   auto tap9 = [&](int q) { return nt == 3 ? q : (t0 + (q >> 1)) * 3 + (t0 + (q & 1)); };
   const uint32_t Ab = (uint32_t)NKC * WRp * 16, Bb = (uint32_t)ntap * NKC * Ns * 16;
@@ -151,9 +156,9 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
   // voxel offset of every window row for the three plane taps (-1 = padding);
   // mode 1: (even-corner input voxel << 3) | which odd parities exist per axis
   const d2ip_act x = a.x;
-  for (int i = tid; i < 3 * WR; i += kTcThreads) {
+  for (int i = tid; i < (PW ? WR : 3 * WR); i += kTcThreads) {
     const int kd = i / WR, r = i - kd * WR;
-    const int u = u0 + (kd - 1) * a.Sh - a.Sw - 1 + r;
+    const int u = PW ? u0 + r : u0 + (kd - 1) * a.Sh - a.Sw - 1 + r;
     int off = -1;
     if (u >= 0) {
       const int dp = u / a.Sh, rem = u - dp * a.Sh;
@@ -197,7 +202,7 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
         const uint64_t boff = slot ? (uint64_t)(Sb >> 4) : 0;
         for (int tq = 0; tq < ntap; ++tq) {
           const int t9 = tap9(tq);
-          const int rowoff = (t9 >= 6 ? 2 : t9 >= 3 ? 1 : 0) * a.Sw + (t9 % 3);
+          const int rowoff = PW ? 0 : (t9 >= 6 ? 2 : t9 >= 3 ? 1 : 0) * a.Sw + (t9 % 3);
 #pragma unroll
           for (int j = 0; j < NKC / 2; ++j) {
             const uint64_t bo = boff + (uint64_t)((tq * NKC + 2 * j) * Ns);
@@ -230,7 +235,7 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
       if (s >= 2) tc::mbar_wait(&empty[slot], (uint32_t)(((s >> 1) - 1) & 1));
       const int sg = s_lo + s;
       const int kdi = sg / a.n_cb, cb = sg - kdi * a.n_cb;
-      const int kd = t0 + kdi;
+      const int kd = PW ? 0 : t0 + kdi;
       const int* rm = rowmap + kd * WR;
       uint8_t* A = smem + slot * Sb;
       if (BF) {
@@ -299,7 +304,7 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
       const int gwarp = gtid >> 5;
       for (int q = gwarp; q < ntap * NKC; q += GT / 32) {
         const int tq = q / NKC, kcl = q % NKC;
-        const int t9 = tap9(tq);
+        const int t9 = PW ? 0 : tap9(tq);
         const float* src = wk + ((long long)t9 * kc_all + kcl) * a.Np * 4;
         uint8_t* dst = Bt + (size_t)q * Ns * 16;
         for (int n = lane; n < Ns; n += 32) {
@@ -452,8 +457,10 @@ __device__ __forceinline__ int s2_axis(int ta, int pa, int dgrad) {
 }
 
 // One packed weight: code 0 forward, 1 stride-1 dgrad, 2 stride-2 forward
-// (k = p C_in + ci), 3 stride-2 dgrad (n = p C_in + ci); + kTcBf16: bf16 layout.
+// (k = p C_in + ci), 3 stride-2 dgrad (n = p C_in + ci); + kTcBf16: bf16 layout;
+// + kTcPw: 1^3 weights (one tap).
 __device__ __forceinline__ float pack_val(const float* wb, int K, int N, int code, int t, int k, int n) {
+  if (code & kTcPw) return (code & 1) ? wb[(long long)k * N + n] : wb[(long long)n * K + k];  // 1^3: [co][ci]
   code &= 3;
   if (code == 0) return wb[((long long)n * K + k) * 27 + t];
   if (code == 1) return wb[((long long)k * N + n) * 27 + (26 - t)];
@@ -504,7 +511,7 @@ __global__ void conv_tc_pack_k(const float* __restrict__ w, long long wbs, int K
   const float val = n < N ? pack_val(w + b * wbs, K, N, dgrad, t, k, n) : 0.f;
   const float hi = tf32_hi(val);
   out[b * obs + i] = hi;
-  out[b * obs + half + i] = val - hi;
+  out[b * obs + obs / 2 + i] = val - hi;  // lo half at the fixed offset the kernel reads (wlo)
 }
 
 // All layers' packs in one launch: blockIdx.x walks the concatenated job ranges.
@@ -518,8 +525,7 @@ __global__ void conv_tc_pack_multi_k(PackJobs j) {
   if (i >= half) return;
   const int K = j.K[q], N = j.N[q], Np = np_of(N);
   if (j.dgrad[q] & kTcBf16) {
-    pack_bf16(j.w[q] + b * j.wbs, K, N, Np, j.dgrad[q], i,
-              reinterpret_cast<__nv_bfloat16*>(j.out[q] + b * 2 * half));
+    pack_bf16(j.w[q] + b * j.wbs, K, N, Np, j.dgrad[q], i, reinterpret_cast<__nv_bfloat16*>(j.out[q] + b * j.obs[q]));
     return;
   }
   const int jj = (int)(i & 3);
@@ -531,9 +537,9 @@ __global__ void conv_tc_pack_multi_k(PackJobs j) {
   const int k = 4 * kc + jj;
   const float val = n < N ? pack_val(j.w[q] + b * j.wbs, K, N, j.dgrad[q], t, k, n) : 0.f;
   const float hi = tf32_hi(val);
-  float* out = j.out[q] + b * 2 * half;
+  float* out = j.out[q] + b * j.obs[q];
   out[i] = hi;
-  out[half + i] = val - hi;
+  out[j.obs[q] / 2 + i] = val - hi;
 }
 
 int conv_tc_pack_multi(const PackJobs& jobs, int batch, cudaStream_t st) {
@@ -550,12 +556,14 @@ void pack_jobs_add(PackJobs& j, const float* w, int K, int N, int dgrad, float* 
   j.K[q] = K;
   j.N[q] = N;
   j.dgrad[q] = dgrad;
-  j.half[q] = 27LL * K * np_of(N);
+  j.half[q] = ((dgrad & kTcPw) ? 1LL : 27LL) * K * np_of(N);
+  j.obs[q] = conv_tc_pack_floats(K, N);
   j.block0[q + 1] = j.block0[q] + (int)((j.half[q] + 255) / 256);
 }
 
 bool conv_tc_supported(int cin, int cout, int ks, int stride, int precision) {
-  if ((precision != D2IP_PREC_TF32 && precision != D2IP_PREC_BF16) || ks != 3 || stride != 1) return false;
+  if ((precision != D2IP_PREC_TF32 && precision != D2IP_PREC_BF16) || (ks != 3 && ks != 1) || stride != 1)
+    return false;
   if (cin % 8 || cin < 8 || cout < 1 || np_of(cout) > 1024) return false;
   return true;
 }
@@ -565,8 +573,8 @@ bool conv_tc_layer(int cin, int cout, int ks, int stride, int dgrad, int precisi
   if (stride == 1) {
     r.K = dgrad ? cout : cin;
     r.N = dgrad ? cin : cout;
-    r.mode = 0;
-    r.pack = dgrad;
+    r.mode = ks == 1 ? 3 : 0;
+    r.pack = dgrad | (ks == 1 ? kTcPw : 0);
     if (!conv_tc_supported(r.K, r.N, ks, 1, precision)) return false;
     // bf16: 16-channel K steps; K % 16 != 0 (e.g. the 8-channel stem) keeps 3xTF32
     if (precision == D2IP_PREC_BF16 && r.K % 16 == 0) {
@@ -604,7 +612,7 @@ bool conv_tc_layer(int cin, int cout, int ks, int stride, int dgrad, int precisi
 long long conv_tc_pack_floats(int K, int N) { return 2 * 27LL * K * np_of(N); }
 
 int conv_tc_pack(const float* w, long long wbs, int K, int N, int dgrad, float* out, int batch, cudaStream_t st) {
-  const long long total = conv_tc_pack_floats(K, N), half = total / 2;
+  const long long total = conv_tc_pack_floats(K, N), half = ((dgrad & kTcPw) ? 1LL : 27LL) * K * np_of(N);
   D2IP_CUDA(launch_pdl(conv_tc_pack_k, dim3(cdiv(half, 256), batch), 256, 0, st, w, wbs, K, N, np_of(N), dgrad, out, half, total));
   D2IP_LAUNCH_CHECK();
   return D2IP_OK;
@@ -635,8 +643,8 @@ static bool tc_plan(int D, int H, int W, int K, int N, int batch, TcConv& a, int
   // a stage costs max(cp.async landing ~1.5, its MMAs: 27/8 CB T x 57 cycles).
   const bool large = (long long)tiles1 * batch >= 4LL * 296;
   for (int T : {1, 2, 4}) {
-    if (T > 1 && (!large || nt != 3)) break;
-    const int wr = wr_of(a.Sw, T), wrp = wrp_of(wr);
+    if (T > 1 && (!large || nt == 2)) break;
+    const int wr = nt == 1 ? T * kTcRows : wr_of(a.Sw, T), wrp = wrp_of(wr);
     const int tl = cdiv(tiles1, T);
     for (int ns = std::min(a.Np, 256); ns >= 16; ns -= 16) {
       if (a.Np % ns) continue;
@@ -685,7 +693,8 @@ static bool tc_plan(int D, int H, int W, int K, int N, int batch, TcConv& a, int
 size_t conv_tc_ws_bytes(int D, int H, int W, int K, int N, int batch, int mode) {
   TcConv a{};
   int tiles;
-  if (!tc_plan(D, H, W, K, N, batch, a, &tiles, (mode & 3) ? 2 : 3, (mode & kTcBf16) != 0) || a.kspl <= 1)
+  const int m3 = mode & 3;
+  if (!tc_plan(D, H, W, K, N, batch, a, &tiles, m3 == 3 ? 1 : m3 ? 2 : 3, (mode & kTcBf16) != 0) || a.kspl <= 1)
     return 0;
   // mode 2 partials are [V_gx][C_gx]: V_gx C_gx <= 8 V N / 8 (gx dims <= 2 x the row grid)
   return (size_t)batch * a.kspl * a.vout * N * sizeof(float);
@@ -708,6 +717,11 @@ template <int NKC, bool BF>
 static int tc_dispatch(const TcConv& a, dim3 grid, size_t smem, cudaStream_t st, int mode, bool pg2) {
   if (mode == 1) return tc_launch<NKC, 1, 1, 1, BF>(a, grid, smem, st);
   if (mode == 2) return tc_launch<NKC, 1, 1, 2, BF>(a, grid, smem, st);
+  if (mode == 3) {
+    if (a.T == 4) return tc_launch<NKC, 4, 1, 3, BF>(a, grid, smem, st);
+    if (a.T == 2) return tc_launch<NKC, 2, 1, 3, BF>(a, grid, smem, st);
+    return tc_launch<NKC, 1, 1, 3, BF>(a, grid, smem, st);
+  }
   if (!BF && pg2) {
     if (a.T == 4) return tc_launch<NKC, 4, 2, 0, BF>(a, grid, smem, st);
     if (a.T == 2) return tc_launch<NKC, 2, 2, 0, BF>(a, grid, smem, st);
@@ -745,11 +759,12 @@ int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, lo
   if (mode == 2) D2IP_CHECK_ARG(g.d == (y.d + 1) / 2 && g.h == (y.h + 1) / 2 && g.w == (y.w + 1) / 2, "conv_tc: stride-2 shape");
   TcConv a{};
   int tiles = 0;
-  D2IP_CHECK_ARG(tc_plan(g.d, g.h, g.w, K, N, batch, a, &tiles, mode ? 2 : 3, bf),
+  const int ntm = mode == 3 ? 1 : mode ? 2 : 3;
+  D2IP_CHECK_ARG(tc_plan(g.d, g.h, g.w, K, N, batch, a, &tiles, ntm, bf),
                  "conv_tc: no channel blocking fits shared memory (K=%d N=%d W=%d)", K, N, g.w);
   a.mode = mode;
   a.t0 = mode == 2 ? 1 : 0;
-  a.nt = mode ? 2 : 3;
+  a.nt = ntm;
   a.gd = g.d;
   a.gh = g.h;
   a.gw = g.w;

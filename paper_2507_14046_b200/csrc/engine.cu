@@ -195,6 +195,7 @@ static size_t plan_workspace(d2ip_engine& E, char* base) {
   for (auto& w : E.lane_ws) w = A.take(E.wg_ws_bytes);
   E.na_ws = A.take(E.na_ws_bytes);
   E.tc_ws = E.tc_ws_bytes ? reinterpret_cast<float*>(A.take(E.tc_ws_bytes)) : nullptr;
+  E.tc_ws2 = E.tc_ws_bytes ? reinterpret_cast<float*>(A.take(E.tc_ws_bytes)) : nullptr;
   return A.total();
 }
 
@@ -238,12 +239,16 @@ static void plan_views(d2ip_engine& E) {
 
 // Forward conv; with `sk`, a split-K tcgen05 result is left as partials for
 // the consuming LayerNorm kernel to reduce (one launch fewer per layer).
+// Split-K partial buffer of the stream a convolution runs on (main or side2):
+// concurrent convolutions must not share one.
+static float* tcws(Ctx& k) { return k.st == k.E.side2 ? k.E.tc_ws2 : k.E.tc_ws; }
+
 int cfwd(Ctx& k, const ConvP& c, d2ip_act x, d2ip_act y, int acc, SplitK* sk) {
   if (c.tcf) {
     int kspl = 0;
-    D2IP_RET(conv_tc_run(x, c.pkf, c.tdf.K, c.tdf.N, k.th() + c.ob, k.pbs, y, acc, k.E.tc_ws, k.E.tc_ws_bytes, k.B,
+    D2IP_RET(conv_tc_run(x, c.pkf, c.tdf.K, c.tdf.N, k.th() + c.ob, k.pbs, y, acc, tcws(k), k.E.tc_ws_bytes, k.B,
                          k.st, sk && !acc ? &kspl : nullptr, c.tdf.mode));
-    if (sk) *sk = kspl ? SplitK{k.E.tc_ws, kspl, k.th() + c.ob, k.pbs} : SplitK{};
+    if (sk) *sk = kspl ? SplitK{tcws(k), kspl, k.th() + c.ob, k.pbs} : SplitK{};
     return D2IP_OK;
   }
   if (sk) *sk = SplitK{};
@@ -255,9 +260,9 @@ int cfwd(Ctx& k, const ConvP& c, d2ip_act x, d2ip_act y, int acc, SplitK* sk) {
 int cdgrad(Ctx& k, const ConvP& c, d2ip_act gy, d2ip_act gx, int acc, SplitK* sk) {
   if (c.tcd) {
     int kspl = 0;
-    D2IP_RET(conv_tc_run(gy, c.pkd, c.tdd.K, c.tdd.N, nullptr, 0, gx, acc, k.E.tc_ws, k.E.tc_ws_bytes, k.B, k.st,
+    D2IP_RET(conv_tc_run(gy, c.pkd, c.tdd.K, c.tdd.N, nullptr, 0, gx, acc, tcws(k), k.E.tc_ws_bytes, k.B, k.st,
                          sk && !acc ? &kspl : nullptr, c.tdd.mode));
-    if (sk) *sk = kspl ? SplitK{k.E.tc_ws, kspl, nullptr, 0} : SplitK{};
+    if (sk) *sk = kspl ? SplitK{tcws(k), kspl, nullptr, 0} : SplitK{};
     return D2IP_OK;
   }
   if (sk) *sk = SplitK{};

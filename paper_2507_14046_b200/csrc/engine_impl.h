@@ -65,6 +65,7 @@ struct d2ip_engine {
   size_t wg_ws_bytes = 0;
   void* na_ws = nullptr;
   float* tc_ws = nullptr;
+  float* tc_ws2 = nullptr;  // split-K partials of convolutions on the side2 stream (1^3 skips)
   size_t tc_ws_bytes = 0;
   d2ip::PackJobs packjobs;
   size_t na_ws_bytes = 0;

@@ -67,6 +67,7 @@ bool conv_tc_supported(int cin, int cout, int ks, int stride, int precision);
 // kernel mode (0 stride 1, 1 stride-2 forward, 2 stride-2 dgrad) and pack code;
 // both carry kTcBf16 when the layer runs with bf16 operands (kind::f16).
 constexpr int kTcBf16 = 4;
+constexpr int kTcPw = 8;  // pack code: 1^3 weights (mode 3)
 struct TcDims {
   int K, N, mode, pack;
 };
@@ -82,7 +83,8 @@ struct PackJobs {
   const float* w[kMax];
   float* out[kMax];
   int K[kMax], N[kMax], dgrad[kMax];
-  long long half[kMax];
+  long long half[kMax];  // packed elements per half (27 or 1 taps x K x Np)
+  long long obs[kMax];   // per-sequence stride of the pack buffer (conv_tc_pack_floats)
   int block0[kMax + 1] = {0};
 };
 void pack_jobs_add(PackJobs& j, const float* w, int K, int N, int dgrad, float* out);

@@ -73,6 +73,9 @@ CONV_CASES = [
     (4, 8, 3, 2, (6, 6, 6)),
     (128, 128, 3, 1, (8, 8, 4)),
     (192, 64, 3, 1, (16, 16, 8)),
+    # 1^3 on the tensor cores (pointwise mode), large enough for T > 1 tiles
+    (96, 32, 1, 1, (32, 32, 16)),
+    (64, 64, 1, 1, (16, 16, 16)),
     # large grids (cfg2 / cfg4 scale tiles)
     (16, 32, 3, 1, (64, 64, 32)),
     (32, 16, 3, 1, (48, 48, 32)),
@@ -86,9 +89,9 @@ def s2_big(cin, cout, sp):
 
 def bf16_tc(cin, cout, ks, stride, sp, dgrad):
     """bf16 operands on the tensor cores (conv_tc_layer): 16-channel K steps, 8-channel parity chunks."""
-    if ks != 3:
-        return False
     K = cout if dgrad else cin
+    if ks == 1:
+        return stride == 1 and K % 16 == 0
     if stride == 1:
         return K % 16 == 0
     return s2_big(cin, cout, sp) and cin % 8 == 0 and (8 * cin if not dgrad else cout) % 16 == 0 and (not dgrad or cout % 8 == 0)
@@ -120,7 +123,7 @@ def test_conv3d_fwd(cin, cout, ks, stride, sp, prec):
                            P, ks, stride, ya, 0, N.PREC[prec], C.c_void_p(ws.data_ptr()), wsn, B, stream())
     N.check(rc, "conv3d_fwd")
     torch.cuda.synchronize()
-    if prec == "tf32" and ks == 3 and ((stride == 1 and cin % 8 == 0) or (stride == 2 and cin % 4 == 0 and s2_big(cin, cout, sp))):
+    if prec == "tf32" and ((stride == 1 and cin % 8 == 0) or (ks == 3 and stride == 2 and cin % 4 == 0 and s2_big(cin, cout, sp))):
         assert L.d2ip_last_variant().startswith(b"tcgen05_tf32x3")
     if prec == "bf16" and bf16_tc(cin, cout, ks, stride, sp, False):
         assert L.d2ip_last_variant().startswith(b"tcgen05_bf16")
@@ -171,7 +174,7 @@ def test_conv3d_dgrad_wgrad(cin, cout, ks, stride, sp, prec, wgrad_variant):
     wsd = torch.empty(max(wsn, 16), dtype=torch.uint8, device="cuda")
     N.check(N.lib().d2ip_conv3d_dgrad(act_of(gyd), C.c_void_p(params.data_ptr()), P, ks, stride, act_of(gx), 0,
                                       N.PREC[prec], C.c_void_p(wsd.data_ptr()), wsn, B, stream()), "dgrad")
-    if prec == "tf32" and ks == 3 and cout % 8 == 0 and cin % 8 == 0 and (stride == 1 or s2_big(cin, cout, sp)):
+    if prec == "tf32" and cout % 8 == 0 and cin % 8 == 0 and (stride == 1 or (ks == 3 and s2_big(cin, cout, sp))):
         assert N.lib().d2ip_last_variant().startswith(b"tcgen05_tf32x3")
     if prec == "bf16" and bf16_tc(cin, cout, ks, stride, sp, True):
         assert N.lib().d2ip_last_variant().startswith(b"tcgen05_bf16")
