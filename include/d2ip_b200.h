@@ -35,7 +35,7 @@
 extern "C" {
 #endif
 
-#define D2IP_ABI_VERSION 3
+#define D2IP_ABI_VERSION 4
 
 enum {
   D2IP_OK = 0,
@@ -52,13 +52,18 @@ enum {
   D2IP_ARCH_FAST_RESUNET = 1    /* reference FastResUNet3D (priornet.py:183-232; SiLU, SE, ASPP, attention) */
 };
 
-/* A channels-last activation view (see conventions). */
+/* A channels-last activation view (see conventions). `bf16` optionally points
+ * at a bf16 twin with the same element layout (element i of the view at
+ * ((uint16_t*)bf16)[i offset]): producers write it when set, bf16-precision
+ * tensor-core kernels stream it with async copies instead of converting the
+ * fp32 values. NULL = no twin. */
 typedef struct {
   float* ptr;
   int d, h, w;
   int c;
   int cstride;
   long long bstride;
+  void* bf16;
 } d2ip_act;
 
 int d2ip_abi_version(void);

@@ -14,7 +14,7 @@ from pathlib import Path
 from .errors import NativeLibraryError
 
 LIB_PATH = Path(__file__).resolve().parent / "_d2ip_b200.so"
-ABI_VERSION = 3
+ABI_VERSION = 4
 ARCH_CONFIG_RESUNET = 0  # D2IP_ARCH_* (include/d2ip_b200.h)
 ARCH_FAST_RESUNET = 1
 
@@ -35,6 +35,7 @@ class Act(C.Structure):
         ("c", C.c_int),
         ("cstride", C.c_int),
         ("bstride", C.c_longlong),
+        ("bf16", C.c_void_p),  # optional bf16 twin (same element layout); NULL = none
     ]
 
 

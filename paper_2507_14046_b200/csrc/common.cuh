@@ -1,6 +1,7 @@
 // Shared helpers for the sm_100a DIP-step kernels.
 #pragma once
 
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 #include <stdio.h>
@@ -80,6 +81,23 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
 }
 
 inline int cdiv(long long a, long long b) { return (int)((a + b - 1) / b); }
+
+// Division by a runtime constant d (1 <= d < 2^14) of 0 <= n < 2^28 as a
+// multiply-high: q = (n * floor(2^42 / d + 1)) >> 42 (exact in that range).
+struct FastDiv {
+  uint32_t d;
+  unsigned long long m;
+};
+inline FastDiv fastdiv(uint32_t d) { return FastDiv{d, (1ull << 42) / d + 1}; }
+__device__ __forceinline__ int fdiv(int n, const FastDiv& f) {
+  return (int)(((unsigned long long)(uint32_t)n * f.m) >> 42);
+}
+
+// two floats -> packed bf16x2 (round to nearest even), low half = a
+__device__ __forceinline__ uint32_t bf16x2(float a, float b) {
+  const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
+  return *reinterpret_cast<const uint32_t*>(&h);
+}
 
 __device__ __forceinline__ long long vox_count(const d2ip_act& a) {
   return (long long)a.d * a.h * a.w;

@@ -93,6 +93,7 @@ struct TcConv {
   int gd, gh, gw;  // row-space grid (stride 1: x; mode 1: y; mode 2: gy)
   int bf;          // bf16 operands (kind::f16)
   int vec;         // y rows (and bias) 16-byte aligned: float4 epilogue stores
+  int xtw;         // bf16: stream x from its bf16 twin (cp.async) instead of converting fp32 rows
 };
 
 // Per stage: A hi + A lo windows, B hi + B lo tiles (nt^2 taps); bf16: one
@@ -199,6 +200,7 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
         const int slot = s & 1;
         tc::mbar_wait(&full[slot], (uint32_t)((s >> 1) & 1));
         tc::fence_after();
+        if (BF) tc::fence_proxy_async();
         const uint64_t boff = slot ? (uint64_t)(Sb >> 4) : 0;
         for (int tq = 0; tq < ntap; ++tq) {
           const int t9 = tap9(tq);
@@ -238,7 +240,25 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
       const int kd = PW ? 0 : t0 + kdi;
       const int* rm = rowmap + kd * WR;
       uint8_t* A = smem + slot * Sb;
-      if (BF) {
+      if (BF && a.xtw) {
+        // bf16 twin of x: one 16-byte async copy per (row, 8-channel chunk); zero-fill for padding rows
+        const uint16_t* xt = reinterpret_cast<const uint16_t*>(x.bf16) + b * x.bstride;
+        const long long plane = (long long)x.h * x.w;
+        for (int i = gtid; i < nA; i += GT) {
+          const int r = i / NKC, kc = i % NKC;
+          const int off = rm[r];
+          const uint16_t* src = nullptr;
+          if (MODE == 1) {
+            const int c = cb * CB + 8 * kc, p = c / x.c, ci = c - p * x.c;
+            const int pd = p >> 2, ph = (p >> 1) & 1, pw = p & 1;
+            if (off >= 0 && (!pd || (off & 4)) && (!ph || (off & 2)) && (!pw || (off & 1)))
+              src = xt + ((off >> 3) + pd * plane + ph * x.w + pw) * (long long)x.cstride + ci;
+          } else if (off >= 0) {
+            src = xt + (long long)off * x.cstride + cb * CB + 8 * kc;
+          }
+          tc::cp_async16(A + ((size_t)kc * WRp + r) * 16, src ? src : xt, src ? 16u : 0u);
+        }
+      } else if (BF) {
         // fp32 window -> registers -> bf16 rows. A work item is one float4 (4
         // channels; consecutive threads read consecutive 16 B of a voxel row) that
         // lands as 8 bytes, half of a 16-byte chunk; eight loads in flight per thread.
@@ -781,6 +801,7 @@ int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, lo
   a.y = y;
   a.accumulate = accumulate;
   a.vec = y.cstride % 4 == 0 && ((uintptr_t)y.ptr & 15) == 0;
+  a.xtw = bf && x.bf16 && x.cstride % 8 == 0 && x.c % 8 == 0 && ((uintptr_t)x.bf16 & 15) == 0;
   int cols = 32;
   while (cols < a.T * a.Ns) cols *= 2;
   a.tmem_cols = cols;

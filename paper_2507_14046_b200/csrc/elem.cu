@@ -51,6 +51,7 @@ __global__ void __launch_bounds__(256) upsample2x_fwd_k(d2ip_act x, d2ip_act y) 
   const float v11 = lw.l0 * at(ld.i1, lh.i1, lw.i0) + lw.l1 * at(ld.i1, lh.i1, lw.i1);
   const float r = ld.l0 * (lh.l0 * v00 + lh.l1 * v01) + ld.l1 * (lh.l0 * v10 + lh.l1 * v11);
   y.ptr[b * y.bstride + v * y.cstride + c] = r;
+  if (y.bf16) reinterpret_cast<__nv_bfloat16*>(y.bf16)[b * y.bstride + v * y.cstride + c] = __float2bfloat16_rn(r);
 }
 
 // float4 variant: one thread per (voxel, 4 channels) -- a quarter of the index
@@ -87,6 +88,9 @@ __global__ void __launch_bounds__(256) upsample2x_fwd4_k(d2ip_act x, d2ip_act y)
   D2IP_UP(x) D2IP_UP(y) D2IP_UP(z) D2IP_UP(w)
 #undef D2IP_UP
   *reinterpret_cast<float4*>(y.ptr + b * y.bstride + v * y.cstride + c) = r;
+  if (y.bf16)
+    *reinterpret_cast<uint2*>(reinterpret_cast<uint16_t*>(y.bf16) + b * y.bstride + v * y.cstride + c) =
+        make_uint2(bf16x2(r.x, r.y), bf16x2(r.z, r.w));
 }
 
 static bool aligned4(const d2ip_act& a) { return a.c % 4 == 0 && a.cstride % 4 == 0 && ((uintptr_t)a.ptr & 15) == 0; }

@@ -118,6 +118,28 @@ static void config_plan_workspace(d2ip_engine& E, Arena& A) {
   saved(E.neck);
   for (auto& bl : E.dec) saved(bl);
   E.maxvc = maxvc;
+  // bf16 twins of every tensor a bf16 tensor-core convolution reads: block inputs
+  // (concat buffers, the last encoder output), h1, and the gradients gc1 / gc2 /
+  // gpre / stem gc; their producers (LayerNorm fwd/bwd, upsample) write both copies
+  if (E.d.precision == D2IP_PREC_BF16) {
+    auto twin = [&](float* p, long long n) {
+      void* t = A.take((size_t)n * 2);
+      if (p && t) E.twins.push_back({p, n, t});
+    };
+    for (int l = 0; l + 1 < L; ++l) twin(E.cat[l], (long long)B * E.V[l] * E.catw[l]);
+    twin(E.elast, (long long)B * E.V[L - 1] * c[L - 1]);
+    twin(E.stem_gc, (long long)B * E.V[0] * c[0]);
+    auto tw_block = [&](Block& bl) {
+      const long long vc = (long long)B * E.V[bl.lout] * bl.c1.cout;
+      twin(bl.h1, vc);
+      twin(bl.gc1, vc);
+      twin(bl.gc2, vc);
+      twin(bl.gpre, vc);
+    };
+    for (auto& bl : E.enc) tw_block(bl);
+    tw_block(E.neck);
+    for (auto& bl : E.dec) tw_block(bl);
+  }
   E.raw = takef(B * maxvc);
   E.raw2 = takef(B * maxvc);
   for (int i = 0; i < 5; ++i) E.sc[i] = takef(B * maxvc);
@@ -174,6 +196,7 @@ static void config_plan_workspace(d2ip_engine& E, Arena& A) {
 // Assign workspace pointers (base may be null: size query). Returns bytes.
 static size_t plan_workspace(d2ip_engine& E, char* base) {
   Arena A{base};
+  E.twins.clear();
   const int B = E.d.batch;
   if (E.d.arch == D2IP_ARCH_FAST_RESUNET)
     refnet_plan_workspace(E, A);

@@ -90,6 +90,14 @@ struct d2ip_engine {
   float* stem_gc = nullptr;
   float* stem_np = nullptr;
   d2ip::RefNet* ref = nullptr;  // arch == 1: FastResUNet3D program (refnet.cu)
+  // bf16 twins (precision BF16) of the buffers the tensor-core convolutions read:
+  // [base, base + n) fp32 elements <-> bf16 copy with the same element layout
+  struct Twin {
+    const float* base;
+    long long n;
+    void* tw;
+  };
+  std::vector<Twin> twins;
 };
 
 namespace d2ip {
@@ -108,8 +116,15 @@ struct Arena {
   size_t total() const { return (off + 255) & ~(size_t)255; }
 };
 
+inline void* twin_of(const d2ip_engine& E, const float* p) {
+  for (const auto& t : E.twins)
+    if (p >= t.base && p < t.base + t.n) return reinterpret_cast<uint16_t*>(t.tw) + (p - t.base);
+  return nullptr;
+}
+
 inline d2ip_act view(const d2ip_engine& E, float* p, int lvl, int c, int cs) {
   d2ip_act a;
+  a.bf16 = twin_of(E, p);
   a.ptr = p;
   a.d = E.D[lvl];
   a.h = E.H[lvl];

@@ -52,6 +52,19 @@ __device__ __forceinline__ void st(float* p, const float (&v)[VPL]) {
   for (int i = 0; i < VPL; i += 4) *reinterpret_cast<float4*>(p + i) = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
 }
 
+// bf16 twin of an fp32 row (round to nearest): VPL x 2 bytes
+template <int VPL>
+__device__ __forceinline__ void st_bf(const d2ip_act& a, long long off, const float (&v)[VPL]) {
+  uint32_t w[VPL / 2];
+#pragma unroll
+  for (int i = 0; i < VPL; i += 2) w[i / 2] = bf16x2(v[i], v[i + 1]);
+  uint16_t* p = reinterpret_cast<uint16_t*>(a.bf16) + off;
+  if (VPL == 4) *reinterpret_cast<uint2*>(p) = make_uint2(w[0], w[1]);
+  else
+#pragma unroll
+    for (int i = 0; i < VPL / 2; i += 4) *reinterpret_cast<uint4*>(p + 2 * i) = make_uint4(w[i], w[i + 1], w[i + 2], w[i + 3]);
+}
+
 template <int VPL>
 __global__ void __launch_bounds__(kNormThreads) norm_act_fwd_k(d2ip_act y, const float* __restrict__ gamma,
                                                                const float* __restrict__ beta, long long pbs,
@@ -122,6 +135,7 @@ __global__ void __launch_bounds__(kNormThreads) norm_act_fwd_k(d2ip_act y, const
       if (pre.ptr) st<VPL>(pre.ptr + b * pre.bstride + v * pre.cstride + c0, pr);
       st<VPL>(xhat + ((long long)b * V + v) * C + c0, xh);
       st<VPL>(out.ptr + b * out.bstride + v * out.cstride + c0, o);
+      if (out.bf16) st_bf<VPL>(out, b * out.bstride + v * out.cstride + c0, o);
       if (li == 0) rstd[b * V + v] = rs;
     }
   }
@@ -230,7 +244,9 @@ __global__ void __launch_bounds__(kNormThreads) norm_act_bwd_k(d2ip_act gout, d2
         cs2[i] += g[i];
       }
       if (gpre.ptr) st<VPL>(gpre.ptr + b * gpre.bstride + v * gpre.cstride + c0, g);
+      if (gpre.ptr && gpre.bf16) st_bf<VPL>(gpre, b * gpre.bstride + v * gpre.cstride + c0, g);
       st<VPL>(gc.ptr + b * gc.bstride + v * gc.cstride + c0, o);
+      if (gc.bf16) st_bf<VPL>(gc, b * gc.bstride + v * gc.cstride + c0, o);
     }
   }
   if (active) {

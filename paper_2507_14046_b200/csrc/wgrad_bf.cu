@@ -23,6 +23,7 @@
 // (deterministic, no atomics). The bias gradient is summed in fp32 from the
 // unconverted gy values by the CTAs of tap group 0 / channel block 0.
 #include <algorithm>
+#include <cstdlib>
 
 #include <cuda_bf16.h>
 
@@ -38,23 +39,42 @@ constexpr int kWbMaxStages = 4;
 
 struct WgBf {
   d2ip_act x, gy;
-  int Sw, Sh, u_first, u_last;
+  int Sw, Sh, u_first, u_last;  // virtual grid with an 8-row-aligned pitch (Sw % 8 == 0)
+  int v_start;        // first row of chunk 0 (8-aligned, <= u_first - 1)
   int ks, ntaps;
-  int G, ngroups;     // taps per CTA, tap groups
+  int nkh;            // kh accumulators per CTA: 3 (a kd plane) or 1 (a (kd, kh) row); 1^3: 1
+  int ngroups;        // tap groups (3 kd planes, 9 kd-kh rows, 1 for 1^3)
   int cib, ncib;      // input channels per block, blocks
-  int M, N;           // MMA shape
-  int ngx, ngg;       // 8-channel group columns per stage: x (>= M / 8, the MMA reads M / 8), gy (N / 8)
+  int M, N;           // MMA shape: N = 3 C_out (kw copies stacked) or C_out
+  int nmma;           // MMAs per kh per 16 rows: 1 (N = 3 C_out) or 3 (one per kw copy, N = C_out); 1^3: 1
+  int ncp;            // gy copies: 3 stacked kw-shifted copies (kd planes), or 1 unshifted copy of the
+                      // map rows whose B descriptors start bsh0 + c * bstep rows in (a 16-byte move)
+  int bsh0, bstep;    // single-copy B row shift of MMA c (kh rows: 2 - kw; one tap: 2 - kw; 1^3: 1)
+  int tapmode;        // one tap per CTA (C_out = 256: a kh row of 3 x 256 columns exceeds TMEM)
+  int ngx, ngc;       // 8-channel group columns: x (real), gy per copy
   int RS, WR, WRp, RSp;  // rows per stage (K chunk), x window rows, padded column lengths
+  int halo;           // x rows carried from the previous stage's window (2 Sw for kd planes)
   int NST;            // ring depth
   int nchunk, chunks_per_rg, nrg;
   int tmem_cols;
   int gshift;         // log2(C_out / 4): float4 pieces per gy row
   uint32_t Sx, Sb;    // bytes: x region of a stage, whole stage
+  uint32_t pad;       // bytes after the last stage the M = 64 MMA may read past a small x block
   uint32_t idesc;
-  float* part;        // [b][rg][ntaps][Cin][Cout] + [Cout] bias
+  int xtw, gtw;       // stream x / gy from their bf16 twins with cp.async (else fp32 loads + conversion)
+  int nyb;            // bias partial slots per row group (= CTAs sharing it: tap groups x channel blocks)
+  FastDiv fSh, fSw;   // row -> (plane, line, column) without integer division
+  int dbg;            // D2IP_WB_DBG=1: producers skip the fills (measures the MMA side alone; wrong results)
+  float* part;        // [b][rg][ntaps][Cin][Cout] + [nyb][Cout] bias
 };
 
-static inline int wb_pad(int rows) { return rows + ((1 - rows) % 8 + 8) % 8; }  // = 1 mod 8: spread banks
+__device__ __forceinline__ void cp_async16_ca(void* dst_smem, const void* src, uint32_t src_bytes) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16, %2;" ::"r"(tc::smem_u32(dst_smem)), "l"(src),
+               "r"(src_bytes)
+               : "memory");
+}
+
+static inline int r8(int v) { return (v + 7) & ~7; }
 
 __device__ __forceinline__ uint32_t bf2w(float a, float b) {
   const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
@@ -64,26 +84,29 @@ __device__ __forceinline__ uint32_t bf2w(float a, float b) {
 // voxel offset of virtual row u in a (D, H, W) grid, -1 for padding rows
 __device__ __forceinline__ int wb_voxel(const WgBf& a, int u, int D, int H, int W) {
   if (u < 0) return -1;
-  const int dp = u / a.Sh, r = u - dp * a.Sh;
-  const int hp = r / a.Sw, wp = r - hp * a.Sw;
+  const int dp = fdiv(u, a.fSh), r = u - dp * a.Sh;
+  const int hp = fdiv(r, a.fSw), wp = r - hp * a.Sw;
   if (dp < 1 || dp > D || hp < 1 || hp > H || wp < 1 || wp > W) return -1;
   return ((dp - 1) * H + (hp - 1)) * W + (wp - 1);
 }
 
-// row offset of the CTA's x window (relative to the chunk's first gy row) and
-// of tap q of the group inside it
+// Row offset (from the chunk's first row v0) of the CTA's x window: tap
+// (kd, kh, kw) pairs x row v + (kd-1) Sh + (kh-1) Sw with gy row v + 1 - kw
+// (the kw shift lives in the gy copies), so the window starts at the kd plane's
+// kh = 0 row (kd plane) or at the (kd, kh) row; always a multiple of 8.
 __device__ __forceinline__ int wb_base(const WgBf& a, int grp) {
   if (a.ks == 1) return 0;
-  if (a.G == 9) return (grp - 1) * a.Sh - a.Sw - 1;
-  if (a.G == 3) return (grp / 3 - 1) * a.Sh + (grp % 3 - 1) * a.Sw - 1;
-  return (grp / 9 - 1) * a.Sh + ((grp / 3) % 3 - 1) * a.Sw + (grp % 3 - 1);
-}
-__device__ __forceinline__ int wb_rel(const WgBf& a, int q) {
-  if (a.G == 9) return (q / 3) * a.Sw + (q % 3);
-  return q;  // G = 3: kw; G = 1: 0
+  if (a.tapmode) return (grp / 9 - 1) * a.Sh + ((grp / 3) % 3 - 1) * a.Sw;
+  if (a.nkh == 3) return (grp - 1) * a.Sh - a.Sw;
+  return (grp / 3 - 1) * a.Sh + (grp % 3 - 1) * a.Sw;
 }
 
-template <int NCX>  // float4 pieces per x row = cib / 4
+// NCX: float4 pieces per x row (cib / 4); NKH / NMMA: kh accumulators per CTA
+// and MMAs per kh (compile-time, so the issue loop is a fixed run of MMAs on
+// descriptors advanced by constant adds -- tools/umma_chains.cu measured a
+// general per-MMA descriptor computation at ~140-390 cycles per MMA, against
+// ~40 for the operand reads themselves).
+template <int NCX, int NKH, int NMMA>
 __global__ void __launch_bounds__(kWbThreads) wgrad_bf_k(WgBf a) {
   D2IP_PDL_ENTRY();
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -92,9 +115,10 @@ __global__ void __launch_bounds__(kWbThreads) wgrad_bf_k(WgBf a) {
   const int grp = blockIdx.y % a.ngroups, cb = blockIdx.y / a.ngroups;
   const int b = blockIdx.z;
   const int WR = a.WR, RS = a.RS, WRp = a.WRp, RSp = a.RSp, NST = a.NST;
-  // layout: NST stages [x groups][gy groups], row maps [2][WR + RS], barriers, TMEM slot, bias scratch
-  int* rmap = reinterpret_cast<int*>(smem + (size_t)NST * a.Sb);
-  uint64_t* full = reinterpret_cast<uint64_t*>(rmap + 2 * (WR + RS) + ((2 * (WR + RS)) & 1));
+  const int NM = RS + 2;  // gy row map: rows v0 - 1 .. v0 + RS
+  // layout: NST stages [x groups][gy copies x groups] (+ pad), row maps [2][WR + NM], barriers, TMEM slot, bias scratch
+  int* rmap = reinterpret_cast<int*>(smem + (size_t)NST * a.Sb + a.pad);
+  uint64_t* full = reinterpret_cast<uint64_t*>(rmap + 2 * (WR + NM) + ((2 * (WR + NM)) & 1));
   uint64_t* empty = full + kWbMaxStages;
   uint64_t* done = empty + kWbMaxStages;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
@@ -103,7 +127,7 @@ __global__ void __launch_bounds__(kWbThreads) wgrad_bf_k(WgBf a) {
   if (warp == 0) tc::tmem_alloc(tslot, a.tmem_cols);
   if (tid == 0) {
     for (int i = 0; i < NST; ++i) {
-      tc::mbar_init(&full[i], kWbProd);
+      tc::mbar_init(&full[i], 2 * kWbProd);  // async (copies landed) + plain (halo carry done) per thread
       tc::mbar_init(&empty[i], 1);
     }
     tc::mbar_init(done, 1);
@@ -116,28 +140,41 @@ __global__ void __launch_bounds__(kWbThreads) wgrad_bf_k(WgBf a) {
   const int c_lo = rg * a.chunks_per_rg;
   const int S = min(a.nchunk, c_lo + a.chunks_per_rg) - c_lo;  // this CTA's chunks
   const int base = wb_base(a, grp);
-  const int Gq = a.G;
+  constexpr int nkh = NKH, nmma = NMMA;
 
   if (warp == 0) {
-    // ---- MMA issue: the whole warp walks the loop, one elected lane issues
-    const uint32_t sbase = tc::smem_u32(smem);
-    for (int s = 0; s < S; ++s) {
-      const int slot = s % NST;
-      tc::mbar_wait(&full[slot], (uint32_t)((s / NST) & 1));
-      tc::fence_after();
-      const uint32_t xs = sbase + slot * a.Sb, gs = xs + a.Sx;
-      for (int k16 = 0; k16 < RS / 16; ++k16) {
-        const uint64_t db = tc::make_desc(gs + k16 * 256, 128, RSp * 16);
-        for (int q = 0; q < Gq; ++q) {
-          const uint64_t da = tc::make_desc(xs + (k16 * 16 + wb_rel(a, q)) * 16, 128, WRp * 16);
-          tc::mma_f16_warp(tmem + (uint32_t)(q * a.N), da, db, a.idesc, (s | k16) ? 1u : 0u);
+    // ---- MMA issue: one thread; descriptors advance by constant adds to the
+    // start-address field (units of 16 B). Every operand block is 128-byte
+    // aligned (8-row pitch, 8-aligned windows).
+    if (lane == 0) {
+      const uint32_t sbase = tc::smem_u32(smem);
+      const uint64_t dA0 = tc::make_desc(sbase, 128, WRp * 16);
+      const uint64_t dB0 = tc::make_desc(sbase + a.Sx, 128, RSp * 16);
+      const uint32_t cpy16 = ((uint32_t)a.ngc * RSp * 16) >> 4;  // one gy copy
+      const uint32_t sw16 = (uint32_t)a.Sw;                       // one kh row: Sw rows x 16 B
+      const uint32_t idesc = a.idesc, N = a.N;
+      const bool stacked = a.ncp == 3;
+      const int bsh = a.tapmode ? 2 - grp % 3 : a.bsh0;  // single copy: B starts bsh rows into the map rows
+      for (int s = 0; s < S; ++s) {
+        const int slot = s % NST;
+        tc::mbar_wait(&full[slot], (uint32_t)((s / NST) & 1));
+        tc::fence_after();
+        tc::fence_proxy_async();
+        const uint64_t so = (uint64_t)((slot * a.Sb) >> 4);
+        for (int k16 = 0; k16 < RS / 16; ++k16) {
+          const uint64_t da = dA0 + so + (uint64_t)(k16 * 16), db = dB0 + so + (uint64_t)(k16 * 16);
+          const uint32_t acc = (s | k16) ? 1u : 0u;
+#pragma unroll
+          for (int kh = 0; kh < NKH; ++kh)
+#pragma unroll
+            for (int c = 0; c < NMMA; ++c)
+              tc::mma_f16(tmem + (uint32_t)(kh * NMMA + c) * N, da + (uint64_t)(kh * sw16),
+                          db + (uint64_t)(stacked ? c * cpy16 : bsh + c * a.bstep), idesc, acc);
         }
+        tc::commit(&empty[slot]);
       }
-      __syncwarp();
-      if (lane == 0) tc::commit(&empty[slot]);
-      __syncwarp();
+      if (S > 0) tc::commit(done);
     }
-    if (lane == 0 && S > 0) tc::commit(done);
     __syncwarp();
   } else {
     // ---- producers
@@ -146,54 +183,96 @@ __global__ void __launch_bounds__(kWbThreads) wgrad_bf_k(WgBf a) {
     const float* xb = x.ptr + b * x.bstride + cb * a.cib;
     const float* gb = gy.ptr + b * gy.bstride;
     const int gmask = (1 << a.gshift) - 1;
-    const bool do_bias = blockIdx.y == 0;
+    // the bias of chunk c is summed (fp32) by the CTA with blockIdx.y == c % nyb: balanced, fixed order
+    const int ybias = blockIdx.y;
+    const int ncp = a.ncp;
+    const uint32_t cpy = (uint32_t)a.ngc * RSp * 16;
     float4 bsum = make_float4(0.f, 0.f, 0.f, 0.f);
     for (int s = 0; s < S; ++s) {
       const int slot = s % NST;
       if (s >= NST) tc::mbar_wait(&empty[slot], (uint32_t)(((s / NST) - 1) & 1));
-      const int u0 = a.u_first + (c_lo + s) * RS;
-      int* rm = rmap + (s & 1) * (WR + RS);
-      for (int r = gtid; r < WR + RS; r += kWbProd) {
-        int off;
-        if (r < WR) off = wb_voxel(a, u0 + base + r, x.d, x.h, x.w);
-        else {
-          const int u = u0 + (r - WR);
-          off = u > a.u_last ? -1 : wb_voxel(a, u, gy.d, gy.h, gy.w);
+      if (a.dbg) {
+        tc::mbar_arrive(&full[slot]);
+        tc::mbar_arrive(&full[slot]);
+        continue;
+      }
+      const int v0 = a.v_start + (c_lo + s) * RS;
+      const bool carry = s > 0 && a.halo > 0;  // first `halo` x rows = the previous window's last rows
+      const int xr0 = carry ? a.halo : 0;
+      int* rm = rmap + (s & 1) * (WR + NM);
+      for (int r = gtid; r < WR + NM; r += kWbProd) {
+        int off = -1;
+        if (r < WR) {
+          if (r >= xr0) off = wb_voxel(a, v0 + base + r, x.d, x.h, x.w);
+        } else {
+          const int u = v0 - 1 + (r - WR);
+          off = (u < a.u_first || u > a.u_last) ? -1 : wb_voxel(a, u, gy.d, gy.h, gy.w);
         }
         rm[r] = off;
       }
       asm volatile("bar.sync 1, 256;" ::: "memory");
       uint8_t* X = smem + (size_t)slot * a.Sb;
       uint8_t* Gs = X + a.Sx;
-      // x window: WR rows x NCX float4 pieces -> bf16 halves of 16-byte group rows
+      // x window rows [xr0, WR): NCX float4 pieces per row -> bf16 halves of 16-byte group rows
       constexpr int NP = NCX;
-      const int nX = WR * NP;
-      for (int i0 = gtid; i0 < nX; i0 += 8 * kWbProd) {
-        float4 v[8];
+      const int nX = a.xtw ? 0 : (WR - xr0) * NP;
+      if (a.xtw) {  // bf16 twin: one 16-byte async copy per (row, 8-channel group), zero-fill for padding rows
+        const uint16_t* xt = reinterpret_cast<const uint16_t*>(x.bf16) + b * x.bstride + cb * a.cib;
+        constexpr int NGX = NCX / 2;
+        const int n16 = (WR - xr0) * NGX;
+        for (int i = gtid; i < n16; i += kWbProd) {
+          const int r = xr0 + i / NGX, g = i % NGX;
+          const int off = rm[r];
+          tc::cp_async16(X + ((size_t)g * WRp + r) * 16, off >= 0 ? xt + (long long)off * x.cstride + 8 * g : xt,
+                         off >= 0 ? 16u : 0u);
+        }
+      }
+      for (int i0 = gtid; i0 < nX; i0 += 16 * kWbProd) {
+        float4 v[16];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
+        for (int q = 0; q < 16; ++q) {
           const int i = i0 + q * kWbProd;
           v[q] = make_float4(0.f, 0.f, 0.f, 0.f);
           if (i < nX) {
-            const int off = rm[i / NP];
+            const int off = rm[xr0 + i / NP];
             if (off >= 0) v[q] = *reinterpret_cast<const float4*>(xb + (long long)off * x.cstride + 4 * (i % NP));
           }
         }
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
+        for (int q = 0; q < 16; ++q) {
           const int i = i0 + q * kWbProd;
           if (i >= nX) continue;
-          const int r = i / NP, pc = i % NP;
+          const int r = xr0 + i / NP, pc = i % NP;
           *reinterpret_cast<uint2*>(X + ((size_t)(pc >> 1) * WRp + r) * 16 + (pc & 1) * 8) =
               make_uint2(bf2w(v[q].x, v[q].y), bf2w(v[q].z, v[q].w));
         }
       }
-      // gy rows: RS x (C_out / 4) pieces; the bias sum takes the fp32 values
-      const int nG = RS << a.gshift;
-      for (int i0 = gtid; i0 < nG; i0 += 8 * kWbProd) {
-        float4 v[8];
+      // gy map rows m = 0 .. RS + 1 (row v0 - 1 + m); copy c row j = map row j + 2 - c
+      // (1^3: one copy, row j = map row j + 1). The bias sum counts rows m = 1 .. RS once.
+      const bool bias_here = (c_lo + s) % a.nyb == ybias;
+      if (a.gtw) {  // bf16 twin: the kw copies are three async copies of the same 16 bytes (L1-allocating)
+        const uint16_t* gt = reinterpret_cast<const uint16_t*>(gy.bf16) + b * gy.bstride;
+        const int cs = a.gshift - 1;  // log2(C_out / 8): 8-channel groups per gy row
+        const int n16 = NM << cs;
+        for (int i = gtid; i < n16; i += kWbProd) {
+          const int m = i >> cs, g = i & ((1 << cs) - 1);
+          const int off = rm[WR + m];
+          const uint16_t* src = off >= 0 ? gt + (long long)off * gy.cstride + 8 * g : gt;
+          if (ncp == 1) {
+            tc::cp_async16(Gs + ((size_t)g * RSp + m) * 16, src, off >= 0 ? 16u : 0u);
+          } else {
+            for (int c = 0; c < ncp; ++c) {
+              const int j = m + c - 2;
+              if (j >= 0 && j < RS) cp_async16_ca(Gs + c * cpy + ((size_t)g * RSp + j) * 16, src, off >= 0 ? 16u : 0u);
+            }
+          }
+        }
+      }
+      const int nG = (!a.gtw || bias_here) ? NM << a.gshift : 0;
+      for (int i0 = gtid; i0 < nG; i0 += 16 * kWbProd) {
+        float4 v[16];
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
+        for (int q = 0; q < 16; ++q) {
           const int i = i0 + q * kWbProd;
           v[q] = make_float4(0.f, 0.f, 0.f, 0.f);
           if (i < nG) {
@@ -202,15 +281,36 @@ __global__ void __launch_bounds__(kWbThreads) wgrad_bf_k(WgBf a) {
           }
         }
 #pragma unroll
-        for (int q = 0; q < 8; ++q) {
+        for (int q = 0; q < 16; ++q) {
           const int i = i0 + q * kWbProd;
           if (i >= nG) continue;
-          const int r = i >> a.gshift, pc = i & gmask;
-          if (do_bias) {
+          const int m = i >> a.gshift, pc = i & gmask;
+          if (bias_here && m >= 1 && m <= RS) {
             bsum.x += v[q].x; bsum.y += v[q].y; bsum.z += v[q].z; bsum.w += v[q].w;
           }
-          *reinterpret_cast<uint2*>(Gs + ((size_t)(pc >> 1) * RSp + r) * 16 + (pc & 1) * 8) =
-              make_uint2(bf2w(v[q].x, v[q].y), bf2w(v[q].z, v[q].w));
+          if (a.gtw) continue;  // fp32 pass for the bias only
+          const uint2 o = make_uint2(bf2w(v[q].x, v[q].y), bf2w(v[q].z, v[q].w));
+          for (int c = 0; c < ncp; ++c) {
+            const int j = ncp == 1 ? m : m + c - 2;
+            if (j >= 0 && j < (ncp == 1 ? NM : RS))
+              *reinterpret_cast<uint2*>(Gs + c * cpy + ((size_t)(pc >> 1) * RSp + j) * 16 + (pc & 1) * 8) = o;
+          }
+        }
+      }
+      // two arrivals per producer thread and stage: an async one when this
+      // thread's copies have landed (no wait here: later stages' copies are
+      // issued while these fly), and a plain one after the halo carry, which
+      // first waits for the previous stage's window to land
+      asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(tc::smem_u32(&full[slot])) : "memory");
+      if (carry) {
+        tc::mbar_wait(&full[(s - 1) % NST], (uint32_t)(((s - 1) / NST) & 1));
+        // halo carry: x rows [RS, RS + halo) of the previous stage's window are rows [0, halo) of this one
+        const uint8_t* Xp = smem + (size_t)((s - 1) % NST) * a.Sb;
+        const int n16 = a.ngx * a.halo;
+        for (int i = gtid; i < n16; i += kWbProd) {
+          const int g = i / a.halo, r = i - g * a.halo;
+          *reinterpret_cast<uint4*>(X + ((size_t)g * WRp + r) * 16) =
+              *reinterpret_cast<const uint4*>(Xp + ((size_t)g * WRp + RS + r) * 16);
         }
       }
       tc::fence_proxy_async();
@@ -219,7 +319,7 @@ __global__ void __launch_bounds__(kWbThreads) wgrad_bf_k(WgBf a) {
 
     // ---- epilogue: TMEM -> per-row-group partials [t][ci][co]
     const int Cin = x.c, Cout = gy.c;
-    float* pb = a.part + ((long long)b * a.nrg + rg) * ((long long)a.ntaps * Cin * Cout + Cout);
+    float* pb = a.part + ((long long)b * a.nrg + rg) * ((long long)a.ntaps * Cin * Cout + (long long)a.nyb * Cout);
     if (S > 0) {
       tc::mbar_wait(done, 0);
       tc::fence_after();
@@ -232,20 +332,31 @@ __global__ void __launch_bounds__(kWbThreads) wgrad_bf_k(WgBf a) {
     const int ci = cb * a.cib + m;
     const bool live = m >= 0 && m < a.cib;
     const uint32_t trow = tmem + ((uint32_t)(quad * 32) << 16);
-    const int nck = (Gq * a.N) / 8;
-    for (int c = half; c < nck; c += 2) {
+    // accumulator columns: kh block of 3 C_out (kw copy c = kw, then co)
+    const int nck = (nkh * 3 * Cout) / 8;
+    const int nck_all = (a.ks == 1 || a.tapmode) ? Cout / 8 : nck;
+    for (int c8 = half; c8 < nck_all; c8 += 2) {
       float vals[8];
-      tc::tmem_ld8(trow + (uint32_t)(c * 8), vals);
-      const int q = (c * 8) / a.N, n = (c * 8) % a.N;
-      if (!live || n >= Cout) continue;
-      const int t = a.ks == 1 ? 0 : (Gq == 9 ? grp * 9 + q : Gq == 3 ? grp * 3 + q : grp);
+      tc::tmem_ld8(trow + (uint32_t)(c8 * 8), vals);
+      const int col = c8 * 8;
+      int t, n;
+      if (a.ks == 1 || a.tapmode) {
+        t = a.ks == 1 ? 0 : grp;
+        n = col;
+      } else {
+        const int khl = col / (3 * Cout), rem = col - khl * 3 * Cout, kw = rem / Cout;
+        n = rem - kw * Cout;
+        const int kd = nkh == 3 ? grp : grp / 3, kh = nkh == 3 ? khl : grp % 3;
+        t = kd * 9 + kh * 3 + kw;
+      }
+      if (!live) continue;
       float4* dst = reinterpret_cast<float4*>(pb + ((long long)t * Cin + ci) * Cout + n);
       const bool z = S <= 0;
       dst[0] = z ? make_float4(0.f, 0.f, 0.f, 0.f) : make_float4(vals[0], vals[1], vals[2], vals[3]);
       dst[1] = z ? make_float4(0.f, 0.f, 0.f, 0.f) : make_float4(vals[4], vals[5], vals[6], vals[7]);
     }
-    if (do_bias) {
-      // fixed-order sum of the per-thread partials (thread gtid always held piece gtid % (C_out / 4))
+    {
+      // fixed-order sum of the per-thread partials (thread gtid always held piece gtid % (C_out / 4)) into slot y
       bscr[gtid] = bsum;
       asm volatile("bar.sync 1, 256;" ::: "memory");
       const int np = 1 << a.gshift;
@@ -255,7 +366,7 @@ __global__ void __launch_bounds__(kWbThreads) wgrad_bf_k(WgBf a) {
           const float4 v = bscr[j];
           s4.x += v.x; s4.y += v.y; s4.z += v.z; s4.w += v.w;
         }
-        *reinterpret_cast<float4*>(pb + (long long)a.ntaps * Cin * Cout + 4 * gtid) = s4;
+        *reinterpret_cast<float4*>(pb + (long long)a.ntaps * Cin * Cout + (long long)ybias * Cout + 4 * gtid) = s4;
       }
     }
   }
@@ -265,8 +376,8 @@ __global__ void __launch_bounds__(kWbThreads) wgrad_bf_k(WgBf a) {
 }
 
 static size_t wb_smem(const WgBf& a) {
-  return (size_t)a.NST * a.Sb + 2 * (size_t)(a.WR + a.RS) * sizeof(int) + 16 + (2 * kWbMaxStages + 1) * 8 + 16 +
-         kWbProd * 16 + 64;
+  return (size_t)a.NST * a.Sb + a.pad + 2 * (size_t)(a.WR + a.RS + 2) * sizeof(int) + 16 +
+         (2 * kWbMaxStages + 1) * 8 + 16 + kWbProd * 16 + 64;
 }
 
 static bool pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
@@ -275,10 +386,11 @@ static bool wb_plan(int D, int H, int W, int Cin, int Cout, int ks, int batch, W
   if ((ks != 1 && ks != 3) || Cout < 16 || Cout > 256 || !pow2(Cout) || Cin % 8 || Cin < 8) return false;
   a.ks = ks;
   a.ntaps = ks == 3 ? 27 : 1;
-  a.Sw = W + 2;
+  a.Sw = r8(W + 2);  // 8-row pitch: every kh / kd shift keeps MMA operand blocks 128-byte aligned
   a.Sh = (H + 2) * a.Sw;
   a.u_first = a.Sh + a.Sw + 1;
   a.u_last = D * a.Sh + H * a.Sw + W;
+  a.v_start = (a.u_first - 1) & ~7;
   // input-channel block: <= 128 rows of the MMA; 96 fills an M = 128 MMA three quarters
   a.ncib = 1;
   while (Cin / a.ncib > 128 || Cin % a.ncib || (Cin / a.ncib) % 8) ++a.ncib;
@@ -286,25 +398,61 @@ static bool wb_plan(int D, int H, int W, int Cin, int Cout, int ks, int batch, W
   const int ncx = a.cib / 4;
   if (ncx != 2 && ncx != 4 && ncx != 8 && ncx != 12 && ncx != 16 && ncx != 24 && ncx != 32) return false;
   a.M = a.cib <= 64 ? 64 : 128;
-  a.N = Cout;
-  a.G = ks == 1 ? 1 : (9 * a.N <= 512 ? 9 : (3 * a.N <= 512 ? 3 : 1));
-  a.ngroups = a.ntaps / a.G;
+  a.tapmode = 0;
+  a.bstep = 0;
+  a.bsh0 = 0;
+  if (ks == 1) {
+    a.nkh = 1;
+    a.ngroups = 1;
+    a.ncp = 1;
+    a.nmma = 1;
+    a.N = Cout;
+    a.bsh0 = 1;  // map row m = row v0 - 1 + m
+  } else if (9 * Cout <= 512) {
+    // kd plane: three kh accumulators of 3 C_out columns, the kw copies stacked along N
+    a.nkh = 3;
+    a.ncp = 3;
+    a.nmma = 1;
+    a.N = 3 * Cout;
+    a.ngroups = 3;
+  } else if (3 * Cout <= 512) {
+    // (kd, kh) row: three MMAs (one per kw) on one gy copy, B started 2 - kw rows in
+    a.nkh = 1;
+    a.ncp = 1;
+    a.nmma = 3;
+    a.N = Cout;
+    a.bsh0 = 2;
+    a.bstep = -1;
+    a.ngroups = 9;
+  } else {
+    a.nkh = 1;
+    a.ncp = 1;
+    a.nmma = 1;
+    a.N = Cout;
+    a.tapmode = 1;
+    a.ngroups = 27;
+  }
   int cols = 32;
-  while (cols < a.G * a.N) cols *= 2;
+  while (cols < a.nkh * a.nmma * a.N) cols *= 2;
   a.tmem_cols = cols;
-  a.ngx = std::max(a.cib / 8, a.M / 8);
-  a.ngg = a.N / 8;
+  if (cols > 512) return false;
+  a.ngx = a.cib / 8;
+  a.ngc = Cout / 8;
   a.gshift = 0;
   while ((4 << a.gshift) < Cout) ++a.gshift;
-  const int halo = ks == 1 || a.G == 1 ? 0 : (a.G == 9 ? 2 * a.Sw + 2 : 2);
-  const int rows = a.u_last - a.u_first + 1;
+  a.halo = (ks == 3 && a.nkh == 3) ? 2 * a.Sw : 0;
+  const int rows = a.u_last + 2 - a.v_start;  // chunks cover v_start .. u_last + 1
   a.RS = 0;
-  // the largest chunk (amortises the x halo) that double-buffers in ~200 KB; then up to 4 stages
-  for (int rs : {1024, 768, 512, 384, 256, 128, 64, 32, 16}) {
+  // the largest chunk that double-buffers in ~200 KB; then a third stage if it fits
+  for (int rs : {1024, 768, 512, 384, 256, 192, 128, 64, 32, 16}) {
     if (rs > 16 && rs / 2 >= rows) continue;
-    const int wr = rs + halo;
-    const int wrp = wb_pad(wr), rsp = wb_pad(rs);
-    const uint32_t sx = (uint32_t)a.ngx * wrp * 16, sb = ((sx + (uint32_t)a.ngg * rsp * 16) + 1023) & ~1023u;
+    const int wr = rs + a.halo;
+    const int wrp = r8(wr), rsp = r8(a.ncp == 1 ? rs + 2 : rs);  // single copy: all RS + 2 map rows
+    const uint32_t sx = (uint32_t)a.ngx * wrp * 16;
+    const uint32_t sb = ((sx + (uint32_t)a.ncp * a.ngc * rsp * 16) + 1023) & ~1023u;
+    // the M = 64 / 128 MMA reads M / 8 group columns: past a smaller x block into the stage's gy copies or the pad
+    const long long over = (long long)(a.M / 8 - a.ngx) * wrp * 16 - (long long)(sb - sx);
+    a.pad = over > 0 ? (uint32_t)((over + 1023) & ~1023LL) : 0;
     a.WR = wr;
     a.RS = rs;
     a.WRp = wrp;
@@ -312,11 +460,11 @@ static bool wb_plan(int D, int H, int W, int Cin, int Cout, int ks, int batch, W
     a.Sx = sx;
     a.Sb = sb;
     a.NST = 2;
-    if (wb_smem(a) > (size_t)200 * 1024) {
+    if (wb_smem(a) > (size_t)205 * 1024) {
       a.RS = 0;
       continue;
     }
-    while (a.NST < 3 && (a.NST + 1) * (size_t)sb + wb_smem(a) - a.NST * (size_t)sb <= (size_t)200 * 1024) ++a.NST;
+    if (wb_smem(a) + sb <= (size_t)205 * 1024) a.NST = 3;
     break;
   }
   if (!a.RS) return false;
@@ -328,7 +476,35 @@ static bool wb_plan(int D, int H, int W, int Cin, int Cout, int ks, int batch, W
   a.chunks_per_rg = cdiv(a.nchunk, nrg);
   a.nrg = cdiv(a.nchunk, a.chunks_per_rg);
   a.idesc = tc::make_idesc(1, a.M, a.N) | (1u << 15) | (1u << 16);  // bf16, A and B MN-major
-  return true;
+  a.nyb = a.ngroups * a.ncib;
+  a.fSh = fastdiv((uint32_t)a.Sh);
+  a.fSw = fastdiv((uint32_t)a.Sw);
+  return a.Sh < (1 << 14) && a.u_last + 2 * a.Sh < (1 << 28);  // fdiv range
+}
+
+// dW[b] = sum_rg part[b][rg] (weights, [t][ci][co] -> OIDHW), db = sum_rg sum_y bias slots (fixed order)
+__global__ void __launch_bounds__(256) wgrad_bf_reduce_k(const float* __restrict__ part, int nrg, int nyb, int ntaps,
+                                                         int Cin, int Cout, float* __restrict__ out, long long obs) {
+  D2IP_PDL_ENTRY();
+  const int b = blockIdx.y;
+  const long long nw = (long long)ntaps * Cin * Cout, blk = nw + (long long)nyb * Cout;
+  const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= nw + Cout) return;
+  const float* p = part + (long long)b * nrg * blk;
+  float s = 0.f;
+  if (e < nw) {
+#pragma unroll 8
+    for (int r = 0; r < nrg; ++r) s += __ldg(p + (long long)r * blk + e);
+    const int co = (int)(e % Cout);
+    const long long q = e / Cout;
+    const int ci = (int)(q % Cin), t = (int)(q / Cin);
+    out[b * obs + ((long long)co * Cin + ci) * ntaps + t] = s;
+  } else {
+    const int co = (int)(e - nw);
+    for (int r = 0; r < nrg; ++r)
+      for (int y = 0; y < nyb; ++y) s += p[(long long)r * blk + nw + (long long)y * Cout + co];
+    out[b * obs + nw + co] = s;
+  }
 }
 
 bool wgrad_bf_supported(d2ip_act x, d2ip_act gy, int ks) {
@@ -341,18 +517,26 @@ bool wgrad_bf_supported(d2ip_act x, d2ip_act gy, int ks) {
 size_t wgrad_bf_ws_bytes(int D, int H, int W, int Cin, int Cout, int ks, int batch) {
   WgBf a{};
   if (!wb_plan(D, H, W, Cin, Cout, ks, batch, a)) return 0;
-  return (size_t)batch * a.nrg * ((size_t)a.ntaps * Cin * Cout + Cout) * sizeof(float);
+  return (size_t)batch * a.nrg * ((size_t)a.ntaps * Cin * Cout + (size_t)a.nyb * Cout) * sizeof(float);
+}
+
+template <int NCX, int NKH, int NMMA>
+static int wb_launch3(const WgBf& a, dim3 grid, size_t smem, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    D2IP_CUDA(cudaFuncSetAttribute(wgrad_bf_k<NCX, NKH, NMMA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   227 * 1024));
+    attr = true;
+  }
+  D2IP_CUDA(launch_pdl(wgrad_bf_k<NCX, NKH, NMMA>, grid, kWbThreads, smem, st, a));
+  return D2IP_OK;
 }
 
 template <int NCX>
 static int wb_launch(const WgBf& a, dim3 grid, size_t smem, cudaStream_t st) {
-  static bool attr = false;
-  if (!attr) {
-    D2IP_CUDA(cudaFuncSetAttribute(wgrad_bf_k<NCX>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
-    attr = true;
-  }
-  D2IP_CUDA(launch_pdl(wgrad_bf_k<NCX>, grid, kWbThreads, smem, st, a));
-  return D2IP_OK;
+  if (a.nkh == 3) return wb_launch3<NCX, 3, 1>(a, grid, smem, st);
+  if (a.nmma == 3) return wb_launch3<NCX, 1, 3>(a, grid, smem, st);
+  return wb_launch3<NCX, 1, 1>(a, grid, smem, st);
 }
 
 int wgrad_bf(d2ip_act x, d2ip_act gy, int ks, float* gw, long long gwbs, void* ws, size_t ws_bytes, int batch,
@@ -363,6 +547,16 @@ int wgrad_bf(d2ip_act x, d2ip_act gy, int ks, float* gw, long long gwbs, void* w
   a.x = x;
   a.gy = gy;
   a.part = reinterpret_cast<float*>(ws);
+  auto twin_ok = [](const d2ip_act& t, int c0) {
+    return t.bf16 && t.cstride % 8 == 0 && c0 % 8 == 0 && ((uintptr_t)t.bf16 & 15) == 0;
+  };
+  a.xtw = twin_ok(x, 0);
+  a.gtw = twin_ok(gy, 0);
+  static const int dbg = [] {
+    const char* v = getenv("D2IP_WB_DBG");
+    return v ? atoi(v) : 0;
+  }();
+  a.dbg = dbg;
   const size_t smem = wb_smem(a);
   const dim3 grid(a.nrg, a.ngroups * a.ncib, batch);
   switch (a.cib / 4) {
@@ -376,7 +570,11 @@ int wgrad_bf(d2ip_act x, d2ip_act gy, int ks, float* gw, long long gwbs, void* w
     default: D2IP_CHECK_ARG(false, "wgrad_bf: channel block %d unsupported", a.cib);
   }
   D2IP_LAUNCH_CHECK();
-  return wgrad_reduce(a.part, a.nrg, a.ntaps, x.c, gy.c, gw, gwbs, batch, st);
+  const long long n = (long long)a.ntaps * x.c * gy.c + gy.c;
+  D2IP_CUDA(launch_pdl(wgrad_bf_reduce_k, dim3(cdiv(n, 256), batch), 256, 0, st, a.part, a.nrg, a.nyb, a.ntaps, x.c,
+                       gy.c, gw, gwbs));
+  D2IP_LAUNCH_CHECK();
+  return D2IP_OK;
 }
 
 }  // namespace d2ip

@@ -39,10 +39,17 @@ def from_ndhwc(t):
     return t.permute(0, 4, 1, 2, 3).contiguous().cpu()
 
 
-def act_of(t, c=None, coff=0):
+_TWINS = []  # keep bf16 twins alive for the duration of a call
+
+
+def act_of(t, c=None, coff=0, twin=False):
     B, D, H, W, CS = t.shape
     a = N.Act()
     a.ptr = t.data_ptr() + coff * 4
+    if twin:  # bf16 twin with the same element layout (what the engine's producers write)
+        tw = t.to(torch.bfloat16)
+        _TWINS.append(tw)
+        a.bf16 = tw.data_ptr() + coff * 2
     a.d, a.h, a.w = D, H, W
     a.c = CS if c is None else c
     a.cstride = CS
@@ -76,6 +83,8 @@ CONV_CASES = [
     # 1^3 on the tensor cores (pointwise mode), large enough for T > 1 tiles
     (96, 32, 1, 1, (32, 32, 16)),
     (64, 64, 1, 1, (16, 16, 16)),
+    # C_out = 256: one tap per CTA in the bf16 weight gradient
+    (16, 256, 3, 1, (4, 4, 6)),
     # large grids (cfg2 / cfg4 scale tiles)
     (16, 32, 3, 1, (64, 64, 32)),
     (32, 16, 3, 1, (48, 48, 32)),
@@ -97,9 +106,11 @@ def bf16_tc(cin, cout, ks, stride, sp, dgrad):
     return s2_big(cin, cout, sp) and cin % 8 == 0 and (8 * cin if not dgrad else cout) % 16 == 0 and (not dgrad or cout % 8 == 0)
 
 
-@pytest.mark.parametrize("prec", ["fp32", "tf32", "bf16"])
+@pytest.mark.parametrize("prec", ["fp32", "tf32", "bf16", "bf16-twin"])
 @pytest.mark.parametrize("cin,cout,ks,stride,sp", CONV_CASES)
 def test_conv3d_fwd(cin, cout, ks, stride, sp, prec):
+    twin = prec == "bf16-twin"
+    prec = "bf16" if twin else prec
     torch.manual_seed(0)
     B = 2
     x = torch.randn(B, cin, *sp)
@@ -114,7 +125,7 @@ def test_conv3d_fwd(cin, cout, ks, stride, sp, prec):
     params = torch.cat([torch.cat([w[i].reshape(-1), b[i]]) for i in range(B)]).cuda()
     P = params.numel() // B
     out = torch.zeros(B, *ref.shape[2:], cout, device="cuda")
-    xa = act_of(xb, cin, pad)
+    xa = act_of(xb, cin, pad, twin=twin)
     ya = act_of(out)
     L = N.lib()
     wsn = L.d2ip_conv3d_ws_bytes(cin, cout, ks, stride, N.PREC[prec], B)
@@ -155,9 +166,11 @@ def bf16_wgrad_tc(cin, cout, stride):
     return cin // nb // 4 in (2, 4, 8, 12, 16, 24, 32)
 
 
-@pytest.mark.parametrize("prec", ["fp32", "tf32", "bf16"])
+@pytest.mark.parametrize("prec", ["fp32", "tf32", "bf16", "bf16-twin"])
 @pytest.mark.parametrize("cin,cout,ks,stride,sp", CONV_CASES)
 def test_conv3d_dgrad_wgrad(cin, cout, ks, stride, sp, prec, wgrad_variant):
+    twin = prec == "bf16-twin"
+    prec = "bf16" if twin else prec
     torch.manual_seed(1)
     B = 2
     x = torch.randn(B, cin, *sp, requires_grad=True)
@@ -172,7 +185,7 @@ def test_conv3d_dgrad_wgrad(cin, cout, ks, stride, sp, prec, wgrad_variant):
     gx = torch.full((B, *sp, cin), 7.0, device="cuda")
     wsn = N.lib().d2ip_conv3d_ws_bytes(cin, cout, ks, stride, N.PREC[prec], B)
     wsd = torch.empty(max(wsn, 16), dtype=torch.uint8, device="cuda")
-    N.check(N.lib().d2ip_conv3d_dgrad(act_of(gyd), C.c_void_p(params.data_ptr()), P, ks, stride, act_of(gx), 0,
+    N.check(N.lib().d2ip_conv3d_dgrad(act_of(gyd, twin=twin), C.c_void_p(params.data_ptr()), P, ks, stride, act_of(gx), 0,
                                       N.PREC[prec], C.c_void_p(wsd.data_ptr()), wsn, B, stream()), "dgrad")
     if prec == "tf32" and cout % 8 == 0 and cin % 8 == 0 and (stride == 1 or (ks == 3 and s2_big(cin, cout, sp))):
         assert N.lib().d2ip_last_variant().startswith(b"tcgen05_tf32x3")
@@ -182,7 +195,7 @@ def test_conv3d_dgrad_wgrad(cin, cout, ks, stride, sp, prec, wgrad_variant):
     gw = torch.zeros(B, P, device="cuda")
     ws_n = N.lib().d2ip_conv3d_wgrad_ws_bytes(act_of(xd), act_of(gyd), ks, B)
     ws = torch.empty(max(ws_n, 1), dtype=torch.uint8, device="cuda")
-    N.check(N.lib().d2ip_conv3d_wgrad(act_of(xd), act_of(gyd), ks, stride, C.c_void_p(gw.data_ptr()), P,
+    N.check(N.lib().d2ip_conv3d_wgrad(act_of(xd, twin=twin), act_of(gyd, twin=twin), ks, stride, C.c_void_p(gw.data_ptr()), P,
                                       C.c_void_p(ws.data_ptr()), ws_n, N.PREC[prec], B, stream()), "wgrad")
     torch.cuda.synchronize()
     if wgrad_variant == 1 and prec == "tf32" and stride == 1 and cin % 4 == 0 and cout % 4 == 0 and cout <= 128:

@@ -6,6 +6,7 @@ Prints the forward and data-gradient time for precision fp32 (the direct
 CUDA-core kernels) and tf32 (the tcgen05 kernels, weight pack included).
 """
 import ctypes as C
+import os
 import sys
 
 import torch
@@ -28,11 +29,19 @@ P = w.numel()
 V = Do * Ho * Wo
 
 
-def act(t, c, dims):
+twins = {}  # bf16 twins (the engine's bf16 layers carry them; TWIN=0 times the fp32-conversion path)
+USE_TWIN = os.environ.get("TWIN", "1") == "1"
+
+
+def act(t, c, dims, prec="fp32"):
     a = N.Act()
     a.ptr, a.c, a.cstride = t.data_ptr(), c, c
     a.d, a.h, a.w = dims
     a.bstride = dims[0] * dims[1] * dims[2] * c
+    if prec == "bf16" and USE_TWIN:
+        if t.data_ptr() not in twins:
+            twins[t.data_ptr()] = t.to(torch.bfloat16)
+        a.bf16 = twins[t.data_ptr()].data_ptr()
     return a
 
 
@@ -42,13 +51,13 @@ for prec in precs:
     ws = torch.empty(wsn, dtype=torch.uint8, device="cuda")
 
     def fwd():
-        N.check(L.d2ip_conv3d_fwd(act(x, cin, (Dd, Hd, Wd)), C.c_void_p(w.data_ptr()),
+        N.check(L.d2ip_conv3d_fwd(act(x, cin, (Dd, Hd, Wd), prec), C.c_void_p(w.data_ptr()),
                                   C.c_void_p(w.data_ptr() + 4 * cout * cin * 27), P, 3, stride,
                                   act(y, cout, (Do, Ho, Wo)), 0,
                                   N.PREC[prec], C.c_void_p(ws.data_ptr()), wsn, 1, st), "fwd")
 
     def dgrad():
-        N.check(L.d2ip_conv3d_dgrad(act(y, cout, (Do, Ho, Wo)), C.c_void_p(w.data_ptr()), P, 3, stride,
+        N.check(L.d2ip_conv3d_dgrad(act(y, cout, (Do, Ho, Wo), prec), C.c_void_p(w.data_ptr()), P, 3, stride,
                                     act(gx, cin, (Dd, Hd, Wd)), 0,
                                     N.PREC[prec], C.c_void_p(ws.data_ptr()), wsn, 1, st), "dgrad")
 
@@ -57,7 +66,7 @@ for prec in precs:
     wgs = torch.empty(wgn, dtype=torch.uint8, device="cuda")
 
     def wgrad():
-        N.check(L.d2ip_conv3d_wgrad(act(x, cin, (Dd, Hd, Wd)), act(y, cout, (Do, Ho, Wo)), 3, stride,
+        N.check(L.d2ip_conv3d_wgrad(act(x, cin, (Dd, Hd, Wd), prec), act(y, cout, (Do, Ho, Wo), prec), 3, stride,
                                     C.c_void_p(gw.data_ptr()), P, C.c_void_p(wgs.data_ptr()), wgn, N.PREC[prec], 1,
                                     st), "wgrad")
 

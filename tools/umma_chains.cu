@@ -107,12 +107,71 @@ static void run(int M, int N, int nw, long long* d, cudaEvent_t e0, cudaEvent_t 
          flops / (ms * 1e-3) / 1e12);
 }
 
-int main(int argc, char**) {
+
+// wgrad-shaped issue loop: M x N MN-major bf16 MMAs into `nacc` accumulators at
+// column stride `cstride`, A / B group strides sboa / sbob, the A start moving by
+// `ashift` bytes per MMA (tap shifts) -- isolates the operand / accumulator
+// layout costs of wgrad_bf.cu.
+__global__ void wg_shape_k(int M, int N, int nacc, int cstride, int sboa, int sbob, int ashift, int nmma,
+                           long long* cycles) {
+  extern __shared__ __align__(1024) uint8_t smem[];
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(smem + 200 * 1024);
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(mbar + 1);
+  if (threadIdx.x < 32) tc::tmem_alloc(tslot, 512);
+  if (threadIdx.x == 0) { tc::mbar_init(mbar, 1); tc::fence_mbar_init(); }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tslot;
+  long long t0 = clock64();
+  if (threadIdx.x < 32) {
+    const uint32_t idesc = tc::make_idesc(1, M, N) | (1u << 15) | (1u << 16);
+    const uint32_t sb = tc::smem_u32(smem);
+    for (int i = 0; i < nmma; ++i) {
+      const int a = i % nacc;
+      const uint64_t da = tc::make_desc(sb + ((i * ashift) & 32767), 128, sboa);
+      const uint64_t db = tc::make_desc(sb + 100 * 1024 + ((i & 7) * 256), 128, sbob);
+      tc::mma_f16_warp(tmem + (uint32_t)(a * cstride), da, db, idesc, i >= nacc ? 1u : 0u);
+    }
+    if (threadIdx.x == 0) tc::commit(mbar);
+    __syncwarp();
+    tc::mbar_wait(mbar, 0);
+  }
+  __syncthreads();
+  long long t2 = clock64();
+  if (blockIdx.x == 0 && threadIdx.x == 0) cycles[0] = t2 - t0;
+  tc::fence_before();
+  __syncthreads();
+  if (threadIdx.x < 32) tc::tmem_free(tmem, 512);
+}
+
+static void wg_shape(int M, int N, int nacc, int cstride, int sboa, int sbob, int ashift, long long* d) {
+  cudaFuncSetAttribute(wg_shape_k, cudaFuncAttributeMaxDynamicSharedMemorySize, 210 * 1024);
+  const int nmma = 3072;
+  wg_shape_k<<<148, 128, 205 * 1024>>>(M, N, nacc, cstride, sboa, sbob, ashift, nmma, d);
+  cudaError_t e = cudaDeviceSynchronize();
+  if (e != cudaSuccess) { printf("err %s\n", cudaGetErrorString(e)); exit(1); }
+  long long h;
+  cudaMemcpy(&h, d, 8, cudaMemcpyDeviceToHost);
+  printf("wgrad-shape M=%d N=%3d nacc=%d colstride=%3d SBO a/b=%5d/%5d A shift/MMA=%4d B: %.1f cyc/mma\n", M, N, nacc,
+         cstride, sboa, sbob, ashift, (double)h / nmma);
+}
+
+int main(int argc, char** argv) {
   long long* d;
   cudaMalloc(&d, 16);
   cudaEvent_t e0, e1;
   cudaEventCreate(&e0);
   cudaEventCreate(&e1);
+  if (argc > 1 && argv[1][0] == 'w') {
+    for (int ash : {0, 256, 16, 1568})
+      for (int cs : {96, 128}) wg_shape(64, 96, 3, cs, 7424, 4096, ash, d);
+    wg_shape(64, 96, 3, 128, 2048, 2048, 0, d);
+    wg_shape(64, 96, 1, 96, 7424, 4096, 256, d);
+    wg_shape(64, 32, 3, 32, 7424, 4096, 256, d);
+    wg_shape(128, 96, 3, 96, 7424, 4096, 256, d);
+    return 0;
+  }
   if (argc > 1) {  // operand-major comparison at the weight-gradient shapes
     for (int M : {64, 128})
       for (int N : {16, 32, 64, 128, 256})
