@@ -534,32 +534,68 @@ __global__ void conv_tc_pack_k(const float* __restrict__ w, long long wbs, int K
   out[b * obs + obs / 2 + i] = val - hi;  // lo half at the fixed offset the kernel reads (wlo)
 }
 
-// All layers' packs in one launch: blockIdx.x walks the concatenated job ranges.
+// All layers' packs in one launch, source-major: one thread per (co, ci)
+// weight vector reads its 27 contiguous taps (coalesced across the warp) and
+// scatters each into its packed slot(s); blockIdx.x walks the concatenated
+// job ranges. Slots no weight maps to (N / K padding, stride-2 parity combos
+// without a tap) are never written: they stay zero from the workspace clear.
+__device__ __forceinline__ void pack_put(float* out, long long obs, int code, int K, int Np, int t, int k, int n,
+                                         float val) {
+  if (code & kTcBf16) {
+    const long long i = (((long long)t * (K / 8) + k / 8) * Np + n) * 8 + (k & 7);
+    reinterpret_cast<__nv_bfloat16*>(out)[i] = __float2bfloat16_rn(val);
+  } else {
+    const long long i = (((long long)t * (K / 4) + k / 4) * Np + n) * 4 + (k & 3);
+    const float hi = tf32_hi(val);
+    out[i] = hi;
+    out[obs / 2 + i] = val - hi;
+  }
+}
+
+// stride-2 parity decomposition, per axis: source tap k -> (parity, GEMM tap)
+// forward: k = 0 -> (1, 0), 1 -> (0, 1), 2 -> (1, 1); dgrad: 0 -> (1, 2), 1 -> (0, 1), 2 -> (1, 1)
+__device__ __forceinline__ void s2_inv(int k, int dgrad, int* p, int* ta) {
+  *p = k != 1;
+  *ta = k == 0 ? (dgrad ? 2 : 0) : 1;
+}
+
 __global__ void conv_tc_pack_multi_k(PackJobs j) {
   D2IP_PDL_ENTRY();
   const int b = blockIdx.y;
   int q = 0;
   while (q + 1 < j.n && blockIdx.x >= j.block0[q + 1]) ++q;
-  const long long half = j.half[q];
+  const int cin = j.cin[q], cout = j.cout[q];
   const long long i = (long long)(blockIdx.x - j.block0[q]) * blockDim.x + threadIdx.x;
-  if (i >= half) return;
-  const int K = j.K[q], N = j.N[q], Np = np_of(N);
-  if (j.dgrad[q] & kTcBf16) {
-    pack_bf16(j.w[q] + b * j.wbs, K, N, Np, j.dgrad[q], i, reinterpret_cast<__nv_bfloat16*>(j.out[q] + b * j.obs[q]));
+  if (i >= (long long)cin * cout) return;
+  const int co = (int)(i / cin), ci = (int)(i - (long long)co * cin);
+  const int code = j.dgrad[q], K = j.K[q], Np = np_of(j.N[q]);
+  float* out = j.out[q] + b * j.obs[q];
+  const float* src = j.w[q] + b * j.wbs;
+  if (code & kTcPw) {  // 1^3: W[co][ci]
+    const float val = __ldg(src + i);
+    if (code & 1) pack_put(out, j.obs[q], code, K, Np, 0, co, ci, val);
+    else pack_put(out, j.obs[q], code, K, Np, 0, ci, co, val);
     return;
   }
-  const int jj = (int)(i & 3);
-  const long long qq = i >> 2;
-  const int n = (int)(qq % Np);
-  const long long q2 = qq / Np;
-  const int kc = (int)(q2 % (K / 4));
-  const int t = (int)(q2 / (K / 4));
-  const int k = 4 * kc + jj;
-  const float val = n < N ? pack_val(j.w[q] + b * j.wbs, K, N, j.dgrad[q], t, k, n) : 0.f;
-  const float hi = tf32_hi(val);
-  float* out = j.out[q] + b * j.obs[q];
-  out[i] = hi;
-  out[j.obs[q] / 2 + i] = val - hi;
+  const float* wv = src + i * 27;  // W[co][ci][27]
+  const int c3 = code & 3;
+#pragma unroll 3
+  for (int t = 0; t < 27; ++t) {
+    const float val = __ldg(wv + t);
+    if (c3 == 0) {
+      pack_put(out, j.obs[q], code, K, Np, t, ci, co, val);
+    } else if (c3 == 1) {
+      pack_put(out, j.obs[q], code, K, Np, 26 - t, co, ci, val);
+    } else {
+      int pd, pa, ph, pb, pw, pc;
+      s2_inv(t / 9, c3 == 3, &pd, &pa);
+      s2_inv((t / 3) % 3, c3 == 3, &ph, &pb);
+      s2_inv(t % 3, c3 == 3, &pw, &pc);
+      const int p = (pd << 2) | (ph << 1) | pw, tg = pa * 9 + pb * 3 + pc;
+      if (c3 == 2) pack_put(out, j.obs[q], code, K, Np, tg, p * cin + ci, co, val);
+      else pack_put(out, j.obs[q], code, K, Np, tg, co, p * cin + ci, val);
+    }
+  }
 }
 
 int conv_tc_pack_multi(const PackJobs& jobs, int batch, cudaStream_t st) {
@@ -570,6 +606,10 @@ int conv_tc_pack_multi(const PackJobs& jobs, int batch, cudaStream_t st) {
 }
 
 void pack_jobs_add(PackJobs& j, const float* w, int K, int N, int dgrad, float* out) {
+  // layer channels from the GEMM view: codes 0 / 2 (forward) K = C_in (x 8), N = C_out; 1 / 3 transposed
+  const int c3 = dgrad & 3;
+  const int cin = c3 == 0 ? K : c3 == 1 ? N : c3 == 2 ? K / 8 : N / 8;
+  const int cout = (c3 == 0 || c3 == 2) ? N : K;
   const int q = j.n++;
   j.w[q] = w;
   j.out[q] = out;
@@ -578,7 +618,9 @@ void pack_jobs_add(PackJobs& j, const float* w, int K, int N, int dgrad, float* 
   j.dgrad[q] = dgrad;
   j.half[q] = ((dgrad & kTcPw) ? 1LL : 27LL) * K * np_of(N);
   j.obs[q] = conv_tc_pack_floats(K, N);
-  j.block0[q + 1] = j.block0[q] + (int)((j.half[q] + 255) / 256);
+  j.cin[q] = cin;
+  j.cout[q] = cout;
+  j.block0[q + 1] = j.block0[q] + (int)(((long long)cin * cout + 255) / 256);
 }
 
 bool conv_tc_supported(int cin, int cout, int ks, int stride, int precision) {

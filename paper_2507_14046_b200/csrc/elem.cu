@@ -1,3 +1,4 @@
+#include <algorithm>
 // Per-voxel kernels: trilinear x2 upsample (align_corners=False) forward and
 // gather backward, and the tail conv + sigmoid + output map + mask gather.
 // (ChannelLayerNorm / activation kernels live in norm.cu.)
@@ -261,13 +262,275 @@ __global__ void __launch_bounds__(96) tail_fwd_k(d2ip_act x, const float* __rest
   if (col >= 0) sigma_c[b * sc_bs + col] = mp;
 }
 
+// ---------------------------------------------------------------------------
+// The C_out = 1 tail convolution (priornet.py:215-232 restated: 3^3, padding 1)
+// with lane groups: G = C / 4 lanes share a voxel, lane l owns channels
+// 4l .. 4l + 3 (float4 loads: a group reads its voxel row in one coalesced
+// 16 G-byte run), and the G partial dot products are combined with a fixed
+// xor-shuffle tree. Replaces the one-thread-per-voxel kernels, which read a
+// 128-byte row per thread per tap (a 27-deep chain of uncoalesced loads).
+
+template <int G>
+__device__ __forceinline__ float group_sum(float v) {
+#pragma unroll
+  for (int o = G >> 1; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+template <int G>
+__global__ void __launch_bounds__(256) tail_fwd_g_k(d2ip_act x, const float* __restrict__ w,
+                                                    const float* __restrict__ bias, long long wbs, float lo,
+                                                    float scale, float* __restrict__ sig, float* __restrict__ mapped,
+                                                    float* __restrict__ sigma_c, long long sc_bs,
+                                                    const int* __restrict__ col_of_vox) {
+  D2IP_PDL_ENTRY();
+  __shared__ float4 sw[27 * G];  // [tap][lane] = W[0][4 lane .. 4 lane + 3][tap]
+  const int b = blockIdx.y;
+  const float* wb = w + b * wbs;
+  for (int i = threadIdx.x; i < 27 * G; i += blockDim.x) {
+    const int t = i / G, l = i % G;
+    sw[i] = make_float4(__ldg(wb + (4 * l) * 27 + t), __ldg(wb + (4 * l + 1) * 27 + t),
+                        __ldg(wb + (4 * l + 2) * 27 + t), __ldg(wb + (4 * l + 3) * 27 + t));
+  }
+  __syncthreads();
+  const long long V = (long long)x.d * x.h * x.w;
+  const long long v = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / G;
+  const int l = threadIdx.x % G;
+  float acc = 0.f;
+  if (v < V) {
+    const int ow = (int)(v % x.w), oh = (int)((v / x.w) % x.h), od = (int)(v / ((long long)x.w * x.h));
+    const float* xb = x.ptr + b * x.bstride + 4 * l;
+#pragma unroll 3
+    for (int kd = 0; kd < 3; ++kd) {
+      const int id = od + kd - 1;
+      if (id < 0 || id >= x.d) continue;
+#pragma unroll
+      for (int kh = 0; kh < 3; ++kh) {
+        const int ih = oh + kh - 1;
+        if (ih < 0 || ih >= x.h) continue;
+#pragma unroll
+        for (int kw = 0; kw < 3; ++kw) {
+          const int iw = ow + kw - 1;
+          if (iw < 0 || iw >= x.w) continue;
+          const float4 q = __ldg(reinterpret_cast<const float4*>(xb + (((long long)id * x.h + ih) * x.w + iw) * x.cstride));
+          const float4 wq = sw[((kd * 3 + kh) * 3 + kw) * G + l];
+          acc = fmaf(q.x, wq.x, fmaf(q.y, wq.y, fmaf(q.z, wq.z, fmaf(q.w, wq.w, acc))));
+        }
+      }
+    }
+  }
+  acc = group_sum<G>(acc);
+  if (v >= V || l != 0) return;
+  const float a = __ldg(bias + b * wbs) + acc;
+  const float s = 1.0f / (1.0f + expf(-a));
+  const float mp = lo + scale * s;
+  sig[b * V + v] = s;
+  mapped[b * V + v] = mp;
+  const int col = col_of_vox[v];
+  if (col >= 0) sigma_c[b * sc_bs + col] = mp;
+}
+
+// gx[v][c] = sum_t W[0][c][t] gt[v - off_t]  (conv_transpose of the C_out = 1 tail)
+template <int G>
+__global__ void __launch_bounds__(256) tail_dgrad_g_k(const float* __restrict__ gt, const float* __restrict__ w,
+                                                      long long wbs, d2ip_act gx) {
+  D2IP_PDL_ENTRY();
+  __shared__ float4 sw[27 * G];
+  const int b = blockIdx.y;
+  const float* wb = w + b * wbs;
+  for (int i = threadIdx.x; i < 27 * G; i += blockDim.x) {
+    const int t = i / G, l = i % G;
+    sw[i] = make_float4(__ldg(wb + (4 * l) * 27 + t), __ldg(wb + (4 * l + 1) * 27 + t),
+                        __ldg(wb + (4 * l + 2) * 27 + t), __ldg(wb + (4 * l + 3) * 27 + t));
+  }
+  __syncthreads();
+  const long long V = (long long)gx.d * gx.h * gx.w;
+  const long long v = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / G;
+  const int l = threadIdx.x % G;
+  if (v >= V) return;
+  const int ow = (int)(v % gx.w), oh = (int)((v / gx.w) % gx.h), od = (int)(v / ((long long)gx.w * gx.h));
+  const float* g = gt + b * V;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll 3
+  for (int kd = 0; kd < 3; ++kd) {
+    const int id = od - kd + 1;
+    if (id < 0 || id >= gx.d) continue;
+#pragma unroll
+    for (int kh = 0; kh < 3; ++kh) {
+      const int ih = oh - kh + 1;
+      if (ih < 0 || ih >= gx.h) continue;
+#pragma unroll
+      for (int kw = 0; kw < 3; ++kw) {
+        const int iw = ow - kw + 1;
+        if (iw < 0 || iw >= gx.w) continue;
+        const float s = __ldg(g + ((long long)id * gx.h + ih) * gx.w + iw);
+        const float4 wq = sw[((kd * 3 + kh) * 3 + kw) * G + l];
+        acc.x = fmaf(s, wq.x, acc.x);
+        acc.y = fmaf(s, wq.y, acc.y);
+        acc.z = fmaf(s, wq.z, acc.z);
+        acc.w = fmaf(s, wq.w, acc.w);
+      }
+    }
+  }
+  *reinterpret_cast<float4*>(gx.ptr + b * gx.bstride + v * gx.cstride + 4 * l) = acc;
+}
+
+// Weight + bias gradient of the tail: dW[c][t] = sum_v x[v][c] gt[v - off_t],
+// db = sum_v gt[v]. Each CTA walks a voxel range (one float4 x load and 27 gt
+// scalars per voxel), reduces its lane groups with a fixed shuffle tree and a
+// fixed-order pass over its warps, and writes one partial [27 C + 1]; a second
+// pass sums the partials in CTA order.
+template <int G>
+__global__ void __launch_bounds__(256) tail_wgrad_g_k(d2ip_act x, const float* __restrict__ gt, int vchunk,
+                                                      float* __restrict__ part) {
+  D2IP_PDL_ENTRY();
+  constexpr int VPW = 32 / G;  // voxel groups per warp
+  __shared__ float red[8][G][27 * 4 + 1];
+  const int b = blockIdx.y;
+  const int C = 4 * G;
+  const long long V = (long long)x.d * x.h * x.w;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, l = lane % G, grp = threadIdx.x / G;
+  float acc[27][4];
+#pragma unroll
+  for (int t = 0; t < 27; ++t) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.f;
+  float bsum = 0.f;
+  const float* g = gt + b * V;
+  const long long v_lo = (long long)blockIdx.x * vchunk, v_hi = min(V, v_lo + vchunk);
+  for (long long v = v_lo + grp; v < v_hi; v += 256 / G) {
+    const int ow = (int)(v % x.w), oh = (int)((v / x.w) % x.h), od = (int)(v / ((long long)x.w * x.h));
+    const float4 q = __ldg(reinterpret_cast<const float4*>(x.ptr + b * x.bstride + v * x.cstride + 4 * l));
+    if (l == 0) bsum += g[v];
+#pragma unroll
+    for (int kd = 0; kd < 3; ++kd) {
+      const int id = od - kd + 1;
+#pragma unroll
+      for (int kh = 0; kh < 3; ++kh) {
+        const int ih = oh - kh + 1;
+#pragma unroll
+        for (int kw = 0; kw < 3; ++kw) {
+          const int iw = ow - kw + 1;
+          const bool in = id >= 0 && id < x.d && ih >= 0 && ih < x.h && iw >= 0 && iw < x.w;
+          const float s = in ? __ldg(g + ((long long)id * x.h + ih) * x.w + iw) : 0.f;
+          const int t = (kd * 3 + kh) * 3 + kw;
+          acc[t][0] = fmaf(q.x, s, acc[t][0]);
+          acc[t][1] = fmaf(q.y, s, acc[t][1]);
+          acc[t][2] = fmaf(q.z, s, acc[t][2]);
+          acc[t][3] = fmaf(q.w, s, acc[t][3]);
+        }
+      }
+    }
+  }
+  // fold the VPW voxel groups of the warp (lanes l, l + G, ...): fixed xor tree
+#pragma unroll
+  for (int t = 0; t < 27; ++t)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      float v = acc[t][j];
+#pragma unroll
+      for (int o = 16; o >= G; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+      acc[t][j] = v;
+    }
+  for (int o = 16; o >= 1; o >>= 1) bsum += __shfl_xor_sync(0xffffffffu, bsum, o);
+  if (lane < G) {
+#pragma unroll
+    for (int t = 0; t < 27; ++t)
+#pragma unroll
+      for (int j = 0; j < 4; ++j) red[warp][l][t * 4 + j] = acc[t][j];
+    if (lane == 0) red[warp][0][27 * 4] = bsum;
+  }
+  __syncthreads();
+  float* pb = part + ((long long)b * gridDim.x + blockIdx.x) * (27 * C + 1);
+  for (int i = threadIdx.x; i < 27 * C + 1; i += blockDim.x) {
+    float s = 0.f;
+    if (i < 27 * C) {
+      const int c = i / 27, t = i % 27, ll = c / 4, j = c % 4;  // output order: OIDHW [c][t]
+      for (int wi = 0; wi < 8; ++wi) s += red[wi][ll][t * 4 + j];
+    } else {
+      for (int wi = 0; wi < 8; ++wi) s += red[wi][0][27 * 4];
+    }
+    pb[i] = s;
+  }
+  (void)VPW;
+}
+
+__global__ void tail_wgrad_reduce_k(const float* __restrict__ part, int nblk, int n, float* __restrict__ gw,
+                                    long long gwbs) {
+  D2IP_PDL_ENTRY();
+  const int b = blockIdx.y;
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float* p = part + (long long)b * nblk * n + i;
+  float s = 0.f;
+#pragma unroll 8
+  for (int k = 0; k < nblk; ++k) s += __ldg(p + (long long)k * n);
+  gw[b * gwbs + i] = s;  // [c][t] weights then the bias: the OIDHW + bias parameter layout
+}
+
+static bool tail_g_ok(const d2ip_act& x) {
+  const int G = x.c / 4;
+  return x.c % 4 == 0 && (G == 1 || G == 2 || G == 4 || G == 8) && x.cstride % 4 == 0 &&
+         ((uintptr_t)x.ptr & 15) == 0;
+}
+
 int tail_fwd(d2ip_act x, const float* w, const float* bias, long long wbs, float lo, float scale,
              float* sig, float* mapped, float* sigma_c, long long sc_bs, const int* col_of_vox,
              int batch, cudaStream_t st) {
   const long long V = (long long)x.d * x.h * x.w;
+  if (tail_g_ok(x)) {
+    const dim3 grid(cdiv(V * (x.c / 4), 256), batch);
+#define D2IP_TAILF(G_)                                                                                          \
+  case G_:                                                                                                      \
+    D2IP_CUDA(launch_pdl(tail_fwd_g_k<G_>, grid, 256, 0, st, x, w, bias, wbs, lo, scale, sig, mapped, sigma_c, \
+                         sc_bs, col_of_vox));                                                                   \
+    break;
+    switch (x.c / 4) { D2IP_TAILF(1) D2IP_TAILF(2) D2IP_TAILF(4) D2IP_TAILF(8) }
+#undef D2IP_TAILF
+    D2IP_LAUNCH_CHECK();
+    return D2IP_OK;
+  }
   D2IP_CHECK_ARG(27 * x.c * sizeof(float) <= 40 * 1024, "tail: C_in too large");
   D2IP_CUDA(launch_pdl(tail_fwd_k, dim3(cdiv(V, 32), batch), 96, (27 * x.c + 96) * sizeof(float), st, x, w, bias,
                        wbs, lo, scale, sig, mapped, sigma_c, sc_bs, col_of_vox));
+  D2IP_LAUNCH_CHECK();
+  return D2IP_OK;
+}
+
+bool tail_bwd_supported(d2ip_act x) { return tail_g_ok(x); }
+
+int tail_dgrad(const float* gt, const float* w, long long wbs, d2ip_act gx, int batch, cudaStream_t st) {
+  D2IP_CHECK_ARG(tail_g_ok(gx), "tail_dgrad: channels must be 4, 8, 16 or 32, 16-byte aligned");
+  const long long V = (long long)gx.d * gx.h * gx.w;
+  const dim3 grid(cdiv(V * (gx.c / 4), 256), batch);
+#define D2IP_TAILD(G_) \
+  case G_: D2IP_CUDA(launch_pdl(tail_dgrad_g_k<G_>, grid, 256, 0, st, gt, w, wbs, gx)); break;
+  switch (gx.c / 4) { D2IP_TAILD(1) D2IP_TAILD(2) D2IP_TAILD(4) D2IP_TAILD(8) }
+#undef D2IP_TAILD
+  D2IP_LAUNCH_CHECK();
+  return D2IP_OK;
+}
+
+static int tail_wgrad_blocks(long long V) { return (int)std::min<long long>(296, std::max<long long>(1, V / 256)); }
+
+size_t tail_wgrad_ws(int C, long long V, int batch) {
+  return (size_t)batch * tail_wgrad_blocks(V) * (27 * C + 1) * sizeof(float);
+}
+
+int tail_wgrad(d2ip_act x, const float* gt, float* gw, long long gwbs, void* ws, size_t ws_bytes, int batch,
+               cudaStream_t st) {
+  D2IP_CHECK_ARG(tail_g_ok(x), "tail_wgrad: channels must be 4, 8, 16 or 32, 16-byte aligned");
+  const long long V = (long long)x.d * x.h * x.w;
+  const int nblk = tail_wgrad_blocks(V);
+  D2IP_CHECK_ARG(ws_bytes >= tail_wgrad_ws(x.c, V, batch), "tail_wgrad: workspace too small");
+  const int vchunk = cdiv(V, nblk);
+  float* part = reinterpret_cast<float*>(ws);
+  const dim3 grid(nblk, batch);
+#define D2IP_TAILW(G_) \
+  case G_: D2IP_CUDA(launch_pdl(tail_wgrad_g_k<G_>, grid, 256, 0, st, x, gt, vchunk, part)); break;
+  switch (x.c / 4) { D2IP_TAILW(1) D2IP_TAILW(2) D2IP_TAILW(4) D2IP_TAILW(8) }
+#undef D2IP_TAILW
+  D2IP_LAUNCH_CHECK();
+  const int n = 27 * x.c + 1;
+  D2IP_CUDA(launch_pdl(tail_wgrad_reduce_k, dim3(cdiv(n, 256), batch), 256, 0, st, part, nblk, n, gw, gwbs));
   D2IP_LAUNCH_CHECK();
   return D2IP_OK;
 }

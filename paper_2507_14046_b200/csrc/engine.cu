@@ -158,6 +158,7 @@ static void config_plan_workspace(d2ip_engine& E, Arena& A) {
   };
   conv_ws(E.stem, 0);
   conv_ws(E.tail, 0);
+  wg = std::max(wg, tail_wgrad_ws(c[0], E.V[0], B));
   {
     size_t s = norm_act_bwd_ws(E.V[0], c[0], B);
     if (s > na) na = s;
@@ -490,8 +491,15 @@ static int backward(Ctx& k) {
   }
   d2ip_act gt = view(E, E.gtail, 0, 1, 1);
   Block& last = E.dec.back();
-  D2IP_RET(cwgrad_side(k, E.tail, last.out, gt));
-  D2IP_RET(cdgrad(k, E.tail, gt, last.gout, 0));
+  if (tail_bwd_supported(last.out)) {  // C_out = 1: lane-group kernels (no GEMM shape to tile)
+    Ctx ks = k;
+    D2IP_RET(side_ctx(k, ks));
+    D2IP_RET(tail_wgrad(last.out, E.gtail, k.gr() + E.tail.ow, k.pbs, ks.wgws, E.wg_ws_bytes, k.B, ks.st));
+    D2IP_RET(tail_dgrad(E.gtail, k.th() + E.tail.ow, k.pbs, last.gout, k.B, k.st));
+  } else {
+    D2IP_RET(cwgrad_side(k, E.tail, last.out, gt));
+    D2IP_RET(cdgrad(k, E.tail, gt, last.gout, 0));
+  }
   for (int j = (int)E.dec.size() - 1; j >= 0; --j) {
     Block& bl = E.dec[j];
     const int l = bl.lout;

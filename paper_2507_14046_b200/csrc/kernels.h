@@ -85,6 +85,7 @@ struct PackJobs {
   int K[kMax], N[kMax], dgrad[kMax];
   long long half[kMax];  // packed elements per half (27 or 1 taps x K x Np)
   long long obs[kMax];   // per-sequence stride of the pack buffer (conv_tc_pack_floats)
+  int cin[kMax], cout[kMax];  // layer channels: one thread per (co, ci) weight vector
   int block0[kMax + 1] = {0};
 };
 void pack_jobs_add(PackJobs& j, const float* w, int K, int N, int dgrad, float* out);
@@ -128,6 +129,12 @@ int upsample2x_bwd(d2ip_act gy, d2ip_act gx, int accumulate, int batch, cudaStre
 int tail_fwd(d2ip_act x, const float* w, const float* bias, long long wbs, float lo, float scale,
              float* sig, float* mapped, float* sigma_c, long long sc_bs, const int* col_of_vox,
              int batch, cudaStream_t st);
+// C_out = 1 tail convolution backward (lane-group kernels; C = 4, 8, 16, 32)
+bool tail_bwd_supported(d2ip_act x);
+int tail_dgrad(const float* gt, const float* w, long long wbs, d2ip_act gx, int batch, cudaStream_t st);
+size_t tail_wgrad_ws(int C, long long V, int batch);
+int tail_wgrad(d2ip_act x, const float* gt, float* gw, long long gwbs, void* ws, size_t ws_bytes, int batch,
+               cudaStream_t st);
 int tail_bwd_prep(const float* gmapped, const float* sig, float scale, float* gtail, long long V0,
                   int batch, cudaStream_t st);
 

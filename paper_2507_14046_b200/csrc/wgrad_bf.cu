@@ -501,8 +501,12 @@ __global__ void __launch_bounds__(256) wgrad_bf_reduce_k(const float* __restrict
     out[b * obs + ((long long)co * Cin + ci) * ntaps + t] = s;
   } else {
     const int co = (int)(e - nw);
-    for (int r = 0; r < nrg; ++r)
-      for (int y = 0; y < nyb; ++y) s += p[(long long)r * blk + nw + (long long)y * Cout + co];
+    const int n = nrg * nyb;  // (rg, y) slots in order; loads batched, adds in fixed order
+#pragma unroll 8
+    for (int q = 0; q < n; ++q) {
+      const int r = q / nyb, y = q - r * nyb;
+      s += __ldg(p + (long long)r * blk + nw + (long long)y * Cout + co);
+    }
     out[b * obs + nw + co] = s;
   }
 }
