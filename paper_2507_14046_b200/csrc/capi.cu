@@ -52,9 +52,9 @@ size_t conv_wgrad_ws(int cin, int cout, int ks, int D, int H, int W, int batch, 
 
 int conv_wgrad(d2ip_act x, d2ip_act gy, int ks, int stride, float* gw, long long gwbs, void* ws,
                size_t ws_bytes, int precision, int batch, cudaStream_t st) {
-  if (stride == 1 && precision == D2IP_PREC_BF16 && g_wgrad_variant == 1 && wgrad_bf_supported(x, gy, ks)) {
+  if (precision == D2IP_PREC_BF16 && g_wgrad_variant == 1 && wgrad_bf_supported(x, gy, ks, stride)) {
     set_variant("wgrad_tcgen05_bf16");
-    return wgrad_bf(x, gy, ks, gw, gwbs, ws, ws_bytes, batch, st);
+    return wgrad_bf(x, gy, ks, gw, gwbs, ws, ws_bytes, batch, st, stride);
   }
   if (stride == 1 && g_wgrad_variant == 1 && wgrad_tc_supported(x, gy, ks, precision)) {
     set_variant("wgrad_tcgen05_tf32x3");

@@ -52,11 +52,11 @@ size_t wgrad_tc_ws_bytes(int D, int H, int W, int Cin, int Cout, int ks, int bat
 int wgrad_tc(d2ip_act x, d2ip_act gy, int ks, float* gw, long long gwbs, void* ws, size_t ws_bytes, int batch,
              cudaStream_t st);
 
-// wgrad_bf.cu — tcgen05 kind::f16 weight gradient of stride-1 3^3 / 1^3 convolutions (bf16 layers)
-bool wgrad_bf_supported(d2ip_act x, d2ip_act gy, int ks);
+// wgrad_bf.cu — tcgen05 kind::f16 weight gradient of 3^3 (stride 1 and 2) / 1^3 convolutions (bf16 layers)
+bool wgrad_bf_supported(d2ip_act x, d2ip_act gy, int ks, int stride = 1);
 size_t wgrad_bf_ws_bytes(int D, int H, int W, int Cin, int Cout, int ks, int batch);
 int wgrad_bf(d2ip_act x, d2ip_act gy, int ks, float* gw, long long gwbs, void* ws, size_t ws_bytes, int batch,
-             cudaStream_t st);
+             cudaStream_t st, int stride = 1);
 // fixed-order reduction of [b][rg][ntaps][Cin][Cout] + [Cout] partials into OIDHW + bias
 int wgrad_reduce(const float* part, int nrg, int ntaps, int Cin, int Cout, float* gw, long long gwbs, int batch,
                  cudaStream_t st);

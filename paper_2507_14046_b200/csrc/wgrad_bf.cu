@@ -51,6 +51,10 @@ struct WgBf {
                       // map rows whose B descriptors start bsh0 + c * bstep rows in (a 16-byte move)
   int bsh0, bstep;    // single-copy B row shift of MMA c (kh rows: 2 - kw; one tap: 2 - kw; 1^3: 1)
   int tapmode;        // one tap per CTA (C_out = 256: a kh row of 3 x 256 columns exceeds TMEM)
+  int s2;             // stride-2 3^3 layer by parity decomposition (see wb_s2_*): rows = the gy grid,
+                      // the x window holds the two parity blocks (pw = 0, 1) of the CTA's (pd, ph)
+  int mrows;          // real MMA rows (input channels of the block; C_in for stride 2)
+  int carry;          // carry the x halo between stages (kd planes)
   int ngx, ngc;       // 8-channel group columns: x (real), gy per copy
   int RS, WR, WRp, RSp;  // rows per stage (K chunk), x window rows, padded column lengths
   int halo;           // x rows carried from the previous stage's window (2 Sw for kd planes)
@@ -94,7 +98,17 @@ __device__ __forceinline__ int wb_voxel(const WgBf& a, int u, int D, int H, int 
 // (kd, kh, kw) pairs x row v + (kd-1) Sh + (kh-1) Sw with gy row v + 1 - kw
 // (the kw shift lives in the gy copies), so the window starts at the kd plane's
 // kh = 0 row (kd plane) or at the (kd, kh) row; always a multiple of 8.
+// Stride 2: x = 2 o + k - 1 per axis, so tap k reads parity p = (k != 1) at
+// output offset delta = (k == 0 ? -1 : 0). A CTA owns (kd, kh) (or one tap):
+// its window rows start at delta_d Sh + delta_h Sw - 1 (delta_w = -1 is row 0),
+// tap kw reads parity block pw = (kw != 1) at row offset 1 + delta_w.
+__device__ __forceinline__ int wb_s2_delta(int k) { return k == 0 ? -1 : 0; }
+
 __device__ __forceinline__ int wb_base(const WgBf& a, int grp) {
+  if (a.s2) {
+    const int kd = a.tapmode ? grp / 9 : grp / 3, kh = a.tapmode ? (grp / 3) % 3 : grp % 3;
+    return wb_s2_delta(kd) * a.Sh + wb_s2_delta(kh) * a.Sw - 1;
+  }
   if (a.ks == 1) return 0;
   if (a.tapmode) return (grp / 9 - 1) * a.Sh + ((grp / 3) % 3 - 1) * a.Sw;
   if (a.nkh == 3) return (grp - 1) * a.Sh - a.Sw;
@@ -154,7 +168,14 @@ __global__ void __launch_bounds__(kWbThreads) wgrad_bf_k(WgBf a) {
       const uint32_t sw16 = (uint32_t)a.Sw;                       // one kh row: Sw rows x 16 B
       const uint32_t idesc = a.idesc, N = a.N;
       const bool stacked = a.ncp == 3;
-      const int bsh = a.tapmode ? 2 - grp % 3 : a.bsh0;  // single copy: B starts bsh rows into the map rows
+      const int bsh = (a.tapmode && !a.s2) ? 2 - grp % 3 : a.bsh0;  // single copy: B starts bsh rows into the map rows
+      // stride 2: MMA c (kw = c, or the CTA's one kw) reads parity block (kw != 1) from row 1 + delta_w
+      uint32_t aoff[3] = {0u, 0u, 0u};
+      if (a.s2)
+        for (int c = 0; c < 3; ++c) {
+          const int kw = a.tapmode ? grp % 3 : c;
+          aoff[c] = (uint32_t)((kw != 1) * (a.mrows / 8) * WRp + 1 + wb_s2_delta(kw));
+        }
       for (int s = 0; s < S; ++s) {
         const int slot = s % NST;
         tc::mbar_wait(&full[slot], (uint32_t)((s / NST) & 1));
@@ -168,7 +189,7 @@ __global__ void __launch_bounds__(kWbThreads) wgrad_bf_k(WgBf a) {
           for (int kh = 0; kh < NKH; ++kh)
 #pragma unroll
             for (int c = 0; c < NMMA; ++c)
-              tc::mma_f16(tmem + (uint32_t)(kh * NMMA + c) * N, da + (uint64_t)(kh * sw16),
+              tc::mma_f16(tmem + (uint32_t)(kh * NMMA + c) * N, da + (uint64_t)(kh * sw16 + aoff[c]),
                           db + (uint64_t)(stacked ? c * cpy16 : bsh + c * a.bstep), idesc, acc);
         }
         tc::commit(&empty[slot]);
@@ -197,13 +218,26 @@ __global__ void __launch_bounds__(kWbThreads) wgrad_bf_k(WgBf a) {
         continue;
       }
       const int v0 = a.v_start + (c_lo + s) * RS;
-      const bool carry = s > 0 && a.halo > 0;  // first `halo` x rows = the previous window's last rows
+      const bool carry = s > 0 && a.carry;  // first `halo` x rows = the previous window's last rows
       const int xr0 = carry ? a.halo : 0;
       int* rm = rmap + (s & 1) * (WR + NM);
       for (int r = gtid; r < WR + NM; r += kWbProd) {
         int off = -1;
         if (r < WR) {
-          if (r >= xr0) off = wb_voxel(a, v0 + base + r, x.d, x.h, x.w);
+          if (r >= xr0) {
+            if (a.s2) {
+              // (x voxel of (2 od + pd, 2 oh + ph, 2 ow)) << 1 | (2 ow + 1 inside); -1: none
+              const int o = wb_voxel(a, v0 + base + r, gy.d, gy.h, gy.w);
+              if (o >= 0) {
+                const int kd = a.tapmode ? grp / 9 : grp / 3, kh = a.tapmode ? (grp / 3) % 3 : grp % 3;
+                const int ow = o % gy.w, oh = (o / gy.w) % gy.h, od = o / (gy.w * gy.h);
+                const int xd = 2 * od + (kd != 1), xh = 2 * oh + (kh != 1), xw = 2 * ow;
+                if (xd < x.d && xh < x.h) off = (((xd * x.h + xh) * x.w + xw) << 1) | (xw + 1 < x.w);
+              }
+            } else {
+              off = wb_voxel(a, v0 + base + r, x.d, x.h, x.w);
+            }
+          }
         } else {
           const int u = v0 - 1 + (r - WR);
           off = (u < a.u_first || u > a.u_last) ? -1 : wb_voxel(a, u, gy.d, gy.h, gy.w);
@@ -223,8 +257,16 @@ __global__ void __launch_bounds__(kWbThreads) wgrad_bf_k(WgBf a) {
         for (int i = gtid; i < n16; i += kWbProd) {
           const int r = xr0 + i / NGX, g = i % NGX;
           const int off = rm[r];
-          tc::cp_async16(X + ((size_t)g * WRp + r) * 16, off >= 0 ? xt + (long long)off * x.cstride + 8 * g : xt,
-                         off >= 0 ? 16u : 0u);
+          const uint16_t* src = xt;
+          bool ok = off >= 0;
+          if (a.s2) {  // group g of parity block g / (C_in / 8)
+            const int gb = a.mrows / 8, bk = g / gb;
+            ok = ok && (bk == 0 || (off & 1));
+            if (ok) src = xt + (long long)((off >> 1) + bk) * x.cstride + 8 * (g - bk * gb);
+          } else if (ok) {
+            src = xt + (long long)off * x.cstride + 8 * g;
+          }
+          tc::cp_async16(X + ((size_t)g * WRp + r) * 16, src, ok ? 16u : 0u);
         }
       }
       for (int i0 = gtid; i0 < nX; i0 += 16 * kWbProd) {
@@ -235,7 +277,13 @@ __global__ void __launch_bounds__(kWbThreads) wgrad_bf_k(WgBf a) {
           v[q] = make_float4(0.f, 0.f, 0.f, 0.f);
           if (i < nX) {
             const int off = rm[xr0 + i / NP];
-            if (off >= 0) v[q] = *reinterpret_cast<const float4*>(xb + (long long)off * x.cstride + 4 * (i % NP));
+            if (a.s2) {  // piece pc of parity block pc / (C_in / 4)
+              const int pb = a.mrows / 4, pc = i % NP, bk = pc / pb;
+              if (off >= 0 && (bk == 0 || (off & 1)))
+                v[q] = *reinterpret_cast<const float4*>(xb + (long long)((off >> 1) + bk) * x.cstride + 4 * (pc - bk * pb));
+            } else if (off >= 0) {
+              v[q] = *reinterpret_cast<const float4*>(xb + (long long)off * x.cstride + 4 * (i % NP));
+            }
           }
         }
 #pragma unroll
@@ -329,8 +377,8 @@ __global__ void __launch_bounds__(kWbThreads) wgrad_bf_k(WgBf a) {
     int m = -1;
     if (a.M == 128) m = quad * 32 + lane;
     else if (lane < 16) m = quad * 16 + lane;
-    const int ci = cb * a.cib + m;
-    const bool live = m >= 0 && m < a.cib;
+    const int ci = cb * a.mrows + m;
+    const bool live = m >= 0 && m < a.mrows;
     const uint32_t trow = tmem + ((uint32_t)(quad * 32) << 16);
     // accumulator columns: kh block of 3 C_out (kw copy c = kw, then co)
     const int nck = (nkh * 3 * Cout) / 8;
@@ -382,7 +430,10 @@ static size_t wb_smem(const WgBf& a) {
 
 static bool pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
 
-static bool wb_plan(int D, int H, int W, int Cin, int Cout, int ks, int batch, WgBf& a) {
+// (D, H, W): the gy grid (the layer's output)
+static bool wb_plan(int D, int H, int W, int Cin, int Cout, int ks, int batch, WgBf& a, int stride = 1) {
+  a.s2 = stride == 2;
+  if (a.s2 && (ks != 3 || Cin > 64)) return false;
   if ((ks != 1 && ks != 3) || Cout < 16 || Cout > 256 || !pow2(Cout) || Cin % 8 || Cin < 8) return false;
   a.ks = ks;
   a.ntaps = ks == 3 ? 27 : 1;
@@ -395,9 +446,11 @@ static bool wb_plan(int D, int H, int W, int Cin, int Cout, int ks, int batch, W
   a.ncib = 1;
   while (Cin / a.ncib > 128 || Cin % a.ncib || (Cin / a.ncib) % 8) ++a.ncib;
   a.cib = Cin / a.ncib;
+  a.mrows = a.cib;
+  if (a.s2) a.cib = 2 * Cin;  // the window holds two parity blocks
   const int ncx = a.cib / 4;
   if (ncx != 2 && ncx != 4 && ncx != 8 && ncx != 12 && ncx != 16 && ncx != 24 && ncx != 32) return false;
-  a.M = a.cib <= 64 ? 64 : 128;
+  a.M = a.mrows <= 64 ? 64 : 128;
   a.tapmode = 0;
   a.bstep = 0;
   a.bsh0 = 0;
@@ -408,6 +461,19 @@ static bool wb_plan(int D, int H, int W, int Cin, int Cout, int ks, int batch, W
     a.nmma = 1;
     a.N = Cout;
     a.bsh0 = 1;  // map row m = row v0 - 1 + m
+  } else if (a.s2) {
+    a.nkh = 1;
+    a.ncp = 1;
+    a.bsh0 = 1;  // gy rows unshifted: map row m = row v0 - 1 + m
+    a.N = Cout;
+    if (3 * Cout <= 512) {
+      a.nmma = 3;
+      a.ngroups = 9;
+    } else {
+      a.nmma = 1;
+      a.tapmode = 1;
+      a.ngroups = 27;
+    }
   } else if (9 * Cout <= 512) {
     // kd plane: three kh accumulators of 3 C_out columns, the kw copies stacked along N
     a.nkh = 3;
@@ -440,7 +506,8 @@ static bool wb_plan(int D, int H, int W, int Cin, int Cout, int ks, int batch, W
   a.ngc = Cout / 8;
   a.gshift = 0;
   while ((4 << a.gshift) < Cout) ++a.gshift;
-  a.halo = (ks == 3 && a.nkh == 3) ? 2 * a.Sw : 0;
+  a.halo = (ks == 3 && a.nkh == 3) ? 2 * a.Sw : a.s2 ? 1 : 0;
+  a.carry = ks == 3 && a.nkh == 3;
   const int rows = a.u_last + 2 - a.v_start;  // chunks cover v_start .. u_last + 1
   a.RS = 0;
   // the largest chunk that double-buffers in ~200 KB; then a third stage if it fits
@@ -451,7 +518,8 @@ static bool wb_plan(int D, int H, int W, int Cin, int Cout, int ks, int batch, W
     const uint32_t sx = (uint32_t)a.ngx * wrp * 16;
     const uint32_t sb = ((sx + (uint32_t)a.ncp * a.ngc * rsp * 16) + 1023) & ~1023u;
     // the M = 64 / 128 MMA reads M / 8 group columns: past a smaller x block into the stage's gy copies or the pad
-    const long long over = (long long)(a.M / 8 - a.ngx) * wrp * 16 - (long long)(sb - sx);
+    const int blk1 = a.s2 ? a.mrows / 8 : 0;  // stride 2: the pw = 1 block's MMA reads start here
+    const long long over = (long long)(blk1 + a.M / 8 - a.ngx) * wrp * 16 - (long long)(sb - sx);
     a.pad = over > 0 ? (uint32_t)((over + 1023) & ~1023LL) : 0;
     a.WR = wr;
     a.RS = rs;
@@ -511,17 +579,23 @@ __global__ void __launch_bounds__(256) wgrad_bf_reduce_k(const float* __restrict
   }
 }
 
-bool wgrad_bf_supported(d2ip_act x, d2ip_act gy, int ks) {
-  if (x.d != gy.d || x.h != gy.h || x.w != gy.w) return false;
+bool wgrad_bf_supported(d2ip_act x, d2ip_act gy, int ks, int stride) {
+  if (stride == 1 && (x.d != gy.d || x.h != gy.h || x.w != gy.w)) return false;
+  if (stride == 2 && (gy.d != (x.d + 1) / 2 || gy.h != (x.h + 1) / 2 || gy.w != (x.w + 1) / 2)) return false;
+  if (stride != 1 && stride != 2) return false;
   if (x.cstride % 4 || gy.cstride % 4 || ((uintptr_t)x.ptr & 15) || ((uintptr_t)gy.ptr & 15)) return false;
   WgBf a{};
-  return wb_plan(x.d, x.h, x.w, x.c, gy.c, ks, 1, a);
+  return wb_plan(gy.d, gy.h, gy.w, x.c, gy.c, ks, 1, a, stride);
 }
 
 size_t wgrad_bf_ws_bytes(int D, int H, int W, int Cin, int Cout, int ks, int batch) {
-  WgBf a{};
-  if (!wb_plan(D, H, W, Cin, Cout, ks, batch, a)) return 0;
-  return (size_t)batch * a.nrg * ((size_t)a.ntaps * Cin * Cout + (size_t)a.nyb * Cout) * sizeof(float);
+  size_t best = 0;  // (D, H, W): the gy grid; the larger of the stride-1 and stride-2 plans
+  for (int stride : {1, 2}) {
+    WgBf a{};
+    if (!wb_plan(D, H, W, Cin, Cout, ks, batch, a, stride)) continue;
+    best = std::max(best, (size_t)batch * a.nrg * ((size_t)a.ntaps * Cin * Cout + (size_t)a.nyb * Cout) * sizeof(float));
+  }
+  return best;
 }
 
 template <int NCX, int NKH, int NMMA>
@@ -544,10 +618,10 @@ static int wb_launch(const WgBf& a, dim3 grid, size_t smem, cudaStream_t st) {
 }
 
 int wgrad_bf(d2ip_act x, d2ip_act gy, int ks, float* gw, long long gwbs, void* ws, size_t ws_bytes, int batch,
-             cudaStream_t st) {
+             cudaStream_t st, int stride) {
   WgBf a{};
-  D2IP_CHECK_ARG(wb_plan(x.d, x.h, x.w, x.c, gy.c, ks, batch, a), "wgrad_bf: unsupported shape");
-  D2IP_CHECK_ARG(ws_bytes >= wgrad_bf_ws_bytes(x.d, x.h, x.w, x.c, gy.c, ks, batch), "wgrad_bf: workspace too small");
+  D2IP_CHECK_ARG(wb_plan(gy.d, gy.h, gy.w, x.c, gy.c, ks, batch, a, stride), "wgrad_bf: unsupported shape");
+  D2IP_CHECK_ARG(ws_bytes >= wgrad_bf_ws_bytes(gy.d, gy.h, gy.w, x.c, gy.c, ks, batch), "wgrad_bf: workspace too small");
   a.x = x;
   a.gy = gy;
   a.part = reinterpret_cast<float*>(ws);

@@ -83,6 +83,9 @@ CONV_CASES = [
     # 1^3 on the tensor cores (pointwise mode), large enough for T > 1 tiles
     (96, 32, 1, 1, (32, 32, 16)),
     (64, 64, 1, 1, (16, 16, 16)),
+    # stride-2 bf16 weight gradients (parity blocks), incl. C_out = 256 single taps
+    (16, 64, 3, 2, (12, 10, 8)),
+    (32, 256, 3, 2, (6, 6, 4)),
     # C_out = 256: one tap per CTA in the bf16 weight gradient
     (16, 256, 3, 1, (4, 4, 6)),
     # large grids (cfg2 / cfg4 scale tiles)
@@ -156,10 +159,12 @@ def wgrad_variant(request):
     L.d2ip_set_wgrad_variant(before)
 
 
-def bf16_wgrad_tc(cin, cout, stride):
-    """Stride-1 weight gradients of bf16 layers on kind::f16 MMAs (wgrad_bf.cu plan)."""
-    if stride != 1 or cin % 8 or cout < 16 or cout > 256 or cout & (cout - 1):
+def bf16_wgrad_tc(cin, cout, stride, ks=3):
+    """Weight gradients of bf16 layers on kind::f16 MMAs (wgrad_bf.cu plan; stride 2: 3^3, C_in <= 64)."""
+    if cin % 8 or cout < 16 or cout > 256 or cout & (cout - 1):
         return False
+    if stride == 2:
+        return ks == 3 and cin <= 64
     nb = 1
     while cin // nb > 128 or cin % nb or (cin // nb) % 8:
         nb += 1
@@ -200,7 +205,7 @@ def test_conv3d_dgrad_wgrad(cin, cout, ks, stride, sp, prec, wgrad_variant):
     torch.cuda.synchronize()
     if wgrad_variant == 1 and prec == "tf32" and stride == 1 and cin % 4 == 0 and cout % 4 == 0 and cout <= 128:
         assert N.lib().d2ip_last_variant() == b"wgrad_tcgen05_tf32x3"
-    if wgrad_variant == 1 and prec == "bf16" and bf16_wgrad_tc(cin, cout, stride):
+    if wgrad_variant == 1 and prec == "bf16" and bf16_wgrad_tc(cin, cout, stride, ks):
         assert N.lib().d2ip_last_variant() == b"wgrad_tcgen05_bf16"
     assert rel(from_ndhwc(gx), x.grad) < TOL[prec]
     ref_gw = torch.cat([torch.cat([w.grad[i].reshape(-1), b.grad[i]]) for i in range(B)]).reshape(B, P)
