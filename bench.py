@@ -290,6 +290,8 @@ def run_gpu(args):
     # dominant kernel: the tcgen05 conv on cfg1's largest layer (dec0.conv1,
     # 48 -> 16 channels at 32^3), one launch timed live through the C ABI
     conv_roof = conv_probe(L, N, C, st, pk, pk_kind, flush, t_flush) if spec.channels[0] == 16 and args.net == "config" else None
+    # the bf16 tensor-core kernels on cfg4's largest layer (dec0.conv1, 96 -> 32 at 96x96x48)
+    conv_bf16 = None if args.skip_probe else conv_bf16_probe(L, N, C, st, flush, t_flush)
     # whole-iteration tensor-throughput view of the convolutions
     conv_tflops = units["conv_flops"] * units_per_step / (t_dev / args.steps) / 1e12
     roofline = conv_roof or jac_cfg
@@ -319,6 +321,7 @@ def run_gpu(args):
         "roofline": roofline,
         "roofline_jac_cfg": jac_cfg,
         "roofline_jac_hbm": hbm_probe,
+        "roofline_conv_bf16_cfg4": conv_bf16,
         "clocks": clk.summary(),
     }
     if units_per_step > 1:
@@ -368,7 +371,7 @@ def conv_probe(L, N, C, st, pk, pk_kind, flush, t_flush):
     peak = TF32_PEAK_TFLOPS
     traffic = None  # DRAM bytes of this launch from the committed `ncu --set full` capture
     try:
-        prof = json.loads((Path(__file__).resolve().parent / "profiles" / "r1_conv_tc_dec0c1_full.json").read_text())
+        prof = json.loads((Path(__file__).resolve().parent / "profiles" / "r1_ncu_cfg1dec0c1.json").read_text())
         scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
         traffic = sum(float(prof[k]["value"]) * scale[prof[k]["unit"]]
                       for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
@@ -377,10 +380,72 @@ def conv_probe(L, N, C, st, pk, pk_kind, flush, t_flush):
     return {"bound": "tensor", "kernel": "conv_tc_k (K1, tcgen05 3xTF32 implicit GEMM) incl. weight pack",
             "layer": "dec0.conv1 48->16 @ 32^3", "achieved": round(flops / t / 1e12, 2), "peak": peak,
             "unit": "TFLOP/s", "frac": round(flops / t / 1e12 / peak, 4), "traffic": traffic,
-            "traffic_source": "profiles/r1_conv_tc_dec0c1_full.json (ncu --set full, dram read+write bytes)",
+            "traffic_source": "profiles/r1_ncu_cfg1dec0c1.json (ncu --set full, dram read+write bytes)",
             "algorithmic_flops_per_launch": flops, "avg_launch_s": t,
             "peak_source": "measured dense kind::tf32 tcgen05.mma peak on this pool's B200 (profiles/r1_umma_rate.txt); "
                            "3xTF32 issues 3 MMAs per product"}
+
+
+# dense kind::f16 peak measured the same way (profiles/r1_umma_rate.txt): 2,209 TFLOP/s.
+# At N = 32 output channels an M = 128 MMA reads 4 KB (A) + 1 KB (B) of shared
+# memory in ~40 cycles (tools/umma_chains.cu), which caps it at 40 % of that peak.
+F16_PEAK_TFLOPS = 2209.1
+F16_N32_BOUND_TFLOPS = F16_PEAK_TFLOPS * (2 * 128 * 32 * 16 / 40) / 8192  # 3,277 of 8,192 flop/cycle/SM
+
+
+def conv_bf16_probe(L, N, C, st, flush, t_flush):
+    """bf16 (kind::f16) forward conv and weight gradient of cfg4's dec0.conv1 (96 -> 32
+    channels at 96x96x48), inputs with their bf16 twins as in the engine; one launch
+    each timed with CUDA events (weight pack included in the forward)."""
+    import torch
+
+    cin, cout, dims = 96, 32, (96, 96, 48)
+    V = dims[0] * dims[1] * dims[2]
+    x = torch.randn(1, *dims, cin, device="cuda")
+    y = torch.randn(1, *dims, cout, device="cuda")
+    xt, yt = x.to(torch.bfloat16), y.to(torch.bfloat16)
+    w = torch.randn(cout * cin * 27 + cout, device="cuda") * 0.05
+    gw = torch.zeros_like(w)
+
+    def act(t, tw, c):
+        a = N.Act()
+        a.ptr, a.c, a.cstride = t.data_ptr(), c, c
+        a.d, a.h, a.w = dims
+        a.bstride = V * c
+        a.bf16 = tw.data_ptr()
+        return a
+
+    xa, ya = act(x, xt, cin), act(y, yt, cout)
+    wsn = L.d2ip_conv3d_ws_bytes(cin, cout, 3, 1, N.PREC["bf16"], 1)
+    ws = torch.empty(wsn, dtype=torch.uint8, device="cuda")
+    wgn = L.d2ip_conv3d_wgrad_ws_bytes(xa, ya, 3, 1)
+    wgs = torch.empty(wgn, dtype=torch.uint8, device="cuda")
+
+    def fwd():
+        flush.zero_()
+        N.check(L.d2ip_conv3d_fwd(xa, C.c_void_p(w.data_ptr()), C.c_void_p(w.data_ptr() + 4 * cout * cin * 27), 0,
+                                  3, 1, act(y, yt, cout), 0, N.PREC["bf16"], C.c_void_p(ws.data_ptr()), wsn, 1, st),
+                "conv bf16")
+
+    def wgrad():
+        flush.zero_()
+        N.check(L.d2ip_conv3d_wgrad(xa, ya, 3, 1, C.c_void_p(gw.data_ptr()), 0, C.c_void_p(wgs.data_ptr()), wgn,
+                                    N.PREC["bf16"], 1, st), "wgrad bf16")
+    flops = 2.0 * 27 * cin * cout * V
+    out = {"bound": "tensor", "layer": "cfg4 dec0.conv1 96->32 @ 96x96x48, bf16 operands (twins), fp32 accumulate",
+           "algorithmic_flops_per_launch": flops, "unit": "TFLOP/s", "peak": F16_PEAK_TFLOPS,
+           "peak_source": "measured dense kind::f16 tcgen05.mma peak (profiles/r1_umma_rate.txt)",
+           "n32_operand_bound": round(F16_N32_BOUND_TFLOPS, 1),
+           "n32_operand_bound_source": "M=128 x N=32 MMA = 40 cycles of shared-memory operand reads "
+                                       "(tools/umma_chains.cu); the layer's 32 output channels cap kind::f16 there"}
+    for name, fn, kern in (("fwd", fwd, "conv_tc_k<bf16> (K1) incl. weight pack"),
+                           ("wgrad", wgrad, "wgrad_bf_k (K3, kind::f16) incl. partial reduction")):
+        t = max(time_kernel(fn) - t_flush, 1e-9)
+        tf = flops / t / 1e12
+        out[name] = {"kernel": kern, "avg_launch_s": t, "achieved": round(tf, 1),
+                     "frac": round(tf / F16_PEAK_TFLOPS, 4), "frac_of_n32_bound": round(tf / F16_N32_BOUND_TFLOPS, 4)}
+    del x, y, xt, yt, ws, wgs
+    return out
 
 
 def run_e2e(spec, wl, args, ws):
