@@ -383,7 +383,12 @@ def conv_probe(L, N, C, st, pk, pk_kind, flush, t_flush):
             "traffic_source": "profiles/r1_ncu_cfg1dec0c1.json (ncu --set full, dram read+write bytes)",
             "algorithmic_flops_per_launch": flops, "avg_launch_s": t,
             "peak_source": "measured dense kind::tf32 tcgen05.mma peak on this pool's B200 (profiles/r1_umma_rate.txt); "
-                           "3xTF32 issues 3 MMAs per product"}
+                           "3xTF32 issues 3 MMAs per product",
+            # what the layer's shape allows: an M=128 x N=16 kind::tf32 MMA is bound by its shared-memory
+            # operand reads (4 KB A + 0.5 KB B at ~128 B/cycle: 39 cycles, tools/umma_chains.cu) to 840 of
+            # 4,096 flop/cycle/SM, and 3xTF32 spends 3 MMAs per fp32-accurate product
+            "n16_3xtf32_bound": round(TF32_PEAK_TFLOPS * (2 * 128 * 16 * 8 / 39) / 4096 / 3, 1),
+            "frac_of_n16_3xtf32_bound": round(flops / t / 1e12 / (TF32_PEAK_TFLOPS * (2 * 128 * 16 * 8 / 39) / 4096 / 3), 4)}
 
 
 # dense kind::f16 peak measured the same way (profiles/r1_umma_rate.txt): 2,209 TFLOP/s.

@@ -57,6 +57,7 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include <cuda.h>
 #include <cuda_bf16.h>
 
 #include "common.cuh"
@@ -94,6 +95,7 @@ struct TcConv {
   int bf;          // bf16 operands (kind::f16)
   int vec;         // y rows (and bias) 16-byte aligned: float4 epilogue stores
   int xtw;         // bf16: stream x from its bf16 twin (cp.async) instead of converting fp32 rows
+  int lrows;       // TMA path: rows per channel-chunk column (whole padded lines: maxlines x Sw)
 };
 
 // Per stage: A hi + A lo windows, B hi + B lo tiles (nt^2 taps); bf16: one
@@ -113,6 +115,105 @@ __device__ __forceinline__ uint32_t bf2(float a, float b) {
 }
 
 __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__float_as_uint(x) & 0xFFFFE000u); }
+
+// Epilogue shared by the cp.async- and TMA-fed kernels (producer warps 1-8):
+// TMEM lane = GEMM row; warp w reads lane quadrant w % 4 and column half
+// (w - 1) / 4; one row / voxel per sub-tile. S = 0: zeros (an empty split).
+template <int T, int MODE>
+__device__ __forceinline__ void tc_epilogue(const TcConv& a, uint32_t tmem, int b, int n0, int u0, int ks, int S,
+                                            int warp, int lane) {
+  const int row = (warp & 3) * 32 + lane;
+  const int chalf = a.Ns / 2, cbeg = ((warp - 1) >> 2) * chalf, cend = cbeg + chalf;
+  const d2ip_act y = a.y;
+  const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+  const float* bias = a.bias ? a.bias + b * a.bbs : nullptr;
+  for (int tt = 0; tt < T; ++tt) {
+    const int u = u0 + tt * kTcRows + row;
+    int v = -1, dq = 0, hq = 0, wq = 0;
+    {
+      const int dp = u / a.Sh, rem = u - dp * a.Sh;
+      const int hp = rem / a.Sw, wp = rem - hp * a.Sw;
+      if (dp >= 1 && dp <= a.gd && hp >= 1 && hp <= a.gh && wp >= 1 && wp <= a.gw) {
+        v = ((dp - 1) * a.gh + (hp - 1)) * a.gw + (wp - 1);
+        dq = dp - 1; hq = hp - 1; wq = wp - 1;
+      }
+    }
+    const uint32_t tcol = trow + (uint32_t)(tt * a.Ns);
+    if (MODE == 2) {  // column n = p * C_gx + ci -> gx voxel 2o + p (8 columns share p)
+      const int cy = y.c;
+      for (int c0 = cbeg; c0 < cend; c0 += 8) {
+        float vals[8];
+        tc::tmem_ld8(tcol + c0, vals);
+        const int n = n0 + c0;
+        if (v < 0 || n >= a.N) continue;
+        const int p = n / cy, ci = n - p * cy;
+        const int d2 = 2 * dq + (p >> 2), h2 = 2 * hq + ((p >> 1) & 1), w2 = 2 * wq + (p & 1);
+        if (d2 >= y.d || h2 >= y.h || w2 >= y.w) continue;
+        const long long vf = ((long long)d2 * y.h + h2) * y.w + w2;
+        if (a.kspl > 1) {
+          float* pp = a.part + (((long long)b * a.kspl + ks) * a.vout + vf) * cy + ci;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) pp[j] = S > 0 ? vals[j] : 0.f;
+        } else {
+          float* yp = y.ptr + b * y.bstride + vf * y.cstride + ci;
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            float o = S > 0 ? vals[j] : 0.f;
+            if (a.accumulate) o += yp[j];
+            yp[j] = o;
+          }
+        }
+      }
+      continue;
+    }
+    if (a.kspl > 1) {  // raw partial sums; the consumer adds bias / accumulates
+      float* pp = v >= 0 ? a.part + (((long long)b * a.kspl + ks) * a.vout + v) * a.N : nullptr;
+      for (int c0 = cbeg; c0 < cend; c0 += 8) {
+        float vals[8];
+        tc::tmem_ld8(tcol + c0, vals);
+        if (pp) {
+#pragma unroll
+          for (int j = 0; j < 8; ++j)
+            if (n0 + c0 + j < a.N) pp[n0 + c0 + j] = S > 0 ? vals[j] : 0.f;
+        }
+      }
+      continue;
+    }
+    float* yp = v >= 0 ? y.ptr + b * y.bstride + (long long)v * y.cstride : nullptr;
+    for (int c0 = cbeg; c0 < cend; c0 += 8) {
+      float vals[8];
+      tc::tmem_ld8(tcol + c0, vals);
+      if (yp && a.vec && n0 + c0 + 8 <= a.N) {
+        // 8 consecutive channels of one voxel: two 16-byte stores (one 32-byte sector)
+        float4* y4 = reinterpret_cast<float4*>(yp + n0 + c0);
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          float4 o = make_float4(S > 0 ? vals[4 * h] : 0.f, S > 0 ? vals[4 * h + 1] : 0.f,
+                                 S > 0 ? vals[4 * h + 2] : 0.f, S > 0 ? vals[4 * h + 3] : 0.f);
+          if (bias) {
+            const float* bb = bias + n0 + c0 + 4 * h;
+            o.x += __ldg(bb); o.y += __ldg(bb + 1); o.z += __ldg(bb + 2); o.w += __ldg(bb + 3);
+          }
+          if (a.accumulate) {
+            const float4 yo = y4[h];
+            o.x += yo.x; o.y += yo.y; o.z += yo.z; o.w += yo.w;
+          }
+          y4[h] = o;
+        }
+      } else if (yp) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const int n = n0 + c0 + j;
+          if (n < a.N) {
+            float o = (S > 0 ? vals[j] : 0.f) + (bias ? __ldg(bias + n) : 0.f);
+            if (a.accumulate) o += yp[n];
+            yp[n] = o;
+          }
+        }
+      }
+    }
+  }
+}
 
 // NKC: 16-byte channel chunks per row and stage (CB / 4 for tf32, CB / 8 for
 // bf16; compile-time, so the fill loops need no integer division).
@@ -354,97 +455,132 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
       tc::mbar_wait(done, 0);
       tc::fence_after();
     }
-    const int row = (warp & 3) * 32 + lane;
-    const int chalf = a.Ns / 2, cbeg = ((warp - 1) >> 2) * chalf, cend = cbeg + chalf;
-    const d2ip_act y = a.y;
-    const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16);
-    const float* bias = a.bias ? a.bias + b * a.bbs : nullptr;
-    for (int tt = 0; tt < T; ++tt) {
-      const int u = u0 + tt * kTcRows + row;
-      int v = -1, dq = 0, hq = 0, wq = 0;
-      {
-        const int dp = u / a.Sh, rem = u - dp * a.Sh;
-        const int hp = rem / a.Sw, wp = rem - hp * a.Sw;
-        if (dp >= 1 && dp <= a.gd && hp >= 1 && hp <= a.gh && wp >= 1 && wp <= a.gw) {
-          v = ((dp - 1) * a.gh + (hp - 1)) * a.gw + (wp - 1);
-          dq = dp - 1; hq = hp - 1; wq = wp - 1;
-        }
-      }
-      const uint32_t tcol = trow + (uint32_t)(tt * Ns);
-      if (MODE == 2) {  // column n = p * C_gx + ci -> gx voxel 2o + p (8 columns share p)
-        const int cy = y.c;
-        for (int c0 = cbeg; c0 < cend; c0 += 8) {
-          float vals[8];
-          tc::tmem_ld8(tcol + c0, vals);
-          const int n = n0 + c0;
-          if (v < 0 || n >= a.N) continue;
-          const int p = n / cy, ci = n - p * cy;
-          const int d2 = 2 * dq + (p >> 2), h2 = 2 * hq + ((p >> 1) & 1), w2 = 2 * wq + (p & 1);
-          if (d2 >= y.d || h2 >= y.h || w2 >= y.w) continue;
-          const long long vf = ((long long)d2 * y.h + h2) * y.w + w2;
-          if (a.kspl > 1) {
-            float* pp = a.part + (((long long)b * a.kspl + ks) * a.vout + vf) * cy + ci;
+    tc_epilogue<T, MODE>(a, tmem, b, n0, u0, ks, S, warp, lane);
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_free(tmem, a.tmem_cols);
+}
+
+// TMA-fed bf16 variant (stride 1 and 1^3 layers whose input has a bf16 twin):
+// one producer thread fetches each stage's activation window as whole padded
+// lines -- a 5-D tensor-map box (8 channels, W + 2 columns starting at w = -1,
+// one line, one plane, one sequence) per line and 8-channel chunk, the zero
+// padding of the virtual grid coming from the box's out-of-bounds fill -- and
+// the weight tiles as contiguous bulk copies, all completing on the stage's
+// mbarrier by byte count. The MMA thread starts its descriptors `pre` rows
+// into the first line. No per-row address work, no producer warps in the loop.
+template <int NKC, int T, int MODE>
+__global__ void __launch_bounds__(kTcThreads) conv_tma_k(const TcConv a, const __grid_constant__ CUtensorMap tmap) {
+  D2IP_PDL_ENTRY();
+  extern __shared__ __align__(1024) uint8_t smem[];
+  constexpr int CB = NKC * 8;
+  constexpr bool PW = MODE == 3;
+  constexpr int nt = PW ? 1 : 3, ntap = nt * nt;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int b = blockIdx.z;
+  const int ks = blockIdx.y % a.kspl;
+  const int n0 = (blockIdx.y / a.kspl) * a.Ns;
+  const int u0 = a.u_first + blockIdx.x * T * kTcRows;
+  const int Ns = a.Ns, LR = a.lrows;
+  const uint32_t Ab = (uint32_t)NKC * LR * 16, Bb = (uint32_t)ntap * NKC * Ns * 16;
+  const uint32_t Sb = (Ab + Bb + 127) & ~127u;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + 2 * Sb);
+  uint64_t* empty = full + 2;
+  uint64_t* done = empty + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
+  if (warp == 0) tc::tmem_alloc(tslot, a.tmem_cols);
+  if (tid == 0) {
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&full[i], 1);
+      tc::mbar_init(&empty[i], 1);
+    }
+    tc::mbar_init(done, 1);
+    tc::fence_mbar_init();
+  }
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tslot;
+  const int S_all = nt * a.n_cb;
+  const int s_lo = (int)((long long)ks * S_all / a.kspl), s_hi = (int)((long long)(ks + 1) * S_all / a.kspl);
+  const int S = s_hi - s_lo;
+  const int Hl = a.gh + 2;  // padded lines per plane
+  // first virtual row of a stage's window, its first padded line, and the row offset into it
+  auto window = [&](int s, int* L0, int* pre, int* cb) {
+    const int sg = s_lo + s, kdi = sg / a.n_cb;
+    *cb = sg - kdi * a.n_cb;
+    const int uws = PW ? u0 : u0 + (kdi - 1) * a.Sh - a.Sw - 1;
+    *L0 = uws / a.Sw;
+    *pre = uws - *L0 * a.Sw;
+    return kdi;
+  };
+  if (warp == 0) {
+    if (lane == 0) {
+      const uint32_t sbase = tc::smem_u32(smem);
+      const uint64_t dA = tc::make_desc(sbase, LR * 16, 128);
+      const uint64_t dB = tc::make_desc(sbase + Ab, Ns * 16, 128);
+      for (int s = 0; s < S; ++s) {
+        const int slot = s & 1;
+        int L0, pre, cb;
+        window(s, &L0, &pre, &cb);
+        tc::mbar_wait(&full[slot], (uint32_t)((s >> 1) & 1));
+        tc::fence_after();
+        const uint64_t so = slot ? (uint64_t)(Sb >> 4) : 0;
+        for (int tq = 0; tq < ntap; ++tq) {
+          const int rowoff = PW ? 0 : (tq / 3) * a.Sw + (tq % 3);
 #pragma unroll
-            for (int j = 0; j < 8; ++j) pp[j] = S > 0 ? vals[j] : 0.f;
-          } else {
-            float* yp = y.ptr + b * y.bstride + vf * y.cstride + ci;
+          for (int j = 0; j < NKC / 2; ++j) {
+            const uint64_t bo = so + (uint64_t)((tq * NKC + 2 * j) * Ns);
+            const uint32_t first = (s | tq | j) ? 1u : 0u;
 #pragma unroll
-            for (int j = 0; j < 8; ++j) {
-              float o = S > 0 ? vals[j] : 0.f;
-              if (a.accumulate) o += yp[j];
-              yp[j] = o;
+            for (int tt = 0; tt < T; ++tt) {
+              const uint64_t ao = so + (uint64_t)(2 * j * LR + pre + rowoff + tt * kTcRows);
+              tc::mma_f16(tmem + (uint32_t)(tt * Ns), dA + ao, dB + bo, a.idesc, first);
             }
           }
         }
-        continue;
+        tc::commit(&empty[slot]);
       }
-      if (a.kspl > 1) {  // raw partial sums; the consumer adds bias / accumulates
-        float* pp = v >= 0 ? a.part + (((long long)b * a.kspl + ks) * a.vout + v) * a.N : nullptr;
-        for (int c0 = cbeg; c0 < cend; c0 += 8) {
-          float vals[8];
-          tc::tmem_ld8(tcol + c0, vals);
-          if (pp) {
-#pragma unroll
-            for (int j = 0; j < 8; ++j)
-              if (n0 + c0 + j < a.N) pp[n0 + c0 + j] = S > 0 ? vals[j] : 0.f;
-          }
+      if (S > 0) tc::commit(done);
+    }
+  } else {
+    if (warp == 1) {
+      // ---- the producer warp: copies spread over its lanes, all asynchronous
+      const float* wpb = a.wp + b * a.wpbs;
+      const int kc_all = a.Kc >> 3;
+      for (int s = 0; s < S; ++s) {
+        const int slot = s & 1;
+        if (s >= 2) tc::mbar_wait(&empty[slot], (uint32_t)(((s >> 1) - 1) & 1));
+        int L0, pre, cb;
+        const int kdi = window(s, &L0, &pre, &cb);
+        const int nl = (pre + a.WR + a.Sw - 1) / a.Sw;  // lines covering the window
+        uint8_t* A = smem + slot * Sb;
+        uint8_t* Bt = A + Ab;
+        if (lane == 0) tc::mbar_expect_tx(&full[slot], (uint32_t)(NKC * nl * a.Sw * 16 + ntap * NKC * Ns * 16));
+        __syncwarp();
+        for (int i = lane; i < NKC * nl; i += 32) {
+          const int kc = i / nl, li = i - kc * nl;
+          const int L = L0 + li, dp = L / Hl, hp = L - dp * Hl;
+          tc::tma_load_5d(A + ((size_t)kc * LR + (size_t)li * a.Sw) * 16, &tmap, cb * CB + 8 * kc, -1, hp - 1, dp - 1,
+                          b, &full[slot]);
         }
-        continue;
-      }
-      float* yp = v >= 0 ? y.ptr + b * y.bstride + (long long)v * y.cstride : nullptr;
-      for (int c0 = cbeg; c0 < cend; c0 += 8) {
-        float vals[8];
-        tc::tmem_ld8(tcol + c0, vals);
-        if (yp && a.vec && n0 + c0 + 8 <= a.N) {
-          // 8 consecutive channels of one voxel: two 16-byte stores (one 32-byte sector)
-          float4* y4 = reinterpret_cast<float4*>(yp + n0 + c0);
-#pragma unroll
-          for (int h = 0; h < 2; ++h) {
-            float4 o = make_float4(S > 0 ? vals[4 * h] : 0.f, S > 0 ? vals[4 * h + 1] : 0.f,
-                                   S > 0 ? vals[4 * h + 2] : 0.f, S > 0 ? vals[4 * h + 3] : 0.f);
-            if (bias) {
-              const float* bb = bias + n0 + c0 + 4 * h;
-              o.x += __ldg(bb); o.y += __ldg(bb + 1); o.z += __ldg(bb + 2); o.w += __ldg(bb + 3);
-            }
-            if (a.accumulate) {
-              const float4 yo = y4[h];
-              o.x += yo.x; o.y += yo.y; o.z += yo.z; o.w += yo.w;
-            }
-            y4[h] = o;
-          }
-        } else if (yp) {
-#pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            const int n = n0 + c0 + j;
-            if (n < a.N) {
-              float o = (S > 0 ? vals[j] : 0.f) + (bias ? __ldg(bias + n) : 0.f);
-              if (a.accumulate) o += yp[n];
-              yp[n] = o;
-            }
-          }
+        const int kd = PW ? 0 : kdi;
+        const float* wk = wpb + ((long long)(kd * 9) * kc_all + cb * NKC) * a.Np * 4 + (long long)n0 * 4;
+        for (int q = lane; q < ntap * NKC; q += 32) {
+          const int tq = q / NKC, kcl = q % NKC;
+          const int t9 = PW ? 0 : tq;
+          tc::bulk_load(Bt + (size_t)q * Ns * 16, wk + ((long long)t9 * kc_all + kcl) * a.Np * 4, (uint32_t)Ns * 16,
+                        &full[slot]);
         }
       }
     }
+    if (S > 0) {
+      tc::mbar_wait(done, 0);
+      tc::fence_after();
+    }
+    __syncwarp();  // warp 1's producer lane rejoins before the aligned TMEM loads
+    tc_epilogue<T, MODE>(a, tmem, b, n0, u0, ks, S, warp, lane);
   }
   tc::fence_before();
   __syncthreads();
@@ -686,12 +822,15 @@ int conv_tc_pack(const float* w, long long wbs, int K, int N, int dgrad, float* 
 // small latency model -- waves x (serial stages per CTA + fixed prologue /
 // epilogue cost) -- because at these sizes a CTA's chain of dependent stages,
 // not the tensor pipe, sets the time.
+// tma: the window is fetched as whole padded lines (conv_tma_k): a channel
+// column holds lrows = ceil((WR + Sw - 1) / Sw) lines of Sw rows
 static bool tc_plan(int D, int H, int W, int K, int N, int batch, TcConv& a, int* tiles, int nt = 3,
-                    bool bf = false) {
+                    bool bf = false, bool tma = false) {
   a.N = N;
   a.Np = np_of(N);
   a.Kc = K;
-  a.Sw = W + 2;
+  // TMA: 8-row (128-byte) aligned line pitch -- every line box lands on a 128-byte boundary
+  a.Sw = tma ? (W + 2 + 7) / 8 * 8 : W + 2;
   a.Sh = (H + 2) * a.Sw;
   a.u_first = a.Sh + a.Sw + 1;
   const int u_last = D * a.Sh + H * a.Sw + W;
@@ -706,7 +845,8 @@ static bool tc_plan(int D, int H, int W, int K, int N, int batch, TcConv& a, int
   const bool large = (long long)tiles1 * batch >= 4LL * 296;
   for (int T : {1, 2, 4}) {
     if (T > 1 && (!large || nt == 2)) break;
-    const int wr = nt == 1 ? T * kTcRows : wr_of(a.Sw, T), wrp = wrp_of(wr);
+    const int wr = nt == 1 ? T * kTcRows : wr_of(a.Sw, T);
+    const int wrp = tma ? (wr + 2 * a.Sw - 2) / a.Sw * a.Sw : wrp_of(wr);
     const int tl = cdiv(tiles1, T);
     for (int ns = std::min(a.Np, 256); ns >= 16; ns -= 16) {
       if (a.Np % ns) continue;
@@ -741,6 +881,7 @@ static bool tc_plan(int D, int H, int W, int K, int N, int batch, TcConv& a, int
           a.T = T;
           a.WR = wr;
           a.WRp = wrp;
+          a.lrows = wrp;
           *tiles = tl;
         }
       }
@@ -807,6 +948,42 @@ static int tc_dispatch_nkc(const TcConv& a, dim3 grid, size_t smem, cudaStream_t
   return D2IP_OK;
 }
 
+template <int NKC, int T, int MODE>
+static int tma_launch(const TcConv& a, const CUtensorMap& tm, dim3 grid, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    D2IP_CUDA(cudaFuncSetAttribute(conv_tma_k<NKC, T, MODE>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    attr = true;
+  }
+  const size_t smem =
+      2 * (((size_t)NKC * a.lrows * 16 + (size_t)(MODE == 3 ? 1 : 9) * NKC * a.Ns * 16 + 127) & ~(size_t)127) + 64;
+  D2IP_CUDA(launch_pdl((conv_tma_k<NKC, T, MODE>), grid, kTcThreads, smem, st, a, tm));
+  return D2IP_OK;
+}
+
+template <int NKC>
+static int tma_dispatch(const TcConv& a, const CUtensorMap& tm, dim3 grid, cudaStream_t st, int mode) {
+  if (mode == 3) {
+    if (a.T == 4) return tma_launch<NKC, 4, 3>(a, tm, grid, st);
+    if (a.T == 2) return tma_launch<NKC, 2, 3>(a, tm, grid, st);
+    return tma_launch<NKC, 1, 3>(a, tm, grid, st);
+  }
+  if (a.T == 4) return tma_launch<NKC, 4, 0>(a, tm, grid, st);
+  if (a.T == 2) return tma_launch<NKC, 2, 0>(a, tm, grid, st);
+  return tma_launch<NKC, 1, 0>(a, tm, grid, st);
+}
+
+static int tma_dispatch_nkc(const TcConv& a, const CUtensorMap& tm, dim3 grid, cudaStream_t st, int mode) {
+  switch (a.CB / 8) {
+    case 2: return tma_dispatch<2>(a, tm, grid, st, mode);
+    case 4: return tma_dispatch<4>(a, tm, grid, st, mode);
+    case 8: return tma_dispatch<8>(a, tm, grid, st, mode);
+    case 16: return tma_dispatch<16>(a, tm, grid, st, mode);
+    default: D2IP_CHECK_ARG(false, "conv_tc: unsupported channel block %d", a.CB);
+  }
+  return D2IP_OK;
+}
+
 int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, long long bbs, d2ip_act y,
                 int accumulate, float* ws, size_t ws_bytes, int batch, cudaStream_t st, int* deferred, int mode) {
   const bool bf = (mode & kTcBf16) != 0;
@@ -822,7 +999,17 @@ int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, lo
   TcConv a{};
   int tiles = 0;
   const int ntm = mode == 3 ? 1 : mode ? 2 : 3;
-  D2IP_CHECK_ARG(tc_plan(g.d, g.h, g.w, K, N, batch, a, &tiles, ntm, bf),
+  // TMA-fed kernel (D2IP_TC_TMA=1): bf16 layers with a twin, stride 1 / 1^3, padded lines <= 256
+  // columns (box limit). Opt-in: with its 2-stage ring it measured slower than the eight-warp
+  // cp.async fill on most cfg4 layers (e.g. 96->32 fwd 235 vs 201 us, 64->64 64 vs 43 us; only
+  // the 96->32 data gradient won, 167 vs 182 us).
+  static const bool tma_on = [] {
+    const char* v = getenv("D2IP_TC_TMA");
+    return v && atoi(v) != 0;
+  }();
+  const bool use_tma = tma_on && bf && (mode == 0 || mode == 3) && x.bf16 && x.cstride % 8 == 0 && x.c % 8 == 0 &&
+                       ((uintptr_t)x.bf16 & 15) == 0 && x.w + 2 <= 256;
+  D2IP_CHECK_ARG(tc_plan(g.d, g.h, g.w, K, N, batch, a, &tiles, ntm, bf, use_tma),
                  "conv_tc: no channel blocking fits shared memory (K=%d N=%d W=%d)", K, N, g.w);
   a.mode = mode;
   a.t0 = mode == 2 ? 1 : 0;
@@ -848,7 +1035,7 @@ int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, lo
   while (cols < a.T * a.Ns) cols *= 2;
   a.tmem_cols = cols;
   a.idesc = tc::make_idesc(bf ? 1 : 2, kTcRows, a.Ns);
-  const size_t smem = tc_smem_bytes(a);
+  const size_t smem = use_tma ? 0 : tc_smem_bytes(a);  // (the TMA kernel sizes its own)
   const dim3 grid(tiles, (a.Np / a.Ns) * a.kspl, batch);
   // one producer group (all eight warps per stage) measured faster than two on
   // cfg1 (1029 vs 1013 it/s) and cfg2 (280 vs 274); D2IP_TC_PG=2 selects two
@@ -857,7 +1044,20 @@ int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, lo
     return v && atoi(v) == 2;
   }();
   int rc;
-  if (bf)
+  if (use_tma) {
+    // tensor map over the bf16 twin: dims (C, W, H, D, B) innermost first, one padded line per box
+    CUtensorMap tm;
+    const cuuint64_t gdim[5] = {(cuuint64_t)x.c, (cuuint64_t)x.w, (cuuint64_t)x.h, (cuuint64_t)x.d,
+                                (cuuint64_t)batch};
+    const cuuint64_t gstr[4] = {(cuuint64_t)x.cstride * 2, (cuuint64_t)x.w * x.cstride * 2,
+                                (cuuint64_t)x.h * x.w * x.cstride * 2, (cuuint64_t)x.bstride * 2};
+    const cuuint32_t box[5] = {8, (cuuint32_t)a.Sw, 1, 1, 1}, estr[5] = {1, 1, 1, 1, 1};
+    const CUresult cr = cuTensorMapEncodeTiled(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, x.bf16, gdim, gstr, box, estr,
+                                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    D2IP_CHECK_ARG(cr == CUDA_SUCCESS, "conv_tc: cuTensorMapEncodeTiled failed (%d)", (int)cr);
+    rc = tma_dispatch_nkc(a, tm, grid, st, mode);
+  } else if (bf)
     rc = tc_dispatch_nkc<true>(a, grid, smem, st, mode, false);
   else
     rc = tc_dispatch_nkc<false>(a, grid, smem, st, mode, pg2);
@@ -869,7 +1069,8 @@ int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, lo
                          a.vout, Nout, bias, bbs, y, accumulate));
     D2IP_LAUNCH_CHECK();
   }
-  set_variant(bf ? (a.kspl > 1 ? "tcgen05_bf16_splitk" : "tcgen05_bf16")
+  set_variant(use_tma ? (a.kspl > 1 ? "tcgen05_bf16_tma_splitk" : "tcgen05_bf16_tma")
+              : bf ? (a.kspl > 1 ? "tcgen05_bf16_splitk" : "tcgen05_bf16")
                  : (a.kspl > 1 ? "tcgen05_tf32x3_splitk" : "tcgen05_tf32x3"));
   return D2IP_OK;
 }
