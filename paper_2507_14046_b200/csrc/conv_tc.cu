@@ -96,17 +96,19 @@ struct TcConv {
   int vec;         // y rows (and bias) 16-byte aligned: float4 epilogue stores
   int xtw;         // bf16: stream x from its bf16 twin (cp.async) instead of converting fp32 rows
   int lrows;       // TMA path: rows per channel-chunk column (whole padded lines: maxlines x Sw)
+  int b3;          // 3xbf16 (TF32-precision layer): hi + lo bf16 operands, three MMAs per K step
 };
 
 // Per stage: A hi + A lo windows, B hi + B lo tiles (nt^2 taps); bf16: one
 // A window and one B tile of 2-byte elements.
-static size_t stage_bytes(int cb, int np, int wrp, int nt = 3, bool bf = false) {
+static size_t stage_bytes(int cb, int np, int wrp, int nt = 3, bool bf = false, bool b3 = false) {
+  if (b3) return 2 * ((size_t)cb * wrp * 2 + (size_t)nt * nt * cb * np * 2);
   if (bf) return (size_t)cb * wrp * 2 + (size_t)nt * nt * cb * np * 2;
   return 2 * ((size_t)cb * wrp * 4 + (size_t)nt * nt * cb * np * 4);
 }
 
 static size_t tc_smem_bytes(const TcConv& a) {
-  return 2 * stage_bytes(a.CB, a.Ns, a.WRp, a.nt, a.bf) + 3 * a.WR * sizeof(int) + 8 + 5 * 8 + 16;
+  return 2 * stage_bytes(a.CB, a.Ns, a.WRp, a.nt, a.bf, a.b3) + 3 * a.WR * sizeof(int) + 8 + 5 * 8 + 16;
 }
 
 __device__ __forceinline__ uint32_t bf2(float a, float b) {
@@ -221,12 +223,15 @@ __device__ __forceinline__ void tc_epilogue(const TcConv& a, uint32_t tmem, int 
 // groups of four fill alternate stages, two stages in flight).
 // MODE: 0 stride 1, 1 / 2 stride-2 forward / data gradient (compile-time, so
 // the stride-1 issue loop keeps its constant tap arithmetic).
-template <int NKC, int T, int PG, int MODE, bool BF = false>
+// BFM: 0 3xTF32, 1 bf16, 2 3xbf16 (x = hi + lo in bf16, hi*hi + hi*lo + lo*hi on kind::f16:
+// ~2^-16 per product, for the TF32-precision configs at half the MMAs of 3xTF32)
+template <int NKC, int T, int PG, int MODE, int BFM = 0>
 __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
+  constexpr bool BF = BFM != 0, B3 = BFM == 2;
   D2IP_PDL_ENTRY();
   extern __shared__ __align__(1024) uint8_t smem[];
   constexpr int CB = NKC * (BF ? 8 : 4);
-  constexpr int NH = BF ? 1 : 2;  // operand halves per stage (3xTF32: hi, lo)
+  constexpr int NH = BFM == 1 ? 1 : 2;  // operand halves per stage (3xTF32 / 3xbf16: hi, lo)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const int b = blockIdx.z;
   const int ks = blockIdx.y % a.kspl;
@@ -314,7 +319,11 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
             for (int tt = 0; tt < T; ++tt) {  // sub-tile tt: rows + 128 tt, accumulator columns + tt Ns
               const uint64_t ao = boff + (uint64_t)(2 * j * WRp + rowoff + tt * kTcRows);
               const uint32_t d = tmem + (uint32_t)(tt * Ns);
-              if (BF) {
+              if (B3) {
+                tc::mma_f16(d, dAlo + ao, dBhi + bo, a.idesc, first);
+                tc::mma_f16(d, dAhi + ao, dBlo + bo, a.idesc, 1u);
+                tc::mma_f16(d, dAhi + ao, dBhi + bo, a.idesc, 1u);
+              } else if (BF) {
                 tc::mma_f16(d, dAhi + ao, dBhi + bo, a.idesc, first);
               } else {
                 tc::mma_tf32(d, dAlo + ao, dBhi + bo, a.idesc, first);
@@ -341,7 +350,7 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
       const int kd = PW ? 0 : t0 + kdi;
       const int* rm = rowmap + kd * WR;
       uint8_t* A = smem + slot * Sb;
-      if (BF && a.xtw) {
+      if (BF && !B3 && a.xtw) {
         // bf16 twin of x: one 16-byte async copy per (row, 8-channel chunk); zero-fill for padding rows
         const uint16_t* xt = reinterpret_cast<const uint16_t*>(x.bf16) + b * x.bstride;
         const long long plane = (long long)x.h * x.w;
@@ -394,6 +403,12 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
             o.x = bf2(v[q].x, v[q].y);
             o.y = bf2(v[q].z, v[q].w);
             *reinterpret_cast<uint2*>(A + ((size_t)(pc >> 1) * WRp + r) * 16 + (pc & 1) * 8) = o;
+            if (B3) {  // lo = bf16(x - hi)
+              const float2 h0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&o.x));
+              const float2 h1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&o.y));
+              const uint2 l = make_uint2(bf2(v[q].x - h0.x, v[q].y - h0.y), bf2(v[q].z - h1.x, v[q].w - h1.y));
+              *reinterpret_cast<uint2*>(A + Ab + ((size_t)(pc >> 1) * WRp + r) * 16 + (pc & 1) * 8) = l;
+            }
           }
         }
       } else if (MODE == 1) {
@@ -430,7 +445,7 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
         uint8_t* dst = Bt + (size_t)q * Ns * 16;
         for (int n = lane; n < Ns; n += 32) {
           tc::cp_async16(dst + n * 16, src + n * 4, 16u);
-          if (!BF) tc::cp_async16(dst + Bb + n * 16, src + a.wlo + n * 4, 16u);
+          if (NH == 2) tc::cp_async16(dst + Bb + n * 16, src + a.wlo + n * 4, 16u);
         }
       }
       tc::cp_async_commit();
@@ -636,7 +651,7 @@ __device__ __forceinline__ float pack_val(const float* wb, int K, int N, int cod
 //   stride 2: the parity layouts of pack_val (codes 2, 3)
 // bf16 (code & kTcBf16): [b][tap][K/8][Np][8] bf16, element i of `half`.
 __device__ __forceinline__ void pack_bf16(const float* wb, int K, int N, int Np, int code, long long i,
-                                          __nv_bfloat16* out) {
+                                          __nv_bfloat16* out, __nv_bfloat16* lo = nullptr) {
   const int j = (int)(i & 7);
   const long long q = i >> 3;
   const int n = (int)(q % Np);
@@ -644,7 +659,9 @@ __device__ __forceinline__ void pack_bf16(const float* wb, int K, int N, int Np,
   const int kc = (int)(q2 % (K / 8));
   const int t = (int)(q2 / (K / 8));
   const float val = n < N ? pack_val(wb, K, N, code, t, 8 * kc + j, n) : 0.f;
-  out[i] = __float2bfloat16_rn(val);
+  const __nv_bfloat16 h = __float2bfloat16_rn(val);
+  out[i] = h;
+  if (lo) lo[i] = __float2bfloat16_rn(val - __bfloat162float(h));  // 3xbf16: the residual
 }
 
 __global__ void conv_tc_pack_k(const float* __restrict__ w, long long wbs, int K, int N, int Np, int dgrad,
@@ -653,8 +670,9 @@ __global__ void conv_tc_pack_k(const float* __restrict__ w, long long wbs, int K
   const int b = blockIdx.y;
   const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= half) return;
-  if (dgrad & kTcBf16) {
-    pack_bf16(w + b * wbs, K, N, Np, dgrad, i, reinterpret_cast<__nv_bfloat16*>(out + b * obs));
+  if (dgrad & (kTcBf16 | kTcBf3)) {
+    pack_bf16(w + b * wbs, K, N, Np, dgrad, i, reinterpret_cast<__nv_bfloat16*>(out + b * obs),
+              (dgrad & kTcBf3) ? reinterpret_cast<__nv_bfloat16*>(out + b * obs + obs / 2) : nullptr);
     return;
   }
   const int j = (int)(i & 3);
@@ -677,9 +695,11 @@ __global__ void conv_tc_pack_k(const float* __restrict__ w, long long wbs, int K
 // without a tap) are never written: they stay zero from the workspace clear.
 __device__ __forceinline__ void pack_put(float* out, long long obs, int code, int K, int Np, int t, int k, int n,
                                          float val) {
-  if (code & kTcBf16) {
+  if (code & (kTcBf16 | kTcBf3)) {
     const long long i = (((long long)t * (K / 8) + k / 8) * Np + n) * 8 + (k & 7);
-    reinterpret_cast<__nv_bfloat16*>(out)[i] = __float2bfloat16_rn(val);
+    const __nv_bfloat16 h = __float2bfloat16_rn(val);
+    reinterpret_cast<__nv_bfloat16*>(out)[i] = h;
+    if (code & kTcBf3) reinterpret_cast<__nv_bfloat16*>(out + obs / 2)[i] = __float2bfloat16_rn(val - __bfloat162float(h));
   } else {
     const long long i = (((long long)t * (K / 4) + k / 4) * Np + n) * 4 + (k & 3);
     const float hi = tf32_hi(val);
@@ -766,6 +786,14 @@ bool conv_tc_supported(int cin, int cout, int ks, int stride, int precision) {
   return true;
 }
 
+static bool tf32_bf3() {
+  static const bool on = [] {
+    const char* v = getenv("D2IP_TF32_BF3");
+    return !v || atoi(v) != 0;
+  }();
+  return on;
+}
+
 bool conv_tc_layer(int cin, int cout, int ks, int stride, int dgrad, int precision, long long vout, TcDims* d) {
   TcDims r{};
   if (stride == 1) {
@@ -778,6 +806,11 @@ bool conv_tc_layer(int cin, int cout, int ks, int stride, int dgrad, int precisi
     if (precision == D2IP_PREC_BF16 && r.K % 16 == 0) {
       r.mode |= kTcBf16;
       r.pack |= kTcBf16;
+    }
+    // TF32 precision: 3xbf16 (D2IP_TF32_BF3=0 keeps 3xTF32)
+    if (precision == D2IP_PREC_TF32 && r.K % 16 == 0 && tf32_bf3()) {
+      r.mode |= kTcBf3;
+      r.pack |= kTcBf3;
     }
   } else {
     // Below ~4M output-voxel x channel-pair products the direct CUDA-core kernel
@@ -802,6 +835,10 @@ bool conv_tc_layer(int cin, int cout, int ks, int stride, int dgrad, int precisi
       r.mode |= kTcBf16;
       r.pack |= kTcBf16;
     }
+    if (precision == D2IP_PREC_TF32 && r.K % 16 == 0 && (dgrad || cin % 8 == 0) && tf32_bf3()) {
+      r.mode |= kTcBf3;
+      r.pack |= kTcBf3;
+    }
   }
   if (d) *d = r;
   return true;
@@ -825,7 +862,8 @@ int conv_tc_pack(const float* w, long long wbs, int K, int N, int dgrad, float* 
 // tma: the window is fetched as whole padded lines (conv_tma_k): a channel
 // column holds lrows = ceil((WR + Sw - 1) / Sw) lines of Sw rows
 static bool tc_plan(int D, int H, int W, int K, int N, int batch, TcConv& a, int* tiles, int nt = 3,
-                    bool bf = false, bool tma = false) {
+                    bool bf = false, bool tma = false, bool b3 = false) {
+  if (b3) bf = true;
   a.N = N;
   a.Np = np_of(N);
   a.Kc = K;
@@ -853,7 +891,7 @@ static bool tc_plan(int D, int H, int W, int K, int N, int batch, TcConv& a, int
       if (T * ns > 512) continue;  // TMEM columns
       for (int cb = bf ? 16 : 8; cb <= K && cb <= (bf ? 128 : 64); cb *= 2) {
         if (K % cb) continue;
-        const size_t sm = 2 * stage_bytes(cb, ns, wrp, nt, bf) + 3 * wr * sizeof(int) + 64;
+        const size_t sm = 2 * stage_bytes(cb, ns, wrp, nt, bf, b3) + 3 * wr * sizeof(int) + 64;
         if (sm > (size_t)210 * 1024) continue;
         const int per_sm = sm <= (size_t)110 * 1024 ? 2 : 1;
         const long long ctas0 = (long long)tl * (a.Np / ns) * batch;
@@ -867,8 +905,8 @@ static bool tc_plan(int D, int H, int W, int K, int N, int batch, TcConv& a, int
         } else {
           // bf16: one MMA per 16 channels at max(N/2, (4096 + 32 N)/128) + issue cycles
           const double mma_us =
-              bf ? nt * nt * (cb / 16.0) * T * (std::max(ns / 2.0, (4096.0 + 32.0 * ns) / 128.0) + 6.0) / 1900.0 *
-                       (per_sm == 2 ? 1.4 : 1.0)
+              bf ? (b3 ? 3.0 : 1.0) * nt * nt * (cb / 16.0) * T * (std::max(ns / 2.0, (4096.0 + 32.0 * ns) / 128.0) + 6.0) /
+                       1900.0 * (per_sm == 2 ? 1.4 : 1.0)
                  : 3.0 * nt * nt / 8.0 * cb * T * 57.0 / 1900.0 * (per_sm == 2 ? 1.4 : 1.0);
           const double stage_us = std::max(1.5, mma_us);
           cost = (double)waves * ((S + kspl - 1) / kspl * stage_us + 2.0 + 0.5 * T) + (kspl > 1 ? 3.0 : 0.0);
@@ -890,6 +928,7 @@ static bool tc_plan(int D, int H, int W, int K, int N, int batch, TcConv& a, int
   if (a.CB < 8) return false;
   a.n_cb = K / a.CB;
   a.bf = bf;
+  a.b3 = b3;
   return true;
 }
 
@@ -897,14 +936,16 @@ size_t conv_tc_ws_bytes(int D, int H, int W, int K, int N, int batch, int mode) 
   TcConv a{};
   int tiles;
   const int m3 = mode & 3;
-  if (!tc_plan(D, H, W, K, N, batch, a, &tiles, m3 == 3 ? 1 : m3 ? 2 : 3, (mode & kTcBf16) != 0) || a.kspl <= 1)
+  if (!tc_plan(D, H, W, K, N, batch, a, &tiles, m3 == 3 ? 1 : m3 ? 2 : 3, (mode & kTcBf16) != 0, false,
+               (mode & kTcBf3) != 0) ||
+      a.kspl <= 1)
     return 0;
   // mode 2 partials are [V_gx][C_gx]: V_gx C_gx <= 8 V N / 8 (gx dims <= 2 x the row grid)
   return (size_t)batch * a.kspl * a.vout * N * sizeof(float);
 }
 
 // Launch one instantiation (the >48 KB shared-memory opt-in is set on first use).
-template <int NKC, int T, int PG, int MODE, bool BF>
+template <int NKC, int T, int PG, int MODE, int BF>
 static int tc_launch(const TcConv& a, dim3 grid, size_t smem, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
@@ -916,7 +957,7 @@ static int tc_launch(const TcConv& a, dim3 grid, size_t smem, cudaStream_t st) {
   return D2IP_OK;
 }
 
-template <int NKC, bool BF>
+template <int NKC, int BF>
 static int tc_dispatch(const TcConv& a, dim3 grid, size_t smem, cudaStream_t st, int mode, bool pg2) {
   if (mode == 1) return tc_launch<NKC, 1, 1, 1, BF>(a, grid, smem, st);
   if (mode == 2) return tc_launch<NKC, 1, 1, 2, BF>(a, grid, smem, st);
@@ -925,7 +966,7 @@ static int tc_dispatch(const TcConv& a, dim3 grid, size_t smem, cudaStream_t st,
     if (a.T == 2) return tc_launch<NKC, 2, 1, 3, BF>(a, grid, smem, st);
     return tc_launch<NKC, 1, 1, 3, BF>(a, grid, smem, st);
   }
-  if (!BF && pg2) {
+  if (BF == 0 && pg2) {
     if (a.T == 4) return tc_launch<NKC, 4, 2, 0, BF>(a, grid, smem, st);
     if (a.T == 2) return tc_launch<NKC, 2, 2, 0, BF>(a, grid, smem, st);
     return tc_launch<NKC, 1, 2, 0, BF>(a, grid, smem, st);
@@ -936,9 +977,9 @@ static int tc_dispatch(const TcConv& a, dim3 grid, size_t smem, cudaStream_t st,
 }
 
 // NKC = 16-byte chunks per row: CB / 4 (tf32, CB 8..64) or CB / 8 (bf16, CB 16..128)
-template <bool BF>
+template <int BF>
 static int tc_dispatch_nkc(const TcConv& a, dim3 grid, size_t smem, cudaStream_t st, int mode, bool pg2) {
-  switch (a.CB / (BF ? 8 : 4)) {
+  switch (a.CB / (BF != 0 ? 8 : 4)) {
     case 2: return tc_dispatch<2, BF>(a, grid, smem, st, mode, pg2);
     case 4: return tc_dispatch<4, BF>(a, grid, smem, st, mode, pg2);
     case 8: return tc_dispatch<8, BF>(a, grid, smem, st, mode, pg2);
@@ -986,7 +1027,8 @@ static int tma_dispatch_nkc(const TcConv& a, const CUtensorMap& tm, dim3 grid, c
 
 int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, long long bbs, d2ip_act y,
                 int accumulate, float* ws, size_t ws_bytes, int batch, cudaStream_t st, int* deferred, int mode) {
-  const bool bf = (mode & kTcBf16) != 0;
+  const bool b3 = (mode & kTcBf3) != 0;
+  const bool bf = b3 || (mode & kTcBf16) != 0;
   mode &= 3;
   D2IP_CHECK_ARG(!bf || K % 16 == 0, "conv_tc: bf16 needs K %% 16 == 0 (K=%d)", K);
   D2IP_CHECK_ARG((mode == 1 ? 8 * x.c : x.c) == K && (mode == 2 ? 8 * y.c : y.c) == N, "conv_tc: channel mismatch");
@@ -1007,9 +1049,9 @@ int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, lo
     const char* v = getenv("D2IP_TC_TMA");
     return v && atoi(v) != 0;
   }();
-  const bool use_tma = tma_on && bf && (mode == 0 || mode == 3) && x.bf16 && x.cstride % 8 == 0 && x.c % 8 == 0 &&
+  const bool use_tma = tma_on && bf && !b3 && (mode == 0 || mode == 3) && x.bf16 && x.cstride % 8 == 0 && x.c % 8 == 0 &&
                        ((uintptr_t)x.bf16 & 15) == 0 && x.w + 2 <= 256;
-  D2IP_CHECK_ARG(tc_plan(g.d, g.h, g.w, K, N, batch, a, &tiles, ntm, bf, use_tma),
+  D2IP_CHECK_ARG(tc_plan(g.d, g.h, g.w, K, N, batch, a, &tiles, ntm, bf, use_tma, b3),
                  "conv_tc: no channel blocking fits shared memory (K=%d N=%d W=%d)", K, N, g.w);
   a.mode = mode;
   a.t0 = mode == 2 ? 1 : 0;
@@ -1030,7 +1072,7 @@ int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, lo
   a.y = y;
   a.accumulate = accumulate;
   a.vec = y.cstride % 4 == 0 && ((uintptr_t)y.ptr & 15) == 0;
-  a.xtw = bf && x.bf16 && x.cstride % 8 == 0 && x.c % 8 == 0 && ((uintptr_t)x.bf16 & 15) == 0;
+  a.xtw = bf && !b3 && x.bf16 && x.cstride % 8 == 0 && x.c % 8 == 0 && ((uintptr_t)x.bf16 & 15) == 0;
   int cols = 32;
   while (cols < a.T * a.Ns) cols *= 2;
   a.tmem_cols = cols;
@@ -1057,10 +1099,12 @@ int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, lo
                                                CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     D2IP_CHECK_ARG(cr == CUDA_SUCCESS, "conv_tc: cuTensorMapEncodeTiled failed (%d)", (int)cr);
     rc = tma_dispatch_nkc(a, tm, grid, st, mode);
-  } else if (bf)
-    rc = tc_dispatch_nkc<true>(a, grid, smem, st, mode, false);
+  } else if (b3)
+    rc = tc_dispatch_nkc<2>(a, grid, smem, st, mode, false);
+  else if (bf)
+    rc = tc_dispatch_nkc<1>(a, grid, smem, st, mode, false);
   else
-    rc = tc_dispatch_nkc<false>(a, grid, smem, st, mode, pg2);
+    rc = tc_dispatch_nkc<0>(a, grid, smem, st, mode, pg2);
   D2IP_RET(rc);
   D2IP_LAUNCH_CHECK();
   if (deferred) *deferred = a.kspl > 1 ? a.kspl : 0;
@@ -1069,7 +1113,8 @@ int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, lo
                          a.vout, Nout, bias, bbs, y, accumulate));
     D2IP_LAUNCH_CHECK();
   }
-  set_variant(use_tma ? (a.kspl > 1 ? "tcgen05_bf16_tma_splitk" : "tcgen05_bf16_tma")
+  set_variant(b3 ? (a.kspl > 1 ? "tcgen05_bf16x3_splitk" : "tcgen05_bf16x3")
+              : use_tma ? (a.kspl > 1 ? "tcgen05_bf16_tma_splitk" : "tcgen05_bf16_tma")
               : bf ? (a.kspl > 1 ? "tcgen05_bf16_splitk" : "tcgen05_bf16")
                  : (a.kspl > 1 ? "tcgen05_tf32x3_splitk" : "tcgen05_tf32x3"));
   return D2IP_OK;

@@ -68,6 +68,7 @@ bool conv_tc_supported(int cin, int cout, int ks, int stride, int precision);
 // both carry kTcBf16 when the layer runs with bf16 operands (kind::f16).
 constexpr int kTcBf16 = 4;
 constexpr int kTcPw = 8;  // pack code: 1^3 weights (mode 3)
+constexpr int kTcBf3 = 16;  // mode / pack code: TF32-precision layer on 3xbf16 (hi + lo split) kind::f16 MMAs
 struct TcDims {
   int K, N, mode, pack;
 };
