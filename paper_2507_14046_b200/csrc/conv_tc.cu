@@ -786,7 +786,7 @@ bool conv_tc_supported(int cin, int cout, int ks, int stride, int precision) {
   return true;
 }
 
-static bool tf32_bf3() {
+bool tf32_bf3_enabled() {
   static const bool on = [] {
     const char* v = getenv("D2IP_TF32_BF3");
     return !v || atoi(v) != 0;
@@ -808,7 +808,7 @@ bool conv_tc_layer(int cin, int cout, int ks, int stride, int dgrad, int precisi
       r.pack |= kTcBf16;
     }
     // TF32 precision: 3xbf16 (D2IP_TF32_BF3=0 keeps 3xTF32)
-    if (precision == D2IP_PREC_TF32 && r.K % 16 == 0 && tf32_bf3()) {
+    if (precision == D2IP_PREC_TF32 && r.K % 16 == 0 && tf32_bf3_enabled()) {
       r.mode |= kTcBf3;
       r.pack |= kTcBf3;
     }
@@ -835,7 +835,7 @@ bool conv_tc_layer(int cin, int cout, int ks, int stride, int dgrad, int precisi
       r.mode |= kTcBf16;
       r.pack |= kTcBf16;
     }
-    if (precision == D2IP_PREC_TF32 && r.K % 16 == 0 && (dgrad || cin % 8 == 0) && tf32_bf3()) {
+    if (precision == D2IP_PREC_TF32 && r.K % 16 == 0 && (dgrad || cin % 8 == 0) && tf32_bf3_enabled()) {
       r.mode |= kTcBf3;
       r.pack |= kTcBf3;
     }

@@ -53,10 +53,11 @@ int wgrad_tc(d2ip_act x, d2ip_act gy, int ks, float* gw, long long gwbs, void* w
              cudaStream_t st);
 
 // wgrad_bf.cu — tcgen05 kind::f16 weight gradient of 3^3 (stride 1 and 2) / 1^3 convolutions (bf16 layers)
-bool wgrad_bf_supported(d2ip_act x, d2ip_act gy, int ks, int stride = 1);
+// b3: a TF32-precision layer on 3xbf16 (hi + lo operands, three MMAs per K step)
+bool wgrad_bf_supported(d2ip_act x, d2ip_act gy, int ks, int stride = 1, bool b3 = false);
 size_t wgrad_bf_ws_bytes(int D, int H, int W, int Cin, int Cout, int ks, int batch);
 int wgrad_bf(d2ip_act x, d2ip_act gy, int ks, float* gw, long long gwbs, void* ws, size_t ws_bytes, int batch,
-             cudaStream_t st, int stride = 1);
+             cudaStream_t st, int stride = 1, bool b3 = false);
 // fixed-order reduction of [b][rg][ntaps][Cin][Cout] + [Cout] partials into OIDHW + bias
 int wgrad_reduce(const float* part, int nrg, int ntaps, int Cin, int Cout, float* gw, long long gwbs, int batch,
                  cudaStream_t st);
@@ -69,6 +70,8 @@ bool conv_tc_supported(int cin, int cout, int ks, int stride, int precision);
 constexpr int kTcBf16 = 4;
 constexpr int kTcPw = 8;  // pack code: 1^3 weights (mode 3)
 constexpr int kTcBf3 = 16;  // mode / pack code: TF32-precision layer on 3xbf16 (hi + lo split) kind::f16 MMAs
+// TF32-precision layers run 3xbf16 tensor-core kernels (D2IP_TF32_BF3=0: 3xTF32)
+bool tf32_bf3_enabled();
 struct TcDims {
   int K, N, mode, pack;
 };

@@ -62,7 +62,9 @@ struct WgBf {
   int nchunk, chunks_per_rg, nrg;
   int tmem_cols;
   int gshift;         // log2(C_out / 4): float4 pieces per gy row
-  uint32_t Sx, Sb;    // bytes: x region of a stage, whole stage
+  uint32_t Sx, Sb;    // bytes: x region of a stage (one half), whole stage
+  uint32_t Sg;        // bytes: gy region (one half)
+  int b3;             // 3xbf16: [x hi][x lo][gy hi][gy lo], three MMAs (lo*hi, hi*lo, hi*hi) per K step
   uint32_t pad;       // bytes after the last stage the M = 64 MMA may read past a small x block
   uint32_t idesc;
   int xtw, gtw;       // stream x / gy from their bf16 twins with cp.async (else fp32 loads + conversion)
@@ -79,6 +81,13 @@ __device__ __forceinline__ void cp_async16_ca(void* dst_smem, const void* src, u
 }
 
 static inline int r8(int v) { return (v + 7) & ~7; }
+
+// lo = bf16(x - hi) of four values whose bf16 hi pair is h (3xbf16 split)
+__device__ __forceinline__ uint2 bf16_lo(const float4& v, uint2 h) {
+  const float2 h0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&h.x));
+  const float2 h1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&h.y));
+  return make_uint2(bf16x2(v.x - h0.x, v.y - h0.y), bf16x2(v.z - h1.x, v.w - h1.y));
+}
 
 __device__ __forceinline__ uint32_t bf2w(float a, float b) {
   const __nv_bfloat162 h = __floats2bfloat162_rn(a, b);
@@ -120,7 +129,7 @@ __device__ __forceinline__ int wb_base(const WgBf& a, int grp) {
 // descriptors advanced by constant adds -- tools/umma_chains.cu measured a
 // general per-MMA descriptor computation at ~140-390 cycles per MMA, against
 // ~40 for the operand reads themselves).
-template <int NCX, int NKH, int NMMA>
+template <int NCX, int NKH, int NMMA, bool B3>
 __global__ void __launch_bounds__(kWbThreads) wgrad_bf_k(WgBf a) {
   D2IP_PDL_ENTRY();
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -163,7 +172,8 @@ __global__ void __launch_bounds__(kWbThreads) wgrad_bf_k(WgBf a) {
     if (lane == 0) {
       const uint32_t sbase = tc::smem_u32(smem);
       const uint64_t dA0 = tc::make_desc(sbase, 128, WRp * 16);
-      const uint64_t dB0 = tc::make_desc(sbase + a.Sx, 128, RSp * 16);
+      const uint64_t dB0 = tc::make_desc(sbase + (B3 ? 2 : 1) * a.Sx, 128, RSp * 16);
+      const uint32_t xlo16 = a.Sx >> 4, glo16 = a.Sg >> 4;  // B3: the lo halves
       const uint32_t cpy16 = ((uint32_t)a.ngc * RSp * 16) >> 4;  // one gy copy
       const uint32_t sw16 = (uint32_t)a.Sw;                       // one kh row: Sw rows x 16 B
       const uint32_t idesc = a.idesc, N = a.N;
@@ -188,9 +198,18 @@ __global__ void __launch_bounds__(kWbThreads) wgrad_bf_k(WgBf a) {
 #pragma unroll
           for (int kh = 0; kh < NKH; ++kh)
 #pragma unroll
-            for (int c = 0; c < NMMA; ++c)
-              tc::mma_f16(tmem + (uint32_t)(kh * NMMA + c) * N, da + (uint64_t)(kh * sw16 + aoff[c]),
-                          db + (uint64_t)(stacked ? c * cpy16 : bsh + c * a.bstep), idesc, acc);
+            for (int c = 0; c < NMMA; ++c) {
+              const uint32_t d = tmem + (uint32_t)(kh * NMMA + c) * N;
+              const uint64_t aa = da + (uint64_t)(kh * sw16 + aoff[c]);
+              const uint64_t bb = db + (uint64_t)(stacked ? c * cpy16 : bsh + c * a.bstep);
+              if (B3) {
+                tc::mma_f16(d, aa + xlo16, bb, idesc, acc);
+                tc::mma_f16(d, aa, bb + glo16, idesc, 1u);
+                tc::mma_f16(d, aa, bb, idesc, 1u);
+              } else {
+                tc::mma_f16(d, aa, bb, idesc, acc);
+              }
+            }
         }
         tc::commit(&empty[slot]);
       }
@@ -246,7 +265,7 @@ __global__ void __launch_bounds__(kWbThreads) wgrad_bf_k(WgBf a) {
       }
       asm volatile("bar.sync 1, 256;" ::: "memory");
       uint8_t* X = smem + (size_t)slot * a.Sb;
-      uint8_t* Gs = X + a.Sx;
+      uint8_t* Gs = X + (B3 ? 2 : 1) * a.Sx;
       // x window rows [xr0, WR): NCX float4 pieces per row -> bf16 halves of 16-byte group rows
       constexpr int NP = NCX;
       const int nX = a.xtw ? 0 : (WR - xr0) * NP;
@@ -291,8 +310,9 @@ __global__ void __launch_bounds__(kWbThreads) wgrad_bf_k(WgBf a) {
           const int i = i0 + q * kWbProd;
           if (i >= nX) continue;
           const int r = xr0 + i / NP, pc = i % NP;
-          *reinterpret_cast<uint2*>(X + ((size_t)(pc >> 1) * WRp + r) * 16 + (pc & 1) * 8) =
-              make_uint2(bf2w(v[q].x, v[q].y), bf2w(v[q].z, v[q].w));
+          const uint2 h = make_uint2(bf2w(v[q].x, v[q].y), bf2w(v[q].z, v[q].w));
+          *reinterpret_cast<uint2*>(X + ((size_t)(pc >> 1) * WRp + r) * 16 + (pc & 1) * 8) = h;
+          if (B3) *reinterpret_cast<uint2*>(X + a.Sx + ((size_t)(pc >> 1) * WRp + r) * 16 + (pc & 1) * 8) = bf16_lo(v[q], h);
         }
       }
       // gy map rows m = 0 .. RS + 1 (row v0 - 1 + m); copy c row j = map row j + 2 - c
@@ -338,10 +358,14 @@ __global__ void __launch_bounds__(kWbThreads) wgrad_bf_k(WgBf a) {
           }
           if (a.gtw) continue;  // fp32 pass for the bias only
           const uint2 o = make_uint2(bf2w(v[q].x, v[q].y), bf2w(v[q].z, v[q].w));
+          const uint2 ol = B3 ? bf16_lo(v[q], o) : o;
           for (int c = 0; c < ncp; ++c) {
             const int j = ncp == 1 ? m : m + c - 2;
-            if (j >= 0 && j < (ncp == 1 ? NM : RS))
-              *reinterpret_cast<uint2*>(Gs + c * cpy + ((size_t)(pc >> 1) * RSp + j) * 16 + (pc & 1) * 8) = o;
+            if (j >= 0 && j < (ncp == 1 ? NM : RS)) {
+              uint8_t* g = Gs + c * cpy + ((size_t)(pc >> 1) * RSp + j) * 16 + (pc & 1) * 8;
+              *reinterpret_cast<uint2*>(g) = o;
+              if (B3) *reinterpret_cast<uint2*>(g + a.Sg) = ol;
+            }
           }
         }
       }
@@ -355,11 +379,12 @@ __global__ void __launch_bounds__(kWbThreads) wgrad_bf_k(WgBf a) {
         // halo carry: x rows [RS, RS + halo) of the previous stage's window are rows [0, halo) of this one
         const uint8_t* Xp = smem + (size_t)((s - 1) % NST) * a.Sb;
         const int n16 = a.ngx * a.halo;
-        for (int i = gtid; i < n16; i += kWbProd) {
-          const int g = i / a.halo, r = i - g * a.halo;
-          *reinterpret_cast<uint4*>(X + ((size_t)g * WRp + r) * 16) =
-              *reinterpret_cast<const uint4*>(Xp + ((size_t)g * WRp + RS + r) * 16);
-        }
+        for (int hl = 0; hl < (B3 ? 2 : 1); ++hl)  // B3: the hi and the lo window
+          for (int i = gtid; i < n16; i += kWbProd) {
+            const int g = i / a.halo, r = i - g * a.halo;
+            *reinterpret_cast<uint4*>(X + hl * a.Sx + ((size_t)g * WRp + r) * 16) =
+                *reinterpret_cast<const uint4*>(Xp + hl * a.Sx + ((size_t)g * WRp + RS + r) * 16);
+          }
       }
       tc::fence_proxy_async();
       tc::mbar_arrive(&full[slot]);
@@ -431,8 +456,10 @@ static size_t wb_smem(const WgBf& a) {
 static bool pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
 
 // (D, H, W): the gy grid (the layer's output)
-static bool wb_plan(int D, int H, int W, int Cin, int Cout, int ks, int batch, WgBf& a, int stride = 1) {
+static bool wb_plan(int D, int H, int W, int Cin, int Cout, int ks, int batch, WgBf& a, int stride = 1,
+                    bool b3 = false) {
   a.s2 = stride == 2;
+  a.b3 = b3;
   if (a.s2 && (ks != 3 || Cin > 64)) return false;
   if ((ks != 1 && ks != 3) || Cout < 16 || Cout > 256 || !pow2(Cout) || Cin % 8 || Cin < 8) return false;
   a.ks = ks;
@@ -515,17 +542,19 @@ static bool wb_plan(int D, int H, int W, int Cin, int Cout, int ks, int batch, W
     if (rs > 16 && rs / 2 >= rows) continue;
     const int wr = rs + a.halo;
     const int wrp = r8(wr), rsp = r8(a.ncp == 1 ? rs + 2 : rs);  // single copy: all RS + 2 map rows
-    const uint32_t sx = (uint32_t)a.ngx * wrp * 16;
-    const uint32_t sb = ((sx + (uint32_t)a.ncp * a.ngc * rsp * 16) + 1023) & ~1023u;
+    const uint32_t sx = (uint32_t)a.ngx * wrp * 16, sg = (uint32_t)a.ncp * a.ngc * rsp * 16;
+    const uint32_t sb = ((b3 ? 2 : 1) * (sx + sg) + 1023) & ~1023u;
     // the M = 64 / 128 MMA reads M / 8 group columns: past a smaller x block into the stage's gy copies or the pad
     const int blk1 = a.s2 ? a.mrows / 8 : 0;  // stride 2: the pw = 1 block's MMA reads start here
-    const long long over = (long long)(blk1 + a.M / 8 - a.ngx) * wrp * 16 - (long long)(sb - sx);
+    // (B3: the lo window's reads start Sx further in)
+    const long long over = (long long)(b3 ? sx : 0) + (long long)(blk1 + a.M / 8) * wrp * 16 - (long long)sb;
     a.pad = over > 0 ? (uint32_t)((over + 1023) & ~1023LL) : 0;
     a.WR = wr;
     a.RS = rs;
     a.WRp = wrp;
     a.RSp = rsp;
     a.Sx = sx;
+    a.Sg = sg;
     a.Sb = sb;
     a.NST = 2;
     if (wb_smem(a) > (size_t)205 * 1024) {
@@ -579,35 +608,40 @@ __global__ void __launch_bounds__(256) wgrad_bf_reduce_k(const float* __restrict
   }
 }
 
-bool wgrad_bf_supported(d2ip_act x, d2ip_act gy, int ks, int stride) {
+bool wgrad_bf_supported(d2ip_act x, d2ip_act gy, int ks, int stride, bool b3) {
   if (stride == 1 && (x.d != gy.d || x.h != gy.h || x.w != gy.w)) return false;
   if (stride == 2 && (gy.d != (x.d + 1) / 2 || gy.h != (x.h + 1) / 2 || gy.w != (x.w + 1) / 2)) return false;
   if (stride != 1 && stride != 2) return false;
   if (x.cstride % 4 || gy.cstride % 4 || ((uintptr_t)x.ptr & 15) || ((uintptr_t)gy.ptr & 15)) return false;
   WgBf a{};
-  return wb_plan(gy.d, gy.h, gy.w, x.c, gy.c, ks, 1, a, stride);
+  return wb_plan(gy.d, gy.h, gy.w, x.c, gy.c, ks, 1, a, stride, b3);
 }
 
 size_t wgrad_bf_ws_bytes(int D, int H, int W, int Cin, int Cout, int ks, int batch) {
   size_t best = 0;  // (D, H, W): the gy grid; the larger of the stride-1 and stride-2 plans
-  for (int stride : {1, 2}) {
+  for (int v = 0; v < 4; ++v) {  // stride 1 / 2, bf16 / 3xbf16
     WgBf a{};
-    if (!wb_plan(D, H, W, Cin, Cout, ks, batch, a, stride)) continue;
+    if (!wb_plan(D, H, W, Cin, Cout, ks, batch, a, 1 + (v & 1), v >= 2)) continue;
     best = std::max(best, (size_t)batch * a.nrg * ((size_t)a.ntaps * Cin * Cout + (size_t)a.nyb * Cout) * sizeof(float));
   }
   return best;
 }
 
-template <int NCX, int NKH, int NMMA>
-static int wb_launch3(const WgBf& a, dim3 grid, size_t smem, cudaStream_t st) {
+template <int NCX, int NKH, int NMMA, bool B3>
+static int wb_launch4(const WgBf& a, dim3 grid, size_t smem, cudaStream_t st) {
   static bool attr = false;
   if (!attr) {
-    D2IP_CUDA(cudaFuncSetAttribute(wgrad_bf_k<NCX, NKH, NMMA>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    D2IP_CUDA(cudaFuncSetAttribute(wgrad_bf_k<NCX, NKH, NMMA, B3>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    227 * 1024));
     attr = true;
   }
-  D2IP_CUDA(launch_pdl(wgrad_bf_k<NCX, NKH, NMMA>, grid, kWbThreads, smem, st, a));
+  D2IP_CUDA(launch_pdl(wgrad_bf_k<NCX, NKH, NMMA, B3>, grid, kWbThreads, smem, st, a));
   return D2IP_OK;
+}
+
+template <int NCX, int NKH, int NMMA>
+static int wb_launch3(const WgBf& a, dim3 grid, size_t smem, cudaStream_t st) {
+  return a.b3 ? wb_launch4<NCX, NKH, NMMA, true>(a, grid, smem, st) : wb_launch4<NCX, NKH, NMMA, false>(a, grid, smem, st);
 }
 
 template <int NCX>
@@ -618,9 +652,9 @@ static int wb_launch(const WgBf& a, dim3 grid, size_t smem, cudaStream_t st) {
 }
 
 int wgrad_bf(d2ip_act x, d2ip_act gy, int ks, float* gw, long long gwbs, void* ws, size_t ws_bytes, int batch,
-             cudaStream_t st, int stride) {
+             cudaStream_t st, int stride, bool b3) {
   WgBf a{};
-  D2IP_CHECK_ARG(wb_plan(gy.d, gy.h, gy.w, x.c, gy.c, ks, batch, a, stride), "wgrad_bf: unsupported shape");
+  D2IP_CHECK_ARG(wb_plan(gy.d, gy.h, gy.w, x.c, gy.c, ks, batch, a, stride, b3), "wgrad_bf: unsupported shape");
   D2IP_CHECK_ARG(ws_bytes >= wgrad_bf_ws_bytes(gy.d, gy.h, gy.w, x.c, gy.c, ks, batch), "wgrad_bf: workspace too small");
   a.x = x;
   a.gy = gy;
@@ -628,8 +662,8 @@ int wgrad_bf(d2ip_act x, d2ip_act gy, int ks, float* gw, long long gwbs, void* w
   auto twin_ok = [](const d2ip_act& t, int c0) {
     return t.bf16 && t.cstride % 8 == 0 && c0 % 8 == 0 && ((uintptr_t)t.bf16 & 15) == 0;
   };
-  a.xtw = twin_ok(x, 0);
-  a.gtw = twin_ok(gy, 0);
+  a.xtw = !b3 && twin_ok(x, 0);  // (3xbf16 splits fp32 values: no twins)
+  a.gtw = !b3 && twin_ok(gy, 0);
   static const int dbg = [] {
     const char* v = getenv("D2IP_WB_DBG");
     return v ? atoi(v) : 0;
