@@ -1,3 +1,4 @@
+#include <cstdlib>
 #include <string>
 #include <vector>
 #include <cstring>
@@ -59,8 +60,17 @@ int conv_wgrad(d2ip_act x, d2ip_act gy, int ks, int stride, float* gw, long long
   // TF32 layers: the 3xbf16 weight gradient pays off on large grids only (cfg2 level 0,
   // 131 K voxels: 358 -> 369 it/s); on cfg1's 32^3 grid the 3xTF32 kernel is faster
   // (1,186 vs 1,066 it/s with it everywhere)
-  if (precision == D2IP_PREC_TF32 && g_wgrad_variant == 1 && tf32_bf3_enabled() &&
-      (long long)gy.d * gy.h * gy.w >= 100000 && wgrad_bf_supported(x, gy, ks, stride, true)) {
+  static const long long bf3_min = [] {  // D2IP_WGBF3_MIN: smallest grid (voxels) for the 3xbf16 kernel
+    const char* v = getenv("D2IP_WGBF3_MIN");
+    return v ? atoll(v) : 100000LL;
+  }();
+  // Standalone, 3xbf16 is faster for most stride-1 cfg1 layers too (48->16 at 32^3: 56 vs 79 us), but in
+  // the step it costs (1,238 -> 1,185 it/s): its ~200 KB of shared memory per CTA takes whole SMs from
+  // the data-gradient chain it runs beside. Large grids only.
+  const long long vg = (long long)gy.d * gy.h * gy.w;
+  const bool b3_wins = vg >= bf3_min;
+  if (precision == D2IP_PREC_TF32 && g_wgrad_variant == 1 && tf32_bf3_enabled() && b3_wins &&
+      wgrad_bf_supported(x, gy, ks, stride, true)) {
     set_variant("wgrad_tcgen05_bf16x3");
     return wgrad_bf(x, gy, ks, gw, gwbs, ws, ws_bytes, batch, st, stride, true);
   }
