@@ -500,6 +500,24 @@ static bool wt_nopack() {
   return v;
 }
 
+// Knobs for the side-lane scheduling study: shared memory per CTA (D2IP_WG_SMEM_KB, default 220)
+// and CTAs per launch (D2IP_WG_CTAS, default 148). A weight-gradient CTA that fills an SM's shared
+// memory keeps the data-gradient chain's CTAs off that SM while it runs.
+static size_t wt_smem_cap() {
+  static const size_t v = [] {
+    const char* e = getenv("D2IP_WG_SMEM_KB");
+    return (size_t)(e ? atoi(e) : 220) * 1024;
+  }();
+  return v;
+}
+static long long wt_cta_target() {
+  static const long long v = [] {
+    const char* e = getenv("D2IP_WG_CTAS");
+    return e ? atoll(e) : 148LL;
+  }();
+  return v;
+}
+
 static bool wt_plan(int D, int H, int W, int Cin, int Cout, int ks, int batch, WgTc& a) {
   if (Cin % 4 || Cout % 4 || Cin < 4 || Cout > 128 || (ks != 1 && ks != 3)) return false;
   a.ntaps = ks == 3 ? 27 : 1;
@@ -529,9 +547,9 @@ static bool wt_plan(int D, int H, int W, int Cin, int Cout, int ks, int batch, W
       auto total = [&](int nst) {
         return (size_t)nst * sb + (((2 * nst + 1) * 8 + 15) & ~15) + 16 + kWtProd * 16 + 8 * (size_t)(nx + ng) + 64;
       };
-      if (total(2) > (size_t)220 * 1024) continue;
+      if (total(2) > wt_smem_cap()) continue;
       a.NSTG = 2;
-      while (a.NSTG < 4 && total(a.NSTG + 1) <= (size_t)220 * 1024) ++a.NSTG;
+      while (a.NSTG < 4 && total(a.NSTG + 1) <= wt_smem_cap()) ++a.NSTG;
       a.RS = rs;
       a.WR = nx;
       a.RSg = ng;
@@ -577,10 +595,10 @@ static bool wt_plan(int D, int H, int W, int Cin, int Cout, int ks, int batch, W
     // one real block is read with LBO = 0; otherwise the MMA runs mbx - nbx blocks past the x lo region
     const uint32_t pad = (nbx == 1 || nbx == mbx) ? 0 : align1k((size_t)(mbx - nbx) * bx);
     const size_t total = 2 * (size_t)sb + pad + 64 + kWtProd * 16 + 8 * (size_t)(wr + rsg) + 64;
-    if (total <= (size_t)220 * 1024) {
+    if (total <= wt_smem_cap()) {
       a.NSTG = 2;
       while (a.NSTG < 4 && (size_t)(a.NSTG + 1) * sb + pad + 128 + kWtProd * 16 + 8 * (size_t)(wr + rsg) + 64 <=
-                               (size_t)220 * 1024)
+                               wt_smem_cap())
         ++a.NSTG;
       a.RS = rs;
       a.RSg = rsg;
@@ -601,7 +619,7 @@ static bool wt_plan(int D, int H, int W, int Cin, int Cout, int ks, int batch, W
   a.nchunk = cdiv(a.u_last - a.u_first + 1, a.RS);
   // row groups: ~1 CTA per SM overall, >= 2 chunks each when there are enough
   const long long jobs = (long long)a.ngroups * a.ncib * batch;
-  int nrg = (int)std::max(1LL, (148LL + jobs - 1) / jobs);
+  int nrg = (int)std::max(1LL, (wt_cta_target() + jobs - 1) / jobs);
   nrg = std::min(nrg, std::max(1, a.nchunk / 2));
   a.chunks_per_rg = cdiv(a.nchunk, nrg);
   a.nrg = cdiv(a.nchunk, a.chunks_per_rg);
