@@ -304,7 +304,10 @@ def run_gpu(args):
     out = {
         "metric": "DIP iters/sec", "value": round(its, 2), "unit": "it/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(1e3 * t_dev / args.steps, 4), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "f32 (TF32 conv operands)" if (args.precision or spec.precision) == "tf32" else "f32",
+        "scaling": "weak", "vs_baseline": None, "dtype": ("f32 (TF32-class convs: 3xbf16 hi/lo operand splits on kind::f16, fp32 accumulate)"
+                  if os.environ.get("D2IP_TF32_BF3", "1") != "0" else "f32 (3xTF32 conv operands)")
+                 if (args.precision or spec.precision) == "tf32" else
+                 ("f32 (bf16 conv operands, fp32 accumulate)" if (args.precision or spec.precision) == "bf16" else "f32"),
         "data": "synthetic (seeded BASELINE cfg generator; random-init weights)",
         "config": {"workload": args.workload + ("" if args.net == "config" else
                                                 f"+FastResUNet3D(b={args.base_channels},{'dense' if args.dense else 'depthwise'})"),
@@ -368,7 +371,7 @@ def conv_probe(L, N, C, st, pk, pk_kind, flush, t_flush):
                                   3, 1, ya, 0, N.PREC["tf32"], C.c_void_p(ws.data_ptr()), wsn, 1, st), "conv")
     t = max(time_kernel(run) - t_flush, 1e-9)
     flops = 2.0 * 27 * cin * cout * D ** 3
-    peak = TF32_PEAK_TFLOPS
+    peak = pk.get("bf16_tflops", 1665.3)  # MEASURED_PEAKS.json: dense bf16 (the operand type the kernel runs)
     traffic = None  # DRAM bytes of this launch from the committed `ncu --set full` capture
     try:
         prof = json.loads((Path(__file__).resolve().parent / "profiles" / "r1_ncu_cfg1dec0c1.json").read_text())
@@ -377,18 +380,24 @@ def conv_probe(L, N, C, st, pk, pk_kind, flush, t_flush):
                       for k in ("dram__bytes_read.sum", "dram__bytes_write.sum"))
     except Exception:
         traffic = None
-    return {"bound": "tensor", "kernel": "conv_tc_k (K1, tcgen05 3xTF32 implicit GEMM) incl. weight pack",
+    b3 = os.environ.get("D2IP_TF32_BF3", "1") != "0"
+    # shape bound: an M=128 x N=16 MMA reads 4 KB (A) + 0.5 KB (B) of shared memory in ~39 cycles
+    # (tools/umma_chains.cu): kind::f16 does 2*128*16*16 flop in it (of 8,192 flop/cycle/SM at
+    # the 2,209 TFLOP/s probe peak), kind::tf32 half that; 3x MMAs per fp32-accurate product
+    f16_probe = F16_PEAK_TFLOPS
+    n16 = f16_probe * (2 * 128 * 16 * 16 / 39) / 8192 / 3 if b3 else TF32_PEAK_TFLOPS * (2 * 128 * 16 * 8 / 39) / 4096 / 3
+    return {"bound": "tensor",
+            "kernel": "conv_tc_k (K1, tcgen05 %s implicit GEMM) incl. weight pack" % ("3xbf16 kind::f16" if b3 else "3xTF32"),
             "layer": "dec0.conv1 48->16 @ 32^3", "achieved": round(flops / t / 1e12, 2), "peak": peak,
             "unit": "TFLOP/s", "frac": round(flops / t / 1e12 / peak, 4), "traffic": traffic,
             "traffic_source": "profiles/r1_ncu_cfg1dec0c1.json (ncu --set full, dram read+write bytes)",
             "algorithmic_flops_per_launch": flops, "avg_launch_s": t,
-            "peak_source": "measured dense kind::tf32 tcgen05.mma peak on this pool's B200 (profiles/r1_umma_rate.txt); "
-                           "3xTF32 issues 3 MMAs per product",
-            # what the layer's shape allows: an M=128 x N=16 kind::tf32 MMA is bound by its shared-memory
-            # operand reads (4 KB A + 0.5 KB B at ~128 B/cycle: 39 cycles, tools/umma_chains.cu) to 840 of
-            # 4,096 flop/cycle/SM, and 3xTF32 spends 3 MMAs per fp32-accurate product
-            "n16_3xtf32_bound": round(TF32_PEAK_TFLOPS * (2 * 128 * 16 * 8 / 39) / 4096 / 3, 1),
-            "frac_of_n16_3xtf32_bound": round(flops / t / 1e12 / (TF32_PEAK_TFLOPS * (2 * 128 * 16 * 8 / 39) / 4096 / 3), 4)}
+            "peak_source": "MEASURED_PEAKS.json bf16_tflops (cuBLAS 8192^3 burst); the kernel's pipe peak from "
+                           "tools/umma_rate.cu is %.1f (kind::f16) / %.1f (kind::tf32) TFLOP/s" % (f16_probe, TF32_PEAK_TFLOPS),
+            "n16_shape_bound": round(n16, 1),
+            "n16_shape_bound_source": "16 output channels: M=128 x N=16 MMAs bound by shared-memory operand reads "
+                                      "(39 cycles each, tools/umma_chains.cu), 3 MMAs per fp32-accurate product",
+            "frac_of_n16_shape_bound": round(flops / t / 1e12 / n16, 4)}
 
 
 # dense kind::f16 peak measured the same way (profiles/r1_umma_rate.txt): 2,209 TFLOP/s.
@@ -437,9 +446,11 @@ def conv_bf16_probe(L, N, C, st, flush, t_flush):
         N.check(L.d2ip_conv3d_wgrad(xa, ya, 3, 1, C.c_void_p(gw.data_ptr()), 0, C.c_void_p(wgs.data_ptr()), wgn,
                                     N.PREC["bf16"], 1, st), "wgrad bf16")
     flops = 2.0 * 27 * cin * cout * V
+    pk, _ = peaks()
+    peak = pk.get("bf16_tflops", 1665.3)
     out = {"bound": "tensor", "layer": "cfg4 dec0.conv1 96->32 @ 96x96x48, bf16 operands (twins), fp32 accumulate",
-           "algorithmic_flops_per_launch": flops, "unit": "TFLOP/s", "peak": F16_PEAK_TFLOPS,
-           "peak_source": "measured dense kind::f16 tcgen05.mma peak (profiles/r1_umma_rate.txt)",
+           "algorithmic_flops_per_launch": flops, "unit": "TFLOP/s", "peak": peak,
+           "peak_source": "MEASURED_PEAKS.json bf16_tflops (cuBLAS burst); tcgen05 kind::f16 probe peak %.1f" % F16_PEAK_TFLOPS,
            "n32_operand_bound": round(F16_N32_BOUND_TFLOPS, 1),
            "n32_operand_bound_source": "M=128 x N=32 MMA = 40 cycles of shared-memory operand reads "
                                        "(tools/umma_chains.cu); the layer's 32 output channels cap kind::f16 there"}
@@ -448,7 +459,7 @@ def conv_bf16_probe(L, N, C, st, flush, t_flush):
         t = max(time_kernel(fn) - t_flush, 1e-9)
         tf = flops / t / 1e12
         out[name] = {"kernel": kern, "avg_launch_s": t, "achieved": round(tf, 1),
-                     "frac": round(tf / F16_PEAK_TFLOPS, 4), "frac_of_n32_bound": round(tf / F16_N32_BOUND_TFLOPS, 4)}
+                     "frac": round(tf / peak, 4), "frac_of_n32_bound": round(tf / F16_N32_BOUND_TFLOPS, 4)}
     del x, y, xt, yt, ws, wgs
     return out
 
