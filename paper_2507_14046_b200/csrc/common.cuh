@@ -49,7 +49,10 @@ inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 // its top, and immediately allows its successor to be scheduled — so the ~110
 // launches of an iteration overlap their launch latency with the previous
 // kernel's tail. The wait covers the whole predecessor grid and its memory, so
-// early triggering is always safe; dependencies are transitive.
+// early triggering is always safe; dependencies are transitive. (Measured: an
+// explicit griddepcontrol.launch_dependents at kernel entry makes successors
+// resident early and costs 9 % at cfg1 -- 1,238 -> 1,130 it/s -- their shared
+// memory holds SMs the side-stream kernels need; the implicit trigger at exit stays.)
 #define D2IP_PDL_ENTRY()                                              \
   do {                                                                \
     asm volatile("griddepcontrol.wait;" ::: "memory");                \
