@@ -442,8 +442,127 @@ static DirectPlan direct_plan(long long V, int C, int ks, int batch, int live_ta
   return p;
 }
 
+// ---------------------------------------------------------------------------
+// 1^3 stride-2 convolutions (the encoder blocks' skip path): y[o] = b + W x[2o]
+// and its data gradient gx[2o] = W^T gy[o] (gx = 0 at the other seven parities).
+// Lane groups: G = C / 4 lanes share an output voxel and own 4 channels each;
+// the weights sit in shared memory transposed for float4 reads, the voxel's
+// input row is read once by the group (128-bit loads, L1 broadcast), and every
+// store is a coalesced float4 -- the generic direct kernel re-derived taps and
+// strided indices per thread (up to 15x slower on cfg4's 442 K-voxel level).
+
+template <int G>
+__global__ void __launch_bounds__(256) pw_s2_fwd_k(d2ip_act x, const float* __restrict__ w,
+                                                   const float* __restrict__ bias, long long wbs, d2ip_act y,
+                                                   int accumulate) {
+  D2IP_PDL_ENTRY();
+  extern __shared__ float4 sw4[];  // [ci][G]: W[4 l .. 4 l + 3][ci]
+  const int b = blockIdx.y, cin = x.c;
+  const float* wb = w + b * wbs;
+  for (int i = threadIdx.x; i < cin * G; i += blockDim.x) {
+    const int ci = i / G, l = i % G;
+    sw4[i] = make_float4(__ldg(wb + (4 * l) * cin + ci), __ldg(wb + (4 * l + 1) * cin + ci),
+                         __ldg(wb + (4 * l + 2) * cin + ci), __ldg(wb + (4 * l + 3) * cin + ci));
+  }
+  __syncthreads();
+  const long long V = (long long)y.d * y.h * y.w;
+  const long long o = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / G;
+  const int l = threadIdx.x % G;
+  if (o >= V) return;
+  const int ow = (int)(o % y.w), oh = (int)((o / y.w) % y.h), od = (int)(o / ((long long)y.w * y.h));
+  const float* xr = x.ptr + b * x.bstride + (((long long)(2 * od) * x.h + 2 * oh) * x.w + 2 * ow) * x.cstride;
+  float4 acc = bias ? make_float4(__ldg(bias + b * wbs + 4 * l), __ldg(bias + b * wbs + 4 * l + 1),
+                                  __ldg(bias + b * wbs + 4 * l + 2), __ldg(bias + b * wbs + 4 * l + 3))
+                    : make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int c0 = 0; c0 < cin; c0 += 4) {
+    const float4 q = __ldg(reinterpret_cast<const float4*>(xr + c0));
+    const float qq[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float4 wq = sw4[(c0 + j) * G + l];
+      acc.x = fmaf(qq[j], wq.x, acc.x);
+      acc.y = fmaf(qq[j], wq.y, acc.y);
+      acc.z = fmaf(qq[j], wq.z, acc.z);
+      acc.w = fmaf(qq[j], wq.w, acc.w);
+    }
+  }
+  float4* yp = reinterpret_cast<float4*>(y.ptr + b * y.bstride + o * y.cstride + 4 * l);
+  if (accumulate) {
+    const float4 p0 = *yp;
+    acc.x += p0.x; acc.y += p0.y; acc.z += p0.z; acc.w += p0.w;
+  }
+  *yp = acc;
+}
+
+template <int G>
+__global__ void __launch_bounds__(256) pw_s2_dgrad_k(d2ip_act gy, const float* __restrict__ w, long long wbs,
+                                                     d2ip_act gx, int accumulate) {
+  D2IP_PDL_ENTRY();
+  extern __shared__ float4 sw4[];  // [co][G]: W[co][4 l .. 4 l + 3]
+  const int b = blockIdx.y, cout = gy.c, cin = gx.c;
+  const float* wb = w + b * wbs;
+  for (int i = threadIdx.x; i < cout * G; i += blockDim.x) {
+    const int co = i / G, l = i % G;
+    const float* r = wb + (long long)co * cin + 4 * l;  // (theta offsets need not be 16-byte aligned)
+    sw4[i] = make_float4(__ldg(r), __ldg(r + 1), __ldg(r + 2), __ldg(r + 3));
+  }
+  __syncthreads();
+  const long long V = (long long)gx.d * gx.h * gx.w;
+  const long long v = ((long long)blockIdx.x * blockDim.x + threadIdx.x) / G;
+  const int l = threadIdx.x % G;
+  if (v >= V) return;
+  const int iw = (int)(v % gx.w), ih = (int)((v / gx.w) % gx.h), id = (int)(v / ((long long)gx.w * gx.h));
+  float4* gp = reinterpret_cast<float4*>(gx.ptr + b * gx.bstride + v * gx.cstride + 4 * l);
+  if ((iw | ih | id) & 1) {  // no output voxel reads an odd-parity input
+    if (!accumulate) *gp = make_float4(0.f, 0.f, 0.f, 0.f);
+    return;
+  }
+  const float* gr = gy.ptr + b * gy.bstride + (((long long)(id >> 1) * gy.h + (ih >> 1)) * gy.w + (iw >> 1)) * gy.cstride;
+  float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int c0 = 0; c0 < cout; c0 += 4) {
+    const float4 q = __ldg(reinterpret_cast<const float4*>(gr + c0));
+    const float qq[4] = {q.x, q.y, q.z, q.w};
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const float4 wq = sw4[(c0 + j) * G + l];
+      acc.x = fmaf(qq[j], wq.x, acc.x);
+      acc.y = fmaf(qq[j], wq.y, acc.y);
+      acc.z = fmaf(qq[j], wq.z, acc.z);
+      acc.w = fmaf(qq[j], wq.w, acc.w);
+    }
+  }
+  if (accumulate) {
+    const float4 p0 = *gp;
+    acc.x += p0.x; acc.y += p0.y; acc.z += p0.z; acc.w += p0.w;
+  }
+  *gp = acc;
+}
+
+static bool pw_s2_ok(const d2ip_act& in, const d2ip_act& out) {
+  const int G = out.c / 4;
+  auto al = [](const d2ip_act& a) { return a.cstride % 4 == 0 && ((uintptr_t)a.ptr & 15) == 0; };
+  return out.c % 4 == 0 && in.c % 4 == 0 && (G == 1 || G == 2 || G == 4 || G == 8 || G == 16 || G == 32) &&
+         al(in) && al(out) && (size_t)in.c * G * 16 <= 96 * 1024;
+}
+
 int conv_fwd_direct(d2ip_act x, const float* w, const float* bias, long long wbs, int ks, int stride,
                     d2ip_act y, int accumulate, int batch, cudaStream_t st, int dil) {
+  if (ks == 1 && stride == 2 && pw_s2_ok(x, y) && y.d == (x.d + 1) / 2 && y.h == (x.h + 1) / 2 &&
+      y.w == (x.w + 1) / 2) {
+    const long long Vo = (long long)y.d * y.h * y.w;
+    const size_t sm = (size_t)x.c * (y.c / 4) * 16;
+    const dim3 grid(cdiv(Vo * (y.c / 4), 256), batch);
+#define D2IP_PWF(G_)                                                                                  \
+  case G_:                                                                                           \
+    D2IP_RET(smem_opt_in(pw_s2_fwd_k<G_>, sm));                                                      \
+    D2IP_CUDA(launch_pdl(pw_s2_fwd_k<G_>, grid, 256, sm, st, x, w, bias, wbs, y, accumulate));       \
+    break;
+    switch (y.c / 4) { D2IP_PWF(1) D2IP_PWF(2) D2IP_PWF(4) D2IP_PWF(8) D2IP_PWF(16) D2IP_PWF(32) }
+#undef D2IP_PWF
+    set_variant("direct_fp32_pw_s2");
+    D2IP_LAUNCH_CHECK();
+    return D2IP_OK;
+  }
   const long long V = (long long)y.d * y.h * y.w;
   const int vec = vec_ok(x) ? 1 : 0;
   const DirectPlan p = direct_plan(V, y.c, ks, batch, 27, x.c);
@@ -475,6 +594,22 @@ int conv_fwd_direct(d2ip_act x, const float* w, const float* bias, long long wbs
 
 int conv_dgrad_direct(d2ip_act gy, const float* w, long long wbs, int ks, int stride, d2ip_act gx,
                       int accumulate, int batch, cudaStream_t st, int dil) {
+  if (ks == 1 && stride == 2 && pw_s2_ok(gy, gx) && gy.d == (gx.d + 1) / 2 && gy.h == (gx.h + 1) / 2 &&
+      gy.w == (gx.w + 1) / 2) {
+    const long long V = (long long)gx.d * gx.h * gx.w;
+    const size_t sm = (size_t)gy.c * (gx.c / 4) * 16;
+    const dim3 grid(cdiv(V * (gx.c / 4), 256), batch);
+#define D2IP_PWD(G_)                                                                                  \
+  case G_:                                                                                           \
+    D2IP_RET(smem_opt_in(pw_s2_dgrad_k<G_>, sm));                                                    \
+    D2IP_CUDA(launch_pdl(pw_s2_dgrad_k<G_>, grid, 256, sm, st, gy, w, wbs, gx, accumulate));          \
+    break;
+    switch (gx.c / 4) { D2IP_PWD(1) D2IP_PWD(2) D2IP_PWD(4) D2IP_PWD(8) D2IP_PWD(16) D2IP_PWD(32) }
+#undef D2IP_PWD
+    set_variant("direct_fp32_pw_s2");
+    D2IP_LAUNCH_CHECK();
+    return D2IP_OK;
+  }
   const long long V = (long long)gx.d * gx.h * gx.w;
   const int vec = vec_ok(gy) ? 1 : 0;
   const DirectPlan p = direct_plan(V, gx.c, ks, batch, stride == 1 ? 27 : 4, gy.c);
