@@ -97,6 +97,7 @@ struct TcConv {
   int xtw;         // bf16: stream x from its bf16 twin (cp.async) instead of converting fp32 rows
   int lrows;       // TMA path: rows per channel-chunk column (whole padded lines: maxlines x Sw)
   int b3;          // 3xbf16 (TF32-precision layer): hi + lo bf16 operands, three MMAs per K step
+  int nst;         // conv_tc_k ring depth: 2, or 3 when a third stage fits shared memory
 };
 
 // Per stage: A hi + A lo windows, B hi + B lo tiles (nt^2 taps); bf16: one
@@ -108,7 +109,7 @@ static size_t stage_bytes(int cb, int np, int wrp, int nt = 3, bool bf = false, 
 }
 
 static size_t tc_smem_bytes(const TcConv& a) {
-  return 2 * stage_bytes(a.CB, a.Ns, a.WRp, a.nt, a.bf, a.b3) + 3 * a.WR * sizeof(int) + 8 + 5 * 8 + 16;
+  return (size_t)a.nst * stage_bytes(a.CB, a.Ns, a.WRp, a.nt, a.bf, a.b3) + 3 * a.WR * sizeof(int) + 8 + 7 * 8 + 16;
 }
 
 __device__ __forceinline__ uint32_t bf2(float a, float b) {
@@ -245,15 +246,16 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
   const uint32_t Ab = (uint32_t)NKC * WRp * 16, Bb = (uint32_t)ntap * NKC * Ns * 16;
   const uint32_t Sb = NH * (Ab + Bb);
   // layout: 2 stages of [A hi][A lo][B hi][B lo] (bf16: [A][B]), row map, barriers full[2] empty[2] done, TMEM slot
-  int* rowmap = reinterpret_cast<int*>(smem + 2 * Sb);
+  const int NST = a.nst;  // ring depth (2 or 3 stages)
+  int* rowmap = reinterpret_cast<int*>(smem + NST * Sb);
   uint64_t* full = reinterpret_cast<uint64_t*>(rowmap + 3 * WR + ((3 * WR) & 1));
-  uint64_t* empty = full + 2;
-  uint64_t* done = empty + 2;
+  uint64_t* empty = full + 3;
+  uint64_t* done = empty + 3;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
 
   if (warp == 0) tc::tmem_alloc(tslot, a.tmem_cols);
   if (tid == 0) {
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NST; ++i) {
       tc::mbar_init(&full[i], kTcProd / PG);  // one producer group fills a stage
       tc::mbar_init(&empty[i], 1);
     }
@@ -303,11 +305,11 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
       const uint64_t dAhi = tc::make_desc(sbase, WRp * 16, 128), dAlo = dAhi + (Ab >> 4);
       const uint64_t dBhi = tc::make_desc(sbase + NH * Ab, Ns * 16, 128), dBlo = dBhi + (Bb >> 4);
       for (int s = 0; s < S; ++s) {
-        const int slot = s & 1;
-        tc::mbar_wait(&full[slot], (uint32_t)((s >> 1) & 1));
+        const int slot = s % NST;
+        tc::mbar_wait(&full[slot], (uint32_t)((s / NST) & 1));
         tc::fence_after();
         if (BF) tc::fence_proxy_async();
-        const uint64_t boff = slot ? (uint64_t)(Sb >> 4) : 0;
+        const uint64_t boff = (uint64_t)slot * (Sb >> 4);
         for (int tq = 0; tq < ntap; ++tq) {
           const int t9 = tap9(tq);
           const int rowoff = PW ? 0 : (t9 >= 6 ? 2 : t9 >= 3 ? 1 : 0) * a.Sw + (t9 % 3);
@@ -343,8 +345,8 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
     constexpr int GT = kTcProd / PG;
     const int pg = PG == 2 ? (warp - 1) >> 2 : 0, gtid = tid - 32 - pg * GT;
     for (int s = pg; s < S; s += PG) {
-      const int slot = s & 1;
-      if (s >= 2) tc::mbar_wait(&empty[slot], (uint32_t)(((s >> 1) - 1) & 1));
+      const int slot = s % NST;
+      if (s >= NST) tc::mbar_wait(&empty[slot], (uint32_t)(((s / NST) - 1) & 1));
       const int sg = s_lo + s;
       const int kdi = sg / a.n_cb, cb = sg - kdi * a.n_cb;
       const int kd = PW ? 0 : t0 + kdi;
@@ -1079,6 +1081,21 @@ int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, lo
   while (cols < a.T * a.Ns) cols *= 2;
   a.tmem_cols = cols;
   a.idesc = tc::make_idesc(bf ? 1 : 2, kTcRows, a.Ns);
+  // D2IP_TC_NST=3: a third stage when it fits without costing occupancy. Measured neutral at
+  // cfg4 (137.9 vs 138.2 it/s) and a loss at cfg1 (1,218 vs 1,244): two stages stay the default.
+  static const int nst_max = [] {
+    const char* v = getenv("D2IP_TC_NST");
+    return v ? std::max(2, std::min(3, atoi(v))) : 2;
+  }();
+  // (never at the cost of a co-resident CTA: the plan's 2-stage footprint decides CTAs per SM)
+  a.nst = 2;
+  if (nst_max >= 3 && !use_tma) {
+    const size_t two = tc_smem_bytes(a);
+    a.nst = 3;
+    const size_t three = tc_smem_bytes(a);
+    const bool keeps_occupancy = two > (size_t)110 * 1024 ? three <= (size_t)220 * 1024 : three <= (size_t)110 * 1024;
+    if (!keeps_occupancy) a.nst = 2;
+  }
   const size_t smem = use_tma ? 0 : tc_smem_bytes(a);  // (the TMA kernel sizes its own)
   const dim3 grid(tiles, (a.Np / a.Ns) * a.kspl, batch);
   // one producer group (all eight warps per stage) measured faster than two on
