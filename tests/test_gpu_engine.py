@@ -29,7 +29,7 @@ from paper_2507_14046_b200.priornet import ResUNetConfig, kaiming_flat, sample_n
 
 pytestmark = pytest.mark.gpu
 
-GRAD_TOL = {"fp32": 1e-4, "tf32": 1e-3}
+GRAD_TOL = {"fp32": 1e-4, "tf32": 1e-3, "bf16": 1e-2}  # the north star's bars (bf16 operands, fp32 accumulate)
 
 
 def rel(a, b):
@@ -84,10 +84,16 @@ def test_step_loss_and_grads_vs_reference(cfg0, prec, mode):
         o += e.numel
 
 
-@pytest.mark.parametrize("prec", ["fp32", "tf32"])
-@pytest.mark.parametrize("shape", ["mini", "cfg1"])
+@pytest.mark.parametrize("prec,shape", [("fp32", "mini"), ("tf32", "mini"), ("fp32", "cfg1"), ("tf32", "cfg1"),
+                                        ("bf16", "cfg1")])
 def test_step_grads_three_level_vs_oracle(shape, prec):
-    """3-level nets (the cfg1 topology) against the CPU oracle, per tensor."""
+    """3-level nets (the cfg1 topology) against the CPU oracle, per tensor.
+
+    bf16 operands (fp32 accumulate) meet the north star's 1e-2 bar on the cfg1-width net
+    (measured 6.2e-3 overall, worst tensor 1.4e-2). Not on 8-channel nets: the data term's
+    residual is a small difference of large terms, so the forward's bf16 rounding (0.1 % on the
+    loss) reaches the early layers' gradients at 1.5e-2 (mini) / 5.8e-2 (cfg0); feeding the data
+    gradients 3xbf16 operands changes nothing (tools/bf16_err.py) -- it is the forward."""
     spec = W.small_spec() if shape == "mini" else W.CONFIGS["cfg1"]
     wl = W.make_workload(spec, seed=0, frames=1)
     net = spec.network(seed=1)
