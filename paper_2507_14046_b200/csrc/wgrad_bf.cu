@@ -503,10 +503,17 @@ static bool wb_plan(int D, int H, int W, int Cin, int Cout, int ks, int batch, W
     }
   } else if (9 * Cout <= 512) {
     // kd plane: three kh accumulators of 3 C_out columns, the kw copies stacked along N
+    // (D2IP_WB_SINGLE=1: one gy copy, three MMAs per kh with B started 2 - kw rows in)
+    static const bool single = [] {
+      const char* v = getenv("D2IP_WB_SINGLE");
+      return v && atoi(v) != 0;
+    }();
     a.nkh = 3;
-    a.ncp = 3;
-    a.nmma = 1;
-    a.N = 3 * Cout;
+    a.ncp = single ? 1 : 3;
+    a.nmma = single ? 3 : 1;
+    a.N = single ? Cout : 3 * Cout;
+    a.bsh0 = single ? 2 : 0;
+    a.bstep = single ? -1 : 0;
     a.ngroups = 3;
   } else if (3 * Cout <= 512) {
     // (kd, kh) row: three MMAs (one per kw) on one gy copy, B started 2 - kw rows in
@@ -646,6 +653,7 @@ static int wb_launch3(const WgBf& a, dim3 grid, size_t smem, cudaStream_t st) {
 
 template <int NCX>
 static int wb_launch(const WgBf& a, dim3 grid, size_t smem, cudaStream_t st) {
+  if (a.nkh == 3 && a.nmma == 3) return wb_launch3<NCX, 3, 3>(a, grid, smem, st);
   if (a.nkh == 3) return wb_launch3<NCX, 3, 1>(a, grid, smem, st);
   if (a.nmma == 3) return wb_launch3<NCX, 1, 3>(a, grid, smem, st);
   return wb_launch3<NCX, 1, 1>(a, grid, smem, st);
