@@ -292,6 +292,26 @@ def run_gpu(args):
     conv_roof = conv_probe(L, N, C, st, pk, pk_kind, flush, t_flush) if spec.channels[0] == 16 and args.net == "config" else None
     # the bf16 tensor-core kernels on cfg4's largest layer (dec0.conv1, 96 -> 32 at 96x96x48)
     conv_bf16 = None if args.skip_probe else conv_bf16_probe(L, N, C, st, flush, t_flush)
+    # K7 Adam on cfg4's flat parameter buffer (9.53 M parameters, 28 B each per step)
+    adam_roof = None
+    if not args.skip_probe:
+        n_ad = 9_529_233
+        bufs = [torch.randn(n_ad, device="cuda") for _ in range(4)]
+        bufs[3].abs_()
+        stepv = torch.ones(1, dtype=torch.int32, device="cuda")
+
+        def adam_run():
+            flush.zero_()
+            N.check(L.d2ip_adam(*[C.c_void_p(b.data_ptr()) for b in bufs], n_ad, 1e-3, 0.9, 0.999, 1e-8,
+                                C.c_void_p(stepv.data_ptr()), st), "adam")
+        t_ad = max(time_kernel(adam_run) - t_flush, 1e-9)
+        byt = 28.0 * n_ad
+        adam_roof = {"bound": "hbm", "kernel": "adam_k (K7, flat float4 Adam)", "n_params": n_ad,
+                     "algorithmic_bytes_per_launch": byt, "avg_launch_s": t_ad,
+                     "achieved": round(byt / t_ad / 1e9, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
+                     "frac": round(byt / t_ad / 1e9 / pk["hbm_gbs"], 4), "peak_source": pk_kind,
+                     "note": f"p, g, m, v read + p, m, v written; vs the 8,000 GB/s nominal: {byt / t_ad / 8e12:.3f}"}
+        del bufs
     # whole-iteration tensor-throughput view of the convolutions
     conv_tflops = units["conv_flops"] * units_per_step / (t_dev / args.steps) / 1e12
     roofline = conv_roof or jac_cfg
@@ -325,6 +345,7 @@ def run_gpu(args):
         "roofline_jac_cfg": jac_cfg,
         "roofline_jac_hbm": hbm_probe,
         "roofline_conv_bf16_cfg4": conv_bf16,
+        "roofline_adam_cfg4": adam_roof,
         "clocks": clk.summary(),
     }
     if units_per_step > 1:
