@@ -98,6 +98,7 @@ struct TcConv {
   int lrows;       // TMA path: rows per channel-chunk column (whole padded lines: maxlines x Sw)
   int b3;          // 3xbf16 (TF32-precision layer): hi + lo bf16 operands, three MMAs per K step
   int nst;         // conv_tc_k ring depth: 2, or 3 when a third stage fits shared memory
+  int async_arrive;  // bf16 twin path: stages complete by cp.async.mbarrier.arrive (D2IP_TC_ASYNC)
 };
 
 // Per stage: A hi + A lo windows, B hi + B lo tiles (nt^2 taps); bf16: one
@@ -449,6 +450,14 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
           tc::cp_async16(dst + n * 16, src + n * 4, 16u);
           if (NH == 2) tc::cp_async16(dst + Bb + n * 16, src + a.wlo + n * 4, 16u);
         }
+      }
+      if (BF && !B3 && a.xtw && a.async_arrive) {
+        // every operand of the stage is an async copy: arrive when this thread's copies
+        // land (no wait here -- the next stage's copies are issued while these fly);
+        // the MMA thread's proxy fence makes them visible to the tensor core
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(tc::smem_u32(&full[slot]))
+                     : "memory");
+        continue;
       }
       tc::cp_async_commit();
       tc::cp_async_wait<0>();
@@ -1096,6 +1105,11 @@ int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, lo
     const bool keeps_occupancy = two > (size_t)110 * 1024 ? three <= (size_t)220 * 1024 : three <= (size_t)110 * 1024;
     if (!keeps_occupancy) a.nst = 2;
   }
+  static const int async_on = [] {
+    const char* v = getenv("D2IP_TC_ASYNC");
+    return v ? atoi(v) : 1;
+  }();
+  a.async_arrive = async_on;
   const size_t smem = use_tma ? 0 : tc_smem_bytes(a);  // (the TMA kernel sizes its own)
   const dim3 grid(tiles, (a.Np / a.Ns) * a.kspl, batch);
   // one producer group (all eight warps per stage) measured faster than two on

@@ -671,6 +671,13 @@ int wgrad_bf(d2ip_act x, d2ip_act gy, int ks, float* gw, long long gwbs, void* w
     return t.bf16 && t.cstride % 8 == 0 && c0 % 8 == 0 && ((uintptr_t)t.bf16 & 15) == 0;
   };
   a.xtw = !b3 && twin_ok(x, 0);  // (3xbf16 splits fp32 values: no twins)
+  // D2IP_WB_CARRY=0: reload the x halo every stage instead of carrying it (no wait on the
+  // previous stage's landing; 1.8x the x window bytes at cfg4's level 0)
+  static const int carry_on = [] {
+    const char* v = getenv("D2IP_WB_CARRY");
+    return v ? atoi(v) : 1;
+  }();
+  if (!carry_on && a.carry) a.carry = 0;
   a.gtw = !b3 && twin_ok(gy, 0);
   static const int dbg = [] {
     const char* v = getenv("D2IP_WB_DBG");
