@@ -99,6 +99,7 @@ struct TcConv {
   int b3;          // 3xbf16 (TF32-precision layer): hi + lo bf16 operands, three MMAs per K step
   int nst;         // conv_tc_k ring depth: 2, or 3 when a third stage fits shared memory
   int async_arrive;  // bf16 twin path: stages complete by cp.async.mbarrier.arrive (D2IP_TC_ASYNC)
+  int dbg;           // D2IP_TC_DBG=1: producers skip the fills (MMA-side timing only)
 };
 
 // Per stage: A hi + A lo windows, B hi + B lo tiles (nt^2 taps); bf16: one
@@ -348,6 +349,10 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
     for (int s = pg; s < S; s += PG) {
       const int slot = s % NST;
       if (s >= NST) tc::mbar_wait(&empty[slot], (uint32_t)(((s / NST) - 1) & 1));
+      if (a.dbg) {  // D2IP_TC_DBG=1: no fills (measures the MMA side alone; wrong results)
+        tc::mbar_arrive(&full[slot]);
+        continue;
+      }
       const int sg = s_lo + s;
       const int kdi = sg / a.n_cb, cb = sg - kdi * a.n_cb;
       const int kd = PW ? 0 : t0 + kdi;
@@ -894,8 +899,13 @@ static bool tc_plan(int D, int H, int W, int K, int N, int batch, TcConv& a, int
   // stage's weight tile and per-CTA overhead; scored by a latency model in us:
   // a stage costs max(cp.async landing ~1.5, its MMAs: 27/8 CB T x 57 cycles).
   const bool large = (long long)tiles1 * batch >= 4LL * 296;
+  static const int t_force = [] {  // D2IP_TC_T=1/2/4: tiles per CTA for large layers (study knob)
+    const char* v = getenv("D2IP_TC_T");
+    return v ? atoi(v) : 0;
+  }();
   for (int T : {1, 2, 4}) {
     if (T > 1 && (!large || nt == 2)) break;
+    if (t_force && large && nt != 2 && T != t_force) continue;
     const int wr = nt == 1 ? T * kTcRows : wr_of(a.Sw, T);
     const int wrp = tma ? (wr + 2 * a.Sw - 2) / a.Sw * a.Sw : wrp_of(wr);
     const int tl = cdiv(tiles1, T);
@@ -1110,6 +1120,11 @@ int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, lo
     return v ? atoi(v) : 1;
   }();
   a.async_arrive = async_on;
+  static const int dbg_on = [] {
+    const char* v = getenv("D2IP_TC_DBG");
+    return v ? atoi(v) : 0;
+  }();
+  a.dbg = dbg_on;
   const size_t smem = use_tma ? 0 : tc_smem_bytes(a);  // (the TMA kernel sizes its own)
   const dim3 grid(tiles, (a.Np / a.Ns) * a.kspl, batch);
   // one producer group (all eight warps per stage) measured faster than two on
