@@ -100,6 +100,7 @@ struct TcConv {
   int nst;         // conv_tc_k ring depth: 2, or 3 when a third stage fits shared memory
   int async_arrive;  // bf16 twin path: stages complete by cp.async.mbarrier.arrive (D2IP_TC_ASYNC)
   int dbg;           // D2IP_TC_DBG=1: producers skip the fills (MMA-side timing only)
+  int ntiles;        // persistent kernel: tiles (blocks of T x 128 rows) of the grid
 };
 
 // Per stage: A hi + A lo windows, B hi + B lo tiles (nt^2 taps); bf16: one
@@ -126,9 +127,13 @@ __device__ __forceinline__ float tf32_hi(float x) { return __uint_as_float(__flo
 // (w - 1) / 4; one row / voxel per sub-tile. S = 0: zeros (an empty split).
 template <int T, int MODE>
 __device__ __forceinline__ void tc_epilogue(const TcConv& a, uint32_t tmem, int b, int n0, int u0, int ks, int S,
-                                            int warp, int lane) {
+                                            int warp, int lane, int cbeg = -1, int cend = -1) {
   const int row = (warp & 3) * 32 + lane;
-  const int chalf = a.Ns / 2, cbeg = ((warp - 1) >> 2) * chalf, cend = cbeg + chalf;
+  if (cbeg < 0) {  // warps 1-8: two warps per lane quadrant, one column half each
+    const int chalf = a.Ns / 2;
+    cbeg = ((warp - 1) >> 2) * chalf;
+    cend = cbeg + chalf;
+  }
   const d2ip_act y = a.y;
   const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16);
   const float* bias = a.bias ? a.bias + b * a.bbs : nullptr;
@@ -492,6 +497,290 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
   __syncthreads();
   if (warp == 0) tc::tmem_free(tmem, a.tmem_cols);
 }
+
+// Persistent variant for large grids (split-K off): a CTA walks tiles blockIdx.x, +gridDim.x, ...;
+// warp 0 issues MMAs into one of two TMEM accumulators, warps 1-4 compute each tile's row map
+// and fill the stage ring (its counter runs across tiles), warps 5-8 drain the other
+// accumulator -- the epilogue and the next tile's prologue overlap the MMAs instead of
+// serialising with them (one-tile CTAs spent ~2.6x the operand-bound MMA time there).
+template <int NKC, int T, int MODE, int BFM>
+__global__ void __launch_bounds__(kTcThreads) conv_tcp_k(TcConv a) {
+  constexpr int PG = 1;
+  constexpr bool BF = BFM != 0, B3 = BFM == 2;
+  D2IP_PDL_ENTRY();
+  extern __shared__ __align__(1024) uint8_t smem[];
+  constexpr int CB = NKC * (BF ? 8 : 4);
+  constexpr int NH = BFM == 1 ? 1 : 2;  // operand halves per stage (3xTF32 / 3xbf16: hi, lo)
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const int b = blockIdx.z;
+  const int ks = blockIdx.y % a.kspl;
+  const int n0 = (blockIdx.y / a.kspl) * a.Ns;  // first output channel of this CTA's slice
+  const int Ns = a.Ns, WR = a.WR, WRp = a.WRp;
+  constexpr bool PW = MODE == 3;  // 1^3: one tap, window = the tile rows
+  constexpr int nt = PW ? 1 : MODE ? 2 : 3, t0 = MODE == 2 ? 1 : 0, ntap = nt * nt;
+  // (kh, kw) of the q-th live tap as a 3x3 index: nt = 3 -> q; nt = 2 -> the 2x2 block at (t0, t0)
+  auto tap9 = [&](int q) { return nt == 3 ? q : (t0 + (q >> 1)) * 3 + (t0 + (q & 1)); };
+  const uint32_t Ab = (uint32_t)NKC * WRp * 16, Bb = (uint32_t)ntap * NKC * Ns * 16;
+  const uint32_t Sb = NH * (Ab + Bb);
+  // layout: 2 stages of [A hi][A lo][B hi][B lo] (bf16: [A][B]), row map, barriers full[2] empty[2] done, TMEM slot
+  const int NST = a.nst;  // ring depth (2 or 3 stages)
+  int* rowmap2 = reinterpret_cast<int*>(smem + NST * Sb);  // [2][3 WR]: tile parity
+  uint64_t* full = reinterpret_cast<uint64_t*>(rowmap2 + 6 * WR);
+  uint64_t* empty = full + 3;
+  uint64_t* tfull = empty + 3;  // [2]: accumulator ready (MMA -> epilogue)
+  uint64_t* tempty = tfull + 2; // [2]: accumulator drained (epilogue -> MMA)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tempty + 2);
+  const int nct = (a.ntiles - (int)blockIdx.x + (int)gridDim.x - 1) / (int)gridDim.x;  // this CTA's tiles
+
+  if (warp == 0) tc::tmem_alloc(tslot, a.tmem_cols);
+  if (tid == 0) {
+    for (int i = 0; i < NST; ++i) {
+      tc::mbar_init(&full[i], 128);  // producer warps 1-4
+      tc::mbar_init(&empty[i], 1);
+    }
+    for (int i = 0; i < 2; ++i) {
+      tc::mbar_init(&tfull[i], 1);
+      tc::mbar_init(&tempty[i], 4);  // one arrival per epilogue warp
+    }
+    tc::fence_mbar_init();
+  }
+  const d2ip_act x = a.x;
+  tc::fence_before();
+  __syncthreads();
+  tc::fence_after();
+  const uint32_t tmem = *tslot;
+  const float* xb = x.ptr + b * x.bstride;
+  const float* wpb = a.wp + b * a.wpbs;
+  const int S_all = nt * a.n_cb;
+  const int s_lo = (int)((long long)ks * S_all / a.kspl), s_hi = (int)((long long)(ks + 1) * S_all / a.kspl);
+  const int S = s_hi - s_lo;  // this CTA's stages: s_lo + [0, S)
+  const int nA = WR * NKC;
+  const int kc_all = BF ? a.Kc >> 3 : a.Kc >> 2;  // 16-byte chunks per K
+
+  if (warp == 0) {
+    // ---- MMA issue (one elected thread); stage s lives in slot s & 1
+    if (lane == 0) {
+      // descriptors of slot 0; a tap / K step / slot is an add to the 14-bit
+      // start-address field (smem addresses < 256 KB never carry out of it)
+      const uint32_t sbase = tc::smem_u32(smem);
+      const uint64_t dAhi = tc::make_desc(sbase, WRp * 16, 128), dAlo = dAhi + (Ab >> 4);
+      const uint64_t dBhi = tc::make_desc(sbase + NH * Ab, Ns * 16, 128), dBlo = dBhi + (Bb >> 4);
+      int g = 0;  // stage counter across tiles
+      for (int it = 0; it < nct; ++it) {
+      const int acc = it & 1;
+      if (it >= 2) tc::mbar_wait(&tempty[acc], (uint32_t)(((it >> 1) - 1) & 1));
+      tc::fence_after();
+      const uint32_t tacc = tmem + (uint32_t)(acc * T * Ns);
+      for (int s = 0; s < S; ++s, ++g) {
+        const int slot = g % NST;
+        tc::mbar_wait(&full[slot], (uint32_t)((g / NST) & 1));
+        tc::fence_after();
+        if (BF) tc::fence_proxy_async();
+        const uint64_t boff = (uint64_t)slot * (Sb >> 4);
+        for (int tq = 0; tq < ntap; ++tq) {
+          const int t9 = tap9(tq);
+          const int rowoff = PW ? 0 : (t9 >= 6 ? 2 : t9 >= 3 ? 1 : 0) * a.Sw + (t9 % 3);
+#pragma unroll
+          for (int j = 0; j < NKC / 2; ++j) {
+            const uint64_t bo = boff + (uint64_t)((tq * NKC + 2 * j) * Ns);
+            const uint32_t first = (s | tq | j) ? 1u : 0u;
+#pragma unroll
+            for (int tt = 0; tt < T; ++tt) {  // sub-tile tt: rows + 128 tt, accumulator columns + tt Ns
+              const uint64_t ao = boff + (uint64_t)(2 * j * WRp + rowoff + tt * kTcRows);
+              const uint32_t d = tacc + (uint32_t)(tt * Ns);
+              if (B3) {
+                tc::mma_f16(d, dAlo + ao, dBhi + bo, a.idesc, first);
+                tc::mma_f16(d, dAhi + ao, dBlo + bo, a.idesc, 1u);
+                tc::mma_f16(d, dAhi + ao, dBhi + bo, a.idesc, 1u);
+              } else if (BF) {
+                tc::mma_f16(d, dAhi + ao, dBhi + bo, a.idesc, first);
+              } else {
+                tc::mma_tf32(d, dAlo + ao, dBhi + bo, a.idesc, first);
+                tc::mma_tf32(d, dAhi + ao, dBlo + bo, a.idesc, 1u);
+                tc::mma_tf32(d, dAhi + ao, dBhi + bo, a.idesc, 1u);
+              }
+            }
+          }
+        }
+        tc::commit(&empty[slot]);
+      }
+      tc::commit(&tfull[acc]);
+      }
+    }
+  } else if (warp <= 4) {
+    // ---- producers (warps 1-4): per tile its row map, then its stages
+    constexpr int GT = 128;
+    const int gtid = tid - 32;
+    int g = 0;
+    for (int it = 0; it < nct; ++it) {
+    const int u0 = a.u_first + ((int)blockIdx.x + it * (int)gridDim.x) * T * kTcRows;
+    int* rowmap = rowmap2 + (it & 1) * 3 * WR;
+    for (int i = gtid; i < (PW ? WR : 3 * WR); i += GT) {
+      const int kd = i / WR, r = i - kd * WR;
+      const int u = PW ? u0 + r : u0 + (kd - 1) * a.Sh - a.Sw - 1 + r;
+      int off = -1;
+      if (u >= 0) {
+        const int dp = u / a.Sh, rem = u - dp * a.Sh;
+        const int hp = rem / a.Sw, wp = rem - hp * a.Sw;
+        if (dp >= 1 && dp <= a.gd && hp >= 1 && hp <= a.gh && wp >= 1 && wp <= a.gw)
+          off = ((dp - 1) * a.gh + (hp - 1)) * a.gw + (wp - 1);
+      }
+      rowmap[i] = off;
+    }
+    asm volatile("bar.sync 1, 128;" ::: "memory");
+    for (int s = 0; s < S; ++s, ++g) {
+      const int slot = g % NST;
+      if (g >= NST) tc::mbar_wait(&empty[slot], (uint32_t)(((g / NST) - 1) & 1));
+      if (a.dbg) {  // D2IP_TC_DBG=1: no fills (measures the MMA side alone; wrong results)
+        tc::mbar_arrive(&full[slot]);
+        continue;
+      }
+      const int sg = s_lo + s;
+      const int kdi = sg / a.n_cb, cb = sg - kdi * a.n_cb;
+      const int kd = PW ? 0 : t0 + kdi;
+      const int* rm = rowmap + kd * WR;
+      uint8_t* A = smem + slot * Sb;
+      if (BF && !B3 && a.xtw) {
+        // bf16 twin of x: one 16-byte async copy per (row, 8-channel chunk); zero-fill for padding rows
+        const uint16_t* xt = reinterpret_cast<const uint16_t*>(x.bf16) + b * x.bstride;
+        const long long plane = (long long)x.h * x.w;
+        for (int i = gtid; i < nA; i += GT) {
+          const int r = i / NKC, kc = i % NKC;
+          const int off = rm[r];
+          const uint16_t* src = nullptr;
+          if (MODE == 1) {
+            const int c = cb * CB + 8 * kc, p = c / x.c, ci = c - p * x.c;
+            const int pd = p >> 2, ph = (p >> 1) & 1, pw = p & 1;
+            if (off >= 0 && (!pd || (off & 4)) && (!ph || (off & 2)) && (!pw || (off & 1)))
+              src = xt + ((off >> 3) + pd * plane + ph * x.w + pw) * (long long)x.cstride + ci;
+          } else if (off >= 0) {
+            src = xt + (long long)off * x.cstride + cb * CB + 8 * kc;
+          }
+          tc::cp_async16(A + ((size_t)kc * WRp + r) * 16, src ? src : xt, src ? 16u : 0u);
+        }
+      } else if (BF) {
+        // fp32 window -> registers -> bf16 rows. A work item is one float4 (4
+        // channels; consecutive threads read consecutive 16 B of a voxel row) that
+        // lands as 8 bytes, half of a 16-byte chunk; eight loads in flight per thread.
+        constexpr int PPR = 2 * NKC;  // float4 pieces per window row
+        const int nP = WR * PPR;
+        const long long plane = (long long)x.h * x.w;
+        for (int i0 = gtid; i0 < nP; i0 += 8 * GT) {
+          float4 v[8];
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int i = i0 + q * GT;
+            v[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+            if (i >= nP) continue;
+            const int r = i / PPR, pc = i % PPR;
+            const int off = rm[r];
+            if (MODE == 1) {
+              const int c = cb * CB + 4 * pc, p = c / x.c, ci = c - p * x.c;
+              const int pd = p >> 2, ph = (p >> 1) & 1, pw = p & 1;
+              if (off >= 0 && (!pd || (off & 4)) && (!ph || (off & 2)) && (!pw || (off & 1)))
+                v[q] = *reinterpret_cast<const float4*>(
+                    xb + ((off >> 3) + pd * plane + ph * x.w + pw) * (long long)x.cstride + ci);
+            } else if (off >= 0) {
+              v[q] = *reinterpret_cast<const float4*>(xb + (long long)off * x.cstride + cb * CB + 4 * pc);
+            }
+          }
+#pragma unroll
+          for (int q = 0; q < 8; ++q) {
+            const int i = i0 + q * GT;
+            if (i >= nP) continue;
+            const int r = i / PPR, pc = i % PPR;
+            uint2 o;
+            o.x = bf2(v[q].x, v[q].y);
+            o.y = bf2(v[q].z, v[q].w);
+            *reinterpret_cast<uint2*>(A + ((size_t)(pc >> 1) * WRp + r) * 16 + (pc & 1) * 8) = o;
+            if (B3) {  // lo = bf16(x - hi)
+              const float2 h0 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&o.x));
+              const float2 h1 = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&o.y));
+              const uint2 l = make_uint2(bf2(v[q].x - h0.x, v[q].y - h0.y), bf2(v[q].z - h1.x, v[q].w - h1.y));
+              *reinterpret_cast<uint2*>(A + Ab + ((size_t)(pc >> 1) * WRp + r) * 16 + (pc & 1) * 8) = l;
+            }
+          }
+        }
+      } else if (MODE == 1) {
+        // parity gather: virtual channel c = p * C_x + ci reads input voxel 2o + p
+        const long long plane = (long long)x.h * x.w;
+        for (int i = gtid; i < nA; i += GT) {
+          const int r = i / NKC, kc = i % NKC;
+          const int off = rm[r];
+          const int c = cb * CB + 4 * kc, p = c / x.c, ci = c - p * x.c;
+          const int pd = p >> 2, ph = (p >> 1) & 1, pw = p & 1;
+          const bool ok = off >= 0 && (!pd || (off & 4)) && (!ph || (off & 2)) && (!pw || (off & 1));
+          const float* src =
+              ok ? xb + ((off >> 3) + pd * plane + ph * x.w + pw) * (long long)x.cstride + ci : xb;
+          tc::cp_async16(A + ((size_t)kc * WRp + r) * 16, src, ok ? 16u : 0u);
+        }
+      } else {
+        const float* xc = xb + cb * CB;
+        for (int i = gtid; i < nA; i += GT) {
+          const int r = i / NKC, kc = i % NKC;
+          const int off = rm[r];
+          const float* src = off >= 0 ? xc + (long long)off * x.cstride + 4 * kc : xb;
+          tc::cp_async16(A + ((size_t)kc * WRp + r) * 16, src, off >= 0 ? 16u : 0u);
+        }
+      }
+      // B: nt^2 taps x NKC chunks, each a contiguous run of Ns 16-byte rows; one warp per run
+      // (16-byte rows: 4 floats, or 8 bf16 = 4 float slots of the pack buffer)
+      uint8_t* Bt = A + NH * Ab;
+      const float* wk = wpb + ((long long)(kd * 9) * kc_all + cb * NKC) * a.Np * 4 + (long long)n0 * 4;
+      const int gwarp = gtid >> 5;
+      for (int q = gwarp; q < ntap * NKC; q += GT / 32) {
+        const int tq = q / NKC, kcl = q % NKC;
+        const int t9 = PW ? 0 : tap9(tq);
+        const float* src = wk + ((long long)t9 * kc_all + kcl) * a.Np * 4;
+        uint8_t* dst = Bt + (size_t)q * Ns * 16;
+        for (int n = lane; n < Ns; n += 32) {
+          tc::cp_async16(dst + n * 16, src + n * 4, 16u);
+          if (NH == 2) tc::cp_async16(dst + Bb + n * 16, src + a.wlo + n * 4, 16u);
+        }
+      }
+      if (BF && !B3 && a.xtw && a.async_arrive) {
+        // every operand of the stage is an async copy: arrive when this thread's copies
+        // land (no wait here -- the next stage's copies are issued while these fly);
+        // the MMA thread's proxy fence makes them visible to the tensor core
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(tc::smem_u32(&full[slot]))
+                     : "memory");
+        continue;
+      }
+      tc::cp_async_commit();
+      tc::cp_async_wait<0>();
+      // lo half of the landed activation window; the raw fp32 window is the hi
+      // operand (the tensor core truncates fp32 to TF32: tools/tf32_round_probe.cu)
+      if (!BF)
+      for (int i = gtid; i < nA; i += GT) {
+        const int r = i / NKC, kc = i % NKC;
+        const float4 v = *reinterpret_cast<const float4*>(A + ((size_t)kc * WRp + r) * 16);
+        float4 l;
+        l.x = v.x - tf32_hi(v.x); l.y = v.y - tf32_hi(v.y); l.z = v.z - tf32_hi(v.z); l.w = v.w - tf32_hi(v.w);
+        *reinterpret_cast<float4*>(A + Ab + ((size_t)kc * WRp + r) * 16) = l;
+      }
+      tc::fence_proxy_async();
+      tc::mbar_arrive(&full[slot]);
+    }
+
+    }  // tiles
+  } else {
+    // ---- epilogue (warps 5-8): one warp per TMEM lane quadrant, all columns
+    for (int it = 0; it < nct; ++it) {
+      const int acc = it & 1;
+      const int u0 = a.u_first + ((int)blockIdx.x + it * (int)gridDim.x) * T * kTcRows;
+      tc::mbar_wait(&tfull[acc], (uint32_t)((it >> 1) & 1));
+      tc::fence_after();
+      tc_epilogue<T, MODE>(a, tmem + (uint32_t)(acc * T * Ns), b, n0, u0, ks, S, warp, lane, 0, Ns);
+      tc::fence_before();
+      __syncwarp();
+      if (lane == 0) tc::mbar_arrive(&tempty[acc]);
+    }
+  }
+  tc::fence_before();
+  __syncthreads();
+  if (warp == 0) tc::tmem_free(tmem, a.tmem_cols);
+}
+
 
 // TMA-fed bf16 variant (stride 1 and 1^3 layers whose input has a bf16 twin):
 // one producer thread fetches each stage's activation window as whole padded
@@ -1012,6 +1301,41 @@ static int tc_dispatch_nkc(const TcConv& a, dim3 grid, size_t smem, cudaStream_t
   return D2IP_OK;
 }
 
+template <int NKC, int T, int MODE, int BFM>
+static int tcp_launch(const TcConv& a, dim3 grid, size_t smem, cudaStream_t st) {
+  static bool attr = false;
+  if (!attr) {
+    D2IP_CUDA(cudaFuncSetAttribute(conv_tcp_k<NKC, T, MODE, BFM>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
+    attr = true;
+  }
+  D2IP_CUDA(launch_pdl((conv_tcp_k<NKC, T, MODE, BFM>), grid, kTcThreads, smem, st, a));
+  return D2IP_OK;
+}
+
+template <int NKC, int BFM>
+static int tcp_dispatch(const TcConv& a, dim3 grid, size_t smem, cudaStream_t st, int mode) {
+  if (mode == 3) {
+    if (a.T == 4) return tcp_launch<NKC, 4, 3, BFM>(a, grid, smem, st);
+    if (a.T == 2) return tcp_launch<NKC, 2, 3, BFM>(a, grid, smem, st);
+    return tcp_launch<NKC, 1, 3, BFM>(a, grid, smem, st);
+  }
+  if (a.T == 4) return tcp_launch<NKC, 4, 0, BFM>(a, grid, smem, st);
+  if (a.T == 2) return tcp_launch<NKC, 2, 0, BFM>(a, grid, smem, st);
+  return tcp_launch<NKC, 1, 0, BFM>(a, grid, smem, st);
+}
+
+template <int BFM>
+static int tcp_dispatch_nkc(const TcConv& a, dim3 grid, size_t smem, cudaStream_t st, int mode) {
+  switch (a.CB / (BFM != 0 ? 8 : 4)) {
+    case 2: return tcp_dispatch<2, BFM>(a, grid, smem, st, mode);
+    case 4: return tcp_dispatch<4, BFM>(a, grid, smem, st, mode);
+    case 8: return tcp_dispatch<8, BFM>(a, grid, smem, st, mode);
+    case 16: return tcp_dispatch<16, BFM>(a, grid, smem, st, mode);
+    default: D2IP_CHECK_ARG(false, "conv_tc: unsupported channel block %d", a.CB);
+  }
+  return D2IP_OK;
+}
+
 template <int NKC, int T, int MODE>
 static int tma_launch(const TcConv& a, const CUtensorMap& tm, dim3 grid, cudaStream_t st) {
   static bool attr = false;
@@ -1134,6 +1458,31 @@ int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, lo
     return v && atoi(v) == 2;
   }();
   int rc;
+  // persistent kernel (D2IP_TC_PERSIST=1, opt-in): large stride-1 / 1^3 layers without split-K
+  static const bool persist_on = [] {
+    const char* v = getenv("D2IP_TC_PERSIST");
+    return v && atoi(v) != 0;
+  }();
+  if (persist_on && !use_tma && a.kspl == 1 && (mode == 0 || mode == 3) && 2 * a.T * a.Ns <= 512 &&
+      (long long)tiles * (a.Np / a.Ns) * batch >= 2 * 148) {
+    TcConv p = a;
+    p.ntiles = tiles;
+    int cols = 32;
+    while (cols < 2 * p.T * p.Ns) cols *= 2;
+    p.tmem_cols = cols;
+    const size_t sm = (size_t)p.nst * stage_bytes(p.CB, p.Ns, p.WRp, p.nt, p.bf, p.b3) + 6 * (size_t)p.WR * 4 + 10 * 8 + 16;
+    const int per_sm = std::max(1, std::min((int)((size_t)227 * 1024 / sm), 512 / cols));
+    const int ctas = std::min(tiles, std::max(1, 148 * per_sm / std::max(1, (p.Np / p.Ns) * batch)));
+    const dim3 pgrid(ctas, p.Np / p.Ns, batch);
+    if (b3) rc = tcp_dispatch_nkc<2>(p, pgrid, sm, st, mode);
+    else if (bf) rc = tcp_dispatch_nkc<1>(p, pgrid, sm, st, mode);
+    else rc = tcp_dispatch_nkc<0>(p, pgrid, sm, st, mode);
+    D2IP_RET(rc);
+    D2IP_LAUNCH_CHECK();
+    if (deferred) *deferred = 0;
+    set_variant(b3 ? "tcgen05_bf16x3_persistent" : bf ? "tcgen05_bf16_persistent" : "tcgen05_tf32x3_persistent");
+    return D2IP_OK;
+  }
   if (use_tma) {
     // tensor map over the bf16 twin: dims (C, W, H, D, B) innermost first, one padded line per box
     CUtensorMap tm;

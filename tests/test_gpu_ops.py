@@ -329,8 +329,12 @@ def test_adam_matches_torch():
     assert rel(pd.cpu(), p.detach()) < 1e-6
 
 
-def test_conv_tma_variant_subprocess():
-    """The opt-in TMA-fed bf16 conv (D2IP_TC_TMA=1, read once per process) against torch."""
+@pytest.mark.parametrize("knob,prefix,cin,prec", [("D2IP_TC_TMA", "tcgen05_bf16_tma", 32, "bf16"),
+                                                  ("D2IP_TC_PERSIST", "tcgen05_bf16_persistent", 32, "bf16"),
+                                                  ("D2IP_TC_PERSIST", "tcgen05_bf16x3_persistent", 32, "tf32")])
+def test_conv_optin_variant_subprocess(knob, prefix, cin, prec):
+    """Opt-in conv variants (env knobs are read once per process) against torch: the TMA-fed
+    bf16 kernel and the persistent kernel (large grids)."""
     import os
     import subprocess
     import sys
@@ -339,7 +343,7 @@ import ctypes as C, torch, torch.nn.functional as F, sys
 sys.path.insert(0, '.')
 from paper_2507_14046_b200 import _native as N
 torch.manual_seed(0)
-cin, cout, sp = 32, 32, (12, 10, 9)
+cin, cout, sp = @CIN@, 32, @SPATIAL@
 x = torch.randn(1, cin, *sp); w = torch.randn(cout, cin, 3, 3, 3) * 0.05; bias = torch.randn(cout)
 ref = F.conv3d(x, w, bias, padding=1)
 xd = x.permute(0, 2, 3, 4, 1).contiguous().cuda(); xt = xd.to(torch.bfloat16)
@@ -349,19 +353,22 @@ def act(t, c, tw=None):
     a = N.Act(); a.ptr = t.data_ptr(); a.d, a.h, a.w = sp; a.c = a.cstride = c; a.bstride = t.numel()
     if tw is not None: a.bf16 = tw.data_ptr()
     return a
-L = N.lib(); ws_n = L.d2ip_conv3d_ws_bytes(cin, cout, 3, 1, N.PREC['bf16'], 1)
+L = N.lib(); ws_n = L.d2ip_conv3d_ws_bytes(cin, cout, 3, 1, N.PREC[@PREC@], 1)
 ws = torch.empty(max(ws_n, 16), dtype=torch.uint8, device='cuda')
 st = C.c_void_p(torch.cuda.current_stream().cuda_stream)
 N.check(L.d2ip_conv3d_fwd(act(xd, cin, xt), C.c_void_p(P.data_ptr()), C.c_void_p(P.data_ptr() + 4 * w.numel()),
-        0, 3, 1, act(y, cout), 0, N.PREC['bf16'], C.c_void_p(ws.data_ptr()), ws_n, 1, st), 'fwd')
+        0, 3, 1, act(y, cout), 0, N.PREC[@PREC@], C.c_void_p(ws.data_ptr()), ws_n, 1, st), 'fwd')
 torch.cuda.synchronize()
 out = y.permute(0, 4, 1, 2, 3).cpu()
 print(L.d2ip_last_variant().decode(), float((out - ref).norm() / ref.norm()))
 """
-    env = dict(os.environ, D2IP_TC_TMA="1")
-    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=300,
+    # the persistent kernel only takes grids of >= 2 x 148 tiles: a 48 x 48 x 40 volume
+    spatial = (12, 10, 9) if knob == "D2IP_TC_TMA" else (48, 48, 40)
+    code = code.replace("@CIN@", str(cin)).replace("@SPATIAL@", str(spatial)).replace("@PREC@", repr(prec))
+    env = dict(os.environ, **{knob: "1"})
+    r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600,
                        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert r.returncode == 0, r.stderr[-2000:]
     variant, err = r.stdout.split()
-    assert variant.startswith("tcgen05_bf16_tma")
-    assert float(err) < TOL["bf16"]
+    assert variant.startswith(prefix), variant
+    assert float(err) < TOL[prec]
