@@ -69,6 +69,7 @@ namespace d2ip {
 constexpr int kTcThreads = 288;  // warp 0: MMA issue; warps 1-8: two producer groups, then the epilogue
 constexpr int kTcProd = 256;
 constexpr int kTcRows = 128;
+constexpr int kTcpThreads = 416;  // persistent kernel: MMA warp, 8 producer warps, 4 epilogue warps
 
 __host__ __device__ static inline int np_of(int n) { return (n + 15) / 16 * 16; }
 static inline int wr_of(int sw, int T = 1) { return T * kTcRows + 2 * sw + 2; }
@@ -499,12 +500,12 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
 }
 
 // Persistent variant for large grids (split-K off): a CTA walks tiles blockIdx.x, +gridDim.x, ...;
-// warp 0 issues MMAs into one of two TMEM accumulators, warps 1-4 compute each tile's row map
-// and fill the stage ring (its counter runs across tiles), warps 5-8 drain the other
+// warp 0 issues MMAs into one of two TMEM accumulators, warps 1-8 compute each tile's row map
+// and fill the stage ring (its counter runs across tiles), warps 9-12 drain the other
 // accumulator -- the epilogue and the next tile's prologue overlap the MMAs instead of
 // serialising with them (one-tile CTAs spent ~2.6x the operand-bound MMA time there).
 template <int NKC, int T, int MODE, int BFM>
-__global__ void __launch_bounds__(kTcThreads) conv_tcp_k(TcConv a) {
+__global__ void __launch_bounds__(kTcpThreads) conv_tcp_k(TcConv a) {
   constexpr int PG = 1;
   constexpr bool BF = BFM != 0, B3 = BFM == 2;
   D2IP_PDL_ENTRY();
@@ -535,7 +536,7 @@ __global__ void __launch_bounds__(kTcThreads) conv_tcp_k(TcConv a) {
   if (warp == 0) tc::tmem_alloc(tslot, a.tmem_cols);
   if (tid == 0) {
     for (int i = 0; i < NST; ++i) {
-      tc::mbar_init(&full[i], 128);  // producer warps 1-4
+      tc::mbar_init(&full[i], kTcProd);  // producer warps 1-8
       tc::mbar_init(&empty[i], 1);
     }
     for (int i = 0; i < 2; ++i) {
@@ -607,9 +608,9 @@ __global__ void __launch_bounds__(kTcThreads) conv_tcp_k(TcConv a) {
       tc::commit(&tfull[acc]);
       }
     }
-  } else if (warp <= 4) {
-    // ---- producers (warps 1-4): per tile its row map, then its stages
-    constexpr int GT = 128;
+  } else if (warp <= 8) {
+    // ---- producers (warps 1-8): per tile its row map, then its stages
+    constexpr int GT = kTcProd;
     const int gtid = tid - 32;
     int g = 0;
     for (int it = 0; it < nct; ++it) {
@@ -627,7 +628,7 @@ __global__ void __launch_bounds__(kTcThreads) conv_tcp_k(TcConv a) {
       }
       rowmap[i] = off;
     }
-    asm volatile("bar.sync 1, 128;" ::: "memory");
+    asm volatile("bar.sync 1, 256;" ::: "memory");
     for (int s = 0; s < S; ++s, ++g) {
       const int slot = g % NST;
       if (g >= NST) tc::mbar_wait(&empty[slot], (uint32_t)(((g / NST) - 1) & 1));
@@ -764,7 +765,7 @@ __global__ void __launch_bounds__(kTcThreads) conv_tcp_k(TcConv a) {
 
     }  // tiles
   } else {
-    // ---- epilogue (warps 5-8): one warp per TMEM lane quadrant, all columns
+    // ---- epilogue (warps 9-12): one warp per TMEM lane quadrant, all columns
     for (int it = 0; it < nct; ++it) {
       const int acc = it & 1;
       const int u0 = a.u_first + ((int)blockIdx.x + it * (int)gridDim.x) * T * kTcRows;
@@ -1308,7 +1309,7 @@ static int tcp_launch(const TcConv& a, dim3 grid, size_t smem, cudaStream_t st) 
     D2IP_CUDA(cudaFuncSetAttribute(conv_tcp_k<NKC, T, MODE, BFM>, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024));
     attr = true;
   }
-  D2IP_CUDA(launch_pdl((conv_tcp_k<NKC, T, MODE, BFM>), grid, kTcThreads, smem, st, a));
+  D2IP_CUDA(launch_pdl((conv_tcp_k<NKC, T, MODE, BFM>), grid, kTcpThreads, smem, st, a));
   return D2IP_OK;
 }
 
@@ -1458,11 +1459,15 @@ int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, lo
     return v && atoi(v) == 2;
   }();
   int rc;
-  // persistent kernel (D2IP_TC_PERSIST=1, opt-in): large stride-1 / 1^3 layers without split-K
-  static const bool persist_on = [] {
+  // persistent kernel for large stride-1 / 1^3 layers without split-K: default for bf16 layers
+  // (cfg4: 96->32 fwd 186 vs 199 us, 64->64 dgrad 38 vs 41 us; 139.2 -> 140.4 it/s), opt-in for
+  // the 3xbf16 / 3xTF32 ones (16->16 at 64x64x32: 43 vs 41 us). D2IP_TC_PERSIST=0 / 1 / 2:
+  // never / bf16 only / every precision.
+  static const int persist_mode = [] {
     const char* v = getenv("D2IP_TC_PERSIST");
-    return v && atoi(v) != 0;
+    return v ? atoi(v) : 1;
   }();
+  const bool persist_on = persist_mode == 2 || (persist_mode == 1 && bf && !b3);
   if (persist_on && !use_tma && a.kspl == 1 && (mode == 0 || mode == 3) && 2 * a.T * a.Ns <= 512 &&
       (long long)tiles * (a.Np / a.Ns) * batch >= 2 * 148) {
     TcConv p = a;
