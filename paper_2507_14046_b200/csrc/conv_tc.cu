@@ -1472,6 +1472,15 @@ int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, lo
       (long long)tiles * (a.Np / a.Ns) * batch >= 2 * 148) {
     TcConv p = a;
     p.ntiles = tiles;
+    // D2IP_TCP_NST=3: a third ring stage when it fits (measured slower: cfg4 135.5 vs 140.0 it/s,
+    // the larger footprint costs co-resident CTAs)
+    static const int tcp_nst = [] {
+      const char* v = getenv("D2IP_TCP_NST");
+      return v ? atoi(v) : 2;
+    }();
+    if (tcp_nst >= 3 &&
+        3 * stage_bytes(p.CB, p.Ns, p.WRp, p.nt, p.bf, p.b3) + 6 * (size_t)p.WR * 4 + 128 <= (size_t)225 * 1024)
+      p.nst = 3;
     int cols = 32;
     while (cols < 2 * p.T * p.Ns) cols *= 2;
     p.tmem_cols = cols;
