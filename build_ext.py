@@ -12,6 +12,7 @@ from __future__ import annotations
 import os
 import subprocess
 import sys
+from concurrent.futures import ThreadPoolExecutor
 from pathlib import Path
 
 ROOT = Path(__file__).resolve().parent
@@ -35,21 +36,29 @@ def headers():
 def build(force: bool = False, verbose: bool = False) -> Path:
     BUILD.mkdir(parents=True, exist_ok=True)
     hdr_mtime = max(p.stat().st_mtime for p in headers())
-    objs = []
+    objs, todo = [], []
     for src in sources():
         obj = BUILD / (src.stem + ".o")
         objs.append(obj)
         if not force and obj.exists() and obj.stat().st_mtime > max(src.stat().st_mtime, hdr_mtime):
             continue
+        todo.append((src, obj))
+
+    def compile_one(job):
+        src, obj = job
         cmd = [NVCC, *ARCH, *FLAGS, "-c", str(src), "-o", str(obj)]
-        res = subprocess.run(cmd, capture_output=True, text=True)
-        if res.returncode != 0:
-            sys.stderr.write(res.stdout + res.stderr)
-            raise RuntimeError(f"nvcc failed on {src.name}")
-        log = BUILD / (src.stem + ".ptxas.log")
-        log.write_text(res.stdout + res.stderr)
-        if verbose:
-            print(res.stderr)
+        return src, obj, subprocess.run(cmd, capture_output=True, text=True)
+
+    # translation units compile independently: in parallel, the largest first
+    todo.sort(key=lambda j: -j[0].stat().st_size)
+    with ThreadPoolExecutor(max_workers=max(1, min(len(todo), os.cpu_count() or 1))) as pool:
+        for src, obj, res in pool.map(compile_one, todo):
+            if res.returncode != 0:
+                sys.stderr.write(res.stdout + res.stderr)
+                raise RuntimeError(f"nvcc failed on {src.name}")
+            (BUILD / (src.stem + ".ptxas.log")).write_text(res.stdout + res.stderr)
+            if verbose:
+                print(res.stderr)
     if force or not OUT.exists() or OUT.stat().st_mtime < max(o.stat().st_mtime for o in objs):
         cmd = [NVCC, *ARCH, "-shared", "-cudart", "static", "-o", str(OUT), *map(str, objs), "-lcuda"]
         res = subprocess.run(cmd, capture_output=True, text=True)
