@@ -58,6 +58,7 @@
 #include <cstdlib>
 
 #include <cuda.h>
+#include <cudaTypedefs.h>
 #include <cuda_bf16.h>
 
 #include "common.cuh"
@@ -1505,9 +1506,20 @@ int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, lo
     const cuuint64_t gstr[4] = {(cuuint64_t)x.cstride * 2, (cuuint64_t)x.w * x.cstride * 2,
                                 (cuuint64_t)x.h * x.w * x.cstride * 2, (cuuint64_t)x.bstride * 2};
     const cuuint32_t box[5] = {8, (cuuint32_t)a.Sw, 1, 1, 1}, estr[5] = {1, 1, 1, 1, 1};
-    const CUresult cr = cuTensorMapEncodeTiled(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, x.bf16, gdim, gstr, box, estr,
-                                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
-                                               CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    // the driver entry point is resolved through the runtime (no libcuda link dependency: the
+    // library must load on machines without a driver, e.g. for the CPU-side ABI tests)
+    static PFN_cuTensorMapEncodeTiled_v12000 encode = [] {
+      void* fn = nullptr;
+      cudaDriverEntryPointQueryResult q;
+      if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+          q != cudaDriverEntryPointSuccess)
+        fn = nullptr;
+      return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+    }();
+    D2IP_CHECK_ARG(encode != nullptr, "conv_tc: cuTensorMapEncodeTiled unavailable");
+    const CUresult cr = encode(&tm, CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 5, x.bf16, gdim, gstr, box, estr,
+                               CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                               CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     D2IP_CHECK_ARG(cr == CUDA_SUCCESS, "conv_tc: cuTensorMapEncodeTiled failed (%d)", (int)cr);
     rc = tma_dispatch_nkc(a, tm, grid, st, mode);
   } else if (b3)
