@@ -5,4 +5,5 @@ echo ncu rc $?
 ncu -i gpurun_out/ncu_$TAG.ncu-rep --page details --csv > gpurun_out/ncu_$TAG.details.csv 2>/dev/null
 ncu -i gpurun_out/ncu_$TAG.ncu-rep --page raw --csv > gpurun_out/ncu_$TAG.raw.csv 2>/dev/null
 ncu -i gpurun_out/ncu_$TAG.ncu-rep --page source --csv > gpurun_out/ncu_$TAG.source.csv 2>/dev/null
+rm -f gpurun_out/ncu_$TAG.ncu-rep gpurun_out/ncu_$TAG.source.csv  # (keep the copy-back under 64 MiB)
 ls -la gpurun_out/ncu_$TAG*
