@@ -348,24 +348,34 @@ class DeviceNet:
     def status_host(self) -> np.ndarray:
         return self.status.cpu().numpy()
 
-    def fetch_frame(self, b: int, n: int):
-        """One synchronisation for a finished frame: status, the first n trace rows, the
-        output sigmoid volume and theta, copied device -> pinned host in stream order
-        (the caller enqueued the output forward first). Returns host tensors."""
-        if getattr(self, "_pin", None) is None or self._pin["trace"].shape[0] < self.trace.shape[1]:
-            self._pin = {
+    def enqueue_fetch(self, b: int, n: int, slot: int = 0) -> dict:
+        """Device -> pinned host copies of a finished frame's status, first n trace rows,
+        output sigmoid volume and theta, in stream order (no synchronisation). Two slots:
+        a frame's results stay intact while the next frame runs (pipelined TPP chain)."""
+        pins = getattr(self, "_pins", None)
+        if pins is None or pins[0]["trace"].shape[0] < self.trace.shape[1]:
+            pins = [{
                 "status": torch.empty(self.status.shape, dtype=self.status.dtype, pin_memory=True),
                 "trace": torch.empty(self.trace.shape[1:], dtype=self.trace.dtype, pin_memory=True),
                 "sig": torch.empty(self.sig.shape[1:], dtype=self.sig.dtype, pin_memory=True),
                 "theta": torch.empty(self.theta.shape[1:], dtype=self.theta.dtype, pin_memory=True),
-            }
-        p = self._pin
+            } for _ in range(2)]
+            self._pins = pins
+        p = pins[slot]
         p["status"].copy_(self.status, non_blocking=True)
         if n > 0:
             p["trace"][:n].copy_(self.trace[b, :n], non_blocking=True)
         p["sig"].copy_(self.sig[b], non_blocking=True)
         p["theta"].copy_(self.theta[b], non_blocking=True)
-        torch.cuda.current_stream().synchronize()
+        ev = torch.cuda.Event()
+        ev.record()
+        return {"buf": p, "n": n, "event": ev}
+
+    def fetch_frame(self, b: int, n: int):
+        """enqueue_fetch + wait: (status, trace rows, sig, theta) host views."""
+        f = self.enqueue_fetch(b, n)
+        f["event"].synchronize()
+        p = f["buf"]
         return p["status"].numpy(), p["trace"][:n].numpy(), p["sig"], p["theta"]
 
     def trace_host(self, b: int, n: int) -> np.ndarray:
