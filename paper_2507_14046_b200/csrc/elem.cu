@@ -376,53 +376,51 @@ __global__ void __launch_bounds__(256) tail_dgrad_g_k(const float* __restrict__ 
 }
 
 // Weight + bias gradient of the tail: dW[c][t] = sum_v x[v][c] gt[v - off_t],
-// db = sum_v gt[v]. Each CTA walks a voxel range (one float4 x load and 27 gt
-// scalars per voxel), reduces its lane groups with a fixed shuffle tree and a
-// fixed-order pass over its warps, and writes one partial [27 C + 1]; a second
-// pass sums the partials in CTA order.
+// db = sum_v gt[v]. Each CTA walks a voxel range for the nine taps of one kd
+// plane (blockIdx.z; 36 accumulators per lane instead of 108, so several CTAs
+// per SM hide the gt load latency), reduces its lane groups with a fixed
+// shuffle tree and a fixed-order pass over its warps, and writes its taps of
+// one partial [27 C + 1]; a second pass sums the partials in CTA order.
 template <int G>
 __global__ void __launch_bounds__(256) tail_wgrad_g_k(d2ip_act x, const float* __restrict__ gt, int vchunk,
                                                       float* __restrict__ part) {
   D2IP_PDL_ENTRY();
-  constexpr int VPW = 32 / G;  // voxel groups per warp
-  __shared__ float red[8][G][27 * 4 + 1];
-  const int b = blockIdx.y;
+  __shared__ float red[8][G][9 * 4 + 1];
+  const int b = blockIdx.y, kd = blockIdx.z;
   const int C = 4 * G;
   const long long V = (long long)x.d * x.h * x.w;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, l = lane % G, grp = threadIdx.x / G;
-  float acc[27][4];
+  float acc[9][4];
 #pragma unroll
-  for (int t = 0; t < 27; ++t) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.f;
+  for (int t = 0; t < 9; ++t) acc[t][0] = acc[t][1] = acc[t][2] = acc[t][3] = 0.f;
   float bsum = 0.f;
   const float* g = gt + b * V;
   const long long v_lo = (long long)blockIdx.x * vchunk, v_hi = min(V, v_lo + vchunk);
   for (long long v = v_lo + grp; v < v_hi; v += 256 / G) {
     const int ow = (int)(v % x.w), oh = (int)((v / x.w) % x.h), od = (int)(v / ((long long)x.w * x.h));
     const float4 q = __ldg(reinterpret_cast<const float4*>(x.ptr + b * x.bstride + v * x.cstride + 4 * l));
-    if (l == 0) bsum += g[v];
+    if (l == 0 && kd == 0) bsum += g[v];
+    const int id = od - kd + 1;
+    if (id < 0 || id >= x.d) continue;
 #pragma unroll
-    for (int kd = 0; kd < 3; ++kd) {
-      const int id = od - kd + 1;
+    for (int kh = 0; kh < 3; ++kh) {
+      const int ih = oh - kh + 1;
 #pragma unroll
-      for (int kh = 0; kh < 3; ++kh) {
-        const int ih = oh - kh + 1;
-#pragma unroll
-        for (int kw = 0; kw < 3; ++kw) {
-          const int iw = ow - kw + 1;
-          const bool in = id >= 0 && id < x.d && ih >= 0 && ih < x.h && iw >= 0 && iw < x.w;
-          const float s = in ? __ldg(g + ((long long)id * x.h + ih) * x.w + iw) : 0.f;
-          const int t = (kd * 3 + kh) * 3 + kw;
-          acc[t][0] = fmaf(q.x, s, acc[t][0]);
-          acc[t][1] = fmaf(q.y, s, acc[t][1]);
-          acc[t][2] = fmaf(q.z, s, acc[t][2]);
-          acc[t][3] = fmaf(q.w, s, acc[t][3]);
-        }
+      for (int kw = 0; kw < 3; ++kw) {
+        const int iw = ow - kw + 1;
+        const bool in = ih >= 0 && ih < x.h && iw >= 0 && iw < x.w;
+        const float s = in ? __ldg(g + ((long long)id * x.h + ih) * x.w + iw) : 0.f;
+        const int t = kh * 3 + kw;
+        acc[t][0] = fmaf(q.x, s, acc[t][0]);
+        acc[t][1] = fmaf(q.y, s, acc[t][1]);
+        acc[t][2] = fmaf(q.z, s, acc[t][2]);
+        acc[t][3] = fmaf(q.w, s, acc[t][3]);
       }
     }
   }
-  // fold the VPW voxel groups of the warp (lanes l, l + G, ...): fixed xor tree
+  // fold the 32 / G voxel groups of the warp (lanes l, l + G, ...): fixed xor tree
 #pragma unroll
-  for (int t = 0; t < 27; ++t)
+  for (int t = 0; t < 9; ++t)
 #pragma unroll
     for (int j = 0; j < 4; ++j) {
       float v = acc[t][j];
@@ -433,24 +431,24 @@ __global__ void __launch_bounds__(256) tail_wgrad_g_k(d2ip_act x, const float* _
   for (int o = 16; o >= 1; o >>= 1) bsum += __shfl_xor_sync(0xffffffffu, bsum, o);
   if (lane < G) {
 #pragma unroll
-    for (int t = 0; t < 27; ++t)
+    for (int t = 0; t < 9; ++t)
 #pragma unroll
       for (int j = 0; j < 4; ++j) red[warp][l][t * 4 + j] = acc[t][j];
-    if (lane == 0) red[warp][0][27 * 4] = bsum;
+    if (lane == 0) red[warp][0][9 * 4] = bsum;
   }
   __syncthreads();
   float* pb = part + ((long long)b * gridDim.x + blockIdx.x) * (27 * C + 1);
-  for (int i = threadIdx.x; i < 27 * C + 1; i += blockDim.x) {
+  for (int i = threadIdx.x; i < 9 * C + 1; i += blockDim.x) {
     float s = 0.f;
-    if (i < 27 * C) {
-      const int c = i / 27, t = i % 27, ll = c / 4, j = c % 4;  // output order: OIDHW [c][t]
+    if (i < 9 * C) {
+      const int c = i / 9, t = i % 9, ll = c / 4, j = c % 4;  // output order: OIDHW [c][kd * 9 + t]
       for (int wi = 0; wi < 8; ++wi) s += red[wi][ll][t * 4 + j];
-    } else {
-      for (int wi = 0; wi < 8; ++wi) s += red[wi][0][27 * 4];
+      pb[c * 27 + kd * 9 + t] = s;
+    } else if (kd == 0) {
+      for (int wi = 0; wi < 8; ++wi) s += red[wi][0][9 * 4];
+      pb[27 * C] = s;
     }
-    pb[i] = s;
   }
-  (void)VPW;
 }
 
 __global__ void tail_wgrad_reduce_k(const float* __restrict__ part, int nblk, int n, float* __restrict__ gw,
@@ -523,7 +521,7 @@ int tail_wgrad(d2ip_act x, const float* gt, float* gw, long long gwbs, void* ws,
   D2IP_CHECK_ARG(ws_bytes >= tail_wgrad_ws(x.c, V, batch), "tail_wgrad: workspace too small");
   const int vchunk = cdiv(V, nblk);
   float* part = reinterpret_cast<float*>(ws);
-  const dim3 grid(nblk, batch);
+  const dim3 grid(nblk, batch, 3);
 #define D2IP_TAILW(G_) \
   case G_: D2IP_CUDA(launch_pdl(tail_wgrad_g_k<G_>, grid, 256, 0, st, x, gt, vchunk, part)); break;
   switch (x.c / 4) { D2IP_TAILW(1) D2IP_TAILW(2) D2IP_TAILW(4) D2IP_TAILW(8) }
