@@ -147,20 +147,21 @@ __global__ void __launch_bounds__(256) dw_wgrad_k(d2ip_act x, d2ip_act gy, int s
 // (float4 loads of gy and of the 27 x taps, coalesced across the group), a CTA walks a
 // voxel range, folds its voxel groups with a fixed xor-shuffle tree and its warps in a
 // fixed order, and writes one partial [C][27] + [C] per CTA for reduce_chunks (~300
-// partials instead of ~1,000 single-channel chunk sums).
+// partials instead of ~1,000 single-channel chunk sums). blockIdx.z = the kd plane:
+// nine taps per CTA (36 accumulators per lane instead of 108, several CTAs per SM).
 template <int G>
 __global__ void __launch_bounds__(256) dw_wgrad_g_k(d2ip_act x, d2ip_act gy, int stride, float* __restrict__ partial,
                                                     int vchunk) {
   D2IP_PDL_ENTRY();
   extern __shared__ float red_dyn[];  // [8 warps][G][27 * 4 + 5]
   auto red = reinterpret_cast<float(*)[G][27 * 4 + 5]>(red_dyn);
-  const int b = blockIdx.y;
+  const int b = blockIdx.y, kd = blockIdx.z;
   const int C = 4 * G;
   const long long V = (long long)gy.d * gy.h * gy.w;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31, l = lane % G, grp = threadIdx.x / G;
-  float4 acc[27];
+  float4 acc[9];
 #pragma unroll
-  for (int t = 0; t < 27; ++t) acc[t] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int t = 0; t < 9; ++t) acc[t] = make_float4(0.f, 0.f, 0.f, 0.f);
   float4 bs = make_float4(0.f, 0.f, 0.f, 0.f);
   const float* xb = x.ptr + b * x.bstride + 4 * l;
   const float* gb = gy.ptr + b * gy.bstride + 4 * l;
@@ -169,8 +170,7 @@ __global__ void __launch_bounds__(256) dw_wgrad_g_k(d2ip_act x, d2ip_act gy, int
     const int ow = (int)(o % gy.w), oh = (int)((o / gy.w) % gy.h), od = (int)(o / ((long long)gy.w * gy.h));
     const float4 g = __ldg(reinterpret_cast<const float4*>(gb + o * gy.cstride));
     bs.x += g.x; bs.y += g.y; bs.z += g.z; bs.w += g.w;
-#pragma unroll
-    for (int kd = 0; kd < 3; ++kd) {
+    {
       const int id = od * stride + kd - 1;
 #pragma unroll
       for (int kh = 0; kh < 3; ++kh) {
@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(256) dw_wgrad_g_k(d2ip_act x, d2ip_act gy, int
           const int iw = ow * stride + kw - 1;
           if (id >= 0 && id < x.d && ih >= 0 && ih < x.h && iw >= 0 && iw < x.w) {
             const float4 q = __ldg(reinterpret_cast<const float4*>(xb + (((long long)id * x.h + ih) * x.w + iw) * x.cstride));
-            float4& a = acc[(kd * 3 + kh) * 3 + kw];
+            float4& a = acc[kh * 3 + kw];
             a.x = fmaf(g.x, q.x, a.x);
             a.y = fmaf(g.y, q.y, a.y);
             a.z = fmaf(g.z, q.z, a.z);
@@ -196,13 +196,13 @@ __global__ void __launch_bounds__(256) dw_wgrad_g_k(d2ip_act x, d2ip_act gy, int
     return v;
   };
 #pragma unroll
-  for (int t = 0; t < 27; ++t) {
+  for (int t = 0; t < 9; ++t) {
     acc[t].x = fold(acc[t].x); acc[t].y = fold(acc[t].y); acc[t].z = fold(acc[t].z); acc[t].w = fold(acc[t].w);
   }
   bs.x = fold(bs.x); bs.y = fold(bs.y); bs.z = fold(bs.z); bs.w = fold(bs.w);
   if (lane < G) {
 #pragma unroll
-    for (int t = 0; t < 27; ++t) {
+    for (int t = 0; t < 9; ++t) {
       red[warp][l][t * 4 + 0] = acc[t].x; red[warp][l][t * 4 + 1] = acc[t].y;
       red[warp][l][t * 4 + 2] = acc[t].z; red[warp][l][t * 4 + 3] = acc[t].w;
     }
@@ -210,20 +210,23 @@ __global__ void __launch_bounds__(256) dw_wgrad_g_k(d2ip_act x, d2ip_act gy, int
   }
   __syncthreads();
   float* p = partial + ((long long)b * gridDim.x + blockIdx.x) * 28 * C;
-  for (int i = threadIdx.x; i < 28 * C; i += blockDim.x) {
-    int ll, k;
-    if (i < 27 * C) {
-      const int c = i / 27, t = i % 27;  // [c][t]
+  for (int i = threadIdx.x; i < 10 * C; i += blockDim.x) {
+    int ll, k, dst;
+    if (i < 9 * C) {
+      const int c = i / 9, t = i % 9;  // [c][kd * 9 + t]
       ll = c / 4;
       k = t * 4 + (c & 3);
+      dst = c * 27 + kd * 9 + t;
     } else {
-      const int c = i - 27 * C;
+      if (kd != 0) break;  // the bias sums come from plane 0
+      const int c = i - 9 * C;
       ll = c / 4;
       k = 108 + (c & 3);
+      dst = 27 * C + c;
     }
     float sum = 0.f;
     for (int w = 0; w < 8; ++w) sum += red[w][ll][k];
-    p[i] = sum;
+    p[dst] = sum;
   }
 }
 
@@ -274,7 +277,7 @@ int dw_conv_wgrad(d2ip_act x, d2ip_act gy, int stride, float* gw, long long gwbs
     D2IP_CHECK_ARG(ws_bytes >= (size_t)batch * nblk * 28 * C * sizeof(float), "dw_wgrad: workspace too small");
     float* partial = reinterpret_cast<float*>(ws);
     const int vchunk = cdiv(V, nblk);
-    const dim3 grid(nblk, batch);
+    const dim3 grid(nblk, batch, 3);
     const size_t sm = (size_t)8 * (C / 4) * (27 * 4 + 5) * sizeof(float);
 #define D2IP_DWG(G_)                                                                                  \
   case G_: {                                                                                         \
