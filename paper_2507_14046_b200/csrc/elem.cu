@@ -300,21 +300,25 @@ __global__ void __launch_bounds__(256) tail_fwd_g_k(d2ip_act x, const float* __r
   if (v < V) {
     const int ow = (int)(v % x.w), oh = (int)((v / x.w) % x.h), od = (int)(v / ((long long)x.w * x.h));
     const float* xb = x.ptr + b * x.bstride + 4 * l;
-#pragma unroll 3
+    // branch-free taps (out-of-grid taps load the centre voxel and are skipped by a
+    // select): all 27 loads can be in flight at once; same summation order.
+#pragma unroll
     for (int kd = 0; kd < 3; ++kd) {
       const int id = od + kd - 1;
-      if (id < 0 || id >= x.d) continue;
+      const bool okd = id >= 0 && id < x.d;
 #pragma unroll
       for (int kh = 0; kh < 3; ++kh) {
         const int ih = oh + kh - 1;
-        if (ih < 0 || ih >= x.h) continue;
+        const bool okh = okd && ih >= 0 && ih < x.h;
 #pragma unroll
         for (int kw = 0; kw < 3; ++kw) {
           const int iw = ow + kw - 1;
-          if (iw < 0 || iw >= x.w) continue;
-          const float4 q = __ldg(reinterpret_cast<const float4*>(xb + (((long long)id * x.h + ih) * x.w + iw) * x.cstride));
+          const bool ok = okh && iw >= 0 && iw < x.w;
+          const long long off = ok ? (((long long)id * x.h + ih) * x.w + iw) * x.cstride : v * x.cstride;
+          const float4 q = __ldg(reinterpret_cast<const float4*>(xb + off));
           const float4 wq = sw[((kd * 3 + kh) * 3 + kw) * G + l];
-          acc = fmaf(q.x, wq.x, fmaf(q.y, wq.y, fmaf(q.z, wq.z, fmaf(q.w, wq.w, acc))));
+          const float t = fmaf(q.x, wq.x, fmaf(q.y, wq.y, fmaf(q.z, wq.z, fmaf(q.w, wq.w, acc))));
+          acc = ok ? t : acc;
         }
       }
     }
@@ -351,19 +355,22 @@ __global__ void __launch_bounds__(256) tail_dgrad_g_k(const float* __restrict__ 
   const int ow = (int)(v % gx.w), oh = (int)((v / gx.w) % gx.h), od = (int)(v / ((long long)gx.w * gx.h));
   const float* g = gt + b * V;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
-#pragma unroll 3
+  // branch-free taps as in tail_fwd_g_k: an out-of-grid tap contributes s = 0
+  // (fmaf(0, w, acc) == acc for finite w), all 27 loads in flight
+#pragma unroll
   for (int kd = 0; kd < 3; ++kd) {
     const int id = od - kd + 1;
-    if (id < 0 || id >= gx.d) continue;
+    const bool okd = id >= 0 && id < gx.d;
 #pragma unroll
     for (int kh = 0; kh < 3; ++kh) {
       const int ih = oh - kh + 1;
-      if (ih < 0 || ih >= gx.h) continue;
+      const bool okh = okd && ih >= 0 && ih < gx.h;
 #pragma unroll
       for (int kw = 0; kw < 3; ++kw) {
         const int iw = ow - kw + 1;
-        if (iw < 0 || iw >= gx.w) continue;
-        const float s = __ldg(g + ((long long)id * gx.h + ih) * gx.w + iw);
+        const bool ok = okh && iw >= 0 && iw < gx.w;
+        const float s0 = __ldg(g + (ok ? ((long long)id * gx.h + ih) * gx.w + iw : v));
+        const float s = ok ? s0 : 0.f;
         const float4 wq = sw[((kd * 3 + kh) * 3 + kw) * G + l];
         acc.x = fmaf(s, wq.x, acc.x);
         acc.y = fmaf(s, wq.y, acc.y);
