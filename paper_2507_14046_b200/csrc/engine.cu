@@ -526,8 +526,9 @@ static int backward(Ctx& k) {
 
 static int adam(Ctx& k) {
   d2ip_engine& E = k.E;
-  return adam_flat(E.b.theta, E.b.grad, E.b.adam_m, E.b.adam_v, (long long)k.B * E.nparams, E.d.lr, E.d.beta1,
-                   E.d.beta2, E.d.eps, E.b.status, E.b.status + 1, k.st);
+  // one segment per sequence: each reads its own step / bad flag (status[b * 4 + {0, 1}])
+  return adam_flat(E.b.theta, E.b.grad, E.b.adam_m, E.b.adam_v, (long long)E.nparams, E.d.lr, E.d.beta1,
+                   E.d.beta2, E.d.eps, E.b.status, E.b.status + 1, k.st, k.B, 4);
 }
 
 static Ctx ctx(d2ip_engine& E, void* stream) {

@@ -165,7 +165,7 @@ int tv_fwd_bwd(const float* mapped, const float* history, int max_history, const
                float* gmapped, float* reg_partial, int batch, cudaStream_t st);
 
 // adam.cu
-int adam_flat(float* p, const float* g, float* m, float* v, long long n, float lr, float b1, float b2,
-              float eps, const int* step, const int* bad, cudaStream_t st);
+int adam_flat(float* p, const float* g, float* m, float* v, long long nper, float lr, float b1, float b2,
+              float eps, const int* step, const int* bad, cudaStream_t st, int batch = 1, int sstride = 0);
 
 }  // namespace d2ip

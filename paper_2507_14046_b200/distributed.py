@@ -59,15 +59,42 @@ def allreduce_grads(grad: torch.Tensor) -> None:
         dist.all_reduce(grad, op=dist.ReduceOp.SUM)
 
 
-def joint_upws(engine, iters: int, on_step=None) -> None:
-    """Data-parallel joint warm-start: per iteration grads -> all-reduce ->
-    Adam. `engine.reset_frame()` must have been called (fresh optimiser)."""
+def allreduce_status(status: torch.Tensor) -> None:
+    """MAX of the per-sequence status words over ranks, in place and in stream order
+    (step and history count are equal on every rank; the bad flag becomes "any rank
+    saw a non-finite loss", so every rank skips the same Adam updates)."""
+    world, _ = world_info()
+    if world > 1:
+        dist.all_reduce(status, op=dist.ReduceOp.MAX)
+
+
+def joint_upws(engine, iters: int, data_norm: str = "l2sq", on_step=None) -> None:
+    """Data-parallel joint warm-start: per iteration grads -> all-reduce(grad, SUM)
+    -> all-reduce(status, MAX) -> Adam. `engine.reset_frame()` must have been called
+    (fresh optimiser). The summed per-rank gradients are the gradient of the joint
+    loss only for the squared norm (sum_f ||J sigma - dv_f||^2); with "l2" each rank's
+    sqrt(local sum) would be a different objective, so it is rejected. A non-finite
+    loss on any rank freezes theta on every rank and raises NumericalError on every
+    rank after the loop (the device never waits on the host inside the loop)."""
+    if data_norm != "l2sq":
+        raise ValueError(f"joint warm-start needs data_norm='l2sq' (sum of per-frame squared misfits), "
+                         f"got {data_norm!r}")
+    status = getattr(engine, "status", None)
     for k in range(1, iters + 1):
         engine.grads()
         allreduce_grads(engine.grad)
+        if status is not None:
+            allreduce_status(status)
         engine.adam()
         if on_step is not None:
             on_step(k)
+    if status is not None:
+        st = status.cpu().numpy().reshape(-1, 4)
+        if (st[:, 1] != 0).any():
+            from .errors import NumericalError
+            exc = NumericalError(f"non-finite loss in the joint warm-start at iteration {int(st[:, 1].max())}")
+            exc.iteration = int(st[:, 1].max())
+            raise exc
 
 
 # ---------------------------------------------------------------------------

@@ -19,6 +19,7 @@ extension's kernels. Data layout in HBM:
 from __future__ import annotations
 
 import math
+import warnings
 from dataclasses import dataclass
 
 import numpy as np
@@ -66,19 +67,29 @@ class ColumnMap:
         return cls(perm, vox, col)
 
 
+def host_tensor(arr: np.ndarray) -> torch.Tensor:
+    """CPU tensor view of a host array for a device upload (read-only arrays included:
+    the view is only ever read, so torch's non-writable warning does not apply)."""
+    if not arr.flags.writeable:
+        with warnings.catch_warnings():
+            warnings.simplefilter("ignore", UserWarning)
+            return torch.from_numpy(arr)
+    return torch.from_numpy(arr)
+
+
 def noise_to_device(values: np.ndarray) -> torch.Tensor:
     """(R,C,P) or (C_z,R,C,P) host noise -> [R][C][P][C_z] fp32 on the GPU."""
     v = np.asarray(values)
     if v.ndim == 3:
         v = v[None]
-    t = torch.from_numpy(np.ascontiguousarray(v, dtype=np.float32))
+    t = host_tensor(np.ascontiguousarray(v, dtype=np.float32))
     return t.permute(1, 2, 3, 0).contiguous().cuda()
 
 
 def upload_masked_J(values: np.ndarray, perm: np.ndarray, vp: int) -> torch.Tensor:
     """Host M x V block -> device M x Vp fp32, columns permuted to memory order."""
     M, V = values.shape
-    raw = torch.from_numpy(np.ascontiguousarray(values, dtype=np.float32)).cuda()
+    raw = host_tensor(np.ascontiguousarray(values, dtype=np.float32)).cuda()
     out = torch.zeros((M, vp), dtype=torch.float32, device="cuda")
     out[:, :V] = raw.index_select(1, torch.from_numpy(perm).long().cuda())
     return out

@@ -36,12 +36,18 @@ class LstsqEngine:
         self.v = torch.zeros_like(x0)
         self.t = 0
         self.lr = lr
+        self.status = torch.zeros((1, 4), dtype=torch.int32)  # [step, bad iteration, n_hist, -]
 
     def grads(self):
         r = sum(self.A @ self.theta - d for d in self.frames) if self.frames else torch.zeros(self.A.shape[0])
         self.grad.copy_(2 * self.A.T @ r)
+        self.status[0, 0] += 1
+        if not torch.isfinite(r).all() and self.status[0, 1] == 0:
+            self.status[0, 1] = int(self.status[0, 0])
 
     def adam(self):
+        if self.status[0, 1] != 0:
+            return
         self.t += 1
         b1, b2, eps = 0.9, 0.999, 1e-8
         self.m.lerp_(self.grad, 1 - b1)
@@ -57,6 +63,28 @@ def _problem():
     frames = [torch.randn(12, generator=g, dtype=torch.float64) for _ in range(4)]
     x0 = torch.zeros(5, dtype=torch.float64)
     return A, frames, x0
+
+
+def _worker_nan(rank, world, port, out):
+    """rank 1 sees a non-finite frame: every rank must freeze theta and raise."""
+    from paper_2507_14046_b200.errors import NumericalError
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        A, frames, x0 = _problem()
+        mine = [frames[i] for i in shard(len(frames), world, rank)]
+        if rank == 1:
+            mine[0] = mine[0].clone()
+            mine[0][3] = float("nan")
+        eng = LstsqEngine(A, mine, x0)
+        try:
+            joint_upws(eng, 5)
+            out.put((rank, "no error", None))
+        except NumericalError as e:
+            out.put((rank, "raised", (e.iteration, eng.theta.tolist())))
+    finally:
+        dist.destroy_process_group()
 
 
 def _worker(rank, world, port, out):
@@ -103,3 +131,27 @@ def test_joint_upws_allreduce_matches_single_process():
     assert torch.allclose(torch.tensor(thetas[0], dtype=torch.float64), ref.theta, rtol=1e-12, atol=1e-12)
     # the 64 cfg3 sequences are split 32/32 and gathered in rank order
     assert [i for s in seqs for i in s] == list(range(64))
+
+
+def test_joint_upws_rejects_l2_norm():
+    A, frames, x0 = _problem()
+    with pytest.raises(ValueError):
+        joint_upws(LstsqEngine(A, frames, x0), 1, data_norm="l2")
+
+
+def test_joint_upws_nonfinite_raises_on_every_rank():
+    world = 2
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker_nan, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert [r[1] for r in res] == ["raised", "raised"]
+    # both ranks report the same iteration and kept the identical (initial) theta
+    assert res[0][2] == res[1][2]
+    assert res[0][2][0] == 1 and res[0][2][1] == [0.0] * 5

@@ -304,6 +304,42 @@ def test_batched_sequences_match_single():
         assert torch.equal(bn.theta[s], nets[s].theta[0])
 
 
+def test_batched_divergence_is_per_sequence():
+    """A sequence whose loss goes non-finite skips only its own Adam updates
+    (status word per sequence): the others equal their separate runs."""
+    spec = W.small_spec(grid=(8, 8, 8), channels=(8, 16), in_channels=4, rings=(0.5,))
+    wls = [W.make_workload(spec, seed=s, frames=1) for s in range(3)]
+    net = spec.network()
+    bad = 1
+    ref = []
+    for s, wl in enumerate(wls):
+        dn = DeviceNet(net, wl.grid.shape, wl.matrix.n_measurements, wl.matrix.mask, output_map=(-0.6, 0.3),
+                       max_iters=8)
+        dn.set_noise(sample_noise_input(wl.grid, s, 4, 0.1).values)
+        dn.set_J_host(wl.matrix.values)
+        dn.set_theta(kaiming_flat(net, seed=s + 1))
+        dn.set_dv(wl.voltages.frames[0].values)
+        dn.reset_frame(); dn.run(4)
+        ref.append(dn.theta[0].clone())
+    bn = DeviceNet(net, wls[0].grid.shape, wls[0].matrix.n_measurements, wls[0].matrix.mask, batch=3,
+                   j_shared=False, output_map=(-0.6, 0.3), max_iters=8)
+    for s, wl in enumerate(wls):
+        bn.set_noise(sample_noise_input(wl.grid, s, 4, 0.1).values, b=s)
+        bn.set_J_host(wl.matrix.values, b=s)
+        bn.set_theta(kaiming_flat(net, seed=s + 1), b=s)
+        dv = wl.voltages.frames[0].values.copy()
+        if s == bad:
+            dv[0] = np.nan
+        bn.set_dv(dv, b=s)
+    bn.reset_frame(); bn.run(4)
+    torch.cuda.synchronize()
+    st = bn.status_host()
+    assert st[bad, 1] == 1 and st[0, 1] == 0 and st[2, 1] == 0
+    assert torch.equal(bn.theta[bad].cpu(), torch.as_tensor(kaiming_flat(net, seed=bad + 1)).float())
+    for s in (0, 2):
+        assert torch.equal(bn.theta[s], ref[s])
+
+
 def test_batched_driver_matches_sequence_driver():
     """cfg3 per-rank body: sequences in lockstep == reconstruct_sequence each."""
     from paper_2507_14046_b200.distributed import reconstruct_batched
