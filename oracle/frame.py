@@ -112,6 +112,26 @@ class OracleFrameOptimizer:
         g = {k: p.grad.detach().clone() for k, p in self.model.named_parameters()}
         return float(total), float(data), float(reg), g, mapped.detach()
 
+    def iterate(self, dv, history, iters, opt=None, frame_label=1):
+        """`iters` bodies of the loop at pipeline.py:310-331 (loss terms, finiteness check,
+        trace record, zero_grad, backward, Adam step) against a persistent optimiser and
+        nothing else -- the bench's CPU arm times exactly one training iteration per step
+        (no per-call Adam construction, no final output forward). Returns the optimiser."""
+        if opt is None:
+            opt = torch.optim.Adam(self.model.parameters(), lr=self.lr, betas=self.betas)
+        dv_t = dv if torch.is_tensor(dv) else torch.as_tensor(np.asarray(dv), dtype=torch.float32)
+        start = time.perf_counter()
+        for k in range(1, iters + 1):
+            total, data, reg, _ = self.loss_terms(dv_t, history)
+            if not torch.isfinite(total):
+                raise FloatingPointError(f"non-finite loss at stage frame={frame_label} iteration={k}")
+            _ = (frame_label, k, float(data.detach()), float(torch.as_tensor(reg).detach()),
+                 float(total.detach()), time.perf_counter() - start)
+            opt.zero_grad(set_to_none=True)
+            total.backward()
+            opt.step()
+        return opt
+
     def optimize(self, dv, history, iters, frame_label=1):
         opt = torch.optim.Adam(self.model.parameters(), lr=self.lr, betas=self.betas)
         dv_t = torch.as_tensor(np.asarray(dv), dtype=torch.float32)
