@@ -161,6 +161,21 @@ size_t d2ip_jac_adj_ws_bytes(int m, int vp, int batch);
 int d2ip_adam(float* p, const float* g, float* m, float* v, long long n, float lr, float beta1,
               float beta2, float eps, const int* step, void* stream);
 
+/* ---- Standalone 4D-TV (drop-in spatial_tv / temporal_tv / tv4d) ---------
+ * Replaces pkg/src/d2ip/regularizers.py:86-140 for one (R, C, P) fp32 volume
+ * (p fastest) and n_history past volumes [n][R][C][P]:
+ *   *value = lambda_s * spatial_tv(current) + lambda_t * temporal_tv(history, current)
+ * (device float), grad (optional, [R][C][P]) = d value / d current.
+ * ws: d2ip_tv4d_ws_bytes(R, C, P) bytes. */
+size_t d2ip_tv4d_ws_bytes(int R, int C, int P);
+int d2ip_tv4d(const float* current, const float* history, int n_history, int R, int C, int P, float lambda_s,
+              float lambda_t, float epsilon, float* value, float* grad, void* ws, size_t ws_bytes, void* stream);
+
+/* ---- fp64 projection (drop-in forward_project) --------------------------
+ * y[m] = sum_j A[m][j] x[j] in float64 (pkg/src/d2ip/forward.py:115-122),
+ * A row-major with leading dimension lda; deterministic fixed-order sums. */
+int d2ip_project_f64(const double* A, long long lda, const double* x, int m, int n, double* y, void* stream);
+
 /* ---- Sensitivity operator assembly ---------------------
  * Replaces assemble_sensitivity + normalize_sensitivity
  * (pkg/src/d2ip/forward.py:58-112) on the device, fp64:
@@ -252,6 +267,9 @@ int d2ip_engine_predict(d2ip_engine* e, float* y, void* stream);
 int d2ip_engine_adam(d2ip_engine* e, void* stream);
 /* Forward + loss + backward without the Adam update (gradient parity). */
 int d2ip_engine_grads(d2ip_engine* e, void* stream);
+/* The same gradient program replayed from a CUDA graph captured on first use (the
+ * joint warm-start's per-iteration grads -> NCCL all-reduce -> d2ip_engine_adam). */
+int d2ip_engine_grads_graph(d2ip_engine* e, void* stream);
 /* Kernel launches one graph-replayed iteration issues. */
 int d2ip_engine_launches_per_iter(const d2ip_engine* e);
 

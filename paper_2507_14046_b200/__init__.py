@@ -19,7 +19,9 @@ from .forward import (  # noqa: F401
     SensitivityMatrix,
     VoltageFrame,
     VoltageSequence,
+    forward_project,
 )
+from .model import DeviceModel, build_model, extract_parameters, forward_volume, load_parameters  # noqa: F401
 from .geometry import GridGeometry, cylinder_mask, devectorize, vectorize  # noqa: F401
 from .priornet import (  # noqa: F401
     NetworkConfig,
@@ -32,7 +34,7 @@ from .priornet import (  # noqa: F401
     sample_noise_input,
     save_checkpoint,
 )
-from .regularizers import FrameHistory, TVWeights, decay_weight  # noqa: F401
+from .regularizers import FrameHistory, TVWeights, decay_weight, spatial_tv, temporal_tv, tv4d  # noqa: F401
 from .sensitivity import (  # noqa: F401
     assemble_masked_device,
     assemble_sensitivity,
@@ -45,6 +47,7 @@ from .sensitivity import (  # noqa: F401
 )
 from .pipeline import (  # noqa: F401
     LossTrace,
+    BatchedSequenceResult,
     ReconstructionResult,
     RunConfig,
     ablation_mode,
@@ -52,7 +55,10 @@ from .pipeline import (  # noqa: F401
     loss,
     predict_measurements,
     reconstruct_frame,
+    joint_upws_pretrain,
     reconstruct_sequence,
+    reconstruct_sequence_joint,
+    reconstruct_sequences_batched,
     upws_pretrain,
 )
 

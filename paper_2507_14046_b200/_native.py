@@ -131,6 +131,10 @@ _SIGS = {
                                C.c_void_p, C.c_size_t, C.c_int, C.c_void_p]),
     "d2ip_adam": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_longlong, C.c_float, C.c_float,
                             C.c_float, C.c_float, C.c_void_p, C.c_void_p]),
+    "d2ip_tv4d_ws_bytes": (C.c_size_t, [C.c_int, C.c_int, C.c_int]),
+    "d2ip_tv4d": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_float, C.c_float,
+                            C.c_float, C.c_void_p, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p]),
+    "d2ip_project_f64": (C.c_int, [C.c_void_p, C.c_longlong, C.c_void_p, C.c_int, C.c_int, C.c_void_p, C.c_void_p]),
     "d2ip_engine_create": (C.c_int, [C.POINTER(NetDesc), C.POINTER(C.c_void_p)]),
     "d2ip_engine_destroy": (None, [C.c_void_p]),
     "d2ip_engine_param_count": (C.c_longlong, [C.c_void_p]),
@@ -142,6 +146,7 @@ _SIGS = {
     "d2ip_engine_run": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
     "d2ip_engine_forward": (C.c_int, [C.c_void_p, C.c_int, C.c_void_p]),
     "d2ip_engine_grads": (C.c_int, [C.c_void_p, C.c_void_p]),
+    "d2ip_engine_grads_graph": (C.c_int, [C.c_void_p, C.c_void_p]),
     "d2ip_engine_predict": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "d2ip_engine_adam": (C.c_int, [C.c_void_p, C.c_void_p]),
     "d2ip_engine_launches_per_iter": (C.c_int, [C.c_void_p]),

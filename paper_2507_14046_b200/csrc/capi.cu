@@ -282,4 +282,16 @@ int d2ip_adam(float* p, const float* g, float* m, float* v, long long n, float l
   return d2ip::adam_flat(p, g, m, v, n, lr, beta1, beta2, eps, step, nullptr, d2ip::S(stream));
 }
 
+size_t d2ip_tv4d_ws_bytes(int R, int C, int P) { return d2ip::tv4d_ws_bytes(R, C, P); }
+
+int d2ip_tv4d(const float* current, const float* history, int n_history, int R, int C, int P, float lambda_s,
+              float lambda_t, float epsilon, float* value, float* grad, void* ws, size_t ws_bytes, void* stream) {
+  return d2ip::tv4d_standalone(current, history, n_history, R, C, P, lambda_s, lambda_t, epsilon, value, grad, ws,
+                               ws_bytes, d2ip::S(stream));
+}
+
+int d2ip_project_f64(const double* A, long long lda, const double* x, int m, int n, double* y, void* stream) {
+  return d2ip::project_f64(A, lda, x, m, n, y, d2ip::S(stream));
+}
+
 }  // extern "C"

@@ -1101,6 +1101,34 @@ bool tf32_bf3_enabled() {
   return on;
 }
 
+// TF32 precision: which layer classes take 3xbf16 instead of 3xTF32 (bit 1 stride-1 3^3
+// forward, 2 stride-1 dgrad, 4 stride-2 forward, 8 stride-2 dgrad, 16 1^3). Default 30:
+// stride-1 3^3 FORWARDS stay 3xTF32. Their 3xbf16 error (~4.5e-6 per op vs 7.6e-7,
+// tools/conv_acc.py) crosses a threshold of the network itself: perturbing ONE forward
+// conv of the reference net (cfg2 widths, CPU oracle) by 5e-6 relative noise moves the
+// gradients by 4.8e-4, by 1e-6 noise only 7e-7 -- and the cfg2-width engine with 3xbf16
+// forwards lands 3.7e-3 from the oracle (1e-3 bar), with 3xTF32 forwards 4.7e-6.
+static bool bf3_class(int cls) {
+  static const int m = [] {
+    const char* v = getenv("D2IP_BF3_MASK");
+    return v ? atoi(v) : 30;
+  }();
+  return (m & cls) != 0;
+}
+
+// bf16 precision: forward convolutions on 3xbf16 hi/lo bf16 operands (fp32 accumulate),
+// data / weight gradients single-pass bf16. Single-pass bf16 forwards miss the north
+// star's 1e-2 gradient bar on the cfg4 network (measured 1.7e-2 overall, worst tensor
+// 3.6e-2 on a 32x32x16 grid; tools/l4err.py) -- the forward's rounding reaches the
+// gradients through LayerNorm; with 3xbf16 forwards 2.9e-3. D2IP_BF16_FWD3=0: all bf16.
+bool bf16_fwd3_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("D2IP_BF16_FWD3");
+    return !v || atoi(v) != 0;
+  }();
+  return on;
+}
+
 bool conv_tc_layer(int cin, int cout, int ks, int stride, int dgrad, int precision, long long vout, TcDims* d) {
   TcDims r{};
   if (stride == 1) {
@@ -1111,11 +1139,14 @@ bool conv_tc_layer(int cin, int cout, int ks, int stride, int dgrad, int precisi
     if (!conv_tc_supported(r.K, r.N, ks, 1, precision)) return false;
     // bf16: 16-channel K steps; K % 16 != 0 (e.g. the 8-channel stem) keeps 3xTF32
     if (precision == D2IP_PREC_BF16 && r.K % 16 == 0) {
-      r.mode |= kTcBf16;
-      r.pack |= kTcBf16;
+      const int bit = (!dgrad && bf16_fwd3_enabled()) ? kTcBf3 : kTcBf16;
+      r.mode |= bit;
+      r.pack |= bit;
     }
     // TF32 precision: 3xbf16 (D2IP_TF32_BF3=0 keeps 3xTF32)
-    if (precision == D2IP_PREC_TF32 && r.K % 16 == 0 && tf32_bf3_enabled()) {
+    static const int only_k = [] { const char* v = getenv("D2IP_BF3_ONLYK"); return v ? atoi(v) : 0; }();
+    if (precision == D2IP_PREC_TF32 && r.K % 16 == 0 && tf32_bf3_enabled() &&
+        bf3_class(ks == 1 ? 16 : dgrad ? 2 : 1) && (!only_k || (only_k == r.K && ks == 3 && !dgrad))) {
       r.mode |= kTcBf3;
       r.pack |= kTcBf3;
     }
@@ -1141,10 +1172,12 @@ bool conv_tc_layer(int cin, int cout, int ks, int stride, int dgrad, int precisi
     }
     // bf16: 8-channel chunks must not straddle two parities (mode 1: C_in % 8)
     if (precision == D2IP_PREC_BF16 && r.K % 16 == 0 && (dgrad || cin % 8 == 0)) {
-      r.mode |= kTcBf16;
-      r.pack |= kTcBf16;
+      const int bit = (!dgrad && bf16_fwd3_enabled()) ? kTcBf3 : kTcBf16;
+      r.mode |= bit;
+      r.pack |= bit;
     }
-    if (precision == D2IP_PREC_TF32 && r.K % 16 == 0 && (dgrad || cin % 8 == 0) && tf32_bf3_enabled()) {
+    if (precision == D2IP_PREC_TF32 && r.K % 16 == 0 && (dgrad || cin % 8 == 0) && tf32_bf3_enabled() &&
+        bf3_class(dgrad ? 8 : 4)) {
       r.mode |= kTcBf3;
       r.pack |= kTcBf3;
     }

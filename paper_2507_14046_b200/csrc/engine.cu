@@ -598,32 +598,48 @@ int engine_set_history(d2ip_engine& E, int n, void* stream) {
 static void drop_graph(d2ip_engine& E) {
   if (E.gexec) cudaGraphExecDestroy(E.gexec);
   if (E.graph) cudaGraphDestroy(E.graph);
+  if (E.ggexec) cudaGraphExecDestroy(E.ggexec);
+  if (E.ggraph) cudaGraphDestroy(E.ggraph);
   E.gexec = nullptr;
   E.graph = nullptr;
+  E.ggexec = nullptr;
+  E.ggraph = nullptr;
 }
 
-int engine_run(d2ip_engine& E, int iters, void* stream) {
-  cudaStream_t st = S(stream);
-  if (!E.gexec) {
-    // Capture on a private non-blocking stream (the caller's stream may be the
-    // legacy default stream, which cannot be captured); replay on the caller's.
-    if (!E.cap_stream) D2IP_CUDA(cudaStreamCreateWithFlags(&E.cap_stream, cudaStreamNonBlocking));
-    D2IP_CUDA(cudaStreamBeginCapture(E.cap_stream, cudaStreamCaptureModeThreadLocal));
-    int rc = engine_step(E, E.cap_stream);
-    cudaGraph_t g = nullptr;
-    cudaError_t ce = cudaStreamEndCapture(E.cap_stream, &g);
-    if (rc != D2IP_OK) {
-      if (g) cudaGraphDestroy(g);
-      return rc;
-    }
-    D2IP_CUDA(ce);
-    E.graph = g;
-    D2IP_CUDA(cudaGraphInstantiate(&E.gexec, g, 0));
+// Capture one iteration program (step: forward + loss + backward + Adam; grads: without
+// Adam) once on a private non-blocking stream (the caller's stream may be the legacy
+// default stream, which cannot be captured); replay it on the caller's stream.
+static int capture(d2ip_engine& E, bool grads_only, cudaGraph_t* graph, cudaGraphExec_t* exec) {
+  if (!E.cap_stream) D2IP_CUDA(cudaStreamCreateWithFlags(&E.cap_stream, cudaStreamNonBlocking));
+  D2IP_CUDA(cudaStreamBeginCapture(E.cap_stream, cudaStreamCaptureModeThreadLocal));
+  int rc = grads_only ? engine_grads(E, E.cap_stream) : engine_step(E, E.cap_stream);
+  cudaGraph_t g = nullptr;
+  cudaError_t ce = cudaStreamEndCapture(E.cap_stream, &g);
+  if (rc != D2IP_OK) {
+    if (g) cudaGraphDestroy(g);
+    return rc;
+  }
+  D2IP_CUDA(ce);
+  *graph = g;
+  D2IP_CUDA(cudaGraphInstantiate(exec, g, 0));
+  if (!grads_only) {
     size_t n = 0;
     D2IP_CUDA(cudaGraphGetNodes(g, nullptr, &n));
     E.launches = (int)n;
   }
+  return D2IP_OK;
+}
+
+int engine_run(d2ip_engine& E, int iters, void* stream) {
+  cudaStream_t st = S(stream);
+  if (!E.gexec) D2IP_RET(capture(E, false, &E.graph, &E.gexec));
   for (int i = 0; i < iters; ++i) D2IP_CUDA(cudaGraphLaunch(E.gexec, st));
+  return D2IP_OK;
+}
+
+int engine_grads_graph(d2ip_engine& E, void* stream) {
+  if (!E.ggexec) D2IP_RET(capture(E, true, &E.ggraph, &E.ggexec));
+  D2IP_CUDA(cudaGraphLaunch(E.ggexec, S(stream)));
   return D2IP_OK;
 }
 
@@ -743,6 +759,12 @@ int d2ip_engine_grads(d2ip_engine* e, void* stream) {
   using namespace d2ip;
   D2IP_CHECK_ARG(e && e->bound, "engine not bound");
   return engine_grads(*e, stream);
+}
+
+int d2ip_engine_grads_graph(d2ip_engine* e, void* stream) {
+  using namespace d2ip;
+  D2IP_CHECK_ARG(e && e->bound, "engine not bound");
+  return engine_grads_graph(*e, stream);
 }
 
 int d2ip_engine_run(d2ip_engine* e, int iters, void* stream) {

@@ -74,6 +74,8 @@ struct d2ip_engine {
   int nseg = 0, rsplit = 0, n_reg = 0;
   cudaGraph_t graph = nullptr;
   cudaGraphExec_t gexec = nullptr;
+  cudaGraph_t ggraph = nullptr;      // grads-only iteration (forward + loss + backward), for the joint warm-start
+  cudaGraphExec_t ggexec = nullptr;
   cudaStream_t cap_stream = nullptr;
   int launches = 0;
   // weight gradients (and dgamma/dbeta sums) run on a pool of side lanes, off the

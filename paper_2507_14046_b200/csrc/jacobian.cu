@@ -246,4 +246,28 @@ int jac_adj_finish(const float* partial, int rsplit, int vp, int v, const int* v
   return D2IP_OK;
 }
 
+// fp64 projection y = A x (the drop-in `forward_project`, forward.py:115-122:
+// `matrix.values @ vec` in float64). One warp per row, each lane a strided
+// fixed-order partial, then a fixed xor-shuffle tree: deterministic.
+__global__ void __launch_bounds__(256) project_f64_k(const double* __restrict__ A, long long lda,
+                                                     const double* __restrict__ x, int m, int n,
+                                                     double* __restrict__ y) {
+  const int warp = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
+  if (warp >= m) return;
+  const double* a = A + (long long)warp * lda;
+  double s = 0.0;
+  for (int j = lane; j < n; j += 32) s = fma(a[j], x[j], s);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  if (lane == 0) y[warp] = s;
+}
+
+int project_f64(const double* A, long long lda, const double* x, int m, int n, double* y, cudaStream_t st) {
+  D2IP_CHECK_ARG(A && x && y && m >= 0 && n >= 0 && lda >= n, "project_f64: bad arguments");
+  if (m == 0) return D2IP_OK;
+  project_f64_k<<<cdiv((long long)m * 32, 256), 256, 0, st>>>(A, lda, x, m, n, y);
+  D2IP_LAUNCH_CHECK();
+  return D2IP_OK;
+}
+
 }  // namespace d2ip

@@ -168,4 +168,10 @@ int tv_fwd_bwd(const float* mapped, const float* history, int max_history, const
 int adam_flat(float* p, const float* g, float* m, float* v, long long nper, float lr, float b1, float b2,
               float eps, const int* step, const int* bad, cudaStream_t st, int batch = 1, int sstride = 0);
 
+// standalone drop-in helpers (tv.cu, jacobian.cu)
+size_t tv4d_ws_bytes(int R, int C, int P);
+int tv4d_standalone(const float* current, const float* history, int n_history, int R, int C, int P, float lam_s,
+                    float lam_t, float eps, float* value, float* grad, void* ws, size_t ws_bytes, cudaStream_t st);
+int project_f64(const double* A, long long lda, const double* x, int m, int n, double* y, cudaStream_t st);
+
 }  // namespace d2ip

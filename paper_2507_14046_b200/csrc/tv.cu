@@ -88,4 +88,45 @@ int tv_fwd_bwd(const float* mapped, const float* history, int max_history, const
   return D2IP_OK;
 }
 
+// Standalone 4D-TV (the drop-in `spatial_tv` / `temporal_tv` / `tv4d`,
+// regularizers.py:86-140): value = lam_s * spatial + lam_t * temporal and its
+// gradient w.r.t. `current`, for one volume and n_history past volumes. The
+// history count lives in a device int (the engine kernel's status word), the
+// block partials are summed in fixed order by one more block.
+__global__ void tv_setn_k(int* st, int n) {
+  st[0] = 0; st[1] = 0; st[2] = n; st[3] = 0;
+}
+
+__global__ void __launch_bounds__(kTvThreads) tv_reduce_k(const float* __restrict__ part, int n,
+                                                          float* __restrict__ value) {
+  __shared__ float red[kTvThreads / 32];
+  float s = 0.f;
+  for (int i = threadIdx.x; i < n; i += kTvThreads) s += part[i];
+  s = block_sum<kTvThreads>(s, red);
+  if (threadIdx.x == 0) *value = s;
+}
+
+size_t tv4d_ws_bytes(int R, int C, int P) {
+  const long long Q = (long long)R * C * P;
+  return 16 + (size_t)tv_nblocks(Q) * sizeof(float) + (size_t)Q * sizeof(float);
+}
+
+int tv4d_standalone(const float* current, const float* history, int n_history, int R, int C, int P, float lam_s,
+                    float lam_t, float eps, float* value, float* grad, void* ws, size_t ws_bytes, cudaStream_t st) {
+  D2IP_CHECK_ARG(current && value && R > 0 && C > 0 && P > 0 && n_history >= 0 && (n_history == 0 || history),
+                 "tv4d: bad arguments");
+  D2IP_CHECK_ARG(ws && ws_bytes >= tv4d_ws_bytes(R, C, P), "tv4d: workspace too small");
+  const long long Q = (long long)R * C * P;
+  int* stw = reinterpret_cast<int*>(ws);
+  float* part = reinterpret_cast<float*>(reinterpret_cast<char*>(ws) + 16);
+  float* gbuf = grad ? grad : part + tv_nblocks(Q);
+  tv_setn_k<<<1, 1, 0, st>>>(stw, n_history);
+  D2IP_LAUNCH_CHECK();
+  D2IP_RET(tv_fwd_bwd(current, history, n_history > 0 ? n_history : 1, stw, R, C, P, 1.0f, lam_s, lam_t, eps, gbuf,
+                      part, 1, st));
+  tv_reduce_k<<<1, kTvThreads, 0, st>>>(part, tv_nblocks(Q), value);
+  D2IP_LAUNCH_CHECK();
+  return D2IP_OK;
+}
+
 }  // namespace d2ip

@@ -68,7 +68,7 @@ def allreduce_status(status: torch.Tensor) -> None:
         dist.all_reduce(status, op=dist.ReduceOp.MAX)
 
 
-def joint_upws(engine, iters: int, data_norm: str = "l2sq", on_step=None) -> None:
+def joint_upws(engine, iters: int, data_norm: str = "l2sq", on_step=None, graph: bool = True) -> None:
     """Data-parallel joint warm-start: per iteration grads -> all-reduce(grad, SUM)
     -> all-reduce(status, MAX) -> Adam. `engine.reset_frame()` must have been called
     (fresh optimiser). The summed per-rank gradients are the gradient of the joint
@@ -81,7 +81,7 @@ def joint_upws(engine, iters: int, data_norm: str = "l2sq", on_step=None) -> Non
                          f"got {data_norm!r}")
     status = getattr(engine, "status", None)
     for k in range(1, iters + 1):
-        engine.grads()
+        engine.grads(graph=graph)  # one CUDA-graph replay of forward + loss + backward
         allreduce_grads(engine.grad)
         if status is not None:
             allreduce_status(status)

@@ -95,6 +95,46 @@ def upload_masked_J(values: np.ndarray, perm: np.ndarray, vp: int) -> torch.Tens
     return out
 
 
+# Device copies of J keyed by the identity of the host operator (its read-only values
+# array) and the mask: standalone `upws_pretrain` / `reconstruct_frame` calls on the same
+# matrix reuse one upload (1.6 GB at cfg2) instead of re-uploading per call as the
+# reference re-casts per runner (pipeline.py:273,406,428). Entries die with the host
+# array (weakref finalizer); at most _J_CACHE_MAX operators are kept.
+_J_CACHE: "OrderedDict[tuple, tuple]" = None
+_J_CACHE_MAX = 2
+
+
+def cached_device_J(masked, perm: np.ndarray, vp: int) -> torch.Tensor:
+    global _J_CACHE
+    import hashlib
+    import weakref
+    from collections import OrderedDict
+
+    if _J_CACHE is None:
+        _J_CACHE = OrderedDict()
+    vals = masked.values
+    key = (id(vals), vals.shape, vp, hashlib.sha1(np.packbits(masked.mask).tobytes()).hexdigest())
+    ent = _J_CACHE.get(key)
+    if ent is not None and ent[0]() is vals and not vals.flags.writeable:
+        _J_CACHE.move_to_end(key)
+        return ent[1]
+    J = upload_masked_J(vals, perm, vp)
+    try:
+        ref = weakref.ref(vals)
+        weakref.finalize(vals, _J_CACHE.pop, key, None)
+    except TypeError:
+        return J
+    _J_CACHE[key] = (ref, J)
+    while len(_J_CACHE) > _J_CACHE_MAX:
+        _J_CACHE.popitem(last=False)
+    return J
+
+
+def clear_J_cache() -> None:
+    if _J_CACHE is not None:
+        _J_CACHE.clear()
+
+
 def net_fields(cfg) -> dict:
     """Engine description of a network config (d2ip_net_desc's network fields).
 
@@ -213,6 +253,12 @@ class DeviceNet:
                 self.J = torch.zeros((self.batch, self.M, self.Vp), dtype=torch.float32, device="cuda")
             self.J[b].copy_(Jd)
             self._bound = False
+
+    def set_J_cached(self, masked) -> None:
+        """Shared J from the device cache (uploaded once per host operator)."""
+        if not self.j_shared:
+            raise ValueError("the J cache serves shared-J engines")
+        self.set_J(cached_device_J(masked, self.colmap.perm, self.Vp))
 
     def set_J_device(self, J_canon: torch.Tensor, b: int | None = None) -> None:
         """J already on the GPU, [M][V] in canonical (q-ordered) mask columns."""
@@ -335,9 +381,12 @@ class DeviceNet:
         N.check(N.lib().d2ip_engine_forward(self._h, 1 if with_loss else 0, N.C.c_void_p(_stream_ptr())),
                 "engine_forward")
 
-    def grads(self) -> None:
+    def grads(self, graph: bool = False) -> None:
+        """One forward + loss + backward (gradient in `self.grad`); graph=True replays it
+        from a CUDA graph captured on first use."""
         self._bind()
-        N.check(N.lib().d2ip_engine_grads(self._h, N.C.c_void_p(_stream_ptr())), "engine_grads")
+        fn = N.lib().d2ip_engine_grads_graph if graph else N.lib().d2ip_engine_grads
+        N.check(fn(self._h, N.C.c_void_p(_stream_ptr())), "engine_grads")
 
     def adam(self) -> None:
         """Adam on the current gradient buffer (after an external all-reduce)."""

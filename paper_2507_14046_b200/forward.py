@@ -204,3 +204,29 @@ class ConductivitySequence:
 
     def frame(self, i: int) -> np.ndarray:
         return self.values[:, i - 1]
+
+
+def forward_project(matrix, dsigma) -> np.ndarray:
+    """Measurement-space projection of a conductivity-change vector
+    (`pkg/src/d2ip/forward.py:115-122`): ``matrix.values @ vec`` in float64, computed
+    on the GPU by the deterministic fp64 kernel `d2ip_project_f64`. Accepts the
+    reference's dense operator (Q columns) or the masked block (its masked columns
+    of the Q-vector)."""
+    import torch
+
+    from . import _native as N
+    from .engine import _stream_ptr, require_cuda
+
+    vec = np.asarray(dsigma, dtype=np.float64)
+    if vec.shape != (matrix.n_voxels,):
+        raise ValueError(f"conductivity vector shape {vec.shape} does not match Q={matrix.n_voxels}")
+    if isinstance(matrix, MaskedSensitivity):
+        vec = vec[matrix.columns_q()]
+    require_cuda()
+    A = torch.as_tensor(np.asarray(matrix.values), device="cuda").to(torch.float64).contiguous()
+    x = torch.as_tensor(vec, device="cuda").contiguous()
+    M, n = A.shape
+    y = torch.empty(M, dtype=torch.float64, device="cuda")
+    N.check(N.lib().d2ip_project_f64(N.C.c_void_p(A.data_ptr()), n, N.C.c_void_p(x.data_ptr()), M, n,
+                                     N.C.c_void_p(y.data_ptr()), N.C.c_void_p(_stream_ptr())), "project_f64")
+    return y.cpu().numpy()

@@ -252,9 +252,105 @@ def case_sequence_long():
     print("long sequence: final data terms", [float(out[f"trace_frame_{i}"][-1, 1]) for i in range(1, 5)])
 
 
+def case_level4():
+    """A 4-level injected net (channels 4/8/16/32 on a 16x16x16 grid, the cfg2 / cfg4
+    topology at a fixture-sized width): step-1 loss + gradients and theta after 5 Adam
+    steps, pinning the oracle / engine at L = 4 (SURVEY §7.1 restatement of
+    priornet.py:183-232). theta0 is stored by checksum (kaiming, bit-reproducible)."""
+    spec = W.small_spec(name="l4", grid=(16, 16, 16), channels=(4, 8, 16, 32), in_channels=4,
+                        rings=(0.3, 0.7), frames=1)
+    wl = W.make_workload(spec, seed=2)
+    grid = wl.grid
+    noise = sample_noise_input(grid, 2, spec.in_channels, 0.1)
+    net = GoldenNetCfg(spec.channels, spec.in_channels, seed=3, depth=4)
+    cfg = P.RunConfig(iters_warm=5, iters_first=5, iters_next=5, learning_rate=1e-3,
+                      tv_weights=TVWeights(lambda_tv=0.0), seed=2, network=net,
+                      output_map=wl.output_map, data_norm="l2sq")
+    matrix = dense_matrix(wl.matrix)
+    dv = wl.voltages.frames[0].values
+    theta0 = N.init_parameters(net)
+    runner = P._FrameOptimizer(cfg, matrix, _Noise(noise))
+    out = {"theta0_sha": theta0.checksum(), "J_sha": sha(wl.matrix.values),
+           "dv": dv, "z_sha": noise.sha256(), "output_map": np.array(wl.output_map),
+           "channels": np.array(spec.channels), "grid": np.array(grid.shape), "net_seed": 3}
+    t, d, r, g = grads_of(runner, theta0, dv, FrameHistory(), cfg)
+    out.update(l2sq_total=t, l2sq_data=d, l2sq_grads=g)
+    for k in (5,):
+        vol, mapped, th, tr = runner.optimize(theta0, dv, FrameHistory(), k, frame_label=0)
+        out[f"theta{k}"] = flat_state(th)
+        out[f"trace{k}"] = np.array([[r.iteration, r.data_term, r.total] for r in tr.records])
+    np.savez_compressed(OUT / "level4.npz", **out)
+    print("level4: params", out["l2sq_grads"].size, "step-1 data", d)
+
+
+def case_joint():
+    """cfg4's joint warm-start check (SURVEY §8(e)): the reference's `upws_pretrain`
+    with dv0 = the mean of F frames (one shared Z), 10 iterations. The joint loss
+    sum_f ||J sigma - dv_f||^2 has F times this gradient; Adam is scale-invariant
+    up to eps, so the engine's joint run must land on the same theta."""
+    spec = W.small_spec(grid=(8, 8, 8), channels=(8, 16), in_channels=4, rings=(0.5,), frames=4)
+    wl = W.make_workload(spec, seed=0)
+    grid = wl.grid
+    noise = sample_noise_input(grid, 0, 4, 0.1)
+    net = GoldenNetCfg(spec.channels, spec.in_channels, seed=1)
+    cfg = P.RunConfig(iters_warm=10, iters_first=10, iters_next=10, learning_rate=1e-3,
+                      tv_weights=TVWeights(lambda_tv=0.0), seed=0, network=net,
+                      output_map=wl.output_map, data_norm="l2sq")
+    dvs = np.stack([f.values for f in wl.voltages.frames])
+    theta0 = N.init_parameters(net)
+    state, trace = P.upws_pretrain(dense_matrix(wl.matrix), dvs.mean(0), _Noise(noise), cfg, theta_init=theta0)
+    np.savez_compressed(OUT / "joint_upws.npz", dvs=dvs, theta0=flat_state(theta0), theta10=flat_state(state),
+                        output_map=np.array(wl.output_map),
+                        trace=np.array([[r.iteration, r.data_term, r.total] for r in trace.records]))
+    print("joint: final data", trace.records[-1].data_term)
+
+
+def case_cfg1_sequence(frames: int = 4):
+    """BASELINE cfg1 budgets on the cfg1 workload: UPWS 2,000 on frame 1, then frame 1
+    (100) and a TPP chain of frames 2..`frames` (100 each), run by the reference with
+    its dense operator (all host threads: `serial=False`). The oracle with the compact
+    masked J (same algorithm, only J.sigma's fp32 summation order changed) gives the
+    natural variability band the GPU result is judged against."""
+    spec = W.CONFIGS["cfg1"]
+    wl = W.make_workload(spec, seed=0, frames=frames)
+    grid = wl.grid
+    net = GoldenNetCfg(spec.channels, spec.in_channels, seed=0)
+    P.sample_noise_input = lambda g, s: _Noise(sample_noise_input(grid, s, spec.in_channels, 0.1))
+    cfg = P.RunConfig(iters_warm=2000, iters_first=100, iters_next=100, learning_rate=1e-3,
+                      tv_weights=TVWeights(lambda_tv=0.0), seed=0, network=net,
+                      output_map=wl.output_map, data_norm="l2sq", serial=False)
+    torch.set_num_threads(max(1, __import__("os").cpu_count()))
+    matrix = dense_matrix(wl.matrix)
+    volts = VoltageSequence([VoltageFrame(f.values, f.frame_index) for f in wl.voltages.frames])
+    res = P.reconstruct_sequence(matrix, volts, cfg, grid)
+    out = {"values": res.sequence.values.astype(np.float32), "output_map": np.array(wl.output_map),
+           "iterations": np.array([f.iterations for f in res.frame_records]),
+           "theta0": flat_state(res.states["init"]), "J_sha": sha(wl.matrix.values)}
+    for key, tr in res.traces.items():
+        out[f"trace_{key}"] = np.array([r.data_term for r in tr.records], dtype=np.float32)
+    from oracle import oracle_reconstruct_sequence
+    band = oracle_reconstruct_sequence(spec.channels, spec.in_channels,
+                                       sample_noise_input(grid, 0, spec.in_channels, 0.1).values,
+                                       wl.matrix.values, wl.matrix.columns_q(),
+                                       [f.values for f in wl.voltages.frames], out["theta0"], wl.output_map,
+                                       2000, 100, 100, 1e-3)
+    out["band_values"] = band["columns"].astype(np.float32)
+    for key, tr in band["traces"].items():
+        out[f"band_trace_{key}"] = np.array([r[2] for r in tr], dtype=np.float32)
+    np.savez_compressed(OUT / "seq_cfg1.npz", **out)
+    print("cfg1 sequence: final data", [float(out[f"trace_frame_{i}"][-1]) for i in range(1, frames + 1)],
+          "band", [float(out[f"band_trace_frame_{i}"][-1]) for i in range(1, frames + 1)])
+
+
 if __name__ == "__main__":
     torch.set_num_threads(1)
-    which = sys.argv[1:] or ["cfg0", "sequence", "long"]
+    which = sys.argv[1:] or ["cfg0", "sequence", "long", "level4", "joint", "cfg1seq"]
+    if "level4" in which:
+        case_level4()
+    if "joint" in which:
+        case_joint()
+    if "cfg1seq" in which:
+        case_cfg1_sequence()
     if "cfg0" in which:
         case_cfg0()
     if "sequence" in which:

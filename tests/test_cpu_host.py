@@ -175,3 +175,23 @@ def test_reference_network_engine_fields():
     assert param_schema(NetworkConfig())[0].name == "stem.0.weight"
     names = [n for n, _ in N.NetDesc._fields_]
     assert names[-4:] == ["arch", "depthwise", "n_dil", "dil"]
+
+
+# names the reference exports for the DIP path (pkg/src/d2ip/__init__.py:15-48) plus the
+# priornet / pipeline functions SURVEY §8(b) lists (priornet.py:285-317, pipeline.py:341-391)
+REFERENCE_DIP_NAMES = [
+    "GridGeometry", "vectorize", "devectorize",
+    "SensitivityMatrix", "VoltageFrame", "VoltageSequence", "assemble_sensitivity", "forward_project",
+    "normalize_sensitivity",
+    "FrameHistory", "TVWeights", "decay_weight", "spatial_tv", "temporal_tv", "tv4d",
+    "NetworkConfig", "NoiseInput", "ParameterState", "init_parameters", "sample_noise_input",
+    "build_model", "extract_parameters", "load_parameters", "forward_volume", "save_checkpoint", "load_checkpoint",
+    "ReconstructionResult", "RunConfig", "ablation_mode", "reconstruct_frame", "reconstruct_sequence",
+    "upws_pretrain", "loss", "predict_measurements",
+]
+
+
+def test_reference_dip_path_names_exported():
+    import paper_2507_14046_b200 as D
+    missing = [n for n in REFERENCE_DIP_NAMES if not callable(getattr(D, n, None))]
+    assert not missing, missing

@@ -38,7 +38,7 @@ class LstsqEngine:
         self.lr = lr
         self.status = torch.zeros((1, 4), dtype=torch.int32)  # [step, bad iteration, n_hist, -]
 
-    def grads(self):
+    def grads(self, graph=False):
         r = sum(self.A @ self.theta - d for d in self.frames) if self.frames else torch.zeros(self.A.shape[0])
         self.grad.copy_(2 * self.A.T @ r)
         self.status[0, 0] += 1

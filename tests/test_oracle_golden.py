@@ -142,3 +142,54 @@ def test_oracle_tv_sequence_matches_reference():
     np.testing.assert_array_equal(res["columns"], g["tv_values"])
     for key in ("warm", "frame_2", "frame_3"):
         np.testing.assert_array_equal([t[4] for t in res["traces"][key]], g[f"tvtrace_{key}"][:, 2])
+
+
+# ---------------------------------------------------------------------------
+# 4-level net (cfg2 / cfg4 topology) and the joint warm-start, pinned bit for bit
+
+
+def _l4():
+    g = np.load(GOLDEN / "level4.npz")
+    spec = W.small_spec(name="l4", grid=(16, 16, 16), channels=tuple(int(c) for c in g["channels"]),
+                        in_channels=4, rings=(0.3, 0.7), frames=1)
+    wl = W.make_workload(spec, seed=2)
+    noise = sample_noise_input(wl.grid, 2, spec.in_channels, 0.1)
+    return g, spec, wl, noise
+
+
+def test_oracle_level4_matches_reference():
+    torch.set_num_threads(1)
+    g, spec, wl, noise = _l4()
+    assert sha(wl.matrix.values) == str(g["J_sha"]) and noise.sha256() == str(g["z_sha"])
+    net = build_oracle_net(spec.channels, spec.in_channels, seed=int(g["net_seed"]))
+    theta0 = torch.cat([v.reshape(-1) for v in net.state_dict().values()]).numpy()
+    from paper_2507_14046_b200.priornet import kaiming_flat, param_schema, state_from_flat
+    cfgn = spec.network(seed=int(g["net_seed"]))
+    np.testing.assert_array_equal(kaiming_flat(cfgn).numpy(), theta0)
+    assert state_from_flat(torch.from_numpy(theta0), param_schema(cfgn)).checksum() == str(g["theta0_sha"])
+    J = wl.matrix.dense().values
+    r = OracleFrameOptimizer(spec.channels, spec.in_channels, noise.values, J, np.arange(J.shape[1]),
+                             tuple(g["output_map"]), 1e-3)
+    r.load(theta0)
+    _, data, _, grads, _ = r.grads(g["dv"])
+    assert data == float(g["l2sq_data"])
+    np.testing.assert_array_equal(torch.cat([v.reshape(-1) for v in grads.values()]).numpy(), g["l2sq_grads"])
+    r.load(theta0)
+    r.optimize(g["dv"], [], 5, 0)
+    np.testing.assert_array_equal(r.flat().numpy(), g["theta5"])
+
+
+def test_oracle_joint_mean_frame_upws_matches_reference():
+    """The reference's upws_pretrain(dv0 = mean of the frames) is reproduced bit for bit."""
+    torch.set_num_threads(1)
+    g = np.load(GOLDEN / "joint_upws.npz")
+    spec = W.small_spec(grid=(8, 8, 8), channels=(8, 16), in_channels=4, rings=(0.5,), frames=4)
+    wl = W.make_workload(spec, seed=0)
+    np.testing.assert_array_equal(np.stack([f.values for f in wl.voltages.frames]), g["dvs"])
+    noise = sample_noise_input(wl.grid, 0, 4, 0.1)
+    J = wl.matrix.dense().values
+    r = OracleFrameOptimizer(spec.channels, spec.in_channels, noise.values, J, np.arange(J.shape[1]),
+                             tuple(g["output_map"]), 1e-3)
+    r.load(g["theta0"])
+    r.optimize(g["dvs"].mean(0), [], 10, 0)
+    np.testing.assert_array_equal(r.flat().numpy(), g["theta10"])
