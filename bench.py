@@ -375,7 +375,7 @@ def run_gpu(args):
         "metric": "DIP iters/sec", "value": round(its, 2), "unit": "it/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(1e3 * t_dev / args.steps, 4), "higher_is_better": True,
         "scaling": "weak", "vs_baseline": None, "dtype": ("f32 (TF32-class convs: 3xbf16 hi/lo operand splits on kind::f16, fp32 accumulate)"
-                  if os.environ.get("D2IP_TF32_BF3", "1") != "0" else "f32 (3xTF32 conv operands)")
+                  if os.environ.get("D2IP_TF32_BF3", "0") != "0" else "f32 (3xTF32 conv operands)")
                  if (args.precision or spec.precision) == "tf32" else
                  ("f32 (bf16 conv operands, fp32 accumulate)" if (args.precision or spec.precision) == "bf16" else "f32"),
         "data": "synthetic (seeded BASELINE cfg generator; random-init weights)",
@@ -465,7 +465,7 @@ def conv_probe(L, N, C, st, pk, pk_kind, flush, t_flush, cin=48, cout=16, dims=(
     peak = pk.get("bf16_tflops", 1665.3)  # MEASURED_PEAKS.json: dense bf16 (the operand type the kernel runs)
     src = NCU_CONV.get(workload)
     traffic = ncu_traffic(src) if src else None
-    b3 = os.environ.get("D2IP_TF32_BF3", "1") != "0"
+    b3 = os.environ.get("D2IP_TF32_BF3", "0") != "0"
     # shape bound: an M=128 x N=16 MMA reads 4 KB (A) + 0.5 KB (B) of shared memory in ~39 cycles
     # (tools/umma_chains.cu): kind::f16 does 2*128*16*16 flop in it (of 8,192 flop/cycle/SM at
     # the 2,209 TFLOP/s probe peak), kind::tf32 half that; 3x MMAs per fp32-accurate product
