@@ -189,6 +189,7 @@ def run_gpu(args):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     spec = W.CONFIGS[args.workload]
     seed = rank
+    joint = None
     if spec.sequences > 1:
         # cfg3: this rank's share of the independent sequences, batched in lockstep
         from paper_2507_14046_b200.distributed import shard
@@ -206,22 +207,33 @@ def run_gpu(args):
             dn.set_theta(kaiming_flat(net, seed=s + 1), b=b)
             dn.set_dv(wl.voltages.frames[0].values, b=b)
         units_per_step = len(mine)
-    elif spec.n_measurements * int(np.prod(spec.grid)) > 512 * 1024 * 1024:
-        # cfg4: J (5.4 GB) synthesised on the GPU, never on the host
-        J_dev, mask, dv_dev, omap = W.device_frame(spec, seed)
+    elif spec.joint_frames:
+        # cfg4: the joint warm-start step -- one network over `joint_frames` frames, the
+        # frames sharded over the ranks (n_rhs per rank), J (5.4 GB) synthesised on the GPU
+        from paper_2507_14046_b200.distributed import shard
+        mine = list(shard(spec.joint_frames, ws, rank))
+        J_dev, mask, dvs, omap = W.device_frames(spec, 0, spec.joint_frames)
         wl = None
-        net = spec.network(seed=seed + 1)
+        net = spec.network(seed=1)
         grid = spec.geometry()
-        noise = sample_noise_input(grid, seed, spec.in_channels, 0.1)
-        dn = DeviceNet(net, grid.shape, J_dev.shape[0], mask, data_norm="l2sq", output_map=omap,
+        noise = sample_noise_input(grid, 0, spec.in_channels, 0.1)
+        dn = DeviceNet(net, grid.shape, J_dev.shape[0], mask, data_norm="l2sq", output_map=omap, n_rhs=len(mine),
                        lr=spec.learning_rate, precision=args.precision or spec.precision,
                        max_iters=args.warmup + args.steps + 8)
         dn.set_noise(noise.values)
         dn.set_J_device(J_dev)
         del J_dev
         dn.set_theta(kaiming_flat(net))
-        dn.dv[0, 0].copy_(dv_dev)
+        dn.dv[0].copy_(dvs[mine])
+        # the TPP phase's single-frame step on the same device J (rank 0)
+        tpp = DeviceNet(net, grid.shape, dn.M, mask, data_norm="l2sq", output_map=omap, lr=spec.learning_rate,
+                        precision=args.precision or spec.precision, max_iters=args.warmup + args.steps + 8)
+        tpp.set_noise(noise.values)
+        tpp.set_J(dn.J)
+        tpp.set_theta(kaiming_flat(net))
+        tpp.dv[0, 0].copy_(dvs[0])
         units_per_step = 1
+        joint = {"frames": spec.joint_frames, "frames_this_rank": len(mine), "tpp_net": tpp}
     else:
         # cfg0-2: the seeded host workload (cfg2: 1.6 GB J, 100 frames), the same arrays
         # the e2e call and the CPU arm consume
@@ -244,11 +256,22 @@ def run_gpu(args):
     dn.reset_frame()
     torch.cuda.synchronize()
     flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device="cuda")
+    if joint is not None and ws > 1:
+        from paper_2507_14046_b200.distributed import allreduce_grads, allreduce_status
+
+        def step():  # grads graph -> NCCL all-reduce (grad SUM, status MAX) -> Adam
+            dn.grads(graph=True)
+            allreduce_grads(dn.grad)
+            allreduce_status(dn.status)
+            dn.adam()
+    else:
+        def step():
+            dn.run(1)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
     clk = Clocks(local).__enter__()  # sampler started before the warm-up so the timed region is covered
     try:
         for _ in range(args.warmup):
-            dn.run(1)
+            step()
         torch.cuda.synchronize()
         if ws > 1:
             dist.barrier()
@@ -257,7 +280,7 @@ def run_gpu(args):
         for i in range(args.steps):
             flush.zero_()  # L2 flush between timed iterations (outside the events)
             ev[i][0].record()
-            dn.run(1)
+            step()
             ev[i][1].record()
         torch.cuda.synchronize()
         clk.mark("timed_end")
@@ -272,16 +295,33 @@ def run_gpu(args):
     status = dn.status_host()
     assert status[0, 1] == 0, "non-finite loss during the benchmark"
     launches = dn.launches_per_iter()
-    its = ws * units_per_step * args.steps / t_dev
+    # replicas / sharded sequences: every rank's units count; the joint warm-start is ONE
+    # job split over the ranks (strong scaling): its iterations count once
+    its = (1 if joint is not None else ws) * units_per_step * args.steps / t_dev
 
     # --- no-flush steady state (informational): J may stay L2-resident
     torch.cuda.synchronize()
     s0, s1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     s0.record()
-    dn.run(args.steps)
+    for _ in range(args.steps):
+        step()
     s1.record()
     torch.cuda.synchronize()
     its_hot = units_per_step * args.steps / (s0.elapsed_time(s1) / 1e3)
+    tpp_its = None
+    if joint is not None:  # the TPP phase (single frame, one GPU): graph-replayed steps, L2 flushed
+        tn = joint.pop("tpp_net")
+        tn.reset_frame()
+        tn.run(args.warmup)
+        tev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        for i in range(args.steps):
+            flush.zero_()
+            tev[i][0].record()
+            tn.run(1)
+            tev[i][1].record()
+        torch.cuda.synchronize()
+        tpp_its = args.steps / (sum(a.elapsed_time(b) for a, b in tev) / 1e3)
+        tn.close()
 
     # --- roofline of the dominant kernels, timed live on this stream
     pk, pk_kind = peaks()
@@ -361,6 +401,12 @@ def run_gpu(args):
 
     # --- e2e through the public API (rank-local, one full sequence)
     e2e = None
+    dims = (dn.M, dn.V)
+    if not args.skip_e2e and joint is not None and ws == 1:
+        dn.close()
+        del dn
+        torch.cuda.empty_cache()
+        e2e = run_e2e_joint(spec, args)
     if not args.skip_e2e and units_per_step == 1 and wl is not None and args.net == "config":
         e2e = run_e2e(spec, wl, args, ws)
         if ws > 1:  # replicas: all ranks' iterations over the slowest rank's wall time
@@ -374,15 +420,17 @@ def run_gpu(args):
     out = {
         "metric": "DIP iters/sec", "value": round(its, 2), "unit": "it/s", "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": round(1e3 * t_dev / args.steps, 4), "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": ("f32 (TF32-class convs: 3xbf16 hi/lo operand splits on kind::f16, fp32 accumulate)"
+        "scaling": "strong" if joint is not None else "weak", "vs_baseline": None,
+        "dtype": ("f32 (TF32-class convs: 3xbf16 hi/lo operand splits on kind::f16, fp32 accumulate)"
                   if os.environ.get("D2IP_TF32_BF3", "0") != "0" else "f32 (3xTF32 conv operands)")
                  if (args.precision or spec.precision) == "tf32" else
-                 ("f32 (bf16 conv operands, fp32 accumulate)" if (args.precision or spec.precision) == "bf16" else "f32"),
+                 ("f32 (bf16 conv operands, fp32 accumulate; forwards on 3xbf16 hi/lo operands)"
+                  if (args.precision or spec.precision) == "bf16" else "f32"),
         "data": "synthetic (seeded BASELINE cfg generator; random-init weights)",
         "config": {"workload": args.workload + ("" if args.net == "config" else
                                                 f"+FastResUNet3D(b={args.base_channels},{'dense' if args.dense else 'depthwise'})"),
                    "grid": list(spec.grid), "channels": list(spec.channels),
-                   "C_z": spec.in_channels, "M": dn.M, "V": dn.V, "n_params": units["n_params"],
+                   "C_z": spec.in_channels, "M": dims[0], "V": dims[1], "n_params": units["n_params"],
                    "precision": args.precision or spec.precision,
                    "parallelism": f"replicas x{ws}" if ws > 1 else "single GPU",
                    "l2": "flushed between timed iterations (256 MB write)"},
@@ -400,6 +448,14 @@ def run_gpu(args):
         "data_setup": "host-generated seeded workload (J, 100 frames of dv), uploaded once before timing"
                       if wl is not None else "J and dv synthesised on the GPU (torch RNG, seeded)",
     }
+    if joint is not None:
+        out["metric"] = "DIP iters/sec (joint warm-start: one iteration = all joint frames)"
+        out["config"]["joint_frames"] = joint["frames"]
+        out["config"]["parallelism"] = (f"joint warm-start, {joint['frames']} frames sharded over {ws} GPU(s) "
+                                        f"({joint['frames_this_rank']} per rank, NCCL all-reduce of the gradient)"
+                                        if ws > 1 else f"joint warm-start, {joint['frames']} frames as right-hand sides")
+        out["tpp_its_single_gpu"] = round(tpp_its, 2)
+        out["frames_per_sec"] = round(spec.frames / (spec.iters_warm / its + spec.frames * spec.iters_next / tpp_its), 4)
     if units_per_step > 1:
         out["config"]["sequences_per_gpu"] = units_per_step
         out["config"]["parallelism"] = f"{spec.sequences} sequences sharded over {ws} GPU(s), batched in lockstep"
@@ -581,6 +637,40 @@ def run_e2e(spec, wl, args, ws):
             "frames_per_sec": round(frames / secs, 4)}
 
 
+def run_e2e_joint(spec, args):
+    """cfg4 end to end through `reconstruct_sequence_joint` on host inputs: the joint warm
+    start over `joint_frames` frames, then frame 1 + the TPP chain (bounded to
+    --e2e-frames-joint frames), uploads / read-backs inside the timed region."""
+    import torch
+
+    from paper_2507_14046_b200 import reconstruct_sequence_joint
+    from paper_2507_14046_b200 import workloads as W
+    from paper_2507_14046_b200.forward import MaskedSensitivity, VoltageSequence
+
+    frames = max(spec.joint_frames, min(spec.frames, args.e2e_frames_joint))
+    wl = W.make_workload(spec, seed=0, frames=frames)
+    cfg = W.run_config_for(spec, wl.output_map, seed=0, precision=args.precision or spec.precision)
+    matrix = MaskedSensitivity(np.array(wl.matrix.values), wl.matrix.mask)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    res = reconstruct_sequence_joint(matrix, VoltageSequence(wl.voltages.frames), cfg, wl.grid,
+                                     joint_frames=spec.joint_frames)
+    torch.cuda.synchronize()
+    secs = time.perf_counter() - t0
+    iters = cfg.iters_warm + sum(f.iterations for f in res.frame_records)
+    nparam = res.states["init"].flat().numel()
+    h2d = matrix.values.nbytes + 4 * np.prod(wl.grid.shape) * spec.in_channels + (frames + spec.joint_frames) * 4 * \
+        wl.matrix.n_measurements + 4 * nparam
+    d2h = (frames + 1) * (4 * np.prod(wl.grid.shape) + 4 * nparam + 16) + 4 * iters * 4
+    return {"value": round(iters / secs, 2), "unit": "it/s", "h2d_bytes_per_step": int(h2d / iters),
+            "d2h_bytes_per_step": int(d2h / iters), "call": "reconstruct_sequence_joint",
+            "iterations": int(iters), "frames": frames, "seconds": round(secs, 3),
+            "frames_per_sec": round(frames / secs, 4),
+            "note": f"joint warm-start ({cfg.iters_warm} iterations over {spec.joint_frames} frames) + frame 1 and "
+                    f"a TPP chain of {frames - 1} frames ({cfg.iters_next} each): the 100-frame chain bounded to "
+                    f"{frames} frames"}
+
+
 def _oracle_runner(spec, wl):
     from oracle import OracleFrameOptimizer
     from oracle.resunet import kaiming_reset
@@ -720,6 +810,7 @@ def main():
     ap.add_argument("--ref-seconds", type=float, default=90.0, help="cap on the reference arm's timed CPU work")
     ap.add_argument("--e2e-frames", type=int, default=100)
     ap.add_argument("--e2e-warm", type=int, default=2000)
+    ap.add_argument("--e2e-frames-joint", type=int, default=20)
     ap.add_argument("--launch-selftest", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:

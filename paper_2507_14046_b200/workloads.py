@@ -200,6 +200,26 @@ def device_frame(spec: WorkloadSpec, seed: int = 0, t: int = 0):
     return J, mask, dv, (lo, hi)
 
 
+def device_frames(spec: WorkloadSpec, seed: int = 0, T: int = 1):
+    """T frames of the large configs on the GPU (cfg4's joint warm-start): J from
+    `jacobian_device`, dv_t = J sigma_true(t) + 1 % RMS noise, t = 0..T-1; output_map over
+    the T frames. Returns (J [M][V] cuda, mask, dv [T][M] cuda fp32, output_map)."""
+    import torch
+
+    J, mask = jacobian_device(spec, seed)
+    truths = [sigma_true(spec, t) for t in range(T)]
+    cols = torch.from_numpy(np.stack([vectorize(tr)[np.flatnonzero(vectorize(mask))] for tr in truths],
+                                     axis=1)).cuda().float()
+    clean = (J @ cols).T.contiguous()  # [T][M]
+    g = torch.Generator(device="cuda").manual_seed(int(seed) + 7919)
+    rms = clean.pow(2).mean(dim=1, keepdim=True).sqrt()
+    dv = clean + torch.randn(clean.shape, generator=g, device="cuda") * (spec.noise_rel * rms)
+    lo, hi = float(min(t.min() for t in truths)), float(max(t.max() for t in truths))
+    if lo == hi:
+        lo, hi = lo - 0.5, hi + 0.5
+    return J, mask, dv, (lo, hi)
+
+
 def _ellipsoid(grid: GridGeometry, centre, axes) -> np.ndarray:
     ys, xs, zs = grid.axis_centers()
     u = ((xs[None, :, None] - centre[0]) / axes[0]) ** 2
