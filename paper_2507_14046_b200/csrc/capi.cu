@@ -69,7 +69,13 @@ int conv_wgrad(d2ip_act x, d2ip_act gy, int ks, int stride, float* gw, long long
   // the data-gradient chain it runs beside. Large grids only.
   const long long vg = (long long)gy.d * gy.h * gy.w;
   const bool b3_wins = vg >= bf3_min;
-  if (precision == D2IP_PREC_TF32 && g_wgrad_variant == 1 && tf32_bf3_enabled() && b3_wins &&
+  // (independent of the convolutions' D2IP_TF32_BF3: the weight gradients of large grids keep
+  // 3xbf16 unless D2IP_WGRAD_BF3=0; parity: tests/test_gpu_engine.py full-grid cfg2 case)
+  static const bool wg_b3 = [] {
+    const char* v = getenv("D2IP_WGRAD_BF3");
+    return !v || atoi(v) != 0;
+  }();
+  if (precision == D2IP_PREC_TF32 && g_wgrad_variant == 1 && wg_b3 && b3_wins &&
       wgrad_bf_supported(x, gy, ks, stride, true)) {
     set_variant("wgrad_tcgen05_bf16x3");
     return wgrad_bf(x, gy, ks, gw, gwbs, ws, ws_bytes, batch, st, stride, true);

@@ -227,6 +227,107 @@ __device__ __forceinline__ void tc_epilogue(const TcConv& a, uint32_t tmem, int 
   }
 }
 
+// One voxel row's 8 output channels n .. n + 7 (a split-K partial or the result with bias /
+// accumulate), the stride-1 store path of tc_epilogue.
+__device__ __forceinline__ void tc_store8(const TcConv& a, int b, int ks, int v, int n, const float* vals,
+                                          bool zero, const float* bias) {
+  if (v < 0) return;
+  if (a.kspl > 1) {
+    float* pp = a.part + (((long long)b * a.kspl + ks) * a.vout + v) * a.N;
+#pragma unroll
+    for (int j = 0; j < 8; ++j)
+      if (n + j < a.N) pp[n + j] = zero ? 0.f : vals[j];
+    return;
+  }
+  float* yp = a.y.ptr + b * a.y.bstride + (long long)v * a.y.cstride;
+  if (a.vec && n + 8 <= a.N) {
+    float4* y4 = reinterpret_cast<float4*>(yp + n);
+#pragma unroll
+    for (int h = 0; h < 2; ++h) {
+      float4 o = make_float4(zero ? 0.f : vals[4 * h], zero ? 0.f : vals[4 * h + 1], zero ? 0.f : vals[4 * h + 2],
+                             zero ? 0.f : vals[4 * h + 3]);
+      if (bias) {
+        const float* bb = bias + n + 4 * h;
+        o.x += __ldg(bb); o.y += __ldg(bb + 1); o.z += __ldg(bb + 2); o.w += __ldg(bb + 3);
+      }
+      if (a.accumulate) {
+        const float4 yo = y4[h];
+        o.x += yo.x; o.y += yo.y; o.z += yo.z; o.w += yo.w;
+      }
+      y4[h] = o;
+    }
+    return;
+  }
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    if (n + j < a.N) {
+      float o = (zero ? 0.f : vals[j]) + (bias ? __ldg(bias + n + j) : 0.f);
+      if (a.accumulate) o += yp[n + j];
+      yp[n + j] = o;
+    }
+  }
+}
+
+// Epilogue of the kw-folded stride-1 kernel (MODE 4): the accumulator of a sub-tile holds
+// three column blocks P_kw[i][n] = sum over kd, kh, k of window row (i + kh Sw) x W[kd][kh][kw];
+// output row r (0..125) = P_0[r] + P_1[r + 1] + P_2[r + 2]. Rows r + 1 / r + 2 live in other
+// TMEM lanes (other threads, other warps at quadrant edges), so every thread first parks its
+// P_1 / P_2 columns in shared memory (the idle stage buffers), then sums. 256 epilogue threads
+// (warps 1-8) synchronise on named barrier 1.
+template <int T>
+__device__ __forceinline__ void tc_epilogue_kwf(const TcConv& a, uint32_t tmem, int b, int n0, int u0, int ks, int S,
+                                                int warp, int lane, float* xch) {
+  constexpr int RS = kTcRows - 2;
+  const int row = (warp & 3) * 32 + lane;
+  const int Ns = a.Ns;
+  const int chalf = Ns / 2, cbeg = ((warp - 1) >> 2) * chalf, cend = cbeg + chalf;
+  const int xs = 2 * Ns + 4;  // exchange row stride (floats): float4 rows, 4-bank skew between rows
+  const uint32_t trow = tmem + ((uint32_t)((warp & 3) * 32) << 16);
+  const float* bias = a.bias ? a.bias + b * a.bbs : nullptr;
+  for (int tt = 0; tt < T; ++tt) {
+    const uint32_t tcol = trow + (uint32_t)(tt * 3 * Ns);
+    for (int c0 = cbeg; c0 < cend; c0 += 8) {
+      float v1[8], v2[8];
+      tc::tmem_ld8(tcol + Ns + c0, v1);
+      tc::tmem_ld8(tcol + 2 * Ns + c0, v2);
+      float4* d1 = reinterpret_cast<float4*>(xch + row * xs + c0);
+      float4* d2 = reinterpret_cast<float4*>(xch + row * xs + Ns + c0);
+      d1[0] = make_float4(v1[0], v1[1], v1[2], v1[3]);
+      d1[1] = make_float4(v1[4], v1[5], v1[6], v1[7]);
+      d2[0] = make_float4(v2[0], v2[1], v2[2], v2[3]);
+      d2[1] = make_float4(v2[4], v2[5], v2[6], v2[7]);
+    }
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+    // rows 126 / 127 belong to the next sub-tile: they load (tcgen05.ld is warp-collective,
+    // .sync.aligned -- every lane must execute it) but store nothing
+    int v = -1;
+    if (row < RS) {
+      const int u = u0 + tt * RS + row;
+      const int dp = u / a.Sh, rem = u - dp * a.Sh;
+      const int hp = rem / a.Sw, wp = rem - hp * a.Sw;
+      if (dp >= 1 && dp <= a.gd && hp >= 1 && hp <= a.gh && wp >= 1 && wp <= a.gw)
+        v = ((dp - 1) * a.gh + (hp - 1)) * a.gw + (wp - 1);
+    }
+    const int rn = row < RS ? row : RS - 1;  // (in-bounds exchange reads for the idle rows)
+    for (int c0 = cbeg; c0 < cend; c0 += 8) {
+      float vals[8];
+      tc::tmem_ld8(tcol + c0, vals);
+      const float4* p1 = reinterpret_cast<const float4*>(xch + (rn + 1) * xs + c0);
+      const float4* p2 = reinterpret_cast<const float4*>(xch + (rn + 2) * xs + Ns + c0);
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const float4 q1 = p1[h], q2 = p2[h];
+        vals[4 * h] += q1.x + q2.x;
+        vals[4 * h + 1] += q1.y + q2.y;
+        vals[4 * h + 2] += q1.z + q2.z;
+        vals[4 * h + 3] += q1.w + q2.w;
+      }
+      tc_store8(a, b, ks, v, n0 + c0, vals, S <= 0, bias);
+    }
+    asm volatile("bar.sync 1, 256;" ::: "memory");
+  }
+}
+
 // NKC: 16-byte channel chunks per row and stage (CB / 4 for tf32, CB / 8 for
 // bf16; compile-time, so the fill loops need no integer division).
 // PG: producer groups (1: all eight producer warps fill each stage; 2: two
@@ -246,12 +347,14 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
   const int b = blockIdx.z;
   const int ks = blockIdx.y % a.kspl;
   const int n0 = (blockIdx.y / a.kspl) * a.Ns;  // first output channel of this CTA's slice
-  const int u0 = a.u_first + blockIdx.x * T * kTcRows;
   const int Ns = a.Ns, WR = a.WR, WRp = a.WRp;
   constexpr bool PW = MODE == 3;  // 1^3: one tap, window = the tile rows
-  constexpr int nt = PW ? 1 : MODE ? 2 : 3, t0 = MODE == 2 ? 1 : 0, ntap = nt * nt;
+  constexpr bool KWF = MODE == 4;  // stride 1, the three kw taps folded into N (3 column blocks)
+  constexpr int RS = KWF ? kTcRows - 2 : kTcRows;  // output rows per 128-row sub-tile
+  constexpr int nt = PW ? 1 : (MODE == 1 || MODE == 2) ? 2 : 3, t0 = MODE == 2 ? 1 : 0, ntap = nt * nt;
   // (kh, kw) of the q-th live tap as a 3x3 index: nt = 3 -> q; nt = 2 -> the 2x2 block at (t0, t0)
   auto tap9 = [&](int q) { return nt == 3 ? q : (t0 + (q >> 1)) * 3 + (t0 + (q & 1)); };
+  const int u0 = a.u_first + blockIdx.x * T * RS;
   const uint32_t Ab = (uint32_t)NKC * WRp * 16, Bb = (uint32_t)ntap * NKC * Ns * 16;
   const uint32_t Sb = NH * (Ab + Bb);
   // layout: 2 stages of [A hi][A lo][B hi][B lo] (bf16: [A][B]), row map, barriers full[2] empty[2] done, TMEM slot
@@ -312,13 +415,41 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
       // start-address field (smem addresses < 256 KB never carry out of it)
       const uint32_t sbase = tc::smem_u32(smem);
       const uint64_t dAhi = tc::make_desc(sbase, WRp * 16, 128), dAlo = dAhi + (Ab >> 4);
-      const uint64_t dBhi = tc::make_desc(sbase + NH * Ab, Ns * 16, 128), dBlo = dBhi + (Bb >> 4);
+      const uint64_t dBhi = tc::make_desc(sbase + NH * Ab, (KWF ? 3 : 1) * Ns * 16, 128), dBlo = dBhi + (Bb >> 4);
       for (int s = 0; s < S; ++s) {
         const int slot = s % NST;
         tc::mbar_wait(&full[slot], (uint32_t)((s / NST) & 1));
         tc::fence_after();
         if (BF) tc::fence_proxy_async();
         const uint64_t boff = (uint64_t)slot * (Sb >> 4);
+        if (KWF) {
+          // one N = 3 Ns MMA per (kh, K step): B = the kh row's three kw taps side by side
+          for (int kh = 0; kh < 3; ++kh) {
+#pragma unroll
+            for (int j = 0; j < NKC / 2; ++j) {
+              const uint64_t bo = boff + (uint64_t)((kh * NKC + 2 * j) * 3 * Ns);
+              const uint32_t first = (s | kh | j) ? 1u : 0u;
+#pragma unroll
+              for (int tt = 0; tt < T; ++tt) {
+                const uint64_t ao = boff + (uint64_t)(2 * j * WRp + kh * a.Sw + tt * RS);
+                const uint32_t d = tmem + (uint32_t)(tt * 3 * Ns);
+                if (B3) {
+                  tc::mma_f16(d, dAlo + ao, dBhi + bo, a.idesc, first);
+                  tc::mma_f16(d, dAhi + ao, dBlo + bo, a.idesc, 1u);
+                  tc::mma_f16(d, dAhi + ao, dBhi + bo, a.idesc, 1u);
+                } else if (BF) {
+                  tc::mma_f16(d, dAhi + ao, dBhi + bo, a.idesc, first);
+                } else {
+                  tc::mma_tf32(d, dAlo + ao, dBhi + bo, a.idesc, first);
+                  tc::mma_tf32(d, dAhi + ao, dBlo + bo, a.idesc, 1u);
+                  tc::mma_tf32(d, dAhi + ao, dBhi + bo, a.idesc, 1u);
+                }
+              }
+            }
+          }
+          tc::commit(&empty[slot]);
+          continue;
+        }
         for (int tq = 0; tq < ntap; ++tq) {
           const int t9 = tap9(tq);
           const int rowoff = PW ? 0 : (t9 >= 6 ? 2 : t9 >= 3 ? 1 : 0) * a.Sw + (t9 % 3);
@@ -457,7 +588,9 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
         const int tq = q / NKC, kcl = q % NKC;
         const int t9 = PW ? 0 : tap9(tq);
         const float* src = wk + ((long long)t9 * kc_all + kcl) * a.Np * 4;
-        uint8_t* dst = Bt + (size_t)q * Ns * 16;
+        // KWF: [kh][chunk][kw][Ns] -- the three kw taps of a K chunk are one N = 3 Ns run
+        uint8_t* dst = KWF ? Bt + ((size_t)((t9 / 3) * NKC + kcl) * 3 * Ns + (t9 % 3) * Ns) * 16
+                           : Bt + (size_t)q * Ns * 16;
         for (int n = lane; n < Ns; n += 32) {
           tc::cp_async16(dst + n * 16, src + n * 4, 16u);
           if (NH == 2) tc::cp_async16(dst + Bb + n * 16, src + a.wlo + n * 4, 16u);
@@ -493,7 +626,10 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
       tc::mbar_wait(done, 0);
       tc::fence_after();
     }
-    tc_epilogue<T, MODE>(a, tmem, b, n0, u0, ks, S, warp, lane);
+    if (KWF)
+      tc_epilogue_kwf<T>(a, tmem, b, n0, u0, ks, S, warp, lane, reinterpret_cast<float*>(smem));
+    else
+      tc_epilogue<T, MODE>(a, tmem, b, n0, u0, ks, S, warp, lane);
   }
   tc::fence_before();
   __syncthreads();
@@ -519,9 +655,12 @@ __global__ void __launch_bounds__(kTcpThreads) conv_tcp_k(TcConv a) {
   const int n0 = (blockIdx.y / a.kspl) * a.Ns;  // first output channel of this CTA's slice
   const int Ns = a.Ns, WR = a.WR, WRp = a.WRp;
   constexpr bool PW = MODE == 3;  // 1^3: one tap, window = the tile rows
-  constexpr int nt = PW ? 1 : MODE ? 2 : 3, t0 = MODE == 2 ? 1 : 0, ntap = nt * nt;
+  constexpr bool KWF = MODE == 4;  // stride 1, the three kw taps folded into N (3 column blocks)
+  constexpr int RS = KWF ? kTcRows - 2 : kTcRows;  // output rows per 128-row sub-tile
+  constexpr int nt = PW ? 1 : (MODE == 1 || MODE == 2) ? 2 : 3, t0 = MODE == 2 ? 1 : 0, ntap = nt * nt;
   // (kh, kw) of the q-th live tap as a 3x3 index: nt = 3 -> q; nt = 2 -> the 2x2 block at (t0, t0)
   auto tap9 = [&](int q) { return nt == 3 ? q : (t0 + (q >> 1)) * 3 + (t0 + (q & 1)); };
+  const int u0 = a.u_first + blockIdx.x * T * RS;
   const uint32_t Ab = (uint32_t)NKC * WRp * 16, Bb = (uint32_t)ntap * NKC * Ns * 16;
   const uint32_t Sb = NH * (Ab + Bb);
   // layout: 2 stages of [A hi][A lo][B hi][B lo] (bf16: [A][B]), row map, barriers full[2] empty[2] done, TMEM slot
@@ -734,7 +873,9 @@ __global__ void __launch_bounds__(kTcpThreads) conv_tcp_k(TcConv a) {
         const int tq = q / NKC, kcl = q % NKC;
         const int t9 = PW ? 0 : tap9(tq);
         const float* src = wk + ((long long)t9 * kc_all + kcl) * a.Np * 4;
-        uint8_t* dst = Bt + (size_t)q * Ns * 16;
+        // KWF: [kh][chunk][kw][Ns] -- the three kw taps of a K chunk are one N = 3 Ns run
+        uint8_t* dst = KWF ? Bt + ((size_t)((t9 / 3) * NKC + kcl) * 3 * Ns + (t9 % 3) * Ns) * 16
+                           : Bt + (size_t)q * Ns * 16;
         for (int n = lane; n < Ns; n += 32) {
           tc::cp_async16(dst + n * 16, src + n * 4, 16u);
           if (NH == 2) tc::cp_async16(dst + Bb + n * 16, src + a.wlo + n * 4, 16u);
@@ -1208,8 +1349,9 @@ int conv_tc_pack(const float* w, long long wbs, int K, int N, int dgrad, float* 
 // tma: the window is fetched as whole padded lines (conv_tma_k): a channel
 // column holds lrows = ceil((WR + Sw - 1) / Sw) lines of Sw rows
 static bool tc_plan(int D, int H, int W, int K, int N, int batch, TcConv& a, int* tiles, int nt = 3,
-                    bool bf = false, bool tma = false, bool b3 = false) {
+                    bool bf = false, bool tma = false, bool b3 = false, bool kwf = false) {
   if (b3) bf = true;
+  const int rs = kwf ? kTcRows - 2 : kTcRows;  // output rows per sub-tile
   a.N = N;
   a.Np = np_of(N);
   a.Kc = K;
@@ -1218,7 +1360,7 @@ static bool tc_plan(int D, int H, int W, int K, int N, int batch, TcConv& a, int
   a.Sh = (H + 2) * a.Sw;
   a.u_first = a.Sh + a.Sw + 1;
   const int u_last = D * a.Sh + H * a.Sw + W;
-  const int tiles1 = cdiv(u_last - a.u_first + 1, kTcRows);
+  const int tiles1 = cdiv(u_last - a.u_first + 1, rs);
   a.vout = (long long)D * H * W;
   a.CB = 0;
   a.T = 1;
@@ -1239,11 +1381,14 @@ static bool tc_plan(int D, int H, int W, int K, int N, int batch, TcConv& a, int
     const int tl = cdiv(tiles1, T);
     for (int ns = std::min(a.Np, 256); ns >= 16; ns -= 16) {
       if (a.Np % ns) continue;
-      if (T * ns > 512) continue;  // TMEM columns
+      if (T * ns * (kwf ? 3 : 1) > 512) continue;  // TMEM columns
+      if (kwf && 3 * ns > 256) continue;            // one MMA's N
       for (int cb = bf ? 16 : 8; cb <= K && cb <= (bf ? 128 : 64); cb *= 2) {
         if (K % cb) continue;
         const size_t sm = 2 * stage_bytes(cb, ns, wrp, nt, bf, b3) + 3 * wr * sizeof(int) + 64;
         if (sm > (size_t)210 * 1024) continue;
+        // kw folding parks 128 rows x (2 ns + 4) fp32 in the idle stage buffers
+        if (kwf && (size_t)kTcRows * (2 * ns + 4) * 4 > 2 * stage_bytes(cb, ns, wrp, nt, bf, b3)) continue;
         const int per_sm = sm <= (size_t)110 * 1024 ? 2 : 1;
         const long long ctas0 = (long long)tl * (a.Np / ns) * batch;
         const int S = nt * (K / cb);
@@ -1255,10 +1400,12 @@ static bool tc_plan(int D, int H, int W, int K, int N, int batch, TcConv& a, int
           cost = (double)waves * ((S + kspl - 1) / kspl + 2.0) + (kspl > 1 ? 1.0 : 0.0);
         } else {
           // bf16: one MMA per 16 channels at max(N/2, (4096 + 32 N)/128) + issue cycles
+          // kw folding: nt (kh) MMAs of N = 3 ns per K step instead of nt^2 of N = ns
+          const double nq = kwf ? nt : nt * nt, ne = kwf ? 3.0 * ns : ns;
+          const double cyc = std::max(ne / 2.0, (4096.0 + 32.0 * ne) / 128.0);
           const double mma_us =
-              bf ? (b3 ? 3.0 : 1.0) * nt * nt * (cb / 16.0) * T * (std::max(ns / 2.0, (4096.0 + 32.0 * ns) / 128.0) + 6.0) /
-                       1900.0 * (per_sm == 2 ? 1.4 : 1.0)
-                 : 3.0 * nt * nt / 8.0 * cb * T * 57.0 / 1900.0 * (per_sm == 2 ? 1.4 : 1.0);
+              bf ? (b3 ? 3.0 : 1.0) * nq * (cb / 16.0) * T * (cyc + 6.0) / 1900.0 * (per_sm == 2 ? 1.4 : 1.0)
+                 : 3.0 * nq / 8.0 * cb * T * std::max(kwf ? 40.0 : 57.0, cyc) / 1900.0 * (per_sm == 2 ? 1.4 : 1.0);
           const double stage_us = std::max(1.5, mma_us);
           cost = (double)waves * ((S + kspl - 1) / kspl * stage_us + 2.0 + 0.5 * T) + (kspl > 1 ? 3.0 : 0.0);
         }
@@ -1283,17 +1430,32 @@ static bool tc_plan(int D, int H, int W, int K, int N, int batch, TcConv& a, int
   return true;
 }
 
+// kw-folded stride-1 kernel (MODE 4): D2IP_TC_KWF=0 keeps one MMA per tap
+static bool kwf_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("D2IP_TC_KWF");
+    return !v || atoi(v) != 0;
+  }();
+  return on;
+}
+
 size_t conv_tc_ws_bytes(int D, int H, int W, int K, int N, int batch, int mode) {
   TcConv a{};
   int tiles;
   const int m3 = mode & 3;
-  if (!tc_plan(D, H, W, K, N, batch, a, &tiles, m3 == 3 ? 1 : m3 ? 2 : 3, (mode & kTcBf16) != 0, false,
-               (mode & kTcBf3) != 0) ||
-      a.kspl <= 1)
-    return 0;
-  // mode 2 partials are [V_gx][C_gx]: V_gx C_gx <= 8 V N / 8 (gx dims <= 2 x the row grid)
-  return (size_t)batch * a.kspl * a.vout * N * sizeof(float);
+  size_t best = 0;
+  // the larger of the two plans (kw-folded or not) a stride-1 call may take
+  for (int kwf = 0; kwf <= (m3 == 0 && kwf_enabled() ? 1 : 0); ++kwf) {
+    if (!tc_plan(D, H, W, K, N, batch, a, &tiles, m3 == 3 ? 1 : m3 ? 2 : 3, (mode & kTcBf16) != 0, false,
+                 (mode & kTcBf3) != 0, kwf != 0) ||
+        a.kspl <= 1)
+      continue;
+    // mode 2 partials are [V_gx][C_gx]: V_gx C_gx <= 8 V N / 8 (gx dims <= 2 x the row grid)
+    best = std::max(best, (size_t)((size_t)batch * a.kspl * a.vout * N * sizeof(float)));
+  }
+  return best;
 }
+
 
 // Launch one instantiation (the >48 KB shared-memory opt-in is set on first use).
 template <int NKC, int T, int PG, int MODE, int BF>
@@ -1312,6 +1474,11 @@ template <int NKC, int BF>
 static int tc_dispatch(const TcConv& a, dim3 grid, size_t smem, cudaStream_t st, int mode, bool pg2) {
   if (mode == 1) return tc_launch<NKC, 1, 1, 1, BF>(a, grid, smem, st);
   if (mode == 2) return tc_launch<NKC, 1, 1, 2, BF>(a, grid, smem, st);
+  if (mode == 4) {
+    if (a.T == 4) return tc_launch<NKC, 4, 1, 4, BF>(a, grid, smem, st);
+    if (a.T == 2) return tc_launch<NKC, 2, 1, 4, BF>(a, grid, smem, st);
+    return tc_launch<NKC, 1, 1, 4, BF>(a, grid, smem, st);
+  }
   if (mode == 3) {
     if (a.T == 4) return tc_launch<NKC, 4, 1, 3, BF>(a, grid, smem, st);
     if (a.T == 2) return tc_launch<NKC, 2, 1, 3, BF>(a, grid, smem, st);
@@ -1439,7 +1606,19 @@ int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, lo
                        ((uintptr_t)x.bf16 & 15) == 0 && x.w + 2 <= 256;
   D2IP_CHECK_ARG(tc_plan(g.d, g.h, g.w, K, N, batch, a, &tiles, ntm, bf, use_tma, b3),
                  "conv_tc: no channel blocking fits shared memory (K=%d N=%d W=%d)", K, N, g.w);
-  a.mode = mode;
+  // kw folding (MODE 4) for stride-1 3^3 layers on the one-tile kernel: 3x fewer MMAs of 3x
+  // the width; not for the TMA / persistent bf16 kernels
+  bool kwf = false;
+  if (mode == 0 && !use_tma && kwf_enabled() && !(bf && !b3)) {
+    TcConv k2{};
+    int tiles2 = 0;
+    if (tc_plan(g.d, g.h, g.w, K, N, batch, k2, &tiles2, ntm, bf, false, b3, true)) {
+      a = k2;
+      tiles = tiles2;
+      kwf = true;
+    }
+  }
+  a.mode = kwf ? 4 : mode;
   a.t0 = mode == 2 ? 1 : 0;
   a.nt = ntm;
   a.gd = g.d;
@@ -1460,9 +1639,9 @@ int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, lo
   a.vec = y.cstride % 4 == 0 && ((uintptr_t)y.ptr & 15) == 0;
   a.xtw = bf && !b3 && x.bf16 && x.cstride % 8 == 0 && x.c % 8 == 0 && ((uintptr_t)x.bf16 & 15) == 0;
   int cols = 32;
-  while (cols < a.T * a.Ns) cols *= 2;
+  while (cols < a.T * a.Ns * (kwf ? 3 : 1)) cols *= 2;
   a.tmem_cols = cols;
-  a.idesc = tc::make_idesc(bf ? 1 : 2, kTcRows, a.Ns);
+  a.idesc = tc::make_idesc(bf ? 1 : 2, kTcRows, a.Ns * (kwf ? 3 : 1));
   // D2IP_TC_NST=3: a third stage when it fits without costing occupancy. Measured neutral at
   // cfg4 (137.9 vs 138.2 it/s) and a loss at cfg1 (1,218 vs 1,244): two stages stay the default.
   static const int nst_max = [] {
@@ -1506,7 +1685,7 @@ int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, lo
     return v ? atoi(v) : 1;
   }();
   const bool persist_on = persist_mode == 2 || (persist_mode == 1 && bf && !b3);
-  if (persist_on && !use_tma && a.kspl == 1 && (mode == 0 || mode == 3) && 2 * a.T * a.Ns <= 512 &&
+  if (persist_on && !kwf && !use_tma && a.kspl == 1 && (mode == 0 || mode == 3) && 2 * a.T * a.Ns <= 512 &&
       (long long)tiles * (a.Np / a.Ns) * batch >= 2 * 148) {
     TcConv p = a;
     p.ntiles = tiles;
@@ -1560,11 +1739,11 @@ int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, lo
     D2IP_CHECK_ARG(cr == CUDA_SUCCESS, "conv_tc: cuTensorMapEncodeTiled failed (%d)", (int)cr);
     rc = tma_dispatch_nkc(a, tm, grid, st, mode);
   } else if (b3)
-    rc = tc_dispatch_nkc<2>(a, grid, smem, st, mode, false);
+    rc = tc_dispatch_nkc<2>(a, grid, smem, st, a.mode, false);
   else if (bf)
-    rc = tc_dispatch_nkc<1>(a, grid, smem, st, mode, false);
+    rc = tc_dispatch_nkc<1>(a, grid, smem, st, a.mode, false);
   else
-    rc = tc_dispatch_nkc<0>(a, grid, smem, st, mode, pg2);
+    rc = tc_dispatch_nkc<0>(a, grid, smem, st, a.mode, pg2 && !kwf);
   D2IP_RET(rc);
   D2IP_LAUNCH_CHECK();
   if (deferred) *deferred = a.kspl > 1 ? a.kspl : 0;
@@ -1572,6 +1751,11 @@ int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, lo
     D2IP_CUDA(launch_pdl(conv_tc_splitk_reduce_k, dim3(cdiv(a.vout * Nout, 256), batch), 256, 0, st, ws, a.kspl,
                          a.vout, Nout, bias, bbs, y, accumulate));
     D2IP_LAUNCH_CHECK();
+  }
+  if (kwf) {
+    set_variant(b3 ? (a.kspl > 1 ? "tcgen05_bf16x3_kwf_splitk" : "tcgen05_bf16x3_kwf")
+                   : (a.kspl > 1 ? "tcgen05_tf32x3_kwf_splitk" : "tcgen05_tf32x3_kwf"));
+    return D2IP_OK;
   }
   set_variant(b3 ? (a.kspl > 1 ? "tcgen05_bf16x3_splitk" : "tcgen05_bf16x3")
               : use_tma ? (a.kspl > 1 ? "tcgen05_bf16_tma_splitk" : "tcgen05_bf16_tma")

@@ -162,15 +162,17 @@ def test_level4_step_and_adam_vs_reference(prec):
     np.testing.assert_allclose(dn.trace_host(0, 5)[:, 0], g["trace5"][:, 1], rtol=GRAD_TOL[prec])
 
 
-@pytest.mark.parametrize("cfg_name,prec", [("cfg2", "tf32"), ("cfg2", "fp32"), ("cfg4", "bf16")])
-def test_step_grads_four_level_config_width_vs_oracle(cfg_name, prec):
+@pytest.mark.parametrize("cfg_name,prec,grid", [("cfg2", "tf32", (32, 32, 16)), ("cfg2", "fp32", (32, 32, 16)),
+                                                ("cfg4", "bf16", (32, 32, 16)), ("cfg2", "tf32", (64, 64, 32))])
+def test_step_grads_four_level_config_width_vs_oracle(cfg_name, prec, grid):
     """The BASELINE cfg2 (16/32/64/128, TF32) and cfg4 (32/64/128/256, bf16 operands with
     fp32 accumulation) networks on a reduced 32x32x16 grid (4 electrode rings, M = 3,904)
     against the CPU oracle (pinned bit-exact to the reference at L = 4 above): loss and
     every parameter tensor within the north star's bar (1e-3 TF32 / 1e-2 bf16 overall,
-    10x that per tensor)."""
+    10x that per tensor). The 64x64x32 case is BASELINE cfg2 itself (the large-grid kernels:
+    3xbf16 weight gradients, kw-folded forwards / data gradients without split-K)."""
     full = W.CONFIGS[cfg_name]
-    spec = W.WorkloadSpec(cfg_name + "-reduced", (32, 32, 16), full.ring_heights, full.channels, full.in_channels,
+    spec = W.WorkloadSpec(cfg_name + "-reduced", grid, full.ring_heights, full.channels, full.in_channels,
                           1, 1, 1, 1, precision=full.precision)
     wl = W.make_workload(spec, seed=0, frames=1)
     net = spec.network(seed=1)

@@ -368,7 +368,7 @@ print(L.d2ip_last_variant().decode(), float((out - ref).norm() / ref.norm()))
     # single-pass bf16 forwards (D2IP_BF16_FWD3=0) and 3xbf16 stride-1 forwards (D2IP_BF3_MASK=31)
     # are the variants these kernels implement; the defaults route those layers elsewhere
     env = dict(os.environ, **{knob: "2" if knob == "D2IP_TC_PERSIST" else "1"}, D2IP_BF16_FWD3="0",
-               D2IP_BF3_MASK="31", D2IP_TF32_BF3="1")
+               D2IP_BF3_MASK="31", D2IP_TF32_BF3="1", D2IP_TC_KWF="0")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600,
                        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert r.returncode == 0, r.stderr[-2000:]

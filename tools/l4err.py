@@ -8,7 +8,8 @@ from paper_2507_14046_b200.priornet import kaiming_flat, sample_noise_input, par
 torch.set_num_threads(16)
 name, prec = sys.argv[1], sys.argv[2]
 full = W.CONFIGS[name]
-spec = W.WorkloadSpec(name + "-r", (32, 32, 16), full.ring_heights, full.channels, full.in_channels, 1, 1, 1, 1)
+grid = tuple(int(v) for v in sys.argv[3].split("x")) if len(sys.argv) > 3 else (32, 32, 16)
+spec = W.WorkloadSpec(name + "-r", grid, full.ring_heights, full.channels, full.in_channels, 1, 1, 1, 1)
 wl = W.make_workload(spec, seed=0, frames=1)
 net = spec.network(seed=1)
 noise = sample_noise_input(wl.grid, 0, spec.in_channels, 0.1)
