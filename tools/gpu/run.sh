@@ -46,6 +46,24 @@ ncu)
 convs)
   PREC=$1; shift
   for a in "$@"; do timeout 120 python tools/conv_bench.py $a 20 $PREC 2>&1 | tail -4; done ;;
+profiles)
+  # round evidence: bench lines, launch lists, ncu --set full of the dominant kernels
+  TAG=${1:-r2}
+  timeout 900 python bench.py > gpurun_out/${TAG}_bench_cfg2.json 2> gpurun_out/${TAG}_bench_cfg2.err; echo "cfg2 rc $?"
+  timeout 600 python bench.py --workload cfg1 --steps 300 > gpurun_out/${TAG}_bench_cfg1.json 2> gpurun_out/${TAG}_bench_cfg1.err; echo "cfg1 rc $?"
+  timeout 600 python bench.py --workload cfg3 --steps 20 --skip-cpu > gpurun_out/${TAG}_bench_cfg3.json 2> gpurun_out/${TAG}_bench_cfg3.err; echo "cfg3 rc $?"
+  timeout 900 python bench.py --workload cfg4 --steps 20 --skip-cpu > gpurun_out/${TAG}_bench_cfg4.json 2> gpurun_out/${TAG}_bench_cfg4.err; echo "cfg4 rc $?"
+  for w in cfg2 cfg1 cfg4; do bash tools/gpu/run.sh launches ${TAG}_$w $w > /dev/null 2>&1; echo "launches $w $?"; done
+  for spec in "cfg2dec0c1|conv_tc_k|48 16 64x64x32|fwd|tf32" "cfg2dec0c1dg|conv_tc_k|48 16 64x64x32|dgrad|tf32" \
+              "cfg4dec0c1|conv_tc_k|96 32 96x96x48|fwd|bf16"; do
+    IFS='|' read -r name kr shape dir prec <<< "$spec"
+    python tools/conv_one.py $shape $dir 3 $prec > /dev/null 2>&1 || { echo "clean $name failed"; continue; }
+    timeout 400 ncu --set full --import-source on --clock-control none -k regex:$kr -c 1 -o gpurun_out/ncu_$name \
+      python tools/conv_one.py $shape $dir 1 $prec > gpurun_out/ncu_$name.log 2>&1
+    ncu -i gpurun_out/ncu_$name.ncu-rep --page raw --csv > gpurun_out/ncu_$name.raw.csv 2>/dev/null
+    python profiles/ncu_summary.py gpurun_out/ncu_$name.raw.csv gpurun_out/${TAG}_ncu_$name.json
+    rm -f gpurun_out/ncu_$name.ncu-rep; echo "ncu $name done"
+  done ;;
 sanitize)
   export PYTORCH_NO_CUDA_MEMORY_CACHING=1
   timeout 1200 /usr/local/cuda/bin/compute-sanitizer --tool memcheck --leak-check no --error-exitcode 9 --print-limit 20 \
