@@ -293,7 +293,8 @@ def run_gpu(args):
         t_dev = float(t.item())
         dist.barrier()
     status = dn.status_host()
-    assert status[0, 1] == 0, "non-finite loss during the benchmark"
+    # (D2IP_BENCH_NOCHECK=1: timing studies with deliberately wrong kernels, e.g. D2IP_TC_DBG)
+    assert status[0, 1] == 0 or os.environ.get("D2IP_BENCH_NOCHECK") == "1", "non-finite loss during the benchmark"
     launches = dn.launches_per_iter()
     # replicas / sharded sequences: every rank's units count; the joint warm-start is ONE
     # job split over the ranks (strong scaling): its iterations count once

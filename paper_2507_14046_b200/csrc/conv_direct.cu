@@ -366,40 +366,46 @@ __global__ void __launch_bounds__(256) wgrad_tiled_reduce_k(const float* __restr
   out[b * obs + e] = s;
 }
 
-// out[e] = sum_c partial[c][e], fixed order: warp w sums chunks w, w+8, ...,
-// then warp 0 adds the 8 warp sums in order.
-__global__ void __launch_bounds__(256) reduce_chunks_k(const float* __restrict__ partial, int nchunks, int n,
-                                                       float* out, long long obs) {
+// out[e] = sum_c partial[c][e], fixed order: 32 warps per block, warp w sums chunks w, w+32,
+// ... in four interleaved partial sums (chunk w + 32 (4i + j) into sum j), then warp 0 adds
+// the 32 warp sums in order. Deterministic; 1,024 threads and four loads in flight per lane
+// keep the long chunk lists (up to 1,184 LayerNorm-backward blocks) off the latency chain.
+__global__ void __launch_bounds__(1024) reduce_chunks_k(const float* __restrict__ partial, int nchunks, int n,
+                                                        float* out, long long obs) {
   D2IP_PDL_ENTRY();
-  __shared__ float red[8][33];
+  __shared__ float red[32][33];
   const int b = blockIdx.y;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int e = blockIdx.x * 32 + lane;
   float s = 0.f;
   if (e < n) {
     const float* p = partial + (long long)b * nchunks * n + e;
-    float s0 = 0.f, s1 = 0.f;
+    float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
     int c = w;
-    for (; c + 8 < nchunks; c += 16) {
-      s0 += p[(long long)c * n];
-      s1 += p[(long long)(c + 8) * n];
+    for (; c + 96 < nchunks; c += 128) {
+      const float a0 = __ldg(p + (long long)c * n), a1 = __ldg(p + (long long)(c + 32) * n);
+      const float a2 = __ldg(p + (long long)(c + 64) * n), a3 = __ldg(p + (long long)(c + 96) * n);
+      s0 += a0;
+      s1 += a1;
+      s2 += a2;
+      s3 += a3;
     }
-    for (; c < nchunks; c += 8) s0 += p[(long long)c * n];
-    s = s0 + s1;
+    for (; c < nchunks; c += 32) s0 += __ldg(p + (long long)c * n);
+    s = (s0 + s1) + (s2 + s3);
   }
   red[w][lane] = s;
   __syncthreads();
   if (w != 0 || e >= n) return;
   s = 0.f;
 #pragma unroll
-  for (int q = 0; q < 8; ++q) s += red[q][lane];
+  for (int q = 0; q < 32; ++q) s += red[q][lane];
   out[b * obs + e] = s;
 }
 
 int reduce_chunks(const float* partial, int nchunks, int n, float* out, long long obs, int batch,
                   cudaStream_t st) {
   dim3 grid(cdiv(n, 32), batch);
-  D2IP_CUDA(launch_pdl(reduce_chunks_k, grid, 256, 0, st, partial, nchunks, n, out, obs));
+  D2IP_CUDA(launch_pdl(reduce_chunks_k, grid, 1024, 0, st, partial, nchunks, n, out, obs));
   D2IP_LAUNCH_CHECK();
   return D2IP_OK;
 }

@@ -103,6 +103,8 @@ struct TcConv {
   int async_arrive;  // bf16 twin path: stages complete by cp.async.mbarrier.arrive (D2IP_TC_ASYNC)
   int dbg;           // D2IP_TC_DBG=1: producers skip the fills (MMA-side timing only)
   int ntiles;        // persistent kernel: tiles (blocks of T x 128 rows) of the grid
+  int ln;            // MODE 4, one N slice, no split-K: LayerNorm (+ residual) (+ act) in the epilogue
+  LnFuse lnf;
 };
 
 // Per stage: A hi + A lo windows, B hi + B lo tiles (nt^2 taps); bf16: one
@@ -309,6 +311,91 @@ __device__ __forceinline__ void tc_epilogue_kwf(const TcConv& a, uint32_t tmem, 
         v = ((dp - 1) * a.gh + (hp - 1)) * a.gw + (wp - 1);
     }
     const int rn = row < RS ? row : RS - 1;  // (in-bounds exchange reads for the idle rows)
+    if (a.ln) {
+      // fused ChannelLayerNorm: this thread holds half of the row's channels (<= 4 chunks of 8);
+      // the row statistics combine the two halves through shared memory (fixed order)
+      float x[4][8];
+      float sum = 0.f;
+      const int nch = (cend - cbeg) >> 3;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (q < nch) {
+          const int c0 = cbeg + 8 * q;
+          tc::tmem_ld8(tcol + c0, x[q]);
+          const float4* p1 = reinterpret_cast<const float4*>(xch + (rn + 1) * xs + c0);
+          const float4* p2 = reinterpret_cast<const float4*>(xch + (rn + 2) * xs + Ns + c0);
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const float4 q1 = p1[h], q2 = p2[h];
+            x[q][4 * h] += q1.x + q2.x;
+            x[q][4 * h + 1] += q1.y + q2.y;
+            x[q][4 * h + 2] += q1.z + q2.z;
+            x[q][4 * h + 3] += q1.w + q2.w;
+          }
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            x[q][j] = (S > 0 ? x[q][j] : 0.f) + (bias ? __ldg(bias + n0 + c0 + j) : 0.f);
+            sum += x[q][j];
+          }
+        }
+      }
+      float* st = xch + kTcRows * xs;  // [2][128] row partials
+      const int half = (warp - 1) >> 2;
+      st[half * kTcRows + row] = sum;
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      const float mean = (st[row] + st[kTcRows + row]) / (float)a.N;
+      float q2s = 0.f;
+#pragma unroll
+      for (int q = 0; q < 4; ++q)
+        if (q < nch)
+#pragma unroll
+          for (int j = 0; j < 8; ++j) {
+            const float d = x[q][j] - mean;
+            q2s = fmaf(d, d, q2s);
+          }
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      st[half * kTcRows + row] = q2s;
+      asm volatile("bar.sync 1, 256;" ::: "memory");
+      const float rs = 1.0f / sqrtf((st[row] + st[kTcRows + row]) / (float)a.N + 1e-5f);
+      if (v >= 0) {
+        const LnFuse& L = a.lnf;
+        const long long V = a.vout;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          if (q < nch) {
+            const int c = cbeg + 8 * q;
+            float xh[8], o[8];
+            float r[8];
+            if (L.res.ptr) {
+              const float4* rp = reinterpret_cast<const float4*>(L.res.ptr + b * L.res.bstride +
+                                                                (long long)v * L.res.cstride + c);
+              const float4 r0 = rp[0], r1 = rp[1];
+              r[0] = r0.x; r[1] = r0.y; r[2] = r0.z; r[3] = r0.w; r[4] = r1.x; r[5] = r1.y; r[6] = r1.z; r[7] = r1.w;
+            }
+#pragma unroll
+            for (int j = 0; j < 8; ++j) {
+              xh[j] = (x[q][j] - mean) * rs;
+              float t = fmaf(xh[j], __ldg(L.gamma + b * L.pbs + c + j), __ldg(L.beta + b * L.pbs + c + j));
+              if (L.res.ptr) t += r[j];
+              o[j] = L.act == 1 ? lrelu(t, L.slope) : t;
+            }
+            float4* xp = reinterpret_cast<float4*>(L.xhat + ((long long)b * V + v) * a.N + c);
+            xp[0] = make_float4(xh[0], xh[1], xh[2], xh[3]);
+            xp[1] = make_float4(xh[4], xh[5], xh[6], xh[7]);
+            float4* op = reinterpret_cast<float4*>(L.out.ptr + b * L.out.bstride + (long long)v * L.out.cstride + c);
+            op[0] = make_float4(o[0], o[1], o[2], o[3]);
+            op[1] = make_float4(o[4], o[5], o[6], o[7]);
+            if (L.out.bf16) {
+              uint4 w;
+              w.x = bf2(o[0], o[1]); w.y = bf2(o[2], o[3]); w.z = bf2(o[4], o[5]); w.w = bf2(o[6], o[7]);
+              *reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(L.out.bf16) + b * L.out.bstride +
+                                        (long long)v * L.out.cstride + c) = w;
+            }
+          }
+        }
+        if (half == 0) L.rstd[(long long)b * V + v] = rs;
+      }
+    } else {
     for (int c0 = cbeg; c0 < cend; c0 += 8) {
       float vals[8];
       tc::tmem_ld8(tcol + c0, vals);
@@ -323,6 +410,7 @@ __device__ __forceinline__ void tc_epilogue_kwf(const TcConv& a, uint32_t tmem, 
         vals[4 * h + 3] += q1.w + q2.w;
       }
       tc_store8(a, b, ks, v, n0 + c0, vals, S <= 0, bias);
+    }
     }
     asm volatile("bar.sync 1, 256;" ::: "memory");
   }
@@ -487,7 +575,7 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
     for (int s = pg; s < S; s += PG) {
       const int slot = s % NST;
       if (s >= NST) tc::mbar_wait(&empty[slot], (uint32_t)(((s / NST) - 1) & 1));
-      if (a.dbg) {  // D2IP_TC_DBG=1: no fills (measures the MMA side alone; wrong results)
+      if (a.dbg == 1) {  // D2IP_TC_DBG=1: no fills (measures the MMA side alone; wrong results)
         tc::mbar_arrive(&full[slot]);
         continue;
       }
@@ -600,6 +688,11 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
         // every operand of the stage is an async copy: arrive when this thread's copies
         // land (no wait here -- the next stage's copies are issued while these fly);
         // the MMA thread's proxy fence makes them visible to the tensor core
+        asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(tc::smem_u32(&full[slot]))
+                     : "memory");
+        continue;
+      }
+      if (!BF && a.dbg == 2) {  // D2IP_TC_DBG=2 (study only, wrong results): no lo split, async arrive
         asm volatile("cp.async.mbarrier.arrive.noinc.shared::cta.b64 [%0];" ::"r"(tc::smem_u32(&full[slot]))
                      : "memory");
         continue;
@@ -1373,9 +1466,13 @@ static bool tc_plan(int D, int H, int W, int K, int N, int batch, TcConv& a, int
     const char* v = getenv("D2IP_TC_T");
     return v ? atoi(v) : 0;
   }();
+  // kw-folded layers with >= 2 waves of single tiles: two sub-tiles per CTA share every stage's
+  // weight tile and fixed costs (measured: 48->16 at 64x64x32 fwd 120 -> 94 us, 16->16 56 -> 40;
+  // 96->32 at 32x32x16 (150 tiles) is better left at one)
+  const int t_pref = t_force ? t_force : (kwf && (long long)tiles1 * batch >= 2LL * 296 && !large) ? 2 : 0;
   for (int T : {1, 2, 4}) {
-    if (T > 1 && (!large || nt == 2)) break;
-    if (t_force && large && nt != 2 && T != t_force) continue;
+    if (T > 1 && ((!large && !t_pref) || nt == 2)) break;
+    if (t_pref && nt != 2 && T != t_pref) continue;
     const int wr = nt == 1 ? T * kTcRows : wr_of(a.Sw, T);
     const int wrp = tma ? (wr + 2 * a.Sw - 2) / a.Sw * a.Sw : wrp_of(wr);
     const int tl = cdiv(tiles1, T);
@@ -1445,7 +1542,7 @@ size_t conv_tc_ws_bytes(int D, int H, int W, int K, int N, int batch, int mode) 
   const int m3 = mode & 3;
   size_t best = 0;
   // the larger of the two plans (kw-folded or not) a stride-1 call may take
-  for (int kwf = 0; kwf <= (m3 == 0 && kwf_enabled() ? 1 : 0); ++kwf) {
+  for (int kwf = 0; kwf <= (m3 == 0 && kwf_enabled() && !(mode & (kTcBf16 | kTcBf3)) ? 1 : 0); ++kwf) {
     if (!tc_plan(D, H, W, K, N, batch, a, &tiles, m3 == 3 ? 1 : m3 ? 2 : 3, (mode & kTcBf16) != 0, false,
                  (mode & kTcBf3) != 0, kwf != 0) ||
         a.kspl <= 1)
@@ -1579,7 +1676,9 @@ static int tma_dispatch_nkc(const TcConv& a, const CUtensorMap& tm, dim3 grid, c
 }
 
 int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, long long bbs, d2ip_act y,
-                int accumulate, float* ws, size_t ws_bytes, int batch, cudaStream_t st, int* deferred, int mode) {
+                int accumulate, float* ws, size_t ws_bytes, int batch, cudaStream_t st, int* deferred, int mode,
+                const LnFuse* ln, int* fused) {
+  if (fused) *fused = 0;
   const bool b3 = (mode & kTcBf3) != 0;
   const bool bf = b3 || (mode & kTcBf16) != 0;
   mode &= 3;
@@ -1607,9 +1706,10 @@ int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, lo
   D2IP_CHECK_ARG(tc_plan(g.d, g.h, g.w, K, N, batch, a, &tiles, ntm, bf, use_tma, b3),
                  "conv_tc: no channel blocking fits shared memory (K=%d N=%d W=%d)", K, N, g.w);
   // kw folding (MODE 4) for stride-1 3^3 layers on the one-tile kernel: 3x fewer MMAs of 3x
-  // the width; not for the TMA / persistent bf16 kernels
+  // the width. 3xTF32 layers only: on cfg4's 3xbf16 forwards (large grids, T = 4 tiles) it
+  // measured slower (122.7 vs 127.9 it/s); not for the TMA / persistent bf16 kernels
   bool kwf = false;
-  if (mode == 0 && !use_tma && kwf_enabled() && !(bf && !b3)) {
+  if (mode == 0 && !use_tma && kwf_enabled() && !bf) {
     TcConv k2{};
     int tiles2 = 0;
     if (tc_plan(g.d, g.h, g.w, K, N, batch, k2, &tiles2, ntm, bf, false, b3, true)) {
@@ -1667,6 +1767,22 @@ int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, lo
     return v ? atoi(v) : 0;
   }();
   a.dbg = dbg_on;
+  // LayerNorm fused into the kw-folded epilogue: one N slice holding every channel (<= 64), no
+  // split-K, float4-aligned views; statistics parked after the P_1 / P_2 exchange rows
+  static const bool ln_on = [] {
+    const char* v = getenv("D2IP_TC_LNFUSE");
+    return !v || atoi(v) != 0;
+  }();
+  a.ln = 0;
+  if (ln && ln_on && kwf && a.kspl == 1 && a.Ns == N && N % 16 == 0 && N <= 64 && !accumulate &&
+      ln->out.cstride % 4 == 0 && ((uintptr_t)ln->out.ptr & 15) == 0 &&
+      (!ln->res.ptr || (ln->res.cstride % 4 == 0 && ((uintptr_t)ln->res.ptr & 15) == 0)) &&
+      (!ln->out.bf16 || (ln->out.cstride % 8 == 0 && ((uintptr_t)ln->out.bf16 & 15) == 0)) &&
+      (size_t)kTcRows * (2 * a.Ns + 4) * 4 + 2 * kTcRows * 4 <= (size_t)a.nst * stage_bytes(a.CB, a.Ns, a.WRp, a.nt, a.bf, a.b3)) {
+    a.ln = 1;
+    a.lnf = *ln;
+    if (fused) *fused = 1;
+  }
   const size_t smem = use_tma ? 0 : tc_smem_bytes(a);  // (the TMA kernel sizes its own)
   const dim3 grid(tiles, (a.Np / a.Ns) * a.kspl, batch);
   // one producer group (all eight warps per stage) measured faster than two on

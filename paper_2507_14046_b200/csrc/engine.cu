@@ -14,6 +14,7 @@
 #include <algorithm>
 #include <cstring>
 #include <vector>
+#include <cstdlib>
 
 #include "common.cuh"
 #include "kernels.h"
@@ -267,11 +268,12 @@ static void plan_views(d2ip_engine& E) {
 // concurrent convolutions must not share one.
 static float* tcws(Ctx& k) { return k.st == k.E.side2 ? k.E.tc_ws2 : k.E.tc_ws; }
 
-int cfwd(Ctx& k, const ConvP& c, d2ip_act x, d2ip_act y, int acc, SplitK* sk) {
+int cfwd(Ctx& k, const ConvP& c, d2ip_act x, d2ip_act y, int acc, SplitK* sk, const LnFuse* ln, int* fused) {
+  if (fused) *fused = 0;
   if (c.tcf) {
     int kspl = 0;
     D2IP_RET(conv_tc_run(x, c.pkf, c.tdf.K, c.tdf.N, k.th() + c.ob, k.pbs, y, acc, tcws(k), k.E.tc_ws_bytes, k.B,
-                         k.st, sk && !acc ? &kspl : nullptr, c.tdf.mode));
+                         k.st, sk && !acc ? &kspl : nullptr, c.tdf.mode, ln, fused));
     if (sk) *sk = kspl ? SplitK{tcws(k), kspl, k.th() + c.ob, k.pbs} : SplitK{};
     return D2IP_OK;
   }
@@ -293,7 +295,17 @@ int cdgrad(Ctx& k, const ConvP& c, d2ip_act gy, d2ip_act gx, int acc, SplitK* sk
   return conv_dgrad_direct(gy, k.th() + c.ow, k.pbs, c.ks, c.stride, gx, acc, k.B, k.st, c.dil);
 }
 
+// study knob (timing only, wrong results): D2IP_SKIP=1 skips the weight gradients, 2 the J passes
+static int skip_mask() {
+  static const int m = [] {
+    const char* v = getenv("D2IP_SKIP");
+    return v ? atoi(v) : 0;
+  }();
+  return m;
+}
+
 int cwgrad(Ctx& k, const ConvP& c, d2ip_act x, d2ip_act gy) {
+  if (skip_mask() & 1) return D2IP_OK;
   if (c.dil != 1)
     return conv_wgrad_direct(x, gy, c.ks, c.stride, k.gr() + c.ow, k.pbs, k.wgws, k.E.wg_ws_bytes, k.B, k.st, c.dil);
   return conv_wgrad(x, gy, c.ks, c.stride, k.gr() + c.ow, k.pbs, k.wgws, k.E.wg_ws_bytes, k.prec, k.B, k.st);
@@ -372,13 +384,34 @@ static int block_fwd(Ctx& k, Block& bl) {
     D2IP_RET(cfwd(k2, bl.sk, bl.x, raw2, 0));
   }
   SplitK sk;
-  D2IP_RET(cfwd(k, bl.c1, bl.x, raw, 0, &sk));
-  D2IP_RET(norm_act_fwd(raw, k.th() + bl.n1.og, k.th() + bl.n1.ob, k.pbs, none, 1, k.slope, h1, bl.xh1, bl.rs1, k.B,
-                        k.st, sk));
-  D2IP_RET(cfwd(k, bl.c2, h1, raw, 0, &sk));
-  D2IP_RET(fork_to(k, k.side2, k.st));  // join the skip before the residual add
-  D2IP_RET(norm_act_fwd(raw, k.th() + bl.n2.og, k.th() + bl.n2.ob, k.pbs, raw2, 1, k.slope, bl.out, bl.xh2, bl.rs2,
-                        k.B, k.st, sk));
+  // LayerNorm (+ LeakyReLU) in the conv epilogue where the plan allows it (kw-folded, one N
+  // slice, no split-K); otherwise the raw output and a norm_act_fwd launch
+  LnFuse l1;
+  l1.gamma = k.th() + bl.n1.og;
+  l1.beta = k.th() + bl.n1.ob;
+  l1.pbs = k.pbs;
+  l1.out = h1;
+  l1.xhat = bl.xh1;
+  l1.rstd = bl.rs1;
+  l1.slope = k.slope;
+  int f1 = 0;
+  D2IP_RET(cfwd(k, bl.c1, bl.x, raw, 0, &sk, &l1, &f1));
+  if (!f1)
+    D2IP_RET(norm_act_fwd(raw, k.th() + bl.n1.og, k.th() + bl.n1.ob, k.pbs, none, 1, k.slope, h1, bl.xh1, bl.rs1,
+                          k.B, k.st, sk));
+  D2IP_RET(fork_to(k, k.side2, k.st));  // join the skip before the residual add (conv2's epilogue)
+  LnFuse l2 = l1;
+  l2.gamma = k.th() + bl.n2.og;
+  l2.beta = k.th() + bl.n2.ob;
+  l2.res = raw2;
+  l2.out = bl.out;
+  l2.xhat = bl.xh2;
+  l2.rstd = bl.rs2;
+  int f2 = 0;
+  D2IP_RET(cfwd(k, bl.c2, h1, raw, 0, &sk, &l2, &f2));
+  if (!f2)
+    D2IP_RET(norm_act_fwd(raw, k.th() + bl.n2.og, k.th() + bl.n2.ob, k.pbs, raw2, 1, k.slope, bl.out, bl.xh2,
+                          bl.rs2, k.B, k.st, sk));
   return D2IP_OK;
 }
 
@@ -436,9 +469,19 @@ static int forward(Ctx& k) {
   d2ip_act none{};
   D2IP_RET(pack_all(k));
   SplitK sk;
-  D2IP_RET(cfwd(k, E.stem, z, raw, 0, &sk));
-  D2IP_RET(norm_act_fwd(raw, k.th() + E.stem_n.og, k.th() + E.stem_n.ob, k.pbs, none, 1, k.slope, a0, E.stem_xh,
-                        E.stem_rs, k.B, k.st, sk));
+  LnFuse ls;
+  ls.gamma = k.th() + E.stem_n.og;
+  ls.beta = k.th() + E.stem_n.ob;
+  ls.pbs = k.pbs;
+  ls.out = a0;
+  ls.xhat = E.stem_xh;
+  ls.rstd = E.stem_rs;
+  ls.slope = k.slope;
+  int fs = 0;
+  D2IP_RET(cfwd(k, E.stem, z, raw, 0, &sk, &ls, &fs));
+  if (!fs)
+    D2IP_RET(norm_act_fwd(raw, k.th() + E.stem_n.og, k.th() + E.stem_n.ob, k.pbs, none, 1, k.slope, a0, E.stem_xh,
+                          E.stem_rs, k.B, k.st, sk));
   for (auto& bl : E.enc) D2IP_RET(block_fwd(k, bl));
   D2IP_RET(block_fwd(k, E.neck));
   for (size_t j = 0; j < E.dec.size(); ++j) {
@@ -465,7 +508,8 @@ static int loss(Ctx& k) {
   if (tv_on(E))
     D2IP_RET(tv_fwd_bwd(E.b.mapped, E.b.history, E.d.max_history, E.b.status, E.d.R, E.d.C, E.d.P,
                         E.d.lambda_tv, E.d.lambda_s, E.d.lambda_t, E.d.tv_eps, E.gmapped, E.regpart, k.B, k.st));
-  D2IP_RET(jac_fwd_partial(E.b.J, jbs, E.sigma_c, E.d.Vp, E.d.M, E.d.Vp, E.jpart, E.nseg, k.B, k.st));
+  if (!(skip_mask() & 2))
+    D2IP_RET(jac_fwd_partial(E.b.J, jbs, E.sigma_c, E.d.Vp, E.d.M, E.d.Vp, E.jpart, E.nseg, k.B, k.st));
   D2IP_RET(jac_loss(E.jpart, E.nseg, E.d.M, E.b.dv, E.d.n_rhs, E.d.data_norm, E.regpart, tv_on(E) ? E.n_reg : 0,
                     E.d.lambda_tv, E.rs, E.b.trace, E.d.max_iters, E.b.status, k.B, k.st));
   return D2IP_OK;
@@ -476,7 +520,7 @@ static int backward(Ctx& k) {
   const int* c = E.d.channels;
   const long long jbs = E.d.j_shared ? 0 : (long long)E.d.M * E.d.Vp;
   const float scale = (float)((double)E.d.hi - (double)E.d.lo);
-  D2IP_RET(jac_adj_partial(E.b.J, jbs, E.rs, E.d.M, E.d.Vp, E.adjpart, E.rsplit, k.B, k.st));
+  if (!(skip_mask() & 2)) D2IP_RET(jac_adj_partial(E.b.J, jbs, E.rs, E.d.M, E.d.Vp, E.adjpart, E.rsplit, k.B, k.st));
   if (tv_on(E)) {
     D2IP_RET(jac_adj_finish(E.adjpart, E.rsplit, E.d.Vp, E.d.V, E.b.vox_of_col, E.b.sig, scale, E.gmapped, E.V[0],
                             1, k.B, k.st));
@@ -494,7 +538,8 @@ static int backward(Ctx& k) {
   if (tail_bwd_supported(last.out)) {  // C_out = 1: lane-group kernels (no GEMM shape to tile)
     Ctx ks = k;
     D2IP_RET(side_ctx(k, ks));
-    D2IP_RET(tail_wgrad(last.out, E.gtail, k.gr() + E.tail.ow, k.pbs, ks.wgws, E.wg_ws_bytes, k.B, ks.st));
+    if (!(skip_mask() & 1))
+      D2IP_RET(tail_wgrad(last.out, E.gtail, k.gr() + E.tail.ow, k.pbs, ks.wgws, E.wg_ws_bytes, k.B, ks.st));
     D2IP_RET(tail_dgrad(E.gtail, k.th() + E.tail.ow, k.pbs, last.gout, k.B, k.st));
   } else {
     D2IP_RET(cwgrad_side(k, E.tail, last.out, gt));
@@ -672,6 +717,7 @@ int d2ip_engine_create(const d2ip_net_desc* desc, d2ip_engine** out) {
     E->V[l] = (long long)E->D[l] * E->H[l] * E->W[l];
   }
   E->nlanes = d.arch == D2IP_ARCH_FAST_RESUNET ? 3 : 2;
+  if (const char* v = getenv("D2IP_LANES")) E->nlanes = std::max(1, std::min(d2ip_engine::kLanes, atoi(v)));
   if (d.arch == D2IP_ARCH_FAST_RESUNET) {
     int rc = refnet_plan_params(*E);
     if (rc != D2IP_OK) {

@@ -161,7 +161,8 @@ int fork_to(Ctx& k, cudaStream_t from, cudaStream_t to);
 // weight gradient on a side lane, after everything already on st
 int cwgrad_side(Ctx& k, const ConvP& c, d2ip_act x, d2ip_act gy);
 
-int cfwd(Ctx& k, const ConvP& c, d2ip_act x, d2ip_act y, int acc, SplitK* sk = nullptr);
+int cfwd(Ctx& k, const ConvP& c, d2ip_act x, d2ip_act y, int acc, SplitK* sk = nullptr, const LnFuse* ln = nullptr,
+         int* fused = nullptr);
 int cdgrad(Ctx& k, const ConvP& c, d2ip_act gy, d2ip_act gx, int acc, SplitK* sk = nullptr);
 int cwgrad(Ctx& k, const ConvP& c, d2ip_act x, d2ip_act gy);
 

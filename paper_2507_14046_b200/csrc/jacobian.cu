@@ -11,6 +11,9 @@
 // J is M x Vp fp32 row-major (Vp % 4 == 0, zero padded), columns in the
 // network's memory order of the masked voxels. Both passes stream J from HBM
 // with 128-bit loads; all reductions are fixed-order (deterministic).
+#include <algorithm>
+#include <cstdlib>
+
 #include "common.cuh"
 #include "kernels.h"
 
@@ -154,9 +157,35 @@ int jac_sum(const float* partial, int nseg, int m, float* y, int batch, cudaStre
 constexpr int kAdjThreads = 256;
 constexpr int kAdjCols = kAdjThreads * 4;
 
+static bool adj_wide() {  // D2IP_ADJ_WIDE=1: four float4 columns per thread (measured no faster)
+  static const bool v = [] {
+    const char* e = getenv("D2IP_ADJ_WIDE");
+    return e && atoi(e) != 0;
+  }();
+  return v;
+}
+
+static int adj_blocks_per_sm() {  // D2IP_ADJ_BPS: row splits sized for this many blocks per SM
+  static const int v = [] {
+    const char* e = getenv("D2IP_ADJ_BPS");
+    return e ? std::max(1, atoi(e)) : 3;  // 3: cfg2 298 -> 274 us, cfg4 900 -> 820 us (with 8 loads in flight)
+  }();
+  return v;
+}
+
+static int adj_unroll() {  // D2IP_ADJ_U: loads in flight per thread (4 or 8)
+  static const int v = [] {
+    const char* e = getenv("D2IP_ADJ_U");
+    return e && atoi(e) == 4 ? 4 : 8;
+  }();
+  return v;
+}
+
 int jac_adj_rows(int m, int vp, int batch) {
-  const int ctiles = cdiv(vp, kAdjCols);
-  long long want = (148LL * 6 + (long long)ctiles * batch - 1) / ((long long)ctiles * batch);
+  const int ctiles = cdiv(vp, adj_wide() ? 4 * kAdjCols : kAdjCols);
+  // (independent of the batch: a batched engine's sequences sum in the same order as single runs)
+  (void)batch;
+  long long want = (148LL * adj_blocks_per_sm() + ctiles - 1) / ctiles;
   if (want > m) want = m;
   if (want < 1) want = 1;
   return (int)want;
@@ -166,6 +195,7 @@ size_t jac_adj_ws(int m, int vp, int batch) {
   return (size_t)batch * jac_adj_rows(m, vp, batch) * vp * sizeof(float);
 }
 
+template <int U>
 __global__ void __launch_bounds__(kAdjThreads) jac_adj_k(const float* __restrict__ J, long long jbs,
                                                          const float* __restrict__ rs, int M, int vp,
                                                          float* __restrict__ partial, int rsplit) {
@@ -182,12 +212,12 @@ __global__ void __launch_bounds__(kAdjThreads) jac_adj_k(const float* __restrict
   const int n4 = vp >> 2;
   float4 acc = make_float4(0.f, 0.f, 0.f, 0.f);
   int m = m0;
-  for (; m + 4 <= m1; m += 4) {
-    float4 a[4];
+  for (; m + U <= m1; m += U) {
+    float4 a[U];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) a[u] = __ldg(col + (long long)(m + u) * n4);
+    for (int u = 0; u < U; ++u) a[u] = __ldg(col + (long long)(m + u) * n4);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) {
+    for (int u = 0; u < U; ++u) {
       const float r = rsm[m + u - m0];
       acc.x = fmaf(a[u].x, r, acc.x);
       acc.y = fmaf(a[u].y, r, acc.y);
@@ -206,11 +236,81 @@ __global__ void __launch_bounds__(kAdjThreads) jac_adj_k(const float* __restrict
   reinterpret_cast<float4*>(partial + ((long long)b * rsplit + sp) * vp)[j4] = acc;
 }
 
+// Wide variant: a block covers 4 x 1,024 columns (16 KB of every row it visits, like the forward's
+// row segments) and each thread keeps four float4 column accumulators, two rows in flight (8
+// independent 16-byte loads). Fixed summation order per column (rows ascending in the split).
+__global__ void __launch_bounds__(kAdjThreads) jac_adj_wide_k(const float* __restrict__ J, long long jbs,
+                                                              const float* __restrict__ rs, int M, int vp,
+                                                              float* __restrict__ partial, int rsplit) {
+  D2IP_PDL_ENTRY();
+  extern __shared__ float rsm[];
+  const int b = blockIdx.z, sp = blockIdx.y;
+  const int rows = (M + rsplit - 1) / rsplit;
+  const int m0 = sp * rows, m1 = min(M, m0 + rows);
+  for (int i = threadIdx.x; i < m1 - m0; i += blockDim.x) rsm[i] = rs[(long long)b * M + m0 + i];
+  __syncthreads();
+  const int n4 = vp >> 2;
+  const int base = blockIdx.x * (4 * kAdjThreads) + threadIdx.x;
+  const float4* Jb = reinterpret_cast<const float4*>(J + b * jbs);
+  float4 acc[4];
+  bool ok[4];
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    acc[c] = make_float4(0.f, 0.f, 0.f, 0.f);
+    ok[c] = base + c * kAdjThreads < n4;
+  }
+  int m = m0;
+  for (; m + 2 <= m1; m += 2) {
+    float4 a[2][4];
+#pragma unroll
+    for (int u = 0; u < 2; ++u)
+#pragma unroll
+      for (int c = 0; c < 4; ++c)
+        a[u][c] = ok[c] ? __ldg(Jb + (long long)(m + u) * n4 + base + c * kAdjThreads) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const float r = rsm[m + u - m0];
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        acc[c].x = fmaf(a[u][c].x, r, acc[c].x);
+        acc[c].y = fmaf(a[u][c].y, r, acc[c].y);
+        acc[c].z = fmaf(a[u][c].z, r, acc[c].z);
+        acc[c].w = fmaf(a[u][c].w, r, acc[c].w);
+      }
+    }
+  }
+  for (; m < m1; ++m) {
+    const float r = rsm[m - m0];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      if (!ok[c]) continue;
+      const float4 a = __ldg(Jb + (long long)m * n4 + base + c * kAdjThreads);
+      acc[c].x = fmaf(a.x, r, acc[c].x);
+      acc[c].y = fmaf(a.y, r, acc[c].y);
+      acc[c].z = fmaf(a.z, r, acc[c].z);
+      acc[c].w = fmaf(a.w, r, acc[c].w);
+    }
+  }
+  float4* out = reinterpret_cast<float4*>(partial + ((long long)b * rsplit + sp) * vp);
+#pragma unroll
+  for (int c = 0; c < 4; ++c)
+    if (ok[c]) out[base + c * kAdjThreads] = acc[c];
+}
+
 int jac_adj_partial(const float* J, long long jbs, const float* rs, int m, int vp, float* partial,
                     int rsplit, int batch, cudaStream_t st) {
   const int rows = cdiv(m, rsplit);
+  if (adj_wide()) {
+    dim3 gw(cdiv(vp, 4 * kAdjCols), rsplit, batch);
+    D2IP_CUDA(launch_pdl(jac_adj_wide_k, gw, kAdjThreads, rows * sizeof(float), st, J, jbs, rs, m, vp, partial, rsplit));
+    D2IP_LAUNCH_CHECK();
+    return D2IP_OK;
+  }
   dim3 grid(cdiv(vp, kAdjCols), rsplit, batch);
-  D2IP_CUDA(launch_pdl(jac_adj_k, grid, kAdjThreads, rows * sizeof(float), st, J, jbs, rs, m, vp, partial, rsplit));
+  if (adj_unroll() == 8)
+    D2IP_CUDA(launch_pdl(jac_adj_k<8>, grid, kAdjThreads, rows * sizeof(float), st, J, jbs, rs, m, vp, partial, rsplit));
+  else
+    D2IP_CUDA(launch_pdl(jac_adj_k<4>, grid, kAdjThreads, rows * sizeof(float), st, J, jbs, rs, m, vp, partial, rsplit));
   D2IP_LAUNCH_CHECK();
   return D2IP_OK;
 }

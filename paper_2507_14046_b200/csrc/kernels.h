@@ -99,9 +99,24 @@ int conv_tc_pack_multi(const PackJobs& jobs, int batch, cudaStream_t st);
 size_t conv_tc_ws_bytes(int D, int H, int W, int K, int N, int batch, int mode = 0);
 // deferred != null: a split-K result is left as partials in ws (*deferred =
 // kspl, 0 if not split) for the consumer to reduce (norm_act_fwd's `part`).
+// ChannelLayerNorm (+ residual) (+ LeakyReLU) fused into a convolution's epilogue
+// (priornet.py:96-108,145-148): out = act(gamma * (x - mean) * rstd + beta [+ res]), with
+// xhat [b][V][C] and rstd [b][V] saved for the backward -- norm_act_fwd's contract.
+struct LnFuse {
+  const float* gamma = nullptr;
+  const float* beta = nullptr;
+  long long pbs = 0;
+  d2ip_act res{};
+  d2ip_act out{};
+  float* xhat = nullptr;
+  float* rstd = nullptr;
+  int act = 1;
+  float slope = 0.2f;
+};
+
 int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, long long bbs, d2ip_act y,
                 int accumulate, float* ws, size_t ws_bytes, int batch, cudaStream_t st, int* deferred = nullptr,
-                int mode = 0);
+                int mode = 0, const LnFuse* ln = nullptr, int* fused = nullptr);
 
 // Split-K partial sums handed from a convolution to its consumer:
 // y[v][n] = bias[n] + sum_k part[b][k][v][n].

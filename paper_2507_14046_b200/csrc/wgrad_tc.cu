@@ -464,14 +464,19 @@ __global__ void __launch_bounds__(256) wgrad_tc_reduce_k(const float* __restrict
   const long long e = (long long)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= n) return;
   const float* p = part + (long long)b * nrg * n + e;
-  float s0 = 0.f, s1 = 0.f;
+  // four interleaved partial sums, four loads in flight (fixed order: row group r -> sum r % 4)
+  float s0 = 0.f, s1 = 0.f, s2 = 0.f, s3 = 0.f;
   int r = 0;
-  for (; r + 1 < nrg; r += 2) {
-    s0 += p[(long long)r * n];
-    s1 += p[(long long)(r + 1) * n];
+  for (; r + 3 < nrg; r += 4) {
+    const float a0 = __ldg(p + (long long)r * n), a1 = __ldg(p + (long long)(r + 1) * n);
+    const float a2 = __ldg(p + (long long)(r + 2) * n), a3 = __ldg(p + (long long)(r + 3) * n);
+    s0 += a0;
+    s1 += a1;
+    s2 += a2;
+    s3 += a3;
   }
-  if (r < nrg) s0 += p[(long long)r * n];
-  const float s = s0 + s1;
+  for (; r < nrg; ++r) s0 += __ldg(p + (long long)r * n);
+  const float s = (s0 + s1) + (s2 + s3);
   long long o;
   if (e < nw) {
     const int co = (int)(e % Cout);
