@@ -670,15 +670,40 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
       // B: nt^2 taps x NKC chunks, each a contiguous run of Ns 16-byte rows; one warp per run
       // (16-byte rows: 4 floats, or 8 bf16 = 4 float slots of the pack buffer)
       uint8_t* Bt = A + NH * Ab;
-      const float* wk = wpb + ((long long)(kd * 9) * kc_all + cb * NKC) * a.Np * 4 + (long long)n0 * 4;
       const int gwarp = gtid >> 5;
-      for (int q = gwarp; q < ntap * NKC; q += GT / 32) {
+      if (KWF) {
+        // kw-folded layout [kd kh][K/4][kw][Np][4]: per kh the stage's B tile is NKC x 3 x Np
+        // contiguous 16-byte rows. One slice of all N: three bulk copies per operand half,
+        // completing on the stage barrier by byte count; else 16-byte async copies per row
+        const float* wkd = wpb + (long long)(kd * 3) * kc_all * 3 * a.Np * 4;
+        if (Ns == a.Np) {
+          if (gtid == 0) {
+            const uint32_t run = (uint32_t)NKC * 3 * Ns * 16;
+            tc::mbar_expect_tx_only(&full[slot], 3 * NH * run);
+            for (int kh = 0; kh < 3; ++kh) {
+              const float* src = wkd + ((long long)kh * kc_all + cb * NKC) * 3 * a.Np * 4;
+              tc::bulk_load(Bt + (size_t)kh * run, src, run, &full[slot]);
+              if (NH == 2) tc::bulk_load(Bt + Bb + (size_t)kh * run, src + a.wlo, run, &full[slot]);
+            }
+          }
+        } else {
+          for (int q = gwarp; q < 9 * NKC; q += GT / 32) {  // q = (kh, kcl, kw)
+            const int kw = q % 3, kcl = (q / 3) % NKC, kh = q / (3 * NKC);
+            const float* src = wkd + ((((long long)kh * kc_all + cb * NKC + kcl) * 3 + kw) * a.Np + n0) * 4;
+            uint8_t* dst = Bt + ((size_t)(kh * NKC + kcl) * 3 * Ns + kw * Ns) * 16;
+            for (int n = lane; n < Ns; n += 32) {
+              tc::cp_async16(dst + n * 16, src + n * 4, 16u);
+              if (NH == 2) tc::cp_async16(dst + Bb + n * 16, src + a.wlo + n * 4, 16u);
+            }
+          }
+        }
+      }
+      const float* wk = wpb + ((long long)(kd * 9) * kc_all + cb * NKC) * a.Np * 4 + (long long)n0 * 4;
+      for (int q = gwarp; q < (KWF ? 0 : ntap * NKC); q += GT / 32) {
         const int tq = q / NKC, kcl = q % NKC;
         const int t9 = PW ? 0 : tap9(tq);
         const float* src = wk + ((long long)t9 * kc_all + kcl) * a.Np * 4;
-        // KWF: [kh][chunk][kw][Ns] -- the three kw taps of a K chunk are one N = 3 Ns run
-        uint8_t* dst = KWF ? Bt + ((size_t)((t9 / 3) * NKC + kcl) * 3 * Ns + (t9 % 3) * Ns) * 16
-                           : Bt + (size_t)q * Ns * 16;
+        uint8_t* dst = Bt + (size_t)q * Ns * 16;
         for (int n = lane; n < Ns; n += 32) {
           tc::cp_async16(dst + n * 16, src + n * 4, 16u);
           if (NH == 2) tc::cp_async16(dst + Bb + n * 16, src + a.wlo + n * 4, 16u);
@@ -960,15 +985,40 @@ __global__ void __launch_bounds__(kTcpThreads) conv_tcp_k(TcConv a) {
       // B: nt^2 taps x NKC chunks, each a contiguous run of Ns 16-byte rows; one warp per run
       // (16-byte rows: 4 floats, or 8 bf16 = 4 float slots of the pack buffer)
       uint8_t* Bt = A + NH * Ab;
-      const float* wk = wpb + ((long long)(kd * 9) * kc_all + cb * NKC) * a.Np * 4 + (long long)n0 * 4;
       const int gwarp = gtid >> 5;
-      for (int q = gwarp; q < ntap * NKC; q += GT / 32) {
+      if (KWF) {
+        // kw-folded layout [kd kh][K/4][kw][Np][4]: per kh the stage's B tile is NKC x 3 x Np
+        // contiguous 16-byte rows. One slice of all N: three bulk copies per operand half,
+        // completing on the stage barrier by byte count; else 16-byte async copies per row
+        const float* wkd = wpb + (long long)(kd * 3) * kc_all * 3 * a.Np * 4;
+        if (Ns == a.Np) {
+          if (gtid == 0) {
+            const uint32_t run = (uint32_t)NKC * 3 * Ns * 16;
+            tc::mbar_expect_tx_only(&full[slot], 3 * NH * run);
+            for (int kh = 0; kh < 3; ++kh) {
+              const float* src = wkd + ((long long)kh * kc_all + cb * NKC) * 3 * a.Np * 4;
+              tc::bulk_load(Bt + (size_t)kh * run, src, run, &full[slot]);
+              if (NH == 2) tc::bulk_load(Bt + Bb + (size_t)kh * run, src + a.wlo, run, &full[slot]);
+            }
+          }
+        } else {
+          for (int q = gwarp; q < 9 * NKC; q += GT / 32) {  // q = (kh, kcl, kw)
+            const int kw = q % 3, kcl = (q / 3) % NKC, kh = q / (3 * NKC);
+            const float* src = wkd + ((((long long)kh * kc_all + cb * NKC + kcl) * 3 + kw) * a.Np + n0) * 4;
+            uint8_t* dst = Bt + ((size_t)(kh * NKC + kcl) * 3 * Ns + kw * Ns) * 16;
+            for (int n = lane; n < Ns; n += 32) {
+              tc::cp_async16(dst + n * 16, src + n * 4, 16u);
+              if (NH == 2) tc::cp_async16(dst + Bb + n * 16, src + a.wlo + n * 4, 16u);
+            }
+          }
+        }
+      }
+      const float* wk = wpb + ((long long)(kd * 9) * kc_all + cb * NKC) * a.Np * 4 + (long long)n0 * 4;
+      for (int q = gwarp; q < (KWF ? 0 : ntap * NKC); q += GT / 32) {
         const int tq = q / NKC, kcl = q % NKC;
         const int t9 = PW ? 0 : tap9(tq);
         const float* src = wk + ((long long)t9 * kc_all + kcl) * a.Np * 4;
-        // KWF: [kh][chunk][kw][Ns] -- the three kw taps of a K chunk are one N = 3 Ns run
-        uint8_t* dst = KWF ? Bt + ((size_t)((t9 / 3) * NKC + kcl) * 3 * Ns + (t9 % 3) * Ns) * 16
-                           : Bt + (size_t)q * Ns * 16;
+        uint8_t* dst = Bt + (size_t)q * Ns * 16;
         for (int n = lane; n < Ns; n += 32) {
           tc::cp_async16(dst + n * 16, src + n * 4, 16u);
           if (NH == 2) tc::cp_async16(dst + Bb + n * 16, src + a.wlo + n * 4, 16u);
@@ -1219,9 +1269,17 @@ __global__ void conv_tc_pack_k(const float* __restrict__ w, long long wbs, int K
   const int j = (int)(i & 3);
   const long long q = i >> 2;
   const int n = (int)(q % Np);
-  const long long q2 = q / Np;
-  const int kc = (int)(q2 % (K / 4));
-  const int t = (int)(q2 / (K / 4));
+  long long q2 = q / Np;
+  int kc, t;
+  if (dgrad & kTcKwf) {  // [kd kh][K/4][kw][Np][4]
+    const int kw = (int)(q2 % 3);
+    q2 /= 3;
+    kc = (int)(q2 % (K / 4));
+    t = (int)(q2 / (K / 4)) * 3 + kw;
+  } else {
+    kc = (int)(q2 % (K / 4));
+    t = (int)(q2 / (K / 4));
+  }
   const int k = 4 * kc + j;
   const float val = n < N ? pack_val(w + b * wbs, K, N, dgrad, t, k, n) : 0.f;
   const float hi = tf32_hi(val);
@@ -1242,7 +1300,9 @@ __device__ __forceinline__ void pack_put(float* out, long long obs, int code, in
     reinterpret_cast<__nv_bfloat16*>(out)[i] = h;
     if (code & kTcBf3) reinterpret_cast<__nv_bfloat16*>(out + obs / 2)[i] = __float2bfloat16_rn(val - __bfloat162float(h));
   } else {
-    const long long i = (((long long)t * (K / 4) + k / 4) * Np + n) * 4 + (k & 3);
+    // kw-folded layers: [kd kh][K/4][kw][Np][4]; otherwise [tap][K/4][Np][4]
+    const long long i = (code & kTcKwf) ? ((((long long)(t / 3) * (K / 4) + k / 4) * 3 + t % 3) * Np + n) * 4 + (k & 3)
+                                        : (((long long)t * (K / 4) + k / 4) * Np + n) * 4 + (k & 3);
     const float hi = tf32_hi(val);
     out[i] = hi;
     out[obs / 2 + i] = val - hi;
@@ -1327,6 +1387,15 @@ bool conv_tc_supported(int cin, int cout, int ks, int stride, int precision) {
   return true;
 }
 
+// kw-folded stride-1 kernel (MODE 4): D2IP_TC_KWF=0 keeps one MMA per tap
+static bool kwf_enabled() {
+  static const bool on = [] {
+    const char* v = getenv("D2IP_TC_KWF");
+    return !v || atoi(v) != 0;
+  }();
+  return on;
+}
+
 bool tf32_bf3_enabled() {
   static const bool on = [] {
     const char* v = getenv("D2IP_TF32_BF3");
@@ -1387,6 +1456,11 @@ bool conv_tc_layer(int cin, int cout, int ks, int stride, int dgrad, int precisi
         bf3_class(ks == 1 ? 16 : dgrad ? 2 : 1) && (!only_k || (only_k == r.K && ks == 3 && !dgrad))) {
       r.mode |= kTcBf3;
       r.pack |= kTcBf3;
+    }
+    // 3xTF32 stride-1 3^3 layers run kw-folded (MODE 4) with its weight layout
+    if (ks == 3 && !(r.mode & (kTcBf16 | kTcBf3)) && kwf_enabled()) {
+      r.mode |= kTcKwf;
+      r.pack |= kTcKwf;
     }
   } else {
     // Below ~4M output-voxel x channel-pair products the direct CUDA-core kernel
@@ -1527,22 +1601,13 @@ static bool tc_plan(int D, int H, int W, int K, int N, int batch, TcConv& a, int
   return true;
 }
 
-// kw-folded stride-1 kernel (MODE 4): D2IP_TC_KWF=0 keeps one MMA per tap
-static bool kwf_enabled() {
-  static const bool on = [] {
-    const char* v = getenv("D2IP_TC_KWF");
-    return !v || atoi(v) != 0;
-  }();
-  return on;
-}
-
 size_t conv_tc_ws_bytes(int D, int H, int W, int K, int N, int batch, int mode) {
   TcConv a{};
   int tiles;
   const int m3 = mode & 3;
   size_t best = 0;
   // the larger of the two plans (kw-folded or not) a stride-1 call may take
-  for (int kwf = 0; kwf <= (m3 == 0 && kwf_enabled() && !(mode & (kTcBf16 | kTcBf3)) ? 1 : 0); ++kwf) {
+  for (int kwf = (mode & kTcKwf) ? 1 : 0; kwf <= ((mode & kTcKwf) ? 1 : 0); ++kwf) {
     if (!tc_plan(D, H, W, K, N, batch, a, &tiles, m3 == 3 ? 1 : m3 ? 2 : 3, (mode & kTcBf16) != 0, false,
                  (mode & kTcBf3) != 0, kwf != 0) ||
         a.kspl <= 1)
@@ -1681,6 +1746,7 @@ int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, lo
   if (fused) *fused = 0;
   const bool b3 = (mode & kTcBf3) != 0;
   const bool bf = b3 || (mode & kTcBf16) != 0;
+  const bool kwf_bit = (mode & kTcKwf) != 0;  // the weights were packed for the kw-folded kernel
   mode &= 3;
   D2IP_CHECK_ARG(!bf || K % 16 == 0, "conv_tc: bf16 needs K %% 16 == 0 (K=%d)", K);
   D2IP_CHECK_ARG((mode == 1 ? 8 * x.c : x.c) == K && (mode == 2 ? 8 * y.c : y.c) == N, "conv_tc: channel mismatch");
@@ -1709,14 +1775,15 @@ int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, lo
   // the width. 3xTF32 layers only: on cfg4's 3xbf16 forwards (large grids, T = 4 tiles) it
   // measured slower (122.7 vs 127.9 it/s); not for the TMA / persistent bf16 kernels
   bool kwf = false;
-  if (mode == 0 && !use_tma && kwf_enabled() && !bf) {
+  if (kwf_bit) {
+    D2IP_CHECK_ARG(mode == 0 && !use_tma && !bf, "conv_tc: kw-folded packing on a layer that cannot run it");
     TcConv k2{};
     int tiles2 = 0;
-    if (tc_plan(g.d, g.h, g.w, K, N, batch, k2, &tiles2, ntm, bf, false, b3, true)) {
-      a = k2;
-      tiles = tiles2;
-      kwf = true;
-    }
+    D2IP_CHECK_ARG(tc_plan(g.d, g.h, g.w, K, N, batch, k2, &tiles2, ntm, bf, false, b3, true),
+                   "conv_tc: no kw-folded plan fits (K=%d N=%d W=%d)", K, N, g.w);
+    a = k2;
+    tiles = tiles2;
+    kwf = true;
   }
   a.mode = kwf ? 4 : mode;
   a.t0 = mode == 2 ? 1 : 0;

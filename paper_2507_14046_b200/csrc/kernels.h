@@ -69,6 +69,8 @@ bool conv_tc_supported(int cin, int cout, int ks, int stride, int precision);
 // both carry kTcBf16 when the layer runs with bf16 operands (kind::f16).
 constexpr int kTcBf16 = 4;
 constexpr int kTcPw = 8;  // pack code: 1^3 weights (mode 3)
+constexpr int kTcKwf = 32;  // mode / pack code: stride-1 3^3 with the kw taps folded into N (MODE 4);
+                            // pack layout [kd kh][K/4][kw][Np][4] so a stage's B tile per kh is contiguous
 constexpr int kTcBf3 = 16;  // mode / pack code: TF32-precision layer on 3xbf16 (hi + lo split) kind::f16 MMAs
 // TF32-precision layers run 3xbf16 tensor-core kernels (D2IP_TF32_BF3=0: 3xTF32)
 bool tf32_bf3_enabled();
