@@ -56,6 +56,7 @@
 // them to that stage's mbarrier, which gates the refill of the buffer.
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 
 #include <cuda.h>
 #include <cudaTypedefs.h>
@@ -103,6 +104,7 @@ struct TcConv {
   int async_arrive;  // bf16 twin path: stages complete by cp.async.mbarrier.arrive (D2IP_TC_ASYNC)
   int dbg;           // D2IP_TC_DBG=1: producers skip the fills (MMA-side timing only)
   int ntiles;        // persistent kernel: tiles (blocks of T x 128 rows) of the grid
+  int tma;           // MODE 4, 3xTF32: the hi window lines arrive by TMA (tensor map = the kernel's tmap)
   int ln;            // MODE 4, one N slice, no split-K: LayerNorm (+ residual) (+ act) in the epilogue
   LnFuse lnf;
 };
@@ -116,7 +118,7 @@ static size_t stage_bytes(int cb, int np, int wrp, int nt = 3, bool bf = false, 
 }
 
 static size_t tc_smem_bytes(const TcConv& a) {
-  return (size_t)a.nst * stage_bytes(a.CB, a.Ns, a.WRp, a.nt, a.bf, a.b3) + 3 * a.WR * sizeof(int) + 8 + 7 * 8 + 16;
+  return (size_t)a.nst * stage_bytes(a.CB, a.Ns, a.WRp, a.nt, a.bf, a.b3) + 3 * a.WR * sizeof(int) + 8 + 10 * 8 + 16;
 }
 
 __device__ __forceinline__ uint32_t bf2(float a, float b) {
@@ -425,7 +427,7 @@ __device__ __forceinline__ void tc_epilogue_kwf(const TcConv& a, uint32_t tmem, 
 // BFM: 0 3xTF32, 1 bf16, 2 3xbf16 (x = hi + lo in bf16, hi*hi + hi*lo + lo*hi on kind::f16:
 // ~2^-16 per product, for the TF32-precision configs at half the MMAs of 3xTF32)
 template <int NKC, int T, int PG, int MODE, int BFM = 0>
-__global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
+__global__ void __launch_bounds__(kTcThreads) conv_tc_k(const TcConv a, const __grid_constant__ CUtensorMap tmap) {
   constexpr bool BF = BFM != 0, B3 = BFM == 2;
   D2IP_PDL_ENTRY();
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -451,13 +453,15 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
   uint64_t* full = reinterpret_cast<uint64_t*>(rowmap + 3 * WR + ((3 * WR) & 1));
   uint64_t* empty = full + 3;
   uint64_t* done = empty + 3;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
+  uint64_t* landed = done + 1;  // TMA path: the stage's hi window + weights have landed
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(landed + 3);
 
   if (warp == 0) tc::tmem_alloc(tslot, a.tmem_cols);
   if (tid == 0) {
     for (int i = 0; i < NST; ++i) {
       tc::mbar_init(&full[i], kTcProd / PG);  // one producer group fills a stage
       tc::mbar_init(&empty[i], 1);
+      tc::mbar_init(&landed[i], 1);
     }
     tc::mbar_init(done, 1);
     tc::fence_mbar_init();
@@ -511,6 +515,13 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
         if (BF) tc::fence_proxy_async();
         const uint64_t boff = (uint64_t)slot * (Sb >> 4);
         if (KWF) {
+          // TMA windows start `pre` rows into their first padded line
+          int pre = 0;
+          if (a.tma) {
+            const int sg = s_lo + s, kdi = sg / a.n_cb;
+            const int uws = u0 + (kdi - 1) * a.Sh - a.Sw - 1;
+            pre = uws - (uws / a.Sw) * a.Sw;
+          }
           // one N = 3 Ns MMA per (kh, K step): B = the kh row's three kw taps side by side
           for (int kh = 0; kh < 3; ++kh) {
 #pragma unroll
@@ -519,7 +530,7 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
               const uint32_t first = (s | kh | j) ? 1u : 0u;
 #pragma unroll
               for (int tt = 0; tt < T; ++tt) {
-                const uint64_t ao = boff + (uint64_t)(2 * j * WRp + kh * a.Sw + tt * RS);
+                const uint64_t ao = boff + (uint64_t)(2 * j * WRp + pre + kh * a.Sw + tt * RS);
                 const uint32_t d = tmem + (uint32_t)(tt * 3 * Ns);
                 if (B3) {
                   tc::mma_f16(d, dAlo + ao, dBhi + bo, a.idesc, first);
@@ -584,6 +595,49 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(TcConv a) {
       const int kd = PW ? 0 : t0 + kdi;
       const int* rm = rowmap + kd * WR;
       uint8_t* A = smem + slot * Sb;
+      if (KWF && !BF && a.tma) {
+        // TMA-staged window: warp 1 issues one 5-D box (4 channels x Sw columns from w = -1, one
+        // padded line) per (line, 16-byte channel chunk) -- the zero halo is the boxes'
+        // out-of-bounds fill -- and the weight tile as three bulk runs per operand half, all
+        // completing on landed[slot] by byte count; then every producer thread forms the lo
+        // half of its share of the landed window (x - tf32(x)) and arrives on full[slot]
+        const int uws = u0 + (kdi - 1) * a.Sh - a.Sw - 1;
+        const int L0 = uws / a.Sw, pre = uws - L0 * a.Sw;
+        const int nl = (pre + WR + a.Sw - 1) / a.Sw;
+        const int Hl = a.gh + 2;
+        const int lrows = nl * a.Sw;
+        uint8_t* Bt = A + NH * Ab;
+        const uint32_t run = (uint32_t)NKC * 3 * Ns * 16;
+        if (warp == 1) {
+          if (lane == 0) tc::mbar_expect_tx(&landed[slot], (uint32_t)(NKC * lrows * 16) + 3 * NH * run);
+          __syncwarp();
+          for (int i = lane; i < NKC * nl; i += 32) {
+            const int kc = i / nl, li = i - kc * nl;
+            const int L = L0 + li, dp = L / Hl, hp = L - dp * Hl;
+            tc::tma_load_5d(A + ((size_t)kc * WRp + (size_t)li * a.Sw) * 16, &tmap, cb * CB + 4 * kc, -1, hp - 1,
+                            dp - 1, b, &landed[slot]);
+          }
+          if (lane == 0) {
+            const float* wkd = wpb + (long long)(kd * 3) * kc_all * 3 * a.Np * 4;
+            for (int kh = 0; kh < 3; ++kh) {
+              const float* src = wkd + ((long long)kh * kc_all + cb * NKC) * 3 * a.Np * 4;
+              tc::bulk_load(Bt + (size_t)kh * run, src, run, &landed[slot]);
+              tc::bulk_load(Bt + Bb + (size_t)kh * run, src + a.wlo, run, &landed[slot]);
+            }
+          }
+        }
+        tc::mbar_wait(&landed[slot], (uint32_t)((s / NST) & 1));
+        for (int i = gtid; i < NKC * lrows; i += GT) {
+          const int kc = i / lrows, r = i - kc * lrows;
+          const float4 v = *reinterpret_cast<const float4*>(A + ((size_t)kc * WRp + r) * 16);
+          float4 l;
+          l.x = v.x - tf32_hi(v.x); l.y = v.y - tf32_hi(v.y); l.z = v.z - tf32_hi(v.z); l.w = v.w - tf32_hi(v.w);
+          *reinterpret_cast<float4*>(A + Ab + ((size_t)kc * WRp + r) * 16) = l;
+        }
+        tc::fence_proxy_async();
+        tc::mbar_arrive(&full[slot]);
+        continue;
+      }
       if (BF && !B3 && a.xtw) {
         // bf16 twin of x: one 16-byte async copy per (row, 8-channel chunk); zero-fill for padding rows
         const uint16_t* xt = reinterpret_cast<const uint16_t*>(x.bf16) + b * x.bstride;
@@ -1620,6 +1674,9 @@ size_t conv_tc_ws_bytes(int D, int H, int W, int K, int N, int batch, int mode) 
 
 
 // Launch one instantiation (the >48 KB shared-memory opt-in is set on first use).
+// the window tensor map of the current conv_tc_run call (MODE 4 TMA path; zeros otherwise)
+static thread_local CUtensorMap g_tc_tmap;
+
 template <int NKC, int T, int PG, int MODE, int BF>
 static int tc_launch(const TcConv& a, dim3 grid, size_t smem, cudaStream_t st) {
   static bool attr = false;
@@ -1628,7 +1685,7 @@ static int tc_launch(const TcConv& a, dim3 grid, size_t smem, cudaStream_t st) {
                                    227 * 1024));
     attr = true;
   }
-  D2IP_CUDA(launch_pdl((conv_tc_k<NKC, T, PG, MODE, BF>), grid, kTcThreads, smem, st, a));
+  D2IP_CUDA(launch_pdl((conv_tc_k<NKC, T, PG, MODE, BF>), grid, kTcThreads, smem, st, a, g_tc_tmap));
   return D2IP_OK;
 }
 
@@ -1785,7 +1842,52 @@ int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, lo
     tiles = tiles2;
     kwf = true;
   }
+  // TMA-staged windows for the kw-folded 3xTF32 kernel (D2IP_TC_TMA3=1; one N slice, 16-byte
+  // aligned channel views): one 5-D box per (padded line, 4-channel chunk), the zero halo from the
+  // boxes' out-of-bounds fill, then the lo split in shared memory. Correct (tests/test_gpu_ops.py
+  // with the knob) but measured slower than the cp.async fill -- the 8-row (128-byte) aligned line
+  // pitch adds 18 % virtual rows at W = 32, and the landing -> split -> arrive chain serialises each
+  // stage: 48->16 @ 64x64x32 fwd 147 vs 123 us, dgrad 106 vs 70; cfg1 1,079 vs 1,134 it/s. Opt-in.
+  static const bool tma3_on = [] {
+    const char* v = getenv("D2IP_TC_TMA3");
+    return v && atoi(v) != 0;
+  }();
+  bool tma3 = false;
+  memset(&g_tc_tmap, 0, sizeof(g_tc_tmap));
+  if (kwf && tma3_on && x.c % 4 == 0 && x.cstride % 4 == 0 && ((uintptr_t)x.ptr & 15) == 0 && x.w + 2 <= 256 &&
+      (x.bstride * 4) % 16 == 0) {
+    TcConv k3{};
+    int tiles3 = 0;
+    if (tc_plan(g.d, g.h, g.w, K, N, batch, k3, &tiles3, ntm, false, true, false, true) && k3.Ns == k3.Np) {
+      static PFN_cuTensorMapEncodeTiled_v12000 encode3 = [] {
+        void* fn = nullptr;
+        cudaDriverEntryPointQueryResult q;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) != cudaSuccess ||
+            q != cudaDriverEntryPointSuccess)
+          fn = nullptr;
+        return reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+      }();
+      if (encode3) {
+        const cuuint64_t gdim[5] = {(cuuint64_t)x.c, (cuuint64_t)x.w, (cuuint64_t)x.h, (cuuint64_t)x.d,
+                                    (cuuint64_t)batch};
+        const cuuint64_t gstr[4] = {(cuuint64_t)x.cstride * 4, (cuuint64_t)x.w * x.cstride * 4,
+                                    (cuuint64_t)x.h * x.w * x.cstride * 4, (cuuint64_t)x.bstride * 4};
+        const cuuint32_t box[5] = {4, (cuuint32_t)k3.Sw, 1, 1, 1}, estr[5] = {1, 1, 1, 1, 1};
+        const CUresult cr = encode3(&g_tc_tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 5, x.ptr, gdim, gstr, box, estr,
+                                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE,
+                                    CU_TENSOR_MAP_L2_PROMOTION_L2_128B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+        if (cr == CUDA_SUCCESS) {
+          a = k3;
+          tiles = tiles3;
+          tma3 = true;
+        } else {
+          memset(&g_tc_tmap, 0, sizeof(g_tc_tmap));
+        }
+      }
+    }
+  }
   a.mode = kwf ? 4 : mode;
+  a.tma = tma3 ? 1 : 0;
   a.t0 = mode == 2 ? 1 : 0;
   a.nt = ntm;
   a.gd = g.d;
@@ -1936,8 +2038,8 @@ int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, lo
     D2IP_LAUNCH_CHECK();
   }
   if (kwf) {
-    set_variant(b3 ? (a.kspl > 1 ? "tcgen05_bf16x3_kwf_splitk" : "tcgen05_bf16x3_kwf")
-                   : (a.kspl > 1 ? "tcgen05_tf32x3_kwf_splitk" : "tcgen05_tf32x3_kwf"));
+    set_variant(tma3 ? (a.kspl > 1 ? "tcgen05_tf32x3_kwf_tma_splitk" : "tcgen05_tf32x3_kwf_tma")
+                     : (a.kspl > 1 ? "tcgen05_tf32x3_kwf_splitk" : "tcgen05_tf32x3_kwf"));
     return D2IP_OK;
   }
   set_variant(b3 ? (a.kspl > 1 ? "tcgen05_bf16x3_splitk" : "tcgen05_bf16x3")

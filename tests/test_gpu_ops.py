@@ -329,7 +329,8 @@ def test_adam_matches_torch():
     assert rel(pd.cpu(), p.detach()) < 1e-6
 
 
-@pytest.mark.parametrize("knob,prefix,cin,prec", [("D2IP_TC_TMA", "tcgen05_bf16_tma", 32, "bf16"),
+@pytest.mark.parametrize("knob,prefix,cin,prec", [("D2IP_TC_TMA3", "tcgen05_tf32x3_kwf_tma", 32, "tf32"),
+                                                  ("D2IP_TC_TMA", "tcgen05_bf16_tma", 32, "bf16"),
                                                   ("D2IP_TC_PERSIST", "tcgen05_bf16_persistent", 32, "bf16"),
                                                   ("D2IP_TC_PERSIST", "tcgen05_bf16x3_persistent", 32, "tf32")])
 def test_conv_optin_variant_subprocess(knob, prefix, cin, prec):
@@ -367,8 +368,9 @@ print(L.d2ip_last_variant().decode(), float((out - ref).norm() / ref.norm()))
     code = code.replace("@CIN@", str(cin)).replace("@SPATIAL@", str(spatial)).replace("@PREC@", repr(prec))
     # single-pass bf16 forwards (D2IP_BF16_FWD3=0) and 3xbf16 stride-1 forwards (D2IP_BF3_MASK=31)
     # are the variants these kernels implement; the defaults route those layers elsewhere
-    env = dict(os.environ, **{knob: "2" if knob == "D2IP_TC_PERSIST" else "1"}, D2IP_BF16_FWD3="0",
-               D2IP_BF3_MASK="31", D2IP_TF32_BF3="1", D2IP_TC_KWF="0")
+    env = dict(os.environ, **{knob: "2" if knob == "D2IP_TC_PERSIST" else "1"})
+    if knob != "D2IP_TC_TMA3":
+        env.update(D2IP_BF16_FWD3="0", D2IP_BF3_MASK="31", D2IP_TF32_BF3="1", D2IP_TC_KWF="0")
     r = subprocess.run([sys.executable, "-c", code], env=env, capture_output=True, text=True, timeout=600,
                        cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
     assert r.returncode == 0, r.stderr[-2000:]
