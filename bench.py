@@ -408,6 +408,8 @@ def run_gpu(args):
         del dn
         torch.cuda.empty_cache()
         e2e = run_e2e_joint(spec, args)
+    if not args.skip_e2e and spec.sequences > 1:
+        e2e = run_e2e_batched(spec, args, ws, rank)
     if not args.skip_e2e and units_per_step == 1 and wl is not None and args.net == "config":
         e2e = run_e2e(spec, wl, args, ws)
         if ws > 1:  # replicas: all ranks' iterations over the slowest rank's wall time
@@ -672,6 +674,51 @@ def run_e2e_joint(spec, args):
                     f"{frames} frames"}
 
 
+def run_e2e_batched(spec, args, ws, rank):
+    """cfg3 end to end through `reconstruct_sequences_batched` on host inputs: all the
+    independent sequences (sharded over the ranks, one batched engine per rank, gathered on
+    rank 0), bounded to --e2e-frames-batched frames and a --e2e-warm-batched warm start so the
+    call stays short; uploads and read-backs inside the timed region. Time = max over ranks."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2507_14046_b200 import reconstruct_sequences_batched
+    from paper_2507_14046_b200 import workloads as W
+    from paper_2507_14046_b200.distributed import shard
+
+    frames = min(spec.frames, args.e2e_frames_batched)
+    seeds = list(range(spec.sequences))
+    mine = set(shard(len(seeds), ws, rank))
+    wls = [W.make_workload(spec, seed=s, frames=frames) if s in mine else None for s in seeds]
+    proto = next(w for w in wls if w is not None)
+    # the non-local sequences are never touched on this rank: stand-ins with the same shapes
+    mats = [w.matrix if w is not None else proto.matrix for w in wls]
+    volts = [w.voltages if w is not None else proto.voltages for w in wls]
+    cfg = W.run_config_for(spec, proto.output_map, seed=0, precision=args.precision or spec.precision,
+                           iters_warm=min(spec.iters_warm, args.e2e_warm_batched))
+    torch.cuda.synchronize()
+    if ws > 1:
+        dist.barrier()
+    t0 = time.perf_counter()
+    res = reconstruct_sequences_batched(mats, volts, cfg, proto.grid, seeds=seeds)
+    torch.cuda.synchronize()
+    secs = time.perf_counter() - t0
+    if ws > 1:
+        t = torch.tensor([secs], dtype=torch.float64, device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        secs = float(t)
+    per_seq = cfg.iters_warm + cfg.iters_first + (frames - 1) * cfg.iters_next
+    iters = per_seq * len(seeds)
+    Q = int(np.prod(proto.grid.shape))
+    h2d = len(mine) * (proto.matrix.values.nbytes + 4 * Q * spec.in_channels + frames * 4 * proto.matrix.n_measurements)
+    d2h = len(mine) * frames * 8 * Q
+    return {"value": round(iters / secs, 2), "unit": "it/s", "h2d_bytes_per_step": int(h2d / (iters / ws)),
+            "d2h_bytes_per_step": int(d2h / (iters / ws)), "call": "reconstruct_sequences_batched",
+            "iterations": int(iters), "sequences": len(seeds), "frames": frames, "seconds": round(secs, 3),
+            "note": f"{len(seeds)} sequences x (warm {cfg.iters_warm} + {frames} frames x {cfg.iters_next}); the "
+                    f"50-frame, 2,000-iteration warm-start budget bounded for a short run"}
+
+
 def _oracle_runner(spec, wl):
     from oracle import OracleFrameOptimizer
     from oracle.resunet import kaiming_reset
@@ -812,6 +859,8 @@ def main():
     ap.add_argument("--e2e-frames", type=int, default=100)
     ap.add_argument("--e2e-warm", type=int, default=2000)
     ap.add_argument("--e2e-frames-joint", type=int, default=20)
+    ap.add_argument("--e2e-frames-batched", type=int, default=3)
+    ap.add_argument("--e2e-warm-batched", type=int, default=200)
     ap.add_argument("--launch-selftest", action="store_true", help=argparse.SUPPRESS)
     args = ap.parse_args()
     if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
