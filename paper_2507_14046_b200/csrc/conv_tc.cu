@@ -75,7 +75,13 @@ constexpr int kTcpThreads = 416;  // persistent kernel: MMA warp, 8 producer war
 
 __host__ __device__ static inline int np_of(int n) { return (n + 15) / 16 * 16; }
 static inline int wr_of(int sw, int T = 1) { return T * kTcRows + 2 * sw + 2; }
-static inline int wrp_of(int wr) { return wr + ((1 - wr) % 8 + 8) % 8; }  // = 1 mod 8: conflict-free fills
+// Rows per channel-chunk column, padded so a quarter warp of fill / split threads (16-byte
+// accesses, i -> (row i / NKC, chunk i % NKC)) covers all 32 banks: the column stride is
+// 16 * (8 / min(NKC, 8)) bytes mod 128 (NKC = 2: rows {r..r+3} x 2 columns 64 B apart, ...)
+static inline int wrp_of(int wr, int nkc) {
+  const int t = 8 / std::min(nkc, 8);
+  return wr + ((t - wr) % 8 + 8) % 8;
+}
 
 struct TcConv {
   d2ip_act x;
@@ -427,7 +433,8 @@ __device__ __forceinline__ void tc_epilogue_kwf(const TcConv& a, uint32_t tmem, 
 // BFM: 0 3xTF32, 1 bf16, 2 3xbf16 (x = hi + lo in bf16, hi*hi + hi*lo + lo*hi on kind::f16:
 // ~2^-16 per product, for the TF32-precision configs at half the MMAs of 3xTF32)
 template <int NKC, int T, int PG, int MODE, int BFM = 0>
-__global__ void __launch_bounds__(kTcThreads) conv_tc_k(const TcConv a, const __grid_constant__ CUtensorMap tmap) {
+__global__ void __launch_bounds__(kTcThreads, (MODE == 4 && T == 2 && BFM == 0) ? 2 : 0)
+    conv_tc_k(const TcConv a, const __grid_constant__ CUtensorMap tmap) {
   constexpr bool BF = BFM != 0, B3 = BFM == 2;
   D2IP_PDL_ENTRY();
   extern __shared__ __align__(1024) uint8_t smem[];
@@ -583,6 +590,122 @@ __global__ void __launch_bounds__(kTcThreads) conv_tc_k(const TcConv a, const __
     // the same 16-byte elements
     constexpr int GT = kTcProd / PG;
     const int pg = PG == 2 ? (warp - 1) >> 2 : 0, gtid = tid - 32 - pg * GT;
+    // 3xTF32, one producer group: software-pipelined ring. The copies of stage s + NST - 1 are
+    // issued before the landing of stage s + 1 is waited for (cp.async groups retire in order:
+    // wait_group NST - 2), so the L2 latency of a fill overlaps the lo split of the stage before
+    // it and the MMAs of the stage before that, instead of being paid once per stage. A thread
+    // copies and splits the same 16-byte elements, so no cross-thread sync sits between them.
+    if (!BF && PG == 1 && !a.tma && a.dbg == 0) {
+      const int gwarp = gtid >> 5;
+      auto fill = [&](int s) {
+        const int slot = s % NST;
+        if (s >= NST) tc::mbar_wait(&empty[slot], (uint32_t)(((s / NST) - 1) & 1));
+        const int sg = s_lo + s;
+        const int kdi = sg / a.n_cb, cb = sg - kdi * a.n_cb;
+        const int kd = PW ? 0 : t0 + kdi;
+        const int* rm = rowmap + kd * WR;
+        uint8_t* A = smem + slot * Sb;
+        const long long plane = (long long)x.h * x.w;
+        const float* xc = xb + cb * CB;
+        // four row-map entries, then four copies: the loads are independent of the asm copies
+        for (int i0 = gtid; i0 < nA; i0 += 4 * GT) {
+          int off[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int i = i0 + q * GT;
+            off[q] = i < nA ? rm[i / NKC] : -2;
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int i = i0 + q * GT;
+            if (off[q] == -2) continue;
+            const int r = i / NKC, kc = i % NKC;
+            const float* src = xb;
+            bool ok = off[q] >= 0;
+            if (MODE == 1) {
+              // parity gather: virtual channel c = p * C_x + ci reads input voxel 2o + p
+              const int c = cb * CB + 4 * kc, p = c / x.c, ci = c - p * x.c;
+              const int pd = p >> 2, ph = (p >> 1) & 1, pw = p & 1;
+              ok = ok && (!pd || (off[q] & 4)) && (!ph || (off[q] & 2)) && (!pw || (off[q] & 1));
+              if (ok) src = xb + ((off[q] >> 3) + pd * plane + ph * x.w + pw) * (long long)x.cstride + ci;
+            } else if (ok) {
+              src = xc + (long long)off[q] * x.cstride + 4 * kc;
+            }
+            tc::cp_async16(A + ((size_t)kc * WRp + r) * 16, src, ok ? 16u : 0u);
+          }
+        }
+        uint8_t* Bt = A + NH * Ab;
+        if (KWF) {
+          const float* wkd = wpb + (long long)(kd * 3) * kc_all * 3 * a.Np * 4;
+          if (Ns == a.Np) {
+            if (gtid == 0) {
+              const uint32_t run = (uint32_t)NKC * 3 * Ns * 16;
+              tc::mbar_expect_tx_only(&full[slot], 3 * NH * run);
+              for (int kh = 0; kh < 3; ++kh) {
+                const float* src = wkd + ((long long)kh * kc_all + cb * NKC) * 3 * a.Np * 4;
+                tc::bulk_load(Bt + (size_t)kh * run, src, run, &full[slot]);
+                tc::bulk_load(Bt + Bb + (size_t)kh * run, src + a.wlo, run, &full[slot]);
+              }
+            }
+          } else {
+            for (int q = gwarp; q < 9 * NKC; q += GT / 32) {  // q = (kh, kcl, kw)
+              const int kw = q % 3, kcl = (q / 3) % NKC, kh = q / (3 * NKC);
+              const float* src = wkd + ((((long long)kh * kc_all + cb * NKC + kcl) * 3 + kw) * a.Np + n0) * 4;
+              uint8_t* dst = Bt + ((size_t)(kh * NKC + kcl) * 3 * Ns + kw * Ns) * 16;
+              for (int n = lane; n < Ns; n += 32) {
+                tc::cp_async16(dst + n * 16, src + n * 4, 16u);
+                tc::cp_async16(dst + Bb + n * 16, src + a.wlo + n * 4, 16u);
+              }
+            }
+          }
+        } else {
+          const float* wk = wpb + ((long long)(kd * 9) * kc_all + cb * NKC) * a.Np * 4 + (long long)n0 * 4;
+          for (int q = gwarp; q < ntap * NKC; q += GT / 32) {
+            const int tq = q / NKC, kcl = q % NKC;
+            const int t9 = PW ? 0 : tap9(tq);
+            const float* src = wk + ((long long)t9 * kc_all + kcl) * a.Np * 4;
+            uint8_t* dst = Bt + (size_t)q * Ns * 16;
+            for (int n = lane; n < Ns; n += 32) {
+              tc::cp_async16(dst + n * 16, src + n * 4, 16u);
+              tc::cp_async16(dst + Bb + n * 16, src + a.wlo + n * 4, 16u);
+            }
+          }
+        }
+        tc::cp_async_commit();
+      };
+      const int LA = NST - 1;  // stages in flight ahead of the one being split
+      for (int s = 0; s < LA && s < S; ++s) fill(s);
+      for (int s = 0; s < S; ++s) {
+        if (LA >= 2 && s + 1 < S)
+          tc::cp_async_wait<1>();
+        else
+          tc::cp_async_wait<0>();
+        // lo half of the landed activation window; the raw fp32 window is the hi operand
+        // (the tensor core truncates fp32 to TF32: tools/tf32_round_probe.cu)
+        const int slot = s % NST;
+        uint8_t* A = smem + slot * Sb;
+        for (int i0 = gtid; i0 < nA; i0 += 4 * GT) {
+          float4 v[4];
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int i = i0 + q * GT;
+            if (i < nA) v[q] = *reinterpret_cast<const float4*>(A + ((size_t)(i % NKC) * WRp + i / NKC) * 16);
+          }
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int i = i0 + q * GT;
+            if (i >= nA) continue;
+            float4 l;
+            l.x = v[q].x - tf32_hi(v[q].x); l.y = v[q].y - tf32_hi(v[q].y);
+            l.z = v[q].z - tf32_hi(v[q].z); l.w = v[q].w - tf32_hi(v[q].w);
+            *reinterpret_cast<float4*>(A + Ab + ((size_t)(i % NKC) * WRp + i / NKC) * 16) = l;
+          }
+        }
+        tc::fence_proxy_async();
+        tc::mbar_arrive(&full[slot]);
+        if (s + LA < S) fill(s + LA);
+      }
+    } else
     for (int s = pg; s < S; s += PG) {
       const int slot = s % NST;
       if (s >= NST) tc::mbar_wait(&empty[slot], (uint32_t)(((s / NST) - 1) & 1));
@@ -1570,7 +1693,7 @@ int conv_tc_pack(const float* w, long long wbs, int K, int N, int dgrad, float* 
 // tma: the window is fetched as whole padded lines (conv_tma_k): a channel
 // column holds lrows = ceil((WR + Sw - 1) / Sw) lines of Sw rows
 static bool tc_plan(int D, int H, int W, int K, int N, int batch, TcConv& a, int* tiles, int nt = 3,
-                    bool bf = false, bool tma = false, bool b3 = false, bool kwf = false) {
+                    bool bf = false, bool tma = false, bool b3 = false, bool kwf = false, int nst = 2) {
   if (b3) bf = true;
   const int rs = kwf ? kTcRows - 2 : kTcRows;  // output rows per sub-tile
   a.N = N;
@@ -1602,7 +1725,7 @@ static bool tc_plan(int D, int H, int W, int K, int N, int batch, TcConv& a, int
     if (T > 1 && ((!large && !t_pref) || nt == 2)) break;
     if (t_pref && nt != 2 && T != t_pref) continue;
     const int wr = nt == 1 ? T * kTcRows : wr_of(a.Sw, T);
-    const int wrp = tma ? (wr + 2 * a.Sw - 2) / a.Sw * a.Sw : wrp_of(wr);
+    const int wrp_tma = (wr + 2 * a.Sw - 2) / a.Sw * a.Sw;
     const int tl = cdiv(tiles1, T);
     for (int ns = std::min(a.Np, 256); ns >= 16; ns -= 16) {
       if (a.Np % ns) continue;
@@ -1610,8 +1733,9 @@ static bool tc_plan(int D, int H, int W, int K, int N, int batch, TcConv& a, int
       if (kwf && 3 * ns > 256) continue;            // one MMA's N
       for (int cb = bf ? 16 : 8; cb <= K && cb <= (bf ? 128 : 64); cb *= 2) {
         if (K % cb) continue;
-        const size_t sm = 2 * stage_bytes(cb, ns, wrp, nt, bf, b3) + 3 * wr * sizeof(int) + 64;
-        if (sm > (size_t)210 * 1024) continue;
+        const int wrp = tma ? wrp_tma : wrp_of(wr, cb / (bf ? 8 : 4));
+        const size_t sm = nst * stage_bytes(cb, ns, wrp, nt, bf, b3) + 3 * wr * sizeof(int) + 64;
+        if (sm > (size_t)(nst == 2 ? 210 : 224) * 1024) continue;
         // kw folding parks 128 rows x (2 ns + 4) fp32 in the idle stage buffers
         if (kwf && (size_t)kTcRows * (2 * ns + 4) * 4 > 2 * stage_bytes(cb, ns, wrp, nt, bf, b3)) continue;
         const int per_sm = sm <= (size_t)110 * 1024 ? 2 : 1;
@@ -1655,6 +1779,45 @@ static bool tc_plan(int D, int H, int W, int K, int N, int batch, TcConv& a, int
   return true;
 }
 
+// Ring depth the plan is sized for: three stages for the 3xTF32 layers (the software-pipelined
+// producers keep two fills in flight; D2IP_TC_NST=2 restores the two-stage ring), two for bf16.
+static int plan_nst(bool bf) {
+  static const int nst_tf32 = [] {
+    const char* v = getenv("D2IP_TC_NST");
+    return v ? std::max(2, std::min(3, atoi(v))) : 3;
+  }();
+  return bf ? 2 : nst_tf32;
+}
+
+// The two-stage plan, with a third stage when it costs no co-resident CTA; layers with enough
+// tiles to fill the GPU without split-K re-plan for three stages (a smaller channel block):
+// measured at cfg2, 96->32 @ 32x32x16 fwd 109 -> 58 us, 32->32 47 -> 32 us. Split-K layers (deep
+// levels, < 100 tiles) keep their plan: more, smaller stages made them slower (17 -> 22 us).
+static bool tc_plan_nst(int D, int H, int W, int K, int N, int batch, TcConv& a, int* tiles, int nt, bool bf, bool tma,
+                        bool b3, bool kwf) {
+  if (!tc_plan(D, H, W, K, N, batch, a, tiles, nt, bf, tma, b3, kwf, 2)) return false;
+  a.nst = 2;
+  if (plan_nst(bf || b3) < 3 || tma) return true;
+  const size_t st = stage_bytes(a.CB, a.Ns, a.WRp, nt, bf, b3), fix = 3 * a.WR * sizeof(int) + 128;
+  const size_t two = 2 * st + fix, three = 3 * st + fix;
+  // multi-tile CTAs (large grids): a third stage when it keeps the CTAs per SM
+  if (a.T >= 2 && (two > (size_t)110 * 1024 ? three <= (size_t)224 * 1024 : three <= (size_t)110 * 1024)) {
+    a.nst = 3;
+    return true;
+  }
+  // one CTA per SM with >= 100 tiles (stride 1): re-plan for three stages (a smaller channel block)
+  if (nt == 3 && two > (size_t)110 * 1024 && (long long)*tiles * batch >= 100) {
+    TcConv a3 = a;
+    int tiles3 = 0;
+    if (tc_plan(D, H, W, K, N, batch, a3, &tiles3, nt, bf, tma, b3, kwf, 3)) {
+      a = a3;
+      a.nst = 3;
+      *tiles = tiles3;
+    }
+  }
+  return true;
+}
+
 size_t conv_tc_ws_bytes(int D, int H, int W, int K, int N, int batch, int mode) {
   TcConv a{};
   int tiles;
@@ -1662,8 +1825,8 @@ size_t conv_tc_ws_bytes(int D, int H, int W, int K, int N, int batch, int mode) 
   size_t best = 0;
   // the larger of the two plans (kw-folded or not) a stride-1 call may take
   for (int kwf = (mode & kTcKwf) ? 1 : 0; kwf <= ((mode & kTcKwf) ? 1 : 0); ++kwf) {
-    if (!tc_plan(D, H, W, K, N, batch, a, &tiles, m3 == 3 ? 1 : m3 ? 2 : 3, (mode & kTcBf16) != 0, false,
-                 (mode & kTcBf3) != 0, kwf != 0) ||
+    if (!tc_plan_nst(D, H, W, K, N, batch, a, &tiles, m3 == 3 ? 1 : m3 ? 2 : 3, (mode & kTcBf16) != 0, false,
+                     (mode & kTcBf3) != 0, kwf != 0) ||
         a.kspl <= 1)
       continue;
     // mode 2 partials are [V_gx][C_gx]: V_gx C_gx <= 8 V N / 8 (gx dims <= 2 x the row grid)
@@ -1826,7 +1989,7 @@ int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, lo
   }();
   const bool use_tma = tma_on && bf && !b3 && (mode == 0 || mode == 3) && x.bf16 && x.cstride % 8 == 0 && x.c % 8 == 0 &&
                        ((uintptr_t)x.bf16 & 15) == 0 && x.w + 2 <= 256;
-  D2IP_CHECK_ARG(tc_plan(g.d, g.h, g.w, K, N, batch, a, &tiles, ntm, bf, use_tma, b3),
+  D2IP_CHECK_ARG(tc_plan_nst(g.d, g.h, g.w, K, N, batch, a, &tiles, ntm, bf, use_tma, b3, false),
                  "conv_tc: no channel blocking fits shared memory (K=%d N=%d W=%d)", K, N, g.w);
   // kw folding (MODE 4) for stride-1 3^3 layers on the one-tile kernel: 3x fewer MMAs of 3x
   // the width. 3xTF32 layers only: on cfg4's 3xbf16 forwards (large grids, T = 4 tiles) it
@@ -1836,7 +1999,7 @@ int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, lo
     D2IP_CHECK_ARG(mode == 0 && !use_tma && !bf, "conv_tc: kw-folded packing on a layer that cannot run it");
     TcConv k2{};
     int tiles2 = 0;
-    D2IP_CHECK_ARG(tc_plan(g.d, g.h, g.w, K, N, batch, k2, &tiles2, ntm, bf, false, b3, true),
+    D2IP_CHECK_ARG(tc_plan_nst(g.d, g.h, g.w, K, N, batch, k2, &tiles2, ntm, bf, false, b3, true),
                    "conv_tc: no kw-folded plan fits (K=%d N=%d W=%d)", K, N, g.w);
     a = k2;
     tiles = tiles2;
@@ -1911,21 +2074,8 @@ int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, lo
   while (cols < a.T * a.Ns * (kwf ? 3 : 1)) cols *= 2;
   a.tmem_cols = cols;
   a.idesc = tc::make_idesc(bf ? 1 : 2, kTcRows, a.Ns * (kwf ? 3 : 1));
-  // D2IP_TC_NST=3: a third stage when it fits without costing occupancy. Measured neutral at
-  // cfg4 (137.9 vs 138.2 it/s) and a loss at cfg1 (1,218 vs 1,244): two stages stay the default.
-  static const int nst_max = [] {
-    const char* v = getenv("D2IP_TC_NST");
-    return v ? std::max(2, std::min(3, atoi(v))) : 2;
-  }();
-  // (never at the cost of a co-resident CTA: the plan's 2-stage footprint decides CTAs per SM)
-  a.nst = 2;
-  if (nst_max >= 3 && !use_tma) {
-    const size_t two = tc_smem_bytes(a);
-    a.nst = 3;
-    const size_t three = tc_smem_bytes(a);
-    const bool keeps_occupancy = two > (size_t)110 * 1024 ? three <= (size_t)220 * 1024 : three <= (size_t)110 * 1024;
-    if (!keeps_occupancy) a.nst = 2;
-  }
+  // ring depth: decided with the plan (three stages for 3xTF32 layers where they fit)
+  if (tma3 || use_tma) a.nst = 2;
   static const int async_on = [] {
     const char* v = getenv("D2IP_TC_ASYNC");
     return v ? atoi(v) : 1;
