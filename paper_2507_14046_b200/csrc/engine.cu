@@ -341,6 +341,35 @@ int cwgrad_side(Ctx& k, const ConvP& c, d2ip_act x, d2ip_act gy) {
   return cwgrad(ks, c, x, gy);
 }
 
+// Level-0 weight gradients (the largest: ~150 us each at cfg2, every SM's shared memory) are
+// leaves of the backward graph. Launched where their inputs appear they run beside the level-0
+// data gradients, which fill the GPU too; deferred by D2IP_WG_DEFER decoder blocks they run
+// beside the deep levels' small, latency-bound kernels instead.
+struct DeferredWg {
+  const ConvP* c;
+  d2ip_act x, gy;
+};
+static thread_local std::vector<DeferredWg> g_deferred;
+static int defer_blocks() {
+  static const int n = [] {
+    const char* v = getenv("D2IP_WG_DEFER");
+    return v ? atoi(v) : 0;
+  }();
+  return n;
+}
+static int cwgrad_level(Ctx& k, const ConvP& c, d2ip_act x, d2ip_act gy, int level) {
+  if (defer_blocks() > 0 && level == 0) {
+    g_deferred.push_back(DeferredWg{&c, x, gy});
+    return D2IP_OK;
+  }
+  return cwgrad_side(k, c, x, gy);
+}
+static int flush_deferred(Ctx& k) {
+  for (const DeferredWg& d : g_deferred) D2IP_RET(cwgrad_side(k, *d.c, d.x, d.gy));
+  g_deferred.clear();
+  return D2IP_OK;
+}
+
 // The job table of every tcgen05 layer's weight packs (built once at bind).
 static void build_pack_jobs(d2ip_engine& E) {
   PackJobs& j = E.packjobs;
@@ -435,8 +464,8 @@ static int block_bwd(Ctx& k, Block& bl) {
   D2IP_RET(norm_act_bwd(bl.gout, bl.out, 1, k.slope, bl.xh2, bl.rs2, k.th() + bl.n2.og, k.pbs, gpre, gc2,
                         k.gr() + bl.n2.og, k.pbs, bl.np2, npb, k.B, k.st, &nb));
   D2IP_RET(dgb_side(k, bl.np2, nb, co, bl.n2.og));
-  D2IP_RET(cwgrad_side(k, bl.c2, h1, gc2));
-  D2IP_RET(cwgrad_side(k, bl.sk, bl.x, gpre));
+  D2IP_RET(cwgrad_level(k, bl.c2, h1, gc2, bl.lout));
+  D2IP_RET(cwgrad_level(k, bl.sk, bl.x, gpre, bl.lout));
   // side2: the 1^3 skip's data gradient writes gx first; conv1's accumulates after the join
   D2IP_RET(fork_to(k, k.st, k.side2));
   {
@@ -449,7 +478,7 @@ static int block_bwd(Ctx& k, Block& bl) {
   D2IP_RET(norm_act_bwd(gh1, h1, 1, k.slope, bl.xh1, bl.rs1, k.th() + bl.n1.og, k.pbs, gpre1, gc1,
                         k.gr() + bl.n1.og, k.pbs, bl.np1, npb, k.B, k.st, &nb, skd));
   D2IP_RET(dgb_side(k, bl.np1, nb, co, bl.n1.og));
-  D2IP_RET(cwgrad_side(k, bl.c1, bl.x, gc1));
+  D2IP_RET(cwgrad_level(k, bl.c1, bl.x, gc1, bl.lout));
   D2IP_RET(fork_to(k, k.side2, k.st));
   D2IP_RET(cdgrad(k, bl.c1, gc1, bl.gx, 1));
   return D2IP_OK;
@@ -552,9 +581,15 @@ static int backward(Ctx& k) {
     d2ip_act gup = view(E, E.gcat[l], l, c[l + 1], E.catw[l]);
     d2ip_act gprev = (j == 0) ? E.neck.gout : E.dec[j - 1].gout;
     D2IP_RET(upsample2x_bwd(gup, gprev, 0, k.B, k.st));
+    if ((int)E.dec.size() - j == defer_blocks()) D2IP_RET(flush_deferred(k));
   }
   D2IP_RET(block_bwd(k, E.neck));
-  for (int i = (int)E.enc.size() - 1; i >= 0; --i) D2IP_RET(block_bwd(k, E.enc[i]));
+  if ((int)E.dec.size() + 1 == defer_blocks()) D2IP_RET(flush_deferred(k));
+  for (int i = (int)E.enc.size() - 1; i >= 0; --i) {
+    if (i == 0) D2IP_RET(flush_deferred(k));  // enc[0] is level 0 again
+    D2IP_RET(block_bwd(k, E.enc[i]));
+  }
+  D2IP_RET(flush_deferred(k));
   // stem: LN/act backward + weight gradient (no data gradient: Z is fixed)
   d2ip_act a0 = view(E, E.cat[0] + c[1], 0, c[0], E.catw[0]);
   d2ip_act ga0 = view(E, E.gcat[0] + c[1], 0, c[0], E.catw[0]);

@@ -35,6 +35,8 @@ namespace d2ip {
 
 constexpr int kWbThreads = 288;  // warp 0: MMA issue; warps 1-8: producers, then the epilogue
 constexpr int kWbProd = 256;
+constexpr int kWbThreads3 = 544;  // 3xbf16: sixteen producer warps
+constexpr int kWbProd3 = 512;
 constexpr int kWbMaxStages = 4;
 
 struct WgBf {
@@ -130,7 +132,16 @@ __device__ __forceinline__ int wb_base(const WgBf& a, int grp) {
 // general per-MMA descriptor computation at ~140-390 cycles per MMA, against
 // ~40 for the operand reads themselves).
 template <int NCX, int NKH, int NMMA, bool B3>
-__global__ void __launch_bounds__(kWbThreads) wgrad_bf_k(WgBf a) {
+__global__ void __launch_bounds__(B3 ? kWbThreads3 : kWbThreads) wgrad_bf_k(WgBf a) {
+  // 3xbf16 (fp32 inputs converted and split on the way in; the weight gradients of large
+  // TF32-precision layers): with eight producer warps the kernel was bound by instruction latency
+  // at two warps per scheduler (ncu: 36 k instructions per warp, issue active 29 %), so this
+  // variant runs sixteen producer warps with eight loads in flight each (48->16 @ 64x64x32:
+  // 150 -> 97 us). Measured and not kept: 24 warps (99 us), two producer groups on alternate
+  // stages (105 us), two 9-warp CTAs per SM (141 us).
+  constexpr int NPROD = B3 ? kWbProd3 : kWbProd;  // producer threads
+  constexpr int UL = B3 ? 8 : 16;                 // loads in flight per producer thread
+  constexpr int NPG = 1, GP = NPROD / NPG;  // producer groups, threads per group
   D2IP_PDL_ENTRY();
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -141,7 +152,7 @@ __global__ void __launch_bounds__(kWbThreads) wgrad_bf_k(WgBf a) {
   const int NM = RS + 2;  // gy row map: rows v0 - 1 .. v0 + RS
   // layout: NST stages [x groups][gy copies x groups] (+ pad), row maps [2][WR + NM], barriers, TMEM slot, bias scratch
   int* rmap = reinterpret_cast<int*>(smem + (size_t)NST * a.Sb + a.pad);
-  uint64_t* full = reinterpret_cast<uint64_t*>(rmap + 2 * (WR + NM) + ((2 * (WR + NM)) & 1));
+  uint64_t* full = reinterpret_cast<uint64_t*>(rmap + 4 * (WR + NM));  // row maps: [2][NPG <= 2][WR + NM]
   uint64_t* empty = full + kWbMaxStages;
   uint64_t* done = empty + kWbMaxStages;
   uint32_t* tslot = reinterpret_cast<uint32_t*>(done + 1);
@@ -150,7 +161,7 @@ __global__ void __launch_bounds__(kWbThreads) wgrad_bf_k(WgBf a) {
   if (warp == 0) tc::tmem_alloc(tslot, a.tmem_cols);
   if (tid == 0) {
     for (int i = 0; i < NST; ++i) {
-      tc::mbar_init(&full[i], 2 * kWbProd);  // async (copies landed) + plain (halo carry done) per thread
+      tc::mbar_init(&full[i], 2 * GP);  // async (copies landed) + plain (halo carry done) per thread
       tc::mbar_init(&empty[i], 1);
     }
     tc::mbar_init(done, 1);
@@ -217,8 +228,10 @@ __global__ void __launch_bounds__(kWbThreads) wgrad_bf_k(WgBf a) {
     }
     __syncwarp();
   } else {
-    // ---- producers
+    // ---- producers: NPG groups of GP threads fill alternate stages (3xbf16: two groups, so the
+    // load latency and row-map barrier of one stage overlap the conversion of the other)
     const int gtid = tid - 32;
+    const int pg = gtid / GP, gt = gtid - pg * GP;
     const d2ip_act x = a.x, gy = a.gy;
     const float* xb = x.ptr + b * x.bstride + cb * a.cib;
     const float* gb = gy.ptr + b * gy.bstride;
@@ -228,7 +241,7 @@ __global__ void __launch_bounds__(kWbThreads) wgrad_bf_k(WgBf a) {
     const int ncp = a.ncp;
     const uint32_t cpy = (uint32_t)a.ngc * RSp * 16;
     float4 bsum = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int s = 0; s < S; ++s) {
+    for (int s = pg; s < S; s += NPG) {
       const int slot = s % NST;
       if (s >= NST) tc::mbar_wait(&empty[slot], (uint32_t)(((s / NST) - 1) & 1));
       if (a.dbg) {
@@ -239,8 +252,8 @@ __global__ void __launch_bounds__(kWbThreads) wgrad_bf_k(WgBf a) {
       const int v0 = a.v_start + (c_lo + s) * RS;
       const bool carry = s > 0 && a.carry;  // first `halo` x rows = the previous window's last rows
       const int xr0 = carry ? a.halo : 0;
-      int* rm = rmap + (s & 1) * (WR + NM);
-      for (int r = gtid; r < WR + NM; r += kWbProd) {
+      int* rm = rmap + (((s / NPG) & 1) * NPG + pg) * (WR + NM);
+      for (int r = gt; r < WR + NM; r += GP) {
         int off = -1;
         if (r < WR) {
           if (r >= xr0) {
@@ -263,7 +276,7 @@ __global__ void __launch_bounds__(kWbThreads) wgrad_bf_k(WgBf a) {
         }
         rm[r] = off;
       }
-      asm volatile("bar.sync 1, 256;" ::: "memory");
+      asm volatile("bar.sync %0, %1;" ::"r"(2 + pg), "n"(GP) : "memory");
       uint8_t* X = smem + (size_t)slot * a.Sb;
       uint8_t* Gs = X + (B3 ? 2 : 1) * a.Sx;
       // x window rows [xr0, WR): NCX float4 pieces per row -> bf16 halves of 16-byte group rows
@@ -273,7 +286,7 @@ __global__ void __launch_bounds__(kWbThreads) wgrad_bf_k(WgBf a) {
         const uint16_t* xt = reinterpret_cast<const uint16_t*>(x.bf16) + b * x.bstride + cb * a.cib;
         constexpr int NGX = NCX / 2;
         const int n16 = (WR - xr0) * NGX;
-        for (int i = gtid; i < n16; i += kWbProd) {
+        for (int i = gt; i < n16; i += GP) {
           const int r = xr0 + i / NGX, g = i % NGX;
           const int off = rm[r];
           const uint16_t* src = xt;
@@ -288,11 +301,11 @@ __global__ void __launch_bounds__(kWbThreads) wgrad_bf_k(WgBf a) {
           tc::cp_async16(X + ((size_t)g * WRp + r) * 16, src, ok ? 16u : 0u);
         }
       }
-      for (int i0 = gtid; i0 < nX; i0 += 16 * kWbProd) {
-        float4 v[16];
+      for (int i0 = gt; i0 < nX; i0 += UL * GP) {
+        float4 v[UL];
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          const int i = i0 + q * kWbProd;
+        for (int q = 0; q < UL; ++q) {
+          const int i = i0 + q * GP;
           v[q] = make_float4(0.f, 0.f, 0.f, 0.f);
           if (i < nX) {
             const int off = rm[xr0 + i / NP];
@@ -306,8 +319,8 @@ __global__ void __launch_bounds__(kWbThreads) wgrad_bf_k(WgBf a) {
           }
         }
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          const int i = i0 + q * kWbProd;
+        for (int q = 0; q < UL; ++q) {
+          const int i = i0 + q * GP;
           if (i >= nX) continue;
           const int r = xr0 + i / NP, pc = i % NP;
           const uint2 h = make_uint2(bf2w(v[q].x, v[q].y), bf2w(v[q].z, v[q].w));
@@ -319,13 +332,13 @@ __global__ void __launch_bounds__(kWbThreads) wgrad_bf_k(WgBf a) {
       // (1^3: one copy, row j = map row j + 1). The bias sum counts rows m = 1 .. RS once.
       const bool bias_here = (c_lo + s) % a.nyb == ybias;
       if (a.gtw) {  // bf16 twin: the kw copies are three async copies of the same 16 bytes (L1-allocating)
-        const uint16_t* gt = reinterpret_cast<const uint16_t*>(gy.bf16) + b * gy.bstride;
+        const uint16_t* gtwin = reinterpret_cast<const uint16_t*>(gy.bf16) + b * gy.bstride;
         const int cs = a.gshift - 1;  // log2(C_out / 8): 8-channel groups per gy row
         const int n16 = NM << cs;
-        for (int i = gtid; i < n16; i += kWbProd) {
+        for (int i = gt; i < n16; i += GP) {
           const int m = i >> cs, g = i & ((1 << cs) - 1);
           const int off = rm[WR + m];
-          const uint16_t* src = off >= 0 ? gt + (long long)off * gy.cstride + 8 * g : gt;
+          const uint16_t* src = off >= 0 ? gtwin + (long long)off * gy.cstride + 8 * g : gtwin;
           if (ncp == 1) {
             tc::cp_async16(Gs + ((size_t)g * RSp + m) * 16, src, off >= 0 ? 16u : 0u);
           } else {
@@ -337,11 +350,11 @@ __global__ void __launch_bounds__(kWbThreads) wgrad_bf_k(WgBf a) {
         }
       }
       const int nG = (!a.gtw || bias_here) ? NM << a.gshift : 0;
-      for (int i0 = gtid; i0 < nG; i0 += 16 * kWbProd) {
-        float4 v[16];
+      for (int i0 = gt; i0 < nG; i0 += UL * GP) {
+        float4 v[UL];
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          const int i = i0 + q * kWbProd;
+        for (int q = 0; q < UL; ++q) {
+          const int i = i0 + q * GP;
           v[q] = make_float4(0.f, 0.f, 0.f, 0.f);
           if (i < nG) {
             const int off = rm[WR + (i >> a.gshift)];
@@ -349,8 +362,8 @@ __global__ void __launch_bounds__(kWbThreads) wgrad_bf_k(WgBf a) {
           }
         }
 #pragma unroll
-        for (int q = 0; q < 16; ++q) {
-          const int i = i0 + q * kWbProd;
+        for (int q = 0; q < UL; ++q) {
+          const int i = i0 + q * GP;
           if (i >= nG) continue;
           const int m = i >> a.gshift, pc = i & gmask;
           if (bias_here && m >= 1 && m <= RS) {
@@ -380,7 +393,7 @@ __global__ void __launch_bounds__(kWbThreads) wgrad_bf_k(WgBf a) {
         const uint8_t* Xp = smem + (size_t)((s - 1) % NST) * a.Sb;
         const int n16 = a.ngx * a.halo;
         for (int hl = 0; hl < (B3 ? 2 : 1); ++hl)  // B3: the hi and the lo window
-          for (int i = gtid; i < n16; i += kWbProd) {
+          for (int i = gt; i < n16; i += GP) {
             const int g = i / a.halo, r = i - g * a.halo;
             *reinterpret_cast<uint4*>(X + hl * a.Sx + ((size_t)g * WRp + r) * 16) =
                 *reinterpret_cast<const uint4*>(Xp + hl * a.Sx + ((size_t)g * WRp + RS + r) * 16);
@@ -397,7 +410,7 @@ __global__ void __launch_bounds__(kWbThreads) wgrad_bf_k(WgBf a) {
       tc::mbar_wait(done, 0);
       tc::fence_after();
     }
-    const int quad = warp & 3, half = (warp - 1) >> 2;
+    const int quad = warp & 3, half = (warp - 1) >> 2;  // column interleave over the NPROD / 128 warps of a quadrant
     // M = 128: lane l holds row l; M = 64: rows at lanes (m % 16) + 32 (m / 16)
     int m = -1;
     if (a.M == 128) m = quad * 32 + lane;
@@ -408,7 +421,7 @@ __global__ void __launch_bounds__(kWbThreads) wgrad_bf_k(WgBf a) {
     // accumulator columns: kh block of 3 C_out (kw copy c = kw, then co)
     const int nck = (nkh * 3 * Cout) / 8;
     const int nck_all = (a.ks == 1 || a.tapmode) ? Cout / 8 : nck;
-    for (int c8 = half; c8 < nck_all; c8 += 2) {
+    for (int c8 = half; c8 < nck_all; c8 += NPROD / 128) {
       float vals[8];
       tc::tmem_ld8(trow + (uint32_t)(c8 * 8), vals);
       const int col = c8 * 8;
@@ -431,11 +444,11 @@ __global__ void __launch_bounds__(kWbThreads) wgrad_bf_k(WgBf a) {
     {
       // fixed-order sum of the per-thread partials (thread gtid always held piece gtid % (C_out / 4)) into slot y
       bscr[gtid] = bsum;
-      asm volatile("bar.sync 1, 256;" ::: "memory");
+      asm volatile("bar.sync 1, %0;" ::"n"(NPROD) : "memory");
       const int np = 1 << a.gshift;
       if (gtid < np) {
         float4 s4 = make_float4(0.f, 0.f, 0.f, 0.f);
-        for (int j = gtid; j < kWbProd; j += np) {
+        for (int j = gtid; j < NPROD; j += np) {
           const float4 v = bscr[j];
           s4.x += v.x; s4.y += v.y; s4.z += v.z; s4.w += v.w;
         }
@@ -449,8 +462,8 @@ __global__ void __launch_bounds__(kWbThreads) wgrad_bf_k(WgBf a) {
 }
 
 static size_t wb_smem(const WgBf& a) {
-  return (size_t)a.NST * a.Sb + a.pad + 2 * (size_t)(a.WR + a.RS + 2) * sizeof(int) + 16 +
-         (2 * kWbMaxStages + 1) * 8 + 16 + kWbProd * 16 + 64;
+  return (size_t)a.NST * a.Sb + a.pad + 4 * (size_t)(a.WR + a.RS + 2) * sizeof(int) + 16 +
+         (2 * kWbMaxStages + 1) * 8 + 16 + kWbProd3 * 16 + 64;
 }
 
 static bool pow2(int v) { return v > 0 && (v & (v - 1)) == 0; }
@@ -564,11 +577,12 @@ static bool wb_plan(int D, int H, int W, int Cin, int Cout, int ks, int batch, W
     a.Sg = sg;
     a.Sb = sb;
     a.NST = 2;
-    if (wb_smem(a) > (size_t)205 * 1024) {
+    const size_t lim = (size_t)205 * 1024;
+    if (wb_smem(a) > lim) {
       a.RS = 0;
       continue;
     }
-    if (wb_smem(a) + sb <= (size_t)205 * 1024) a.NST = 3;
+    if (wb_smem(a) + sb <= lim) a.NST = 3;
     break;
   }
   if (!a.RS) return false;
@@ -642,7 +656,7 @@ static int wb_launch4(const WgBf& a, dim3 grid, size_t smem, cudaStream_t st) {
                                    227 * 1024));
     attr = true;
   }
-  D2IP_CUDA(launch_pdl(wgrad_bf_k<NCX, NKH, NMMA, B3>, grid, kWbThreads, smem, st, a));
+  D2IP_CUDA(launch_pdl(wgrad_bf_k<NCX, NKH, NMMA, B3>, grid, B3 ? kWbThreads3 : kWbThreads, smem, st, a));
   return D2IP_OK;
 }
 
