@@ -35,7 +35,9 @@ namespace d2ip {
 
 constexpr int kWbThreads = 288;  // warp 0: MMA issue; warps 1-8: producers, then the epilogue
 constexpr int kWbProd = 256;
-constexpr int kWbThreads3 = 544;  // 3xbf16: sixteen producer warps
+// 3xbf16: sixteen producer warps + one MMA-issue warp per independent accumulator (three for the kd-plane shape)
+__host__ __device__ constexpr int wb_issuers(bool b3, int nkh) { return (b3 && nkh == 3) ? 3 : 1; }
+__host__ __device__ constexpr int wb_threads(bool b3, int nkh) { return 32 * wb_issuers(b3, nkh) + (b3 ? 512 : 256); }
 constexpr int kWbProd3 = 512;
 constexpr int kWbMaxStages = 4;
 
@@ -132,7 +134,7 @@ __device__ __forceinline__ int wb_base(const WgBf& a, int grp) {
 // general per-MMA descriptor computation at ~140-390 cycles per MMA, against
 // ~40 for the operand reads themselves).
 template <int NCX, int NKH, int NMMA, bool B3>
-__global__ void __launch_bounds__(B3 ? kWbThreads3 : kWbThreads) wgrad_bf_k(WgBf a) {
+__global__ void __launch_bounds__(wb_threads(B3, NKH)) wgrad_bf_k(WgBf a) {
   // 3xbf16 (fp32 inputs converted and split on the way in; the weight gradients of large
   // TF32-precision layers): with eight producer warps the kernel was bound by instruction latency
   // at two warps per scheduler (ncu: 36 k instructions per warp, issue active 29 %), so this
@@ -141,7 +143,11 @@ __global__ void __launch_bounds__(B3 ? kWbThreads3 : kWbThreads) wgrad_bf_k(WgBf
   // stages (105 us), two 9-warp CTAs per SM (141 us).
   constexpr int NPROD = B3 ? kWbProd3 : kWbProd;  // producer threads
   constexpr int UL = B3 ? 8 : 16;                 // loads in flight per producer thread
-  constexpr int NPG = 1, GP = NPROD / NPG;  // producer groups, threads per group
+  constexpr int NPG = 1, GP = NPROD / NPG;
+  // MMA-issue warps: a single issuer pays >= 57 cycles per MMA whatever its size (the no-fill
+  // run of this kernel, D2IP_WB_DBG=1, took 77 us of its 97); the kd-plane shape has three
+  // independent accumulators (kh), so three warps issue one each
+  constexpr int NI = wb_issuers(B3, NKH);  // producer groups, threads per group
   D2IP_PDL_ENTRY();
   extern __shared__ __align__(1024) uint8_t smem[];
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
@@ -162,9 +168,9 @@ __global__ void __launch_bounds__(B3 ? kWbThreads3 : kWbThreads) wgrad_bf_k(WgBf
   if (tid == 0) {
     for (int i = 0; i < NST; ++i) {
       tc::mbar_init(&full[i], 2 * GP);  // async (copies landed) + plain (halo carry done) per thread
-      tc::mbar_init(&empty[i], 1);
+      tc::mbar_init(&empty[i], NI);
     }
-    tc::mbar_init(done, 1);
+    tc::mbar_init(done, NI);
     tc::fence_mbar_init();
   }
   tc::fence_before();
@@ -176,8 +182,8 @@ __global__ void __launch_bounds__(B3 ? kWbThreads3 : kWbThreads) wgrad_bf_k(WgBf
   const int base = wb_base(a, grp);
   constexpr int nkh = NKH, nmma = NMMA;
 
-  if (warp == 0) {
-    // ---- MMA issue: one thread; descriptors advance by constant adds to the
+  if (warp < NI) {
+    // ---- MMA issue: one thread per issuing warp; descriptors advance by constant adds to the
     // start-address field (units of 16 B). Every operand block is 128-byte
     // aligned (8-row pitch, 8-aligned windows).
     if (lane == 0) {
@@ -205,9 +211,9 @@ __global__ void __launch_bounds__(B3 ? kWbThreads3 : kWbThreads) wgrad_bf_k(WgBf
         const uint64_t so = (uint64_t)((slot * a.Sb) >> 4);
         for (int k16 = 0; k16 < RS / 16; ++k16) {
           const uint64_t da = dA0 + so + (uint64_t)(k16 * 16), db = dB0 + so + (uint64_t)(k16 * 16);
-          const uint32_t acc = (s | k16) ? 1u : 0u;
+          const uint32_t acc = (s | k16) ? 1u : 0u;  // (per accumulator: every issuer starts its own)
 #pragma unroll
-          for (int kh = 0; kh < NKH; ++kh)
+          for (int kh = (NI == 1 ? 0 : warp); kh < (NI == 1 ? NKH : warp + 1); ++kh)
 #pragma unroll
             for (int c = 0; c < NMMA; ++c) {
               const uint32_t d = tmem + (uint32_t)(kh * NMMA + c) * N;
@@ -230,7 +236,7 @@ __global__ void __launch_bounds__(B3 ? kWbThreads3 : kWbThreads) wgrad_bf_k(WgBf
   } else {
     // ---- producers: NPG groups of GP threads fill alternate stages (3xbf16: two groups, so the
     // load latency and row-map barrier of one stage overlap the conversion of the other)
-    const int gtid = tid - 32;
+    const int gtid = tid - 32 * NI;
     const int pg = gtid / GP, gt = gtid - pg * GP;
     const d2ip_act x = a.x, gy = a.gy;
     const float* xb = x.ptr + b * x.bstride + cb * a.cib;
@@ -410,7 +416,7 @@ __global__ void __launch_bounds__(B3 ? kWbThreads3 : kWbThreads) wgrad_bf_k(WgBf
       tc::mbar_wait(done, 0);
       tc::fence_after();
     }
-    const int quad = warp & 3, half = (warp - 1) >> 2;  // column interleave over the NPROD / 128 warps of a quadrant
+    const int quad = warp & 3, half = (warp - NI) >> 2;  // column interleave over the NPROD / 128 warps of a quadrant
     // M = 128: lane l holds row l; M = 64: rows at lanes (m % 16) + 32 (m / 16)
     int m = -1;
     if (a.M == 128) m = quad * 32 + lane;
@@ -656,7 +662,7 @@ static int wb_launch4(const WgBf& a, dim3 grid, size_t smem, cudaStream_t st) {
                                    227 * 1024));
     attr = true;
   }
-  D2IP_CUDA(launch_pdl(wgrad_bf_k<NCX, NKH, NMMA, B3>, grid, B3 ? kWbThreads3 : kWbThreads, smem, st, a));
+  D2IP_CUDA(launch_pdl(wgrad_bf_k<NCX, NKH, NMMA, B3>, grid, wb_threads(B3, NKH), smem, st, a));
   return D2IP_OK;
 }
 
