@@ -63,7 +63,16 @@ profiles)
     ncu -i gpurun_out/ncu_$name.ncu-rep --page raw --csv > gpurun_out/ncu_$name.raw.csv 2>/dev/null
     python profiles/ncu_summary.py gpurun_out/ncu_$name.raw.csv gpurun_out/${TAG}_ncu_$name.json
     rm -f gpurun_out/ncu_$name.ncu-rep; echo "ncu $name done"
-  done ;;
+  done
+  # the level-0 weight gradient (3xbf16, wgrad_bf_k) through conv_bench (fwd / dgrad / wgrad of one layer)
+  name=cfg2dec0c1wg
+  if python tools/conv_bench.py 48 16 64x64x32 1 3 tf32 > /dev/null 2>&1; then
+    timeout 400 ncu --set full --import-source on --clock-control none -k regex:wgrad_bf_k -c 1 -o gpurun_out/ncu_$name \
+      python tools/conv_bench.py 48 16 64x64x32 1 1 tf32 > gpurun_out/ncu_$name.log 2>&1
+    ncu -i gpurun_out/ncu_$name.ncu-rep --page raw --csv > gpurun_out/ncu_$name.raw.csv 2>/dev/null
+    python profiles/ncu_summary.py gpurun_out/ncu_$name.raw.csv gpurun_out/${TAG}_ncu_$name.json
+    rm -f gpurun_out/ncu_$name.ncu-rep; echo "ncu $name done"
+  fi ;;
 sanitize)
   export PYTORCH_NO_CUDA_MEMORY_CACHING=1
   timeout 1200 /usr/local/cuda/bin/compute-sanitizer --tool memcheck --leak-check no --error-exitcode 9 --print-limit 20 \
