@@ -45,8 +45,15 @@
 
 namespace d2ip {
 
-constexpr int kWtThreads = 160;  // warp 0: MMA issue; warps 1-4: producers (loads, splits, epilogue)
-constexpr int kWtProd = 128;
+// warp 0: MMA issue; then two producer groups of kWtW warps (loads, splits, epilogue). Eight
+// warps per group: with two (64 threads per stage, synchronous copy -> wait -> split) the
+// producers were bound by latency at one warp per scheduler
+constexpr int kWtW = 8;
+constexpr int kWtProd = 2 * kWtW * 32;
+// MMA-issue warps: a single issuer pays >= 57 cycles per MMA (more with runtime descriptor
+// arithmetic), so the accumulators of a CTA (kh rows / taps) are dealt round-robin to three
+constexpr int kWtI = 3;
+constexpr int kWtThreads = 32 * kWtI + kWtProd;
 
 struct WgTc {
   d2ip_act x, gy;
@@ -126,9 +133,9 @@ __global__ void __launch_bounds__(kWtThreads) wgrad_tc_k(WgTc a) {
   if (tid == 0) {
     for (int i = 0; i < NSTG; ++i) {
       tc::mbar_init(&full[i], kWtProd / 2);  // one producer group (2 warps) fills a stage
-      tc::mbar_init(&empty[i], 1);
+      tc::mbar_init(&empty[i], kWtI);
     }
-    tc::mbar_init(done, 1);
+    tc::mbar_init(done, kWtI);
     tc::fence_mbar_init();
   }
   tc::fence_before();
@@ -140,8 +147,8 @@ __global__ void __launch_bounds__(kWtThreads) wgrad_tc_k(WgTc a) {
   const int Cin = x.c, Cout = gy.c;
   float* pb = a.part + ((long long)b * a.nrg + rg) * ((long long)a.ntaps * Cin * Cout + Cout);
 
-  if (warp == 0) {
-    // ---- MMA issue
+  if (warp < kWtI) {
+    // ---- MMA issue: issuer w takes accumulators w, w + kWtI, ...
     if (lane == 0) {
       const uint32_t sbase = tc::smem_u32(smem);
       const uint64_t dXhi = tc::make_desc_mn32(sbase, a.lbox), dXlo = dXhi + (a.Sx >> 4);
@@ -152,7 +159,7 @@ __global__ void __launch_bounds__(kWtThreads) wgrad_tc_k(WgTc a) {
         tc::fence_after();
         const uint64_t boff = (uint64_t)(slot * a.Sb) >> 4;
         const int nacc = a.stack ? 3 : a.G;  // accumulators: kh rows (stacked) or taps
-        for (int i = 0; i < nacc; ++i) {
+        for (int i = warp; i < nacc; i += kWtI) {
           const int t = t0 + (a.stack ? 3 * i : i);
           const int tt = a.ntaps == 27 ? t % 9 : 0;
           const int rowoff = a.ntaps == 27 ? (tt / 3) * a.Sw + (a.stack ? 0 : tt % 3) : 0;
@@ -176,7 +183,7 @@ __global__ void __launch_bounds__(kWtThreads) wgrad_tc_k(WgTc a) {
     // are in flight; a group first maps its stage's rows to voxels once (one
     // division pair per row, not per 16-byte chunk), then copies and splits
     // with fixed (row, chunk) ownership per thread.
-    const int ptid = tid - 32, pg = (warp - 1) >> 1, gw = (warp - 1) & 1, gtid = gw * 32 + lane;
+    const int ptid = tid - 32 * kWtI, pg = (warp - kWtI) / kWtW, gw = (warp - kWtI) % kWtW, gtid = gw * 32 + lane;
     const int xshift = a.ntaps == 27 ? (kd - 1) * a.Sh - a.Sw - (a.stack ? 0 : 1) : 0;
     constexpr int XR = 32 / NCHXP, GR = 32 / NCHGP;  // rows per warp step
     const int xr = lane / NCHXP, xc = lane % NCHXP, gr = lane / NCHGP, gc = lane % NCHGP;
@@ -186,12 +193,12 @@ __global__ void __launch_bounds__(kWtThreads) wgrad_tc_k(WgTc a) {
       const int slot = s % NSTG;
       if (s >= NSTG) tc::mbar_wait(&empty[slot], (uint32_t)((s / NSTG - 1) & 1));
       const int u0 = a.u_first + (c_lo + s) * RS;
-      for (int i = gtid; i < WR + RSg; i += 64)
+      for (int i = gtid; i < WR + RSg; i += 32 * kWtW)
         rm[i] = i < WR ? wg_voxel(a, u0 + xshift + i) : wg_voxel(a, u0 - a.stack + (i - WR));
-      asm volatile("bar.sync %0, 64;" ::"r"(1 + pg) : "memory");
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + pg), "n"(32 * kWtW) : "memory");
       uint8_t* X = smem + (size_t)slot * a.Sb;
       uint8_t* Gt = X + 2 * a.Sx;
-      for (int r0 = gw * XR; r0 < WR; r0 += 2 * XR) {
+      for (int r0 = gw * XR; r0 < WR; r0 += kWtW * XR) {
         const int r = r0 + xr;
         if (r < WR && xc < a.nchx) {
           const int v = rm[r];
@@ -199,7 +206,7 @@ __global__ void __launch_bounds__(kWtThreads) wgrad_tc_k(WgTc a) {
           tc::cp_async16(X + mn32_off(r, xc, a.Bx), src, v >= 0 ? 16u : 0u);
         }
       }
-      for (int r0 = gw * GR; r0 < RSg; r0 += 2 * GR) {
+      for (int r0 = gw * GR; r0 < RSg; r0 += kWtW * GR) {
         const int r = r0 + gr;
         if (r < RSg && gc < a.nchg) {
           const int v = rm[WR + r];
@@ -210,7 +217,7 @@ __global__ void __launch_bounds__(kWtThreads) wgrad_tc_k(WgTc a) {
       tc::cp_async_commit();
       tc::cp_async_wait<0>();
       // lo halves (the raw fp32 operand is the hi half: the tensor core truncates to TF32)
-      for (int r0 = gw * XR; r0 < WR; r0 += 2 * XR) {
+      for (int r0 = gw * XR; r0 < WR; r0 += kWtW * XR) {
         const int r = r0 + xr;
         if (r < WR && xc < a.nchx) {
           const uint32_t o = mn32_off(r, xc, a.Bx);
@@ -220,7 +227,7 @@ __global__ void __launch_bounds__(kWtThreads) wgrad_tc_k(WgTc a) {
           *reinterpret_cast<float4*>(X + a.Sx + o) = l;
         }
       }
-      for (int r0 = gw * GR; r0 < RSg; r0 += 2 * GR) {
+      for (int r0 = gw * GR; r0 < RSg; r0 += kWtW * GR) {
         const int r = r0 + gr;
         if (r < RSg && gc < a.nchg) {
           const uint32_t o = mn32_off(r, gc, a.Bg);
@@ -235,13 +242,13 @@ __global__ void __launch_bounds__(kWtThreads) wgrad_tc_k(WgTc a) {
       }
       tc::fence_proxy_async();
       tc::mbar_arrive(&full[slot]);
-      asm volatile("bar.sync %0, 64;" ::"r"(1 + pg) : "memory");  // rm is rebuilt next stage
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + pg), "n"(32 * kWtW) : "memory");  // rm is rebuilt next stage
     }
     if (do_bias) bred[ptid] = bacc;
   }
   __syncthreads();
-  if (warp != 0) {
-    const int ptid = tid - 32;
+  if (warp >= kWtI) {
+    const int ptid = tid - 32 * kWtI;
     if (do_bias && ptid < a.nchg) {  // fixed-order column sum of gy over this CTA's rows
       float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
       for (int q = 0; q < kWtProd; ++q) {
@@ -264,6 +271,8 @@ __global__ void __launch_bounds__(kWtThreads) wgrad_tc_k(WgTc a) {
     const bool row_ok = m >= 0 && m < a.cib;
     const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
     const int nacc = a.stack ? 3 : a.G;
+    const int sub = (warp - kWtI) >> 2;  // the 2 kWtW / 4 warps of a quadrant take 8-column chunks in turn
+    int chunk = 0;
     for (int i = 0; i < nacc; ++i) {
       for (int blk = 0; blk < (a.stack ? 3 : 1); ++blk) {
         // stacked: TMEM block blk of accumulator i is tap (kd, kh = i, kw = 2 - blk)
@@ -271,6 +280,7 @@ __global__ void __launch_bounds__(kWtThreads) wgrad_tc_k(WgTc a) {
         float* dst = pb + ((long long)t * Cin + ci) * Cout;
         const int cb = a.stack ? blk * 32 : 0, cw = a.stack ? 32 : a.N;
         for (int c0 = 0; c0 < cw && c0 < ((Cout + 7) & ~7); c0 += 8) {
+          if ((chunk++) % (2 * kWtW / 4) != sub) continue;
           float v[8];
           tc::tmem_ld8(trow + (uint32_t)(i * a.N + cb + c0), v);
           if (row_ok) {
@@ -328,8 +338,8 @@ __global__ void __launch_bounds__(kWtThreads) wgrad_tc_pack_k(WgTc a) {
   const int Cin = x.c, Cout = gy.c;
   float* pb = a.part + ((long long)b * a.nrg + rg) * ((long long)27 * Cin * Cout + Cout);
 
-  if (warp == 0) {
-    if (lane == 0) {
+  if (warp < kWtI) {
+    if (warp == 0 && lane == 0) {  // one accumulator: one issuer
       const uint32_t sbase = tc::smem_u32(smem);
       const uint64_t dXhi = tc::make_desc_mn32(sbase, a.lbox), dXlo = dXhi + (a.Sx >> 4);
       const uint64_t dGhi = tc::make_desc_mn32(sbase + 2 * a.Sx, a.lbog), dGlo = dGhi + (a.Sg >> 4);
@@ -350,7 +360,7 @@ __global__ void __launch_bounds__(kWtThreads) wgrad_tc_pack_k(WgTc a) {
       if (S > 0) tc::commit(done);
     }
   } else {
-    const int ptid = tid - 32, pg = (warp - 1) >> 1, gtid = ((warp - 1) & 1) * 32 + lane;
+    const int ptid = tid - 32 * kWtI, pg = (warp - kWtI) / kWtW, gtid = ((warp - kWtI) % kWtW) * 32 + lane;
     const int xshift = (kd - 1) * a.Sh - a.Sw;
     int* rm = rowmaps + pg * (NX + NG);
     const int nchx = Cin / 4, nchg = Cout / 4;
@@ -359,13 +369,13 @@ __global__ void __launch_bounds__(kWtThreads) wgrad_tc_pack_k(WgTc a) {
       const int slot = s % NSTG;
       if (s >= NSTG) tc::mbar_wait(&empty[slot], (uint32_t)((s / NSTG - 1) & 1));
       const int u0 = a.u_first + (c_lo + s) * RS;
-      for (int i = gtid; i < NX + NG; i += 64)
+      for (int i = gtid; i < NX + NG; i += 32 * kWtW)
         rm[i] = i < NX ? wg_voxel(a, u0 + xshift + i) : wg_voxel(a, u0 - 2 + (i - NX));
-      asm volatile("bar.sync %0, 64;" ::"r"(1 + pg) : "memory");
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + pg), "n"(32 * kWtW) : "memory");
       uint8_t* X = smem + (size_t)slot * a.Sb;
       uint8_t* Gt = X + 2 * a.Sx;
       // x: slot c = 4 (3 halves: block 0 lo / hi half, block 1 lo half) x chunk; kh = c / 4
-      for (int i = gtid; i < RS * 16; i += 64) {
+      for (int i = gtid; i < RS * 16; i += 32 * kWtW) {
         const int r = i >> 4, c = i & 15, kh = c >> 2, cc = c & 3;
         if (kh < 3 && cc < nchx) {
           const int v = rm[r + kh * a.Sw];
@@ -374,7 +384,7 @@ __global__ void __launch_bounds__(kWtThreads) wgrad_tc_pack_k(WgTc a) {
         }
       }
       // gy line j = [gy(u0 - 1 + j) | gy(u0 - 2 + j)]
-      for (int i = gtid; i < (RS + 2) * 8; i += 64) {
+      for (int i = gtid; i < (RS + 2) * 8; i += 32 * kWtW) {
         const int j = i >> 3, h = (i >> 2) & 1, cc = i & 3;
         if (cc < nchg) {
           const int v = rm[NX + j + 1 - h];
@@ -384,7 +394,7 @@ __global__ void __launch_bounds__(kWtThreads) wgrad_tc_pack_k(WgTc a) {
       }
       tc::cp_async_commit();
       tc::cp_async_wait<0>();
-      for (int i = gtid; i < RS * 16; i += 64) {
+      for (int i = gtid; i < RS * 16; i += 32 * kWtW) {
         const int r = i >> 4, c = i & 15, kh = c >> 2, cc = c & 3;
         if (kh < 3 && cc < nchx) {
           const uint32_t o = mn32_off(r, (kh & 1) * 4 + cc + (kh >> 1) * 8, a.Bx);
@@ -394,7 +404,7 @@ __global__ void __launch_bounds__(kWtThreads) wgrad_tc_pack_k(WgTc a) {
           *reinterpret_cast<float4*>(X + a.Sx + o) = l;
         }
       }
-      for (int i = gtid; i < (RS + 2) * 8; i += 64) {
+      for (int i = gtid; i < (RS + 2) * 8; i += 32 * kWtW) {
         const int j = i >> 3, h = (i >> 2) & 1, cc = i & 3;
         if (cc < nchg) {
           const uint32_t o = mn32_off(j, h * 4 + cc, a.Bg);
@@ -409,13 +419,13 @@ __global__ void __launch_bounds__(kWtThreads) wgrad_tc_pack_k(WgTc a) {
       }
       tc::fence_proxy_async();
       tc::mbar_arrive(&full[slot]);
-      asm volatile("bar.sync %0, 64;" ::"r"(1 + pg) : "memory");
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + pg), "n"(32 * kWtW) : "memory");
     }
     if (do_bias) bred[ptid] = bacc;
   }
   __syncthreads();
-  if (warp != 0) {
-    const int ptid = tid - 32;
+  if (warp >= kWtI) {
+    const int ptid = tid - 32 * kWtI;
     if (do_bias && ptid < Cout / 4) {  // fixed-order column sum: thread q held chunk q % 4 (h == 0 slots)
       float4 sum = make_float4(0.f, 0.f, 0.f, 0.f);
       for (int q = 0; q < kWtProd; ++q) {
@@ -432,7 +442,7 @@ __global__ void __launch_bounds__(kWtThreads) wgrad_tc_pack_k(WgTc a) {
     }
     // D row m = 16 kh + ci in TMEM lane (m % 16) + 32 (m / 16): quadrant q = kh
     const int q = warp & 3, ci = lane;
-    if (q < 3) {
+    if (q < 3 && warp >= 4 && warp <= 6) {  // one warp per quadrant (kh) drains it
       const uint32_t trow = tmem + ((uint32_t)(q * 32) << 16);
       for (int c0 = 0; c0 < 64; c0 += 8) {
         const int blk = c0 >> 4 >> 1, h = (c0 >> 4) & 1, co0 = c0 & 15;
