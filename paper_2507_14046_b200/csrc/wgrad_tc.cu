@@ -284,9 +284,16 @@ __global__ void __launch_bounds__(kWtThreads) wgrad_tc_k(WgTc a) {
           float v[8];
           tc::tmem_ld8(trow + (uint32_t)(i * a.N + cb + c0), v);
           if (row_ok) {
+            if ((Cout & 7) == 0 && (reinterpret_cast<uintptr_t>(pb) & 15) == 0) {  // 32 contiguous bytes per row: two 16-byte stores
+              const bool z = S <= 0;
+              float4* d4 = reinterpret_cast<float4*>(dst + c0);
+              d4[0] = z ? make_float4(0.f, 0.f, 0.f, 0.f) : make_float4(v[0], v[1], v[2], v[3]);
+              d4[1] = z ? make_float4(0.f, 0.f, 0.f, 0.f) : make_float4(v[4], v[5], v[6], v[7]);
+            } else {
 #pragma unroll
-            for (int j = 0; j < 8; ++j)
-              if (c0 + j < Cout) dst[c0 + j] = S > 0 ? v[j] : 0.f;
+              for (int j = 0; j < 8; ++j)
+                if (c0 + j < Cout) dst[c0 + j] = S > 0 ? v[j] : 0.f;
+            }
           }
         }
       }
