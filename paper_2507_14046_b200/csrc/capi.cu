@@ -68,7 +68,20 @@ int conv_wgrad(d2ip_act x, d2ip_act gy, int ks, int stride, float* gw, long long
   // the step it costs (1,238 -> 1,185 it/s): its ~200 KB of shared memory per CTA takes whole SMs from
   // the data-gradient chain it runs beside. Large grids only.
   const long long vg = (long long)gy.d * gy.h * gy.w;
-  const bool b3_wins = vg >= bf3_min;
+  // stride-2 3^3 layers with >= 5,000 output voxels take it too: their alternative is the
+  // CUDA-core tiled kernel. Standalone it wins at every size (cfg2: 16->32 64 -> 61 us, 32->64
+  // 43 -> 33 us, 64->128 31 -> 23 us; 404 -> 410 it/s with all three), but on cfg1's small grids
+  // its shared-memory footprint costs the chain beside it (1,212 -> 1,196 it/s), hence the
+  // threshold (cfg2 406, cfg1 1,215). D2IP_WGBF3_S2=0 restores the tiled kernel
+  static const bool b3_s2 = [] {
+    const char* v = getenv("D2IP_WGBF3_S2");
+    return !v || atoi(v) != 0;
+  }();
+  static const long long s2_min = [] {  // D2IP_WGBF3_S2MIN: smallest output grid (voxels) for it
+    const char* v = getenv("D2IP_WGBF3_S2MIN");
+    return v ? atoll(v) : 5000LL;
+  }();
+  const bool b3_wins = vg >= bf3_min || (b3_s2 && stride == 2 && vg >= s2_min);
   // (independent of the convolutions' D2IP_TF32_BF3: the weight gradients of large grids keep
   // 3xbf16 unless D2IP_WGRAD_BF3=0; parity: tests/test_gpu_engine.py full-grid cfg2 case)
   static const bool wg_b3 = [] {
