@@ -103,6 +103,7 @@ struct TcConv {
   int gd, gh, gw;  // row-space grid (stride 1: x; mode 1: y; mode 2: gy)
   int bf;          // bf16 operands (kind::f16)
   int vec;         // y rows (and bias) 16-byte aligned: float4 epilogue stores
+  int pvec;        // split-K partial rows 16-byte aligned (N % 4 == 0, aligned workspace): float4 partial stores
   int xtw;         // bf16: stream x from its bf16 twin (cp.async) instead of converting fp32 rows
   int lrows;       // TMA path: rows per channel-chunk column (whole padded lines: maxlines x Sw)
   int b3;          // 3xbf16 (TF32-precision layer): hi + lo bf16 operands, three MMAs per K step
@@ -172,17 +173,29 @@ __device__ __forceinline__ void tc_epilogue(const TcConv& a, uint32_t tmem, int 
         const int d2 = 2 * dq + (p >> 2), h2 = 2 * hq + ((p >> 1) & 1), w2 = 2 * wq + (p & 1);
         if (d2 >= y.d || h2 >= y.h || w2 >= y.w) continue;
         const long long vf = ((long long)d2 * y.h + h2) * y.w + w2;
+        const bool z = S <= 0;
         if (a.kspl > 1) {
           float* pp = a.part + (((long long)b * a.kspl + ks) * a.vout + vf) * cy + ci;
+          if (a.pvec) {  // 8 channels of one gx voxel: two 16-byte stores
+            float4* p4 = reinterpret_cast<float4*>(pp);
+            p4[0] = z ? make_float4(0.f, 0.f, 0.f, 0.f) : make_float4(vals[0], vals[1], vals[2], vals[3]);
+            p4[1] = z ? make_float4(0.f, 0.f, 0.f, 0.f) : make_float4(vals[4], vals[5], vals[6], vals[7]);
+          } else {
 #pragma unroll
-          for (int j = 0; j < 8; ++j) pp[j] = S > 0 ? vals[j] : 0.f;
+            for (int j = 0; j < 8; ++j) pp[j] = z ? 0.f : vals[j];
+          }
         } else {
-          float* yp = y.ptr + b * y.bstride + vf * y.cstride + ci;
+          // (the view is 16-byte aligned with C % 8 == 0: checked by conv_tc_run)
+          float4* y4 = reinterpret_cast<float4*>(y.ptr + b * y.bstride + vf * y.cstride + ci);
 #pragma unroll
-          for (int j = 0; j < 8; ++j) {
-            float o = S > 0 ? vals[j] : 0.f;
-            if (a.accumulate) o += yp[j];
-            yp[j] = o;
+          for (int h = 0; h < 2; ++h) {
+            float4 o = z ? make_float4(0.f, 0.f, 0.f, 0.f)
+                         : make_float4(vals[4 * h], vals[4 * h + 1], vals[4 * h + 2], vals[4 * h + 3]);
+            if (a.accumulate) {
+              const float4 yo = y4[h];
+              o.x += yo.x; o.y += yo.y; o.z += yo.z; o.w += yo.w;
+            }
+            y4[h] = o;
           }
         }
       }
@@ -193,7 +206,12 @@ __device__ __forceinline__ void tc_epilogue(const TcConv& a, uint32_t tmem, int 
       for (int c0 = cbeg; c0 < cend; c0 += 8) {
         float vals[8];
         tc::tmem_ld8(tcol + c0, vals);
-        if (pp) {
+        if (pp && a.pvec && n0 + c0 + 8 <= a.N) {
+          float4* p4 = reinterpret_cast<float4*>(pp + n0 + c0);
+          const bool z = S <= 0;
+          p4[0] = z ? make_float4(0.f, 0.f, 0.f, 0.f) : make_float4(vals[0], vals[1], vals[2], vals[3]);
+          p4[1] = z ? make_float4(0.f, 0.f, 0.f, 0.f) : make_float4(vals[4], vals[5], vals[6], vals[7]);
+        } else if (pp) {
 #pragma unroll
           for (int j = 0; j < 8; ++j)
             if (n0 + c0 + j < a.N) pp[n0 + c0 + j] = S > 0 ? vals[j] : 0.f;
@@ -244,6 +262,12 @@ __device__ __forceinline__ void tc_store8(const TcConv& a, int b, int ks, int v,
   if (v < 0) return;
   if (a.kspl > 1) {
     float* pp = a.part + (((long long)b * a.kspl + ks) * a.vout + v) * a.N;
+    if (a.pvec && n + 8 <= a.N) {
+      float4* p4 = reinterpret_cast<float4*>(pp + n);
+      p4[0] = zero ? make_float4(0.f, 0.f, 0.f, 0.f) : make_float4(vals[0], vals[1], vals[2], vals[3]);
+      p4[1] = zero ? make_float4(0.f, 0.f, 0.f, 0.f) : make_float4(vals[4], vals[5], vals[6], vals[7]);
+      return;
+    }
 #pragma unroll
     for (int j = 0; j < 8; ++j)
       if (n + j < a.N) pp[n + j] = zero ? 0.f : vals[j];
@@ -2069,6 +2093,7 @@ int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, lo
   a.y = y;
   a.accumulate = accumulate;
   a.vec = y.cstride % 4 == 0 && ((uintptr_t)y.ptr & 15) == 0;
+  a.pvec = Nout % 4 == 0 && ((uintptr_t)ws & 15) == 0;
   a.xtw = bf && !b3 && x.bf16 && x.cstride % 8 == 0 && x.c % 8 == 0 && ((uintptr_t)x.bf16 & 15) == 0;
   int cols = 32;
   while (cols < a.T * a.Ns * (kwf ? 3 : 1)) cols *= 2;
