@@ -459,9 +459,16 @@ __global__ void __launch_bounds__(kWtThreads) wgrad_tc_pack_k(WgTc a) {
         tc::tmem_ld8(trow + (uint32_t)c0, v);
         if (ci < Cin && lane < 16) {
           float* dst = pb + ((long long)(kd * 9 + q * 3 + kw) * Cin + ci) * Cout + co0;
+          if ((Cout & 7) == 0 && (reinterpret_cast<uintptr_t>(pb) & 15) == 0) {
+            const bool z = S <= 0;
+            float4* d4 = reinterpret_cast<float4*>(dst);
+            d4[0] = z ? make_float4(0.f, 0.f, 0.f, 0.f) : make_float4(v[0], v[1], v[2], v[3]);
+            d4[1] = z ? make_float4(0.f, 0.f, 0.f, 0.f) : make_float4(v[4], v[5], v[6], v[7]);
+          } else {
 #pragma unroll
-          for (int jj = 0; jj < 8; ++jj)
-            if (co0 + jj < Cout) dst[jj] = S > 0 ? v[jj] : 0.f;
+            for (int jj = 0; jj < 8; ++jj)
+              if (co0 + jj < Cout) dst[jj] = S > 0 ? v[jj] : 0.f;
+          }
         }
       }
     }
