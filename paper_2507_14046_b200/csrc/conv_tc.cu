@@ -1404,11 +1404,61 @@ __global__ void conv_tc_splitk_reduce_k(const float* __restrict__ part, int kspl
   const long long v = i / N;
   const int n = (int)(i - v * N);
   const float* p = part + (long long)b * kspl * vout * N + i;
+  const long long ps = vout * N;
+  // fixed order k = 0, 1, ...; four loads in flight
   float s = 0.f;
-  for (int k = 0; k < kspl; ++k) s += p[(long long)k * vout * N];
+  int k = 0;
+  for (; k + 3 < kspl; k += 4) {
+    const float a0 = p[(long long)k * ps], a1 = p[(long long)(k + 1) * ps], a2 = p[(long long)(k + 2) * ps],
+                a3 = p[(long long)(k + 3) * ps];
+    s += a0;
+    s += a1;
+    s += a2;
+    s += a3;
+  }
+  for (; k < kspl; ++k) s += p[(long long)k * ps];
   if (bias) s += __ldg(bias + b * bbs + n);
   float* yp = y.ptr + b * y.bstride + v * y.cstride + n;
   *yp = accumulate ? *yp + s : s;
+}
+
+// the same sum for four consecutive channels per thread (N % 4 == 0, 16-byte aligned views)
+__global__ void conv_tc_splitk_reduce4_k(const float* __restrict__ part, int kspl, long long vout, int N,
+                                         const float* __restrict__ bias, long long bbs, d2ip_act y, int accumulate) {
+  D2IP_PDL_ENTRY();
+  const int b = blockIdx.y;
+  const int n4 = N >> 2;
+  const long long i = (long long)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= vout * n4) return;
+  const long long v = i / n4;
+  const int n = (int)(i - v * n4) * 4;
+  const long long ps = vout * N;
+  const float4* p = reinterpret_cast<const float4*>(part + (long long)b * kspl * ps + v * N + n);
+  const long long ps4 = ps >> 2;
+  float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+  int k = 0;
+  for (; k + 3 < kspl; k += 4) {
+    const float4 a0 = p[(long long)k * ps4], a1 = p[(long long)(k + 1) * ps4], a2 = p[(long long)(k + 2) * ps4],
+                 a3 = p[(long long)(k + 3) * ps4];
+    s.x += a0.x; s.y += a0.y; s.z += a0.z; s.w += a0.w;
+    s.x += a1.x; s.y += a1.y; s.z += a1.z; s.w += a1.w;
+    s.x += a2.x; s.y += a2.y; s.z += a2.z; s.w += a2.w;
+    s.x += a3.x; s.y += a3.y; s.z += a3.z; s.w += a3.w;
+  }
+  for (; k < kspl; ++k) {
+    const float4 a0 = p[(long long)k * ps4];
+    s.x += a0.x; s.y += a0.y; s.z += a0.z; s.w += a0.w;
+  }
+  if (bias) {
+    const float* bb = bias + b * bbs + n;
+    s.x += __ldg(bb); s.y += __ldg(bb + 1); s.z += __ldg(bb + 2); s.w += __ldg(bb + 3);
+  }
+  float4* yp = reinterpret_cast<float4*>(y.ptr + b * y.bstride + v * y.cstride + n);
+  if (accumulate) {
+    const float4 yo = *yp;
+    s.x += yo.x; s.y += yo.y; s.z += yo.z; s.w += yo.w;
+  }
+  *yp = s;
 }
 
 // Stride-2 parity taps: the original tap index along one axis that pairs GEMM
@@ -2208,8 +2258,12 @@ int conv_tc_run(d2ip_act x, const float* wp, int K, int N, const float* bias, lo
   D2IP_LAUNCH_CHECK();
   if (deferred) *deferred = a.kspl > 1 ? a.kspl : 0;
   if (a.kspl > 1 && !deferred) {
-    D2IP_CUDA(launch_pdl(conv_tc_splitk_reduce_k, dim3(cdiv(a.vout * Nout, 256), batch), 256, 0, st, ws, a.kspl,
-                         a.vout, Nout, bias, bbs, y, accumulate));
+    if (a.pvec && a.vec && (a.vout * Nout) % 4 == 0)
+      D2IP_CUDA(launch_pdl(conv_tc_splitk_reduce4_k, dim3(cdiv(a.vout * Nout / 4, 256), batch), 256, 0, st, ws, a.kspl,
+                           a.vout, Nout, bias, bbs, y, accumulate));
+    else
+      D2IP_CUDA(launch_pdl(conv_tc_splitk_reduce_k, dim3(cdiv(a.vout * Nout, 256), batch), 256, 0, st, ws, a.kspl,
+                           a.vout, Nout, bias, bbs, y, accumulate));
     D2IP_LAUNCH_CHECK();
   }
   if (kwf) {
