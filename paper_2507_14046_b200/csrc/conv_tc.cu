@@ -1815,8 +1815,15 @@ static bool tc_plan(int D, int H, int W, int K, int N, int batch, TcConv& a, int
         const int per_sm = sm <= (size_t)110 * 1024 ? 2 : 1;
         const long long ctas0 = (long long)tl * (a.Np / ns) * batch;
         const int S = nt * (K / cb);
-        // split the stage chain across CTAs until ~2 CTAs per SM are busy
-        const int kspl = (int)std::min<long long>(S, std::max(1LL, (296 + ctas0 - 1) / ctas0));
+        // CTAs the split-K aims for (D2IP_TC_KSPL). Two per SM (296) was round 1's choice; every
+        // split costs a prologue, an epilogue and a partial-sum plane, and ~100 measured best on
+        // both small-grid regimes (cfg2 / cfg1 it/s: 592: 416 / 1,351, 296: 434 / 1,417,
+        // 148: 447 / 1,491, 100: 454 / 1,535, 74: 455 / 1,396, 50: 452 / 1,405)
+        static const long long kspl_target = [] {
+          const char* v = getenv("D2IP_TC_KSPL");
+          return v ? atoll(v) : 100LL;
+        }();
+        const int kspl = (int)std::min<long long>(S, std::max(1LL, (kspl_target + ctas0 - 1) / ctas0));
         const long long waves = (ctas0 * kspl + 148LL * per_sm - 1) / (148LL * per_sm);
         double cost;
         if (!large) {

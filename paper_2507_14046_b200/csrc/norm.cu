@@ -98,9 +98,26 @@ __global__ void __launch_bounds__(kNormThreads) norm_act_fwd_k(d2ip_act y, const
         const float* p = sk.part + ((long long)b * sk.kspl * V + v) * C + c0;
 #pragma unroll
         for (int i = 0; i < VPL; ++i) x[i] = __ldg(sk.bias + b * sk.bbs + c0 + i);
-        for (int k = 0; k < sk.kspl; ++k) {
+        // (four partial loads in flight; the sum keeps the order k = 0, 1, ...)
+        const long long ps = V * C;
+        int k = 0;
+        for (; k + 3 < sk.kspl; k += 4) {
+          float t0[VPL], t1[VPL], t2[VPL], t3[VPL];
+          ld<VPL>(p + (long long)k * ps, t0);
+          ld<VPL>(p + (long long)(k + 1) * ps, t1);
+          ld<VPL>(p + (long long)(k + 2) * ps, t2);
+          ld<VPL>(p + (long long)(k + 3) * ps, t3);
+#pragma unroll
+          for (int i = 0; i < VPL; ++i) {
+            x[i] += t0[i];
+            x[i] += t1[i];
+            x[i] += t2[i];
+            x[i] += t3[i];
+          }
+        }
+        for (; k < sk.kspl; ++k) {
           float t[VPL];
-          ld<VPL>(p + (long long)k * V * C, t);
+          ld<VPL>(p + (long long)k * ps, t);
 #pragma unroll
           for (int i = 0; i < VPL; ++i) x[i] += t[i];
         }
@@ -202,9 +219,25 @@ __global__ void __launch_bounds__(kNormThreads) norm_act_bwd_k(d2ip_act gout, d2
     if (ok) {
       if (sk.part) {  // the producing data-gradient convolution's split-K partials (fixed order, no bias)
         const float* p = sk.part + ((long long)b * sk.kspl * V + v) * C + c0;
-        for (int k = 0; k < sk.kspl; ++k) {
+        const long long ps = V * C;
+        int k = 0;
+        for (; k + 3 < sk.kspl; k += 4) {  // four partial loads in flight, same summation order
+          float t0[VPL], t1[VPL], t2[VPL], t3[VPL];
+          ld<VPL>(p + (long long)k * ps, t0);
+          ld<VPL>(p + (long long)(k + 1) * ps, t1);
+          ld<VPL>(p + (long long)(k + 2) * ps, t2);
+          ld<VPL>(p + (long long)(k + 3) * ps, t3);
+#pragma unroll
+          for (int i = 0; i < VPL; ++i) {
+            g[i] += t0[i];
+            g[i] += t1[i];
+            g[i] += t2[i];
+            g[i] += t3[i];
+          }
+        }
+        for (; k < sk.kspl; ++k) {
           float t[VPL];
-          ld<VPL>(p + (long long)k * V * C, t);
+          ld<VPL>(p + (long long)k * ps, t);
 #pragma unroll
           for (int i = 0; i < VPL; ++i) g[i] += t[i];
         }

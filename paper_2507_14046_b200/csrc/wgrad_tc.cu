@@ -530,8 +530,10 @@ static bool wt_nopack() {
 }
 
 // Knobs for the side-lane scheduling study: shared memory per CTA (D2IP_WG_SMEM_KB, default 220)
-// and CTAs per launch (D2IP_WG_CTAS, default 148). A weight-gradient CTA that fills an SM's shared
-// memory keeps the data-gradient chain's CTAs off that SM while it runs.
+// and CTAs per launch (D2IP_WG_CTAS, default 100: with sixteen producer warps per CTA fewer,
+// longer row groups win -- cfg2 / cfg1 it/s at 222: 450 / 1,501, 148: 455 / 1,535, 100: 458 / 1,580,
+// 74: 460 / 1,556). A weight-gradient CTA that fills an SM's shared memory keeps the
+// data-gradient chain's CTAs off that SM while it runs.
 static size_t wt_smem_cap() {
   static const size_t v = [] {
     const char* e = getenv("D2IP_WG_SMEM_KB");
@@ -542,7 +544,7 @@ static size_t wt_smem_cap() {
 static long long wt_cta_target() {
   static const long long v = [] {
     const char* e = getenv("D2IP_WG_CTAS");
-    return e ? atoll(e) : 148LL;
+    return e ? atoll(e) : 100LL;
   }();
   return v;
 }
