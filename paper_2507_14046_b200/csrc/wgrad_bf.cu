@@ -595,7 +595,11 @@ static bool wb_plan(int D, int H, int W, int Cin, int Cout, int ks, int batch, W
   a.nchunk = cdiv(rows, a.RS);
   // row groups: one wave of ~1 CTA per SM
   const long long jobs = (long long)a.ngroups * a.ncib * batch;
-  int nrg = (int)std::max(1LL, 148LL / jobs);
+  static const long long cta_target = [] {  // D2IP_WB_CTAS: CTAs per launch the row groups aim for
+    const char* v = getenv("D2IP_WB_CTAS");
+    return v ? atoll(v) : 148LL;
+  }();
+  int nrg = (int)std::max(1LL, cta_target / jobs);
   nrg = std::min(nrg, a.nchunk);
   a.chunks_per_rg = cdiv(a.nchunk, nrg);
   a.nrg = cdiv(a.nchunk, a.chunks_per_rg);

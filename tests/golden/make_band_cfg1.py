@@ -4,7 +4,8 @@ seq_cfg1.npz holds the real reference's run (dense operator, all host threads) a
 reordering of the same arithmetic (the oracle -- bit-exact with the reference on the golden
 cases -- with the compact operator). This script adds reorderings that change nothing but the
 host thread count (the CPU convolution / reduction partitioning, hence the fp32 summation
-order): the oracle with the compact operator at 2 and 4 threads. The GPU test judges its
+order): the oracle with the compact operator at 2, 4 and 8 threads (8 reproduces the band of
+seq_cfg1.npz bit for bit on an 8-core host). The GPU test judges its
 distance from the reference against the spread of ALL these reference-side reorderings.
 
 Needs only this repository (no /root/reference): python tests/golden/make_band_cfg1.py
@@ -24,7 +25,7 @@ from paper_2507_14046_b200.priornet import sample_noise_input  # noqa: E402
 OUT = Path(__file__).resolve().parent
 
 
-def main(threads=(2, 4)):
+def main(threads=(2, 4, 8)):
     gq = np.load(OUT / "seq_cfg1.npz")
     spec = W.CONFIGS["cfg1"]
     wl = W.make_workload(spec, seed=0, frames=4)
@@ -41,4 +42,4 @@ def main(threads=(2, 4)):
 
 
 if __name__ == "__main__":
-    main(tuple(int(a) for a in sys.argv[1:]) or (2, 4))
+    main(tuple(int(a) for a in sys.argv[1:]) or (2, 4, 8))
