@@ -193,3 +193,18 @@ def test_oracle_joint_mean_frame_upws_matches_reference():
     r.load(g["theta0"])
     r.optimize(g["dvs"].mean(0), [], 10, 0)
     np.testing.assert_array_equal(r.flat().numpy(), g["theta10"])
+
+
+def test_cfg1_band_fixture_is_consistent():
+    """tests/golden/seq_cfg1_band.npz (make_band_cfg1.py: the oracle at other host thread counts)
+    holds distinct reorderings of the cfg1-budget run, and its 8-thread member reproduces the band
+    of seq_cfg1.npz (written beside the real reference's run) bit for bit."""
+    gq = np.load(GOLDEN / "seq_cfg1.npz")
+    gb = np.load(GOLDEN / "seq_cfg1_band.npz")
+    members = {k: gb[k] for k in gb.files if k.startswith("values_t")}
+    assert set(members) == {"values_t2", "values_t4", "values_t8"}
+    for v in members.values():
+        assert v.shape == gq["values"].shape and np.isfinite(v).all()
+    np.testing.assert_array_equal(members["values_t8"], gq["band_values"])
+    assert not np.array_equal(members["values_t2"], members["values_t4"])
+    assert not np.array_equal(members["values_t4"], members["values_t8"])
