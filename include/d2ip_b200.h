@@ -144,7 +144,8 @@ int d2ip_upsample2x_bwd(d2ip_act gy, d2ip_act gx, int accumulate, int batch, voi
  * y = J sigma_V (J: M x Vp fp32 row-major, Vp % 4 == 0, zero padded),
  * r_f = y - dv_f for n_rhs frames; data = sum_f |r_f|^2 ("l2sq") or its sqrt
  * ("l2"). Writes rs[m] = c * sum_f r_f[m] with c = dData/d(sum r^2)*2, the
- * adjoint's right-hand side. Replaces `operator @ _vectorize_t(mapped)`,
+ * adjoint's right-hand side. `partial` holds [batch][nseg][m] column-segment sums (nseg =
+ * d2ip_jac_nseg(vp)), summed in segment order by the loss. Replaces `operator @ _vectorize_t(mapped)`,
  * `dv - ...` and `_data_term` (pipeline.py:257-263,279). */
 int d2ip_jac_fwd(const float* J, long long jbstride, const float* sigma, long long sbstride,
                  int m, int vp, float* partial, int nseg, int batch, void* stream);

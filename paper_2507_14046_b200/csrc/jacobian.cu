@@ -57,7 +57,8 @@ __global__ void __launch_bounds__(kGemvThreads) jac_fwd_k(const float* __restric
     acc = fmaf(a[u].w, s[u].w, acc);
   }
   acc = block_sum<kGemvThreads>(acc, red);
-  if (threadIdx.x == 0) partial[((long long)b * gridDim.y + m) * nseg + seg] = acc;
+  // partials are [b][segment][row]: the consumers read consecutive rows (coalesced)
+  if (threadIdx.x == 0) partial[((long long)b * nseg + seg) * gridDim.y + m] = acc;
 }
 
 int jac_fwd_partial(const float* J, long long jbs, const float* sigma, long long sbs, int m, int vp,
@@ -83,9 +84,9 @@ __global__ void __launch_bounds__(1024) jac_loss_k(const float* __restrict__ par
   const int b = blockIdx.x;
   float acc = 0.f;
   for (int m = threadIdx.x; m < M; m += blockDim.x) {
-    const float* p = partial + ((long long)b * M + m) * nseg;
+    const float* p = partial + (long long)b * nseg * M + m;
     float y = 0.f;
-    for (int s = 0; s < nseg; ++s) y += p[s];
+    for (int s = 0; s < nseg; ++s) y += p[(long long)s * M];
     float rsum = 0.f;
     for (int f = 0; f < n_rhs; ++f) {
       const float r = y - dv[((long long)b * n_rhs + f) * M + m];
@@ -141,9 +142,9 @@ __global__ void jac_sum_k(const float* __restrict__ partial, int nseg, int M, fl
   const int b = blockIdx.y;
   const int m = blockIdx.x * blockDim.x + threadIdx.x;
   if (m >= M) return;
-  const float* p = partial + ((long long)b * M + m) * nseg;
+  const float* p = partial + (long long)b * nseg * M + m;
   float acc = 0.f;
-  for (int s = 0; s < nseg; ++s) acc += p[s];
+  for (int s = 0; s < nseg; ++s) acc += p[(long long)s * M];
   y[(long long)b * M + m] = acc;
 }
 

@@ -291,7 +291,7 @@ def test_jacobian_fwd_adj(M, V, B):
     Jd, sd, rd = J.cuda(), s.cuda(), r.cuda()
     L = N.lib()
     nseg = L.d2ip_jac_nseg(Vp)
-    part = torch.zeros(B, M, nseg, device="cuda")
+    part = torch.zeros(B, nseg, M, device="cuda")  # partial sums [b][column segment][row]
     N.check(L.d2ip_jac_fwd(C.c_void_p(Jd.data_ptr()), M * Vp, C.c_void_p(sd.data_ptr()), Vp, M, Vp,
                            C.c_void_p(part.data_ptr()), nseg, B, stream()), "jac fwd")
     g = torch.zeros(B, Vp, device="cuda")
@@ -300,7 +300,7 @@ def test_jacobian_fwd_adj(M, V, B):
     N.check(L.d2ip_jac_adj(C.c_void_p(Jd.data_ptr()), M * Vp, C.c_void_p(rd.data_ptr()), M, Vp,
                            C.c_void_p(g.data_ptr()), Vp, C.c_void_p(ws.data_ptr()), wsn, B, stream()), "jac adj")
     torch.cuda.synchronize()
-    y = part.sum(-1).cpu()
+    y = part.sum(1).cpu()
     assert rel(y, torch.einsum("bmv,bv->bm", J, s)) < 1e-5
     assert rel(g.cpu(), torch.einsum("bmv,bm->bv", J, r)) < 1e-5
 
