@@ -37,7 +37,7 @@ constexpr int kWbThreads = 288;  // warp 0: MMA issue; warps 1-8: producers, the
 constexpr int kWbProd = 256;
 // 3xbf16: sixteen producer warps + one MMA-issue warp per independent accumulator (three for the kd-plane shape)
 __host__ __device__ constexpr int wb_issuers(bool b3, int nkh) { return (b3 && nkh == 3) ? 3 : 1; }
-__host__ __device__ constexpr int wb_threads(bool b3, int nkh) { return 32 * wb_issuers(b3, nkh) + (b3 ? 512 : 256); }
+__host__ __device__ constexpr int wb_threads(bool b3, int nkh) { return 32 * wb_issuers(b3, nkh) + 512; }
 constexpr int kWbProd3 = 512;
 constexpr int kWbMaxStages = 4;
 
@@ -135,14 +135,14 @@ __device__ __forceinline__ int wb_base(const WgBf& a, int grp) {
 // ~40 for the operand reads themselves).
 template <int NCX, int NKH, int NMMA, bool B3>
 __global__ void __launch_bounds__(wb_threads(B3, NKH)) wgrad_bf_k(WgBf a) {
-  // 3xbf16 (fp32 inputs converted and split on the way in; the weight gradients of large
-  // TF32-precision layers): with eight producer warps the kernel was bound by instruction latency
-  // at two warps per scheduler (ncu: 36 k instructions per warp, issue active 29 %), so this
-  // variant runs sixteen producer warps with eight loads in flight each (48->16 @ 64x64x32:
-  // 150 -> 97 us). Measured and not kept: 24 warps (99 us), two producer groups on alternate
-  // stages (105 us), two 9-warp CTAs per SM (141 us).
-  constexpr int NPROD = B3 ? kWbProd3 : kWbProd;  // producer threads
-  constexpr int UL = B3 ? 8 : 16;                 // loads in flight per producer thread
+  // Sixteen producer warps with eight loads in flight each. With eight the 3xbf16 variant (fp32
+  // inputs converted and split on the way in: the weight gradients of large TF32-precision
+  // layers) was bound by instruction latency at two warps per scheduler (ncu: 36 k instructions
+  // per warp, issue active 29 %; 48->16 @ 64x64x32 150 -> 97 us), and the bf16 twin path gains
+  // too (cfg4 139.8 -> 143.1 it/s). Measured and not kept: 24 warps (99 us), two producer groups
+  // on alternate stages (105 us), two 9-warp CTAs per SM (141 us).
+  constexpr int NPROD = kWbProd3;  // producer threads
+  constexpr int UL = 8;                 // loads in flight per producer thread
   constexpr int NPG = 1, GP = NPROD / NPG;
   // MMA-issue warps: a single issuer pays >= 57 cycles per MMA whatever its size (the no-fill
   // run of this kernel, D2IP_WB_DBG=1, took 77 us of its 97); the kd-plane shape has three
