@@ -1725,7 +1725,9 @@ bool conv_tc_layer(int cin, int cout, int ks, int stride, int dgrad, int precisi
     if (!s2 || (precision != D2IP_PREC_TF32 && precision != D2IP_PREC_BF16) || ks != 3 || stride != 2) return false;
     // (data gradients: the tensor-core kernel wins at every size since the 3xbf16 path -- cfg1
     // 1,186 -> 1,213 it/s with all stride-2 layers on it; the small forwards stay direct)
-    if (s2 == 1 && !dgrad && vout >= 0 && vout * cin * cout < 4LL * 1024 * 1024) return false;
+    // (wide layers go to the tensor cores at any size -- 64->128 at 8x8x4 out: cfg2 455 -> 461 it/s;
+    // the narrow small ones stay direct: cfg1 1,577 vs 1,568 with everything on tcgen05)
+    if (s2 == 1 && !dgrad && vout >= 0 && vout * cin * cout < 4LL * 1024 * 1024 && cin * cout < 4096) return false;
     if (!dgrad) {  // K = 8 C_in: a 16-byte chunk must not straddle two parities
       if (cin % 4 || cout < 1 || np_of(cout) > 1024) return false;
       r = TcDims{8 * cin, cout, 1, 2};
